@@ -1,0 +1,120 @@
+/*
+ * ddks.h — C ABI of the B200-native exact ddKS library (libddks.so).
+ *
+ * The statistic (PAPER.md = the arxiv 2106.13706 text; P:L<n> = its line n):
+ *   P:L33-35 (§2.1, Eq. 1)   D = max |C_P(x) - C_T(x)|, C = orthant occupancy about x.
+ *   P:L40-44 (§2.1, Eq. 2)   evaluated at every point of both samples (pooled origins: P rows, then Q rows).
+ *   P:L59-67 (§2.2.1, Eq. 3) orthant bit k = [x_k >= o_k] (element-wise "greater than or equal"; ties
+ *                            and the origin itself fall on the >= side; reading R1).
+ *   P:L78-81 (Eq. 6), P:L238 per-sample normalised difference |c_P/n_P - c_Q/n_Q| (reading R2), kept exact as
+ *                            num = max_o max_q |c_P[q]*n_Q - c_Q[q]*n_P|,  den = n_P*n_Q,  D = (double)num/(double)den.
+ *   P:L371 (§4.2)            permutation test; p = (1 + #{null_num >= observed_num}) / (1 + n_perm) (reading R9).
+ *
+ * Conventions shared by every call:
+ *   - Points are float32, row-major, contiguous: a sample of n points in d dimensions is n*d floats.
+ *   - Input pointers may be DEVICE pointers (read in place) or HOST pointers (copied to the device on
+ *     `stream` inside the call; this is what the end-to-end measurement times). The kind is detected with
+ *     cudaPointerGetAttributes. Inputs are caller-owned and only read; they must stay valid until the call returns.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream). It is borrowed, never destroyed.
+ *   - Every call is synchronous with respect to its host outputs (it synchronises `stream` before returning).
+ *   - Results go to caller-owned HOST memory.
+ *   - Nothing throws or aborts across the ABI; every call returns a ddks_status. On error the host outputs are
+ *     unspecified and ddks_last_error(ctx) holds a one-line message.
+ *   - A context is bound to one device and one host thread; it is not thread-safe.
+ *   - Multi-GPU (world > 1): every rank makes the same call with the same (replicated) inputs.
+ *       ddks_stat                shards the pooled ORIGINS into `world` contiguous ranges and combines the
+ *                                per-rank maxima with one NCCL all-reduce(max) of a uint64 (+ one all-reduce(min)
+ *                                for the argmax).
+ *       ddks_stat_batch /
+ *       ddks_permutation_null    shard ITEMS (pairs / permutations) contiguously and all-gather the per-item nums,
+ *                                so every rank returns the full result.
+ *   - Limits: 1 <= d <= 8; n_P, n_Q >= 1; n_P + n_Q < 2^31; n_P*n_Q < 2^53 (so D is one exact IEEE division).
+ */
+#ifndef DDKS_H_
+#define DDKS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ddks_ctx ddks_ctx; /* opaque: owns device workspace and (world > 1) an NCCL communicator */
+
+typedef enum {
+    DDKS_OK = 0,
+    DDKS_ERR_INVALID_ARGUMENT = 1, /* null pointer, negative size, B < 1, n_perm < 0, bad flags, bad rank/world */
+    DDKS_ERR_EMPTY_SAMPLE = 2,     /* n_P == 0 || n_Q == 0            (SPEC core-types EmptySample)        */
+    DDKS_ERR_DIM_UNSUPPORTED = 3,  /* d < 1 || d > 8                                                         */
+    DDKS_ERR_NONFINITE = 4,        /* a NaN or +-Inf coordinate        (SPEC core-types NonFiniteValue)     */
+    DDKS_ERR_TOO_LARGE = 5,        /* n_P + n_Q >= 2^31 or n_P*n_Q >= 2^53                                  */
+    DDKS_ERR_CUDA = 6,             /* a CUDA runtime error (message in ddks_last_error)                     */
+    DDKS_ERR_NCCL = 7,             /* an NCCL error                                                          */
+    DDKS_ERR_OOM = 8               /* device workspace allocation failed                                    */
+} ddks_status;
+
+/* Flags for ddks_create. */
+#define DDKS_FLAG_DEFAULT 0u
+#define DDKS_FLAG_NO_VALIDATE 1u /* skip the NaN/Inf check (inputs are still packed and -0 canonicalised)  */
+#define DDKS_FLAG_TIES_GT 2u     /* TEST ONLY: bit k = [x_k > o_k] instead of >= (shows the convention matters) */
+
+typedef struct {
+    uint64_t num;          /* max over origins and orthants of |c_P*n_Q - c_Q*n_P| (exact integer)            */
+    uint64_t den;          /* n_P * n_Q                                                                         */
+    double D;              /* (double)num / (double)den, one IEEE-754 round-to-nearest-even division           */
+    int64_t argmax_origin; /* smallest pooled origin index attaining num (P rows first); -1 if not computed   */
+} ddks_result;
+
+/* NCCL bootstrap: rank 0 calls this, the harness broadcasts the 128 bytes (e.g. via torch.distributed),
+ * and every rank passes them to ddks_create. */
+ddks_status ddks_get_nccl_id(void* out_128_bytes);
+
+/* Create a context on CUDA device `device`. world >= 1, 0 <= rank < world. nccl_id must be NULL iff world == 1.
+ * *out receives the context (NULL on failure). */
+ddks_status ddks_create(ddks_ctx** out, int device, int world, int rank, const void* nccl_id, uint32_t flags);
+
+/* Exact ddKS of one pair. P: [n_P][d], Q: [n_Q][d] (device or host). out: host. */
+ddks_status ddks_stat(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
+                      void* stream, ddks_result* out);
+
+/* B independent pairs (north_star (2); the power-analysis repeats of P:L364-371).
+ * P: [B][n_P][d], Q: [B][n_Q][d] (device or host). out: host [B]; argmax_origin is -1 for batch items. */
+ddks_status ddks_stat_batch(ddks_ctx* ctx, const float* P, const float* Q, int64_t B, int64_t n_P, int64_t n_Q,
+                            int32_t d, void* stream, ddks_result* out);
+
+/* Permutation null. pooled: [n_P+n_Q][d] (device or host), first n_P rows = P.
+ * perms: [n_perm][n_P+n_Q] int32 (device or host); permutation j assigns pooled[perms[j][0..n_P)] to P' and
+ * the rest to Q'; every row must be a permutation of 0..n_P+n_Q-1 (checked: DDKS_ERR_INVALID_ARGUMENT).
+ * Outputs (host): null_num[n_perm]; *observed = the identity split; *p_value = (1 + #{null_num >= observed.num})
+ * / (1 + n_perm). Any of null_num / observed / p_value may be NULL if not wanted. */
+ddks_status ddks_permutation_null(ddks_ctx* ctx, const float* pooled, int64_t n_P, int64_t n_Q, int32_t d,
+                                  const int32_t* perms, int64_t n_perm, void* stream, uint64_t* null_num,
+                                  ddks_result* observed, double* p_value);
+
+/* Debug / sampled-parity export: num(o) = max_q |c_P[q]*n_Q - c_Q[q]*n_P| for pooled origins [o_begin, o_end).
+ * num_out: [o_end - o_begin] uint64, device or host. Single-rank (no collective). */
+ddks_status ddks_stat_per_origin(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
+                                 int64_t o_begin, int64_t o_end, uint64_t* num_out, void* stream);
+
+/* Host-only helper (no GPU needed): the contiguous origin / item range [*begin, *end) that `rank` of `world`
+ * owns out of `total` units. Ranges are balanced to within one unit and cover 0..total exactly. */
+ddks_status ddks_shard_range(int64_t total, int world, int rank, int64_t* begin, int64_t* end);
+
+/* Number of kernels the library launched on this context since creation (for the bench's gpu_launches). */
+int64_t ddks_launch_count(const ddks_ctx* ctx);
+
+/* Destroy a context (NULL-safe). Frees workspace and the NCCL communicator. */
+ddks_status ddks_destroy(ddks_ctx* ctx);
+
+/* Last error message of this context ("" if none); valid until the next call on ctx. ctx may be NULL
+ * (then the message of the last failed ddks_create on this thread). */
+const char* ddks_last_error(const ddks_ctx* ctx);
+
+/* Library version string. */
+const char* ddks_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DDKS_H_ */

@@ -1,0 +1,177 @@
+/*
+ * ddks_oracle.c — TEST INFRASTRUCTURE ONLY. Plain, slow, obviously-correct CPU oracle for the exact
+ * ddKS statistic of arxiv 2106.13706. Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference leg may load or execute this file. The product path
+ * (paper_2106_13706_b200/) never links or imports it, and it shares no code, header, table or
+ * constant generator with the CUDA path.
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, cited as P:L<line>):
+ *   - P:L33-35 (§2.1, Eq. 1): D = max |C_P(x) - C_T(x)|, C = orthant occupancy about x.
+ *   - P:L40-44 (§2.1, Eq. 2): C evaluated at every point of both samples (pooled origins, P then T),
+ *     maximum taken over the concatenation of both evaluation sets.
+ *   - P:L46 (§2.1): "for each test point ... define each orthant ... determine the number of points
+ *     from each sample that exist in that orthant" — the loop method, written out below as-is.
+ *   - P:L59-67 (§2.2.1, Eq. 3): the comparison is element-wise "greater than or equal":
+ *     bit k of the orthant code is [x_k >= o_k]  (reading R1: ties and the origin itself
+ *     land on the >= side). ties_gt=1 switches to [x_k > o_k]; used only by tests to show the
+ *     convention matters.
+ *   - P:L68-75 (Eq. 4-5): the printed square-wave selector is degenerate; the orthant index is the
+ *     binary code sum_k bit_k 2^k (reading R3; the numbering does not change D).
+ *   - P:L78-81 (Eq. 6) and P:L238 (§3): per-sample normalised difference
+ *     |c_P/n_P - c_T/n_T|, kept exact as the integer |c_P*n_T - c_T*n_P| over den = n_P*n_T
+ *     (reading R2); D = (double)num / (double)den, one correctly rounded division (R5).
+ *   - P:L371 (§4.2): permutation test; p = (1 + #{null >= observed}) / (1 + n_perm) (SPEC S:L363
+ *     add-one convention; reading R9).
+ *
+ * Arithmetic: coordinates are read as float32 and compared after widening to double (exact and
+ * order-preserving, so identical to an IEEE float32 ordered >=; -0 == +0; denormals compared
+ * exactly). Counts are int64. No blocking, fusion or loop reordering: for each origin, for each
+ * point, for each dimension — the paper's loop method. Origins are independent, so the outer loop
+ * may run on several OpenMP threads (the integer max does not depend on order).
+ *
+ * Build: gcc -O2 -fopenmp -shared -fPIC -o libddks_oracle.so ddks_oracle.c   (no -ffast-math)
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* P:L46 / P:L59-67: orthant code of `point` about `test_point` (SPEC S:L100-108 orthant_index). */
+int oracle_orthant_index(const float* test_point, const float* point, int d, int ties_gt)
+{
+    int code = 0;
+    for (int k = 0; k < d; ++k) {
+        double x = (double)point[k];
+        double o = (double)test_point[k];
+        int bit = ties_gt ? (x > o) : (x >= o);
+        code += bit << k;
+    }
+    return code;
+}
+
+/* SPEC S:L110-118 membership: counts[i][j] = #{points of `counted` in orthant j about test i}. */
+void oracle_membership(const float* counted, int64_t n_counted, const float* test, int64_t n_test,
+                       int d, int ties_gt, int64_t* counts /* [n_test][2^d] */)
+{
+    int64_t nq = (int64_t)1 << d;
+    for (int64_t i = 0; i < n_test; ++i) {
+        for (int64_t j = 0; j < nq; ++j) counts[i * nq + j] = 0;
+        for (int64_t x = 0; x < n_counted; ++x) {
+            int code = oracle_orthant_index(test + i * d, counted + x * d, d, ties_gt);
+            counts[i * nq + code] += 1;
+        }
+    }
+}
+
+/* Pooled point i: rows of P first, then rows of Q (Eq. 2 concatenation order). */
+static const float* pooled_row(const float* P, int64_t n_P, const float* Q, int d, int64_t i)
+{
+    return (i < n_P) ? (P + i * d) : (Q + (i - n_P) * d);
+}
+
+/* num(o) for one origin: max over orthants q of |cP[q]*n_Q - cQ[q]*n_P|. */
+static uint64_t origin_num(const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d,
+                           int ties_gt, const float* origin, int64_t* cP, int64_t* cQ)
+{
+    int64_t nq = (int64_t)1 << d;
+    for (int64_t q = 0; q < nq; ++q) { cP[q] = 0; cQ[q] = 0; }
+    for (int64_t x = 0; x < n_P; ++x) cP[oracle_orthant_index(origin, P + x * d, d, ties_gt)] += 1;
+    for (int64_t x = 0; x < n_Q; ++x) cQ[oracle_orthant_index(origin, Q + x * d, d, ties_gt)] += 1;
+    uint64_t best = 0;
+    for (int64_t q = 0; q < nq; ++q) {
+        int64_t diff = cP[q] * n_Q - cQ[q] * n_P;
+        uint64_t a = (uint64_t)(diff < 0 ? -diff : diff);
+        if (a > best) best = a;
+    }
+    return best;
+}
+
+/* Per-origin num(o) for pooled origins [o_begin, o_end). out[o - o_begin]. Returns 0 on success. */
+int oracle_ddks_per_origin(const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d, int ties_gt,
+                           int64_t o_begin, int64_t o_end, uint64_t* out, int nthreads)
+{
+    if (d < 1 || d > 20 || n_P < 1 || n_Q < 1 || o_begin < 0 || o_end > n_P + n_Q || o_begin > o_end) return 1;
+    int64_t nq = (int64_t)1 << d;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel
+    {
+        int64_t* cP = (int64_t*)malloc(sizeof(int64_t) * nq);
+        int64_t* cQ = (int64_t*)malloc(sizeof(int64_t) * nq);
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t o = o_begin; o < o_end; ++o)
+            out[o - o_begin] = origin_num(P, n_P, Q, n_Q, d, ties_gt, pooled_row(P, n_P, Q, d, o), cP, cQ);
+        free(cP);
+        free(cQ);
+    }
+    (void)nthreads;
+    return 0;
+}
+
+/* Full statistic: num = max_o num(o), den = n_P*n_Q, argmax = smallest pooled origin index attaining num
+ * (reading R7). Returns 0 on success. */
+int oracle_ddks(const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d, int ties_gt, int nthreads,
+                uint64_t* num, uint64_t* den, double* D, int64_t* argmax)
+{
+    int64_t N = n_P + n_Q;
+    if (d < 1 || d > 20 || n_P < 1 || n_Q < 1) return 1;
+    uint64_t* per = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)N);
+    if (!per) return 2;
+    int rc = oracle_ddks_per_origin(P, n_P, Q, n_Q, d, ties_gt, 0, N, per, nthreads);
+    if (rc) { free(per); return rc; }
+    uint64_t best = 0;
+    int64_t arg = 0;
+    for (int64_t o = 0; o < N; ++o)
+        if (per[o] > best) { best = per[o]; arg = o; }
+    free(per);
+    *num = best;
+    *den = (uint64_t)n_P * (uint64_t)n_Q;
+    *D = (double)(*num) / (double)(*den);
+    *argmax = arg;
+    return 0;
+}
+
+/* Batch: item b is the pair (P + b*n_P*d, Q + b*n_Q*d); each item is the definition above. */
+int oracle_ddks_batch(const float* P, const float* Q, int64_t B, int64_t n_P, int64_t n_Q, int d, int ties_gt,
+                      int nthreads, uint64_t* num_out)
+{
+    for (int64_t b = 0; b < B; ++b) {
+        uint64_t num, den; double D; int64_t arg;
+        int rc = oracle_ddks(P + b * n_P * d, n_P, Q + b * n_Q * d, n_Q, d, ties_gt, nthreads, &num, &den, &D, &arg);
+        if (rc) return rc;
+        num_out[b] = num;
+    }
+    return 0;
+}
+
+/* Permutation null: for permutation j, P' = pooled[perm_j[0..n_P)], Q' = pooled[perm_j[n_P..N)],
+ * then the definition above. observed = identity split. p = (1 + #{null_j >= observed}) / (1 + n_perm),
+ * returned as the exact numerator p_num (denominator 1 + n_perm) and as a double. */
+int oracle_permutation_null(const float* pooled, int64_t n_P, int64_t n_Q, int d, const int32_t* perms,
+                            int64_t n_perm, int ties_gt, int nthreads, uint64_t* null_num, uint64_t* observed,
+                            int64_t* p_num, double* p_value)
+{
+    int64_t N = n_P + n_Q;
+    uint64_t den; double D; int64_t arg;
+    int rc = oracle_ddks(pooled, n_P, pooled + n_P * d, n_Q, d, ties_gt, nthreads, observed, &den, &D, &arg);
+    if (rc) return rc;
+    float* Pp = (float*)malloc(sizeof(float) * (size_t)(n_P * d));
+    float* Qp = (float*)malloc(sizeof(float) * (size_t)(n_Q * d));
+    int64_t ge = 0;
+    for (int64_t j = 0; j < n_perm; ++j) {
+        const int32_t* pj = perms + j * N;
+        for (int64_t i = 0; i < n_P; ++i) memcpy(Pp + i * d, pooled + (int64_t)pj[i] * d, sizeof(float) * d);
+        for (int64_t i = 0; i < n_Q; ++i) memcpy(Qp + i * d, pooled + (int64_t)pj[n_P + i] * d, sizeof(float) * d);
+        rc = oracle_ddks(Pp, n_P, Qp, n_Q, d, ties_gt, nthreads, &null_num[j], &den, &D, &arg);
+        if (rc) break;
+        if (null_num[j] >= *observed) ge += 1;
+    }
+    free(Pp);
+    free(Qp);
+    *p_num = 1 + ge;
+    *p_value = (double)(1 + ge) / (double)(1 + n_perm);
+    return rc;
+}
