@@ -35,6 +35,12 @@
 
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#define DDKS_API __attribute__((visibility("default")))
+#else
+#define DDKS_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -57,6 +63,8 @@ typedef enum {
 #define DDKS_FLAG_DEFAULT 0u
 #define DDKS_FLAG_NO_VALIDATE 1u /* skip the NaN/Inf check (inputs are still packed and -0 canonicalised)  */
 #define DDKS_FLAG_TIES_GT 2u     /* TEST ONLY: bit k = [x_k > o_k] instead of >= (shows the convention matters) */
+#define DDKS_FLAG_FORCE_DIRECT 4u /* TEST ONLY: never split the point axis into segments (exercises the in-kernel
+                                     finalisation at small N; results are identical either way)              */
 
 typedef struct {
     uint64_t num;          /* max over origins and orthants of |c_P*n_Q - c_Q*n_P| (exact integer)            */
@@ -67,19 +75,19 @@ typedef struct {
 
 /* NCCL bootstrap: rank 0 calls this, the harness broadcasts the 128 bytes (e.g. via torch.distributed),
  * and every rank passes them to ddks_create. */
-ddks_status ddks_get_nccl_id(void* out_128_bytes);
+DDKS_API ddks_status ddks_get_nccl_id(void* out_128_bytes);
 
 /* Create a context on CUDA device `device`. world >= 1, 0 <= rank < world. nccl_id must be NULL iff world == 1.
  * *out receives the context (NULL on failure). */
-ddks_status ddks_create(ddks_ctx** out, int device, int world, int rank, const void* nccl_id, uint32_t flags);
+DDKS_API ddks_status ddks_create(ddks_ctx** out, int device, int world, int rank, const void* nccl_id, uint32_t flags);
 
 /* Exact ddKS of one pair. P: [n_P][d], Q: [n_Q][d] (device or host). out: host. */
-ddks_status ddks_stat(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
+DDKS_API ddks_status ddks_stat(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
                       void* stream, ddks_result* out);
 
 /* B independent pairs (north_star (2); the power-analysis repeats of P:L364-371).
  * P: [B][n_P][d], Q: [B][n_Q][d] (device or host). out: host [B]; argmax_origin is -1 for batch items. */
-ddks_status ddks_stat_batch(ddks_ctx* ctx, const float* P, const float* Q, int64_t B, int64_t n_P, int64_t n_Q,
+DDKS_API ddks_status ddks_stat_batch(ddks_ctx* ctx, const float* P, const float* Q, int64_t B, int64_t n_P, int64_t n_Q,
                             int32_t d, void* stream, ddks_result* out);
 
 /* Permutation null. pooled: [n_P+n_Q][d] (device or host), first n_P rows = P.
@@ -87,31 +95,31 @@ ddks_status ddks_stat_batch(ddks_ctx* ctx, const float* P, const float* Q, int64
  * the rest to Q'; every row must be a permutation of 0..n_P+n_Q-1 (checked: DDKS_ERR_INVALID_ARGUMENT).
  * Outputs (host): null_num[n_perm]; *observed = the identity split; *p_value = (1 + #{null_num >= observed.num})
  * / (1 + n_perm). Any of null_num / observed / p_value may be NULL if not wanted. */
-ddks_status ddks_permutation_null(ddks_ctx* ctx, const float* pooled, int64_t n_P, int64_t n_Q, int32_t d,
+DDKS_API ddks_status ddks_permutation_null(ddks_ctx* ctx, const float* pooled, int64_t n_P, int64_t n_Q, int32_t d,
                                   const int32_t* perms, int64_t n_perm, void* stream, uint64_t* null_num,
                                   ddks_result* observed, double* p_value);
 
 /* Debug / sampled-parity export: num(o) = max_q |c_P[q]*n_Q - c_Q[q]*n_P| for pooled origins [o_begin, o_end).
  * num_out: [o_end - o_begin] uint64, device or host. Single-rank (no collective). */
-ddks_status ddks_stat_per_origin(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
+DDKS_API ddks_status ddks_stat_per_origin(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
                                  int64_t o_begin, int64_t o_end, uint64_t* num_out, void* stream);
 
 /* Host-only helper (no GPU needed): the contiguous origin / item range [*begin, *end) that `rank` of `world`
  * owns out of `total` units. Ranges are balanced to within one unit and cover 0..total exactly. */
-ddks_status ddks_shard_range(int64_t total, int world, int rank, int64_t* begin, int64_t* end);
+DDKS_API ddks_status ddks_shard_range(int64_t total, int world, int rank, int64_t* begin, int64_t* end);
 
 /* Number of kernels the library launched on this context since creation (for the bench's gpu_launches). */
-int64_t ddks_launch_count(const ddks_ctx* ctx);
+DDKS_API int64_t ddks_launch_count(const ddks_ctx* ctx);
 
 /* Destroy a context (NULL-safe). Frees workspace and the NCCL communicator. */
-ddks_status ddks_destroy(ddks_ctx* ctx);
+DDKS_API ddks_status ddks_destroy(ddks_ctx* ctx);
 
 /* Last error message of this context ("" if none); valid until the next call on ctx. ctx may be NULL
  * (then the message of the last failed ddks_create on this thread). */
-const char* ddks_last_error(const ddks_ctx* ctx);
+DDKS_API const char* ddks_last_error(const ddks_ctx* ctx);
 
 /* Library version string. */
-const char* ddks_version(void);
+DDKS_API const char* ddks_version(void);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,578 @@
+// ddks_api.cu — host side of libddks.so: the C ABI declared in include/ddks.h.
+//
+// Context = device + grow-only workspace + (world > 1) an NCCL communicator (NCCL 2.28.9, the copy torch
+// bundles). Each public call: argument checks -> optional H2D of host inputs -> k_pack (validate + pack) ->
+// k_count (classify + count + per-origin max) [-> k_finalize] -> k_argmax -> NCCL combine -> one D2H -> sync.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ddks.h"
+#include "ddks_kernels.cuh"
+
+#define DDKS_VERSION "0.1.0-sm100a"
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+struct DevResult {  // device-side result block (one D2H per call)
+    unsigned long long num;
+    unsigned long long arg;
+    uint32_t flag;
+    uint32_t pad;
+};
+
+struct ddks_ctx {
+    int device = 0, world = 1, rank = 0;
+    uint32_t flags = 0;
+    ncclComm_t comm = nullptr;
+    DevBuf raw_a, raw_b, raw_perm, packed, packed2, pool_packed, per_origin, accum, item_num, bitmap, res;
+    void* host_pinned = nullptr;  // DevResult + scratch
+    size_t host_pinned_bytes = 0;
+    int64_t launches = 0;
+    std::string err;
+};
+
+static thread_local std::string g_create_err;
+
+namespace {
+
+ddks_status fail(ddks_ctx* c, ddks_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    else g_create_err = buf;
+    return s;
+}
+
+#define CU(call)                                                                                     \
+    do {                                                                                             \
+        cudaError_t e_ = (call);                                                                     \
+        if (e_ != cudaSuccess)                                                                       \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? DDKS_ERR_OOM : DDKS_ERR_CUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                          \
+    } while (0)
+
+#define NC(call)                                                                                         \
+    do {                                                                                                 \
+        ncclResult_t r_ = (call);                                                                        \
+        if (r_ != ncclSuccess)                                                                           \
+            return fail(ctx, DDKS_ERR_NCCL, "%s: %s (%s:%d)", #call, ncclGetErrorString(r_), __FILE__, __LINE__); \
+    } while (0)
+
+#define CHECK_LAUNCH() CU(cudaGetLastError())
+
+ddks_status ensure(ddks_ctx* ctx, DevBuf& b, size_t bytes) {
+    if (bytes <= b.bytes) return DDKS_OK;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    size_t want = std::max(bytes, (size_t)256);
+    cudaError_t e = cudaMalloc(&b.p, want);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, DDKS_ERR_OOM, "cudaMalloc(%zu) failed: %s", want, cudaGetErrorString(e));
+    }
+    b.bytes = want;
+    return DDKS_OK;
+}
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Bring an input to the device: device pointers are used in place, host pointers are copied on `st`.
+ddks_status stage_input(ddks_ctx* ctx, const void* src, size_t bytes, DevBuf& buf, cudaStream_t st, const void** out) {
+    if (is_device_ptr(src)) {
+        *out = src;
+        return DDKS_OK;
+    }
+    ddks_status s = ensure(ctx, buf, bytes);
+    if (s) return s;
+    CU(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyHostToDevice, st));
+    *out = buf.p;
+    return DDKS_OK;
+}
+
+uint64_t gcd_u64(uint64_t a, uint64_t b) {
+    while (b) {
+        uint64_t t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+ddks_status check_sizes(ddks_ctx* ctx, int64_t n_P, int64_t n_Q, int32_t d) {
+    if (n_P < 0 || n_Q < 0) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "negative sample size");
+    if (n_P == 0 || n_Q == 0) return fail(ctx, DDKS_ERR_EMPTY_SAMPLE, "empty sample (n_P=%lld, n_Q=%lld)",
+                                          (long long)n_P, (long long)n_Q);
+    if (d < 1 || d > 8) return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "d=%d not in [1, 8]", d);
+    if (n_P + n_Q >= (int64_t(1) << 31)) return fail(ctx, DDKS_ERR_TOO_LARGE, "n_P + n_Q >= 2^31");
+    const double den = (double)n_P * (double)n_Q;
+    if (den >= 9007199254740992.0) return fail(ctx, DDKS_ERR_TOO_LARGE, "n_P * n_Q >= 2^53");
+    return DDKS_OK;
+}
+
+int pad_dim(int d) { return d <= 4 ? 4 : 8; }
+
+// ------------------------------------------------------------------------------------- count dispatch
+struct CountPlan {
+    int64_t B;
+    int32_t N, n_P, o_begin, o_end;
+    int64_t nP, nQ;
+    bool split;    // SPLIT counters (c_P, c_Q separately)
+    int segs;      // grid.z point segments (>1 => accumulate + finalize)
+};
+
+template <int D, bool SPLIT, bool GT>
+ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a, cudaStream_t st) {
+    using G = ddks::Geo<D, SPLIT>;
+    auto kern = ddks::k_count<D, SPLIT, GT>;
+    static bool attr_done = false;  // per-process; device attributes are per function
+    if (!attr_done) {
+        CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES));
+        attr_done = true;
+    }
+    const int n_orig = pl.o_end - pl.o_begin;
+    const int blocks_o = (n_orig + G::ORIGINS - 1) / G::ORIGINS;
+    int segs = 1;
+    const int64_t ctas = pl.B * blocks_o;
+    const int n_tiles = (pl.N + G::TILE - 1) / G::TILE;
+    if (ctas < 2 * 148 && !(ctx->flags & DDKS_FLAG_FORCE_DIRECT)) segs = (int)std::min<int64_t>(n_tiles, (2 * 148 + ctas - 1) / ctas);
+    const int tiles_per_seg = (n_tiles + segs - 1) / segs;
+    segs = (n_tiles + tiles_per_seg - 1) / tiles_per_seg;
+    a.seg_points = tiles_per_seg * G::TILE;
+    if (segs > 1) {
+        const size_t acc_bytes = (size_t)pl.B * G::NB * (size_t)n_orig * 4;
+        ddks_status s = ensure(ctx, ctx->accum, acc_bytes);
+        if (s) return s;
+        CU(cudaMemsetAsync(ctx->accum.p, 0, acc_bytes, st));
+        a.accum = (uint32_t*)ctx->accum.p;
+    } else {
+        a.accum = nullptr;
+    }
+    if (pl.B > 0x7fffffff || blocks_o > 65535) return fail(ctx, DDKS_ERR_TOO_LARGE, "grid too large");
+    dim3 grid((unsigned)pl.B, (unsigned)blocks_o, (unsigned)segs);
+    kern<<<grid, G::T, G::SMEM_BYTES, st>>>(a);
+    CHECK_LAUNCH();
+    ctx->launches++;
+    if (segs > 1) {
+        const int64_t total = pl.B * n_orig;
+        const int threads = 256;
+        const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 16);
+        ddks::k_finalize<D, SPLIT><<<blocks, threads, 0, st>>>(a, pl.B);
+        CHECK_LAUNCH();
+        ctx->launches++;
+    }
+    return DDKS_OK;
+}
+
+template <int D>
+ddks_status launch_count_d(ddks_ctx* ctx, const CountPlan& pl, const ddks::CountArgs& a, cudaStream_t st) {
+    const bool gt = (ctx->flags & DDKS_FLAG_TIES_GT) != 0;
+    if (pl.split) return gt ? launch_count_t<D, true, true>(ctx, pl, a, st) : launch_count_t<D, true, false>(ctx, pl, a, st);
+    return gt ? launch_count_t<D, false, true>(ctx, pl, a, st) : launch_count_t<D, false, false>(ctx, pl, a, st);
+}
+
+// Run the count for B items of N packed points each; results: item_num[B] (device), per_origin (B == 1).
+ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int64_t n_P, int64_t n_Q,
+                      int64_t o_begin, int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st) {
+    const int64_t N = n_P + n_Q;
+    const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
+    const uint64_t a_ = (uint64_t)n_Q / g, b_ = (uint64_t)n_P / g;
+    // DIFF counters hold c_P*a - c_Q*b; |value| <= n_P*n_Q/g must fit int32
+    const bool split = (uint64_t)n_P * a_ >= 0x7fffffffull || (uint64_t)n_Q * b_ >= 0x7fffffffull;
+    CountPlan pl{B, (int32_t)N, (int32_t)n_P, (int32_t)o_begin, (int32_t)o_end, n_P, n_Q, split, 1};
+    ddks::CountArgs a{};
+    a.pts = packed;
+    a.item_stride = N * pad_dim(d);
+    a.N = (int32_t)N;
+    a.n_P = (int32_t)n_P;
+    a.o_begin = (int32_t)o_begin;
+    a.o_end = (int32_t)o_end;
+    a.incP = split ? 1u : (uint32_t)a_;
+    a.incQ = split ? 1u : (uint32_t)(0u - (uint32_t)b_);
+    a.g = split ? 1 : g;
+    a.nP = n_P;
+    a.nQ = n_Q;
+    a.item_num = item_num;
+    a.per_origin = per_origin;
+    switch (d) {
+        case 1: return launch_count_d<1>(ctx, pl, a, st);
+        case 2: return launch_count_d<2>(ctx, pl, a, st);
+        case 3: return launch_count_d<3>(ctx, pl, a, st);
+        case 4: return launch_count_d<4>(ctx, pl, a, st);
+        case 5: return launch_count_d<5>(ctx, pl, a, st);
+        case 6: return launch_count_d<6>(ctx, pl, a, st);
+        case 7: return launch_count_d<7>(ctx, pl, a, st);
+        case 8: return launch_count_d<8>(ctx, pl, a, st);
+    }
+    return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "d=%d", d);
+}
+
+ddks_status launch_pack(ddks_ctx* ctx, const float* src, int64_t n_rows, int d, int64_t B, float* dst, int64_t N,
+                        int64_t row_off, uint32_t* flag, cudaStream_t st) {
+    const int64_t total = B * n_rows;
+    if (total == 0) return DDKS_OK;
+    const int threads = 256;
+    const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 8);
+    ddks::k_pack<<<blocks, threads, 0, st>>>(src, n_rows, d, B, dst, N, row_off, pad_dim(d),
+                                            (ctx->flags & DDKS_FLAG_NO_VALIDATE) ? 0 : 1, flag);
+    CHECK_LAUNCH();
+    ctx->launches++;
+    return DDKS_OK;
+}
+
+ddks_status ensure_host(ddks_ctx* ctx, size_t bytes) {
+    if (bytes <= ctx->host_pinned_bytes) return DDKS_OK;
+    if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
+    ctx->host_pinned = nullptr;
+    ctx->host_pinned_bytes = 0;
+    CU(cudaMallocHost(&ctx->host_pinned, bytes));
+    ctx->host_pinned_bytes = bytes;
+    return DDKS_OK;
+}
+
+ddks_status bind_device(ddks_ctx* ctx) {
+    CU(cudaSetDevice(ctx->device));
+    return DDKS_OK;
+}
+
+}  // namespace
+
+// ===================================================================================================== C ABI
+extern "C" {
+
+const char* ddks_version(void) { return DDKS_VERSION; }
+
+ddks_status ddks_shard_range(int64_t total, int world, int rank, int64_t* begin, int64_t* end) {
+    if (!begin || !end || total < 0 || world < 1 || rank < 0 || rank >= world) return DDKS_ERR_INVALID_ARGUMENT;
+    const int64_t base = total / world, rem = total % world;
+    *begin = rank * base + std::min<int64_t>(rank, rem);
+    *end = *begin + base + (rank < rem ? 1 : 0);
+    return DDKS_OK;
+}
+
+ddks_status ddks_get_nccl_id(void* out_128_bytes) {
+    ddks_ctx* ctx = nullptr;
+    if (!out_128_bytes) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "null id buffer");
+    ncclUniqueId id;
+    NC(ncclGetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    memcpy(out_128_bytes, &id, 128);
+    return DDKS_OK;
+}
+
+ddks_status ddks_create(ddks_ctx** out, int device, int world, int rank, const void* nccl_id, uint32_t flags) {
+    ddks_ctx* ctx = nullptr;
+    if (!out) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "null out");
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad world/rank");
+    if ((world == 1) != (nccl_id == nullptr))
+        return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "nccl_id must be NULL iff world == 1");
+    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
+    int ndev = 0;
+    CU(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device %d of %d", device, ndev);
+    CU(cudaSetDevice(device));
+    ctx = new ddks_ctx();
+    ctx->device = device;
+    ctx->world = world;
+    ctx->rank = rank;
+    ctx->flags = flags;
+    if (world > 1) {
+        ncclUniqueId id;
+        memcpy(&id, nccl_id, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&ctx->comm, world, id, rank);
+        if (r != ncclSuccess) {
+            fail(nullptr, DDKS_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+            delete ctx;
+            return DDKS_ERR_NCCL;
+        }
+    }
+    ddks_status s = ensure(ctx, ctx->res, sizeof(DevResult));
+    if (!s) s = ensure_host(ctx, 4096);
+    if (s) {
+        g_create_err = ctx->err;
+        ddks_destroy(ctx);
+        return s;
+    }
+    *out = ctx;
+    return DDKS_OK;
+}
+
+ddks_status ddks_destroy(ddks_ctx* ctx) {
+    if (!ctx) return DDKS_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    for (DevBuf* b : {&ctx->raw_a, &ctx->raw_b, &ctx->raw_perm, &ctx->packed, &ctx->packed2, &ctx->pool_packed, &ctx->per_origin,
+                      &ctx->accum, &ctx->item_num, &ctx->bitmap, &ctx->res})
+        if (b->p) cudaFree(b->p);
+    if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
+    delete ctx;
+    return DDKS_OK;
+}
+
+const char* ddks_last_error(const ddks_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+int64_t ddks_launch_count(const ddks_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// a1-a7 for one pair, origins sharded across ranks; optional per-origin export (debug path, single rank).
+static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
+                             void* stream, ddks_result* out, int64_t o_begin_req, int64_t o_end_req,
+                             uint64_t* per_origin_out) {
+    ctx->err.clear();
+    ddks_status s = check_sizes(ctx, n_P, n_Q, d);
+    if (s) return s;
+    if (!P || !Q) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "null argument");
+    s = bind_device(ctx);
+    if (s) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t N = n_P + n_Q;
+    const int DP = pad_dim(d);
+    const bool export_mode = per_origin_out != nullptr;
+    int64_t ob, oe;
+    if (export_mode) {
+        ob = o_begin_req;
+        oe = o_end_req;
+    } else {
+        ddks_shard_range(N, ctx->world, ctx->rank, &ob, &oe);
+    }
+    const void *dP, *dQ;
+    if ((s = stage_input(ctx, P, (size_t)n_P * d * 4, ctx->raw_a, st, &dP))) return s;
+    if ((s = stage_input(ctx, Q, (size_t)n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
+    if ((s = ensure(ctx, ctx->packed, (size_t)N * DP * 4))) return s;
+    if ((s = ensure(ctx, ctx->per_origin, (size_t)std::max<int64_t>(oe - ob, 1) * 8))) return s;
+    DevResult* dres = (DevResult*)ctx->res.p;
+    DevResult init{0ull, ~0ull, 0u, 0u};
+    DevResult* hres = (DevResult*)ctx->host_pinned;
+    *hres = init;
+    CU(cudaMemcpyAsync(dres, hres, sizeof init, cudaMemcpyHostToDevice, st));
+    float* packed = (float*)ctx->packed.p;
+    if ((s = launch_pack(ctx, (const float*)dP, n_P, d, 1, packed, N, 0, &dres->flag, st))) return s;
+    if ((s = launch_pack(ctx, (const float*)dQ, n_Q, d, 1, packed, N, n_P, &dres->flag, st))) return s;
+    uint64_t* per = (uint64_t*)ctx->per_origin.p;
+    if (oe > ob) {
+        if ((s = run_count(ctx, packed, d, 1, n_P, n_Q, ob, oe, (uint64_t*)&dres->num, per, st))) return s;
+        if (!export_mode) {
+            const int64_t n = oe - ob;
+            const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 4);
+            if (ctx->world > 1) {
+                NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
+            }
+            ddks::k_argmax<<<blocks, 256, 0, st>>>(per, n, ob, (const uint64_t*)&dres->num, &dres->arg);
+            CHECK_LAUNCH();
+            ctx->launches++;
+        }
+    } else if (ctx->world > 1 && !export_mode) {
+        NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
+    }
+    if (ctx->world > 1 && !export_mode) {
+        NC(ncclAllReduce(&dres->arg, &dres->arg, 1, ncclUint64, ncclMin, ctx->comm, st));
+        NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
+    }
+    if (export_mode && oe > ob) {
+        CU(cudaMemcpyAsync(per_origin_out, per, (size_t)(oe - ob) * 8, cudaMemcpyDefault, st));
+    }
+    CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
+    if (out) {
+        out->num = hres->num;
+        out->den = (uint64_t)n_P * (uint64_t)n_Q;
+        out->D = (double)out->num / (double)out->den;
+        out->argmax_origin = hres->arg == ~0ull ? -1 : (int64_t)hres->arg;
+    }
+    return DDKS_OK;
+}
+
+ddks_status ddks_stat(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
+                      void* stream, ddks_result* out) {
+    if (!ctx) return DDKS_ERR_INVALID_ARGUMENT;
+    if (!out) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "null out");
+    return stat_impl(ctx, P, n_P, Q, n_Q, d, stream, out, 0, 0, nullptr);
+}
+
+ddks_status ddks_stat_per_origin(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
+                                 int64_t o_begin, int64_t o_end, uint64_t* num_out, void* stream) {
+    if (!ctx) return DDKS_ERR_INVALID_ARGUMENT;
+    if (!num_out) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "null num_out");
+    if (o_begin < 0 || o_end < o_begin || o_end > n_P + n_Q)
+        return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad origin range [%lld, %lld)", (long long)o_begin, (long long)o_end);
+    if (o_end == o_begin) {
+        ddks_status s = check_sizes(ctx, n_P, n_Q, d);
+        return s;
+    }
+    return stat_impl(ctx, P, n_P, Q, n_Q, d, stream, nullptr, o_begin, o_end, num_out);
+}
+
+// Items [i0, i1) of an already-packed batch -> nums into dev item_num[i0..i1).
+static ddks_status all_gather_items(ddks_ctx* ctx, uint64_t* dev_nums, int64_t total, cudaStream_t st) {
+    // every rank owns a contiguous shard; NCCL all-gather needs equal counts -> pad to the largest shard
+    int64_t b0, b1;
+    ddks_shard_range(total, ctx->world, 0, &b0, &b1);
+    const int64_t chunk = b1 - b0;  // rank 0 holds the largest shard
+    ddks_status s = ensure(ctx, ctx->packed2, (size_t)chunk * ctx->world * 8);
+    if (s) return s;
+    int64_t mb, me;
+    ddks_shard_range(total, ctx->world, ctx->rank, &mb, &me);
+    uint64_t* gathered = (uint64_t*)ctx->packed2.p;
+    NC(ncclAllGather(dev_nums + mb, gathered, (size_t)chunk, ncclUint64, ctx->comm, st));
+    for (int r = 0; r < ctx->world; ++r) {
+        int64_t rb, re;
+        ddks_shard_range(total, ctx->world, r, &rb, &re);
+        if (re > rb)
+            CU(cudaMemcpyAsync(dev_nums + rb, gathered + (int64_t)r * chunk, (size_t)(re - rb) * 8,
+                               cudaMemcpyDeviceToDevice, st));
+    }
+    return DDKS_OK;
+}
+
+ddks_status ddks_stat_batch(ddks_ctx* ctx, const float* P, const float* Q, int64_t B, int64_t n_P, int64_t n_Q,
+                            int32_t d, void* stream, ddks_result* out) {
+    if (!ctx) return DDKS_ERR_INVALID_ARGUMENT;
+    ctx->err.clear();
+    if (B < 1) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "B=%lld < 1", (long long)B);
+    ddks_status s = check_sizes(ctx, n_P, n_Q, d);
+    if (s) return s;
+    if (!P || !Q || !out) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "null argument");
+    if ((s = bind_device(ctx))) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t N = n_P + n_Q;
+    const int DP = pad_dim(d);
+    int64_t ib, ie;
+    ddks_shard_range(B, ctx->world, ctx->rank, &ib, &ie);
+    const void *dP, *dQ;
+    if ((s = stage_input(ctx, P, (size_t)B * n_P * d * 4, ctx->raw_a, st, &dP))) return s;
+    if ((s = stage_input(ctx, Q, (size_t)B * n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
+    if ((s = ensure(ctx, ctx->item_num, (size_t)B * 8))) return s;
+    uint64_t* nums = (uint64_t*)ctx->item_num.p;
+    CU(cudaMemsetAsync(nums, 0, (size_t)B * 8, st));
+    DevResult* dres = (DevResult*)ctx->res.p;
+    CU(cudaMemsetAsync(dres, 0, sizeof(DevResult), st));
+    const int64_t nb = ie - ib;
+    if (nb > 0) {
+        if ((s = ensure(ctx, ctx->packed, (size_t)nb * N * DP * 4))) return s;
+        float* packed = (float*)ctx->packed.p;
+        if ((s = launch_pack(ctx, (const float*)dP + ib * n_P * d, n_P, d, nb, packed, N, 0, &dres->flag, st))) return s;
+        if ((s = launch_pack(ctx, (const float*)dQ + ib * n_Q * d, n_Q, d, nb, packed, N, n_P, &dres->flag, st))) return s;
+        if ((s = run_count(ctx, packed, d, nb, n_P, n_Q, 0, N, nums + ib, nullptr, st))) return s;
+    }
+    if (ctx->world > 1) {
+        if ((s = all_gather_items(ctx, nums, B, st))) return s;
+        NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
+    }
+    if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)B * 8))) return s;
+    DevResult* hres = (DevResult*)ctx->host_pinned;
+    uint64_t* hnums = (uint64_t*)((char*)ctx->host_pinned + sizeof(DevResult));
+    CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(hnums, nums, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
+    const uint64_t den = (uint64_t)n_P * (uint64_t)n_Q;
+    for (int64_t b = 0; b < B; ++b) {
+        out[b].num = hnums[b];
+        out[b].den = den;
+        out[b].D = (double)hnums[b] / (double)den;
+        out[b].argmax_origin = -1;
+    }
+    return DDKS_OK;
+}
+
+ddks_status ddks_permutation_null(ddks_ctx* ctx, const float* pooled, int64_t n_P, int64_t n_Q, int32_t d,
+                                  const int32_t* perms, int64_t n_perm, void* stream, uint64_t* null_num,
+                                  ddks_result* observed, double* p_value) {
+    if (!ctx) return DDKS_ERR_INVALID_ARGUMENT;
+    ctx->err.clear();
+    if (n_perm < 0) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "n_perm < 0");
+    ddks_status s = check_sizes(ctx, n_P, n_Q, d);
+    if (s) return s;
+    if (!pooled || (n_perm > 0 && !perms)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "null argument");
+    if ((s = bind_device(ctx))) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t N = n_P + n_Q;
+    const int DP = pad_dim(d);
+    const void *dpool, *dperm = nullptr;
+    if ((s = stage_input(ctx, pooled, (size_t)N * d * 4, ctx->raw_a, st, &dpool))) return s;
+    if (n_perm > 0 && (s = stage_input(ctx, perms, (size_t)n_perm * N * 4, ctx->raw_perm, st, &dperm))) return s;
+    // slot 0 = observed (identity split), slots 1..n_perm = permutations
+    const int64_t total = n_perm + 1;
+    if ((s = ensure(ctx, ctx->item_num, (size_t)total * 8))) return s;
+    uint64_t* nums = (uint64_t*)ctx->item_num.p;
+    CU(cudaMemsetAsync(nums, 0, (size_t)total * 8, st));
+    DevResult* dres = (DevResult*)ctx->res.p;
+    CU(cudaMemsetAsync(dres, 0, sizeof(DevResult), st));
+    // pack the pooled sample once: [N][DP]
+    if ((s = ensure(ctx, ctx->pool_packed, (size_t)N * DP * 4))) return s;
+    float* pooled_packed = (float*)ctx->pool_packed.p;
+    if ((s = launch_pack(ctx, (const float*)dpool, N, d, 1, pooled_packed, N, 0, &dres->flag, st))) return s;
+    // observed: every rank computes it (cheap relative to the null), no collective needed
+    if ((s = run_count(ctx, pooled_packed, d, 1, n_P, n_Q, 0, N, nums, nullptr, st))) return s;
+    int64_t jb, je;
+    ddks_shard_range(n_perm, ctx->world, ctx->rank, &jb, &je);
+    const int64_t chunk_max = std::max<int64_t>(1, (int64_t)((256ull << 20) / ((size_t)N * DP * 4)));
+    for (int64_t j0 = jb; j0 < je; j0 += chunk_max) {
+        const int64_t nc = std::min(chunk_max, je - j0);
+        if ((s = ensure(ctx, ctx->packed, (size_t)nc * N * DP * 4))) return s;
+        const int64_t words = (N + 31) / 32;
+        if ((s = ensure(ctx, ctx->bitmap, (size_t)nc * words * 4))) return s;
+        CU(cudaMemsetAsync(ctx->bitmap.p, 0, (size_t)nc * words * 4, st));
+        const int64_t tot = nc * N;
+        const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
+        if (DP == 4)
+            ddks::k_gather<4><<<blocks, 256, 0, st>>>(pooled_packed, (const int32_t*)dperm + j0 * N, nc, N,
+                                                      (float*)ctx->packed.p, (uint32_t*)ctx->bitmap.p, &dres->flag);
+        else
+            ddks::k_gather<8><<<blocks, 256, 0, st>>>(pooled_packed, (const int32_t*)dperm + j0 * N, nc, N,
+                                                      (float*)ctx->packed.p, (uint32_t*)ctx->bitmap.p, &dres->flag);
+        CHECK_LAUNCH();
+        ctx->launches++;
+        if ((s = run_count(ctx, (const float*)ctx->packed.p, d, nc, n_P, n_Q, 0, N, nums + 1 + j0, nullptr, st)))
+            return s;
+    }
+    if (ctx->world > 1) {
+        if ((s = all_gather_items(ctx, nums + 1, n_perm, st))) return s;
+        NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
+    }
+    if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)total * 8))) return s;
+    DevResult* hres = (DevResult*)ctx->host_pinned;
+    uint64_t* hnums = (uint64_t*)((char*)ctx->host_pinned + sizeof(DevResult));
+    CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(hnums, nums, (size_t)total * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
+    if (hres->flag & 2u) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "a perms row is not a permutation of 0..N-1");
+    const uint64_t obs = hnums[0];
+    int64_t ge = 0;
+    for (int64_t j = 0; j < n_perm; ++j) {
+        if (null_num) null_num[j] = hnums[1 + j];
+        if (hnums[1 + j] >= obs) ++ge;
+    }
+    if (observed) {
+        observed->num = obs;
+        observed->den = (uint64_t)n_P * (uint64_t)n_Q;
+        observed->D = (double)obs / (double)observed->den;
+        observed->argmax_origin = -1;
+    }
+    if (p_value) *p_value = (double)(1 + ge) / (double)(1 + n_perm);
+    return DDKS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,394 @@
+// ddks_kernels.cuh — sm_100a kernels of the exact ddKS hot path (SURVEY.md §8a rows a1–a9).
+//
+// The statistic (Eq. 1-2, Eq. 3, Eq. 6):
+//   for every pooled origin o (P rows, then Q rows) and every pooled point x:
+//       code(o, x) = sum_k [x_k >= o_k] 2^k          (FP32 ordered compare, no FTZ)
+//       c_P[o][code]++ if x in P else c_Q[o][code]++
+//   num(o) = max_q |c_P[o][q] n_Q - c_Q[o][q] n_P|, num = max_o num(o), den = n_P n_Q.
+//
+// B200 design:
+//   * one thread owns R origins (coordinates in registers); a CTA of T threads owns R*T origins;
+//   * point tiles are streamed HBM/L2 -> SMEM with cp.async.bulk (TMA bulk engine, UBLKCP) into an
+//     S-stage ring guarded by mbarriers; every thread reads each point as a broadcast LDS.128;
+//   * each pair costs d FSET.BF (ALU pipe, the compare roofline) + d FFMA-immediate (FMA pipe) that build
+//     the histogram *byte address* inside a float whose bit pattern is 0x4B000000 + offset, + one
+//     fire-and-forget ATOMS.ADD to a thread-private, bank-conflict-free SMEM counter;
+//   * DIFF mode keeps one signed counter per orthant: c_P*a - c_Q*b with a = n_Q/g, b = n_P/g
+//     (g = gcd(n_P, n_Q)), so |counter| * g is exactly |c_P n_Q - c_Q n_P| (P:L238 cross-multiplied);
+//     SPLIT mode (only when n_P n_Q / g >= 2^31) keeps c_P and c_Q separately;
+//   * finalisation is exact integer arithmetic; the max is a warp-shuffle + CTA + atomicMax(u64) reduction.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ddks {
+
+// ----------------------------------------------------------------------------------------------- config
+template <int D> struct Cfg;
+// R origins per thread, T threads per CTA, TILE points per SMEM stage, S stages.
+// SMEM histogram = 2^D bins x R x T x 4 B (x2 in SPLIT mode) kept at <= 128 KB.
+template <> struct Cfg<1> { static constexpr int R = 4, T = 256, TILE = 512, S = 3; };
+template <> struct Cfg<2> { static constexpr int R = 4, T = 256, TILE = 512, S = 3; };
+template <> struct Cfg<3> { static constexpr int R = 4, T = 256, TILE = 512, S = 3; };
+template <> struct Cfg<4> { static constexpr int R = 4, T = 256, TILE = 512, S = 3; };
+template <> struct Cfg<5> { static constexpr int R = 4, T = 256, TILE = 256, S = 3; };
+template <> struct Cfg<6> { static constexpr int R = 2, T = 256, TILE = 256, S = 3; };
+template <> struct Cfg<7> { static constexpr int R = 1, T = 256, TILE = 256, S = 3; };
+template <> struct Cfg<8> { static constexpr int R = 1, T = 128, TILE = 256, S = 3; };
+
+template <int D> __host__ __device__ constexpr int padded_dim() { return D <= 4 ? 4 : 8; }
+
+template <int D, bool SPLIT> struct Geo {
+    static constexpr int R = (SPLIT && Cfg<D>::R > 1) ? Cfg<D>::R / 2 : Cfg<D>::R;
+    static constexpr int T = (SPLIT && Cfg<D>::R == 1) ? Cfg<D>::T / 2 : Cfg<D>::T;
+    static constexpr int TILE = Cfg<D>::TILE;
+    static constexpr int S = Cfg<D>::S;
+    static constexpr int DP = padded_dim<D>();
+    static constexpr int NB = (1 << D) * (SPLIT ? 2 : 1);      // counters per origin
+    static constexpr int HIST_WORDS = NB * R * T;
+    static constexpr int TILE_BYTES = TILE * DP * 4;
+    static constexpr int SMEM_BYTES = S * TILE_BYTES + HIST_WORDS * 4 + 64;
+    static constexpr int ORIGINS = R * T;
+};
+
+// ----------------------------------------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "DDKS_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra DDKS_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> shared through the TMA engine, completion counted on an mbarrier (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// FP32 ordered compare -> 1.0f / 0.0f (SASS FSET.BF). No .ftz: denormals compare exactly (R6).
+template <bool GT> __device__ __forceinline__ float cmp_bit(float x, float o) {
+    float r;
+    if constexpr (GT) asm("set.gt.f32.f32 %0, %1, %2;" : "=f"(r) : "f"(x), "f"(o));
+    else              asm("set.ge.f32.f32 %0, %1, %2;" : "=f"(r) : "f"(x), "f"(o));
+    return r;
+}
+__device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+template <int D> __device__ __forceinline__ void load_point(const float* sp, float (&x)[D]) {
+    const float4 a = *reinterpret_cast<const float4*>(sp);
+    if constexpr (D >= 1) x[0] = a.x;
+    if constexpr (D >= 2) x[1] = a.y;
+    if constexpr (D >= 3) x[2] = a.z;
+    if constexpr (D >= 4) x[3] = a.w;
+    if constexpr (D >= 5) {
+        if constexpr (D == 5) {
+            x[4] = sp[4];
+        } else {
+            const float4 b = *reinterpret_cast<const float4*>(sp + 4);
+            x[4] = b.x;
+            if constexpr (D >= 6) x[5] = b.y;
+            if constexpr (D >= 7) x[6] = b.z;
+            if constexpr (D >= 8) x[7] = b.w;
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------------------------- a1: validate + pack
+// src: [B][n_rows][d] row-major f32. dst: [B][N][DP] with the segment's rows at row offset `row_off`.
+// -0 -> +0, pad dims = 0. Non-finite -> *flag |= 1 (SPEC core-types NonFiniteValue).
+__global__ void k_pack(const float* __restrict__ src, int64_t n_rows, int d, int64_t B, float* __restrict__ dst,
+                       int64_t N, int64_t row_off, int DP, int validate, uint32_t* flag) {
+    const int64_t total = B * n_rows;
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / n_rows, r = i - b * n_rows;
+        const float* s = src + i * d;
+        float v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            float t = (k < d) ? s[k] : 0.0f;
+            if (k < d && validate && !isfinite(t)) bad = true;
+            v[k] = (t == 0.0f) ? 0.0f : t;
+        }
+        float4* o = reinterpret_cast<float4*>(dst + ((b * N) + row_off + r) * DP);
+        o[0] = make_float4(v[0], v[1], v[2], v[3]);
+        if (DP == 8) o[1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
+    if (bad) atomicOr(flag, 1u);
+}
+
+// Permutation gather (a9): dst[j][i] = pooled[perm[j][i]]; checks every row is a permutation of 0..N-1
+// (range + no duplicates via a per-row bitmap), else *flag |= 2.
+template <int DP>
+__global__ void k_gather(const float* __restrict__ pooled, const int32_t* __restrict__ perms, int64_t n_perm,
+                         int64_t N, float* __restrict__ dst, uint32_t* __restrict__ bitmap, uint32_t* flag) {
+    const int64_t words = (N + 31) / 32;
+    const int64_t total = n_perm * N;
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = i / N;
+        const int32_t src = perms[i];
+        if (src < 0 || src >= N) { bad = true; continue; }
+        const uint32_t bit = 1u << (src & 31);
+        const uint32_t old = atomicOr(&bitmap[j * words + (src >> 5)], bit);
+        if (old & bit) bad = true;
+        const float4* s = reinterpret_cast<const float4*>(pooled + (int64_t)src * DP);
+        float4* o = reinterpret_cast<float4*>(dst + i * DP);
+        o[0] = s[0];
+        if (DP == 8) o[1] = s[1];
+    }
+    if (bad) atomicOr(flag, 2u);
+}
+
+// ----------------------------------------------------------------------------------------------- a3-a6: count
+struct CountArgs {
+    const float* pts;        // packed [B][N][DP]
+    int64_t item_stride;     // floats per item = N * DP
+    int32_t N, n_P;          // pooled points per item; the first n_P are P
+    int32_t o_begin, o_end;  // origin range (pooled indices) this launch owns, per item
+    int32_t seg_points;      // points per grid.z segment (multiple of TILE)
+    uint32_t incP, incQ;     // DIFF: +a and -b (two's complement); SPLIT: 1 and 1
+    uint64_t g;              // DIFF: gcd(n_P, n_Q) multiplier
+    int64_t nP, nQ;          // SPLIT finalisation
+    uint64_t* item_num;      // [B] atomicMax target (direct mode)
+    uint64_t* per_origin;    // [o_end - o_begin] or nullptr (direct mode, B == 1)
+    uint32_t* accum;         // accumulate mode: [B][NB][n_orig] int32 counters (grid.z > 1), else nullptr
+};
+
+template <int D, bool SPLIT>
+__device__ __forceinline__ uint64_t origin_num(const uint32_t* hist, int r, int t, const CountArgs& a) {
+    using G = Geo<D, SPLIT>;
+    constexpr int NQ = 1 << D;
+    uint64_t best = 0;
+    if constexpr (!SPLIT) {
+        uint32_t m = 0;
+#pragma unroll 4
+        for (int q = 0; q < NQ; ++q) {
+            const int32_t v = (int32_t)hist[(q * G::R + r) * G::T + t];
+            const uint32_t av = (uint32_t)(v < 0 ? -v : v);
+            m = av > m ? av : m;
+        }
+        best = (uint64_t)m * a.g;
+    } else {
+#pragma unroll 4
+        for (int q = 0; q < NQ; ++q) {
+            const int64_t cP = (int64_t)hist[(q * G::R + r) * G::T + t];
+            const int64_t cQ = (int64_t)hist[((NQ + q) * G::R + r) * G::T + t];
+            const int64_t df = cP * a.nQ - cQ * a.nP;
+            const uint64_t av = (uint64_t)(df < 0 ? -df : df);
+            best = av > best ? av : best;
+        }
+    }
+    return best;
+}
+
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+
+template <int D, bool SPLIT, bool GT>
+__global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a) {
+    using G = Geo<D, SPLIT>;
+    constexpr int R = G::R, T = G::T, DP = G::DP, TILE = G::TILE, S = G::S;
+    extern __shared__ __align__(128) uint8_t smem[];
+    float* tiles = reinterpret_cast<float*>(smem);                                  // [S][TILE][DP]
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + S * G::TILE_BYTES);          // [NB][R][T]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * G::TILE_BYTES + G::HIST_WORDS * 4);
+
+    const int t = threadIdx.x;
+    const int64_t item = blockIdx.x;
+    const float* pts = a.pts + item * a.item_stride;
+    const int32_t blk_o0 = a.o_begin + (int32_t)blockIdx.y * G::ORIGINS;
+    const int32_t seg0 = (int32_t)blockIdx.z * a.seg_points;
+    const int32_t seg1 = min(a.N, seg0 + a.seg_points);
+    const int n_tiles = (seg1 - seg0 + TILE - 1) / TILE;
+
+    if (t == 0) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = t; i < G::HIST_WORDS; i += T) hist[i] = 0u;
+    __syncthreads();
+
+    // prologue: fill the ring
+    if (t == 0) {
+        for (int s = 0; s < S && s < n_tiles; ++s) {
+            const int32_t p0 = seg0 + s * TILE;
+            const uint32_t bytes = (uint32_t)(min(TILE, seg1 - p0) * DP * 4);
+            mbar_expect_tx(&bars[s], bytes);
+            bulk_g2s(tiles + s * TILE * DP, pts + (int64_t)p0 * DP, bytes, &bars[s]);
+        }
+    }
+
+    // origins owned by this thread: o = blk_o0 + r*T + t (clamped to a valid origin; ignored at the end)
+    float o[R][D];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        int32_t oi = blk_o0 + r * T + t;
+        oi = oi < a.o_end ? oi : a.o_end - 1;
+        const float* op = pts + (int64_t)oi * DP;
+#pragma unroll
+        for (int k = 0; k < D; ++k) o[r][k] = __ldg(op + k);
+    }
+
+    // the histogram byte address lives in the mantissa of a float in [2^23, 2^24): bits = 0x4B000000 + offset
+    const uint32_t ubase = smem_u32(hist) - 0x4B000000u;
+    float baseP[R], baseQ[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        baseP[r] = __uint_as_float(0x4B000000u + 4u * (uint32_t)(r * T + t));
+        baseQ[r] = SPLIT ? __uint_as_float(0x4B000000u + 4u * (uint32_t)(((1 << D) * R + r) * T + t)) : baseP[r];
+    }
+
+    for (int it = 0; it < n_tiles; ++it) {
+        const int s = it % S;
+        mbar_wait(&bars[s], (uint32_t)((it / S) & 1));
+        const float* tile = tiles + s * TILE * DP;
+        const int32_t p0 = seg0 + it * TILE;
+        const int32_t cnt = min(TILE, seg1 - p0);
+        // sample-homogeneous sub-ranges: [p0, n_P) are P points, [n_P, ...) are Q points
+        int32_t split = a.n_P - p0;
+        split = split < 0 ? 0 : (split > cnt ? cnt : split);
+#pragma unroll 1
+        for (int phase = 0; phase < 2; ++phase) {
+            const int32_t lo = phase == 0 ? 0 : split;
+            const int32_t hi = phase == 0 ? split : cnt;
+            const uint32_t inc = phase == 0 ? a.incP : a.incQ;
+            float base[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) base[r] = phase == 0 ? baseP[r] : baseQ[r];
+#pragma unroll 2
+            for (int32_t p = lo; p < hi; ++p) {
+                float x[D];
+                load_point<D>(tile + p * DP, x);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    float f = base[r];
+#pragma unroll
+                    for (int k = 0; k < D; ++k)
+                        f = fmaf(cmp_bit<GT>(x[k], o[r][k]), (float)(4 * (1 << k) * R * T), f);
+                    red_add_shared(__float_as_uint(f) + ubase, inc);
+                }
+            }
+        }
+        __syncthreads();  // every thread is done with stage s
+        if (t == 0 && it + S < n_tiles) {
+            fence_proxy_async();
+            const int32_t q0 = seg0 + (it + S) * TILE;
+            const uint32_t bytes = (uint32_t)(min(TILE, seg1 - q0) * DP * 4);
+            mbar_expect_tx(&bars[s], bytes);
+            bulk_g2s(tiles + s * TILE * DP, pts + (int64_t)q0 * DP, bytes, &bars[s]);
+        }
+    }
+    __syncthreads();  // all red.shared retired before reading the histogram
+
+    const int32_t n_orig = a.o_end - a.o_begin;
+    if (a.accum != nullptr) {
+        // accumulate mode (grid.z > 1 point segments): exact int32 partial counts -> global, finalised later
+        uint32_t* acc = a.accum + item * (int64_t)G::NB * n_orig;
+#pragma unroll 1
+        for (int r = 0; r < R; ++r) {
+            const int32_t oi = blk_o0 + r * T + t;
+            if (oi >= a.o_end) continue;
+            for (int q = 0; q < G::NB; ++q) {
+                const uint32_t v = hist[(q * R + r) * T + t];
+                if (v) atomicAdd(&acc[(int64_t)q * n_orig + (oi - a.o_begin)], v);
+            }
+        }
+        return;
+    }
+    uint64_t best = 0;
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) {
+        const int32_t oi = blk_o0 + r * T + t;
+        if (oi >= a.o_end) continue;
+        const uint64_t m = origin_num<D, SPLIT>(hist, r, t, a);
+        if (a.per_origin) a.per_origin[oi - a.o_begin] = m;
+        best = m > best ? m : best;
+    }
+    best = warp_max_u64(best);
+    __shared__ uint64_t wmax[32];
+    if ((t & 31) == 0) wmax[t >> 5] = best;
+    __syncthreads();
+    if (t == 0) {
+        uint64_t m = 0;
+        for (int w = 0; w < T / 32; ++w) m = wmax[w] > m ? wmax[w] : m;
+        atomicMax(reinterpret_cast<unsigned long long*>(&a.item_num[item]), (unsigned long long)m);
+    }
+}
+
+// Finalise accumulate mode: one thread per (item, origin).
+template <int D, bool SPLIT>
+__global__ void k_finalize(const CountArgs a, int64_t B) {
+    constexpr int NQ = 1 << D;
+    constexpr int NB = Geo<D, SPLIT>::NB;
+    const int32_t n_orig = a.o_end - a.o_begin;
+    const int64_t total = B * (int64_t)n_orig;
+    uint64_t best = 0;
+    int64_t item_of_best = -1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t item = i / n_orig, oi = i - item * n_orig;
+        const uint32_t* acc = a.accum + item * (int64_t)NB * n_orig + oi;
+        uint64_t m = 0;
+        if constexpr (!SPLIT) {
+            uint32_t mm = 0;
+            for (int q = 0; q < NQ; ++q) {
+                const int32_t v = (int32_t)acc[(int64_t)q * n_orig];
+                const uint32_t av = (uint32_t)(v < 0 ? -v : v);
+                mm = av > mm ? av : mm;
+            }
+            m = (uint64_t)mm * a.g;
+        } else {
+            for (int q = 0; q < NQ; ++q) {
+                const int64_t cP = (int64_t)acc[(int64_t)q * n_orig];
+                const int64_t cQ = (int64_t)acc[(int64_t)(NQ + q) * n_orig];
+                const int64_t df = cP * a.nQ - cQ * a.nP;
+                const uint64_t av = (uint64_t)(df < 0 ? -df : df);
+                m = av > m ? av : m;
+            }
+        }
+        if (a.per_origin && B == 1) a.per_origin[oi] = m;
+        if (B == 1) {
+            best = m > best ? m : best;
+        } else {
+            atomicMax(reinterpret_cast<unsigned long long*>(&a.item_num[item]), (unsigned long long)m);
+        }
+        (void)item_of_best;
+    }
+    if (B == 1) {
+        best = warp_max_u64(best);
+        if ((threadIdx.x & 31) == 0)
+            atomicMax(reinterpret_cast<unsigned long long*>(&a.item_num[0]), (unsigned long long)best);
+    }
+}
+
+// argmax (reading R7): smallest pooled origin index whose num(o) equals the global num.
+__global__ void k_argmax(const uint64_t* __restrict__ per_origin, int64_t n, int64_t o_begin,
+                         const uint64_t* __restrict__ num, unsigned long long* __restrict__ arg) {
+    const uint64_t target = *num;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (per_origin[i] == target) atomicMin(arg, (unsigned long long)(o_begin + i));
+}
+
+}  // namespace ddks

@@ -1,0 +1,236 @@
+"""Thin ctypes binding over libddks.so (include/ddks.h). Argument marshalling only: every step of the
+hot path runs in the library's sm_100a kernels. There is no CPU fallback — if the extension is missing
+this module raises at import, and on a machine without a GPU ddks_create returns DDKS_ERR_CUDA.
+
+Inputs may be torch tensors (CUDA: read in place on the current torch stream; CPU: copied H2D inside the
+library call, which is what the end-to-end measurement times) or NumPy arrays (host). Names mirror the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import NamedTuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libddks.so")
+
+DDKS_OK = 0
+STATUS = {0: "DDKS_OK", 1: "DDKS_ERR_INVALID_ARGUMENT", 2: "DDKS_ERR_EMPTY_SAMPLE", 3: "DDKS_ERR_DIM_UNSUPPORTED",
+          4: "DDKS_ERR_NONFINITE", 5: "DDKS_ERR_TOO_LARGE", 6: "DDKS_ERR_CUDA", 7: "DDKS_ERR_NCCL", 8: "DDKS_ERR_OOM"}
+DDKS_FLAG_DEFAULT = 0
+DDKS_FLAG_NO_VALIDATE = 1
+DDKS_FLAG_TIES_GT = 2
+DDKS_FLAG_FORCE_DIRECT = 4
+
+
+class DDKSError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class ddks_result(ctypes.Structure):
+    _fields_ = [("num", ctypes.c_uint64), ("den", ctypes.c_uint64), ("D", ctypes.c_double),
+                ("argmax_origin", ctypes.c_int64)]
+
+
+class Result(NamedTuple):
+    num: int
+    den: int
+    D: float
+    argmax_origin: int
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libddks.so not built at {LIB_PATH}; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is deliberately no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32, u32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32
+    sig = {
+        "ddks_get_nccl_id": ([vp], ctypes.c_int),
+        "ddks_create": ([ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, u32], ctypes.c_int),
+        "ddks_stat": ([vp, vp, i64, vp, i64, i32, vp, ctypes.POINTER(ddks_result)], ctypes.c_int),
+        "ddks_stat_batch": ([vp, vp, vp, i64, i64, i64, i32, vp, ctypes.POINTER(ddks_result)], ctypes.c_int),
+        "ddks_permutation_null": ([vp, vp, i64, i64, i32, vp, i64, vp, vp, ctypes.POINTER(ddks_result),
+                                   ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+        "ddks_stat_per_origin": ([vp, vp, i64, vp, i64, i32, i64, i64, vp, vp], ctypes.c_int),
+        "ddks_shard_range": ([i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)], ctypes.c_int),
+        "ddks_launch_count": ([vp], i64),
+        "ddks_destroy": ([vp], ctypes.c_int),
+        "ddks_last_error": ([vp], ctypes.c_char_p),
+        "ddks_version": ([], ctypes.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+LIB = _load()
+EXPORTED = ("ddks_get_nccl_id", "ddks_create", "ddks_stat", "ddks_stat_batch", "ddks_permutation_null",
+            "ddks_stat_per_origin", "ddks_shard_range", "ddks_launch_count", "ddks_destroy", "ddks_last_error",
+            "ddks_version")
+
+
+def _check(st: int, ctx=None):
+    if st != DDKS_OK:
+        raise DDKSError(st, (LIB.ddks_last_error(ctx) or b"").decode())
+
+
+class _Arg:
+    """Holds a pointer to a float32/int32 C-contiguous buffer (torch tensor or NumPy array) alive for a call."""
+
+    def __init__(self, x, dtype):
+        self.keep = None
+        try:
+            import torch
+            if isinstance(x, torch.Tensor):
+                tdt = torch.float32 if dtype == np.float32 else torch.int32
+                if x.dtype != tdt or not x.is_contiguous():
+                    x = x.to(tdt).contiguous()
+                self.keep = x
+                self.ptr = x.data_ptr()
+                self.shape = tuple(x.shape)
+                self.is_cuda = x.is_cuda
+                return
+        except ImportError:
+            pass
+        a = np.ascontiguousarray(np.asarray(x, dtype=dtype))
+        self.keep = a
+        self.ptr = a.ctypes.data
+        self.shape = a.shape
+        self.is_cuda = False
+
+
+def _stream(stream):
+    if stream is not None:
+        return ctypes.c_void_p(int(stream))
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    except ImportError:
+        pass
+    return ctypes.c_void_p(0)
+
+
+# ------------------------------------------------------------------------------------------ C-ABI mirrors
+
+def ddks_version() -> str:
+    return LIB.ddks_version().decode()
+
+
+def ddks_shard_range(total: int, world: int, rank: int):
+    b, e = ctypes.c_int64(), ctypes.c_int64()
+    _check(LIB.ddks_shard_range(total, world, rank, ctypes.byref(b), ctypes.byref(e)))
+    return b.value, e.value
+
+
+def ddks_get_nccl_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(LIB.ddks_get_nccl_id(buf))
+    return buf.raw
+
+
+def ddks_create(device: int = 0, world: int = 1, rank: int = 0, nccl_id: bytes | None = None,
+                flags: int = DDKS_FLAG_DEFAULT) -> ctypes.c_void_p:
+    ctx = ctypes.c_void_p()
+    idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+    _check(LIB.ddks_create(ctypes.byref(ctx), device, world, rank, idbuf, flags))
+    return ctx
+
+
+def ddks_destroy(ctx) -> None:
+    _check(LIB.ddks_destroy(ctx))
+
+
+def ddks_stat(ctx, P, Q, stream=None) -> Result:
+    p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
+    if len(p.shape) != 2 or len(q.shape) != 2 or p.shape[1] != q.shape[1]:
+        raise ValueError(f"P {p.shape} and Q {q.shape} must be [n, d] with the same d")
+    r = ddks_result()
+    _check(LIB.ddks_stat(ctx, p.ptr, p.shape[0], q.ptr, q.shape[0], p.shape[1], _stream(stream), ctypes.byref(r)), ctx)
+    return Result(r.num, r.den, r.D, r.argmax_origin)
+
+
+def ddks_stat_batch(ctx, P, Q, stream=None) -> list[Result]:
+    p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
+    if len(p.shape) != 3 or len(q.shape) != 3 or p.shape[0] != q.shape[0] or p.shape[2] != q.shape[2]:
+        raise ValueError(f"P {p.shape} and Q {q.shape} must be [B, n, d] with the same B and d")
+    B = p.shape[0]
+    out = (ddks_result * B)()
+    _check(LIB.ddks_stat_batch(ctx, p.ptr, q.ptr, B, p.shape[1], q.shape[1], p.shape[2], _stream(stream), out), ctx)
+    return [Result(o.num, o.den, o.D, o.argmax_origin) for o in out]
+
+
+def ddks_permutation_null(ctx, pooled, n_P: int, perms, stream=None):
+    """-> (null_num: np.uint64 [n_perm], observed: Result, p_value: float)."""
+    a = _Arg(pooled, np.float32)
+    pr = _Arg(perms, np.int32)
+    N, d = a.shape
+    n_perm = pr.shape[0] if len(pr.shape) == 2 else 0
+    if n_perm and pr.shape[1] != N:
+        raise ValueError(f"perms {pr.shape} must be [n_perm, {N}]")
+    null = np.zeros(n_perm, dtype=np.uint64)
+    obs = ddks_result()
+    pv = ctypes.c_double()
+    _check(LIB.ddks_permutation_null(ctx, a.ptr, n_P, N - n_P, d, pr.ptr if n_perm else None, n_perm, _stream(stream),
+                                     null.ctypes.data if n_perm else None, ctypes.byref(obs), ctypes.byref(pv)), ctx)
+    return null, Result(obs.num, obs.den, obs.D, obs.argmax_origin), pv.value
+
+
+def ddks_stat_per_origin(ctx, P, Q, o_begin: int, o_end: int, stream=None) -> np.ndarray:
+    p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
+    out = np.zeros(max(o_end - o_begin, 0), dtype=np.uint64)
+    _check(LIB.ddks_stat_per_origin(ctx, p.ptr, p.shape[0], q.ptr, q.shape[0], p.shape[1], o_begin, o_end,
+                                    out.ctypes.data if out.size else ctypes.c_void_p(8), _stream(stream)), ctx)
+    return out
+
+
+def ddks_launch_count(ctx) -> int:
+    return int(LIB.ddks_launch_count(ctx))
+
+
+class Context:
+    """RAII wrapper: ``with Context() as c: c.stat(P, Q)``."""
+
+    def __init__(self, device: int = 0, world: int = 1, rank: int = 0, nccl_id: bytes | None = None,
+                 flags: int = DDKS_FLAG_DEFAULT):
+        self.ctx = ddks_create(device, world, rank, nccl_id, flags)
+
+    def stat(self, P, Q, stream=None) -> Result:
+        return ddks_stat(self.ctx, P, Q, stream)
+
+    def stat_batch(self, P, Q, stream=None) -> list[Result]:
+        return ddks_stat_batch(self.ctx, P, Q, stream)
+
+    def permutation_null(self, pooled, n_P, perms, stream=None):
+        return ddks_permutation_null(self.ctx, pooled, n_P, perms, stream)
+
+    def stat_per_origin(self, P, Q, o_begin, o_end, stream=None):
+        return ddks_stat_per_origin(self.ctx, P, Q, o_begin, o_end, stream)
+
+    @property
+    def launch_count(self) -> int:
+        return ddks_launch_count(self.ctx)
+
+    def close(self):
+        if self.ctx is not None:
+            ddks_destroy(self.ctx)
+            self.ctx = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

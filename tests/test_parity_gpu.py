@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle, element by element on the same seeded inputs.
+The bar is bit-exact: num and den are integers, D is the same single IEEE division, argmax is the smallest
+pooled index attaining num (R7). Every test here needs a B200 (``-m gpu``)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import oracle as O  # noqa: E402
+from paper_2106_13706_b200 import ddks as K  # noqa: E402
+from paper_2106_13706_b200 import inputs as I  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = K.Context()
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def ctx_direct():
+    c = K.Context(flags=K.DDKS_FLAG_FORCE_DIRECT)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def ctx_gt():
+    c = K.Context(flags=K.DDKS_FLAG_TIES_GT)
+    yield c
+    c.close()
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def check_pair(ctx, P, Q, ties_gt=False, host=False):
+    want = O.ddks(P, Q, ties_gt=ties_gt)
+    got = ctx.stat(P if host else dev(P), Q if host else dev(Q))
+    assert (got.num, got.den, got.argmax_origin) == (want[0], want[1], want[3]), (got, want)
+    assert got.D == want[2] and np.float64(got.D).tobytes() == np.float64(want[2]).tobytes()
+    return got
+
+
+# ----------------------------------------------------------------------------------- worked examples
+
+def test_spec_and_hand_examples(ctx, golden_dir):
+    g = json.load(open(os.path.join(golden_dir, "spec_examples.json")))
+    for c in g["statistic"]:
+        P, Q = np.array(c["P"], np.float32), np.array(c["Q"], np.float32)
+        r = ctx.stat(dev(P), dev(Q))
+        assert r.num * c["D_den"] == r.den * c["D_num"], c["cite"]
+    h = json.load(open(os.path.join(golden_dir, "hand_examples.json")))
+    for c in h["cases"]:
+        P, Q = np.array(c["P"], np.float32), np.array(c["Q"], np.float32)
+        check_pair(ctx, P, Q)
+        r = ctx.stat(dev(P), dev(Q))
+        assert (r.num, r.den) == (c["ge"]["num"], c["ge"]["den"]), c["name"]
+
+
+def test_tie_flag(ctx_gt):
+    h = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "hand_examples.json")))
+    for c in h["cases"]:
+        if "gt" in c:
+            r = ctx_gt.stat(dev(np.array(c["P"], np.float32)), dev(np.array(c["Q"], np.float32)))
+            assert (r.num, r.den) == (c["gt"]["num"], c["gt"]["den"])
+
+
+# ----------------------------------------------------------------------------------- random parity
+
+SIZES = [(1, 1), (1, 7), (2, 3), (31, 33), (200, 200), (255, 257), (511, 513), (997, 1009), (1000, 2000),
+         (1500, 700), (2047, 2049)]
+
+
+@pytest.mark.parametrize("d", range(1, 9))
+@pytest.mark.parametrize("kind", ["normal", "grid", "mixed", "dup"])
+def test_random_parity_all_d(ctx, ctx_direct, d, kind):
+    for i, (n_P, n_Q) in enumerate(SIZES):
+        if d >= 7 and n_P * n_Q > 1_200_000:
+            continue
+        P, Q = I.random_pair(1000 * d + 17 * i + hash(kind) % 97, n_P, n_Q, d, kind)
+        check_pair(ctx, P, Q)
+        if i % 3 == 0:
+            check_pair(ctx_direct, P, Q)
+
+
+@pytest.mark.parametrize("d", [1, 3, 5, 8])
+def test_random_parity_ties_gt(ctx_gt, d):
+    for i, (n_P, n_Q) in enumerate([(33, 31), (500, 700), (1200, 1200)]):
+        P, Q = I.random_pair(77 + i + d, n_P, n_Q, d, "grid")
+        check_pair(ctx_gt, P, Q, ties_gt=True)
+
+
+def test_host_pointer_path_equals_device(ctx):
+    P, Q = I.random_pair(5, 3000, 2500, 5, "mixed")
+    a = check_pair(ctx, P, Q, host=True)
+    b = ctx.stat(dev(P), dev(Q))
+    assert a == b
+    c = ctx.stat(torch.from_numpy(P), torch.from_numpy(Q))  # CPU tensors -> host path
+    assert c == b
+
+
+def test_per_origin_export(ctx):
+    for d in (2, 5, 8):
+        P, Q = I.random_pair(40 + d, 1300, 1100, d, "mixed")
+        N = 2400
+        want = O.per_origin(P, Q)
+        got = ctx.stat_per_origin(dev(P), dev(Q), 0, N)
+        assert np.array_equal(got, want)
+        got = ctx.stat_per_origin(P, Q, 1299, 1302)
+        assert np.array_equal(got, want[1299:1302])
+
+
+def test_symmetry_identity_on_gpu(ctx):
+    for d in (1, 4, 6):
+        P, Q = I.random_pair(90 + d, 800, 600, d, "normal")
+        a, b = ctx.stat(dev(P), dev(Q)), ctx.stat(dev(Q), dev(P))
+        assert (a.num, a.den, a.D) == (b.num, b.den, b.D)
+        assert ctx.stat(dev(P), dev(P)).num == 0
+
+
+def test_split_counter_mode_sampled():
+    # n_P*n_Q/gcd >= 2^31 forces separate c_P, c_Q counters (SPLIT mode); check sampled origins one by one.
+    n_P, n_Q = 50_000, 49_999
+    P, Q = I.random_pair(3, n_P, n_Q, 3, "mixed")
+    with K.Context() as c:
+        idx = [0, 1, 2, 49_999, 50_000, 50_001, 99_998]
+        for o in idx:
+            assert int(c.stat_per_origin(dev(P), dev(Q), o, o + 1)[0]) == int(O.per_origin(P, Q, o, o + 1)[0]), o
+        r = c.stat(dev(P), dev(Q))
+        assert r.den == n_P * n_Q and 0 < r.num <= r.den
+        r2 = c.stat(dev(Q), dev(P))
+        assert r2.num == r.num
+
+
+# ----------------------------------------------------------------------------------- errors / edge cases
+
+def test_errors(ctx):
+    P = np.zeros((4, 3), np.float32)
+    bad = P.copy()
+    bad[2, 1] = np.nan
+    with pytest.raises(K.DDKSError) as e:
+        ctx.stat(dev(bad), dev(P))
+    assert e.value.status == 4
+    bad[2, 1] = np.inf
+    with pytest.raises(K.DDKSError) as e:
+        ctx.stat(dev(P), dev(bad))
+    assert e.value.status == 4
+    with pytest.raises(K.DDKSError) as e:
+        ctx.stat(dev(P), dev(np.zeros((0, 3), np.float32)))
+    assert e.value.status == 2
+    with pytest.raises(K.DDKSError) as e:
+        ctx.stat(dev(np.zeros((4, 9), np.float32)), dev(np.zeros((4, 9), np.float32)))
+    assert e.value.status == 3
+    # context still usable after errors
+    check_pair(ctx, *I.random_pair(1, 10, 12, 3, "grid"))
+    # invalid permutation rows
+    pooled = np.random.default_rng(0).standard_normal((10, 2)).astype(np.float32)
+    perms = np.stack([np.arange(10), np.arange(10)]).astype(np.int32)
+    perms[1, 3] = 4  # duplicate
+    with pytest.raises(K.DDKSError) as e:
+        ctx.permutation_null(dev(pooled), 5, dev(perms))
+    assert e.value.status == 1
+    perms[1, 3] = 10  # out of range
+    with pytest.raises(K.DDKSError):
+        ctx.permutation_null(dev(pooled), 5, dev(perms))
+
+
+def test_extreme_values(ctx):
+    f = np.float32
+    cases = [
+        (np.array([[-0.0]], f), np.array([[0.0]], f)),
+        (np.array([[1.401298464324817e-45]], f), np.array([[2.802596928649634e-45]], f)),
+        (np.array([[3.4e38, -3.4e38], [1.0, 1.0]], f), np.array([[-3.4e38, 3.4e38], [np.nextafter(f(1), f(2)), 1.0]], f)),
+        (np.full((600, 4), 7.0, f), np.full((300, 4), 7.0, f)),  # all identical -> D = 0
+    ]
+    for P, Q in cases:
+        check_pair(ctx, P, Q)
+
+
+# ----------------------------------------------------------------------------------- batch / permutation
+
+def test_batch_parity(ctx, ctx_direct):
+    rng = np.random.default_rng(21)
+    for (B, n_P, n_Q, d) in [(1, 5, 6, 2), (7, 33, 31, 4), (40, 128, 128, 3), (5, 700, 300, 5), (3, 90, 100, 8)]:
+        P = rng.standard_normal((B, n_P, d)).astype(np.float32)
+        Q = (rng.standard_normal((B, n_Q, d)) * 1.2).astype(np.float32)
+        Q[:, ::3] = np.round(Q[:, ::3])
+        want = O.batch(P, Q)
+        for c in (ctx, ctx_direct):
+            got = c.stat_batch(dev(P), dev(Q))
+            assert [r.num for r in got] == want.tolist()
+            assert all(r.den == n_P * n_Q for r in got)
+
+
+def test_permutation_parity(ctx):
+    rng = np.random.default_rng(22)
+    for (n_P, n_Q, d, n_perm) in [(20, 20, 1, 30), (100, 80, 3, 50), (300, 300, 5, 12)]:
+        pooled = rng.standard_normal((n_P + n_Q, d)).astype(np.float32)
+        perms = np.stack([np.arange(n_P + n_Q)] + [rng.permutation(n_P + n_Q) for _ in range(n_perm - 1)]).astype(np.int32)
+        null, obs, p_num, p = O.permutation_null(pooled, n_P, perms)
+        g_null, g_obs, g_p = ctx.permutation_null(dev(pooled), n_P, dev(perms))
+        assert np.array_equal(g_null, null) and g_obs.num == obs and g_p == p
+        g_null2, _, _ = ctx.permutation_null(pooled, n_P, perms)  # host inputs
+        assert np.array_equal(g_null2, null)
+
+
+# ----------------------------------------------------------------------------------- BASELINE configs
+
+def test_config_c1_c2_c3_full(ctx):
+    for name in ("C1", "C2", "C3"):
+        P, Q = I.config(name)
+        check_pair(ctx, P, Q)
+
+
+def test_config_c4_batch_and_perms(ctx):
+    P, Q = I.config("C4")
+    got = ctx.stat_batch(dev(P), dev(Q))
+    idx = [0, 1, 2, 3, 4, 777, 2047, 2048, 2049, 2050, 2051, 2052, 4095]
+    want = O.batch(P[idx], Q[idx])
+    assert [got[i].num for i in idx] == want.tolist()
+    nums = np.array([r.num for r in got], dtype=np.uint64)
+    assert int(nums.max()) == 56_320 and int(nums.sum()) == 122_770_432  # SURVEY.md §8c C4a (independent)
+    perms = I.c4_perms()
+    pooled = np.concatenate([P[I.C4_PERM_PAIR], Q[I.C4_PERM_PAIR]])
+    null, obs, p = ctx.permutation_null(dev(pooled), 512, dev(perms))
+    o_null, o_obs, o_pnum, o_p = O.permutation_null(pooled, 512, perms[:64])
+    assert np.array_equal(null[:64], o_null) and obs.num == o_obs == 39_936
+    assert int(null.max()) == 34_816 and int(null.sum()) == 23_215_616 and p == 1 / 1001
+
+
+def test_config_c5_sampled(ctx):
+    # full size, the bench's launch configuration; sampled origins checked one by one against the oracle
+    P, Q = I.config("C5")
+    dP, dQ = dev(P), dev(Q)
+    rng = np.random.default_rng(5)
+    idx = sorted(set([0, 1, 2, 3, 999_999, 1_000_000, 1_000_001, 1_999_999, 123_456, 1_765_432]
+                     + rng.integers(0, 2_000_000, 22).tolist()))
+    for o in idx:
+        got = int(ctx.stat_per_origin(dP, dQ, o, o + 1)[0])
+        assert got == int(O.per_origin(P, Q, o, o + 1)[0]), o
+    r = ctx.stat(dP, dQ)
+    assert r.den == 10**12 and 0 < r.num <= r.den
+    # the reported max is attained at the reported argmax origin (checked by the oracle) ...
+    assert int(O.per_origin(P, Q, r.argmax_origin, r.argmax_origin + 1)[0]) == r.num
+    # ... and no sampled origin exceeds it
+    assert all(int(O.per_origin(P, Q, o, o + 1)[0]) <= r.num for o in idx[:8])
