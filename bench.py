@@ -1,0 +1,308 @@
+#!/usr/bin/env python
+"""bench.py — exact ddKS throughput on B200 (BASELINE.json metric: point-pair orthant classifications/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N ...
+
+A "step" is one whole exact-ddKS statistic (all SURVEY.md §8a rows: validate+pack, classify+count, per-origin
+max, argmax, and for N > 1 the NCCL all-reduce(max)) on the workload BASELINE.json quotes its target on:
+configs[4] = C5 (d=5, n_P = n_Q = 10^6, 4*10^12 pair classifications per step). Origins are sharded across the
+ranks (strong scaling: the statistic is fixed, every rank does N^2/G pairs).
+
+Timing: W untimed warm-up steps; then K steps bracketed by barrier + cuda synchronize; each step timed with
+CUDA events on the launching stream; L2 flushed (512 MiB write) between steps, outside the events; the
+reported time is the MAX over ranks. `value` = K * N^2 / that time. `e2e` repeats the step through the
+C-ABI with PINNED HOST input buffers (H2D inside the timed call) and the host result read.
+`roofline`: the classify+count kernel's FP32 compares/s (d per pair) vs the ALU-pipe compare peak
+148 SMs x 64 lanes/clk (FSET.BF, measured by microbench/pipes.cu) x sm_max_mhz (MEASURED_PEAKS.json).
+`cpu_baseline`: the CPU oracle (oracle/ddks_oracle.c, as it stands) on this host's cores over a bounded
+sample of origins of the same workload (rank 0, N = 1 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "exact ddKS point-pair orthant classifications/sec at 1/2/4/8 B200 (% roofline)"
+UNIT = "pair-classifications/s"
+FSET_LANES_PER_CLK_PER_SM = 64  # measured: microbench/pipes.cu FSET.BF.GE = 63.9 lanes/clk/SM (profiles/)
+N_SM = 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="C5", choices=["C1", "C2", "C3", "C5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-oracle sample duration")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={','.join(self.FIELDS)}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) == 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) == 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) == 7 for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def workload(name):
+    from paper_2106_13706_b200 import inputs as I
+    P, Q = I.config(name)
+    return P, Q, {"workload": f"{name}: {I.CONFIG_NAMES[name]}", "n_P": int(P.shape[0]), "n_Q": int(Q.shape[0]),
+                  "d": int(P.shape[1]), "pairs_per_step": int((P.shape[0] + Q.shape[0]) ** 2)}
+
+
+def cpu_oracle_sample(P, Q, seconds: float):
+    """Time the CPU oracle (as it stands) on a bounded, evenly spaced sample of origins against all N points."""
+    from oracle import oracle as O
+    N = P.shape[0] + Q.shape[0]
+    cores = os.cpu_count() or 1
+    O.build()
+    n0 = max(cores, 8)
+    t0 = time.perf_counter()
+    O.per_origin(P, Q, 0, n0, threads=cores)
+    dt = time.perf_counter() - t0
+    rate = n0 / max(dt, 1e-6)  # origins / s
+    n_orig = int(min(N, max(cores, rate * seconds)))
+    starts = np.linspace(0, N - 64, max(1, n_orig // 64)).astype(np.int64)
+    t0 = time.perf_counter()
+    done = 0
+    for s in starts:
+        O.per_origin(P, Q, int(s), int(s) + 64, threads=cores)
+        done += 64
+    dt = time.perf_counter() - t0
+    return {"value": done * N / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{done} origins ({len(starts)} evenly spaced blocks of 64) x all {N} points = {done * N:.3e} "
+                      f"pair classifications in {dt:.2f} s, OpenMP over origins on {cores} host threads"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands is this tier's reference arm (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    P, Q, cfg = workload(args.workload)
+    per_step = max(1.0, 60.0 / max(1, args.steps + args.warmup))  # whole run within a few minutes
+    for _ in range(args.warmup):
+        cpu_oracle_sample(P, Q, min(per_step, 2.0))
+    vals, samples = [], []
+    for _ in range(args.steps):
+        r = cpu_oracle_sample(P, Q, per_step)
+        vals.append(r["value"])
+        samples.append(r)
+    v = float(np.median(vals))
+    N = cfg["n_P"] + cfg["n_Q"]
+    cpu = dict(samples[-1])
+    cpu["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": N * N / v * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64-compare/i64-count", "data": "synthetic (seeded, BASELINE.json recipe)",
+            "config": dict(cfg, parallelism="cpu-openmp", l2="n/a (CPU)"),
+            "cpu_baseline": cpu,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0,
+            "note": "reference arm = the plain C oracle on host cores, each step a bounded sample of origins "
+                    "(ms_per_step extrapolates the sample rate to the whole statistic)"}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2106_13706_b200 import ddks as K
+
+    nccl_id = None
+    if world > 1:
+        obj = [K.ddks_get_nccl_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    ctx = K.Context(device=local, world=world, rank=rank, nccl_id=nccl_id, flags=K.DDKS_FLAG_PROFILE)
+
+    P, Q, cfg = workload(args.workload)
+    d = cfg["d"]
+    N = cfg["n_P"] + cfg["n_Q"]
+    pairs_step = N * N
+    stream = torch.cuda.current_stream()
+    dP = torch.from_numpy(P).cuda()
+    dQ = torch.from_numpy(Q).cuda()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    res = None
+    for _ in range(max(3, args.warmup)):
+        res = ctx.stat(dP, dQ)
+    ctx.profile_read()  # discard warm-up profile
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = ctx.launch_count
+    step_ms = []
+    t_wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = ctx.stat(dP, dQ)
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        assert r == res, (r, res)
+    barrier()
+    t_wall = time.perf_counter() - t_wall0
+    launches = ctx.launch_count - launches0
+    kern_ms, kern_launches, kern_pairs = ctx.profile_read()
+    clk = clocks.stop()
+    total_ms = max_over_ranks(float(sum(step_ms)))
+    value = args.steps * pairs_step / (total_ms / 1e3)
+
+    # end-to-end: host (pinned) inputs through the C-ABI, H2D inside the timed call, D2H of the result
+    e2e = None
+    if not args.no_e2e:
+        hP = torch.from_numpy(P).pin_memory()
+        hQ = torch.from_numpy(Q).pin_memory()
+        ctx.stat(hP, hQ)
+        ctx.profile_read()
+        barrier()
+        e2e_s = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = ctx.stat(hP, hQ)
+            e2e_s.append(time.perf_counter() - t0)
+            assert r == res
+        barrier()
+        ctx.profile_read()
+        e2e_total = max_over_ranks(float(sum(e2e_s)))
+        e2e = {"value": args.steps * pairs_step / e2e_total, "unit": UNIT,
+               "h2d_bytes_per_step": int(P.nbytes + Q.nbytes), "d2h_bytes_per_step": 24,
+               "ms_per_step": e2e_total / args.steps * 1e3}
+
+    pk = peaks()
+    sm_max = float(pk.get("sm_max_mhz", 1965.0))
+    # roofline of the dominant kernel (classify+count), per rank, averaged over its timed launches
+    kern_ms_max = max_over_ranks(kern_ms)
+    per_launch_ms = kern_ms / max(kern_launches, 1)
+    pairs_per_launch = kern_pairs / max(kern_launches, 1)
+    achieved = d * pairs_per_launch / (per_launch_ms / 1e3) / 1e12  # T compares / s (per GPU)
+    peak = N_SM * FSET_LANES_PER_CLK_PER_SM * sm_max * 1e6 / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(args.workload)
+        except Exception:
+            traffic = None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_sample(P, Q, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE.json recipe)",
+            "config": dict(cfg, parallelism=f"origins sharded over {world} GPU(s), NCCL all-reduce(max)",
+                           l2="flushed between steps (512 MiB write, outside the step events)"),
+            "result": {"num": res.num, "den": res.den, "D": res.D, "argmax_origin": res.argmax_origin},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tcompare/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_count (classify + count)", "kernel_ms_per_launch": per_launch_ms,
+                         "kernel_share_of_step": kern_ms_max / total_ms if total_ms else None,
+                         "peak_source": f"{N_SM} SMs x {FSET_LANES_PER_CLK_PER_SM} FSET lanes/clk/SM x {sm_max} MHz "
+                                        "(MEASURED_PEAKS.json sm_max_mhz; lane rate measured by microbench/pipes.cu)"},
+            "clocks": clk,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "cpu_baseline": cpu,
+            "wall_s_timed": t_wall,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -65,6 +65,7 @@ typedef enum {
 #define DDKS_FLAG_TIES_GT 2u     /* TEST ONLY: bit k = [x_k > o_k] instead of >= (shows the convention matters) */
 #define DDKS_FLAG_FORCE_DIRECT 4u /* TEST ONLY: never split the point axis into segments (exercises the in-kernel
                                      finalisation at small N; results are identical either way)              */
+#define DDKS_FLAG_PROFILE 8u      /* record CUDA events around every count-kernel launch (see ddks_profile_read) */
 
 typedef struct {
     uint64_t num;          /* max over origins and orthants of |c_P*n_Q - c_Q*n_P| (exact integer)            */
@@ -110,6 +111,12 @@ DDKS_API ddks_status ddks_shard_range(int64_t total, int world, int rank, int64_
 
 /* Number of kernels the library launched on this context since creation (for the bench's gpu_launches). */
 DDKS_API int64_t ddks_launch_count(const ddks_ctx* ctx);
+
+/* Profiling (context created with DDKS_FLAG_PROFILE): totals since the last read, then reset.
+ * count_ms: summed device time of the classify+count kernel launches (CUDA events on the call's stream);
+ * launches: how many such launches; pairs: point-pair orthant classifications they performed (sum of
+ * items x origins x points); any pointer may be NULL. */
+DDKS_API ddks_status ddks_profile_read(ddks_ctx* ctx, double* count_ms, int64_t* launches, uint64_t* pairs);
 
 /* Destroy a context (NULL-safe). Frees workspace and the NCCL communicator. */
 DDKS_API ddks_status ddks_destroy(ddks_ctx* ctx);

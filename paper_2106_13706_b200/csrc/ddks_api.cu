@@ -39,6 +39,12 @@ struct ddks_ctx {
     size_t host_pinned_bytes = 0;
     int64_t launches = 0;
     std::string err;
+    // profiling (DDKS_FLAG_PROFILE)
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending, ev_free;
+    std::vector<uint64_t> ev_pairs;
+    double prof_ms = 0.0;
+    int64_t prof_launches = 0;
+    uint64_t prof_pairs = 0;
 };
 
 static thread_local std::string g_create_err;
@@ -137,8 +143,8 @@ struct CountPlan {
     int64_t B;
     int32_t N, n_P, o_begin, o_end;
     int64_t nP, nQ;
-    bool split;    // SPLIT counters (c_P, c_Q separately)
-    int segs;      // grid.z point segments (>1 => accumulate + finalize)
+    bool split;      // SPLIT counters (c_P, c_Q separately)
+    int64_t window;  // max points per segment so no 16-bit counter half leaves int16
 };
 
 template <int D, bool SPLIT, bool GT>
@@ -152,27 +158,48 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
     }
     const int n_orig = pl.o_end - pl.o_begin;
     const int blocks_o = (n_orig + G::ORIGINS - 1) / G::ORIGINS;
-    int segs = 1;
-    const int64_t ctas = pl.B * blocks_o;
     const int n_tiles = (pl.N + G::TILE - 1) / G::TILE;
-    if (ctas < 2 * 148 && !(ctx->flags & DDKS_FLAG_FORCE_DIRECT)) segs = (int)std::min<int64_t>(n_tiles, (2 * 148 + ctas - 1) / ctas);
-    const int tiles_per_seg = (n_tiles + segs - 1) / segs;
-    segs = (n_tiles + tiles_per_seg - 1) / tiles_per_seg;
+    // segment length: at most the int16 flush window, and short enough to give >= 2 CTAs per SM
+    const int w_tiles = std::max(1, (int)(pl.window / G::TILE));
+    int tiles_per_seg = std::min(n_tiles, w_tiles);
+    const int64_t ctas = pl.B * blocks_o;
+    if (ctas < 2 * 148 && !(ctx->flags & DDKS_FLAG_FORCE_DIRECT)) {
+        const int64_t want_segs = (2 * 148 + ctas - 1) / ctas;
+        tiles_per_seg = std::min<int64_t>(tiles_per_seg, std::max<int64_t>(1, (n_tiles + want_segs - 1) / want_segs));
+    }
+    const int segs = (n_tiles + tiles_per_seg - 1) / tiles_per_seg;
     a.seg_points = tiles_per_seg * G::TILE;
+    if (segs > 65535) return fail(ctx, DDKS_ERR_TOO_LARGE, "too many point segments");
     if (segs > 1) {
         const size_t acc_bytes = (size_t)pl.B * G::NB * (size_t)n_orig * 4;
         ddks_status s = ensure(ctx, ctx->accum, acc_bytes);
         if (s) return s;
         CU(cudaMemsetAsync(ctx->accum.p, 0, acc_bytes, st));
-        a.accum = (uint32_t*)ctx->accum.p;
+        a.accum = (int32_t*)ctx->accum.p;
     } else {
         a.accum = nullptr;
     }
     if (pl.B > 0x7fffffff || blocks_o > 65535) return fail(ctx, DDKS_ERR_TOO_LARGE, "grid too large");
     dim3 grid((unsigned)pl.B, (unsigned)blocks_o, (unsigned)segs);
+    std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+    if (ctx->flags & DDKS_FLAG_PROFILE) {
+        if (!ctx->ev_free.empty()) {
+            ev = ctx->ev_free.back();
+            ctx->ev_free.pop_back();
+        } else {
+            CU(cudaEventCreate(&ev.first));
+            CU(cudaEventCreate(&ev.second));
+        }
+        CU(cudaEventRecord(ev.first, st));
+    }
     kern<<<grid, G::T, G::SMEM_BYTES, st>>>(a);
     CHECK_LAUNCH();
     ctx->launches++;
+    if (ev.first) {
+        CU(cudaEventRecord(ev.second, st));
+        ctx->ev_pending.push_back(ev);
+        ctx->ev_pairs.push_back((uint64_t)pl.B * (uint64_t)n_orig * (uint64_t)pl.N);
+    }
     if (segs > 1) {
         const int64_t total = pl.B * n_orig;
         const int threads = 256;
@@ -197,9 +224,12 @@ ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int6
     const int64_t N = n_P + n_Q;
     const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
     const uint64_t a_ = (uint64_t)n_Q / g, b_ = (uint64_t)n_P / g;
-    // DIFF counters hold c_P*a - c_Q*b; |value| <= n_P*n_Q/g must fit int32
-    const bool split = (uint64_t)n_P * a_ >= 0x7fffffffull || (uint64_t)n_Q * b_ >= 0x7fffffffull;
-    CountPlan pl{B, (int32_t)N, (int32_t)n_P, (int32_t)o_begin, (int32_t)o_end, n_P, n_Q, split, 1};
+    // DIFF counters hold c_P*a - c_Q*b: a 16-bit half stays in int16 over W <= 32767/max(a,b) points, and the
+    // int32 total |value| <= n_P*n_Q/g must fit int32. Otherwise SPLIT: c_P and c_Q separately, W = 32767.
+    const uint64_t mab = std::max(a_, b_);
+    const bool split = mab > 32767 / 4096 || (uint64_t)n_P * a_ >= 0x7fffffffull || (uint64_t)n_Q * b_ >= 0x7fffffffull;
+    const int64_t window = split ? 32767 : (int64_t)(32767 / mab);
+    CountPlan pl{B, (int32_t)N, (int32_t)n_P, (int32_t)o_begin, (int32_t)o_end, n_P, n_Q, split, window};
     ddks::CountArgs a{};
     a.pts = packed;
     a.item_stride = N * pad_dim(d);
@@ -250,6 +280,21 @@ ddks_status ensure_host(ddks_ctx* ctx, size_t bytes) {
     return DDKS_OK;
 }
 
+// After a stream sync: fold the pending count-kernel events into the profile totals.
+ddks_status collect_profile(ddks_ctx* ctx) {
+    for (size_t i = 0; i < ctx->ev_pending.size(); ++i) {
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, ctx->ev_pending[i].first, ctx->ev_pending[i].second));
+        ctx->prof_ms += ms;
+        ctx->prof_launches += 1;
+        ctx->prof_pairs += ctx->ev_pairs[i];
+        ctx->ev_free.push_back(ctx->ev_pending[i]);
+    }
+    ctx->ev_pending.clear();
+    ctx->ev_pairs.clear();
+    return DDKS_OK;
+}
+
 ddks_status bind_device(ddks_ctx* ctx) {
     CU(cudaSetDevice(ctx->device));
     return DDKS_OK;
@@ -287,7 +332,7 @@ ddks_status ddks_create(ddks_ctx** out, int device, int world, int rank, const v
     if (world < 1 || rank < 0 || rank >= world) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad world/rank");
     if ((world == 1) != (nccl_id == nullptr))
         return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "nccl_id must be NULL iff world == 1");
-    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
+    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT | DDKS_FLAG_PROFILE)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
     int ndev = 0;
     CU(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device %d of %d", device, ndev);
@@ -322,6 +367,11 @@ ddks_status ddks_destroy(ddks_ctx* ctx) {
     if (!ctx) return DDKS_OK;
     cudaSetDevice(ctx->device);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
+    for (auto* v : {&ctx->ev_pending, &ctx->ev_free})
+        for (auto& e : *v) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
     for (DevBuf* b : {&ctx->raw_a, &ctx->raw_b, &ctx->raw_perm, &ctx->packed, &ctx->packed2, &ctx->pool_packed, &ctx->per_origin,
                       &ctx->accum, &ctx->item_num, &ctx->bitmap, &ctx->res})
         if (b->p) cudaFree(b->p);
@@ -333,6 +383,19 @@ ddks_status ddks_destroy(ddks_ctx* ctx) {
 const char* ddks_last_error(const ddks_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
 
 int64_t ddks_launch_count(const ddks_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+ddks_status ddks_profile_read(ddks_ctx* ctx, double* count_ms, int64_t* launches, uint64_t* pairs) {
+    if (!ctx) return DDKS_ERR_INVALID_ARGUMENT;
+    ddks_status s = collect_profile(ctx);
+    if (s) return s;
+    if (count_ms) *count_ms = ctx->prof_ms;
+    if (launches) *launches = ctx->prof_launches;
+    if (pairs) *pairs = ctx->prof_pairs;
+    ctx->prof_ms = 0.0;
+    ctx->prof_launches = 0;
+    ctx->prof_pairs = 0;
+    return DDKS_OK;
+}
 
 // a1-a7 for one pair, origins sharded across ranks; optional per-origin export (debug path, single rank).
 static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
@@ -393,6 +456,7 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
     }
     CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    if ((s = collect_profile(ctx))) return s;
     if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
     if (out) {
         out->num = hres->num;
@@ -485,6 +549,7 @@ ddks_status ddks_stat_batch(ddks_ctx* ctx, const float* P, const float* Q, int64
     CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(hnums, nums, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    if ((s = collect_profile(ctx))) return s;
     if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
     const uint64_t den = (uint64_t)n_P * (uint64_t)n_Q;
     for (int64_t b = 0; b < B; ++b) {
@@ -557,6 +622,7 @@ ddks_status ddks_permutation_null(ddks_ctx* ctx, const float* pooled, int64_t n_
     CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(hnums, nums, (size_t)total * 8, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    if ((s = collect_profile(ctx))) return s;
     if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
     if (hres->flag & 2u) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "a perms row is not a permutation of 0..N-1");
     const uint64_t obs = hnums[0];

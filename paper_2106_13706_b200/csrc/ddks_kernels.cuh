@@ -24,31 +24,39 @@
 namespace ddks {
 
 // ----------------------------------------------------------------------------------------------- config
+// Counters are 16-bit halves of 32-bit SMEM words: word (q, rp, t) holds orthant q of origin rp (low half)
+// and of origin rp + R/2 (high half) of thread t. A CTA processes at most W points per launch segment
+// (W chosen by the host so no half can leave int16), then flushes its counters to int32 global accumulators;
+// if the whole point set fits one segment it finalises in-kernel instead.
 template <int D> struct Cfg;
-// R origins per thread, T threads per CTA, TILE points per SMEM stage, S stages.
-// SMEM histogram = 2^D bins x R x T x 4 B (x2 in SPLIT mode) kept at <= 128 KB.
-template <> struct Cfg<1> { static constexpr int R = 4, T = 256, TILE = 512, S = 3; };
-template <> struct Cfg<2> { static constexpr int R = 4, T = 256, TILE = 512, S = 3; };
-template <> struct Cfg<3> { static constexpr int R = 4, T = 256, TILE = 512, S = 3; };
+// R origins per thread (even), T threads per CTA, TILE points per SMEM stage, S stages (DIFF mode).
+template <> struct Cfg<1> { static constexpr int R = 8, T = 256, TILE = 512, S = 3; };
+template <> struct Cfg<2> { static constexpr int R = 8, T = 256, TILE = 512, S = 3; };
+template <> struct Cfg<3> { static constexpr int R = 8, T = 256, TILE = 512, S = 3; };
 template <> struct Cfg<4> { static constexpr int R = 4, T = 256, TILE = 512, S = 3; };
-template <> struct Cfg<5> { static constexpr int R = 4, T = 256, TILE = 256, S = 3; };
-template <> struct Cfg<6> { static constexpr int R = 2, T = 256, TILE = 256, S = 3; };
-template <> struct Cfg<7> { static constexpr int R = 1, T = 256, TILE = 256, S = 3; };
-template <> struct Cfg<8> { static constexpr int R = 1, T = 128, TILE = 256, S = 3; };
+template <> struct Cfg<5> { static constexpr int R = 8, T = 384, TILE = 256, S = 3; };
+template <> struct Cfg<6> { static constexpr int R = 4, T = 256, TILE = 256, S = 3; };
+template <> struct Cfg<7> { static constexpr int R = 2, T = 256, TILE = 256, S = 3; };
+template <> struct Cfg<8> { static constexpr int R = 2, T = 192, TILE = 256, S = 3; };
 
 template <int D> __host__ __device__ constexpr int padded_dim() { return D <= 4 ? 4 : 8; }
 
 template <int D, bool SPLIT> struct Geo {
-    static constexpr int R = (SPLIT && Cfg<D>::R > 1) ? Cfg<D>::R / 2 : Cfg<D>::R;
-    static constexpr int T = (SPLIT && Cfg<D>::R == 1) ? Cfg<D>::T / 2 : Cfg<D>::T;
+    // SPLIT doubles the bins: halve R (keeping it even), or T when R is already 2
+    static constexpr int R = (SPLIT && Cfg<D>::R > 2) ? Cfg<D>::R / 2 : Cfg<D>::R;
+    static constexpr int T = (SPLIT && Cfg<D>::R == 2) ? Cfg<D>::T / 2 : Cfg<D>::T;
+    static constexpr int RP = R / 2;                            // counter words per (bin, thread)
     static constexpr int TILE = Cfg<D>::TILE;
     static constexpr int S = Cfg<D>::S;
     static constexpr int DP = padded_dim<D>();
-    static constexpr int NB = (1 << D) * (SPLIT ? 2 : 1);      // counters per origin
-    static constexpr int HIST_WORDS = NB * R * T;
+    static constexpr int NQ = 1 << D;
+    static constexpr int NB = NQ * (SPLIT ? 2 : 1);            // counters per origin
+    static constexpr int HIST_WORDS = NB * RP * T;
     static constexpr int TILE_BYTES = TILE * DP * 4;
     static constexpr int SMEM_BYTES = S * TILE_BYTES + HIST_WORDS * 4 + 64;
     static constexpr int ORIGINS = R * T;
+    static_assert(R % 2 == 0, "R must be even (two origins per counter word)");
+    static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 };
 
 // ----------------------------------------------------------------------------------------------- PTX helpers
@@ -161,35 +169,41 @@ struct CountArgs {
     int64_t item_stride;     // floats per item = N * DP
     int32_t N, n_P;          // pooled points per item; the first n_P are P
     int32_t o_begin, o_end;  // origin range (pooled indices) this launch owns, per item
-    int32_t seg_points;      // points per grid.z segment (multiple of TILE)
+    int32_t seg_points;      // points per grid.z segment (multiple of TILE, <= the int16 flush window)
     uint32_t incP, incQ;     // DIFF: +a and -b (two's complement); SPLIT: 1 and 1
     uint64_t g;              // DIFF: gcd(n_P, n_Q) multiplier
     int64_t nP, nQ;          // SPLIT finalisation
     uint64_t* item_num;      // [B] atomicMax target (direct mode)
     uint64_t* per_origin;    // [o_end - o_begin] or nullptr (direct mode, B == 1)
-    uint32_t* accum;         // accumulate mode: [B][NB][n_orig] int32 counters (grid.z > 1), else nullptr
+    int32_t* accum;          // accumulate mode: [B][NB][n_orig] int32 counters, else nullptr (direct mode)
 };
 
+// decode the two signed 16-bit halves of a counter word (value = lo + 65536 * hi, both in int16 range)
+__device__ __forceinline__ void split16(uint32_t w, int32_t& lo, int32_t& hi) {
+    lo = (int32_t)(int16_t)(w & 0xffffu);
+    hi = ((int32_t)w - lo) >> 16;
+}
+
+// num(o) of origin r of thread t from the SMEM counters (direct mode)
 template <int D, bool SPLIT>
 __device__ __forceinline__ uint64_t origin_num(const uint32_t* hist, int r, int t, const CountArgs& a) {
     using G = Geo<D, SPLIT>;
-    constexpr int NQ = 1 << D;
+    constexpr int NQ = G::NQ;
+    const int rp = r % G::RP;
+    const bool high = r >= G::RP;
     uint64_t best = 0;
-    if constexpr (!SPLIT) {
-        uint32_t m = 0;
-#pragma unroll 4
-        for (int q = 0; q < NQ; ++q) {
-            const int32_t v = (int32_t)hist[(q * G::R + r) * G::T + t];
-            const uint32_t av = (uint32_t)(v < 0 ? -v : v);
-            m = av > m ? av : m;
-        }
-        best = (uint64_t)m * a.g;
-    } else {
-#pragma unroll 4
-        for (int q = 0; q < NQ; ++q) {
-            const int64_t cP = (int64_t)hist[(q * G::R + r) * G::T + t];
-            const int64_t cQ = (int64_t)hist[((NQ + q) * G::R + r) * G::T + t];
-            const int64_t df = cP * a.nQ - cQ * a.nP;
+    for (int q = 0; q < NQ; ++q) {
+        int32_t lo, hi;
+        split16(hist[(q * G::RP + rp) * G::T + t], lo, hi);
+        const int32_t v = high ? hi : lo;
+        if constexpr (!SPLIT) {
+            const uint64_t av = (uint64_t)(v < 0 ? -v : v) * a.g;
+            best = av > best ? av : best;
+        } else {
+            int32_t lo2, hi2;
+            split16(hist[((NQ + q) * G::RP + rp) * G::T + t], lo2, hi2);
+            const int64_t cQ = high ? hi2 : lo2;
+            const int64_t df = (int64_t)v * a.nQ - cQ * a.nP;
             const uint64_t av = (uint64_t)(df < 0 ? -df : df);
             best = av > best ? av : best;
         }
@@ -206,13 +220,40 @@ __device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
     return v;
 }
 
+// Classify + count the points [lo, hi) of one SMEM tile for the R origins of this thread.
+// Per pair: D x FSET.BF (ALU) + D x FFMA-immediate (FMA) + 1 x ATOMS.ADD; the next point is prefetched.
+template <int D, bool GT, int R, int T, int RP, int DP>
+__device__ __forceinline__ void count_points(const float* tile, int lo, int hi, const float (&o)[R][D],
+                                             const float (&base)[RP], uint32_t ubase, uint32_t inc_lo,
+                                             uint32_t inc_hi) {
+    if (lo >= hi) return;
+    // prefetch the next point unconditionally: index hi <= TILE stays inside the SMEM allocation (the value
+    // read past the valid range is never used)
+    float xn[D];
+    load_point<D>(tile + lo * DP, xn);
+#pragma unroll 2
+    for (int p = lo; p < hi; ++p) {
+        float x[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) x[k] = xn[k];
+        load_point<D>(tile + (p + 1) * DP, xn);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            float f = base[r % RP];
+#pragma unroll
+            for (int k = 0; k < D; ++k) f = fmaf(cmp_bit<GT>(x[k], o[r][k]), (float)(4 * (1 << k) * RP * T), f);
+            red_add_shared(__float_as_uint(f) + ubase, r < RP ? inc_lo : inc_hi);
+        }
+    }
+}
+
 template <int D, bool SPLIT, bool GT>
 __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a) {
     using G = Geo<D, SPLIT>;
-    constexpr int R = G::R, T = G::T, DP = G::DP, TILE = G::TILE, S = G::S;
+    constexpr int R = G::R, RP = G::RP, T = G::T, DP = G::DP, TILE = G::TILE, S = G::S;
     extern __shared__ __align__(128) uint8_t smem[];
     float* tiles = reinterpret_cast<float*>(smem);                                  // [S][TILE][DP]
-    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + S * G::TILE_BYTES);          // [NB][R][T]
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + S * G::TILE_BYTES);          // [NB][RP][T]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * G::TILE_BYTES + G::HIST_WORDS * 4);
 
     const int t = threadIdx.x;
@@ -231,8 +272,7 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
     for (int i = t; i < G::HIST_WORDS; i += T) hist[i] = 0u;
     __syncthreads();
 
-    // prologue: fill the ring
-    if (t == 0) {
+    if (t == 0) {  // prologue: fill the ring
         for (int s = 0; s < S && s < n_tiles; ++s) {
             const int32_t p0 = seg0 + s * TILE;
             const uint32_t bytes = (uint32_t)(min(TILE, seg1 - p0) * DP * 4);
@@ -241,7 +281,7 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
         }
     }
 
-    // origins owned by this thread: o = blk_o0 + r*T + t (clamped to a valid origin; ignored at the end)
+    // origins of this thread: r -> o = blk_o0 + r*T + t (clamped to a valid origin; ignored at the end)
     float o[R][D];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -252,14 +292,15 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
         for (int k = 0; k < D; ++k) o[r][k] = __ldg(op + k);
     }
 
-    // the histogram byte address lives in the mantissa of a float in [2^23, 2^24): bits = 0x4B000000 + offset
+    // the counter byte address lives in the mantissa of a float in [2^23, 2^24): bits = 0x4B000000 + offset
     const uint32_t ubase = smem_u32(hist) - 0x4B000000u;
-    float baseP[R], baseQ[R];
+    float baseP[RP], baseQ[RP];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-        baseP[r] = __uint_as_float(0x4B000000u + 4u * (uint32_t)(r * T + t));
-        baseQ[r] = SPLIT ? __uint_as_float(0x4B000000u + 4u * (uint32_t)(((1 << D) * R + r) * T + t)) : baseP[r];
+    for (int rp = 0; rp < RP; ++rp) {
+        baseP[rp] = __uint_as_float(0x4B000000u + 4u * (uint32_t)(rp * T + t));
+        baseQ[rp] = SPLIT ? __uint_as_float(0x4B000000u + 4u * (uint32_t)((G::NQ * RP + rp) * T + t)) : baseP[rp];
     }
+    const uint32_t incP_hi = a.incP << 16, incQ_hi = a.incQ << 16;
 
     for (int it = 0; it < n_tiles; ++it) {
         const int s = it % S;
@@ -270,28 +311,8 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
         // sample-homogeneous sub-ranges: [p0, n_P) are P points, [n_P, ...) are Q points
         int32_t split = a.n_P - p0;
         split = split < 0 ? 0 : (split > cnt ? cnt : split);
-#pragma unroll 1
-        for (int phase = 0; phase < 2; ++phase) {
-            const int32_t lo = phase == 0 ? 0 : split;
-            const int32_t hi = phase == 0 ? split : cnt;
-            const uint32_t inc = phase == 0 ? a.incP : a.incQ;
-            float base[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) base[r] = phase == 0 ? baseP[r] : baseQ[r];
-#pragma unroll 2
-            for (int32_t p = lo; p < hi; ++p) {
-                float x[D];
-                load_point<D>(tile + p * DP, x);
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    float f = base[r];
-#pragma unroll
-                    for (int k = 0; k < D; ++k)
-                        f = fmaf(cmp_bit<GT>(x[k], o[r][k]), (float)(4 * (1 << k) * R * T), f);
-                    red_add_shared(__float_as_uint(f) + ubase, inc);
-                }
-            }
-        }
+        count_points<D, GT, R, T, RP, DP>(tile, 0, split, o, baseP, ubase, a.incP, incP_hi);
+        count_points<D, GT, R, T, RP, DP>(tile, split, cnt, o, baseQ, ubase, a.incQ, incQ_hi);
         __syncthreads();  // every thread is done with stage s
         if (t == 0 && it + S < n_tiles) {
             fence_proxy_async();
@@ -301,19 +322,21 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
             bulk_g2s(tiles + s * TILE * DP, pts + (int64_t)q0 * DP, bytes, &bars[s]);
         }
     }
-    __syncthreads();  // all red.shared retired before reading the histogram
+    __syncthreads();  // all red.shared retired before reading the counters
 
     const int32_t n_orig = a.o_end - a.o_begin;
     if (a.accum != nullptr) {
-        // accumulate mode (grid.z > 1 point segments): exact int32 partial counts -> global, finalised later
-        uint32_t* acc = a.accum + item * (int64_t)G::NB * n_orig;
+        // flush: exact int32 partial counters -> global (red.global.add), finalised by k_finalize
+        int32_t* acc = a.accum + item * (int64_t)G::NB * n_orig;
 #pragma unroll 1
-        for (int r = 0; r < R; ++r) {
-            const int32_t oi = blk_o0 + r * T + t;
-            if (oi >= a.o_end) continue;
+        for (int rp = 0; rp < RP; ++rp) {
+            const int32_t o_lo = blk_o0 + rp * T + t, o_hi = o_lo + RP * T;
+#pragma unroll 4
             for (int q = 0; q < G::NB; ++q) {
-                const uint32_t v = hist[(q * R + r) * T + t];
-                if (v) atomicAdd(&acc[(int64_t)q * n_orig + (oi - a.o_begin)], v);
+                int32_t lo, hi;
+                split16(hist[(q * RP + rp) * T + t], lo, hi);
+                if (lo && o_lo < a.o_end) atomicAdd(&acc[(int64_t)q * n_orig + (o_lo - a.o_begin)], lo);
+                if (hi && o_hi < a.o_end) atomicAdd(&acc[(int64_t)q * n_orig + (o_hi - a.o_begin)], hi);
             }
         }
         return;
@@ -349,7 +372,7 @@ __global__ void k_finalize(const CountArgs a, int64_t B) {
     int64_t item_of_best = -1;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t item = i / n_orig, oi = i - item * n_orig;
-        const uint32_t* acc = a.accum + item * (int64_t)NB * n_orig + oi;
+        const int32_t* acc = a.accum + item * (int64_t)NB * n_orig + oi;
         uint64_t m = 0;
         if constexpr (!SPLIT) {
             uint32_t mm = 0;

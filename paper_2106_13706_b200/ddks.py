@@ -23,6 +23,7 @@ DDKS_FLAG_DEFAULT = 0
 DDKS_FLAG_NO_VALIDATE = 1
 DDKS_FLAG_TIES_GT = 2
 DDKS_FLAG_FORCE_DIRECT = 4
+DDKS_FLAG_PROFILE = 8
 
 
 class DDKSError(RuntimeError):
@@ -59,6 +60,8 @@ def _load() -> ctypes.CDLL:
         "ddks_stat_per_origin": ([vp, vp, i64, vp, i64, i32, i64, i64, vp, vp], ctypes.c_int),
         "ddks_shard_range": ([i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)], ctypes.c_int),
         "ddks_launch_count": ([vp], i64),
+        "ddks_profile_read": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_uint64)],
+                              ctypes.c_int),
         "ddks_destroy": ([vp], ctypes.c_int),
         "ddks_last_error": ([vp], ctypes.c_char_p),
         "ddks_version": ([], ctypes.c_char_p),
@@ -72,8 +75,8 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 EXPORTED = ("ddks_get_nccl_id", "ddks_create", "ddks_stat", "ddks_stat_batch", "ddks_permutation_null",
-            "ddks_stat_per_origin", "ddks_shard_range", "ddks_launch_count", "ddks_destroy", "ddks_last_error",
-            "ddks_version")
+            "ddks_stat_per_origin", "ddks_shard_range", "ddks_launch_count", "ddks_profile_read", "ddks_destroy",
+            "ddks_last_error", "ddks_version")
 
 
 def _check(st: int, ctx=None):
@@ -195,6 +198,13 @@ def ddks_launch_count(ctx) -> int:
     return int(LIB.ddks_launch_count(ctx))
 
 
+def ddks_profile_read(ctx):
+    """-> (count_kernel_ms, count_launches, pairs) since the last read (context needs DDKS_FLAG_PROFILE)."""
+    ms, n, pairs = ctypes.c_double(), ctypes.c_int64(), ctypes.c_uint64()
+    _check(LIB.ddks_profile_read(ctx, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(pairs)), ctx)
+    return ms.value, n.value, pairs.value
+
+
 class Context:
     """RAII wrapper: ``with Context() as c: c.stat(P, Q)``."""
 
@@ -213,6 +223,9 @@ class Context:
 
     def stat_per_origin(self, P, Q, o_begin, o_end, stream=None):
         return ddks_stat_per_origin(self.ctx, P, Q, o_begin, o_end, stream)
+
+    def profile_read(self):
+        return ddks_profile_read(self.ctx)
 
     @property
     def launch_count(self) -> int:
