@@ -159,15 +159,36 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
     const int n_orig = pl.o_end - pl.o_begin;
     const int blocks_o = (n_orig + G::ORIGINS - 1) / G::ORIGINS;
     const int n_tiles = (pl.N + G::TILE - 1) / G::TILE;
-    // segment length: at most the int16 flush window, and short enough to give >= 2 CTAs per SM
-    const int w_tiles = std::max(1, (int)(pl.window / G::TILE));
-    int tiles_per_seg = std::min(n_tiles, w_tiles);
-    const int64_t ctas = pl.B * blocks_o;
-    if (ctas < 2 * 148 && !(ctx->flags & DDKS_FLAG_FORCE_DIRECT)) {
-        const int64_t want_segs = (2 * 148 + ctas - 1) / ctas;
-        tiles_per_seg = std::min<int64_t>(tiles_per_seg, std::max<int64_t>(1, (n_tiles + want_segs - 1) / want_segs));
+    // segment length: at most the int16 flush window; among the segment counts that respect it, pick the one
+    // whose CTA count fills the resident slots (SMs x CTAs/SM) with the least wave-quantisation loss
+    static int per_sm = 0;
+    if (!per_sm) {
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::T, G::SMEM_BYTES));
+        per_sm = std::max(per_sm, 1);
     }
-    const int segs = (n_tiles + tiles_per_seg - 1) / tiles_per_seg;
+    int nsm = 148;
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
+    const int64_t slots = (int64_t)nsm * per_sm;
+    const int w_tiles = std::max(1, (int)(pl.window / G::TILE));
+    const int min_segs = (n_tiles + w_tiles - 1) / w_tiles;
+    const int64_t base_ctas = pl.B * blocks_o;
+    int segs = min_segs;
+    if (!(ctx->flags & DDKS_FLAG_FORCE_DIRECT)) {
+        double best = -1.0;
+        const int max_segs = (int)std::min<int64_t>(n_tiles, std::max<int64_t>(min_segs, (8 * slots + base_ctas - 1) / base_ctas));
+        for (int sg = min_segs; sg <= max_segs; ++sg) {
+            const int tps = (n_tiles + sg - 1) / sg;
+            const int real = (n_tiles + tps - 1) / tps;
+            if (real != sg) continue;
+            const int64_t ctas = base_ctas * sg;
+            const int64_t waves = (ctas + slots - 1) / slots;
+            // fraction of slot-time doing useful work, minus a small cost per extra segment (flush + setup)
+            const double eff = (double)ctas / (double)(waves * slots) - 0.002 * (sg - min_segs);
+            if (eff > best + 1e-9) { best = eff; segs = sg; }
+        }
+    }
+    const int tiles_per_seg = (n_tiles + segs - 1) / segs;
+    segs = (n_tiles + tiles_per_seg - 1) / tiles_per_seg;
     a.seg_points = tiles_per_seg * G::TILE;
     if (segs > 65535) return fail(ctx, DDKS_ERR_TOO_LARGE, "too many point segments");
     if (segs > 1) {
@@ -257,13 +278,13 @@ ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int6
     return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "d=%d", d);
 }
 
-ddks_status launch_pack(ddks_ctx* ctx, const float* src, int64_t n_rows, int d, int64_t B, float* dst, int64_t N,
-                        int64_t row_off, uint32_t* flag, cudaStream_t st) {
-    const int64_t total = B * n_rows;
+ddks_status launch_pack(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d, int64_t B,
+                        float* dst, uint32_t* flag, cudaStream_t st) {
+    const int64_t total = B * (n_P + n_Q);
     if (total == 0) return DDKS_OK;
     const int threads = 256;
     const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 8);
-    ddks::k_pack<<<blocks, threads, 0, st>>>(src, n_rows, d, B, dst, N, row_off, pad_dim(d),
+    ddks::k_pack<<<blocks, threads, 0, st>>>(P, n_P, Q, n_Q, d, B, dst, pad_dim(d),
                                             (ctx->flags & DDKS_FLAG_NO_VALIDATE) ? 0 : 1, flag);
     CHECK_LAUNCH();
     ctx->launches++;
@@ -429,8 +450,7 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
     *hres = init;
     CU(cudaMemcpyAsync(dres, hres, sizeof init, cudaMemcpyHostToDevice, st));
     float* packed = (float*)ctx->packed.p;
-    if ((s = launch_pack(ctx, (const float*)dP, n_P, d, 1, packed, N, 0, &dres->flag, st))) return s;
-    if ((s = launch_pack(ctx, (const float*)dQ, n_Q, d, 1, packed, N, n_P, &dres->flag, st))) return s;
+    if ((s = launch_pack(ctx, (const float*)dP, n_P, (const float*)dQ, n_Q, d, 1, packed, &dres->flag, st))) return s;
     uint64_t* per = (uint64_t*)ctx->per_origin.p;
     if (oe > ob) {
         if ((s = run_count(ctx, packed, d, 1, n_P, n_Q, ob, oe, (uint64_t*)&dres->num, per, st))) return s;
@@ -535,8 +555,9 @@ ddks_status ddks_stat_batch(ddks_ctx* ctx, const float* P, const float* Q, int64
     if (nb > 0) {
         if ((s = ensure(ctx, ctx->packed, (size_t)nb * N * DP * 4))) return s;
         float* packed = (float*)ctx->packed.p;
-        if ((s = launch_pack(ctx, (const float*)dP + ib * n_P * d, n_P, d, nb, packed, N, 0, &dres->flag, st))) return s;
-        if ((s = launch_pack(ctx, (const float*)dQ + ib * n_Q * d, n_Q, d, nb, packed, N, n_P, &dres->flag, st))) return s;
+        if ((s = launch_pack(ctx, (const float*)dP + ib * n_P * d, n_P, (const float*)dQ + ib * n_Q * d, n_Q, d, nb,
+                             packed, &dres->flag, st)))
+            return s;
         if ((s = run_count(ctx, packed, d, nb, n_P, n_Q, 0, N, nums + ib, nullptr, st))) return s;
     }
     if (ctx->world > 1) {
@@ -587,7 +608,9 @@ ddks_status ddks_permutation_null(ddks_ctx* ctx, const float* pooled, int64_t n_
     // pack the pooled sample once: [N][DP]
     if ((s = ensure(ctx, ctx->pool_packed, (size_t)N * DP * 4))) return s;
     float* pooled_packed = (float*)ctx->pool_packed.p;
-    if ((s = launch_pack(ctx, (const float*)dpool, N, d, 1, pooled_packed, N, 0, &dres->flag, st))) return s;
+    if ((s = launch_pack(ctx, (const float*)dpool, n_P, (const float*)dpool + n_P * d, n_Q, d, 1, pooled_packed,
+                         &dres->flag, st)))
+        return s;
     // observed: every rank computes it (cheap relative to the null), no collective needed
     if ((s = run_count(ctx, pooled_packed, d, 1, n_P, n_Q, 0, N, nums, nullptr, st))) return s;
     int64_t jb, je;

@@ -117,15 +117,16 @@ template <int D> __device__ __forceinline__ void load_point(const float* sp, flo
 }
 
 // ----------------------------------------------------------------------------------------------- a1: validate + pack
-// src: [B][n_rows][d] row-major f32. dst: [B][N][DP] with the segment's rows at row offset `row_off`.
-// -0 -> +0, pad dims = 0. Non-finite -> *flag |= 1 (SPEC core-types NonFiniteValue).
-__global__ void k_pack(const float* __restrict__ src, int64_t n_rows, int d, int64_t B, float* __restrict__ dst,
-                       int64_t N, int64_t row_off, int DP, int validate, uint32_t* flag) {
-    const int64_t total = B * n_rows;
+// P: [B][n_P][d], Q: [B][n_Q][d] row-major f32 -> dst: [B][n_P + n_Q][DP] (P rows, then Q rows).
+// -0 -> +0, pad dims = 0. Non-finite -> *flag |= 1 (SPEC core-types NonFiniteValue). One launch for both samples.
+__global__ void k_pack(const float* __restrict__ P, int64_t n_P, const float* __restrict__ Q, int64_t n_Q, int d,
+                       int64_t B, float* __restrict__ dst, int DP, int validate, uint32_t* flag) {
+    const int64_t N = n_P + n_Q;
+    const int64_t total = B * N;
     bool bad = false;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = i / n_rows, r = i - b * n_rows;
-        const float* s = src + i * d;
+        const int64_t b = i / N, r = i - b * N;
+        const float* s = r < n_P ? P + (b * n_P + r) * d : Q + (b * n_Q + (r - n_P)) * d;
         float v[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -133,7 +134,7 @@ __global__ void k_pack(const float* __restrict__ src, int64_t n_rows, int d, int
             if (k < d && validate && !isfinite(t)) bad = true;
             v[k] = (t == 0.0f) ? 0.0f : t;
         }
-        float4* o = reinterpret_cast<float4*>(dst + ((b * N) + row_off + r) * DP);
+        float4* o = reinterpret_cast<float4*>(dst + i * DP);
         o[0] = make_float4(v[0], v[1], v[2], v[3]);
         if (DP == 8) o[1] = make_float4(v[4], v[5], v[6], v[7]);
     }
@@ -231,7 +232,7 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
     // read past the valid range is never used)
     float xn[D];
     load_point<D>(tile + lo * DP, xn);
-#pragma unroll 2
+#pragma unroll 4
     for (int p = lo; p < hi; ++p) {
         float x[D];
 #pragma unroll
@@ -239,9 +240,22 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
         load_point<D>(tile + (p + 1) * DP, xn);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            float f = base[r % RP];
+            float f;
+            if constexpr (D >= 6) {
+                // two half-length FFMA chains (exact: all partial sums are integers < 2^24) shorten the dependency
+                // chain when few warps are resident (d >= 6 keeps 256+ counters per origin in SMEM)
+                constexpr int H = D / 2;
+                float f0 = base[r % RP], f1 = 0.0f;
 #pragma unroll
-            for (int k = 0; k < D; ++k) f = fmaf(cmp_bit<GT>(x[k], o[r][k]), (float)(4 * (1 << k) * RP * T), f);
+                for (int k = 0; k < H; ++k) f0 = fmaf(cmp_bit<GT>(x[k], o[r][k]), (float)(4 * (1 << k) * RP * T), f0);
+#pragma unroll
+                for (int k = H; k < D; ++k) f1 = fmaf(cmp_bit<GT>(x[k], o[r][k]), (float)(4 * (1 << k) * RP * T), f1);
+                f = f0 + f1;
+            } else {
+                f = base[r % RP];
+#pragma unroll
+                for (int k = 0; k < D; ++k) f = fmaf(cmp_bit<GT>(x[k], o[r][k]), (float)(4 * (1 << k) * RP * T), f);
+            }
             red_add_shared(__float_as_uint(f) + ubase, r < RP ? inc_lo : inc_hi);
         }
     }
