@@ -65,6 +65,9 @@ typedef enum {
 #define DDKS_FLAG_TIES_GT 2u     /* TEST ONLY: bit k = [x_k > o_k] instead of >= (shows the convention matters) */
 #define DDKS_FLAG_FORCE_DIRECT 4u /* TEST ONLY: never split the point axis into segments (exercises the in-kernel
                                      finalisation at small N; results are identical either way)              */
+#define DDKS_FLAG_PERM_GATHER 16u /* TEST ONLY: permutation null by gathering each relabelled sample and re-running the
+                                      full classification (the default label-invariant path classifies each pair once
+                                      for a chunk of permutations; both give identical results)                    */
 #define DDKS_FLAG_PROFILE 8u      /* record CUDA events around every count-kernel launch (see ddks_profile_read) */
 
 typedef struct {

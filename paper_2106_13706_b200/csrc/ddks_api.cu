@@ -34,7 +34,7 @@ struct ddks_ctx {
     int device = 0, world = 1, rank = 0;
     uint32_t flags = 0;
     ncclComm_t comm = nullptr;
-    DevBuf raw_a, raw_b, raw_perm, packed, packed2, pool_packed, per_origin, accum, item_num, bitmap, res;
+    DevBuf raw_a, raw_b, raw_perm, packed, packed2, pool_packed, per_origin, accum, item_num, bitmap, labels, res;
     void* host_pinned = nullptr;  // DevResult + scratch
     size_t host_pinned_bytes = 0;
     int64_t launches = 0;
@@ -291,6 +291,79 @@ ddks_status launch_pack(ddks_ctx* ctx, const float* P, int64_t n_P, const float*
     return DDKS_OK;
 }
 
+// Label-invariant permutation null (NEXT-2): labels + validation, then one classification per pair for J perms.
+template <int D>
+ddks_status launch_perm_d(ddks_ctx* ctx, const float* pooled_packed, const int32_t* perms, int64_t n_perm,
+                          int64_t n_P, int64_t n_Q, uint64_t* nums, uint32_t* flag, cudaStream_t st) {
+    using G = ddks::PermGeo<D>;
+    const bool gt = (ctx->flags & DDKS_FLAG_TIES_GT) != 0;
+    auto kern = gt ? ddks::k_perm_count<D, true> : ddks::k_perm_count<D, false>;
+    static bool attr[2] = {false, false};
+    if (!attr[gt]) {
+        CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES));
+        attr[gt] = true;
+    }
+    const int64_t N = n_P + n_Q;
+    const int64_t chunks = (n_perm + G::J - 1) / G::J;
+    const int64_t words = (N + 31) / 32;
+    // [chunks][chunk_words] increment words; rows padded to 16 bytes (+16: the last bulk copy rounds up to 16)
+    const int64_t chunk_words = (N * G::JP + 3) & ~int64_t(3);
+    const size_t lab_bytes = (size_t)chunks * chunk_words * 4 + 16;
+    ddks_status s;
+    if ((s = ensure(ctx, ctx->labels, lab_bytes))) return s;
+    if ((s = ensure(ctx, ctx->bitmap, (size_t)n_perm * words * 4))) return s;
+    CU(cudaMemsetAsync(ctx->labels.p, 0, lab_bytes, st));
+    CU(cudaMemsetAsync(ctx->bitmap.p, 0, (size_t)n_perm * words * 4, st));
+    const int64_t tot = n_perm * N;
+    const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
+    ddks::k_labels<<<blocks, 256, 0, st>>>(perms, n_perm, N, n_P, G::J, chunk_words, (uint32_t*)ctx->labels.p,
+                                           (uint32_t*)ctx->bitmap.p, flag);
+    CHECK_LAUNCH();
+    ctx->launches++;
+    const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
+    ddks::PermArgs pa{};
+    pa.pts = pooled_packed;
+    pa.labels = (const uint32_t*)ctx->labels.p;
+    pa.chunk_words = chunk_words;
+    pa.N = (int32_t)N;
+    pa.n_perm = (int32_t)n_perm;
+    pa.a = (uint32_t)((uint64_t)n_Q / g);
+    pa.b = (uint32_t)((uint64_t)n_P / g);
+    pa.g = g;
+    pa.num = nums;
+    dim3 grid((unsigned)chunks, (unsigned)((N + G::T - 1) / G::T));
+    std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+    if (ctx->flags & DDKS_FLAG_PROFILE) {
+        CU(cudaEventCreate(&ev.first));
+        CU(cudaEventCreate(&ev.second));
+        CU(cudaEventRecord(ev.first, st));
+    }
+    kern<<<grid, G::T, G::SMEM_BYTES, st>>>(pa);
+    CHECK_LAUNCH();
+    ctx->launches++;
+    if (ev.first) {
+        CU(cudaEventRecord(ev.second, st));
+        ctx->ev_pending.push_back(ev);
+        ctx->ev_pairs.push_back((uint64_t)n_perm * (uint64_t)N * (uint64_t)N);
+    }
+    return DDKS_OK;
+}
+
+ddks_status launch_perm(ddks_ctx* ctx, int d, const float* pooled_packed, const int32_t* perms, int64_t n_perm,
+                        int64_t n_P, int64_t n_Q, uint64_t* nums, uint32_t* flag, cudaStream_t st) {
+    switch (d) {
+        case 1: return launch_perm_d<1>(ctx, pooled_packed, perms, n_perm, n_P, n_Q, nums, flag, st);
+        case 2: return launch_perm_d<2>(ctx, pooled_packed, perms, n_perm, n_P, n_Q, nums, flag, st);
+        case 3: return launch_perm_d<3>(ctx, pooled_packed, perms, n_perm, n_P, n_Q, nums, flag, st);
+        case 4: return launch_perm_d<4>(ctx, pooled_packed, perms, n_perm, n_P, n_Q, nums, flag, st);
+        case 5: return launch_perm_d<5>(ctx, pooled_packed, perms, n_perm, n_P, n_Q, nums, flag, st);
+        case 6: return launch_perm_d<6>(ctx, pooled_packed, perms, n_perm, n_P, n_Q, nums, flag, st);
+        case 7: return launch_perm_d<7>(ctx, pooled_packed, perms, n_perm, n_P, n_Q, nums, flag, st);
+        case 8: return launch_perm_d<8>(ctx, pooled_packed, perms, n_perm, n_P, n_Q, nums, flag, st);
+    }
+    return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "d=%d", d);
+}
+
 ddks_status ensure_host(ddks_ctx* ctx, size_t bytes) {
     if (bytes <= ctx->host_pinned_bytes) return DDKS_OK;
     if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
@@ -353,7 +426,7 @@ ddks_status ddks_create(ddks_ctx** out, int device, int world, int rank, const v
     if (world < 1 || rank < 0 || rank >= world) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad world/rank");
     if ((world == 1) != (nccl_id == nullptr))
         return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "nccl_id must be NULL iff world == 1");
-    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT | DDKS_FLAG_PROFILE)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
+    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT | DDKS_FLAG_PROFILE | DDKS_FLAG_PERM_GATHER)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
     int ndev = 0;
     CU(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device %d of %d", device, ndev);
@@ -394,7 +467,7 @@ ddks_status ddks_destroy(ddks_ctx* ctx) {
             cudaEventDestroy(e.second);
         }
     for (DevBuf* b : {&ctx->raw_a, &ctx->raw_b, &ctx->raw_perm, &ctx->packed, &ctx->packed2, &ctx->pool_packed, &ctx->per_origin,
-                      &ctx->accum, &ctx->item_num, &ctx->bitmap, &ctx->res})
+                      &ctx->accum, &ctx->item_num, &ctx->bitmap, &ctx->labels, &ctx->res})
         if (b->p) cudaFree(b->p);
     if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
     delete ctx;
@@ -615,25 +688,33 @@ ddks_status ddks_permutation_null(ddks_ctx* ctx, const float* pooled, int64_t n_
     if ((s = run_count(ctx, pooled_packed, d, 1, n_P, n_Q, 0, N, nums, nullptr, st))) return s;
     int64_t jb, je;
     ddks_shard_range(n_perm, ctx->world, ctx->rank, &jb, &je);
-    const int64_t chunk_max = std::max<int64_t>(1, (int64_t)((256ull << 20) / ((size_t)N * DP * 4)));
-    for (int64_t j0 = jb; j0 < je; j0 += chunk_max) {
-        const int64_t nc = std::min(chunk_max, je - j0);
-        if ((s = ensure(ctx, ctx->packed, (size_t)nc * N * DP * 4))) return s;
-        const int64_t words = (N + 31) / 32;
-        if ((s = ensure(ctx, ctx->bitmap, (size_t)nc * words * 4))) return s;
-        CU(cudaMemsetAsync(ctx->bitmap.p, 0, (size_t)nc * words * 4, st));
-        const int64_t tot = nc * N;
-        const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
-        if (DP == 4)
-            ddks::k_gather<4><<<blocks, 256, 0, st>>>(pooled_packed, (const int32_t*)dperm + j0 * N, nc, N,
-                                                      (float*)ctx->packed.p, (uint32_t*)ctx->bitmap.p, &dres->flag);
-        else
-            ddks::k_gather<8><<<blocks, 256, 0, st>>>(pooled_packed, (const int32_t*)dperm + j0 * N, nc, N,
-                                                      (float*)ctx->packed.p, (uint32_t*)ctx->bitmap.p, &dres->flag);
-        CHECK_LAUNCH();
-        ctx->launches++;
-        if ((s = run_count(ctx, (const float*)ctx->packed.p, d, nc, n_P, n_Q, 0, N, nums + 1 + j0, nullptr, st)))
+    const bool label_path = N <= 65535 && !(ctx->flags & DDKS_FLAG_PERM_GATHER);
+    if (label_path) {
+        if (je > jb &&
+            (s = launch_perm(ctx, d, pooled_packed, (const int32_t*)dperm + jb * N, je - jb, n_P, n_Q, nums + 1 + jb,
+                             &dres->flag, st)))
             return s;
+    } else {
+        const int64_t chunk_max = std::max<int64_t>(1, (int64_t)((256ull << 20) / ((size_t)N * DP * 4)));
+        for (int64_t j0 = jb; j0 < je; j0 += chunk_max) {
+            const int64_t nc = std::min(chunk_max, je - j0);
+            if ((s = ensure(ctx, ctx->packed, (size_t)nc * N * DP * 4))) return s;
+            const int64_t words = (N + 31) / 32;
+            if ((s = ensure(ctx, ctx->bitmap, (size_t)nc * words * 4))) return s;
+            CU(cudaMemsetAsync(ctx->bitmap.p, 0, (size_t)nc * words * 4, st));
+            const int64_t tot = nc * N;
+            const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
+            if (DP == 4)
+                ddks::k_gather<4><<<blocks, 256, 0, st>>>(pooled_packed, (const int32_t*)dperm + j0 * N, nc, N,
+                                                          (float*)ctx->packed.p, (uint32_t*)ctx->bitmap.p, &dres->flag);
+            else
+                ddks::k_gather<8><<<blocks, 256, 0, st>>>(pooled_packed, (const int32_t*)dperm + j0 * N, nc, N,
+                                                          (float*)ctx->packed.p, (uint32_t*)ctx->bitmap.p, &dres->flag);
+            CHECK_LAUNCH();
+            ctx->launches++;
+            if ((s = run_count(ctx, (const float*)ctx->packed.p, d, nc, n_P, n_Q, 0, N, nums + 1 + j0, nullptr, st)))
+                return s;
+        }
     }
     if (ctx->world > 1) {
         if ((s = all_gather_items(ctx, nums + 1, n_perm, st))) return s;

@@ -19,6 +19,7 @@
 //   * finalisation is exact integer arithmetic; the max is a warp-shuffle + CTA + atomicMax(u64) reduction.
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 namespace ddks {
@@ -417,6 +418,175 @@ __global__ void k_finalize(const CountArgs a, int64_t B) {
         best = warp_max_u64(best);
         if ((threadIdx.x & 31) == 0)
             atomicMax(reinterpret_cast<unsigned long long*>(&a.item_num[0]), (unsigned long long)best);
+    }
+}
+
+// ----------------------------------------------------------------------------------------------- a9: label-invariant permutation null
+// SURVEY.md §8f NEXT-2. code(o, x) does not depend on the labels, so one classification of a pair serves J
+// permutations at once: for permutation j only the P'-count is needed, because with T[q] = all points in orthant q,
+//     c_P' a - c_Q' b = (a + b) c_P' - b T[q]          (a = n_Q/g, b = n_P/g, exact integers).
+// Counters are unsigned 16-bit halves, two permutations per 32-bit word (c_P' <= n_P < 2^16, T <= N < 2^16; the
+// host guarantees N <= 65535). The labels arrive pre-spread: for point x and permutation pair i the increment word
+// is [x in P' of perm 2i] | [x in P' of perm 2i+1] << 16, so per pair the kernel does d FSET + d FFMA (address, once)
+// + one ATOMS for T + J/2 ATOMS with the label word as the increment (no predicates, no branches).
+template <int D> struct PermCfg;
+template <> struct PermCfg<1> { static constexpr int J = 16, T = 256; };
+template <> struct PermCfg<2> { static constexpr int J = 16, T = 256; };
+template <> struct PermCfg<3> { static constexpr int J = 16, T = 256; };
+template <> struct PermCfg<4> { static constexpr int J = 16, T = 256; };
+template <> struct PermCfg<5> { static constexpr int J = 16, T = 160; };
+template <> struct PermCfg<6> { static constexpr int J = 8, T = 128; };
+template <> struct PermCfg<7> { static constexpr int J = 4, T = 128; };
+template <> struct PermCfg<8> { static constexpr int J = 2, T = 96; };
+
+template <int D> struct PermGeo {
+    static constexpr int J = PermCfg<D>::J, T = PermCfg<D>::T, JP = J / 2;
+    static constexpr int NQ = 1 << D, DP = padded_dim<D>(), TILE = 256, S = 2;
+    static constexpr int CNT_WORDS = NQ * (JP + 1) * T;   // [q][JP + 1][T]; slot JP holds T[q]
+    static constexpr int STAGE_BYTES = TILE * DP * 4 + TILE * JP * 4;
+    static constexpr int SMEM_BYTES = CNT_WORDS * 4 + S * STAGE_BYTES + 64;
+    static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+};
+
+struct PermArgs {
+    const float* pts;         // pooled packed [N][DP]
+    const uint32_t* labels;   // [n_chunks][chunk_words] spread increment words [N][JP] (see above)
+    int64_t chunk_words;      // N*JP rounded up to 4 (16-byte aligned chunk rows for the bulk copies)
+    int32_t N, n_perm;
+    uint32_t a, b;            // DIFF weights
+    uint64_t g;
+    uint64_t* num;            // [n_perm] atomicMax targets
+};
+
+// labels + validation: for row j of perms, check it is a permutation of 0..N-1 (range + no duplicate via bitmap,
+// else *flag |= 2) and, for i < n_P, add the P' bit of permutation j to the increment word of point perms[j][i].
+__global__ void k_labels(const int32_t* __restrict__ perms, int64_t n_perm, int64_t N, int64_t n_P, int J,
+                         int64_t chunk_words, uint32_t* __restrict__ labels, uint32_t* __restrict__ bitmap,
+                         uint32_t* flag) {
+    const int64_t words = (N + 31) / 32;
+    const int64_t total = n_perm * N;
+    const int JP = J / 2;
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = i / N, pos = i - j * N;
+        const int32_t src = perms[i];
+        if (src < 0 || src >= N) { bad = true; continue; }
+        const uint32_t bit = 1u << (src & 31);
+        if (atomicOr(&bitmap[j * words + (src >> 5)], bit) & bit) bad = true;
+        if (pos < n_P) {
+            const int64_t jj = j % J;
+            atomicOr(&labels[(j / J) * chunk_words + (int64_t)src * JP + (jj >> 1)], 1u << (16 * (jj & 1)));
+        }
+    }
+    if (bad) atomicOr(flag, 2u);
+}
+
+template <int D, bool GT>
+__global__ void __launch_bounds__(PermGeo<D>::T, 1) k_perm_count(const PermArgs a) {
+    using G = PermGeo<D>;
+    constexpr int J = G::J, JP = G::JP, T = G::T, DP = G::DP, TILE = G::TILE, S = G::S, NQ = G::NQ;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(smem);                                 // [NQ][JP+1][T]
+    uint8_t* stages = smem + G::CNT_WORDS * 4;                                          // S x (points, labels)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stages + S * G::STAGE_BYTES);
+
+    const int t = threadIdx.x;
+    const int chunk = blockIdx.x;
+    const int j0 = chunk * J;
+    const int nj = min(J, a.n_perm - j0);
+    const uint32_t* lab = a.labels + (int64_t)chunk * a.chunk_words;
+    int32_t oi = (int32_t)blockIdx.y * T + t;
+    const bool valid = oi < a.N;
+    oi = valid ? oi : a.N - 1;
+    const int n_tiles = (a.N + TILE - 1) / TILE;
+
+    if (t == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = t; i < G::CNT_WORDS; i += T) cnt[i] = 0u;
+    __syncthreads();
+    auto issue = [&](int it, int s) {
+        const int32_t p0 = it * TILE;
+        const int n = min(TILE, a.N - p0);
+        float* sp = reinterpret_cast<float*>(stages + s * G::STAGE_BYTES);
+        uint32_t* sl = reinterpret_cast<uint32_t*>(stages + s * G::STAGE_BYTES + TILE * DP * 4);
+        const uint32_t pb = (uint32_t)(n * DP * 4), lb = (uint32_t)((n * JP * 4 + 15) & ~15);
+        mbar_expect_tx(&bars[s], pb + lb);
+        bulk_g2s(sp, a.pts + (int64_t)p0 * DP, pb, &bars[s]);
+        bulk_g2s(sl, lab + (int64_t)p0 * JP, lb, &bars[s]);
+    };
+    if (t == 0)
+        for (int s = 0; s < S && s < n_tiles; ++s) issue(s, s);
+
+    float o[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) o[k] = __ldg(a.pts + (int64_t)oi * DP + k);
+    const uint32_t ubase = smem_u32(cnt) - 0x4B000000u;
+    const float base = __uint_as_float(0x4B000000u + 4u * (uint32_t)t);
+    constexpr uint32_t SLOT = 4u * T;  // bytes between permutation-pair slots of one bin
+
+    for (int it = 0; it < n_tiles; ++it) {
+        const int s = it % S;
+        mbar_wait(&bars[s], (uint32_t)((it / S) & 1));
+        const float* sp = reinterpret_cast<const float*>(stages + s * G::STAGE_BYTES);
+        const uint32_t* sl = reinterpret_cast<const uint32_t*>(stages + s * G::STAGE_BYTES + TILE * DP * 4);
+        const int n = min(TILE, a.N - it * TILE);
+#pragma unroll 2
+        for (int p = 0; p < n; ++p) {
+            float x[D];
+            load_point<D>(sp + p * DP, x);
+            float f = base;
+#pragma unroll
+            for (int k = 0; k < D; ++k) f = fmaf(cmp_bit<GT>(x[k], o[k]), (float)(4 * (1 << k) * (JP + 1) * T), f);
+            const uint32_t addr = __float_as_uint(f) + ubase;
+            red_add_shared(addr + JP * SLOT, 1u);  // T[q]
+            const uint32_t* lw = sl + p * JP;
+            if constexpr (JP % 4 == 0) {
+#pragma unroll
+                for (int i = 0; i < JP; i += 4) {
+                    const uint4 w = *reinterpret_cast<const uint4*>(lw + i);
+                    red_add_shared(addr + (i + 0) * SLOT, w.x);
+                    red_add_shared(addr + (i + 1) * SLOT, w.y);
+                    red_add_shared(addr + (i + 2) * SLOT, w.z);
+                    red_add_shared(addr + (i + 3) * SLOT, w.w);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < JP; ++i) red_add_shared(addr + i * SLOT, lw[i]);
+            }
+        }
+        __syncthreads();
+        if (t == 0 && it + S < n_tiles) {
+            fence_proxy_async();
+            issue(it + S, s);
+        }
+    }
+    __syncthreads();
+
+    // finalise: num_j(o) = g * max_q |(a+b) c_P'[q] - b T[q]|, then max over this warp's origins per permutation
+    __shared__ uint64_t wmax[T / 32][J];
+    for (int j = 0; j < nj; ++j) {
+        uint64_t m = 0;
+        if (valid) {
+            for (int q = 0; q < NQ; ++q) {
+                const uint32_t w = cnt[(q * (JP + 1) + (j >> 1)) * T + t];
+                const int64_t cP = (j & 1) ? (w >> 16) : (w & 0xffffu);
+                const int64_t Tq = cnt[(q * (JP + 1) + JP) * T + t] & 0xffffu;
+                const int64_t v = (int64_t)(a.a + a.b) * cP - (int64_t)a.b * Tq;
+                const uint64_t av = (uint64_t)(v < 0 ? -v : v);
+                m = av > m ? av : m;
+            }
+            m *= a.g;
+        }
+        m = warp_max_u64(m);
+        if ((t & 31) == 0) wmax[t >> 5][j] = m;
+    }
+    __syncthreads();
+    if (t < nj) {
+        uint64_t m = 0;
+        for (int w = 0; w < T / 32; ++w) m = wmax[w][t] > m ? wmax[w][t] : m;
+        atomicMax(reinterpret_cast<unsigned long long*>(&a.num[j0 + t]), (unsigned long long)m);
     }
 }
 

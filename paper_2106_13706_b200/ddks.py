@@ -24,6 +24,7 @@ DDKS_FLAG_NO_VALIDATE = 1
 DDKS_FLAG_TIES_GT = 2
 DDKS_FLAG_FORCE_DIRECT = 4
 DDKS_FLAG_PROFILE = 8
+DDKS_FLAG_PERM_GATHER = 16
 
 
 class DDKSError(RuntimeError):

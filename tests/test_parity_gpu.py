@@ -202,16 +202,36 @@ def test_batch_parity(ctx, ctx_direct):
             assert all(r.den == n_P * n_Q for r in got)
 
 
-def test_permutation_parity(ctx):
-    rng = np.random.default_rng(22)
-    for (n_P, n_Q, d, n_perm) in [(20, 20, 1, 30), (100, 80, 3, 50), (300, 300, 5, 12)]:
+@pytest.fixture(scope="module")
+def ctx_gather():
+    c = K.Context(flags=K.DDKS_FLAG_PERM_GATHER)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("d", range(1, 9))
+def test_permutation_parity(ctx, ctx_gather, d):
+    # default path: label-invariant (one classification per pair for J permutations); gather path: relabel + recount
+    rng = np.random.default_rng(22 + d)
+    for (n_P, n_Q, n_perm) in [(20, 21, 33), (100, 80, 50), (301, 299, 17), (1, 6, 5)]:
         pooled = rng.standard_normal((n_P + n_Q, d)).astype(np.float32)
+        pooled[::4] = np.round(pooled[::4])
         perms = np.stack([np.arange(n_P + n_Q)] + [rng.permutation(n_P + n_Q) for _ in range(n_perm - 1)]).astype(np.int32)
         null, obs, p_num, p = O.permutation_null(pooled, n_P, perms)
-        g_null, g_obs, g_p = ctx.permutation_null(dev(pooled), n_P, dev(perms))
-        assert np.array_equal(g_null, null) and g_obs.num == obs and g_p == p
-        g_null2, _, _ = ctx.permutation_null(pooled, n_P, perms)  # host inputs
-        assert np.array_equal(g_null2, null)
+        for c in (ctx, ctx_gather):
+            g_null, g_obs, g_p = c.permutation_null(dev(pooled), n_P, dev(perms))
+            assert np.array_equal(g_null, null) and g_obs.num == obs and g_p == p, (d, n_P, n_Q)
+    g_null2, _, _ = ctx.permutation_null(pooled, n_P, perms)  # host inputs
+    assert np.array_equal(g_null2, null)
+
+
+def test_permutation_ties_gt(ctx_gt):
+    rng = np.random.default_rng(5)
+    pooled = rng.integers(0, 3, (60, 3)).astype(np.float32)
+    perms = np.stack([rng.permutation(60) for _ in range(40)]).astype(np.int32)
+    null, obs, _, p = O.permutation_null(pooled, 25, perms, ties_gt=True)
+    g_null, g_obs, g_p = ctx_gt.permutation_null(dev(pooled), 25, dev(perms))
+    assert np.array_equal(g_null, null) and g_obs.num == obs and g_p == p
 
 
 # ----------------------------------------------------------------------------------- BASELINE configs
