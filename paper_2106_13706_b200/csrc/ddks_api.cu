@@ -200,8 +200,8 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
     } else {
         a.accum = nullptr;
     }
-    if (pl.B > 0x7fffffff || blocks_o > 65535) return fail(ctx, DDKS_ERR_TOO_LARGE, "grid too large");
-    dim3 grid((unsigned)pl.B, (unsigned)blocks_o, (unsigned)segs);
+    if (pl.B > 65535 || blocks_o > 65535) return fail(ctx, DDKS_ERR_TOO_LARGE, "grid too large");
+    dim3 grid((unsigned)segs, (unsigned)blocks_o, (unsigned)pl.B);
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
     if (ctx->flags & DDKS_FLAG_PROFILE) {
         if (!ctx->ev_free.empty()) {
@@ -265,6 +265,15 @@ ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int6
     a.nQ = n_Q;
     a.item_num = item_num;
     a.per_origin = per_origin;
+    if (B > 65535) {  // grid.z limit: run the items in chunks
+        for (int64_t b0 = 0; b0 < B; b0 += 65535) {
+            const int64_t nb = std::min<int64_t>(65535, B - b0);
+            ddks_status s = run_count(ctx, packed + b0 * N * pad_dim(d), d, nb, n_P, n_Q, o_begin, o_end,
+                                      item_num + b0, nullptr, st);
+            if (s) return s;
+        }
+        return DDKS_OK;
+    }
     switch (d) {
         case 1: return launch_count_d<1>(ctx, pl, a, st);
         case 2: return launch_count_d<2>(ctx, pl, a, st);

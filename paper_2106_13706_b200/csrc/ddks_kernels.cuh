@@ -271,11 +271,13 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem + S * G::TILE_BYTES);          // [NB][RP][T]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * G::TILE_BYTES + G::HIST_WORDS * 4);
 
+    // grid: x = point segment (fastest, so the CTAs in flight share origin blocks and their accumulators stay
+    // L2-resident), y = origin block, z = item
     const int t = threadIdx.x;
-    const int64_t item = blockIdx.x;
+    const int64_t item = blockIdx.z;
     const float* pts = a.pts + item * a.item_stride;
     const int32_t blk_o0 = a.o_begin + (int32_t)blockIdx.y * G::ORIGINS;
-    const int32_t seg0 = (int32_t)blockIdx.z * a.seg_points;
+    const int32_t seg0 = (int32_t)blockIdx.x * a.seg_points;
     const int32_t seg1 = min(a.N, seg0 + a.seg_points);
     const int n_tiles = (seg1 - seg0 + TILE - 1) / TILE;
 
