@@ -175,3 +175,71 @@ int oracle_permutation_null(const float* pooled, int64_t n_P, int64_t n_Q, int d
     *p_value = (double)(1 + ge) / (double)(1 + n_perm);
     return rc;
 }
+
+/* ===================================================================================================================
+ * Analytic significance (§3). TEST INFRASTRUCTURE ONLY, like the above.
+ *
+ *   M_T[i,k]  = # points of T (= Q) in orthant i about test point k, test points = all pooled points
+ *   lambda_ik = (M_T[i,k] + 1) / (N_T + 2)                                           (Bayes estimator)
+ *   p(n:m,l)  = C(m,n) l^n (1-l)^(m-n)                                              (binomial pmf)
+ *               or, with `poisson`, the Poisson pmf e^{-ml} (ml)^n / n!
+ *   p(d<=D)   = sum over (n_P, n_T), 0<=n_P<=N_P, 0<=n_T<=N_T, with |n_P/N_P - n_T/N_T| <= D
+ *               of p(n_P:N_P,l) p(n_T:N_T,l)                                        (R12:
+ *               "<=", decided exactly as |n_P N_T - n_T N_P| <= num with D = num / (N_P N_T))
+ *   S         = 1 - prod over the 2^d orthants i and the N test points k of p(d<=D)    (R13)
+ * Written literally: for every cell, the full double sum; the product accumulated as a sum of logs.
+ * ===================================================================================================================*/
+#include <math.h>
+
+/* log of the binomial (or Poisson) pmf of n successes in m trials at rate l (P:L244-250 / P:L278-281). */
+double oracle_log_pmf(int64_t n, int64_t m, double l, int poisson)
+{
+    if (poisson) {
+        double mu = (double)m * l;
+        return -mu + (double)n * log(mu) - lgamma((double)n + 1.0);
+    }
+    return lgamma((double)m + 1.0) - lgamma((double)n + 1.0) - lgamma((double)(m - n) + 1.0)
+         + (double)n * log(l) + (double)(m - n) * log1p(-l);
+}
+
+/* p(d <= D : N_P, N_T, l) with D = num / (N_P N_T): the double sum over the Delta-set band. */
+double oracle_p_le(uint64_t num, int64_t N_P, int64_t N_T, double l, int poisson)
+{
+    double p = 0.0;
+    for (int64_t nP = 0; nP <= N_P; ++nP) {
+        for (int64_t nT = 0; nT <= N_T; ++nT) {
+            int64_t diff = nP * N_T - nT * N_P;
+            uint64_t a = (uint64_t)(diff < 0 ? -diff : diff);
+            if (a <= num)
+                p += exp(oracle_log_pmf(nP, N_P, l, poisson) + oracle_log_pmf(nT, N_T, l, poisson));
+        }
+    }
+    return p;
+}
+
+/* S for the pair (P, Q): computes num (the statistic) and M_T by the loop method above, then the product.
+ * Outputs: *S, *log_prod = sum of log p(d<=D) over all 2^d x N cells, *num_out. Returns 0 on success. */
+int oracle_significance(const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d, int ties_gt, int poisson,
+                        int nthreads, double* S, double* log_prod, uint64_t* num_out)
+{
+    uint64_t num, den; double D; int64_t arg;
+    int rc = oracle_ddks(P, n_P, Q, n_Q, d, ties_gt, nthreads, &num, &den, &D, &arg);
+    if (rc) return rc;
+    int64_t N = n_P + n_Q, nq = (int64_t)1 << d;
+    double acc = 0.0;
+#pragma omp parallel for reduction(+ : acc) schedule(dynamic, 4)
+    for (int64_t k = 0; k < N; ++k) {
+        const float* test = pooled_row(P, n_P, Q, d, k);
+        int64_t* MT = (int64_t*)calloc((size_t)nq, sizeof(int64_t));
+        for (int64_t x = 0; x < n_Q; ++x) MT[oracle_orthant_index(test, Q + x * d, d, ties_gt)] += 1;
+        for (int64_t i = 0; i < nq; ++i) {
+            double l = ((double)MT[i] + 1.0) / ((double)n_Q + 2.0);
+            acc += log(oracle_p_le(num, n_P, n_Q, l, poisson));
+        }
+        free(MT);
+    }
+    *log_prod = acc;
+    *S = 1.0 - exp(acc);
+    *num_out = num;
+    return 0;
+}

@@ -14,6 +14,9 @@ Two independent implementations live here:
   AND_k ([x_k >= o_k] == bit_k(q)) on every point (Eq. 1, Eq. 2), and compares the
   normalised counts as exact Fractions. O(2^d N^2 d): tiny inputs only.
 
+Also the analytic significance of §3 (``log_pmf``, ``p_le``, ``significance``), written literally:
+every cell's full double sum over the Delta-set band, the product as a sum of logs.
+
 Plus ``ks_1d``: the classical two-sample KS statistic by a sort-merge sweep over the pooled values with
 exact integers (the d=1 closed form) — used to pin the oracle, not by the oracle.
 
@@ -65,6 +68,12 @@ def _load():
         lib.oracle_ddks_batch.restype = c_int
         lib.oracle_permutation_null.argtypes = [c_p, c_i64, c_i64, c_int, c_p, c_i64, c_int, c_int, c_p, c_p, c_p, c_p]
         lib.oracle_permutation_null.restype = c_int
+        lib.oracle_log_pmf.argtypes = [c_i64, c_i64, ctypes.c_double, c_int]
+        lib.oracle_log_pmf.restype = ctypes.c_double
+        lib.oracle_p_le.argtypes = [ctypes.c_uint64, c_i64, c_i64, ctypes.c_double, c_int]
+        lib.oracle_p_le.restype = ctypes.c_double
+        lib.oracle_significance.argtypes = [c_p, c_i64, c_p, c_i64, c_int, c_int, c_int, c_int, c_p, c_p, c_p]
+        lib.oracle_significance.restype = c_int
         _lib = lib
     return _lib
 
@@ -144,6 +153,28 @@ def permutation_null(pooled, n_P: int, perms, ties_gt: bool = False, threads: in
     if rc:
         raise ValueError(f"oracle_permutation_null rc={rc}")
     return null, int(obs.value), int(p_num.value), float(p_val.value)
+
+
+def log_pmf(n: int, m: int, lam: float, poisson: bool = False) -> float:
+    """P:L244-250 binomial pmf (or P:L278-281 Poisson pmf) of n successes in m trials at rate lam, as a log."""
+    return float(_load().oracle_log_pmf(n, m, lam, int(poisson)))
+
+
+def p_le(num: int, N_P: int, N_T: int, lam: float, poisson: bool = False) -> float:
+    """p(d <= D) with D = num / (N_P N_T), the double sum over the Delta-set band."""
+    return float(_load().oracle_p_le(num, N_P, N_T, lam, int(poisson)))
+
+
+def significance(P, Q, ties_gt: bool = False, poisson: bool = False, threads: int = 0):
+    """S = 1 - prod over the 2^d x N cells of p(d <= D) with lambda = (M_T + 1)/(N_T + 2).
+    -> (S, log_prod, num)."""
+    P, Q = _f32(P), _f32(Q)
+    S, lp, num = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint64()
+    rc = _load().oracle_significance(_ptr(P), P.shape[0], _ptr(Q), Q.shape[0], P.shape[1], int(ties_gt), int(poisson),
+                                     threads, ctypes.byref(S), ctypes.byref(lp), ctypes.byref(num))
+    if rc:
+        raise ValueError(f"oracle_significance rc={rc}")
+    return float(S.value), float(lp.value), int(num.value)
 
 
 # ---------------------------------------------------------------------------------------------------

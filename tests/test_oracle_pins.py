@@ -298,3 +298,63 @@ def test_c4_spots():
     null, obs, p_num, p = O.permutation_null(pooled, 512, perms)
     assert obs == 39936 and int(null.max()) == 34816 and int(null.sum()) == 23_215_616
     assert p_num == 1 and p == 1 / 1001
+
+
+# ------------------------------------------------------------------------------------ analytic significance (§3)
+
+def test_significance_pmf_pins():
+    import scipy.stats as st
+    # SPEC S:L330-332 binomial_pmf examples and the zero-success closed form
+    assert abs(math.exp(O.log_pmf(1, 2, 0.5)) - 0.5) < 1e-15
+    for m, lam in [(7, 0.3), (50, 0.02), (1000, 0.5)]:
+        assert abs(math.exp(O.log_pmf(0, m, lam)) - (1 - lam) ** m) <= 1e-12 * max((1 - lam) ** m, 1e-300)
+        tot = sum(math.exp(O.log_pmf(n, m, lam)) for n in range(m + 1))
+        assert abs(tot - 1.0) < 1e-10
+        # textbook pmfs (binomial, Poisson) from an independent library implementation
+        for n in (0, 1, m // 3, m):
+            assert abs(math.exp(O.log_pmf(n, m, lam)) - st.binom.pmf(n, m, lam)) <= 1e-11 * max(st.binom.pmf(n, m, lam), 1e-300) + 1e-300
+            assert abs(math.exp(O.log_pmf(n, m, lam, poisson=True)) - st.poisson.pmf(n, m * lam)) <= 1e-11 * max(st.poisson.pmf(n, m * lam), 1e-300) + 1e-300
+
+
+def test_significance_p_le_pins():
+    # SPEC S:L340-342 delta_cdf four-outcome enumerations (n_p = n_t = 1, lambda = 0.5)
+    assert abs(O.p_le(0, 1, 1, 0.5) - 0.5) < 1e-15        # D = 0: (0,0) and (1,1)
+    assert abs(O.p_le(1, 1, 1, 0.5) - 1.0) < 1e-15        # D = 1: everything
+    for lam in (0.1, 0.37, 0.9):                            # closed form P(X = Y), X, Y ~ Bernoulli(lam)
+        assert abs(O.p_le(0, 1, 1, lam) - (lam * lam + (1 - lam) ** 2)) < 1e-14
+    # D = 1 covers the whole Delta-set: the factor is 1 (sum of all pmf products)
+    assert abs(O.p_le(30 * 40, 30, 40, 0.23) - 1.0) < 1e-12
+    # monotone in D; symmetric under lambda -> 1 - lambda when N_P = N_T (n -> N - n maps the band to itself)
+    vals = [O.p_le(num, 20, 20, 0.3) for num in range(0, 401, 20)]
+    assert all(b >= a - 1e-15 for a, b in zip(vals, vals[1:]))
+    assert abs(O.p_le(60, 20, 20, 0.3) - O.p_le(60, 20, 20, 0.7)) < 1e-13
+
+
+def test_significance_p_le_against_monte_carlo():
+    # an independent estimate of P(|X/N_P - Y/N_T| <= D), X ~ Bi(N_P, l), Y ~ Bi(N_T, l): within 5 sigma
+    rng = np.random.default_rng(31)
+    for (N_P, N_T, lam, num) in [(12, 9, 0.3, 20), (50, 50, 0.05, 150), (40, 25, 0.6, 60)]:
+        n = 400_000
+        X = rng.binomial(N_P, lam, n)
+        Y = rng.binomial(N_T, lam, n)
+        frac = np.mean(np.abs(X * N_T - Y * N_P) <= num)
+        p = O.p_le(num, N_P, N_T, lam)
+        assert abs(frac - p) <= 5 * math.sqrt(p * (1 - p) / n) + 1e-9, (N_P, N_T, lam, num, frac, p)
+
+
+def test_significance_statistic_pins():
+    # fully separated samples: D = 1, every factor is 1 -> S = 0
+    rng = np.random.default_rng(32)
+    P = rng.random((12, 2)).astype(np.float32)
+    Q = (rng.random((10, 2)) + 2).astype(np.float32)
+    S, lp, num = O.significance(P, Q)
+    assert num == 120 and abs(S) < 1e-12
+    # identical samples: D = 0, cannot reject (S > 0.9)
+    P = rng.random((50, 3)).astype(np.float32)
+    S, lp, num = O.significance(P, P.copy())
+    assert num == 0 and S > 0.9
+    # S is a probability; Poisson variant close to binomial when rates are small
+    P, Q = I.random_pair(33, 40, 30, 3, "normal")
+    S_b, _, _ = O.significance(P, Q)
+    S_p, _, _ = O.significance(P, Q, poisson=True)
+    assert 0.0 <= S_b <= 1.0 and 0.0 <= S_p <= 1.0
