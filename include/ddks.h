@@ -108,6 +108,34 @@ DDKS_API ddks_status ddks_permutation_null(ddks_ctx* ctx, const float* pooled, i
 DDKS_API ddks_status ddks_stat_per_origin(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
                                  int64_t o_begin, int64_t o_end, uint64_t* num_out, void* stream);
 
+/* ---- Analytic significance (§3) ----------------------------------
+ *   M_T[i,k] = # points of Q ("T") in orthant i about pooled test point k (all N pooled points),
+ *   lambda   = (M_T[i,k] + 1) / (n_Q + 2)                            (Bayes estimator, uniform prior),
+ *   p(d<=D)  = sum over (n_P', n_Q') in 0..n_P x 0..n_Q with |n_P' n_Q - n_Q' n_P| <= num
+ *              of pmf(n_P' : n_P, lambda) pmf(n_Q' : n_Q, lambda)     ("<=" per DESIGN.md R12),
+ *              pmf binomial, or Poisson with mean m*lambda if sig_flags has DDKS_SIG_POISSON,
+ *   S        = 1 - prod over the 2^d orthants i and N test points k of p(d<=D)          (R13).
+ * The statistic itself (out->stat) is computed exactly as ddks_stat does (same num/den/D/argmax).
+ * log_prod = sum of log p(d<=D) over the 2^d N cells (each term computed as log1p(-(1 - p)), the complement summed
+ * directly; R14); S = -expm1(log_prod). Terms of a pmf below e^-100 of its mode are omitted (absolute
+ * error <= N e^-100 per cell).
+ * Optional host/device outputs (NULL if not wanted): mt_hist[n_Q + 1] = number of cells with M_T = m;
+ * log_p_table[n_Q + 1] = log p(d<=D | lambda_m) for every m with mt_hist[m] > 0, 0 elsewhere.
+ * Multi-GPU: origins sharded as in ddks_stat; the histogram is all-reduced (sum) and the table entries are sharded;
+ * every rank returns the full result. */
+#define DDKS_SIG_POISSON 1u
+
+typedef struct {
+    ddks_result stat; /* the ddKS statistic (as ddks_stat) */
+    double S;         /* significance: 1 - prod p(d <= D) (small S: reject "same distribution")  */
+    double log_prod;  /* sum over the cells of log p(d <= D) (<= 0)                              */
+    int64_t cells;    /* 2^d * (n_P + n_Q)                                                         */
+} ddks_significance_result;
+
+DDKS_API ddks_status ddks_significance(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
+                              uint32_t sig_flags, void* stream, ddks_significance_result* out, uint64_t* mt_hist,
+                              double* log_p_table);
+
 /* Host-only helper (no GPU needed): the contiguous origin / item range [*begin, *end) that `rank` of `world`
  * owns out of `total` units. Ranges are balanced to within one unit and cover 0..total exactly. */
 DDKS_API ddks_status ddks_shard_range(int64_t total, int world, int rank, int64_t* begin, int64_t* end);

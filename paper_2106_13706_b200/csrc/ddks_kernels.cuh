@@ -178,6 +178,8 @@ struct CountArgs {
     uint64_t* item_num;      // [B] atomicMax target (direct mode)
     uint64_t* per_origin;    // [o_end - o_begin] or nullptr (direct mode, B == 1)
     int32_t* accum;          // accumulate mode: [B][NB][n_orig] int32 counters, else nullptr (direct mode)
+    unsigned long long* hist;  // SPLIT only, or nullptr: hist[c_Q] += 1 for every (origin, orthant) cell (the M_T
+                               // histogram of the analytic significance, ddks_significance.cuh)
 };
 
 // decode the two signed 16-bit halves of a counter word (value = lo + 65536 * hi, both in int16 range)
@@ -205,6 +207,7 @@ __device__ __forceinline__ uint64_t origin_num(const uint32_t* hist, int r, int 
             int32_t lo2, hi2;
             split16(hist[((NQ + q) * G::RP + rp) * G::T + t], lo2, hi2);
             const int64_t cQ = high ? hi2 : lo2;
+            if (a.hist) atomicAdd(&a.hist[cQ], 1ull);
             const int64_t df = (int64_t)v * a.nQ - cQ * a.nP;
             const uint64_t av = (uint64_t)(df < 0 ? -df : df);
             best = av > best ? av : best;
@@ -403,6 +406,7 @@ __global__ void k_finalize(const CountArgs a, int64_t B) {
             for (int q = 0; q < NQ; ++q) {
                 const int64_t cP = (int64_t)acc[(int64_t)q * n_orig];
                 const int64_t cQ = (int64_t)acc[(int64_t)(NQ + q) * n_orig];
+                if (a.hist) atomicAdd(&a.hist[cQ], 1ull);
                 const int64_t df = cP * a.nQ - cQ * a.nP;
                 const uint64_t av = (uint64_t)(df < 0 ? -df : df);
                 m = av > m ? av : m;

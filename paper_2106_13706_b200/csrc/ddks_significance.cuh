@@ -1,0 +1,218 @@
+// ddks_significance.cuh — analytic significance S of a ddKS statistic (§3).
+//
+//   M_T[i,k]  = # points of T (= Q) in orthant i about pooled test point k
+//   lambda    = (M_T[i,k] + 1) / (N_T + 2)                                              (Bayes estimator)
+//   p(n:m,l)  = C(m,n) l^n (1-l)^(m-n)        or the Poisson pmf e^{-ml}(ml)^n/n!
+//   p(d<=D)   = sum over the Delta band |n_P N_T - n_T N_P| <= num of p(n_P:N_P,l) p(n_T:N_T,l)
+//   S         = 1 - prod over the 2^d x N cells of p(d<=D)
+//
+// B200 design (DESIGN.md §7 "significance"):
+//   * the classify+count pass runs in SPLIT mode (c_P, c_Q kept apart) and its finaliser also histograms the
+//     M_T values: hist[m] = #cells with M_T = m. A cell's factor depends only on m, so the product becomes
+//     sum_m hist[m] * log p(d<=D | lambda_m): at most N_T + 1 table entries instead of 2^d N cells;
+//   * k_sig_table: one persistent CTA per table entry in flight. It evaluates the pmf of n_P over the window
+//     where it is within e^-100 of its mode (binary search on the unimodal log pmf), prefix- and suffix-scans it
+//     in global scratch, and sums the COMPLEMENT q = 1 - p(d<=D) = sum_{n_T} p(n_T) [F_P(lo-1) + (1 - F_P(hi))]
+//     (only tail sums of small positive terms: no cancellation). log p(d<=D) = log1p(-q) (R14);
+//   * log n! comes from a device table LF[n] = lgamma(n+1);
+//   * the sum over the table is a fixed-order block reduction (deterministic run to run).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ddks {
+
+__global__ void k_logfact(double* __restrict__ LF, int64_t n_max) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n_max; i += (int64_t)gridDim.x * blockDim.x)
+        LF[i] = lgamma((double)i + 1.0);
+}
+
+struct SigArgs {
+    const double* LF;                    // [lf_max + 1] log n!
+    int64_t lf_max;                      // >= max(N_P, N_T); Poisson: room for the pmf mass beyond N
+    const unsigned long long* hist;      // [N_T + 1] cells with M_T = m (all ranks' cells)
+    const unsigned long long* num;       // device: the global statistic numerator (after the all-reduce)
+    int64_t N_P, N_T;
+    int64_t m_begin, m_end;              // table entries this rank evaluates
+    int poisson;
+    double* scratch;                     // [gridDim.x][2][W_max]
+    int64_t W_max;
+    double* table;                       // [N_T + 1] log p(d <= D | lambda_m); 0 where hist[m] == 0
+    double* contrib;                     // [N_T + 1] hist[m] * table[m]
+    uint32_t* flag;                      // |= 4 if a window exceeded W_max (host retries with a larger W_max)
+};
+
+// log p(n : m, lambda) (binomial) or log Poisson(n ; m lambda)
+struct LogPmf {
+    const double* LF;
+    int64_t m;
+    double loglam, log1m, mu, logmu;
+    int poisson;
+    __device__ __forceinline__ void init(const double* LF_, int64_t m_, double lam, int poisson_) {
+        LF = LF_;
+        m = m_;
+        poisson = poisson_;
+        loglam = log(lam);
+        log1m = log1p(-lam);
+        mu = (double)m_ * lam;
+        logmu = log(mu);
+    }
+    __device__ __forceinline__ double operator()(int64_t n) const {
+        if (poisson) return -mu + (double)n * logmu - LF[n];
+        return LF[m] - LF[n] - LF[m - n] + (double)n * loglam + (double)(m - n) * log1m;
+    }
+    __device__ __forceinline__ int64_t mode(double lam) const {
+        int64_t k = poisson ? (int64_t)floor(mu) : (int64_t)floor((double)(m + 1) * lam);
+        return k < 0 ? 0 : (k > m ? m : k);
+    }
+    // largest n in [lo, hi] with f(n) >= thr, f non-increasing there (f(lo) >= thr)
+    __device__ int64_t last_above(int64_t lo, int64_t hi, double thr) const {
+        while (lo < hi) {
+            const int64_t mid = lo + (hi - lo + 1) / 2;
+            if ((*this)(mid) >= thr) lo = mid; else hi = mid - 1;
+        }
+        return lo;
+    }
+    // [a, b] = the n in 0..m with log pmf >= log pmf(mode) - 100 (the pmf is unimodal: two binary searches).
+    // Poisson only: [ta, tb] = the n > m (outside the Delta set's 0..m) above the same threshold, tb <= lf_max;
+    // ta > tb if there are none.
+    __device__ void window(double lam, int64_t lf_max, int64_t& a, int64_t& b, int64_t& ta, int64_t& tb) const {
+        const int64_t md = mode(lam);
+        const double thr = (*this)(md) - 100.0;
+        int64_t lo = 0, hi = md;  // smallest n in [0, md] with f(n) >= thr
+        while (lo < hi) {
+            const int64_t mid = lo + (hi - lo) / 2;
+            if ((*this)(mid) >= thr) hi = mid; else lo = mid + 1;
+        }
+        a = lo;
+        b = last_above(md, m, thr);
+        ta = m + 1;
+        tb = m;
+        if (poisson && m < lf_max && (*this)(m + 1) >= thr) tb = last_above(m + 1, lf_max, thr);
+    }
+};
+
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) s += red[w];  // same order in every thread
+    return s;
+}
+
+// In-place inclusive scan of x[0..W) (REV: from the right, x[i] = sum_{j >= i}). Fixed order: each thread owns a
+// contiguous run, runs are combined by an exclusive scan of the run totals.
+template <int NT, bool REV>
+__device__ void block_scan(double* x, int64_t W, double* red) {
+    const int64_t C = (W + NT - 1) / NT;
+    const int64_t b = threadIdx.x * C, e = b + C < W ? b + C : W;
+    double s = 0.0;
+    for (int64_t i = b; i < e; ++i) s += x[REV ? W - 1 - i : i];
+    __syncthreads();
+    red[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double run = 0.0;
+        for (int t = 0; t < NT; ++t) {
+            const double v = red[t];
+            red[t] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    double run = red[threadIdx.x];
+    for (int64_t i = b; i < e; ++i) {
+        const int64_t j = REV ? W - 1 - i : i;
+        run += x[j];
+        x[j] = run;
+    }
+    __syncthreads();
+}
+
+constexpr int SIG_T = 512;
+
+__global__ void __launch_bounds__(SIG_T) k_sig_table(const SigArgs a) {
+    __shared__ double red[SIG_T];
+    __shared__ int64_t win[8];
+    double* A = a.scratch + (int64_t)blockIdx.x * 2 * a.W_max;  // inclusive prefix sums of p(n_P)
+    double* B = A + a.W_max;                                     // inclusive suffix sums of p(n_P)
+    const int64_t num = (int64_t)*a.num;
+    for (int64_t m = a.m_begin + blockIdx.x; m < a.m_end; m += gridDim.x) {
+        const unsigned long long h = a.hist[m];
+        if (h == 0) {
+            if (threadIdx.x == 0) a.table[m] = 0.0, a.contrib[m] = 0.0;
+            continue;
+        }
+        const double lam = ((double)m + 1.0) / ((double)a.N_T + 2.0);
+        LogPmf fP, fT;
+        fP.init(a.LF, a.N_P, lam, a.poisson);
+        fT.init(a.LF, a.N_T, lam, a.poisson);
+        if (threadIdx.x == 0) fP.window(lam, a.lf_max, win[0], win[1], win[4], win[5]);
+        if (threadIdx.x == 32) fT.window(lam, a.lf_max, win[2], win[3], win[6], win[7]);
+        __syncthreads();
+        const int64_t aP = win[0], bP = win[1], aT = win[2], bT = win[3];
+        int64_t W = bP - aP + 1;
+        if (W > a.W_max || (a.poisson && (win[5] == a.lf_max || win[7] == a.lf_max))) {
+            if (threadIdx.x == 0) atomicOr(a.flag, 4u);
+            W = W > a.W_max ? a.W_max : W;
+        }
+        // Poisson: the pmf restricted to the Delta set's 0..N has mass Z = 1 - t < 1, so the band sum p(d<=D)
+        // (P:L255-268 with the Poisson pmf, R12) is Z_P Z_T - (mass outside the band), and
+        // 1 - p = t_P + t_T - t_P t_T + (mass outside the band); t = the Poisson mass beyond N, summed directly
+        double tP = 0.0, tT = 0.0;
+        if (a.poisson) {
+            double sP = 0.0, sT = 0.0;
+            for (int64_t n = win[4] + threadIdx.x; n <= win[5]; n += SIG_T) sP += exp(fP(n));
+            for (int64_t n = win[6] + threadIdx.x; n <= win[7]; n += SIG_T) sT += exp(fT(n));
+            tP = block_sum<SIG_T>(sP, red);
+            tT = block_sum<SIG_T>(sT, red);
+        }
+        for (int64_t i = threadIdx.x; i < W; i += SIG_T) {
+            const double v = exp(fP(aP + i));
+            A[i] = v;
+            B[i] = v;
+        }
+        __syncthreads();
+        block_scan<SIG_T, false>(A, W, red);
+        block_scan<SIG_T, true>(B, W, red);
+        const int64_t eP = aP + W - 1;  // last n_P inside the window
+        double acc = 0.0;
+        for (int64_t nT = aT + threadIdx.x; nT <= bT; nT += SIG_T) {
+            // band of n_P with |n_P N_T - nT N_P| <= num: [lo, hi], exact int64
+            const int64_t x = nT * a.N_P - num;
+            const int64_t lo = x >= 0 ? (x + a.N_T - 1) / a.N_T : -((-x) / a.N_T);
+            const int64_t hi = (nT * a.N_P + num) / a.N_T;
+            const double left = lo <= aP ? 0.0 : A[(lo > eP + 1 ? eP + 1 : lo) - 1 - aP];   // sum_{n_P < lo}
+            const double right = hi >= eP ? 0.0 : B[(hi < aP - 1 ? aP - 1 : hi) + 1 - aP];  // sum_{n_P > hi}
+            const double tail = left + right;
+            if (tail != 0.0) acc += exp(fT(nT)) * tail;
+        }
+        const double q = block_sum<SIG_T>(acc, red) + (tP + tT - tP * tT);
+        if (threadIdx.x == 0) {
+            const double lp = log1p(-q);
+            a.table[m] = lp;
+            a.contrib[m] = (double)h * lp;
+        }
+        __syncthreads();  // scratch and win reused by the next entry
+    }
+}
+
+// Fixed-order sum of contrib[b..e) -> *out (one CTA).
+__global__ void __launch_bounds__(SIG_T) k_sig_sum(const double* __restrict__ contrib, int64_t b, int64_t e,
+                                                   double* out) {
+    __shared__ double red[SIG_T];
+    const int64_t n = e - b;
+    const int64_t C = (n + SIG_T - 1) / SIG_T;
+    const int64_t lo = b + threadIdx.x * C, hi = lo + C < e ? lo + C : e;
+    double s = 0.0;
+    for (int64_t i = lo; i < hi; ++i) s += contrib[i];
+    s = block_sum<SIG_T>(s, red);
+    if (threadIdx.x == 0) *out = s;
+}
+
+}  // namespace ddks

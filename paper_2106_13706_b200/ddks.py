@@ -25,6 +25,7 @@ DDKS_FLAG_TIES_GT = 2
 DDKS_FLAG_FORCE_DIRECT = 4
 DDKS_FLAG_PROFILE = 8
 DDKS_FLAG_PERM_GATHER = 16
+DDKS_SIG_POISSON = 1
 
 
 class DDKSError(RuntimeError):
@@ -36,6 +37,19 @@ class DDKSError(RuntimeError):
 class ddks_result(ctypes.Structure):
     _fields_ = [("num", ctypes.c_uint64), ("den", ctypes.c_uint64), ("D", ctypes.c_double),
                 ("argmax_origin", ctypes.c_int64)]
+
+
+class ddks_significance_result(ctypes.Structure):
+    _fields_ = [("stat", ddks_result), ("S", ctypes.c_double), ("log_prod", ctypes.c_double), ("cells", ctypes.c_int64)]
+
+
+class Significance(NamedTuple):
+    stat: "Result"
+    S: float
+    log_prod: float
+    cells: int
+    mt_hist: np.ndarray | None
+    log_p_table: np.ndarray | None
 
 
 class Result(NamedTuple):
@@ -59,6 +73,8 @@ def _load() -> ctypes.CDLL:
         "ddks_permutation_null": ([vp, vp, i64, i64, i32, vp, i64, vp, vp, ctypes.POINTER(ddks_result),
                                    ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
         "ddks_stat_per_origin": ([vp, vp, i64, vp, i64, i32, i64, i64, vp, vp], ctypes.c_int),
+        "ddks_significance": ([vp, vp, i64, vp, i64, i32, u32, vp, ctypes.POINTER(ddks_significance_result), vp, vp],
+                              ctypes.c_int),
         "ddks_shard_range": ([i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)], ctypes.c_int),
         "ddks_launch_count": ([vp], i64),
         "ddks_profile_read": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_uint64)],
@@ -76,7 +92,7 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 EXPORTED = ("ddks_get_nccl_id", "ddks_create", "ddks_stat", "ddks_stat_batch", "ddks_permutation_null",
-            "ddks_stat_per_origin", "ddks_shard_range", "ddks_launch_count", "ddks_profile_read", "ddks_destroy",
+            "ddks_stat_per_origin", "ddks_significance", "ddks_shard_range", "ddks_launch_count", "ddks_profile_read", "ddks_destroy",
             "ddks_last_error", "ddks_version")
 
 
@@ -195,6 +211,21 @@ def ddks_stat_per_origin(ctx, P, Q, o_begin: int, o_end: int, stream=None) -> np
     return out
 
 
+def ddks_significance(ctx, P, Q, poisson: bool = False, detail: bool = False, stream=None) -> Significance:
+    """Analytic significance (§3). detail=True also returns mt_hist [n_Q+1] and log_p_table [n_Q+1]."""
+    p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
+    if len(p.shape) != 2 or len(q.shape) != 2 or p.shape[1] != q.shape[1]:
+        raise ValueError(f"P {p.shape} and Q {q.shape} must be [n, d] with the same d")
+    r = ddks_significance_result()
+    hist = np.zeros(q.shape[0] + 1, dtype=np.uint64) if detail else None
+    table = np.zeros(q.shape[0] + 1, dtype=np.float64) if detail else None
+    _check(LIB.ddks_significance(ctx, p.ptr, p.shape[0], q.ptr, q.shape[0], p.shape[1],
+                                 DDKS_SIG_POISSON if poisson else 0, _stream(stream), ctypes.byref(r),
+                                 hist.ctypes.data if detail else None, table.ctypes.data if detail else None), ctx)
+    st = r.stat
+    return Significance(Result(st.num, st.den, st.D, st.argmax_origin), r.S, r.log_prod, r.cells, hist, table)
+
+
 def ddks_launch_count(ctx) -> int:
     return int(LIB.ddks_launch_count(ctx))
 
@@ -224,6 +255,9 @@ class Context:
 
     def stat_per_origin(self, P, Q, o_begin, o_end, stream=None):
         return ddks_stat_per_origin(self.ctx, P, Q, o_begin, o_end, stream)
+
+    def significance(self, P, Q, poisson=False, detail=False, stream=None) -> Significance:
+        return ddks_significance(self.ctx, P, Q, poisson, detail, stream)
 
     def profile_read(self):
         return ddks_profile_read(self.ctx)
