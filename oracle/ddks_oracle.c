@@ -243,3 +243,165 @@ int oracle_significance(const float* P, int64_t n_P, const float* Q, int64_t n_Q
     *num_out = num;
     return 0;
 }
+
+/* ===================================================================================================================
+ * Approximations of §2.2.2-2.2.3 (SURVEY.md §8f NEXT-3 vdKS, NEXT-4 rdKS). TEST INFRASTRUCTURE ONLY, like the above.
+ * Both start with NormalizeData ("shifted and rescaled to be between 0 and 1"): per dimension m, over the
+ * pooled points, x' = (x - min_m) / (max_m - min_m) in double; a constant dimension maps to 0.5 (R15).
+ * ===================================================================================================================*/
+void oracle_normalize_pair(const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d, double* out /* [N][d] */)
+{
+    int64_t N = n_P + n_Q;
+    for (int m = 0; m < d; ++m) {
+        double mn = (double)pooled_row(P, n_P, Q, d, 0)[m], mx = mn;
+        for (int64_t i = 1; i < N; ++i) {
+            double x = (double)pooled_row(P, n_P, Q, d, i)[m];
+            if (x < mn) mn = x;
+            if (x > mx) mx = x;
+        }
+        for (int64_t i = 0; i < N; ++i) {
+            double x = (double)pooled_row(P, n_P, Q, d, i)[m];
+            out[i * d + m] = (mx > mn) ? (x - mn) / (mx - mn) : 0.5;
+        }
+    }
+}
+
+/* Alg. 1 IndexFromPoint (SPEC S:L190-197 voxel_index): cell c_m = min(floor(x'_m k), k - 1), flat = sum c_m k^m. */
+int64_t oracle_voxel_index(const double* xn, int d, int64_t k)
+{
+    int64_t flat = 0, stride = 1;
+    for (int m = 0; m < d; ++m) {
+        int64_t c = (int64_t)floor(xn[m] * (double)k);
+        if (c > k - 1) c = k - 1;
+        if (c < 0) c = 0;
+        flat += c * stride;
+        stride *= k;
+    }
+    return flat;
+}
+
+/* vdKS, Alg. 1 step by step:
+ *   VoxelList[id][index] += 1 for every point (id 0 = P, 1 = T = Q), FilledVoxels = indices with a point;
+ *   Diff = VoxelList[1]/n_T - VoxelList[0]/n_P, kept exact as the integer diff[v] = cQ[v] n_P - cP[v] n_Q
+ *   (= n_P n_Q x Diff; R16);
+ *   for every filled voxel v: SumOrthants(Diff at v) = for every voxel u, orthant bit m = [u_m >= v_m] (the voxel
+ *   itself in the all->= orthant, as Eq. 3 puts the origin; R16), sums[code] += diff[u]; TmpD = max_code |sums|;
+ *   D = max over filled voxels. num = max |sum|, den = n_P n_Q, D = num / den. Returns 0 on success. */
+int oracle_vdks(const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d, int64_t k,
+                uint64_t* num, uint64_t* den, double* D)
+{
+    if (d < 1 || d > 20 || n_P < 1 || n_Q < 1 || k < 1) return 1;
+    int64_t N = n_P + n_Q, V = 1;
+    for (int m = 0; m < d; ++m) { V *= k; if (V > ((int64_t)1 << 28)) return 2; }
+    double* xn = (double*)malloc(sizeof(double) * (size_t)(N * d));
+    int64_t* cP = (int64_t*)calloc((size_t)V, sizeof(int64_t));
+    int64_t* cQ = (int64_t*)calloc((size_t)V, sizeof(int64_t));
+    int64_t* diff = (int64_t*)calloc((size_t)V, sizeof(int64_t));
+    int64_t nq = (int64_t)1 << d;
+    oracle_normalize_pair(P, n_P, Q, n_Q, d, xn);
+    for (int64_t i = 0; i < N; ++i) {
+        int64_t v = oracle_voxel_index(xn + i * d, d, k);
+        if (i < n_P) cP[v] += 1; else cQ[v] += 1;
+    }
+    for (int64_t v = 0; v < V; ++v) diff[v] = cQ[v] * n_P - cP[v] * n_Q;
+    uint64_t best = 0;
+#pragma omp parallel
+    {
+        int64_t* sums = (int64_t*)malloc(sizeof(int64_t) * (size_t)nq);
+        int64_t* vc = (int64_t*)malloc(sizeof(int64_t) * (size_t)d);
+        int64_t* uc = (int64_t*)malloc(sizeof(int64_t) * (size_t)d);
+#pragma omp for schedule(dynamic, 8) reduction(max : best)
+        for (int64_t v = 0; v < V; ++v) {
+            if (cP[v] + cQ[v] == 0) continue;  /* not a filled voxel */
+            for (int64_t q = 0; q < nq; ++q) sums[q] = 0;
+            int64_t r = v;
+            for (int m = 0; m < d; ++m) { vc[m] = r % k; r /= k; }
+            for (int64_t u = 0; u < V; ++u) {
+                int64_t s = u;
+                int code = 0;
+                for (int m = 0; m < d; ++m) { uc[m] = s % k; s /= k; code += (uc[m] >= vc[m]) << m; }
+                sums[code] += diff[u];
+            }
+            for (int64_t q = 0; q < nq; ++q) {
+                uint64_t a = (uint64_t)(sums[q] < 0 ? -sums[q] : sums[q]);
+                if (a > best) best = a;
+            }
+        }
+        free(sums); free(vc); free(uc);
+    }
+    free(xn); free(cP); free(cQ); free(diff);
+    *num = best;
+    *den = (uint64_t)n_P * (uint64_t)n_Q;
+    *D = (double)best / (double)(*den);
+    return 0;
+}
+
+/* Alg. 2 GetDFromCornerLists on two ascending lists, as a two-pointer merge that evaluates
+ * |numC1 len(C2) - numC2 len(C1)| only once both pointers have consumed every value <= the current one (DESIGN.md
+ * R17: the printed loop compares C2[0] < C1[0] and cannot advance correctly; absolute value for symmetry).
+ * Returns the integer numerator; the statistic is num / (len(C1) len(C2)). */
+uint64_t oracle_merged_max_diff(const double* c1, int64_t n1, const double* c2, int64_t n2)
+{
+    int64_t i = 0, j = 0;
+    uint64_t best = 0;
+    while (i < n1 || j < n2) {
+        double v;
+        if (i < n1 && (j >= n2 || c1[i] <= c2[j])) v = c1[i]; else v = c2[j];
+        while (i < n1 && c1[i] <= v) ++i;
+        while (j < n2 && c2[j] <= v) ++j;
+        int64_t t = i * n2 - j * n1;
+        uint64_t a = (uint64_t)(t < 0 ? -t : t);
+        if (a > best) best = a;
+    }
+    return best;
+}
+
+static int cmp_double(const void* a, const void* b)
+{
+    double x = *(const double*)a, y = *(const double*)b;
+    return (x > y) - (x < y);
+}
+
+/* rdKS, Alg. 2 step by step: C = IdentifyCorners = the origin of the normalised space and the d unit
+ * axis corners ("(0,0,0), (1,0,0), (0,1,0), (0,0,1)"); for each corner c: Euclidean distances
+ * sqrt(sum_m (x'_m - c_m)^2) (summed m = 0..d-1) of P's and T's points, each list sorted, then
+ * GetDFromCornerLists; D = max over corners. num/den as above; *arg_corner = first corner attaining num. */
+int oracle_rdks(const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d,
+                uint64_t* num, uint64_t* den, double* D, int64_t* arg_corner)
+{
+    if (d < 1 || n_P < 1 || n_Q < 1) return 1;
+    int64_t N = n_P + n_Q;
+    double* xn = (double*)malloc(sizeof(double) * (size_t)(N * d));
+    oracle_normalize_pair(P, n_P, Q, n_Q, d, xn);
+    uint64_t best = 0;
+    int64_t arg = 0;
+#pragma omp parallel
+    {
+        double* dP = (double*)malloc(sizeof(double) * (size_t)n_P);
+        double* dQ = (double*)malloc(sizeof(double) * (size_t)n_Q);
+        double* c = (double*)malloc(sizeof(double) * (size_t)d);
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t ci = 0; ci <= d; ++ci) {
+            for (int m = 0; m < d; ++m) c[m] = (ci >= 1 && m == ci - 1) ? 1.0 : 0.0;
+            for (int64_t i = 0; i < N; ++i) {
+                double s = 0.0;
+                for (int m = 0; m < d; ++m) { double t = xn[i * d + m] - c[m]; s += t * t; }
+                if (i < n_P) dP[i] = sqrt(s); else dQ[i - n_P] = sqrt(s);
+            }
+            qsort(dP, (size_t)n_P, sizeof(double), cmp_double);
+            qsort(dQ, (size_t)n_Q, sizeof(double), cmp_double);
+            uint64_t t = oracle_merged_max_diff(dP, n_P, dQ, n_Q);
+#pragma omp critical
+            {
+                if (t > best || (t == best && ci < arg)) { best = t; arg = ci; }
+            }
+        }
+        free(dP); free(dQ); free(c);
+    }
+    free(xn);
+    *num = best;
+    *den = (uint64_t)n_P * (uint64_t)n_Q;
+    *D = (double)best / (double)(*den);
+    *arg_corner = arg;
+    return 0;
+}

@@ -17,6 +17,8 @@ Two independent implementations live here:
 Also the analytic significance of §3 (``log_pmf``, ``p_le``, ``significance``), written literally:
 every cell's full double sum over the Delta-set band, the product as a sum of logs.
 
+And the two approximations of §2.2.2-2.2.3 (``vdks``, Alg. 1; ``rdks``, Alg. 2), each step in the paper's order.
+
 Plus ``ks_1d``: the classical two-sample KS statistic by a sort-merge sweep over the pooled values with
 exact integers (the d=1 closed form) — used to pin the oracle, not by the oracle.
 
@@ -45,7 +47,7 @@ def build(force: bool = False) -> str:
     os.makedirs(_BUILD, exist_ok=True)
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
         tmp = _SO + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11", "-Wall", "-Wextra",
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared", "-std=c11", "-Wall", "-Wextra",
                                "-o", tmp, _SRC])
         os.replace(tmp, _SO)
     return _SO
@@ -74,6 +76,16 @@ def _load():
         lib.oracle_p_le.restype = ctypes.c_double
         lib.oracle_significance.argtypes = [c_p, c_i64, c_p, c_i64, c_int, c_int, c_int, c_int, c_p, c_p, c_p]
         lib.oracle_significance.restype = c_int
+        lib.oracle_normalize_pair.argtypes = [c_p, c_i64, c_p, c_i64, c_int, c_p]
+        lib.oracle_normalize_pair.restype = None
+        lib.oracle_voxel_index.argtypes = [c_p, c_int, c_i64]
+        lib.oracle_voxel_index.restype = c_i64
+        lib.oracle_vdks.argtypes = [c_p, c_i64, c_p, c_i64, c_int, c_i64, c_p, c_p, c_p]
+        lib.oracle_vdks.restype = c_int
+        lib.oracle_merged_max_diff.argtypes = [c_p, c_i64, c_p, c_i64]
+        lib.oracle_merged_max_diff.restype = ctypes.c_uint64
+        lib.oracle_rdks.argtypes = [c_p, c_i64, c_p, c_i64, c_int, c_p, c_p, c_p, c_p]
+        lib.oracle_rdks.restype = c_int
         _lib = lib
     return _lib
 
@@ -175,6 +187,49 @@ def significance(P, Q, ties_gt: bool = False, poisson: bool = False, threads: in
     if rc:
         raise ValueError(f"oracle_significance rc={rc}")
     return float(S.value), float(lp.value), int(num.value)
+
+
+def normalize_pair(P, Q) -> np.ndarray:
+    """Alg. 1/2 NormalizeData: pooled per-dimension (x - min)/(max - min) in double -> [N, d]."""
+    P, Q = _f32(P), _f32(Q)
+    out = np.zeros((P.shape[0] + Q.shape[0], P.shape[1]), dtype=np.float64)
+    _load().oracle_normalize_pair(_ptr(P), P.shape[0], _ptr(Q), Q.shape[0], P.shape[1], _ptr(out))
+    return out
+
+
+def voxel_index(xn, k: int) -> int:
+    """Alg. 1 IndexFromPoint on a normalised point: sum_m min(floor(x'_m k), k-1) k^m."""
+    x = np.ascontiguousarray(np.asarray(xn, dtype=np.float64).ravel())
+    return int(_load().oracle_voxel_index(_ptr(x), x.size, k))
+
+
+def vdks(P, Q, k: int):
+    """vdKS, Alg. 1 -> (num, den, D) with D = num / den exactly as in ddks()."""
+    P, Q = _f32(P), _f32(Q)
+    num, den, D = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_double()
+    rc = _load().oracle_vdks(_ptr(P), P.shape[0], _ptr(Q), Q.shape[0], P.shape[1], k, ctypes.byref(num),
+                             ctypes.byref(den), ctypes.byref(D))
+    if rc:
+        raise ValueError(f"oracle_vdks rc={rc}")
+    return int(num.value), int(den.value), float(D.value)
+
+
+def merged_max_diff(c1, c2) -> int:
+    """Alg. 2 GetDFromCornerLists on two ascending lists -> integer numerator over len(c1) len(c2)."""
+    a = np.ascontiguousarray(np.asarray(c1, dtype=np.float64))
+    b = np.ascontiguousarray(np.asarray(c2, dtype=np.float64))
+    return int(_load().oracle_merged_max_diff(_ptr(a), a.size, _ptr(b), b.size))
+
+
+def rdks(P, Q):
+    """rdKS, Alg. 2 (P:L158-202) -> (num, den, D, arg_corner)."""
+    P, Q = _f32(P), _f32(Q)
+    num, den, D, arg = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_double(), ctypes.c_int64()
+    rc = _load().oracle_rdks(_ptr(P), P.shape[0], _ptr(Q), Q.shape[0], P.shape[1], ctypes.byref(num),
+                             ctypes.byref(den), ctypes.byref(D), ctypes.byref(arg))
+    if rc:
+        raise ValueError(f"oracle_rdks rc={rc}")
+    return int(num.value), int(den.value), float(D.value), int(arg.value)
 
 
 # ---------------------------------------------------------------------------------------------------

@@ -358,3 +358,112 @@ def test_significance_statistic_pins():
     S_b, _, _ = O.significance(P, Q)
     S_p, _, _ = O.significance(P, Q, poisson=True)
     assert 0.0 <= S_b <= 1.0 and 0.0 <= S_p <= 1.0
+
+
+# ------------------------------------------------------------------------------------ vdKS (Alg. 1) and rdKS (Alg. 2)
+
+def _grid_pair(seed, n_P, n_Q, d, k):
+    """Integer-grid samples whose every coordinate takes values 0..k-1 with both ends present in every dimension
+    (so NormalizeData maps value v to v/(k-1) and Alg. 1's floor(x' k), clamped, is cell v)."""
+    rng = np.random.default_rng(seed)
+    P = rng.integers(0, k, (n_P, d)).astype(np.float32)
+    Q = rng.integers(0, k, (n_Q, d)).astype(np.float32)
+    P[0, :], Q[0, :] = 0, k - 1
+    return P, Q
+
+
+def test_spec_voxel_and_sweep_examples(golden_dir):
+    g = json.load(open(os.path.join(golden_dir, "spec_examples.json")))
+    for c in g["voxel_index"]:
+        assert O.voxel_index(c["point"], c["k"]) == c["expect"], c["cite"]
+    for c in g["vdks"]:
+        num, den, D = O.vdks(np.array(c["P"], np.float32), np.array(c["Q"], np.float32), c["k"])
+        assert Fraction(num, den) == Fraction(c["D_num"], c["D_den"]), c["cite"]
+    for c in g["merged_max_diff"]:
+        num = O.merged_max_diff(c["a"], c["b"])
+        assert Fraction(num, len(c["a"]) * len(c["b"])) == Fraction(c["D_num"], c["D_den"]), c["cite"]
+    for c in g["normalize"]:
+        got = O.normalize_pair(np.array(c["P"], np.float32), np.array(c["Q"], np.float32))
+        assert got.tolist() == c["expect"], c["cite"]
+
+
+def test_vdks_is_exact_ddks_on_cells():
+    # Alg. 1's orthant sums about a filled voxel's lower corner (the voxel itself in the all->= orthant) are the
+    # exact ddKS orthant counts of the cell-index points; the filled voxels are the distinct origins. On an
+    # integer grid 0..k-1 whose ends are present, cell = value, so vdKS(k) == exact ddKS (an independent oracle).
+    for seed, (n_P, n_Q, d, k) in enumerate([(30, 20, 1, 5), (40, 33, 2, 4), (25, 31, 3, 3), (60, 50, 3, 6),
+                                              (20, 24, 4, 3), (12, 15, 5, 2)]):
+        P, Q = _grid_pair(seed, n_P, n_Q, d, k)
+        assert O.vdks(P, Q, k)[:2] == O.ddks(P, Q)[:2], (n_P, n_Q, d, k)
+        # the same holds after strictly increasing affine maps per coordinate (NormalizeData removes them)
+        A = P * np.float32(4.0) - np.float32(3.0)
+        B = Q * np.float32(4.0) - np.float32(3.0)
+        assert O.vdks(A, B, k)[:2] == O.ddks(P, Q)[:2]
+
+
+def test_vdks_properties():
+    P, Q = I.random_pair(51, 90, 70, 3, "normal")
+    assert O.vdks(P, Q, 1)[0] == 0                                  # one voxel: all orthant sums are 0 or total 0
+    assert O.vdks(P, P.copy(), 7)[0] == 0                           # identity
+    for k in (2, 5, 9):
+        a, b = O.vdks(P, Q, k), O.vdks(Q, P, k)
+        assert a[0] == b[0] and 0 <= a[0] <= a[1]                   # symmetry (|.|, R16), range
+    # invariance under per-coordinate scaling by powers of two (exact in float32)
+    s = np.array([2.0, 0.5, 8.0], np.float32)
+    assert O.vdks(P * s, Q * s, 6) == O.vdks(P, Q, 6)
+    # brute force on tiny inputs: the definition of SumOrthants as a Fraction over the cell points
+    for seed in range(40):
+        P, Q = _grid_pair(100 + seed, 3 + seed % 4, 2 + seed % 5, 1 + seed % 3, 2 + seed % 3)
+        num, den, _ = O.vdks(P, Q, 2 + seed % 3)
+        assert Fraction(num, den) == O.brute_force(P, Q)
+
+
+def _normalised_dyadic(seed, n_P, n_Q, d):
+    """Points on the grid {0, 1/4, ..., 1} with 0 and 1 present per dimension: NormalizeData is the identity and
+    every squared distance to a corner is an exact dyadic sum (so any evaluation order gives the same doubles)."""
+    rng = np.random.default_rng(seed)
+    P = (rng.integers(0, 5, (n_P, d)) / 4).astype(np.float32)
+    Q = (rng.integers(0, 5, (n_Q, d)) / 4).astype(np.float32)
+    P[0, :], Q[0, :] = 0, 1
+    return P, Q
+
+
+def _rdks_brute(P, Q):
+    """Definition: max over corners c and radii r of |#P(|x-c| <= r)/n_P - #Q(|x-c| <= r)/n_Q| (Fractions)."""
+    d = P.shape[1]
+    best = Fraction(0)
+    for ci in range(d + 1):
+        c = np.zeros(d)
+        if ci:
+            c[ci - 1] = 1.0
+        dp = [math.sqrt(sum((float(x) - cc) ** 2 for x, cc in zip(row, c))) for row in P.astype(np.float64)]
+        dq = [math.sqrt(sum((float(x) - cc) ** 2 for x, cc in zip(row, c))) for row in Q.astype(np.float64)]
+        for r in dp + dq:
+            v = abs(Fraction(sum(x <= r for x in dp), len(dp)) - Fraction(sum(x <= r for x in dq), len(dq)))
+            best = max(best, v)
+    return best
+
+
+def test_rdks_pins():
+    # d = 1: corner 0's distances are x' itself (sqrt(x'^2) == |x'| in IEEE arithmetic), so rdKS = the classical
+    # two-sample KS (corner 1 can only merge values, never exceed it) — against the independently pinned ks_1d
+    for seed in range(30):
+        rng = np.random.default_rng(200 + seed)
+        u = rng.standard_normal(40 + seed).astype(np.float32)
+        v = (rng.standard_normal(35) + 0.3 * (seed % 3)).astype(np.float32)
+        if seed % 2:
+            u, v = np.round(u * 2).astype(np.float32), np.round(v * 2).astype(np.float32)
+        num, den, _, _ = O.rdks(u[:, None], v[:, None])
+        assert Fraction(num, den) == Fraction(*O.ks_1d(u, v)), seed
+    # brute force on exact dyadic distances
+    for seed in range(25):
+        P, Q = _normalised_dyadic(300 + seed, 3 + seed % 6, 2 + seed % 5, 1 + seed % 4)
+        num, den, _, _ = O.rdks(P, Q)
+        assert Fraction(num, den) == _rdks_brute(P, Q), seed
+    # identity, symmetry, range, invariance under per-coordinate scaling by powers of two
+    P, Q = I.random_pair(61, 120, 90, 4, "normal")
+    assert O.rdks(P, P.copy())[0] == 0
+    a, b = O.rdks(P, Q), O.rdks(Q, P)
+    assert a[0] == b[0] and 0 <= a[0] <= a[1]
+    s = np.array([2.0, 0.25, 4.0, 1.0], np.float32)
+    assert O.rdks(P * s, Q * s)[:2] == a[:2]
