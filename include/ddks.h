@@ -136,6 +136,17 @@ DDKS_API ddks_status ddks_significance(ddks_ctx* ctx, const float* P, int64_t n_
                               uint32_t sig_flags, void* stream, ddks_significance_result* out, uint64_t* mt_hist,
                               double* log_p_table);
 
+/* ---- vdKS: voxel approximation (§2.2.2, Alg. 1) -------------------
+ * NormalizeData: per dimension over the pooled points, x' = (x - min)/(max - min) in double (a constant dimension
+ * maps to 0.5; R15); IndexFromPoint: cell c_m = min(floor(x'_m k), k-1), k voxels per dimension;
+ * Diff = VoxelList[Q]/n_Q - VoxelList[P]/n_P; for every filled voxel, the 2^d orthant sums of Diff split at the
+ * voxel's lower corner (the voxel itself in the all->= orthant, as Eq. 3 places the origin; R16);
+ * out->num = max over filled voxels and orthants of |sum| x n_P n_Q (exact integer), out->den = n_P n_Q,
+ * out->D = num / den; out->argmax_origin = -1. k >= 1 and k^d <= 2^30 (else DDKS_ERR_TOO_LARGE).
+ * Multi-GPU: points sharded for the voxel histogram (all-reduce sum), voxels sharded for the orthant sums. */
+DDKS_API ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
+                               int64_t k, void* stream, ddks_result* out);
+
 /* Host-only helper (no GPU needed): the contiguous origin / item range [*begin, *end) that `rank` of `world`
  * owns out of `total` units. Ranges are balanced to within one unit and cover 0..total exactly. */
 DDKS_API ddks_status ddks_shard_range(int64_t total, int world, int rank, int64_t* begin, int64_t* end);

@@ -75,6 +75,7 @@ def _load() -> ctypes.CDLL:
         "ddks_stat_per_origin": ([vp, vp, i64, vp, i64, i32, i64, i64, vp, vp], ctypes.c_int),
         "ddks_significance": ([vp, vp, i64, vp, i64, i32, u32, vp, ctypes.POINTER(ddks_significance_result), vp, vp],
                               ctypes.c_int),
+        "ddks_vdks": ([vp, vp, i64, vp, i64, i32, i64, vp, ctypes.POINTER(ddks_result)], ctypes.c_int),
         "ddks_shard_range": ([i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)], ctypes.c_int),
         "ddks_launch_count": ([vp], i64),
         "ddks_profile_read": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_uint64)],
@@ -92,7 +93,7 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 EXPORTED = ("ddks_get_nccl_id", "ddks_create", "ddks_stat", "ddks_stat_batch", "ddks_permutation_null",
-            "ddks_stat_per_origin", "ddks_significance", "ddks_shard_range", "ddks_launch_count", "ddks_profile_read", "ddks_destroy",
+            "ddks_stat_per_origin", "ddks_significance", "ddks_vdks", "ddks_shard_range", "ddks_launch_count", "ddks_profile_read", "ddks_destroy",
             "ddks_last_error", "ddks_version")
 
 
@@ -226,6 +227,17 @@ def ddks_significance(ctx, P, Q, poisson: bool = False, detail: bool = False, st
     return Significance(Result(st.num, st.den, st.D, st.argmax_origin), r.S, r.log_prod, r.cells, hist, table)
 
 
+def ddks_vdks(ctx, P, Q, k: int, stream=None) -> Result:
+    """vdKS (Alg. 1) with k voxels per dimension."""
+    p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
+    if len(p.shape) != 2 or len(q.shape) != 2 or p.shape[1] != q.shape[1]:
+        raise ValueError(f"P {p.shape} and Q {q.shape} must be [n, d] with the same d")
+    r = ddks_result()
+    _check(LIB.ddks_vdks(ctx, p.ptr, p.shape[0], q.ptr, q.shape[0], p.shape[1], k, _stream(stream), ctypes.byref(r)),
+           ctx)
+    return Result(r.num, r.den, r.D, r.argmax_origin)
+
+
 def ddks_launch_count(ctx) -> int:
     return int(LIB.ddks_launch_count(ctx))
 
@@ -258,6 +270,9 @@ class Context:
 
     def significance(self, P, Q, poisson=False, detail=False, stream=None) -> Significance:
         return ddks_significance(self.ctx, P, Q, poisson, detail, stream)
+
+    def vdks(self, P, Q, k: int, stream=None) -> Result:
+        return ddks_vdks(self.ctx, P, Q, k, stream)
 
     def profile_read(self):
         return ddks_profile_read(self.ctx)

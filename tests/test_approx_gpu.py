@@ -1,0 +1,80 @@
+"""GPU parity of the two approximations of §2.2.2-2.2.3 against the oracle: vdKS (Alg. 1, voxels) and rdKS
+(Alg. 2, radial corners). Both reduce to exact integers (num over den = n_P n_Q) once the f64 voxel / distance
+decisions are taken in the same precision on both sides (R15-R17), so the bar is bit-exact."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import oracle as O  # noqa: E402
+from paper_2106_13706_b200 import ddks as K  # noqa: E402
+from paper_2106_13706_b200 import inputs as I  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = K.Context()
+    yield c
+    c.close()
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+VDKS_CASES = [(300, 200, 1, 17), (1000, 900, 2, 40), (2500, 2100, 3, 12), (777, 1234, 3, 1), (1500, 1500, 4, 7),
+              (900, 1100, 5, 5), (600, 500, 6, 3), (400, 450, 7, 3), (300, 320, 8, 2), (513, 257, 3, 64)]
+
+
+@pytest.mark.parametrize("n_P,n_Q,d,k", VDKS_CASES)
+@pytest.mark.parametrize("kind", ["normal", "mixed", "dup"])
+def test_vdks_parity(ctx, n_P, n_Q, d, k, kind):
+    P, Q = I.random_pair(4000 + n_P + d * 10 + k, n_P, n_Q, d, kind)
+    want = O.vdks(P, Q, k)
+    got = ctx.vdks(dev(P), dev(Q), k)
+    assert (got.num, got.den) == want[:2] and got.D == want[2], (got, want)
+
+
+def test_vdks_grid_and_edges(ctx):
+    # integer grids: every point on a voxel boundary; k = #values makes vdKS the exact ddKS (oracle pin)
+    rng = np.random.default_rng(8)
+    for d, k in [(2, 4), (3, 5), (4, 3)]:
+        P = rng.integers(0, k, (700, d)).astype(np.float32)
+        Q = rng.integers(0, k, (650, d)).astype(np.float32)
+        P[0], Q[0] = 0, k - 1
+        got = ctx.vdks(dev(P), dev(Q), k)
+        assert (got.num, got.den) == O.ddks(P, Q)[:2] == O.vdks(P, Q, k)[:2]
+    # constant dimension, single points, identical samples, host inputs
+    P, Q = I.random_pair(9, 50, 40, 3, "normal")
+    P[:, 1] = Q[:, 1] = 2.5
+    assert ctx.vdks(P, Q, 6)[:2] == O.vdks(P, Q, 6)[:2]
+    assert ctx.vdks(P[:1], Q[:1], 4)[:2] == O.vdks(P[:1], Q[:1], 4)[:2]
+    assert ctx.vdks(P, P.copy(), 9).num == 0
+    with pytest.raises(K.DDKSError) as e:
+        ctx.vdks(P, Q, 0)
+    assert e.value.status == 1
+    with pytest.raises(K.DDKSError) as e:
+        ctx.vdks(np.zeros((3, 8), np.float32), np.ones((3, 8), np.float32), 20)
+    assert e.value.status == 5
+
+
+def test_vdks_c2_full(ctx):
+    P, Q = I.config("C2")
+    for k in (16, 32):
+        got = ctx.vdks(dev(P), dev(Q), k)
+        assert (got.num, got.den) == O.vdks(P, Q, k)[:2]
+
+
+def test_vdks_c5_properties(ctx):
+    # full C5 (10^6 + 10^6, d = 5, k = 16): the oracle's literal SumOrthants is O(F k^d); use properties that hold
+    # at any size: symmetry and power-of-two scale invariance (NormalizeData removes it exactly)
+    P, Q = I.config("C5")
+    a = ctx.vdks(dev(P), dev(Q), 16)
+    assert a == ctx.vdks(dev(Q), dev(P), 16)
+    s = np.array([2, 4, 0.5, 1, 8], np.float32)
+    assert a == ctx.vdks(dev(P * s), dev(Q * s), 16)
+    assert 0 < a.num <= a.den
