@@ -147,6 +147,16 @@ DDKS_API ddks_status ddks_significance(ddks_ctx* ctx, const float* P, int64_t n_
 DDKS_API ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
                                int64_t k, void* stream, ddks_result* out);
 
+/* ---- rdKS: radial approximation (§2.2.3, Alg. 2) ------------------
+ * NormalizeData as ddks_vdks; corners = the origin and the d unit axis vectors of the normalised space;
+ * for each corner, Euclidean distances sqrt(sum_m (x'_m - c_m)^2) (f64, summed m = 0..d-1, correctly rounded sqrt)
+ * of both samples, sorted, and GetDFromCornerLists = max over distinct distances r of
+ * |#P(dist <= r) n_Q - #Q(dist <= r) n_P| (R17); out->num = the max over corners, out->den = n_P n_Q,
+ * out->D = num / den, out->argmax_origin = the smallest CORNER index attaining num (0 = origin, m + 1 = e_m).
+ * Any d >= 1 (the paper's high-d use: d = 1000); N (d + 1) < 2^34. Multi-GPU: corners sharded across ranks. */
+DDKS_API ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
+                               void* stream, ddks_result* out);
+
 /* Host-only helper (no GPU needed): the contiguous origin / item range [*begin, *end) that `rank` of `world`
  * owns out of `total` units. Ranges are balanced to within one unit and cover 0..total exactly. */
 DDKS_API ddks_status ddks_shard_range(int64_t total, int world, int rank, int64_t* begin, int64_t* end);

@@ -18,6 +18,7 @@
 #include "ddks_kernels.cuh"
 #include "ddks_significance.cuh"
 #include "ddks_vdks.cuh"
+#include "ddks_rdks.cuh"
 
 #define DDKS_VERSION "0.1.0-sm100a"
 
@@ -40,6 +41,7 @@ struct ddks_ctx {
     DevBuf raw_a, raw_b, raw_perm, packed, packed2, pool_packed, per_origin, accum, item_num, bitmap, labels, res;
     DevBuf sig_hist, sig_lf, sig_scratch, sig_table, sig_contrib, sig_part;  // ddks_significance workspace
     DevBuf vox_keys, vox_cnt, vox_S;                                           // ddks_vdks workspace
+    DevBuf rd_keys, rd_xn, rd_k0, rd_k1, rd_hist, rd_tcnt, rd_cnum;              // ddks_rdks workspace
     void* host_pinned = nullptr;  // DevResult + scratch
     size_t host_pinned_bytes = 0;
     int64_t launches = 0;
@@ -486,7 +488,8 @@ ddks_status ddks_destroy(ddks_ctx* ctx) {
     for (DevBuf* b : {&ctx->raw_a, &ctx->raw_b, &ctx->raw_perm, &ctx->packed, &ctx->packed2, &ctx->pool_packed, &ctx->per_origin,
                       &ctx->accum, &ctx->item_num, &ctx->bitmap, &ctx->labels, &ctx->res, &ctx->sig_hist,
                       &ctx->sig_lf, &ctx->sig_scratch, &ctx->sig_table, &ctx->sig_contrib, &ctx->sig_part,
-                      &ctx->vox_keys, &ctx->vox_cnt, &ctx->vox_S})
+                      &ctx->vox_keys, &ctx->vox_cnt, &ctx->vox_S, &ctx->rd_keys, &ctx->rd_xn, &ctx->rd_k0,
+                      &ctx->rd_k1, &ctx->rd_hist, &ctx->rd_tcnt, &ctx->rd_cnum})
         if (b->p) cudaFree(b->p);
     if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
     delete ctx;
@@ -1002,6 +1005,118 @@ ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     out->den = (uint64_t)n_P * (uint64_t)n_Q;
     out->D = (double)out->num / (double)out->den;
     out->argmax_origin = -1;
+    return DDKS_OK;
+}
+
+// ------------------------------------------------------------------------------------- rdKS (Alg. 2)
+// Corners sharded across ranks; the statistic is the max over corners (NCCL all-reduce max, then min of the first
+// attaining corner index).
+ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
+                      void* stream, ddks_result* out) {
+    if (!ctx) return DDKS_ERR_INVALID_ARGUMENT;
+    ctx->err.clear();
+    if (!out) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "null out");
+    if (n_P < 0 || n_Q < 0) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "negative sample size");
+    if (n_P == 0 || n_Q == 0) return fail(ctx, DDKS_ERR_EMPTY_SAMPLE, "empty sample");
+    if (d < 1) return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "d=%d < 1", d);
+    const int64_t N = n_P + n_Q;
+    if (N >= (int64_t(1) << 31) || (double)n_P * (double)n_Q >= 9007199254740992.0 ||
+        (double)N * (double)(d + 1) >= (double)(int64_t(1) << 34))
+        return fail(ctx, DDKS_ERR_TOO_LARGE, "rdKS problem too large (N=%lld, d=%d)", (long long)N, d);
+    if (!P || !Q) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "null argument");
+    ddks_status s;
+    if ((s = bind_device(ctx))) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const void *dP, *dQ;
+    if ((s = stage_input(ctx, P, (size_t)n_P * d * 4, ctx->raw_a, st, &dP))) return s;
+    if ((s = stage_input(ctx, Q, (size_t)n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
+    int64_t cb, ce;
+    ddks_shard_range(d + 1, ctx->world, ctx->rank, &cb, &ce);
+    const int nc = (int)(ce - cb);
+    const int tiles = (int)((N + ddks::RS_TILE - 1) / ddks::RS_TILE);
+    if ((s = ensure(ctx, ctx->rd_keys, (size_t)2 * d * 4))) return s;
+    if ((s = ensure(ctx, ctx->rd_xn, (size_t)N * d * 8))) return s;
+    if ((s = ensure(ctx, ctx->rd_k0, (size_t)std::max(nc, 1) * N * 8))) return s;
+    if ((s = ensure(ctx, ctx->rd_k1, (size_t)std::max(nc, 1) * N * 8))) return s;
+    if ((s = ensure(ctx, ctx->rd_hist, (size_t)std::max(nc, 1) * tiles * 256 * 4))) return s;
+    if ((s = ensure(ctx, ctx->rd_tcnt, (size_t)std::max(nc, 1) * tiles * 4))) return s;
+    if ((s = ensure(ctx, ctx->rd_cnum, (size_t)(d + 1) * 8))) return s;
+    uint32_t* keys = (uint32_t*)ctx->rd_keys.p;
+    double* xn = (double*)ctx->rd_xn.p;
+    uint64_t* k0 = (uint64_t*)ctx->rd_k0.p;
+    uint64_t* k1 = (uint64_t*)ctx->rd_k1.p;
+    uint32_t* hist = (uint32_t*)ctx->rd_hist.p;
+    uint32_t* tcnt = (uint32_t*)ctx->rd_tcnt.p;
+    unsigned long long* cnum = (unsigned long long*)ctx->rd_cnum.p;
+    DevResult* dres = (DevResult*)ctx->res.p;
+    CU(cudaMemsetAsync(dres, 0, sizeof(DevResult), st));
+    CU(cudaMemsetAsync(keys, 0xff, (size_t)d * 4, st));
+    CU(cudaMemsetAsync(keys + d, 0, (size_t)d * 4, st));
+    CU(cudaMemsetAsync(cnum, 0, (size_t)(d + 1) * 8, st));
+    ddks::k_rd_minmax<<<(int)((N + 255) / 256), 256, 0, st>>>((const float*)dP, n_P, (const float*)dQ, n_Q, d, keys,
+                                                             &dres->flag);
+    CHECK_LAUNCH();
+    ctx->launches++;
+    auto grid_for = [](int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); };
+    ddks::k_rd_normalize<<<grid_for(N * d), 256, 0, st>>>((const float*)dP, n_P, (const float*)dQ, n_Q, d, keys, xn);
+    CHECK_LAUNCH();
+    ctx->launches++;
+    if (nc > 0) {
+        ddks::k_rd_keys<<<grid_for(N * nc), 256, 0, st>>>(xn, N, n_P, d, (int)cb, (int)ce, k0);
+        CHECK_LAUNCH();
+        ctx->launches++;
+        const int blocks = nc * tiles;
+        uint64_t *src = k0, *dst = k1;
+        for (int shift = 0; shift < 64; shift += 8) {
+            ddks::k_rs_hist<<<blocks, ddks::RS_T, 0, st>>>(src, N, tiles, shift, hist);
+            ddks::k_rs_scan<<<nc, 256, 0, st>>>(hist, tiles);
+            ddks::k_rs_scatter<<<blocks, ddks::RS_T, 0, st>>>(src, dst, N, tiles, shift, hist);
+            CHECK_LAUNCH();
+            ctx->launches += 3;
+            std::swap(src, dst);
+        }
+        ddks::k_rd_count<<<blocks, ddks::RS_T, 0, st>>>(src, N, tiles, tcnt);
+        ddks::k_rd_sweep<<<blocks, ddks::RS_T, 0, st>>>(src, N, tiles, n_P, n_Q, tcnt, cnum);
+        CHECK_LAUNCH();
+        ctx->launches += 2;
+    }
+    if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)(d + 1) * 8))) return s;
+    DevResult* hres = (DevResult*)ctx->host_pinned;
+    uint64_t* hc = (uint64_t*)((char*)ctx->host_pinned + sizeof(DevResult));
+    CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(hc, cnum, (size_t)std::max(nc, 0) * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (ctx->world > 1) {
+        NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
+        CU(cudaMemcpyAsync(&hres->flag, &dres->flag, 4, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+    }
+    if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
+    uint64_t best = 0;
+    for (int c = 0; c < nc; ++c) best = std::max<uint64_t>(best, hc[c]);
+    uint64_t arg = ~0ull;
+    if (ctx->world > 1) {
+        hres->num = best;
+        CU(cudaMemcpyAsync(&dres->num, &hres->num, 8, cudaMemcpyHostToDevice, st));
+        NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
+        CU(cudaMemcpyAsync(&hres->num, &dres->num, 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        best = hres->num;
+    }
+    for (int c = 0; c < nc; ++c)
+        if (hc[c] == best) { arg = (uint64_t)(cb + c); break; }
+    if (ctx->world > 1) {
+        hres->arg = arg;
+        CU(cudaMemcpyAsync(&dres->arg, &hres->arg, 8, cudaMemcpyHostToDevice, st));
+        NC(ncclAllReduce(&dres->arg, &dres->arg, 1, ncclUint64, ncclMin, ctx->comm, st));
+        CU(cudaMemcpyAsync(&hres->arg, &dres->arg, 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        arg = hres->arg;
+    }
+    out->num = best;
+    out->den = (uint64_t)n_P * (uint64_t)n_Q;
+    out->D = (double)best / (double)out->den;
+    out->argmax_origin = (int64_t)arg;
     return DDKS_OK;
 }
 

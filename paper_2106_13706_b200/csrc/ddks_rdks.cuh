@@ -1,0 +1,267 @@
+// ddks_rdks.cuh — rdKS, the radial approximation of ddKS (§2.2.3, Alg. 2).
+//
+//   NormalizeData (as vdKS), corners C = {0} U {e_m} (d + 1 of them), for every corner c the Euclidean
+//   distances |x' - c| of both samples, sorted, and GetDFromCornerLists = the two-sample KS of the two distance lists
+//   (evaluated once every value <= the current one is consumed, R17); D = max over corners.
+//
+// B200 design (DESIGN.md §7 "rdKS"), O((d+1) N log N) as the paper states, no pair loop:
+//   * k_rd_minmax / k_rd_normalize: x' in f64 with _rn intrinsics (bit-identical to the oracle);
+//   * k_rd_keys: one thread per (point, corner), the literal sequential sum of (x'_m - c_m)^2 (no FMA) and a
+//     correctly rounded sqrt; key = dist bits << 1 | label (label 0 = P, 1 = Q), segment = corner;
+//   * a segmented LSD radix sort, 8 passes of 8-bit digits: per 4096-key tile histogram -> per-segment offsets ->
+//     stable scatter (warp __match_any_sync ranks + per-warp digit counters);
+//   * k_rd_sweep: per tile, the P-count prefix (earlier tiles' counts + a block scan) gives the two ECDFs at every
+//     sorted position; |i_P n_Q - i_Q n_P| is taken only at the last position of each distinct distance.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ddks_vdks.cuh"  // f32_key / key_f32
+
+namespace ddks {
+
+// keys[0..d) = min keys (init 0xffffffff), keys[d..2d) = max keys (init 0), as order-preserving uint32.
+// One thread per point of a 256-point tile, loop over dimensions; non-finite -> *flag |= 1.
+__global__ void k_rd_minmax(const float* __restrict__ P, int64_t n_P, const float* __restrict__ Q, int64_t n_Q, int d,
+                            uint32_t* keys, uint32_t* flag) {
+    const int64_t N = n_P + n_Q;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const float* row = i < n_P ? P + i * d : Q + (i - n_P) * d;
+    bool bad = false;
+    for (int m = 0; m < d; ++m) {
+        uint32_t a = 0xffffffffu, b = 0u;
+        if (i < N) {
+            float x = row[m];
+            bad |= !isfinite(x);
+            x = x == 0.0f ? 0.0f : x;  // -0 -> +0
+            a = b = f32_key(x);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+            b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&keys[m], a);
+            atomicMax(&keys[d + m], b);
+        }
+    }
+    if (bad) atomicOr(flag, 1u);
+}
+
+// xn[i][m] = (x - min_m) / (max_m - min_m) in f64 (0.5 for a constant dimension), pooled order P then Q.
+__global__ void k_rd_normalize(const float* __restrict__ P, int64_t n_P, const float* __restrict__ Q, int64_t n_Q,
+                               int d, const uint32_t* __restrict__ keys, double* __restrict__ xn) {
+    const int64_t total = (n_P + n_Q) * d;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / d;
+        const int m = (int)(e - i * d);
+        const float x = i < n_P ? P[e] : Q[e - n_P * d];
+        const double mn = (double)key_f32(keys[m]);
+        const double rng = __dsub_rn((double)key_f32(keys[d + m]), mn);
+        xn[e] = rng > 0.0 ? __ddiv_rn(__dsub_rn((double)x, mn), rng) : 0.5;
+    }
+}
+
+// key[c][i] = bits(|x'_i - corner_c|) << 1 | (i >= n_P) for corners c in [c_begin, c_end); corner 0 = origin,
+// corner c >= 1 = unit vector e_{c-1}. Threads: corner fastest, so the threads of one point share its row.
+__global__ void k_rd_keys(const double* __restrict__ xn, int64_t N, int64_t n_P, int d, int c_begin, int c_end,
+                          uint64_t* __restrict__ key) {
+    const int nc = c_end - c_begin;
+    const int64_t total = N * nc;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / nc;
+        const int c = (int)(e - i * nc) + c_begin;
+        const double* row = xn + i * d;
+        double s = 0.0;
+        for (int m = 0; m < d; ++m) {
+            const double t = __dsub_rn(row[m], (c >= 1 && m == c - 1) ? 1.0 : 0.0);
+            s = __dadd_rn(s, __dmul_rn(t, t));
+        }
+        const double dist = __dsqrt_rn(s);
+        key[(int64_t)(c - c_begin) * N + i] = ((uint64_t)__double_as_longlong(dist) << 1) | (uint64_t)(i >= n_P);
+    }
+}
+
+// ------------------------------------------------------------------------------------ segmented LSD radix sort
+constexpr int RS_T = 256, RS_ITEMS = 16, RS_TILE = RS_T * RS_ITEMS, RS_WARPS = RS_T / 32;
+
+// hist[(seg * tiles + tile) * 256 + digit]
+__global__ void __launch_bounds__(RS_T) k_rs_hist(const uint64_t* __restrict__ in, int64_t N, int tiles, int shift,
+                                                  uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[256];
+    const int seg = blockIdx.x / tiles, tile = blockIdx.x - seg * tiles;
+    const int64_t base = (int64_t)seg * N + (int64_t)tile * RS_TILE;
+    const int n = (int)min((int64_t)RS_TILE, N - (int64_t)tile * RS_TILE);
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += RS_T) atomicAdd(&h[(uint32_t)(in[base + i] >> shift) & 255u], 1u);
+    __syncthreads();
+    hist[(int64_t)blockIdx.x * 256 + threadIdx.x] = h[threadIdx.x];
+}
+
+// In place: hist -> offsets within the segment, offs[tile][dig] = sum_{d' < dig} total[d'] + sum_{t' < tile} h[t'][dig].
+__global__ void __launch_bounds__(256) k_rs_scan(uint32_t* __restrict__ hist, int tiles) {
+    __shared__ uint32_t tot[256];
+    const int seg = blockIdx.x, dig = threadIdx.x;
+    uint32_t* h = hist + (int64_t)seg * tiles * 256;
+    uint32_t run = 0;
+    for (int t = 0; t < tiles; ++t) {
+        const uint32_t v = h[t * 256 + dig];
+        h[t * 256 + dig] = run;
+        run += v;
+    }
+    tot[dig] = run;
+    __syncthreads();
+    if (dig == 0) {
+        uint32_t r = 0;
+        for (int i = 0; i < 256; ++i) {
+            const uint32_t v = tot[i];
+            tot[i] = r;
+            r += v;
+        }
+    }
+    __syncthreads();
+    const uint32_t b = tot[dig];
+    for (int t = 0; t < tiles; ++t) h[t * 256 + dig] += b;
+}
+
+// Stable scatter of one tile: warp w ranks its 512 keys (rounds of 32, in tile order) with __match_any_sync and a
+// per-warp digit counter; warps are then ordered by an exclusive scan of their counters per digit.
+__global__ void __launch_bounds__(RS_T) k_rs_scatter(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
+                                                     int64_t N, int tiles, int shift,
+                                                     const uint32_t* __restrict__ offs) {
+    __shared__ uint32_t wc[RS_WARPS][256];
+    const int seg = blockIdx.x / tiles, tile = blockIdx.x - seg * tiles;
+    const int64_t sbase = (int64_t)seg * N;
+    const int64_t base = sbase + (int64_t)tile * RS_TILE;
+    const int n = (int)min((int64_t)RS_TILE, N - (int64_t)tile * RS_TILE);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_T) (&wc[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t lt = (1u << lane) - 1u;
+    uint64_t k[RS_ITEMS];
+    uint32_t rank[RS_ITEMS], dg[RS_ITEMS];
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j) {
+        const int idx = w * (RS_ITEMS * 32) + j * 32 + lane;
+        const bool valid = idx < n;
+        k[j] = valid ? in[base + idx] : 0ull;
+        const uint32_t dig = valid ? ((uint32_t)(k[j] >> shift) & 255u) : 256u;
+        dg[j] = dig;
+        const uint32_t peers = __match_any_sync(0xffffffffu, dig);
+        uint32_t b = 0;
+        if (valid) b = wc[w][dig];
+        __syncwarp();
+        rank[j] = b + __popc(peers & lt);
+        if (valid && (peers & lt) == 0) wc[w][dig] = b + __popc(peers);  // the group's lowest lane
+        __syncwarp();
+    }
+    __syncthreads();
+    {
+        uint32_t run = 0;
+#pragma unroll
+        for (int ww = 0; ww < RS_WARPS; ++ww) {
+            const uint32_t v = wc[ww][threadIdx.x];
+            wc[ww][threadIdx.x] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    const uint32_t* o = offs + (int64_t)blockIdx.x * 256;
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j)
+        if (dg[j] < 256u) out[sbase + o[dg[j]] + wc[w][dg[j]] + rank[j]] = k[j];
+}
+
+// ------------------------------------------------------------------------------------ GetDFromCornerLists sweep
+// tcnt[seg * tiles + tile] = # P keys (label 0) in the tile
+__global__ void __launch_bounds__(RS_T) k_rd_count(const uint64_t* __restrict__ key, int64_t N, int tiles,
+                                                   uint32_t* __restrict__ tcnt) {
+    __shared__ uint32_t red[RS_WARPS];
+    const int seg = blockIdx.x / tiles, tile = blockIdx.x - seg * tiles;
+    const int64_t base = (int64_t)seg * N + (int64_t)tile * RS_TILE;
+    const int n = (int)min((int64_t)RS_TILE, N - (int64_t)tile * RS_TILE);
+    uint32_t c = 0;
+    for (int i = threadIdx.x; i < n; i += RS_T) c += (uint32_t)((key[base + i] & 1ull) == 0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t s = 0;
+        for (int i = 0; i < RS_WARPS; ++i) s += red[i];
+        tcnt[blockIdx.x] = s;
+    }
+}
+
+// cnum[seg] = max over the tie-complete positions of |i_P n_Q - i_Q n_P| (atomicMax; init 0)
+__global__ void __launch_bounds__(RS_T) k_rd_sweep(const uint64_t* __restrict__ key, int64_t N, int tiles,
+                                                   int64_t n_P, int64_t n_Q, const uint32_t* __restrict__ tcnt,
+                                                   unsigned long long* __restrict__ cnum) {
+    __shared__ uint32_t red[RS_T];
+    __shared__ int64_t before;
+    const int seg = blockIdx.x / tiles, tile = blockIdx.x - seg * tiles;
+    const int64_t sbase = (int64_t)seg * N;
+    const int64_t p0 = (int64_t)tile * RS_TILE;
+    const int n = (int)min((int64_t)RS_TILE, N - p0);
+    // P keys in earlier tiles of this segment
+    uint32_t c = 0;
+    for (int t = threadIdx.x; t < tile; t += RS_T) c += tcnt[(int64_t)seg * tiles + t];
+    red[threadIdx.x] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t s = 0;
+        for (int i = 0; i < RS_T; ++i) s += red[i];
+        before = s;
+    }
+    // blocked arrangement: thread t owns positions [t * ITEMS, t * ITEMS + ITEMS) of the tile
+    uint64_t k[RS_ITEMS];
+    uint32_t mine = 0;
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j) {
+        const int idx = threadIdx.x * RS_ITEMS + j;
+        k[j] = idx < n ? key[sbase + p0 + idx] : ~0ull;
+        mine += (uint32_t)(idx < n && (k[j] & 1ull) == 0);
+    }
+    __syncthreads();
+    red[threadIdx.x] = mine;
+    __syncthreads();
+    if (threadIdx.x == 0) {  // exclusive scan of the per-thread P counts (256 entries)
+        uint32_t r = 0;
+        for (int i = 0; i < RS_T; ++i) {
+            const uint32_t v = red[i];
+            red[i] = r;
+            r += v;
+        }
+    }
+    __syncthreads();
+    int64_t iP = before + red[threadIdx.x];
+    uint64_t best = 0;
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j) {
+        const int idx = threadIdx.x * RS_ITEMS + j;
+        if (idx >= n) break;
+        iP += (int64_t)((k[j] & 1ull) == 0);
+        const int64_t pos = p0 + idx;  // 0-based position in the merged list; pos + 1 keys consumed
+        bool last = pos == N - 1;
+        if (!last) {
+            const uint64_t nk = (j + 1 < RS_ITEMS && idx + 1 < n) ? k[j + 1] : key[sbase + pos + 1];
+            last = (nk >> 1) != (k[j] >> 1);
+        }
+        if (last) {
+            const int64_t iQ = pos + 1 - iP;
+            const int64_t t = iP * n_Q - iQ * n_P;
+            const uint64_t a = (uint64_t)(t < 0 ? -t : t);
+            best = a > best ? a : best;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t v = __shfl_xor_sync(0xffffffffu, best, o);
+        best = v > best ? v : best;
+    }
+    if ((threadIdx.x & 31) == 0 && best) atomicMax(&cnum[seg], (unsigned long long)best);
+}
+
+}  // namespace ddks

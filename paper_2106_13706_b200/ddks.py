@@ -76,6 +76,7 @@ def _load() -> ctypes.CDLL:
         "ddks_significance": ([vp, vp, i64, vp, i64, i32, u32, vp, ctypes.POINTER(ddks_significance_result), vp, vp],
                               ctypes.c_int),
         "ddks_vdks": ([vp, vp, i64, vp, i64, i32, i64, vp, ctypes.POINTER(ddks_result)], ctypes.c_int),
+        "ddks_rdks": ([vp, vp, i64, vp, i64, i32, vp, ctypes.POINTER(ddks_result)], ctypes.c_int),
         "ddks_shard_range": ([i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)], ctypes.c_int),
         "ddks_launch_count": ([vp], i64),
         "ddks_profile_read": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_uint64)],
@@ -93,7 +94,7 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 EXPORTED = ("ddks_get_nccl_id", "ddks_create", "ddks_stat", "ddks_stat_batch", "ddks_permutation_null",
-            "ddks_stat_per_origin", "ddks_significance", "ddks_vdks", "ddks_shard_range", "ddks_launch_count", "ddks_profile_read", "ddks_destroy",
+            "ddks_stat_per_origin", "ddks_significance", "ddks_vdks", "ddks_rdks", "ddks_shard_range", "ddks_launch_count", "ddks_profile_read", "ddks_destroy",
             "ddks_last_error", "ddks_version")
 
 
@@ -238,6 +239,16 @@ def ddks_vdks(ctx, P, Q, k: int, stream=None) -> Result:
     return Result(r.num, r.den, r.D, r.argmax_origin)
 
 
+def ddks_rdks(ctx, P, Q, stream=None) -> Result:
+    """rdKS (Alg. 2); argmax_origin is the first corner attaining num (0 = origin, m + 1 = e_m)."""
+    p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
+    if len(p.shape) != 2 or len(q.shape) != 2 or p.shape[1] != q.shape[1]:
+        raise ValueError(f"P {p.shape} and Q {q.shape} must be [n, d] with the same d")
+    r = ddks_result()
+    _check(LIB.ddks_rdks(ctx, p.ptr, p.shape[0], q.ptr, q.shape[0], p.shape[1], _stream(stream), ctypes.byref(r)), ctx)
+    return Result(r.num, r.den, r.D, r.argmax_origin)
+
+
 def ddks_launch_count(ctx) -> int:
     return int(LIB.ddks_launch_count(ctx))
 
@@ -273,6 +284,9 @@ class Context:
 
     def vdks(self, P, Q, k: int, stream=None) -> Result:
         return ddks_vdks(self.ctx, P, Q, k, stream)
+
+    def rdks(self, P, Q, stream=None) -> Result:
+        return ddks_rdks(self.ctx, P, Q, stream)
 
     def profile_read(self):
         return ddks_profile_read(self.ctx)

@@ -78,3 +78,48 @@ def test_vdks_c5_properties(ctx):
     s = np.array([2, 4, 0.5, 1, 8], np.float32)
     assert a == ctx.vdks(dev(P * s), dev(Q * s), 16)
     assert 0 < a.num <= a.den
+
+
+# ------------------------------------------------------------------------------------------------ rdKS (Alg. 2)
+
+RDKS_CASES = [(300, 200, 1), (1000, 900, 2), (5000, 4000, 3), (777, 1234, 4), (2100, 2500, 5), (600, 500, 8),
+              (100, 100, 64), (100, 100, 1000), (4096, 1, 3), (1, 4097, 2)]
+
+
+@pytest.mark.parametrize("n_P,n_Q,d", RDKS_CASES)
+@pytest.mark.parametrize("kind", ["normal", "mixed", "dup"])
+def test_rdks_parity(ctx, n_P, n_Q, d, kind):
+    P, Q = I.random_pair(7000 + n_P + d, n_P, n_Q, d, kind)
+    want = O.rdks(P, Q)
+    got = ctx.rdks(dev(P), dev(Q))
+    assert (got.num, got.den, got.argmax_origin) == (want[0], want[1], want[3]) and got.D == want[2], (got, want)
+
+
+def test_rdks_ties_and_edges(ctx):
+    rng = np.random.default_rng(12)
+    # integer grids: many exactly equal distances (tie groups spanning radix tiles)
+    for d, k, n in [(2, 3, 9000), (3, 2, 6000), (5, 3, 3000)]:
+        P = rng.integers(0, k, (n, d)).astype(np.float32)
+        Q = rng.integers(0, k, (n - 7, d)).astype(np.float32)
+        want = O.rdks(P, Q)
+        got = ctx.rdks(dev(P), dev(Q))
+        assert (got.num, got.argmax_origin) == (want[0], want[3])
+    P, Q = I.random_pair(13, 60, 50, 3, "normal")
+    P[:, 2] = Q[:, 2] = -1.25  # constant dimension -> 0.5
+    assert ctx.rdks(P, Q)[:2] == O.rdks(P, Q)[:2]
+    assert ctx.rdks(P, P.copy()).num == 0
+    assert ctx.rdks(P, Q).num == ctx.rdks(Q, P).num
+    Pn = P.copy()
+    Pn[3, 1] = np.inf
+    with pytest.raises(K.DDKSError) as e:
+        ctx.rdks(Pn, Q)
+    assert e.value.status == 4
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C5"])
+def test_rdks_configs_full(ctx, name):
+    # full-size parity: the oracle's rdKS is O((d+1) N log N) too, so it runs on whole BASELINE configs
+    P, Q = I.config(name)
+    want = O.rdks(P, Q)
+    got = ctx.rdks(dev(P), dev(Q))
+    assert (got.num, got.den, got.argmax_origin) == (want[0], want[1], want[3])
