@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -166,8 +167,9 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
     const int n_orig = pl.o_end - pl.o_begin;
     const int blocks_o = (n_orig + G::ORIGINS - 1) / G::ORIGINS;
     const int n_tiles = (pl.N + G::TILE - 1) / G::TILE;
-    // segment length: at most the int16 flush window; among the segment counts that respect it, pick the one
-    // whose CTA count fills the resident slots (SMs x CTAs/SM) with the least wave-quantisation loss
+    // segment length: at most the int16 flush window. Among the segment counts that respect it, pick the one with
+    // the least modelled time: waves x per-CTA cost, where a CTA costs its segment's points (x its origins) plus the
+    // flush of NB int32 partials per origin (global atomics; ~FLUSH_COST point-equivalents each) and the setup.
     static int per_sm = 0;
     if (!per_sm) {
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::T, G::SMEM_BYTES));
@@ -181,18 +183,20 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
     const int64_t base_ctas = pl.B * blocks_o;
     int segs = min_segs;
     if (!(ctx->flags & DDKS_FLAG_FORCE_DIRECT)) {
-        double best = -1.0;
-        const int max_segs = (int)std::min<int64_t>(n_tiles, std::max<int64_t>(min_segs, (8 * slots + base_ctas - 1) / base_ctas));
+        constexpr double FLUSH_COST = 2.0, SETUP_COST = 2.0 * G::TILE;  // calibrated on C3 (segs 2..16 sweep)
+        double best = 1e300;
+        const int max_segs = (int)std::min<int64_t>(n_tiles, std::max<int64_t>(min_segs, (16 * slots + base_ctas - 1) / base_ctas));
         for (int sg = min_segs; sg <= max_segs; ++sg) {
             const int tps = (n_tiles + sg - 1) / sg;
             const int real = (n_tiles + tps - 1) / tps;
             if (real != sg) continue;
             const int64_t ctas = base_ctas * sg;
             const int64_t waves = (ctas + slots - 1) / slots;
-            // fraction of slot-time doing useful work, minus a small cost per extra segment (flush + setup)
-            const double eff = (double)ctas / (double)(waves * slots) - 0.002 * (sg - min_segs);
-            if (eff > best + 1e-9) { best = eff; segs = sg; }
+            const double cta = (double)tps * G::TILE + SETUP_COST + (sg > 1 ? FLUSH_COST * G::NB : 0.0);
+            const double cost = (double)waves * cta;
+            if (cost < best * (1.0 - 1e-9)) { best = cost; segs = sg; }
         }
+        if (const char* e = getenv("DDKS_SEGS")) segs = std::max(min_segs, std::min(n_tiles, atoi(e)));  // tuning override
     }
     const int tiles_per_seg = (n_tiles + segs - 1) / segs;
     segs = (n_tiles + tiles_per_seg - 1) / tiles_per_seg;

@@ -25,12 +25,15 @@
 namespace ddks {
 
 // ----------------------------------------------------------------------------------------------- config
-// Counters are 16-bit halves of 32-bit SMEM words: word (q, rp, t) holds orthant q of origin rp (low half)
-// and of origin rp + R/2 (high half) of thread t. A CTA processes at most W points per launch segment
-// (W chosen by the host so no half can leave int16), then flushes its counters to int32 global accumulators;
-// if the whole point set fits one segment it finalises in-kernel instead.
+// Counters are 16-bit halves of 32-bit SMEM words. A CTA owns R*T origins; origin j = r*T + t (slot r of thread t)
+// lives in word (bin, j mod WPB), low half if j < WPB else high half, WPB = R*T/2 words per bin. For R >= 2 that is
+// word (bin, r mod R/2, t): a thread's two origins r and r + R/2 share a word; for R == 1 threads t and t + T/2
+// share one. Either way the 32 lanes of a warp hit 32 consecutive words (conflict-free). A CTA processes at most W
+// points per launch segment (W chosen by the host so no half can leave int16), then flushes its counters to int32
+// global accumulators; if the whole point set fits one segment it finalises in-kernel instead.
 template <int D> struct Cfg;
-// R origins per thread (even), T threads per CTA, TILE points per SMEM stage, S stages (DIFF mode).
+// R origins per thread (1 or even), T threads per CTA (multiple of 64 when R == 1), TILE points per SMEM stage,
+// S stages (DIFF mode). T is a multiple of 128 so every SMSP gets the same number of warps.
 template <> struct Cfg<1> { static constexpr int R = 8, T = 256, TILE = 512, S = 3; };
 template <> struct Cfg<2> { static constexpr int R = 8, T = 256, TILE = 512, S = 3; };
 template <> struct Cfg<3> { static constexpr int R = 8, T = 256, TILE = 512, S = 3; };
@@ -38,26 +41,31 @@ template <> struct Cfg<4> { static constexpr int R = 4, T = 256, TILE = 512, S =
 template <> struct Cfg<5> { static constexpr int R = 8, T = 384, TILE = 256, S = 3; };
 template <> struct Cfg<6> { static constexpr int R = 4, T = 256, TILE = 256, S = 3; };
 template <> struct Cfg<7> { static constexpr int R = 2, T = 256, TILE = 256, S = 3; };
-template <> struct Cfg<8> { static constexpr int R = 2, T = 192, TILE = 256, S = 3; };
+template <> struct Cfg<8> { static constexpr int R = 1, T = 256, TILE = 256, S = 3; };
 
 template <int D> __host__ __device__ constexpr int padded_dim() { return D <= 4 ? 4 : 8; }
 
 template <int D, bool SPLIT> struct Geo {
-    // SPLIT doubles the bins: halve R (keeping it even), or T when R is already 2
+    // SPLIT doubles the bins: halve R (keeping it even or 1), or T when R is already <= 2
     static constexpr int R = (SPLIT && Cfg<D>::R > 2) ? Cfg<D>::R / 2 : Cfg<D>::R;
-    static constexpr int T = (SPLIT && Cfg<D>::R == 2) ? Cfg<D>::T / 2 : Cfg<D>::T;
-    static constexpr int RP = R / 2;                            // counter words per (bin, thread)
+    static constexpr int T = (SPLIT && Cfg<D>::R <= 2) ? Cfg<D>::T / 2 : Cfg<D>::T;
+    static constexpr int RP = R / 2;                            // counter words per (bin, thread) when R >= 2
+    static constexpr int NBASE = R >= 2 ? RP : 1;               // distinct counter base addresses per thread
+    static constexpr int WPB = R * T / 2;                       // counter words per bin
     static constexpr int TILE = Cfg<D>::TILE;
     static constexpr int S = Cfg<D>::S;
     static constexpr int DP = padded_dim<D>();
     static constexpr int NQ = 1 << D;
     static constexpr int NB = NQ * (SPLIT ? 2 : 1);            // counters per origin
-    static constexpr int HIST_WORDS = NB * RP * T;
+    static constexpr int HIST_WORDS = NB * WPB;
     static constexpr int TILE_BYTES = TILE * DP * 4;
     static constexpr int SMEM_BYTES = S * TILE_BYTES + HIST_WORDS * 4 + 64;
     static constexpr int ORIGINS = R * T;
-    static_assert(R % 2 == 0, "R must be even (two origins per counter word)");
+    static_assert(R == 1 || R % 2 == 0, "R must be 1 or even");
+    static_assert(R >= 2 || T % 64 == 0, "R == 1 pairs thread t with t + T/2: T/2 must be whole warps");
     static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+    __host__ __device__ static constexpr int slot(int r, int t) { return (r * T + t) % WPB; }
+    __host__ __device__ static constexpr bool high(int r, int t) { return r * T + t >= WPB; }
 };
 
 // ----------------------------------------------------------------------------------------------- PTX helpers
@@ -94,8 +102,10 @@ template <bool GT> __device__ __forceinline__ float cmp_bit(float x, float o) {
     else              asm("set.ge.f32.f32 %0, %1, %2;" : "=f"(r) : "f"(x), "f"(o));
     return r;
 }
+// No "memory" clobber: the counters are only read after a __syncthreads() (a compiler and hardware fence), and the
+// point tiles the hot loop loads are disjoint from them, so ptxas may hoist the next point's LDS above these REDs.
 __device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v));
 }
 
 template <int D> __device__ __forceinline__ void load_point(const float* sp, float (&x)[D]) {
@@ -193,19 +203,19 @@ template <int D, bool SPLIT>
 __device__ __forceinline__ uint64_t origin_num(const uint32_t* hist, int r, int t, const CountArgs& a) {
     using G = Geo<D, SPLIT>;
     constexpr int NQ = G::NQ;
-    const int rp = r % G::RP;
-    const bool high = r >= G::RP;
+    const int sl = G::slot(r, t);
+    const bool high = G::high(r, t);
     uint64_t best = 0;
     for (int q = 0; q < NQ; ++q) {
         int32_t lo, hi;
-        split16(hist[(q * G::RP + rp) * G::T + t], lo, hi);
+        split16(hist[q * G::WPB + sl], lo, hi);
         const int32_t v = high ? hi : lo;
         if constexpr (!SPLIT) {
             const uint64_t av = (uint64_t)(v < 0 ? -v : v) * a.g;
             best = av > best ? av : best;
         } else {
             int32_t lo2, hi2;
-            split16(hist[((NQ + q) * G::RP + rp) * G::T + t], lo2, hi2);
+            split16(hist[(NQ + q) * G::WPB + sl], lo2, hi2);
             const int64_t cQ = high ? hi2 : lo2;
             if (a.hist) atomicAdd(&a.hist[cQ], 1ull);
             const int64_t df = (int64_t)v * a.nQ - cQ * a.nP;
@@ -225,53 +235,97 @@ __device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
     return v;
 }
 
+// Float-encoded counter address of the pair (origin o, point x): base + sum_k [x_k >= o_k] * 4 * 2^k * WPB, as d
+// FSET.BF (ALU pipe) + d FFMA-immediate (FMA pipe); exact, every partial sum is an integer < 2^24.
+template <int D, bool GT, int WPB, bool SPLIT_CHAIN = (D >= 6)>
+__device__ __forceinline__ float code_addr(const float (&x)[D], const float (&o)[D], float base) {
+    if constexpr (SPLIT_CHAIN) {
+        // two half-length FFMA chains shorten the dependency chain when few warps are resident (d >= 6 keeps 256+
+        // counters per origin in SMEM)
+        constexpr int H = D / 2;
+        float f0 = base, f1 = 0.0f;
+#pragma unroll
+        for (int k = 0; k < H; ++k) f0 = fmaf(cmp_bit<GT>(x[k], o[k]), (float)(4 * (1 << k) * WPB), f0);
+#pragma unroll
+        for (int k = H; k < D; ++k) f1 = fmaf(cmp_bit<GT>(x[k], o[k]), (float)(4 * (1 << k) * WPB), f1);
+        return f0 + f1;
+    } else {
+        float f = base;
+#pragma unroll
+        for (int k = 0; k < D; ++k) f = fmaf(cmp_bit<GT>(x[k], o[k]), (float)(4 * (1 << k) * WPB), f);
+        return f;
+    }
+}
+
 // Classify + count the points [lo, hi) of one SMEM tile for the R origins of this thread.
-// Per pair: D x FSET.BF (ALU) + D x FFMA-immediate (FMA) + 1 x ATOMS.ADD; the next point is prefetched.
-template <int D, bool GT, int R, int T, int RP, int DP>
+// Per pair: D x FSET.BF (ALU) + D x FFMA-immediate (FMA) + 1 x ATOMS.ADD; the next point(s) are prefetched.
+// base[r % NB_] is the float-encoded address of origin slot r's bin-0 word; weights 4 * 2^k * WPB. inc_lo / inc_hi:
+// the increment for low-half / high-half origins (R == 1: the caller passes this thread's increment in both).
+// With R <= 2 origins per thread two points are classified per step, so a warp has 2R independent chains in flight.
+template <int D, bool GT, int R, int RP, int NB_, int WPB, int DP>
 __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, const float (&o)[R][D],
-                                             const float (&base)[RP], uint32_t ubase, uint32_t inc_lo,
+                                             const float (&base)[NB_], uint32_t ubase, uint32_t inc_lo,
                                              uint32_t inc_hi) {
     if (lo >= hi) return;
-    // prefetch the next point unconditionally: index hi <= TILE stays inside the SMEM allocation (the value
-    // read past the valid range is never used)
+    int p = lo;
+    // prefetches read at most two points past hi <= TILE: still inside the SMEM allocation (the next stage or the
+    // counters), and the values are never used
+    if constexpr (R <= 2) {
+        float na[D], nb[D];
+        load_point<D>(tile + p * DP, na);
+        load_point<D>(tile + (p + 1) * DP, nb);
+#pragma unroll 2
+        for (; p + 1 < hi; p += 2) {
+            float xa[D], xb[D];
+#pragma unroll
+            for (int k = 0; k < D; ++k) xa[k] = na[k], xb[k] = nb[k];
+            load_point<D>(tile + (p + 2) * DP, na);
+            load_point<D>(tile + (p + 3) * DP, nb);
+            float fa[R], fb[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                // two points in flight already give 2R independent chains: no chain split
+                fa[r] = code_addr<D, GT, WPB, false>(xa, o[r], base[r % NB_]);
+                fb[r] = code_addr<D, GT, WPB, false>(xb, o[r], base[r % NB_]);
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t inc = (R >= 2 && r < RP) ? inc_lo : inc_hi;
+                red_add_shared(__float_as_uint(fa[r]) + ubase, inc);
+                red_add_shared(__float_as_uint(fb[r]) + ubase, inc);
+            }
+        }
+        if (p < hi) {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                red_add_shared(__float_as_uint(code_addr<D, GT, WPB>(na, o[r], base[r % NB_])) + ubase,
+                               (R >= 2 && r < RP) ? inc_lo : inc_hi);
+        }
+        return;
+    }
     float xn[D];
-    load_point<D>(tile + lo * DP, xn);
+    load_point<D>(tile + p * DP, xn);
 #pragma unroll 4
-    for (int p = lo; p < hi; ++p) {
+    for (; p < hi; ++p) {
         float x[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) x[k] = xn[k];
         load_point<D>(tile + (p + 1) * DP, xn);
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            float f;
-            if constexpr (D >= 6) {
-                // two half-length FFMA chains (exact: all partial sums are integers < 2^24) shorten the dependency
-                // chain when few warps are resident (d >= 6 keeps 256+ counters per origin in SMEM)
-                constexpr int H = D / 2;
-                float f0 = base[r % RP], f1 = 0.0f;
-#pragma unroll
-                for (int k = 0; k < H; ++k) f0 = fmaf(cmp_bit<GT>(x[k], o[r][k]), (float)(4 * (1 << k) * RP * T), f0);
-#pragma unroll
-                for (int k = H; k < D; ++k) f1 = fmaf(cmp_bit<GT>(x[k], o[r][k]), (float)(4 * (1 << k) * RP * T), f1);
-                f = f0 + f1;
-            } else {
-                f = base[r % RP];
-#pragma unroll
-                for (int k = 0; k < D; ++k) f = fmaf(cmp_bit<GT>(x[k], o[r][k]), (float)(4 * (1 << k) * RP * T), f);
-            }
-            red_add_shared(__float_as_uint(f) + ubase, r < RP ? inc_lo : inc_hi);
-        }
+        for (int r = 0; r < R; ++r)
+            red_add_shared(__float_as_uint(code_addr<D, GT, WPB>(x, o[r], base[r % NB_])) + ubase,
+                           (R >= 2 && r < RP) ? inc_lo : inc_hi);
     }
 }
 
 template <int D, bool SPLIT, bool GT>
 __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a) {
     using G = Geo<D, SPLIT>;
-    constexpr int R = G::R, RP = G::RP, T = G::T, DP = G::DP, TILE = G::TILE, S = G::S;
+    constexpr int R = G::R, RP = G::RP, T = G::T, DP = G::DP, TILE = G::TILE, S = G::S, NBASE = G::NBASE,
+                  WPB = G::WPB;
     extern __shared__ __align__(128) uint8_t smem[];
     float* tiles = reinterpret_cast<float*>(smem);                                  // [S][TILE][DP]
-    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + S * G::TILE_BYTES);          // [NB][RP][T]
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + S * G::TILE_BYTES);          // [NB][WPB]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * G::TILE_BYTES + G::HIST_WORDS * 4);
 
     // grid: x = point segment (fastest, so the CTAs in flight share origin blocks and their accumulators stay
@@ -314,13 +368,17 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
 
     // the counter byte address lives in the mantissa of a float in [2^23, 2^24): bits = 0x4B000000 + offset
     const uint32_t ubase = smem_u32(hist) - 0x4B000000u;
-    float baseP[RP], baseQ[RP];
+    float baseP[NBASE], baseQ[NBASE];
 #pragma unroll
-    for (int rp = 0; rp < RP; ++rp) {
-        baseP[rp] = __uint_as_float(0x4B000000u + 4u * (uint32_t)(rp * T + t));
-        baseQ[rp] = SPLIT ? __uint_as_float(0x4B000000u + 4u * (uint32_t)((G::NQ * RP + rp) * T + t)) : baseP[rp];
+    for (int b = 0; b < NBASE; ++b) {
+        const uint32_t sl = (uint32_t)G::slot(b, t);
+        baseP[b] = __uint_as_float(0x4B000000u + 4u * sl);
+        baseQ[b] = SPLIT ? __uint_as_float(0x4B000000u + 4u * (uint32_t)(G::NQ * WPB + sl)) : baseP[b];
     }
     const uint32_t incP_hi = a.incP << 16, incQ_hi = a.incQ << 16;
+    // R == 1: this thread's single origin is a low or a high half for its whole life
+    const uint32_t incP_lo = (R == 1 && G::high(0, t)) ? incP_hi : a.incP;
+    const uint32_t incQ_lo = (R == 1 && G::high(0, t)) ? incQ_hi : a.incQ;
 
     for (int it = 0; it < n_tiles; ++it) {
         const int s = it % S;
@@ -331,8 +389,8 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
         // sample-homogeneous sub-ranges: [p0, n_P) are P points, [n_P, ...) are Q points
         int32_t split = a.n_P - p0;
         split = split < 0 ? 0 : (split > cnt ? cnt : split);
-        count_points<D, GT, R, T, RP, DP>(tile, 0, split, o, baseP, ubase, a.incP, incP_hi);
-        count_points<D, GT, R, T, RP, DP>(tile, split, cnt, o, baseQ, ubase, a.incQ, incQ_hi);
+        count_points<D, GT, R, RP, NBASE, WPB, DP>(tile, 0, split, o, baseP, ubase, incP_lo, R == 1 ? incP_lo : incP_hi);
+        count_points<D, GT, R, RP, NBASE, WPB, DP>(tile, split, cnt, o, baseQ, ubase, incQ_lo, R == 1 ? incQ_lo : incQ_hi);
         __syncthreads();  // every thread is done with stage s
         if (t == 0 && it + S < n_tiles) {
             fence_proxy_async();
@@ -349,14 +407,17 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
         // flush: exact int32 partial counters -> global (red.global.add), finalised by k_finalize
         int32_t* acc = a.accum + item * (int64_t)G::NB * n_orig;
 #pragma unroll 1
-        for (int rp = 0; rp < RP; ++rp) {
-            const int32_t o_lo = blk_o0 + rp * T + t, o_hi = o_lo + RP * T;
+        for (int r = 0; r < R; ++r) {
+            const int32_t oi = blk_o0 + r * T + t;
+            if (oi >= a.o_end) continue;
+            const int sl = G::slot(r, t);
+            const bool hiw = G::high(r, t);
 #pragma unroll 4
             for (int q = 0; q < G::NB; ++q) {
                 int32_t lo, hi;
-                split16(hist[(q * RP + rp) * T + t], lo, hi);
-                if (lo && o_lo < a.o_end) atomicAdd(&acc[(int64_t)q * n_orig + (o_lo - a.o_begin)], lo);
-                if (hi && o_hi < a.o_end) atomicAdd(&acc[(int64_t)q * n_orig + (o_hi - a.o_begin)], hi);
+                split16(hist[q * WPB + sl], lo, hi);
+                const int32_t v = hiw ? hi : lo;
+                if (v) atomicAdd(&acc[(int64_t)q * n_orig + (oi - a.o_begin)], v);
             }
         }
         return;
