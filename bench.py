@@ -44,7 +44,11 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="C5", choices=["C1", "C2", "C3", "C5"])
+    ap.add_argument("--workload", default="C5", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--method", default="exact", choices=["exact", "significance", "vdks", "rdks"],
+                    help="exact = the headline statistic (C4 = 4096-pair batch + 1000-permutation null); "
+                         "significance = §3 analytic S; vdks / rdks = the §2.2.2-2.2.3 approximations")
+    ap.add_argument("--vdks-k", type=int, default=16, help="voxels per dimension for --method vdks")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-oracle sample duration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -135,6 +139,8 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    if args.workload == "C4" or args.method != "exact":
+        raise SystemExit("--impl reference times the exact statistic on C1/C2/C3/C5")
     P, Q, cfg = workload(args.workload)
     per_step = max(1.0, 60.0 / max(1, args.steps + args.warmup))  # whole run within a few minutes
     for _ in range(args.warmup):
@@ -161,6 +167,90 @@ def run_reference(args):
     return 0
 
 
+class Step:
+    """One step of the chosen method on the chosen workload: device-input and host-input calls, the units a step
+    processes (for `value`), and the algorithmic work of the dominant kernel (for `roofline`)."""
+
+    def __init__(self, args, ctx, K, torch):
+        self.args, self.ctx = args, ctx
+        m, w = args.method, args.workload
+        if w == "C4":
+            if m != "exact":
+                raise SystemExit("--workload C4 is the batch + permutation null of --method exact")
+            from paper_2106_13706_b200 import inputs as I
+            P, Q = I.config("C4")
+            perms = I.c4_perms()
+            pooled = np.concatenate([P[I.C4_PERM_PAIR], Q[I.C4_PERM_PAIR]])
+            B, n, d = P.shape
+            self.cfg = {"workload": f"C4: {I.CONFIG_NAMES['C4']}", "B": B, "n_P": n, "n_Q": n, "d": d,
+                        "n_perm": int(perms.shape[0]),
+                        "pairs_per_step": int(B * (2 * n) ** 2 + perms.shape[0] * (2 * n) ** 2)}
+            self.host = (P, Q, pooled, perms)
+            self.dev = tuple(torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in self.host)
+
+            def call(P, Q, pooled, perms):
+                r = ctx.stat_batch(P, Q)
+                null, obs, pv = ctx.permutation_null(pooled, n, perms)
+                return (tuple(x.num for x in r), tuple(int(v) for v in null), obs.num, pv)
+            self.call = call
+            self.d2h = B * 32 + perms.shape[0] * 8 + 8
+        else:
+            P, Q, cfg = workload(w)
+            self.cfg = cfg
+            self.host = (P, Q)
+            self.dev = (torch.from_numpy(P).cuda(), torch.from_numpy(Q).cuda())
+            if m == "exact":
+                self.call = lambda P, Q: ctx.stat(P, Q)
+            elif m == "significance":
+                self.call = lambda P, Q: ctx.significance(P, Q)
+            elif m == "vdks":
+                self.cfg["k"] = args.vdks_k
+                self.call = lambda P, Q: ctx.vdks(P, Q, args.vdks_k)
+            else:
+                self.call = lambda P, Q: ctx.rdks(P, Q)
+            self.d2h = 56 if m == "significance" else 24
+        self.h2d = int(sum(a.nbytes for a in self.host))
+        N = self.cfg["n_P"] + self.cfg["n_Q"]
+        self.N = N
+        if m in ("exact", "significance"):
+            self.metric, self.unit, self.units = METRIC, UNIT, self.cfg["pairs_per_step"]
+        else:
+            self.metric = f"{m} statistic throughput (pooled points/s)"
+            self.unit, self.units = "points/s", N
+
+    def roofline(self, kern_ms, kern_launches, kern_pairs, step_ms, peaks_):
+        d = self.cfg["d"]
+        sm_max = float(peaks_.get("sm_max_mhz", 1965.0))
+        if self.args.method in ("exact", "significance"):
+            per_launch_ms = kern_ms / max(kern_launches, 1)
+            pairs_per_launch = kern_pairs / max(kern_launches, 1)
+            achieved = d * pairs_per_launch / (per_launch_ms / 1e3) / 1e12  # T compares / s (per GPU)
+            peak = N_SM * FSET_LANES_PER_CLK_PER_SM * sm_max * 1e6 / 1e12
+            return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tcompare/s", "frac": achieved / peak,
+                    "kernel": "k_count / k_perm_count (classify + count)", "kernel_ms_per_launch": per_launch_ms,
+                    "kernel_launches_per_step": kern_launches / max(self.args.steps, 1),
+                    "peak_source": f"{N_SM} SMs x {FSET_LANES_PER_CLK_PER_SM} FSET lanes/clk/SM x {sm_max} MHz "
+                                   "(MEASURED_PEAKS.json sm_max_mhz; lane rate measured by microbench/pipes.cu)"}
+        N = self.N
+        if self.args.method == "vdks":
+            V = self.args.vdks_k ** d
+            # input read + pack write/read, voxel counts, diff, d prefix passes (read + write), one read in the
+            # orthant pass (DESIGN.md §7 vdKS)
+            byts = N * d * 4 + 2 * N * (4 if d <= 4 else 8) * 4 + V * 8 * 2 + V * 8 + 2 * d * V * 8 + V * 8
+            what = "whole vdKS step (pack, voxel histogram, prefix passes, orthant sums)"
+        else:
+            keys = (d + 1) * N * 8
+            # input read, f64 x' write + read, key write, 8 radix passes x (hist read + scatter read + write),
+            # count + sweep reads (DESIGN.md §7 rdKS)
+            byts = N * d * 4 + 2 * N * d * 8 + keys + 8 * 3 * keys + 2 * keys
+            what = "whole rdKS step (normalise, distance keys, 8-pass radix sort, sweep)"
+        achieved = byts / (step_ms / 1e3) / 1e9
+        peak = float(peaks_.get("hbm_gbs", 6536.7))
+        return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "algorithmic_bytes_per_step": int(byts), "kernel": what,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -185,13 +275,9 @@ def main():
         nccl_id = obj[0]
     ctx = K.Context(device=local, world=world, rank=rank, nccl_id=nccl_id, flags=K.DDKS_FLAG_PROFILE)
 
-    P, Q, cfg = workload(args.workload)
-    d = cfg["d"]
-    N = cfg["n_P"] + cfg["n_Q"]
-    pairs_step = N * N
+    step = Step(args, ctx, K, torch)
+    cfg = step.cfg
     stream = torch.cuda.current_stream()
-    dP = torch.from_numpy(P).cuda()
-    dQ = torch.from_numpy(Q).cuda()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
     def barrier():
@@ -209,7 +295,7 @@ def main():
 
     res = None
     for _ in range(max(3, args.warmup)):
-        res = ctx.stat(dP, dQ)
+        res = step.call(*step.dev)
     ctx.profile_read()  # discard warm-up profile
     barrier()
     clocks = ClockSampler(local)
@@ -222,7 +308,7 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        r = ctx.stat(dP, dQ)
+        r = step.call(*step.dev)
         e1.record(stream)
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
@@ -233,14 +319,13 @@ def main():
     kern_ms, kern_launches, kern_pairs = ctx.profile_read()
     clk = clocks.stop()
     total_ms = max_over_ranks(float(sum(step_ms)))
-    value = args.steps * pairs_step / (total_ms / 1e3)
+    value = args.steps * step.units / (total_ms / 1e3)
 
     # end-to-end: host (pinned) inputs through the C-ABI, H2D inside the timed call, D2H of the result
     e2e = None
     if not args.no_e2e:
-        hP = torch.from_numpy(P).pin_memory()
-        hQ = torch.from_numpy(Q).pin_memory()
-        ctx.stat(hP, hQ)
+        hosts = tuple(torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in step.host)
+        step.call(*hosts)
         ctx.profile_read()
         barrier()
         e2e_s = []
@@ -248,49 +333,50 @@ def main():
             flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            r = ctx.stat(hP, hQ)
+            r = step.call(*hosts)
             e2e_s.append(time.perf_counter() - t0)
             assert r == res
         barrier()
         ctx.profile_read()
         e2e_total = max_over_ranks(float(sum(e2e_s)))
-        e2e = {"value": args.steps * pairs_step / e2e_total, "unit": UNIT,
-               "h2d_bytes_per_step": int(P.nbytes + Q.nbytes), "d2h_bytes_per_step": 24,
+        e2e = {"value": args.steps * step.units / e2e_total, "unit": step.unit,
+               "h2d_bytes_per_step": step.h2d, "d2h_bytes_per_step": step.d2h,
                "ms_per_step": e2e_total / args.steps * 1e3}
 
     pk = peaks()
-    sm_max = float(pk.get("sm_max_mhz", 1965.0))
-    # roofline of the dominant kernel (classify+count), per rank, averaged over its timed launches
     kern_ms_max = max_over_ranks(kern_ms)
-    per_launch_ms = kern_ms / max(kern_launches, 1)
-    pairs_per_launch = kern_pairs / max(kern_launches, 1)
-    achieved = d * pairs_per_launch / (per_launch_ms / 1e3) / 1e12  # T compares / s (per GPU)
-    peak = N_SM * FSET_LANES_PER_CLK_PER_SM * sm_max * 1e6 / 1e12
+    roof = step.roofline(kern_ms, kern_launches, kern_pairs, total_ms / args.steps, pk)
+    if args.method in ("exact", "significance"):
+        roof["kernel_share_of_step"] = kern_ms_max / total_ms if total_ms else None
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and args.method == "exact":
         try:
             traffic = json.load(open(tp)).get(args.workload)
         except Exception:
             traffic = None
+    roof = dict({k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac")}, traffic=traffic,
+                **{k: v for k, v in roof.items() if k not in ("bound", "achieved", "peak", "unit", "frac")})
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_oracle_sample(P, Q, args.cpu_seconds)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.method == "exact" and args.workload != "C4":
+        cpu = cpu_oracle_sample(*step.host, args.cpu_seconds)
 
     if rank == 0:
+        if hasattr(res, "_asdict"):
+            result = {k: (v._asdict() if hasattr(v, "_asdict") else v) for k, v in res._asdict().items()
+                      if k not in ("mt_hist", "log_p_table")}
+        else:
+            result = {"batch_num_sum": int(sum(res[0])), "null_num_max": int(max(res[1])), "observed_num": res[2],
+                      "p_value": res[3]}
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": step.metric, "value": value, "unit": step.unit, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE.json recipe)",
-            "config": dict(cfg, parallelism=f"origins sharded over {world} GPU(s), NCCL all-reduce(max)",
+            "config": dict(cfg, method=args.method,
+                           parallelism=f"sharded over {world} GPU(s) (DESIGN.md §8), NCCL combine",
                            l2="flushed between steps (512 MiB write, outside the step events)"),
-            "result": {"num": res.num, "den": res.den, "D": res.D, "argmax_origin": res.argmax_origin},
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tcompare/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_count (classify + count)", "kernel_ms_per_launch": per_launch_ms,
-                         "kernel_share_of_step": kern_ms_max / total_ms if total_ms else None,
-                         "peak_source": f"{N_SM} SMs x {FSET_LANES_PER_CLK_PER_SM} FSET lanes/clk/SM x {sm_max} MHz "
-                                        "(MEASURED_PEAKS.json sm_max_mhz; lane rate measured by microbench/pipes.cu)"},
+            "result": result,
+            "roofline": roof,
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": int(launches),

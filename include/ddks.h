@@ -167,7 +167,8 @@ DDKS_API int64_t ddks_launch_count(const ddks_ctx* ctx);
 /* Profiling (context created with DDKS_FLAG_PROFILE): totals since the last read, then reset.
  * count_ms: summed device time of the classify+count kernel launches (CUDA events on the call's stream);
  * launches: how many such launches; pairs: point-pair orthant classifications they performed (sum of
- * items x origins x points); any pointer may be NULL. */
+ * items x origins x points; for the label-invariant permutation kernel, one classification per pair per chunk of
+ * permutations it serves); any pointer may be NULL. */
 DDKS_API ddks_status ddks_profile_read(ddks_ctx* ctx, double* count_ms, int64_t* launches, uint64_t* pairs);
 
 /* Destroy a context (NULL-safe). Frees workspace and the NCCL communicator. */

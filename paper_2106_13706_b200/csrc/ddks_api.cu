@@ -367,7 +367,8 @@ ddks_status launch_perm_d(ddks_ctx* ctx, const float* pooled_packed, const int32
     if (ev.first) {
         CU(cudaEventRecord(ev.second, st));
         ctx->ev_pending.push_back(ev);
-        ctx->ev_pairs.push_back((uint64_t)n_perm * (uint64_t)N * (uint64_t)N);
+        // classifications actually performed: each pair is classified once per chunk of J permutations
+        ctx->ev_pairs.push_back((uint64_t)chunks * (uint64_t)N * (uint64_t)N);
     }
     return DDKS_OK;
 }
