@@ -68,6 +68,9 @@ typedef enum {
 #define DDKS_FLAG_PERM_GATHER 16u /* TEST ONLY: permutation null by gathering each relabelled sample and re-running the
                                       full classification (the default label-invariant path classifies each pair once
                                       for a chunk of permutations; both give identical results)                    */
+#define DDKS_FLAG_NO_X0 32u        /* TEST ONLY: never use the x0-ordered count (ddks_stat sorts the pooled points by x_0 when
+                                      2 <= d <= 6 and N >= 200000, so whole tiles share bit 0; identical results)   */
+#define DDKS_FLAG_FORCE_X0 64u     /* TEST ONLY: use the x0-ordered count for any N (2 <= d <= 6, DIFF counters)      */
 #define DDKS_FLAG_PROFILE 8u      /* record CUDA events around every count-kernel launch (see ddks_profile_read) */
 
 typedef struct {

@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -43,6 +44,7 @@ struct ddks_ctx {
     DevBuf sig_hist, sig_lf, sig_scratch, sig_table, sig_contrib, sig_part;  // ddks_significance workspace
     DevBuf vox_keys, vox_cnt, vox_S;                                           // ddks_vdks workspace
     DevBuf rd_keys, rd_xn, rd_k0, rd_k1, rd_hist, rd_tcnt, rd_cnum;              // ddks_rdks workspace
+    DevBuf x0_keys0, x0_keys1, x0_hist, x0_pts, x0_perm;                        // x0-ordered count workspace
     void* host_pinned = nullptr;  // DevResult + scratch
     size_t host_pinned_bytes = 0;
     int64_t launches = 0;
@@ -155,10 +157,12 @@ struct CountPlan {
     int64_t window;  // max points per segment so no 16-bit counter half leaves int16
 };
 
-template <int D, bool SPLIT, bool GT>
+template <int D, bool SPLIT, bool GT, bool X0 = false>
 ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a, cudaStream_t st) {
-    using G = ddks::Geo<D, SPLIT>;
-    auto kern = ddks::k_count<D, SPLIT, GT>;
+    using G = std::conditional_t<X0, ddks::Geo<D, false, ddks::sorted_dim<D>()>, ddks::Geo<D, SPLIT>>;
+    void (*kern)(const ddks::CountArgs) = nullptr;
+    if constexpr (X0) kern = ddks::k_count_x0<D, GT>;
+    else kern = ddks::k_count<D, SPLIT, GT>;
     static bool attr_done = false;  // per-process; device attributes are per function
     if (!attr_done) {
         CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES));
@@ -299,6 +303,93 @@ ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int6
         case 8: return launch_count_d<8>(ctx, pl, a, st);
     }
     return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "d=%d", d);
+}
+
+// x0-ordered statistic (B == 1, DIFF counters, 2 <= d <= 6): sort the packed points by x_0, build the sorted rows
+// (coordinates + per-point increments), count with bit-0 elision (k_count_x0), per-origin nums scattered back to
+// pooled order into per_origin[N] (zeroed here). Origins [o_begin, o_end) are positions in the SORTED order.
+template <int D>
+ddks_status run_count_x0_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int64_t n_Q, int64_t o_begin,
+                           int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st) {
+    constexpr int DPS = ddks::sorted_dim<D>();
+    const int64_t N = n_P + n_Q;
+    const int DP = pad_dim(D);
+    const int tiles = (int)((N + ddks::RS_TILE - 1) / ddks::RS_TILE);
+    ddks_status s;
+    if ((s = ensure(ctx, ctx->x0_keys0, (size_t)N * 8))) return s;
+    if ((s = ensure(ctx, ctx->x0_keys1, (size_t)N * 8))) return s;
+    if ((s = ensure(ctx, ctx->x0_hist, (size_t)tiles * 256 * 4))) return s;
+    if ((s = ensure(ctx, ctx->x0_pts, (size_t)(N + 2) * DPS * 4))) return s;
+    if ((s = ensure(ctx, ctx->x0_perm, (size_t)N * 4))) return s;
+    uint64_t* k0 = (uint64_t*)ctx->x0_keys0.p;
+    uint64_t* k1 = (uint64_t*)ctx->x0_keys1.p;
+    uint32_t* hist = (uint32_t*)ctx->x0_hist.p;
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 16));
+    ddks::k_x0_keys<<<g, 256, 0, st>>>(packed, DP, N, k0);
+    CHECK_LAUNCH();
+    ctx->launches++;
+    // stable LSD passes over the key's upper 32 bits only: ties in x_0 keep pooled-index order
+    uint64_t *src = k0, *dst = k1;
+    for (int shift = 32; shift < 64; shift += 8) {
+        ddks::k_rs_hist<<<tiles, ddks::RS_T, 0, st>>>(src, N, tiles, shift, hist);
+        ddks::k_rs_scan<<<1, 256, 0, st>>>(hist, tiles);
+        ddks::k_rs_scatter<<<tiles, ddks::RS_T, 0, st>>>(src, dst, N, tiles, shift, hist);
+        CHECK_LAUNCH();
+        ctx->launches += 3;
+        std::swap(src, dst);
+    }
+    const uint64_t gg = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
+    const uint32_t a_ = (uint32_t)((uint64_t)n_Q / gg), b_ = (uint32_t)((uint64_t)n_P / gg);
+    float* spts = (float*)ctx->x0_pts.p;
+    ddks::k_permute_sorted<<<g, 256, 0, st>>>(packed, DP, DPS, D, N, n_P, src, a_, 0u - b_, spts,
+                                              (int32_t*)ctx->x0_perm.p);
+    CHECK_LAUNCH();
+    ctx->launches++;
+    CU(cudaMemsetAsync(spts + N * DPS, 0, 2 * DPS * 4, st));  // the prefetch past the last point reads zeros
+    CU(cudaMemsetAsync(per_origin, 0, (size_t)N * 8, st));
+    CountPlan pl{1, (int32_t)N, (int32_t)n_P, (int32_t)o_begin, (int32_t)o_end, n_P, n_Q, false,
+                 (int64_t)(32767 / std::max(a_, b_))};
+    ddks::CountArgs a{};
+    a.pts = spts;
+    a.item_stride = N * DPS;
+    a.N = (int32_t)N;
+    a.n_P = (int32_t)n_P;
+    a.o_begin = (int32_t)o_begin;
+    a.o_end = (int32_t)o_end;
+    a.incP = a_;
+    a.incQ = 0u - b_;
+    a.g = gg;
+    a.nP = n_P;
+    a.nQ = n_Q;
+    a.item_num = item_num;
+    a.per_origin = per_origin;
+    a.perm = (const int32_t*)ctx->x0_perm.p;
+    a.hist = nullptr;
+    const bool gt = (ctx->flags & DDKS_FLAG_TIES_GT) != 0;
+    return gt ? launch_count_t<D, false, true, true>(ctx, pl, a, st) : launch_count_t<D, false, false, true>(ctx, pl, a, st);
+}
+
+bool x0_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q) {
+    if (ctx->flags & DDKS_FLAG_NO_X0) return false;
+    const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
+    const uint64_t mab = std::max((uint64_t)n_Q / g, (uint64_t)n_P / g);
+    const bool diff_ok = !(mab > 32767 / 4096 || (uint64_t)n_P * ((uint64_t)n_Q / g) >= 0x7fffffffull ||
+                           (uint64_t)n_Q * ((uint64_t)n_P / g) >= 0x7fffffffull);
+    // the sort (~0.1 ms) pays for itself once the O(N^2) count dominates; DDKS_FLAG_FORCE_X0 (tests) lowers the bar
+    const int64_t min_n = (ctx->flags & DDKS_FLAG_FORCE_X0) ? 2 : 200000;
+    return d >= 2 && d <= 6 && diff_ok && n_P + n_Q >= min_n;
+}
+
+ddks_status run_count_x0(ddks_ctx* ctx, const float* packed, int d, int64_t n_P, int64_t n_Q, int64_t o_begin,
+                         int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st) {
+    switch (d) {
+        case 2: return run_count_x0_d<2>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st);
+        case 3: return run_count_x0_d<3>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st);
+        case 4: return run_count_x0_d<4>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st);
+        case 5: return run_count_x0_d<5>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st);
+        case 6: return run_count_x0_d<6>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st);
+    }
+    return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "x0 mode d=%d", d);
 }
 
 ddks_status launch_pack(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d, int64_t B,
@@ -450,7 +541,7 @@ ddks_status ddks_create(ddks_ctx** out, int device, int world, int rank, const v
     if (world < 1 || rank < 0 || rank >= world) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad world/rank");
     if ((world == 1) != (nccl_id == nullptr))
         return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "nccl_id must be NULL iff world == 1");
-    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT | DDKS_FLAG_PROFILE | DDKS_FLAG_PERM_GATHER)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
+    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT | DDKS_FLAG_PROFILE | DDKS_FLAG_PERM_GATHER | DDKS_FLAG_NO_X0 | DDKS_FLAG_FORCE_X0)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
     int ndev = 0;
     CU(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device %d of %d", device, ndev);
@@ -494,7 +585,8 @@ ddks_status ddks_destroy(ddks_ctx* ctx) {
                       &ctx->accum, &ctx->item_num, &ctx->bitmap, &ctx->labels, &ctx->res, &ctx->sig_hist,
                       &ctx->sig_lf, &ctx->sig_scratch, &ctx->sig_table, &ctx->sig_contrib, &ctx->sig_part,
                       &ctx->vox_keys, &ctx->vox_cnt, &ctx->vox_S, &ctx->rd_keys, &ctx->rd_xn, &ctx->rd_k0,
-                      &ctx->rd_k1, &ctx->rd_hist, &ctx->rd_tcnt, &ctx->rd_cnum})
+                      &ctx->rd_k1, &ctx->rd_hist, &ctx->rd_tcnt, &ctx->rd_cnum, &ctx->x0_keys0,
+                      &ctx->x0_keys1, &ctx->x0_hist, &ctx->x0_pts, &ctx->x0_perm})
         if (b->p) cudaFree(b->p);
     if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
     delete ctx;
@@ -552,7 +644,19 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
     float* packed = (float*)ctx->packed.p;
     if ((s = launch_pack(ctx, (const float*)dP, n_P, (const float*)dQ, n_Q, d, 1, packed, &dres->flag, st))) return s;
     uint64_t* per = (uint64_t*)ctx->per_origin.p;
-    if (oe > ob) {
+    const bool x0 = !export_mode && x0_applicable(ctx, d, n_P, n_Q);
+    if (x0) {
+        // origins are positions of the x_0 order; per-origin nums land in pooled order in per[N] (zeros elsewhere)
+        if ((s = ensure(ctx, ctx->per_origin, (size_t)N * 8))) return s;
+        per = (uint64_t*)ctx->per_origin.p;
+        if (oe > ob && (s = run_count_x0(ctx, packed, d, n_P, n_Q, ob, oe, (uint64_t*)&dres->num, per, st))) return s;
+        if (oe <= ob) CU(cudaMemsetAsync(per, 0, (size_t)N * 8, st));
+        if (ctx->world > 1) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
+        ddks::k_argmax<<<(int)std::min<int64_t>((N + 255) / 256, 148 * 4), 256, 0, st>>>(
+            per, N, 0, (const uint64_t*)&dres->num, &dres->arg);
+        CHECK_LAUNCH();
+        ctx->launches++;
+    } else if (oe > ob) {
         if ((s = run_count(ctx, packed, d, 1, n_P, n_Q, ob, oe, (uint64_t*)&dres->num, per, st))) return s;
         if (!export_mode) {
             const int64_t n = oe - ob;

@@ -45,7 +45,7 @@ template <> struct Cfg<8> { static constexpr int R = 1, T = 256, TILE = 256, S =
 
 template <int D> __host__ __device__ constexpr int padded_dim() { return D <= 4 ? 4 : 8; }
 
-template <int D, bool SPLIT> struct Geo {
+template <int D, bool SPLIT, int DPX = padded_dim<D>()> struct Geo {
     // SPLIT doubles the bins: halve R (keeping it even or 1), or T when R is already <= 2
     static constexpr int R = (SPLIT && Cfg<D>::R > 2) ? Cfg<D>::R / 2 : Cfg<D>::R;
     static constexpr int T = (SPLIT && Cfg<D>::R <= 2) ? Cfg<D>::T / 2 : Cfg<D>::T;
@@ -54,7 +54,7 @@ template <int D, bool SPLIT> struct Geo {
     static constexpr int WPB = R * T / 2;                       // counter words per bin
     static constexpr int TILE = Cfg<D>::TILE;
     static constexpr int S = Cfg<D>::S;
-    static constexpr int DP = padded_dim<D>();
+    static constexpr int DP = DPX;
     static constexpr int NQ = 1 << D;
     static constexpr int NB = NQ * (SPLIT ? 2 : 1);            // counters per origin
     static constexpr int HIST_WORDS = NB * WPB;
@@ -67,6 +67,15 @@ template <int D, bool SPLIT> struct Geo {
     __host__ __device__ static constexpr int slot(int r, int t) { return (r * T + t) % WPB; }
     __host__ __device__ static constexpr bool high(int r, int t) { return r * T + t >= WPB; }
 };
+
+// order-preserving uint32 key of a float (after -0 -> +0 canonicalisation) and its inverse
+__device__ __forceinline__ uint32_t f32_key(float f) {
+    const uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key_f32(uint32_t k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
 
 // ----------------------------------------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -188,6 +197,8 @@ struct CountArgs {
     uint64_t* item_num;      // [B] atomicMax target (direct mode)
     uint64_t* per_origin;    // [o_end - o_begin] or nullptr (direct mode, B == 1)
     int32_t* accum;          // accumulate mode: [B][NB][n_orig] int32 counters, else nullptr (direct mode)
+    const int32_t* perm;     // x0-ordered mode: perm[j] = pooled index of sorted origin j; per_origin is then a
+                             // full [N] array in pooled order (else nullptr: per_origin indexed o - o_begin)
     unsigned long long* hist;  // SPLIT only, or nullptr: hist[c_Q] += 1 for every (origin, orthant) cell (the M_T
                                // histogram of the analytic significance, ddks_significance.cuh)
 };
@@ -428,7 +439,7 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
         const int32_t oi = blk_o0 + r * T + t;
         if (oi >= a.o_end) continue;
         const uint64_t m = origin_num<D, SPLIT>(hist, r, t, a);
-        if (a.per_origin) a.per_origin[oi - a.o_begin] = m;
+        if (a.per_origin) a.per_origin[a.perm ? a.perm[oi] : oi - a.o_begin] = m;
         best = m > best ? m : best;
     }
     best = warp_max_u64(best);
@@ -439,6 +450,187 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
         uint64_t m = 0;
         for (int w = 0; w < T / 32; ++w) m = wmax[w] > m ? wmax[w] : m;
         atomicMax(reinterpret_cast<unsigned long long*>(&a.item_num[item]), (unsigned long long)m);
+    }
+}
+
+// ----------------------------------------------------------------------------------------------- x0-ordered count
+// Bit-0 elision (DESIGN.md §7 "x0 ordering"). The pooled points are reordered by x_0 (a 4-pass radix sort of
+// (key(x_0), index)); a CTA's origins are then R*T consecutive points of that order, so their x_0 values lie in
+// [o_lo, o_hi], and a whole tile of points with max x_0 < o_lo (or min x_0 >= o_hi) has the same bit 0 for every
+// pair of the CTA: bit 0 is decided once per tile and only dims 1..d-1 are compared. Tiles that overlap [o_lo, o_hi]
+// (about (R*T + 2*TILE)/N of them) take the full d compares. The counts are exactly those of k_count.
+// Sorted row layout [N][DPS]: x_0..x_{d-1}, then the point's increment for low-half and high-half counters
+// (DIFF: P -> +a, Q -> -b; the label no longer follows from the position), zero padding.
+template <int D> __host__ __device__ constexpr int sorted_dim() { return D + 2 <= 4 ? 4 : 8; }
+
+__global__ void k_x0_keys(const float* __restrict__ pts, int DP, int64_t N, uint64_t* __restrict__ keys) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        keys[i] = ((uint64_t)f32_key(pts[i * DP]) << 32) | (uint64_t)i;
+}
+
+__global__ void k_permute_sorted(const float* __restrict__ pts, int DP, int DPS, int d, int64_t N, int64_t n_P,
+                                 const uint64_t* __restrict__ keys, uint32_t incP, uint32_t incQ,
+                                 float* __restrict__ out, int32_t* __restrict__ perm) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t idx = (int64_t)(uint32_t)keys[j];
+        const uint32_t inc = idx < n_P ? incP : incQ;
+        for (int k = 0; k < DPS; ++k) {
+            float v = 0.0f;
+            if (k < d) v = pts[idx * DP + k];
+            else if (k == d) v = __uint_as_float(inc);
+            else if (k == d + 1) v = __uint_as_float(inc << 16);
+            out[j * DPS + k] = v;
+        }
+        perm[j] = (int32_t)idx;
+    }
+}
+
+template <int D, int DPS>
+__device__ __forceinline__ void load_sorted(const float* sp, float (&x)[D], uint32_t& inc_lo, uint32_t& inc_hi) {
+    float v[DPS];
+#pragma unroll
+    for (int i = 0; i < DPS; i += 4) {
+        const float4 a = *reinterpret_cast<const float4*>(sp + i);
+        v[i] = a.x, v[i + 1] = a.y, v[i + 2] = a.z, v[i + 3] = a.w;
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) x[k] = v[k];
+    inc_lo = __float_as_uint(v[D]);
+    inc_hi = __float_as_uint(v[D + 1]);
+}
+
+// dims [FIRST, D) of every point in [0, n) against this thread's R origins; base already holds bit 0's weight
+template <int D, bool GT, int FIRST, int R, int RP, int NB_, int WPB, int DPS>
+__device__ __forceinline__ void count_sorted(const float* tile, int n, const float (&o)[R][D], const float (&base)[NB_],
+                                             uint32_t ubase) {
+    float xn[D];
+    uint32_t ln, hn;
+    load_sorted<D, DPS>(tile, xn, ln, hn);
+#pragma unroll 4
+    for (int p = 0; p < n; ++p) {
+        float x[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) x[k] = xn[k];
+        const uint32_t il = ln, ih = hn;
+        load_sorted<D, DPS>(tile + (p + 1) * DPS, xn, ln, hn);  // index n <= TILE: inside the allocation, unused
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            float f = base[r % NB_];
+#pragma unroll
+            for (int k = FIRST; k < D; ++k) f = fmaf(cmp_bit<GT>(x[k], o[r][k]), (float)(4 * (1 << k) * WPB), f);
+            red_add_shared(__float_as_uint(f) + ubase, r < RP ? il : ih);
+        }
+    }
+}
+
+template <int D, bool GT>
+__global__ void __launch_bounds__(Geo<D, false, sorted_dim<D>()>::T, 1) k_count_x0(const CountArgs a) {
+    using G = Geo<D, false, sorted_dim<D>()>;
+    constexpr int R = G::R, RP = G::RP, T = G::T, DPS = G::DP, TILE = G::TILE, S = G::S, NBASE = G::NBASE,
+                  WPB = G::WPB;
+    static_assert(R >= 2, "x0-ordered mode keeps two origins of a thread per counter word");
+    extern __shared__ __align__(128) uint8_t smem[];
+    float* tiles = reinterpret_cast<float*>(smem);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + S * G::TILE_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * G::TILE_BYTES + G::HIST_WORDS * 4);
+    const int t = threadIdx.x;
+    const float* pts = a.pts;
+    const int32_t blk_o0 = a.o_begin + (int32_t)blockIdx.y * G::ORIGINS;
+    const int32_t blk_o1 = min(a.o_end, blk_o0 + G::ORIGINS);
+    const int32_t seg0 = (int32_t)blockIdx.x * a.seg_points;
+    const int32_t seg1 = min(a.N, seg0 + a.seg_points);
+    const int n_tiles = (seg1 - seg0 + TILE - 1) / TILE;
+    if (t == 0) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = t; i < G::HIST_WORDS; i += T) hist[i] = 0u;
+    __syncthreads();
+    if (t == 0) {
+        for (int s = 0; s < S && s < n_tiles; ++s) {
+            const int32_t p0 = seg0 + s * TILE;
+            const uint32_t bytes = (uint32_t)(min(TILE, seg1 - p0) * DPS * 4);
+            mbar_expect_tx(&bars[s], bytes);
+            bulk_g2s(tiles + s * TILE * DPS, pts + (int64_t)p0 * DPS, bytes, &bars[s]);
+        }
+    }
+    float o[R][D];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        int32_t oi = blk_o0 + r * T + t;
+        oi = oi < a.o_end ? oi : a.o_end - 1;
+#pragma unroll
+        for (int k = 0; k < D; ++k) o[r][k] = __ldg(pts + (int64_t)oi * DPS + k);
+    }
+    // x_0 range of this CTA's origins (sorted order: first and last)
+    const float o_lo = __ldg(pts + (int64_t)blk_o0 * DPS), o_hi = __ldg(pts + (int64_t)(blk_o1 - 1) * DPS);
+    const uint32_t ubase = smem_u32(hist) - 0x4B000000u;
+    float base0[NBASE], base1[NBASE];
+#pragma unroll
+    for (int b = 0; b < NBASE; ++b) {
+        base0[b] = __uint_as_float(0x4B000000u + 4u * (uint32_t)G::slot(b, t));
+        base1[b] = base0[b] + (float)(4 * WPB);  // + bit 0's weight (exact: integers < 2^24)
+    }
+    for (int it = 0; it < n_tiles; ++it) {
+        const int s = it % S;
+        mbar_wait(&bars[s], (uint32_t)((it / S) & 1));
+        const float* tile = tiles + s * TILE * DPS;
+        const int32_t p0 = seg0 + it * TILE;
+        const int cnt = min(TILE, seg1 - p0);
+        const float t_lo = tile[0], t_hi = tile[(cnt - 1) * DPS];
+        // bit 0 = [x_0 >= o_0] (GT: >) is uniform over the tile x origins when the value ranges do not interleave
+        const bool all0 = GT ? (t_hi <= o_lo) : (t_hi < o_lo);
+        const bool all1 = GT ? (t_lo > o_hi) : (t_lo >= o_hi);
+        if (all0)      count_sorted<D, GT, 1, R, RP, NBASE, WPB, DPS>(tile, cnt, o, base0, ubase);
+        else if (all1) count_sorted<D, GT, 1, R, RP, NBASE, WPB, DPS>(tile, cnt, o, base1, ubase);
+        else           count_sorted<D, GT, 0, R, RP, NBASE, WPB, DPS>(tile, cnt, o, base0, ubase);
+        __syncthreads();
+        if (t == 0 && it + S < n_tiles) {
+            fence_proxy_async();
+            const int32_t q0 = seg0 + (it + S) * TILE;
+            const uint32_t bytes = (uint32_t)(min(TILE, seg1 - q0) * DPS * 4);
+            mbar_expect_tx(&bars[s], bytes);
+            bulk_g2s(tiles + s * TILE * DPS, pts + (int64_t)q0 * DPS, bytes, &bars[s]);
+        }
+    }
+    __syncthreads();
+    const int32_t n_orig = a.o_end - a.o_begin;
+    if (a.accum != nullptr) {
+        int32_t* acc = a.accum;
+#pragma unroll 1
+        for (int r = 0; r < R; ++r) {
+            const int32_t oi = blk_o0 + r * T + t;
+            if (oi >= a.o_end) continue;
+            const int sl = G::slot(r, t);
+            const bool hiw = G::high(r, t);
+#pragma unroll 4
+            for (int q = 0; q < G::NB; ++q) {
+                int32_t lo, hi;
+                split16(hist[q * WPB + sl], lo, hi);
+                const int32_t v = hiw ? hi : lo;
+                if (v) atomicAdd(&acc[(int64_t)q * n_orig + (oi - a.o_begin)], v);
+            }
+        }
+        return;
+    }
+    uint64_t best = 0;
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) {
+        const int32_t oi = blk_o0 + r * T + t;
+        if (oi >= a.o_end) continue;
+        const uint64_t m = origin_num<D, false>(hist, r, t, a);
+        if (a.per_origin) a.per_origin[a.perm[oi]] = m;
+        best = m > best ? m : best;
+    }
+    best = warp_max_u64(best);
+    __shared__ uint64_t wmax[32];
+    if ((t & 31) == 0) wmax[t >> 5] = best;
+    __syncthreads();
+    if (t == 0) {
+        uint64_t m = 0;
+        for (int w = 0; w < T / 32; ++w) m = wmax[w] > m ? wmax[w] : m;
+        atomicMax(reinterpret_cast<unsigned long long*>(&a.item_num[0]), (unsigned long long)m);
     }
 }
 
@@ -473,7 +665,7 @@ __global__ void k_finalize(const CountArgs a, int64_t B) {
                 m = av > m ? av : m;
             }
         }
-        if (a.per_origin && B == 1) a.per_origin[oi] = m;
+        if (a.per_origin && B == 1) a.per_origin[a.perm ? a.perm[a.o_begin + oi] : oi] = m;
         if (B == 1) {
             best = m > best ? m : best;
         } else {

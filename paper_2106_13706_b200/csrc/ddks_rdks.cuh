@@ -16,7 +16,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-#include "ddks_vdks.cuh"  // f32_key / key_f32
+#include "ddks_kernels.cuh"  // f32_key / key_f32
 
 namespace ddks {
 

@@ -19,15 +19,9 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-namespace ddks {
+#include "ddks_kernels.cuh"  // f32_key / key_f32
 
-__device__ __forceinline__ uint32_t f32_key(float f) {  // order-preserving (after -0 -> +0 canonicalisation)
-    const uint32_t b = __float_as_uint(f);
-    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
-__device__ __forceinline__ float key_f32(uint32_t k) {
-    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
-}
+namespace ddks {
 
 // keys[0..d) = min keys (init 0xffffffff), keys[8..8+d) = max keys (init 0). pts: packed [N][DP].
 __global__ void k_minmax(const float* __restrict__ pts, int64_t n, int d, int DP, uint32_t* keys) {

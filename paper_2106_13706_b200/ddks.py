@@ -25,6 +25,8 @@ DDKS_FLAG_TIES_GT = 2
 DDKS_FLAG_FORCE_DIRECT = 4
 DDKS_FLAG_PROFILE = 8
 DDKS_FLAG_PERM_GATHER = 16
+DDKS_FLAG_NO_X0 = 32
+DDKS_FLAG_FORCE_X0 = 64
 DDKS_SIG_POISSON = 1
 
 

@@ -274,3 +274,52 @@ def test_config_c5_sampled(ctx):
     assert int(O.per_origin(P, Q, r.argmax_origin, r.argmax_origin + 1)[0]) == r.num
     # ... and no sampled origin exceeds it
     assert all(int(O.per_origin(P, Q, o, o + 1)[0]) <= r.num for o in idx[:8])
+    # the bench's x0-ordered kernel and the position-ordered kernel agree on the whole statistic (num and argmax)
+    with K.Context(flags=K.DDKS_FLAG_NO_X0) as c:
+        assert c.stat(dP, dQ) == r
+
+
+# ----------------------------------------------------------------------------------- x0-ordered count (bit-0 elision)
+
+@pytest.fixture(scope="module")
+def ctx_nox0():
+    c = K.Context(flags=K.DDKS_FLAG_NO_X0)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def ctx_x0():
+    c = K.Context(flags=K.DDKS_FLAG_FORCE_X0)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def ctx_x0_gt():
+    c = K.Context(flags=K.DDKS_FLAG_FORCE_X0 | K.DDKS_FLAG_TIES_GT)
+    yield c
+    c.close()
+
+
+X0_CASES = [(300, 200, 2, "grid"), (1500, 1300, 3, "normal"), (5000, 4000, 2, "grid"), (6000, 6000, 3, "mixed"), (4500, 5200, 4, "normal"), (9000, 7001, 5, "grid"),
+            (5000, 5000, 5, "dup"), (4096, 4096, 6, "mixed"), (20000, 1, 3, "normal"), (3, 12000, 5, "grid")]
+
+
+@pytest.mark.parametrize("n_P,n_Q,d,kind", X0_CASES)
+def test_x0_ordered_parity(ctx_x0, ctx_nox0, n_P, n_Q, d, kind):
+    # FORCE_X0 and 2 <= d <= 6 takes the x0-ordered kernel (tiles whose x_0 range does not interleave with the
+    # CTA's origins skip the dim-0 compare); tie-heavy grids put many equal x_0 values on CTA and tile boundaries
+    P, Q = I.random_pair(9100 + n_P + d, n_P, n_Q, d, kind)
+    if kind == "grid":
+        P[:, 0] = np.round(P[:, 0] * 3) / 3
+    got = check_pair(ctx_x0, P, Q)
+    assert ctx_nox0.stat(dev(P), dev(Q)) == got
+
+
+@pytest.mark.parametrize("d", [2, 5])
+def test_x0_ordered_ties_gt(ctx_x0_gt, d):
+    P, Q = I.random_pair(9300 + d, 6000, 5000, d, "grid")
+    want = O.ddks(P, Q, ties_gt=True)
+    got = ctx_x0_gt.stat(dev(P), dev(Q))
+    assert (got.num, got.den, got.argmax_origin) == (want[0], want[1], want[3])
