@@ -5,6 +5,8 @@ configuration on an origin subset via ddks_stat_per_origin, or a whole small con
     python profiles/profile_run.py C5 <o_begin> <o_end>   # C5 origin subset (same kernel, same segments)
     python profiles/profile_run.py C3|C2|C1               # full statistic
     python profiles/profile_run.py C4                     # full 4096-pair batch
+    python profiles/profile_run.py C5x0 <n>               # first n + n points of C5 through the x0-ordered kernel
+                                                          # (same k_count_x0<5> instantiation and CTA shape)
 """
 import os
 import sys
@@ -16,9 +18,17 @@ from paper_2106_13706_b200 import ddks as K  # noqa: E402
 from paper_2106_13706_b200 import inputs as I  # noqa: E402
 
 name = sys.argv[1]
-P, Q = I.config(name)
+flags = 0
+if name == "C5x0":
+    P, Q = I.config("C5")
+    n = int(sys.argv[2])
+    P, Q = P[:n].copy(), Q[:n].copy()
+    flags = K.DDKS_FLAG_FORCE_X0
+    sys.argv = sys.argv[:2]
+else:
+    P, Q = I.config(name)
 dP, dQ = torch.from_numpy(P).cuda(), torch.from_numpy(Q).cuda()
-with K.Context() as c:
+with K.Context(flags=flags) as c:
     for _ in range(2):
         if name == "C4":
             r = c.stat_batch(dP, dQ)[0]
