@@ -1062,7 +1062,8 @@ ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     const int blk = 256;
     auto grid_for = [](int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); };
     if (pe > pb) {
-        ddks::k_minmax<<<grid_for(pe - pb), blk, 0, st>>>(packed + pb * DP, pe - pb, d, DP, keys);
+        ddks::k_minmax<<<(int)std::max<int64_t>(1, std::min<int64_t>((pe - pb + 1023) / 1024, 148 * 2)), blk, 0, st>>>(
+            packed + pb * DP, pe - pb, d, DP, keys);
         CHECK_LAUNCH();
         ctx->launches++;
     }
@@ -1162,8 +1163,8 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     CU(cudaMemsetAsync(keys, 0xff, (size_t)d * 4, st));
     CU(cudaMemsetAsync(keys + d, 0, (size_t)d * 4, st));
     CU(cudaMemsetAsync(cnum, 0, (size_t)(d + 1) * 8, st));
-    ddks::k_rd_minmax<<<(int)((N + 255) / 256), 256, 0, st>>>((const float*)dP, n_P, (const float*)dQ, n_Q, d, keys,
-                                                             &dres->flag);
+    ddks::k_rd_minmax<<<(int)std::max<int64_t>(1, std::min<int64_t>((N + 1023) / 1024, 148 * 2)), 256, 0, st>>>(
+        (const float*)dP, n_P, (const float*)dQ, n_Q, d, keys, &dres->flag);
     CHECK_LAUNCH();
     ctx->launches++;
     auto grid_for = [](int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); };

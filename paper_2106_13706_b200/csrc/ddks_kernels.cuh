@@ -209,6 +209,14 @@ __device__ __forceinline__ void split16(uint32_t w, int32_t& lo, int32_t& hi) {
     hi = ((int32_t)w - lo) >> 16;
 }
 
+// hist[v] += 1 for every active lane, one atomic per distinct v in the warp (the popular small counts of the
+// significance histogram would otherwise serialise on a few addresses)
+__device__ __forceinline__ void hist_add_aggregated(unsigned long long* hist, int64_t v) {
+    const uint32_t mask = __activemask();
+    const uint32_t peers = __match_any_sync(mask, (unsigned long long)v);
+    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[v], (unsigned long long)__popc(peers));
+}
+
 // num(o) of origin r of thread t from the SMEM counters (direct mode)
 template <int D, bool SPLIT>
 __device__ __forceinline__ uint64_t origin_num(const uint32_t* hist, int r, int t, const CountArgs& a) {
@@ -228,7 +236,7 @@ __device__ __forceinline__ uint64_t origin_num(const uint32_t* hist, int r, int 
             int32_t lo2, hi2;
             split16(hist[(NQ + q) * G::WPB + sl], lo2, hi2);
             const int64_t cQ = high ? hi2 : lo2;
-            if (a.hist) atomicAdd(&a.hist[cQ], 1ull);
+            if (a.hist) hist_add_aggregated(a.hist, cQ);
             const int64_t df = (int64_t)v * a.nQ - cQ * a.nP;
             const uint64_t av = (uint64_t)(df < 0 ? -df : df);
             best = av > best ? av : best;
@@ -659,7 +667,7 @@ __global__ void k_finalize(const CountArgs a, int64_t B) {
             for (int q = 0; q < NQ; ++q) {
                 const int64_t cP = (int64_t)acc[(int64_t)q * n_orig];
                 const int64_t cQ = (int64_t)acc[(int64_t)(NQ + q) * n_orig];
-                if (a.hist) atomicAdd(&a.hist[cQ], 1ull);
+                if (a.hist) hist_add_aggregated(a.hist, cQ);
                 const int64_t df = cP * a.nQ - cQ * a.nP;
                 const uint64_t av = (uint64_t)(df < 0 ? -df : df);
                 m = av > m ? av : m;

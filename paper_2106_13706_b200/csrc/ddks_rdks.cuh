@@ -21,30 +21,37 @@
 namespace ddks {
 
 // keys[0..d) = min keys (init 0xffffffff), keys[d..2d) = max keys (init 0), as order-preserving uint32.
-// One thread per point of a 256-point tile, loop over dimensions; non-finite -> *flag |= 1.
-__global__ void k_rd_minmax(const float* __restrict__ P, int64_t n_P, const float* __restrict__ Q, int64_t n_Q, int d,
-                            uint32_t* keys, uint32_t* flag) {
+// Grid-stride over points inside each dimension, block reduction, one atomic pair per (block, dimension);
+// non-finite -> *flag |= 1.
+__global__ void __launch_bounds__(256) k_rd_minmax(const float* __restrict__ P, int64_t n_P,
+                                                   const float* __restrict__ Q, int64_t n_Q, int d, uint32_t* keys,
+                                                   uint32_t* flag) {
+    __shared__ uint32_t sa[8], sb[8];
     const int64_t N = n_P + n_Q;
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const float* row = i < n_P ? P + i * d : Q + (i - n_P) * d;
     bool bad = false;
     for (int m = 0; m < d; ++m) {
         uint32_t a = 0xffffffffu, b = 0u;
-        if (i < N) {
-            float x = row[m];
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+            float x = i < n_P ? P[i * d + m] : Q[(i - n_P) * d + m];
             bad |= !isfinite(x);
             x = x == 0.0f ? 0.0f : x;  // -0 -> +0
-            a = b = f32_key(x);
+            const uint32_t k = f32_key(x);
+            a = min(a, k);
+            b = max(b, k);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
             b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
         }
-        if ((threadIdx.x & 31) == 0) {
+        if ((threadIdx.x & 31) == 0) sa[threadIdx.x >> 5] = a, sb[threadIdx.x >> 5] = b;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < 8; ++w) a = min(a, sa[w]), b = max(b, sb[w]);
             atomicMin(&keys[m], a);
             atomicMax(&keys[d + m], b);
         }
+        __syncthreads();
     }
     if (bad) atomicOr(flag, 1u);
 }
@@ -101,15 +108,21 @@ __global__ void __launch_bounds__(RS_T) k_rs_hist(const uint64_t* __restrict__ i
 }
 
 // In place: hist -> offsets within the segment, offs[tile][dig] = sum_{d' < dig} total[d'] + sum_{t' < tile} h[t'][dig].
+// One CTA per segment, thread = digit; tiles are read 16 at a time so the loads overlap.
 __global__ void __launch_bounds__(256) k_rs_scan(uint32_t* __restrict__ hist, int tiles) {
     __shared__ uint32_t tot[256];
     const int seg = blockIdx.x, dig = threadIdx.x;
     uint32_t* h = hist + (int64_t)seg * tiles * 256;
     uint32_t run = 0;
-    for (int t = 0; t < tiles; ++t) {
-        const uint32_t v = h[t * 256 + dig];
-        h[t * 256 + dig] = run;
-        run += v;
+    for (int t0 = 0; t0 < tiles; t0 += 16) {
+        uint32_t v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = t0 + j < tiles ? h[(t0 + j) * 256 + dig] : 0u;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if (t0 + j < tiles) h[(t0 + j) * 256 + dig] = run;
+            run += v[j];
+        }
     }
     tot[dig] = run;
     __syncthreads();
@@ -127,11 +140,15 @@ __global__ void __launch_bounds__(256) k_rs_scan(uint32_t* __restrict__ hist, in
 }
 
 // Stable scatter of one tile: warp w ranks its 512 keys (rounds of 32, in tile order) with __match_any_sync and a
-// per-warp digit counter; warps are then ordered by an exclusive scan of their counters per digit.
+// per-warp digit counter; warps are then ordered by an exclusive scan of their counters per digit. The tile is
+// first regrouped by digit in SMEM (local position = tile digit base + warp offset + rank) and then written out
+// with consecutive threads on consecutive addresses of each digit's run (coalesced).
 __global__ void __launch_bounds__(RS_T) k_rs_scatter(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
                                                      int64_t N, int tiles, int shift,
                                                      const uint32_t* __restrict__ offs) {
     __shared__ uint32_t wc[RS_WARPS][256];
+    __shared__ uint32_t dbase[256];   // exclusive scan of the tile's digit counts
+    __shared__ uint64_t stage[RS_TILE];
     const int seg = blockIdx.x / tiles, tile = blockIdx.x - seg * tiles;
     const int64_t sbase = (int64_t)seg * N;
     const int64_t base = sbase + (int64_t)tile * RS_TILE;
@@ -166,12 +183,28 @@ __global__ void __launch_bounds__(RS_T) k_rs_scatter(const uint64_t* __restrict_
             wc[ww][threadIdx.x] = run;
             run += v;
         }
+        dbase[threadIdx.x] = run;  // this digit's count in the tile
     }
     __syncthreads();
-    const uint32_t* o = offs + (int64_t)blockIdx.x * 256;
+    if (threadIdx.x == 0) {
+        uint32_t r = 0;
+        for (int i = 0; i < 256; ++i) {
+            const uint32_t v = dbase[i];
+            dbase[i] = r;
+            r += v;
+        }
+    }
+    __syncthreads();
 #pragma unroll
     for (int j = 0; j < RS_ITEMS; ++j)
-        if (dg[j] < 256u) out[sbase + o[dg[j]] + wc[w][dg[j]] + rank[j]] = k[j];
+        if (dg[j] < 256u) stage[dbase[dg[j]] + wc[w][dg[j]] + rank[j]] = k[j];
+    __syncthreads();
+    const uint32_t* o = offs + (int64_t)blockIdx.x * 256;
+    for (int i = threadIdx.x; i < n; i += RS_T) {
+        const uint64_t key = stage[i];
+        const uint32_t dig = (uint32_t)(key >> shift) & 255u;
+        out[sbase + o[dig] + (uint32_t)i - dbase[dig]] = key;
+    }
 }
 
 // ------------------------------------------------------------------------------------ GetDFromCornerLists sweep

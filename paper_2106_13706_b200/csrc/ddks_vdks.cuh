@@ -24,7 +24,9 @@
 namespace ddks {
 
 // keys[0..d) = min keys (init 0xffffffff), keys[8..8+d) = max keys (init 0). pts: packed [N][DP].
-__global__ void k_minmax(const float* __restrict__ pts, int64_t n, int d, int DP, uint32_t* keys) {
+// Grid-stride per thread, block reduction in SMEM, one atomic pair per (block, dimension).
+__global__ void __launch_bounds__(256) k_minmax(const float* __restrict__ pts, int64_t n, int d, int DP, uint32_t* keys) {
+    __shared__ uint32_t sa[8][8], sb[8][8];
     uint32_t mn[8], mx[8];
 #pragma unroll
     for (int m = 0; m < 8; ++m) mn[m] = 0xffffffffu, mx[m] = 0u;
@@ -39,17 +41,21 @@ __global__ void k_minmax(const float* __restrict__ pts, int64_t n, int d, int DP
     }
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
-        if (m >= d) break;
         uint32_t a = mn[m], b = mx[m];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
             b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
         }
-        if ((threadIdx.x & 31) == 0) {
-            atomicMin(&keys[m], a);
-            atomicMax(&keys[8 + m], b);
-        }
+        if ((threadIdx.x & 31) == 0) sa[threadIdx.x >> 5][m] = a, sb[threadIdx.x >> 5][m] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x < d) {
+        const int m = threadIdx.x;
+        uint32_t a = 0xffffffffu, b = 0u;
+        for (int w = 0; w < 8; ++w) a = min(a, sa[w][m]), b = max(b, sb[w][m]);
+        atomicMin(&keys[m], a);
+        atomicMax(&keys[8 + m], b);
     }
 }
 
