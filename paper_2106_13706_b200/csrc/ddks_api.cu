@@ -332,7 +332,7 @@ ddks_status run_count_x0_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     uint64_t *src = k0, *dst = k1;
     for (int shift = 32; shift < 64; shift += 8) {
         ddks::k_rs_hist<<<tiles, ddks::RS_T, 0, st>>>(src, N, tiles, shift, hist);
-        ddks::k_rs_scan<<<1, 256, 0, st>>>(hist, tiles);
+        ddks::k_rs_scan<<<1, 256 * ddks::RS_SCAN_PARTS, 0, st>>>(hist, tiles);
         ddks::k_rs_scatter<<<tiles, ddks::RS_T, 0, st>>>(src, dst, N, tiles, shift, hist);
         CHECK_LAUNCH();
         ctx->launches += 3;
@@ -1179,7 +1179,7 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
         uint64_t *src = k0, *dst = k1;
         for (int shift = 0; shift < 64; shift += 8) {
             ddks::k_rs_hist<<<blocks, ddks::RS_T, 0, st>>>(src, N, tiles, shift, hist);
-            ddks::k_rs_scan<<<nc, 256, 0, st>>>(hist, tiles);
+            ddks::k_rs_scan<<<nc, 256 * ddks::RS_SCAN_PARTS, 0, st>>>(hist, tiles);
             ddks::k_rs_scatter<<<blocks, ddks::RS_T, 0, st>>>(src, dst, N, tiles, shift, hist);
             CHECK_LAUNCH();
             ctx->launches += 3;

@@ -93,6 +93,34 @@ __global__ void k_rd_keys(const double* __restrict__ xn, int64_t N, int64_t n_P,
 // ------------------------------------------------------------------------------------ segmented LSD radix sort
 constexpr int RS_T = 256, RS_ITEMS = 16, RS_TILE = RS_T * RS_ITEMS, RS_WARPS = RS_T / 32;
 
+// Exclusive scan over a 256-thread block (one value per thread; warp shuffles + one warp over the 8 warp totals).
+// *total (if given) receives the block sum. Contains __syncthreads().
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t* total = nullptr) {
+    __shared__ uint32_t wsum[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    __syncthreads();
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t s = lane < 8 ? wsum[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < 8) wsum[lane] = s;  // inclusive warp-total prefix
+    }
+    __syncthreads();
+    if (total) *total = wsum[7];
+    return x - v + (w ? wsum[w - 1] : 0u);
+}
+
 // hist[(seg * tiles + tile) * 256 + digit]
 __global__ void __launch_bounds__(RS_T) k_rs_hist(const uint64_t* __restrict__ in, int64_t N, int tiles, int shift,
                                                   uint32_t* __restrict__ hist) {
@@ -108,35 +136,65 @@ __global__ void __launch_bounds__(RS_T) k_rs_hist(const uint64_t* __restrict__ i
 }
 
 // In place: hist -> offsets within the segment, offs[tile][dig] = sum_{d' < dig} total[d'] + sum_{t' < tile} h[t'][dig].
-// One CTA per segment, thread = digit; tiles are read 16 at a time so the loads overlap.
-__global__ void __launch_bounds__(256) k_rs_scan(uint32_t* __restrict__ hist, int tiles) {
-    __shared__ uint32_t tot[256];
-    const int seg = blockIdx.x, dig = threadIdx.x;
+// One CTA of 1024 threads per segment: thread (part, dig) owns a quarter of the tiles of one digit; tiles are read
+// 16 at a time so the loads overlap.
+constexpr int RS_SCAN_PARTS = 4;
+__global__ void __launch_bounds__(256 * RS_SCAN_PARTS) k_rs_scan(uint32_t* __restrict__ hist, int tiles) {
+    __shared__ uint32_t pt[RS_SCAN_PARTS][256];
+    __shared__ uint32_t dbase[256];
+    __shared__ uint32_t wtot[8];
+    const int seg = blockIdx.x, dig = threadIdx.x & 255, part = threadIdx.x >> 8;
+    const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & 7;
     uint32_t* h = hist + (int64_t)seg * tiles * 256;
+    const int per = (tiles + RS_SCAN_PARTS - 1) / RS_SCAN_PARTS;
+    const int t_begin = min(tiles, part * per), t_end = min(tiles, t_begin + per);
     uint32_t run = 0;
-    for (int t0 = 0; t0 < tiles; t0 += 16) {
+    for (int t0 = t_begin; t0 < t_end; t0 += 16) {
         uint32_t v[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = t0 + j < tiles ? h[(t0 + j) * 256 + dig] : 0u;
+        for (int j = 0; j < 16; ++j) v[j] = t0 + j < t_end ? h[(t0 + j) * 256 + dig] : 0u;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            if (t0 + j < tiles) h[(t0 + j) * 256 + dig] = run;
-            run += v[j];
-        }
+        for (int j = 0; j < 16; ++j) run += v[j];
     }
-    tot[dig] = run;
+    pt[part][dig] = run;
     __syncthreads();
-    if (dig == 0) {
+    uint32_t tot = 0, x = 0;
+    if (part == 0) {
+#pragma unroll
+        for (int p = 0; p < RS_SCAN_PARTS; ++p) tot += pt[p][dig];
+        x = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wtot[w] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
         uint32_t r = 0;
-        for (int i = 0; i < 256; ++i) {
-            const uint32_t v = tot[i];
-            tot[i] = r;
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t v = wtot[i];
+            wtot[i] = r;
             r += v;
         }
     }
     __syncthreads();
-    const uint32_t b = tot[dig];
-    for (int t = 0; t < tiles; ++t) h[t * 256 + dig] += b;
+    if (part == 0) dbase[dig] = x - tot + wtot[w];
+    __syncthreads();
+    run = dbase[dig];
+    for (int p = 0; p < part; ++p) run += pt[p][dig];
+    for (int t0 = t_begin; t0 < t_end; t0 += 16) {
+        uint32_t v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = t0 + j < t_end ? h[(t0 + j) * 256 + dig] : 0u;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (t0 + j < t_end) {
+                h[(t0 + j) * 256 + dig] = run;
+                run += v[j];
+            }
+    }
 }
 
 // Stable scatter of one tile: warp w ranks its 512 keys (rounds of 32, in tile order) with __match_any_sync and a
@@ -183,16 +241,7 @@ __global__ void __launch_bounds__(RS_T) k_rs_scatter(const uint64_t* __restrict_
             wc[ww][threadIdx.x] = run;
             run += v;
         }
-        dbase[threadIdx.x] = run;  // this digit's count in the tile
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t r = 0;
-        for (int i = 0; i < 256; ++i) {
-            const uint32_t v = dbase[i];
-            dbase[i] = r;
-            r += v;
-        }
+        dbase[threadIdx.x] = block_excl_scan256(run);  // exclusive scan of the tile's digit counts
     }
     __syncthreads();
 #pragma unroll
@@ -232,8 +281,6 @@ __global__ void __launch_bounds__(RS_T) k_rd_count(const uint64_t* __restrict__ 
 __global__ void __launch_bounds__(RS_T) k_rd_sweep(const uint64_t* __restrict__ key, int64_t N, int tiles,
                                                    int64_t n_P, int64_t n_Q, const uint32_t* __restrict__ tcnt,
                                                    unsigned long long* __restrict__ cnum) {
-    __shared__ uint32_t red[RS_T];
-    __shared__ int64_t before;
     const int seg = blockIdx.x / tiles, tile = blockIdx.x - seg * tiles;
     const int64_t sbase = (int64_t)seg * N;
     const int64_t p0 = (int64_t)tile * RS_TILE;
@@ -241,13 +288,8 @@ __global__ void __launch_bounds__(RS_T) k_rd_sweep(const uint64_t* __restrict__ 
     // P keys in earlier tiles of this segment
     uint32_t c = 0;
     for (int t = threadIdx.x; t < tile; t += RS_T) c += tcnt[(int64_t)seg * tiles + t];
-    red[threadIdx.x] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int64_t s = 0;
-        for (int i = 0; i < RS_T; ++i) s += red[i];
-        before = s;
-    }
+    uint32_t before = 0;
+    block_excl_scan256(c, &before);
     // blocked arrangement: thread t owns positions [t * ITEMS, t * ITEMS + ITEMS) of the tile
     uint64_t k[RS_ITEMS];
     uint32_t mine = 0;
@@ -257,19 +299,8 @@ __global__ void __launch_bounds__(RS_T) k_rd_sweep(const uint64_t* __restrict__ 
         k[j] = idx < n ? key[sbase + p0 + idx] : ~0ull;
         mine += (uint32_t)(idx < n && (k[j] & 1ull) == 0);
     }
-    __syncthreads();
-    red[threadIdx.x] = mine;
-    __syncthreads();
-    if (threadIdx.x == 0) {  // exclusive scan of the per-thread P counts (256 entries)
-        uint32_t r = 0;
-        for (int i = 0; i < RS_T; ++i) {
-            const uint32_t v = red[i];
-            red[i] = r;
-            r += v;
-        }
-    }
-    __syncthreads();
-    int64_t iP = before + red[threadIdx.x];
+    const uint32_t mine_before = block_excl_scan256(mine);
+    int64_t iP = (int64_t)before + mine_before;
     uint64_t best = 0;
 #pragma unroll
     for (int j = 0; j < RS_ITEMS; ++j) {
