@@ -287,8 +287,19 @@ int64_t oracle_voxel_index(const double* xn, int d, int64_t k)
  *   for every filled voxel v: SumOrthants(Diff at v) = for every voxel u, orthant bit m = [u_m >= v_m] (the voxel
  *   itself in the all->= orthant, as Eq. 3 puts the origin; R16), sums[code] += diff[u]; TmpD = max_code |sums|;
  *   D = max over filled voxels. num = max |sum|, den = n_P n_Q, D = num / den. Returns 0 on success. */
+int oracle_vdks_voxels(const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d, int64_t k,
+                       int64_t v_begin, int64_t v_end, uint64_t* num, uint64_t* den, double* D);
+
 int oracle_vdks(const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d, int64_t k,
                 uint64_t* num, uint64_t* den, double* D)
+{
+    return oracle_vdks_voxels(P, n_P, Q, n_Q, d, k, 0, -1, num, den, D);
+}
+
+/* As oracle_vdks, with the max taken over the filled voxels of flat index range [v_begin, v_end) only (v_end < 0:
+ * all); used by the multi-rank tests to check the voxel-sharded combine. */
+int oracle_vdks_voxels(const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d, int64_t k,
+                       int64_t v_begin, int64_t v_end, uint64_t* num, uint64_t* den, double* D)
 {
     if (d < 1 || d > 20 || n_P < 1 || n_Q < 1 || k < 1) return 1;
     int64_t N = n_P + n_Q, V = 1;
@@ -311,7 +322,7 @@ int oracle_vdks(const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d,
         int64_t* vc = (int64_t*)malloc(sizeof(int64_t) * (size_t)d);
         int64_t* uc = (int64_t*)malloc(sizeof(int64_t) * (size_t)d);
 #pragma omp for schedule(dynamic, 8) reduction(max : best)
-        for (int64_t v = 0; v < V; ++v) {
+        for (int64_t v = v_begin; v < (v_end < 0 ? V : (v_end < V ? v_end : V)); ++v) {
             if (cP[v] + cQ[v] == 0) continue;  /* not a filled voxel */
             for (int64_t q = 0; q < nq; ++q) sums[q] = 0;
             int64_t r = v;
@@ -366,22 +377,33 @@ static int cmp_double(const void* a, const void* b)
  * axis corners ("(0,0,0), (1,0,0), (0,1,0), (0,0,1)"); for each corner c: Euclidean distances
  * sqrt(sum_m (x'_m - c_m)^2) (summed m = 0..d-1) of P's and T's points, each list sorted, then
  * GetDFromCornerLists; D = max over corners. num/den as above; *arg_corner = first corner attaining num. */
+int oracle_rdks_corners(const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d, int64_t c_begin,
+                        int64_t c_end, uint64_t* num, uint64_t* den, double* D, int64_t* arg_corner);
+
 int oracle_rdks(const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d,
                 uint64_t* num, uint64_t* den, double* D, int64_t* arg_corner)
+{
+    return oracle_rdks_corners(P, n_P, Q, n_Q, d, 0, d + 1, num, den, D, arg_corner);
+}
+
+/* As oracle_rdks over corners [c_begin, c_end) only (multi-rank tests: corner-sharded combine); *arg_corner = -1 if
+ * the range is empty. */
+int oracle_rdks_corners(const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d, int64_t c_begin,
+                        int64_t c_end, uint64_t* num, uint64_t* den, double* D, int64_t* arg_corner)
 {
     if (d < 1 || n_P < 1 || n_Q < 1) return 1;
     int64_t N = n_P + n_Q;
     double* xn = (double*)malloc(sizeof(double) * (size_t)(N * d));
     oracle_normalize_pair(P, n_P, Q, n_Q, d, xn);
     uint64_t best = 0;
-    int64_t arg = 0;
+    int64_t arg = c_begin < c_end ? c_begin : -1;
 #pragma omp parallel
     {
         double* dP = (double*)malloc(sizeof(double) * (size_t)n_P);
         double* dQ = (double*)malloc(sizeof(double) * (size_t)n_Q);
         double* c = (double*)malloc(sizeof(double) * (size_t)d);
 #pragma omp for schedule(dynamic, 1)
-        for (int64_t ci = 0; ci <= d; ++ci) {
+        for (int64_t ci = c_begin; ci < c_end; ++ci) {
             for (int m = 0; m < d; ++m) c[m] = (ci >= 1 && m == ci - 1) ? 1.0 : 0.0;
             for (int64_t i = 0; i < N; ++i) {
                 double s = 0.0;

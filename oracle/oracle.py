@@ -84,6 +84,10 @@ def _load():
         lib.oracle_vdks.restype = c_int
         lib.oracle_merged_max_diff.argtypes = [c_p, c_i64, c_p, c_i64]
         lib.oracle_merged_max_diff.restype = ctypes.c_uint64
+        lib.oracle_vdks_voxels.argtypes = [c_p, c_i64, c_p, c_i64, c_int, c_i64, c_i64, c_i64, c_p, c_p, c_p]
+        lib.oracle_vdks_voxels.restype = c_int
+        lib.oracle_rdks_corners.argtypes = [c_p, c_i64, c_p, c_i64, c_int, c_i64, c_i64, c_p, c_p, c_p, c_p]
+        lib.oracle_rdks_corners.restype = c_int
         lib.oracle_rdks.argtypes = [c_p, c_i64, c_p, c_i64, c_int, c_p, c_p, c_p, c_p]
         lib.oracle_rdks.restype = c_int
         _lib = lib
@@ -203,12 +207,13 @@ def voxel_index(xn, k: int) -> int:
     return int(_load().oracle_voxel_index(_ptr(x), x.size, k))
 
 
-def vdks(P, Q, k: int):
-    """vdKS, Alg. 1 -> (num, den, D) with D = num / den exactly as in ddks()."""
+def vdks(P, Q, k: int, v_begin: int = 0, v_end: int = -1):
+    """vdKS, Alg. 1 -> (num, den, D) with D = num / den exactly as in ddks().
+    [v_begin, v_end): restrict the max to filled voxels of that flat-index range (multi-rank tests)."""
     P, Q = _f32(P), _f32(Q)
     num, den, D = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_double()
-    rc = _load().oracle_vdks(_ptr(P), P.shape[0], _ptr(Q), Q.shape[0], P.shape[1], k, ctypes.byref(num),
-                             ctypes.byref(den), ctypes.byref(D))
+    rc = _load().oracle_vdks_voxels(_ptr(P), P.shape[0], _ptr(Q), Q.shape[0], P.shape[1], k, v_begin, v_end,
+                                    ctypes.byref(num), ctypes.byref(den), ctypes.byref(D))
     if rc:
         raise ValueError(f"oracle_vdks rc={rc}")
     return int(num.value), int(den.value), float(D.value)
@@ -221,12 +226,13 @@ def merged_max_diff(c1, c2) -> int:
     return int(_load().oracle_merged_max_diff(_ptr(a), a.size, _ptr(b), b.size))
 
 
-def rdks(P, Q):
-    """rdKS, Alg. 2 (P:L158-202) -> (num, den, D, arg_corner)."""
+def rdks(P, Q, c_begin: int = 0, c_end: int | None = None):
+    """rdKS, Alg. 2 -> (num, den, D, arg_corner); [c_begin, c_end): corner subset (multi-rank tests)."""
     P, Q = _f32(P), _f32(Q)
+    c_end = P.shape[1] + 1 if c_end is None else c_end
     num, den, D, arg = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_double(), ctypes.c_int64()
-    rc = _load().oracle_rdks(_ptr(P), P.shape[0], _ptr(Q), Q.shape[0], P.shape[1], ctypes.byref(num),
-                             ctypes.byref(den), ctypes.byref(D), ctypes.byref(arg))
+    rc = _load().oracle_rdks_corners(_ptr(P), P.shape[0], _ptr(Q), Q.shape[0], P.shape[1], c_begin, c_end,
+                                     ctypes.byref(num), ctypes.byref(den), ctypes.byref(D), ctypes.byref(arg))
     if rc:
         raise ValueError(f"oracle_rdks rc={rc}")
     return int(num.value), int(den.value), float(D.value), int(arg.value)

@@ -1,7 +1,9 @@
 """Multi-rank host logic on CPU (gloo, world_size 2): the sharding the library uses (ddks_shard_range, a
 host-only C-ABI call) and the combine semantics it implements with NCCL — all-reduce(max) of num, then
-all-reduce(min) of the argmax candidates for ddks_stat; contiguous item shards + all-gather for batch and
-permutation calls — reproduce the single-rank oracle result exactly. Per-rank partial results come from the
+all-reduce(min) of the argmax candidates for ddks_stat (position-ordered and x0-ordered origin shards);
+contiguous item shards + all-gather for batch and permutation calls; histogram all-reduce(sum) + sharded table +
+rank-ordered partial sums for the significance; voxel shards (vdKS) and corner shards (rdKS) with max / min-index
+combines — reproduce the single-rank oracle result. Per-rank partial results come from the
 oracle restricted to the rank's shard (there is no GPU here); on a GPU box the same shards run in k_count."""
 import os
 import socket
@@ -68,6 +70,61 @@ def _worker(rank, world, port, q):
             rb, re = K.ddks_shard_range(B, world, r)
             full += gathered[r][: re - rb].tolist()
         out["batch"] = full
+
+        # ---- x0-ordered ddks_stat: ranks shard POSITIONS of the x_0 order (ties keep pooled order); each rank's
+        # per-origin nums land in a zeroed pooled-order array; max, then argmax over the full array, min over ranks
+        P, Q = I.random_pair(733, 90, 70, 4, "grid")
+        pooled = np.concatenate([P, Q])
+        N = pooled.shape[0]
+        order = np.lexsort((np.arange(N), pooled[:, 0]))  # key x_0, then pooled index
+        b, e = K.ddks_shard_range(N, world, rank)
+        per_full = np.zeros(N, np.uint64)
+        for j in range(b, e):
+            o = int(order[j])
+            per_full[o] = O.per_origin(P, Q, o, o + 1)[0]
+        t = torch.tensor([int(per_full.max())], dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        num = int(t.item())
+        hit = np.nonzero(per_full == num)[0]
+        a = torch.tensor([int(hit[0]) if hit.size else 2**62], dtype=torch.int64)
+        dist.all_reduce(a, op=dist.ReduceOp.MIN)
+        out["x0"] = (num, int(a.item()))
+
+        # ---- ddks_significance: origins sharded -> M_T histogram all-reduce(sum); table entries sharded; partial
+        # sums all-gathered and added in rank order
+        P, Q = I.random_pair(741, 30, 25, 2, "normal")
+        pooled = np.concatenate([P, Q])
+        N, n_Q = pooled.shape[0], Q.shape[0]
+        b, e = K.ddks_shard_range(N, world, rank)
+        MT = O.membership(Q, pooled[b:e]) if e > b else np.zeros((0, 4), np.int64)
+        h = torch.from_numpy(np.bincount(MT.ravel(), minlength=n_Q + 1).astype(np.int64))
+        dist.all_reduce(h, op=dist.ReduceOp.SUM)
+        num = O.ddks(P, Q)[0]
+        mb, me = K.ddks_shard_range(n_Q + 1, world, rank)
+        part = sum(int(h[m]) * np.log(O.p_le(num, P.shape[0], n_Q, (m + 1.0) / (n_Q + 2.0)))
+                   for m in range(mb, me) if int(h[m]) > 0)
+        parts = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.tensor([float(part)], dtype=torch.float64))
+        out["sig"] = (h.tolist(), sum(float(x.item()) for x in parts))
+
+        # ---- ddks_vdks: voxel counts all-reduced, voxels sharded, max combine
+        P, Q = I.random_pair(751, 60, 50, 3, "mixed")
+        k = 4
+        vb, ve = K.ddks_shard_range(k ** 3, world, rank)
+        t = torch.tensor([O.vdks(P, Q, k, vb, ve)[0]], dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out["vdks"] = int(t.item())
+
+        # ---- ddks_rdks: corners sharded, max + first attaining corner
+        P, Q = I.random_pair(761, 60, 50, 4, "normal")
+        cb, ce = K.ddks_shard_range(5, world, rank)
+        r = O.rdks(P, Q, cb, ce)
+        t = torch.tensor([r[0]], dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        num = int(t.item())
+        a = torch.tensor([r[3] if (ce > cb and r[0] == num) else 2**62], dtype=torch.int64)
+        dist.all_reduce(a, op=dist.ReduceOp.MIN)
+        out["rdks"] = (num, int(a.item()))
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -100,6 +157,23 @@ def test_sharded_combine_equals_single_rank(world):
     want = O.batch(Pb, Qb).tolist()
     for r in range(world):
         assert res[r]["batch"] == want
+    # x0-ordered sharding == single-rank statistic and argmax
+    P, Q = I.random_pair(733, 90, 70, 4, "grid")
+    num, den, D, arg = O.ddks(P, Q)
+    # significance: the summed histogram is the single-rank one, and the sharded sum of logs matches the oracle
+    Ps, Qs = I.random_pair(741, 30, 25, 2, "normal")
+    S, lp, _ = O.significance(Ps, Qs)
+    pooled = np.concatenate([Ps, Qs])
+    h_full = np.bincount(O.membership(Qs, pooled).ravel(), minlength=Qs.shape[0] + 1).tolist()
+    for r in range(world):
+        assert res[r]["x0"] == (num, arg)
+        assert res[r]["sig"][0] == h_full
+        assert abs(res[r]["sig"][1] - lp) <= 1e-9 * max(1.0, abs(lp))
+        Pv, Qv = I.random_pair(751, 60, 50, 3, "mixed")
+        assert res[r]["vdks"] == O.vdks(Pv, Qv, 4)[0]
+        Pr, Qr = I.random_pair(761, 60, 50, 4, "normal")
+        want_r = O.rdks(Pr, Qr)
+        assert res[r]["rdks"] == (want_r[0], want_r[3])
 
 
 def test_bench_reference_arm_under_torchrun_cpu():
