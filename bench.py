@@ -191,7 +191,7 @@ class Step:
             def call(P, Q, pooled, perms):
                 r = ctx.stat_batch(P, Q)
                 null, obs, pv = ctx.permutation_null(pooled, n, perms)
-                return (tuple(x.num for x in r), tuple(int(v) for v in null), obs.num, pv)
+                return (r.num.tobytes(), null.tobytes(), obs.num, pv)
             self.call = call
             self.d2h = B * 32 + perms.shape[0] * 8 + 8
         else:
@@ -366,8 +366,9 @@ def main():
             result = {k: (v._asdict() if hasattr(v, "_asdict") else v) for k, v in res._asdict().items()
                       if k not in ("mt_hist", "log_p_table")}
         else:
-            result = {"batch_num_sum": int(sum(res[0])), "null_num_max": int(max(res[1])), "observed_num": res[2],
-                      "p_value": res[3]}
+            bn, nn = np.frombuffer(res[0], np.uint64), np.frombuffer(res[1], np.uint64)
+            result = {"batch_num_sum": int(bn.sum()), "batch_num_max": int(bn.max()), "null_num_max": int(nn.max()),
+                      "null_num_sum": int(nn.sum()), "observed_num": res[2], "p_value": res[3]}
         line = {
             "metric": step.metric, "value": value, "unit": step.unit, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps, "higher_is_better": True,

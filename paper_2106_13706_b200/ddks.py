@@ -181,14 +181,41 @@ def ddks_stat(ctx, P, Q, stream=None) -> Result:
     return Result(r.num, r.den, r.D, r.argmax_origin)
 
 
-def ddks_stat_batch(ctx, P, Q, stream=None) -> list[Result]:
+_RESULT_DTYPE = np.dtype([("num", "<u8"), ("den", "<u8"), ("D", "<f8"), ("argmax_origin", "<i8")])
+
+
+class BatchResult:
+    """The B ddks_result structs the C call wrote, viewed as NumPy columns without per-item Python objects
+    (``.num``, ``.den``, ``.D``, ``.argmax_origin``); indexing / iterating yields ``Result`` tuples."""
+
+    def __init__(self, arr: np.ndarray):
+        self.arr = arr
+        self.num, self.den, self.D, self.argmax_origin = (arr[f] for f in _RESULT_DTYPE.names)
+
+    def __len__(self):
+        return len(self.arr)
+
+    def __getitem__(self, i) -> Result:
+        r = self.arr[i]
+        return Result(int(r["num"]), int(r["den"]), float(r["D"]), int(r["argmax_origin"]))
+
+    def __iter__(self):
+        return (self[i] for i in range(len(self)))
+
+    def __eq__(self, other):
+        return isinstance(other, BatchResult) and self.arr.tobytes() == other.arr.tobytes()
+
+
+def ddks_stat_batch(ctx, P, Q, stream=None) -> BatchResult:
     p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
     if len(p.shape) != 3 or len(q.shape) != 3 or p.shape[0] != q.shape[0] or p.shape[2] != q.shape[2]:
         raise ValueError(f"P {p.shape} and Q {q.shape} must be [B, n, d] with the same B and d")
     B = p.shape[0]
-    out = (ddks_result * B)()
-    _check(LIB.ddks_stat_batch(ctx, p.ptr, q.ptr, B, p.shape[1], q.shape[1], p.shape[2], _stream(stream), out), ctx)
-    return [Result(o.num, o.den, o.D, o.argmax_origin) for o in out]
+    arr = np.zeros(B, dtype=_RESULT_DTYPE)
+    assert _RESULT_DTYPE.itemsize == ctypes.sizeof(ddks_result)
+    _check(LIB.ddks_stat_batch(ctx, p.ptr, q.ptr, B, p.shape[1], q.shape[1], p.shape[2], _stream(stream),
+                               arr.ctypes.data_as(ctypes.POINTER(ddks_result))), ctx)
+    return BatchResult(arr)
 
 
 def ddks_permutation_null(ctx, pooled, n_P: int, perms, stream=None):
@@ -272,7 +299,7 @@ class Context:
     def stat(self, P, Q, stream=None) -> Result:
         return ddks_stat(self.ctx, P, Q, stream)
 
-    def stat_batch(self, P, Q, stream=None) -> list[Result]:
+    def stat_batch(self, P, Q, stream=None) -> BatchResult:
         return ddks_stat_batch(self.ctx, P, Q, stream)
 
     def permutation_null(self, pooled, n_P, perms, stream=None):
