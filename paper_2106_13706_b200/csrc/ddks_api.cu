@@ -159,9 +159,9 @@ struct CountPlan {
 
 template <int D, bool SPLIT, bool GT, bool X0 = false>
 ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a, cudaStream_t st) {
-    using G = std::conditional_t<X0, ddks::Geo<D, false, ddks::sorted_dim<D>()>, ddks::Geo<D, SPLIT>>;
+    using G = std::conditional_t<X0, ddks::GeoX0<D, SPLIT>, ddks::Geo<D, SPLIT>>;
     void (*kern)(const ddks::CountArgs) = nullptr;
-    if constexpr (X0) kern = ddks::k_count_x0<D, GT>;
+    if constexpr (X0) kern = ddks::k_count_x0<D, SPLIT, GT>;
     else kern = ddks::k_count<D, SPLIT, GT>;
     static bool attr_done = false;  // per-process; device attributes are per function
     if (!attr_done) {
@@ -305,12 +305,14 @@ ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int6
     return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "d=%d", d);
 }
 
-// x0-ordered statistic (B == 1, DIFF counters, 2 <= d <= 6): sort the packed points by x_0, build the sorted rows
-// (coordinates + per-point increments), count with bit-0 elision (k_count_x0), per-origin nums scattered back to
-// pooled order into per_origin[N] (zeroed here). Origins [o_begin, o_end) are positions in the SORTED order.
+// x0-ordered statistic (B == 1, 2 <= d <= 8): sort the packed points by x_0, build the sorted rows (coordinates + the
+// per-point increment / bin offset), count with bit-0 elision (k_count_x0), per-origin nums scattered back to pooled
+// order into per_origin[N] (zeroed here). Origins [o_begin, o_end) are positions in the SORTED order. split + hist:
+// SPLIT counters and the significance's M_T histogram (as run_count).
 template <int D>
 ddks_status run_count_x0_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int64_t n_Q, int64_t o_begin,
-                           int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st) {
+                           int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st, bool split,
+                           unsigned long long* hist_out) {
     constexpr int DPS = ddks::sorted_dim<D>();
     const int64_t N = n_P + n_Q;
     const int DP = pad_dim(D);
@@ -341,14 +343,24 @@ ddks_status run_count_x0_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     const uint64_t gg = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
     const uint32_t a_ = (uint32_t)((uint64_t)n_Q / gg), b_ = (uint32_t)((uint64_t)n_P / gg);
     float* spts = (float*)ctx->x0_pts.p;
-    ddks::k_permute_sorted<<<g, 256, 0, st>>>(packed, DP, DPS, D, N, n_P, src, a_, 0u - b_, spts,
+    uint32_t vP, vP2, vQ, vQ2;
+    if (split) {  // bin-block byte offset as a float: P -> 0, Q -> 4 * NQ * WPB
+        using G = ddks::GeoX0<D, true>;
+        const float off = (float)(4 * G::NQ * G::WPB);
+        uint32_t ob;
+        memcpy(&ob, &off, 4);
+        vP = 0u, vP2 = 0u, vQ = ob, vQ2 = 0u;
+    } else {      // DIFF increments for low / high 16-bit halves
+        vP = a_, vP2 = a_ << 16, vQ = 0u - b_, vQ2 = (0u - b_) << 16;
+    }
+    ddks::k_permute_sorted<<<g, 256, 0, st>>>(packed, DP, DPS, D, N, n_P, src, vP, vP2, vQ, vQ2, spts,
                                               (int32_t*)ctx->x0_perm.p);
     CHECK_LAUNCH();
     ctx->launches++;
     CU(cudaMemsetAsync(spts + N * DPS, 0, 2 * DPS * 4, st));  // the prefetch past the last point reads zeros
     CU(cudaMemsetAsync(per_origin, 0, (size_t)N * 8, st));
-    CountPlan pl{1, (int32_t)N, (int32_t)n_P, (int32_t)o_begin, (int32_t)o_end, n_P, n_Q, false,
-                 (int64_t)(32767 / std::max(a_, b_))};
+    CountPlan pl{1, (int32_t)N, (int32_t)n_P, (int32_t)o_begin, (int32_t)o_end, n_P, n_Q, split,
+                 split ? 32767 : (int64_t)(32767 / std::max(a_, b_))};
     ddks::CountArgs a{};
     a.pts = spts;
     a.item_stride = N * DPS;
@@ -356,40 +368,86 @@ ddks_status run_count_x0_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     a.n_P = (int32_t)n_P;
     a.o_begin = (int32_t)o_begin;
     a.o_end = (int32_t)o_end;
-    a.incP = a_;
-    a.incQ = 0u - b_;
-    a.g = gg;
+    a.incP = split ? 1u : a_;
+    a.incQ = split ? 1u : 0u - b_;
+    a.g = split ? 1 : gg;
     a.nP = n_P;
     a.nQ = n_Q;
     a.item_num = item_num;
     a.per_origin = per_origin;
     a.perm = (const int32_t*)ctx->x0_perm.p;
-    a.hist = nullptr;
+    a.hist = split ? hist_out : nullptr;
     const bool gt = (ctx->flags & DDKS_FLAG_TIES_GT) != 0;
+    if (split)
+        return gt ? launch_count_t<D, true, true, true>(ctx, pl, a, st) : launch_count_t<D, true, false, true>(ctx, pl, a, st);
     return gt ? launch_count_t<D, false, true, true>(ctx, pl, a, st) : launch_count_t<D, false, false, true>(ctx, pl, a, st);
+}
+
+// DIFF counters fit (|c_P a - c_Q b| stays in int32 and the int16 window is >= 4096 points); else SPLIT
+bool diff_counters_ok(int64_t n_P, int64_t n_Q) {
+    const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
+    const uint64_t a_ = (uint64_t)n_Q / g, b_ = (uint64_t)n_P / g;
+    return !(std::max(a_, b_) > 32767 / 4096 || (uint64_t)n_P * a_ >= 0x7fffffffull || (uint64_t)n_Q * b_ >= 0x7fffffffull);
 }
 
 bool x0_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q) {
     if (ctx->flags & DDKS_FLAG_NO_X0) return false;
-    const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
-    const uint64_t mab = std::max((uint64_t)n_Q / g, (uint64_t)n_P / g);
-    const bool diff_ok = !(mab > 32767 / 4096 || (uint64_t)n_P * ((uint64_t)n_Q / g) >= 0x7fffffffull ||
-                           (uint64_t)n_Q * ((uint64_t)n_P / g) >= 0x7fffffffull);
     // the sort (~0.1 ms) pays for itself once the O(N^2) count dominates; DDKS_FLAG_FORCE_X0 (tests) lowers the bar
     const int64_t min_n = (ctx->flags & DDKS_FLAG_FORCE_X0) ? 2 : 200000;
-    return d >= 2 && d <= 6 && diff_ok && n_P + n_Q >= min_n;
+    return d >= 2 && d <= 8 && n_P + n_Q >= min_n;
 }
 
 ddks_status run_count_x0(ddks_ctx* ctx, const float* packed, int d, int64_t n_P, int64_t n_Q, int64_t o_begin,
-                         int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st) {
+                         int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st, bool split,
+                         unsigned long long* hist) {
     switch (d) {
-        case 2: return run_count_x0_d<2>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st);
-        case 3: return run_count_x0_d<3>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st);
-        case 4: return run_count_x0_d<4>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st);
-        case 5: return run_count_x0_d<5>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st);
-        case 6: return run_count_x0_d<6>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st);
+#define X0_CASE(D) case D: return run_count_x0_d<D>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st, split, hist);
+        X0_CASE(2) X0_CASE(3) X0_CASE(4) X0_CASE(5) X0_CASE(6) X0_CASE(7) X0_CASE(8)
+#undef X0_CASE
     }
     return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "x0 mode d=%d", d);
+}
+
+// One statistic (B == 1) over the origin shard [ob, oe) of this rank: count (x0-ordered when it applies, else
+// position-ordered), then -- unless export_per (debug export of per-origin nums for [ob, oe)) -- the NCCL max of
+// num and this rank's argmax candidate into dres->arg (min-combined by the caller). split/hist: significance.
+ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n_P, int64_t n_Q, int64_t ob,
+                            int64_t oe, DevResult* dres, bool export_per, bool split, unsigned long long* hist,
+                            cudaStream_t st, uint64_t** per_out) {
+    const int64_t N = n_P + n_Q;
+    ddks_status s;
+    const bool x0 = !export_per && x0_applicable(ctx, d, n_P, n_Q) && (split || diff_counters_ok(n_P, n_Q));
+    if (x0) {
+        // origins are positions of the x_0 order; per-origin nums land in pooled order in per[N] (zeros elsewhere)
+        if ((s = ensure(ctx, ctx->per_origin, (size_t)N * 8))) return s;
+        uint64_t* per = (uint64_t*)ctx->per_origin.p;
+        *per_out = per;
+        if (oe > ob) {
+            if ((s = run_count_x0(ctx, packed, d, n_P, n_Q, ob, oe, (uint64_t*)&dres->num, per, st, split, hist))) return s;
+        } else {
+            CU(cudaMemsetAsync(per, 0, (size_t)N * 8, st));
+        }
+        if (ctx->world > 1) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
+        ddks::k_argmax<<<(int)std::min<int64_t>((N + 255) / 256, 148 * 4), 256, 0, st>>>(
+            per, N, 0, (const uint64_t*)&dres->num, &dres->arg);
+        CHECK_LAUNCH();
+        ctx->launches++;
+        return DDKS_OK;
+    }
+    if ((s = ensure(ctx, ctx->per_origin, (size_t)std::max<int64_t>(oe - ob, 1) * 8))) return s;
+    uint64_t* per = (uint64_t*)ctx->per_origin.p;
+    *per_out = per;
+    if (oe > ob && (s = run_count(ctx, packed, d, 1, n_P, n_Q, ob, oe, (uint64_t*)&dres->num, per, st, split, hist)))
+        return s;
+    if (export_per) return DDKS_OK;
+    if (ctx->world > 1) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
+    if (oe > ob) {
+        ddks::k_argmax<<<(int)std::min<int64_t>((oe - ob + 255) / 256, 148 * 4), 256, 0, st>>>(
+            per, oe - ob, ob, (const uint64_t*)&dres->num, &dres->arg);
+        CHECK_LAUNCH();
+        ctx->launches++;
+    }
+    return DDKS_OK;
 }
 
 ddks_status launch_pack(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d, int64_t B,
@@ -643,34 +701,8 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
     CU(cudaMemcpyAsync(dres, hres, sizeof init, cudaMemcpyHostToDevice, st));
     float* packed = (float*)ctx->packed.p;
     if ((s = launch_pack(ctx, (const float*)dP, n_P, (const float*)dQ, n_Q, d, 1, packed, &dres->flag, st))) return s;
-    uint64_t* per = (uint64_t*)ctx->per_origin.p;
-    const bool x0 = !export_mode && x0_applicable(ctx, d, n_P, n_Q);
-    if (x0) {
-        // origins are positions of the x_0 order; per-origin nums land in pooled order in per[N] (zeros elsewhere)
-        if ((s = ensure(ctx, ctx->per_origin, (size_t)N * 8))) return s;
-        per = (uint64_t*)ctx->per_origin.p;
-        if (oe > ob && (s = run_count_x0(ctx, packed, d, n_P, n_Q, ob, oe, (uint64_t*)&dres->num, per, st))) return s;
-        if (oe <= ob) CU(cudaMemsetAsync(per, 0, (size_t)N * 8, st));
-        if (ctx->world > 1) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
-        ddks::k_argmax<<<(int)std::min<int64_t>((N + 255) / 256, 148 * 4), 256, 0, st>>>(
-            per, N, 0, (const uint64_t*)&dres->num, &dres->arg);
-        CHECK_LAUNCH();
-        ctx->launches++;
-    } else if (oe > ob) {
-        if ((s = run_count(ctx, packed, d, 1, n_P, n_Q, ob, oe, (uint64_t*)&dres->num, per, st))) return s;
-        if (!export_mode) {
-            const int64_t n = oe - ob;
-            const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 4);
-            if (ctx->world > 1) {
-                NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
-            }
-            ddks::k_argmax<<<blocks, 256, 0, st>>>(per, n, ob, (const uint64_t*)&dres->num, &dres->arg);
-            CHECK_LAUNCH();
-            ctx->launches++;
-        }
-    } else if (ctx->world > 1 && !export_mode) {
-        NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
-    }
+    uint64_t* per = nullptr;
+    if ((s = count_statistic(ctx, packed, d, n_P, n_Q, ob, oe, dres, export_mode, false, nullptr, st, &per))) return s;
     if (ctx->world > 1 && !export_mode) {
         NC(ncclAllReduce(&dres->arg, &dres->arg, 1, ncclUint64, ncclMin, ctx->comm, st));
         NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
@@ -924,17 +956,8 @@ ddks_status ddks_significance(ddks_ctx* ctx, const float* P, int64_t n_P, const 
     CU(cudaMemcpyAsync(dres, hres, sizeof(DevResult), cudaMemcpyHostToDevice, st));
     float* packed = (float*)ctx->packed.p;
     if ((s = launch_pack(ctx, (const float*)dP, n_P, (const float*)dQ, n_Q, d, 1, packed, &dres->flag, st))) return s;
-    uint64_t* per = (uint64_t*)ctx->per_origin.p;
-    if (oe > ob && (s = run_count(ctx, packed, d, 1, n_P, n_Q, ob, oe, (uint64_t*)&dres->num, per, st, true, hist)))
-        return s;
-    if (ctx->world > 1) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
-    if (oe > ob) {
-        const int64_t n = oe - ob;
-        ddks::k_argmax<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 4), 256, 0, st>>>(
-            per, n, ob, (const uint64_t*)&dres->num, &dres->arg);
-        CHECK_LAUNCH();
-        ctx->launches++;
-    }
+    uint64_t* per = nullptr;
+    if ((s = count_statistic(ctx, packed, d, n_P, n_Q, ob, oe, dres, false, true, hist, st, &per))) return s;
     if (ctx->world > 1) {
         NC(ncclAllReduce(&dres->arg, &dres->arg, 1, ncclUint64, ncclMin, ctx->comm, st));
         NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));

@@ -467,26 +467,28 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
 // [o_lo, o_hi], and a whole tile of points with max x_0 < o_lo (or min x_0 >= o_hi) has the same bit 0 for every
 // pair of the CTA: bit 0 is decided once per tile and only dims 1..d-1 are compared. Tiles that overlap [o_lo, o_hi]
 // (about (R*T + 2*TILE)/N of them) take the full d compares. The counts are exactly those of k_count.
-// Sorted row layout [N][DPS]: x_0..x_{d-1}, then the point's increment for low-half and high-half counters
-// (DIFF: P -> +a, Q -> -b; the label no longer follows from the position), zero padding.
-template <int D> __host__ __device__ constexpr int sorted_dim() { return D + 2 <= 4 ? 4 : 8; }
+// Sorted row layout [N][DPS] (the label no longer follows from the position, so each row carries it):
+//   DIFF:  x_0..x_{d-1}, increment for low-half counters (P -> +a, Q -> -b), the same for high halves (<< 16);
+//   SPLIT: x_0..x_{d-1}, the byte offset of the point's bin block as a float (0 for P, 4*NQ*WPB for Q).
+template <int D> __host__ __device__ constexpr int sorted_dim() { return (D + 2 + 3) / 4 * 4; }
 
 __global__ void k_x0_keys(const float* __restrict__ pts, int DP, int64_t N, uint64_t* __restrict__ keys) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
         keys[i] = ((uint64_t)f32_key(pts[i * DP]) << 32) | (uint64_t)i;
 }
 
+// slot d / d+1 of every row: (valP, valP2) for P points, (valQ, valQ2) for Q points (bit patterns)
 __global__ void k_permute_sorted(const float* __restrict__ pts, int DP, int DPS, int d, int64_t N, int64_t n_P,
-                                 const uint64_t* __restrict__ keys, uint32_t incP, uint32_t incQ,
-                                 float* __restrict__ out, int32_t* __restrict__ perm) {
+                                 const uint64_t* __restrict__ keys, uint32_t valP, uint32_t valP2, uint32_t valQ,
+                                 uint32_t valQ2, float* __restrict__ out, int32_t* __restrict__ perm) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t idx = (int64_t)(uint32_t)keys[j];
-        const uint32_t inc = idx < n_P ? incP : incQ;
+        const bool isP = idx < n_P;
         for (int k = 0; k < DPS; ++k) {
             float v = 0.0f;
             if (k < d) v = pts[idx * DP + k];
-            else if (k == d) v = __uint_as_float(inc);
-            else if (k == d + 1) v = __uint_as_float(inc << 16);
+            else if (k == d) v = __uint_as_float(isP ? valP : valQ);
+            else if (k == d + 1) v = __uint_as_float(isP ? valP2 : valQ2);
             out[j * DPS + k] = v;
         }
         perm[j] = (int32_t)idx;
@@ -494,7 +496,7 @@ __global__ void k_permute_sorted(const float* __restrict__ pts, int DP, int DPS,
 }
 
 template <int D, int DPS>
-__device__ __forceinline__ void load_sorted(const float* sp, float (&x)[D], uint32_t& inc_lo, uint32_t& inc_hi) {
+__device__ __forceinline__ void load_sorted(const float* sp, float (&x)[D], uint32_t& e0, uint32_t& e1) {
     float v[DPS];
 #pragma unroll
     for (int i = 0; i < DPS; i += 4) {
@@ -503,40 +505,46 @@ __device__ __forceinline__ void load_sorted(const float* sp, float (&x)[D], uint
     }
 #pragma unroll
     for (int k = 0; k < D; ++k) x[k] = v[k];
-    inc_lo = __float_as_uint(v[D]);
-    inc_hi = __float_as_uint(v[D + 1]);
+    e0 = __float_as_uint(v[D]);
+    e1 = __float_as_uint(v[D + 1]);
 }
 
-// dims [FIRST, D) of every point in [0, n) against this thread's R origins; base already holds bit 0's weight
-template <int D, bool GT, int FIRST, int R, int RP, int NB_, int WPB, int DPS>
+// dims [FIRST, D) of every point in [0, n) against this thread's R origins; base already holds bit 0's weight.
+// DIFF: the increment comes with the point (e0 for low halves, e1 for high halves; R == 1: HI picks this thread's).
+// SPLIT: the point's bin-block offset e0 is added to the base, the increment is 1 (low half) or 1 << 16 (high).
+template <int D, bool SPLIT, bool GT, int FIRST, int R, int RP, int NB_, int WPB, int DPS>
 __device__ __forceinline__ void count_sorted(const float* tile, int n, const float (&o)[R][D], const float (&base)[NB_],
-                                             uint32_t ubase) {
+                                             uint32_t ubase, bool hi1) {
     float xn[D];
-    uint32_t ln, hn;
-    load_sorted<D, DPS>(tile, xn, ln, hn);
+    uint32_t e0n, e1n;
+    load_sorted<D, DPS>(tile, xn, e0n, e1n);
 #pragma unroll 4
     for (int p = 0; p < n; ++p) {
         float x[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) x[k] = xn[k];
-        const uint32_t il = ln, ih = hn;
-        load_sorted<D, DPS>(tile + (p + 1) * DPS, xn, ln, hn);  // index n <= TILE: inside the allocation, unused
+        const uint32_t e0 = e0n, e1 = e1n;
+        load_sorted<D, DPS>(tile + (p + 1) * DPS, xn, e0n, e1n);  // index n <= TILE: inside the allocation, unused
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            float f = base[r % NB_];
+            const bool high = R >= 2 ? (r >= RP) : hi1;
+            float f = SPLIT ? base[r % NB_] + __uint_as_float(e0) : base[r % NB_];
 #pragma unroll
             for (int k = FIRST; k < D; ++k) f = fmaf(cmp_bit<GT>(x[k], o[r][k]), (float)(4 * (1 << k) * WPB), f);
-            red_add_shared(__float_as_uint(f) + ubase, r < RP ? il : ih);
+            const uint32_t inc = SPLIT ? (high ? (1u << 16) : 1u) : (high ? e1 : e0);
+            red_add_shared(__float_as_uint(f) + ubase, inc);
         }
     }
 }
 
-template <int D, bool GT>
-__global__ void __launch_bounds__(Geo<D, false, sorted_dim<D>()>::T, 1) k_count_x0(const CountArgs a) {
-    using G = Geo<D, false, sorted_dim<D>()>;
+template <int D, bool SPLIT>
+using GeoX0 = Geo<D, SPLIT, sorted_dim<D>()>;
+
+template <int D, bool SPLIT, bool GT>
+__global__ void __launch_bounds__(GeoX0<D, SPLIT>::T, 1) k_count_x0(const CountArgs a) {
+    using G = GeoX0<D, SPLIT>;
     constexpr int R = G::R, RP = G::RP, T = G::T, DPS = G::DP, TILE = G::TILE, S = G::S, NBASE = G::NBASE,
                   WPB = G::WPB;
-    static_assert(R >= 2, "x0-ordered mode keeps two origins of a thread per counter word");
     extern __shared__ __align__(128) uint8_t smem[];
     float* tiles = reinterpret_cast<float*>(smem);
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem + S * G::TILE_BYTES);
@@ -580,6 +588,7 @@ __global__ void __launch_bounds__(Geo<D, false, sorted_dim<D>()>::T, 1) k_count_
         base0[b] = __uint_as_float(0x4B000000u + 4u * (uint32_t)G::slot(b, t));
         base1[b] = base0[b] + (float)(4 * WPB);  // + bit 0's weight (exact: integers < 2^24)
     }
+    const bool hi1 = G::high(0, t);  // R == 1: this thread's origin is a high half
     for (int it = 0; it < n_tiles; ++it) {
         const int s = it % S;
         mbar_wait(&bars[s], (uint32_t)((it / S) & 1));
@@ -590,9 +599,9 @@ __global__ void __launch_bounds__(Geo<D, false, sorted_dim<D>()>::T, 1) k_count_
         // bit 0 = [x_0 >= o_0] (GT: >) is uniform over the tile x origins when the value ranges do not interleave
         const bool all0 = GT ? (t_hi <= o_lo) : (t_hi < o_lo);
         const bool all1 = GT ? (t_lo > o_hi) : (t_lo >= o_hi);
-        if (all0)      count_sorted<D, GT, 1, R, RP, NBASE, WPB, DPS>(tile, cnt, o, base0, ubase);
-        else if (all1) count_sorted<D, GT, 1, R, RP, NBASE, WPB, DPS>(tile, cnt, o, base1, ubase);
-        else           count_sorted<D, GT, 0, R, RP, NBASE, WPB, DPS>(tile, cnt, o, base0, ubase);
+        if (all0)      count_sorted<D, SPLIT, GT, 1, R, RP, NBASE, WPB, DPS>(tile, cnt, o, base0, ubase, hi1);
+        else if (all1) count_sorted<D, SPLIT, GT, 1, R, RP, NBASE, WPB, DPS>(tile, cnt, o, base1, ubase, hi1);
+        else           count_sorted<D, SPLIT, GT, 0, R, RP, NBASE, WPB, DPS>(tile, cnt, o, base0, ubase, hi1);
         __syncthreads();
         if (t == 0 && it + S < n_tiles) {
             fence_proxy_async();
@@ -627,7 +636,7 @@ __global__ void __launch_bounds__(Geo<D, false, sorted_dim<D>()>::T, 1) k_count_
     for (int r = 0; r < R; ++r) {
         const int32_t oi = blk_o0 + r * T + t;
         if (oi >= a.o_end) continue;
-        const uint64_t m = origin_num<D, false>(hist, r, t, a);
+        const uint64_t m = origin_num<D, SPLIT>(hist, r, t, a);
         if (a.per_origin) a.per_origin[a.perm[oi]] = m;
         best = m > best ? m : best;
     }
@@ -643,11 +652,22 @@ __global__ void __launch_bounds__(Geo<D, false, sorted_dim<D>()>::T, 1) k_count_
 }
 
 // Finalise accumulate mode: one thread per (item, origin).
+// SPLIT with a.hist (significance): M_T values below HS are histogrammed in a block-private SMEM histogram first and
+// flushed once per block; larger values (rare) go straight to global memory.
+constexpr int HS = 2048;
+
 template <int D, bool SPLIT>
 __global__ void k_finalize(const CountArgs a, int64_t B) {
     constexpr int NQ = 1 << D;
     constexpr int NB = Geo<D, SPLIT>::NB;
     const int32_t n_orig = a.o_end - a.o_begin;
+    __shared__ uint32_t sh_hist[SPLIT ? HS : 1];
+    if constexpr (SPLIT) {
+        if (a.hist) {
+            for (int i = threadIdx.x; i < HS; i += blockDim.x) sh_hist[i] = 0u;
+            __syncthreads();
+        }
+    }
     const int64_t total = B * (int64_t)n_orig;
     uint64_t best = 0;
     int64_t item_of_best = -1;
@@ -667,7 +687,10 @@ __global__ void k_finalize(const CountArgs a, int64_t B) {
             for (int q = 0; q < NQ; ++q) {
                 const int64_t cP = (int64_t)acc[(int64_t)q * n_orig];
                 const int64_t cQ = (int64_t)acc[(int64_t)(NQ + q) * n_orig];
-                if (a.hist) hist_add_aggregated(a.hist, cQ);
+                if (a.hist) {
+                    if (cQ < HS) atomicAdd(&sh_hist[cQ], 1u);
+                    else hist_add_aggregated(a.hist, cQ);
+                }
                 const int64_t df = cP * a.nQ - cQ * a.nP;
                 const uint64_t av = (uint64_t)(df < 0 ? -df : df);
                 m = av > m ? av : m;
@@ -685,6 +708,13 @@ __global__ void k_finalize(const CountArgs a, int64_t B) {
         best = warp_max_u64(best);
         if ((threadIdx.x & 31) == 0)
             atomicMax(reinterpret_cast<unsigned long long*>(&a.item_num[0]), (unsigned long long)best);
+    }
+    if constexpr (SPLIT) {
+        if (a.hist) {
+            __syncthreads();
+            for (int i = threadIdx.x; i < HS; i += blockDim.x)
+                if (sh_hist[i]) atomicAdd(&a.hist[i], (unsigned long long)sh_hist[i]);
+        }
     }
 }
 

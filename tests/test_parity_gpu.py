@@ -303,7 +303,8 @@ def ctx_x0_gt():
 
 
 X0_CASES = [(300, 200, 2, "grid"), (1500, 1300, 3, "normal"), (5000, 4000, 2, "grid"), (6000, 6000, 3, "mixed"), (4500, 5200, 4, "normal"), (9000, 7001, 5, "grid"),
-            (5000, 5000, 5, "dup"), (4096, 4096, 6, "mixed"), (20000, 1, 3, "normal"), (3, 12000, 5, "grid")]
+            (5000, 5000, 5, "dup"), (4096, 4096, 6, "mixed"), (20000, 1, 3, "normal"), (3, 12000, 5, "grid"),
+            (3000, 2500, 7, "mixed"), (2600, 3100, 8, "normal"), (1500, 1500, 8, "grid"), (40000, 30000, 2, "normal")]
 
 
 @pytest.mark.parametrize("n_P,n_Q,d,kind", X0_CASES)

@@ -139,3 +139,26 @@ def test_significance_errors(ctx):
     with pytest.raises(K.DDKSError) as e:
         ctx.significance(Pn, P)
     assert e.value.status == 4
+
+
+@pytest.mark.parametrize("n_P,n_Q,d,kind", [(40, 30, 2, "grid"), (64, 64, 3, "normal"), (90, 60, 4, "normal"),
+                                            (33, 41, 5, "dup"), (30, 26, 8, "mixed")])
+def test_significance_x0_ordered(n_P, n_Q, d, kind):
+    # the x0-ordered SPLIT kernel (bin-0 elision; the bench's C5 significance path) against the oracle and the
+    # position-ordered kernel: identical histogram and statistic, bit-identical log_prod
+    P, Q = I.random_pair(1000 + 7 * n_P + d, n_P, n_Q, d, kind)
+    with K.Context(flags=K.DDKS_FLAG_FORCE_X0) as cx, K.Context(flags=K.DDKS_FLAG_NO_X0) as cn:
+        a = cx.significance(dev(P), dev(Q), detail=True)
+        b = cn.significance(dev(P), dev(Q), detail=True)
+    assert a.stat == b.stat and np.array_equal(a.mt_hist, b.mt_hist) and a.log_prod == b.log_prod
+    assert np.array_equal(a.mt_hist, oracle_hist(P, Q))
+    want = O.ddks(P, Q)
+    assert (a.stat.num, a.stat.argmax_origin) == (want[0], want[3])
+
+
+def test_significance_x0_c2(ctx):
+    P, Q = I.config("C2")
+    with K.Context(flags=K.DDKS_FLAG_FORCE_X0) as cx:
+        a = cx.significance(dev(P), dev(Q), detail=True)
+    b = ctx.significance(dev(P), dev(Q), detail=True)
+    assert a.stat == b.stat and np.array_equal(a.mt_hist, b.mt_hist) and a.log_prod == b.log_prod
