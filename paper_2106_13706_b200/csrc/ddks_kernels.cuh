@@ -39,9 +39,9 @@ template <> struct Cfg<2> { static constexpr int R = 8, T = 256, TILE = 512, S =
 template <> struct Cfg<3> { static constexpr int R = 8, T = 256, TILE = 512, S = 3; };
 template <> struct Cfg<4> { static constexpr int R = 4, T = 256, TILE = 512, S = 3; };
 template <> struct Cfg<5> { static constexpr int R = 8, T = 384, TILE = 256, S = 3; };
-template <> struct Cfg<6> { static constexpr int R = 4, T = 256, TILE = 256, S = 3; };
-template <> struct Cfg<7> { static constexpr int R = 2, T = 256, TILE = 256, S = 3; };
-template <> struct Cfg<8> { static constexpr int R = 1, T = 256, TILE = 256, S = 3; };
+template <> struct Cfg<6> { static constexpr int R = 4, T = 384, TILE = 256, S = 3; };
+template <> struct Cfg<7> { static constexpr int R = 2, T = 384, TILE = 256, S = 3; };
+template <> struct Cfg<8> { static constexpr int R = 1, T = 384, TILE = 256, S = 3; };
 
 template <int D> __host__ __device__ constexpr int padded_dim() { return D <= 4 ? 4 : 8; }
 
@@ -52,7 +52,7 @@ template <int D, bool SPLIT, int DPX = padded_dim<D>()> struct Geo {
     static constexpr int RP = R / 2;                            // counter words per (bin, thread) when R >= 2
     static constexpr int NBASE = R >= 2 ? RP : 1;               // distinct counter base addresses per thread
     static constexpr int WPB = R * T / 2;                       // counter words per bin
-    static constexpr int TILE = Cfg<D>::TILE;
+    static constexpr int TILE = DPX > 8 ? Cfg<D>::TILE / 2 : Cfg<D>::TILE;  // 48-byte x0 rows: half the points
     static constexpr int S = Cfg<D>::S;
     static constexpr int DP = DPX;
     static constexpr int NQ = 1 << D;
