@@ -24,6 +24,8 @@
 
 #define DDKS_VERSION "0.1.0-sm100a"
 
+constexpr int kMaxDevices = 64;  // per-device, per-kernel launch attributes are cached for this many devices
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -163,10 +165,12 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
     void (*kern)(const ddks::CountArgs) = nullptr;
     if constexpr (X0) kern = ddks::k_count_x0<D, SPLIT, GT>;
     else kern = ddks::k_count<D, SPLIT, GT>;
-    static bool attr_done = false;  // per-process; device attributes are per function
-    if (!attr_done) {
+    // function attributes are per device: remember which devices this instantiation was configured on
+    static bool attr_done[kMaxDevices] = {};
+    if (ctx->device >= kMaxDevices) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device index %d >= %d", ctx->device, kMaxDevices);
+    if (!attr_done[ctx->device]) {
         CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES));
-        attr_done = true;
+        attr_done[ctx->device] = true;
     }
     const int n_orig = pl.o_end - pl.o_begin;
     const int blocks_o = (n_orig + G::ORIGINS - 1) / G::ORIGINS;
@@ -174,7 +178,8 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
     // segment length: at most the int16 flush window. Among the segment counts that respect it, pick the one with
     // the least modelled time: waves x per-CTA cost, where a CTA costs its segment's points (x its origins) plus the
     // flush of NB int32 partials per origin (global atomics; ~FLUSH_COST point-equivalents each) and the setup.
-    static int per_sm = 0;
+    static int per_sm_dev[kMaxDevices] = {};
+    int& per_sm = per_sm_dev[ctx->device];
     if (!per_sm) {
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::T, G::SMEM_BYTES));
         per_sm = std::max(per_sm, 1);
@@ -470,10 +475,11 @@ ddks_status launch_perm_d(ddks_ctx* ctx, const float* pooled_packed, const int32
     using G = ddks::PermGeo<D>;
     const bool gt = (ctx->flags & DDKS_FLAG_TIES_GT) != 0;
     auto kern = gt ? ddks::k_perm_count<D, true> : ddks::k_perm_count<D, false>;
-    static bool attr[2] = {false, false};
-    if (!attr[gt]) {
+    static bool attr[kMaxDevices][2] = {};
+    if (ctx->device >= kMaxDevices) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device index %d >= %d", ctx->device, kMaxDevices);
+    if (!attr[ctx->device][gt]) {
         CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES));
-        attr[gt] = true;
+        attr[ctx->device][gt] = true;
     }
     const int64_t N = n_P + n_Q;
     const int64_t chunks = (n_perm + G::J - 1) / G::J;
