@@ -134,6 +134,43 @@ def cpu_oracle_sample(P, Q, seconds: float):
                       f"pair classifications in {dt:.2f} s, OpenMP over origins on {cores} host threads"}
 
 
+def cpu_oracle_method(method, P, Q, seconds: float, k: int = 16):
+    """The CPU oracle of an approximation, as it stands, on a bounded sample, extrapolated to the whole statistic
+    (unit: pooled points/s, like the GPU line)."""
+    from oracle import oracle as O
+    O.build()
+    cores = os.cpu_count() or 1
+    N, d = P.shape[0] + Q.shape[0], P.shape[1]
+    if method == "rdks":
+        # corner 0 alone, then as many more corners as fit the budget; the statistic needs all d + 1 corners
+        t0 = time.perf_counter()
+        O.rdks(P, Q, 0, 1)
+        dt1 = time.perf_counter() - t0
+        nc = int(min(d + 1, max(1, seconds / max(dt1, 1e-6))))
+        t0 = time.perf_counter()
+        O.rdks(P, Q, 0, nc)
+        dt = time.perf_counter() - t0
+        full = dt * (d + 1) / nc
+        sample = f"{nc} of {d + 1} corners (distances + qsort + merge sweep) in {dt:.2f} s, scaled to all corners"
+    else:  # vdks: the literal SumOrthants loop over a leading range of voxels, scaled by the voxel count
+        V = k ** d
+        nv = max(1, V // 4096)
+        t0 = time.perf_counter()
+        O.vdks(P, Q, k, 0, nv)
+        dt1 = time.perf_counter() - t0
+        while dt1 < seconds / 4 and nv < V:
+            nv = min(V, nv * 4)
+            t0 = time.perf_counter()
+            O.vdks(P, Q, k, 0, nv)
+            dt1 = time.perf_counter() - t0
+        dt = dt1
+        full = dt * V / nv
+        sample = (f"voxels [0, {nv}) of {V} (histogram + literal orthant sums over every voxel) in {dt:.2f} s, "
+                  f"scaled to all voxels")
+    return {"value": N / full, "unit": "points/s", "cores": cores, "kind": "oracle",
+            "sample": sample + f", OpenMP on {cores} host threads"}
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle as it stands is this tier's reference arm (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -358,8 +395,14 @@ def main():
     roof = dict({k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac")}, traffic=traffic,
                 **{k: v for k, v in roof.items() if k not in ("bound", "achieved", "peak", "unit", "frac")})
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.method == "exact" and args.workload != "C4":
-        cpu = cpu_oracle_sample(*step.host, args.cpu_seconds)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload != "C4":
+        if args.method in ("exact", "significance"):
+            cpu = cpu_oracle_sample(*step.host, args.cpu_seconds)
+            if args.method == "significance":
+                cpu["sample"] += ("; the O(N^2) classification only (the oracle's literal Delta-band sum per cell is "
+                                  "(n_P+1)(n_Q+1) terms, not sampled)")
+        else:
+            cpu = cpu_oracle_method(args.method, *step.host, args.cpu_seconds, args.vdks_k)
 
     if rank == 0:
         if hasattr(res, "_asdict"):
