@@ -11,7 +11,8 @@
 //     M_T values: hist[m] = #cells with M_T = m. A cell's factor depends only on m, so the product becomes
 //     sum_m hist[m] * log p(d<=D | lambda_m): at most N_T + 1 table entries instead of 2^d N cells;
 //   * k_sig_table: one persistent CTA per table entry in flight. It evaluates the pmf of n_P over the window
-//     where it is within e^-100 of its mode (binary search on the unimodal log pmf), prefix- and suffix-scans it
+//     where it is within e^-100 of its mode (warp-parallel 32-ary searches on the unimodal log pmf), prefix- and
+//     suffix-scans it
 //     in global scratch, and sums the COMPLEMENT q = 1 - p(d<=D) = sum_{n_T} p(n_T) [F_P(lo-1) + (1 - F_P(hi))]
 //     (only tail sums of small positive terms: no cancellation). log p(d<=D) = log1p(-q) (R14);
 //   * log n! comes from a device table LF[n] = lgamma(n+1);
@@ -65,30 +66,48 @@ struct LogPmf {
         int64_t k = poisson ? (int64_t)floor(mu) : (int64_t)floor((double)(m + 1) * lam);
         return k < 0 ? 0 : (k > m ? m : k);
     }
-    // largest n in [lo, hi] with f(n) >= thr, f non-increasing there (f(lo) >= thr)
-    __device__ int64_t last_above(int64_t lo, int64_t hi, double thr) const {
-        while (lo < hi) {
-            const int64_t mid = lo + (hi - lo + 1) / 2;
-            if ((*this)(mid) >= thr) lo = mid; else hi = mid - 1;
+    // Warp-cooperative 32-ary searches (all 32 lanes call them; every lane gets the result).
+    // Largest n in [lo, hi] with f(n) >= thr, f non-increasing there and f(lo) >= thr.
+    __device__ int64_t warp_last_above(int64_t lo, int64_t hi, double thr) const {
+        const int lane = threadIdx.x & 31;
+        while (hi - lo > 31) {
+            const int64_t step = (hi - lo) / 31 + 1;  // 31 steps reach past hi
+            const int64_t c = lo + lane * step;
+            const uint32_t ok = __ballot_sync(0xffffffffu, c <= hi && (*this)(c) >= thr);  // a prefix of lanes
+            const int k = 31 - __clz(ok);
+            lo = lo + k * step;
+            hi = min(hi, lo + step - 1);
         }
-        return lo;
+        const int64_t c = lo + lane;
+        const uint32_t ok = __ballot_sync(0xffffffffu, c <= hi && (*this)(c) >= thr);
+        return lo + (31 - __clz(ok));
     }
-    // [a, b] = the n in 0..m with log pmf >= log pmf(mode) - 100 (the pmf is unimodal: two binary searches).
-    // Poisson only: [ta, tb] = the n > m (outside the Delta set's 0..m) above the same threshold, tb <= lf_max;
-    // ta > tb if there are none.
+    // Smallest n in [lo, hi] with f(n) >= thr, f non-decreasing there and f(hi) >= thr.
+    __device__ int64_t warp_first_above(int64_t lo, int64_t hi, double thr) const {
+        const int lane = threadIdx.x & 31;
+        while (hi - lo > 31) {
+            const int64_t step = (hi - lo) / 31 + 1;  // 31 steps reach past hi
+            const int64_t c = hi - lane * step;
+            const uint32_t ok = __ballot_sync(0xffffffffu, c >= lo && (*this)(c) >= thr);  // a prefix of lanes
+            const int k = 31 - __clz(ok);
+            hi = hi - k * step;
+            lo = max(lo, hi - step + 1);
+        }
+        const int64_t c = hi - lane;
+        const uint32_t ok = __ballot_sync(0xffffffffu, c >= lo && (*this)(c) >= thr);
+        return hi - (31 - __clz(ok));
+    }
+    // [a, b] = the n in 0..m with log pmf >= log pmf(mode) - 100 (the pmf is unimodal). Poisson only: [ta, tb] =
+    // the n > m (outside the Delta set's 0..m) above the same threshold, tb <= lf_max; ta > tb if there are none.
+    // Called by a whole warp.
     __device__ void window(double lam, int64_t lf_max, int64_t& a, int64_t& b, int64_t& ta, int64_t& tb) const {
         const int64_t md = mode(lam);
         const double thr = (*this)(md) - 100.0;
-        int64_t lo = 0, hi = md;  // smallest n in [0, md] with f(n) >= thr
-        while (lo < hi) {
-            const int64_t mid = lo + (hi - lo) / 2;
-            if ((*this)(mid) >= thr) hi = mid; else lo = mid + 1;
-        }
-        a = lo;
-        b = last_above(md, m, thr);
+        a = warp_first_above(0, md, thr);
+        b = warp_last_above(md, m, thr);
         ta = m + 1;
         tb = m;
-        if (poisson && m < lf_max && (*this)(m + 1) >= thr) tb = last_above(m + 1, lf_max, thr);
+        if (poisson && m < lf_max && (*this)(m + 1) >= thr) tb = warp_last_above(m + 1, lf_max, thr);
     }
 };
 
@@ -105,33 +124,39 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     return s;
 }
 
-// In-place inclusive scan of x[0..W) (REV: from the right, x[i] = sum_{j >= i}). Fixed order: each thread owns a
-// contiguous run, runs are combined by an exclusive scan of the run totals.
+// In-place inclusive scan of x[0..W) (REV: from the right, x[i] = sum_{j >= i}). Fixed order: chunks of NT
+// consecutive elements, one per thread (coalesced), each chunk scanned with warp shuffles + a scan of the warp
+// totals, plus the running carry of the earlier chunks.
 template <int NT, bool REV>
 __device__ void block_scan(double* x, int64_t W, double* red) {
-    const int64_t C = (W + NT - 1) / NT;
-    const int64_t b = threadIdx.x * C, e = b + C < W ? b + C : W;
-    double s = 0.0;
-    for (int64_t i = b; i < e; ++i) s += x[REV ? W - 1 - i : i];
-    __syncthreads();
-    red[threadIdx.x] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double run = 0.0;
-        for (int t = 0; t < NT; ++t) {
-            const double v = red[t];
-            red[t] = run;
-            run += v;
-        }
-    }
-    __syncthreads();
-    double run = red[threadIdx.x];
-    for (int64_t i = b; i < e; ++i) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double carry = 0.0;
+    for (int64_t base = 0; base < W; base += NT) {
+        const int64_t i = base + threadIdx.x;
         const int64_t j = REV ? W - 1 - i : i;
-        run += x[j];
-        x[j] = run;
+        double v = i < W ? x[j] : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        if (lane == 31) red[w] = v;
+        __syncthreads();
+        if (w == 0) {
+            double t = lane < NT / 32 ? red[lane] : 0.0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            if (lane < NT / 32) red[lane] = t;  // inclusive prefix of the warp totals
+        }
+        __syncthreads();
+        const double before = carry + (w ? red[w - 1] : 0.0);
+        if (i < W) x[j] = before + v;
+        carry += red[NT / 32 - 1];
+        __syncthreads();  // red is rewritten by the next chunk
     }
-    __syncthreads();
 }
 
 constexpr int SIG_T = 512;
@@ -152,8 +177,15 @@ __global__ void __launch_bounds__(SIG_T) k_sig_table(const SigArgs a) {
         LogPmf fP, fT;
         fP.init(a.LF, a.N_P, lam, a.poisson);
         fT.init(a.LF, a.N_T, lam, a.poisson);
-        if (threadIdx.x == 0) fP.window(lam, a.lf_max, win[0], win[1], win[4], win[5]);
-        if (threadIdx.x == 32) fT.window(lam, a.lf_max, win[2], win[3], win[6], win[7]);
+        if (threadIdx.x < 32) {  // warp 0: the n_P window, warp 1: the n_T window
+            int64_t w0, w1, w2, w3;
+            fP.window(lam, a.lf_max, w0, w1, w2, w3);
+            if (threadIdx.x == 0) win[0] = w0, win[1] = w1, win[4] = w2, win[5] = w3;
+        } else if (threadIdx.x < 64) {
+            int64_t w0, w1, w2, w3;
+            fT.window(lam, a.lf_max, w0, w1, w2, w3);
+            if (threadIdx.x == 32) win[2] = w0, win[3] = w1, win[6] = w2, win[7] = w3;
+        }
         __syncthreads();
         const int64_t aP = win[0], bP = win[1], aT = win[2], bT = win[3];
         int64_t W = bP - aP + 1;
