@@ -159,6 +159,17 @@ __device__ void block_scan(double* x, int64_t W, double* red) {
     }
 }
 
+// floor(x / n) and ceil(x / n) for n > 0, exact: a double-precision estimate (inv = 1/n) corrected by the integer
+// remainder (64-bit integer division is a long emulated sequence on the GPU; this is two FMAs and a check).
+__device__ __forceinline__ int64_t floor_div(int64_t x, int64_t n, double inv) {
+    int64_t q = (int64_t)floor((double)x * inv);
+    int64_t r = x - q * n;
+    while (r < 0) { --q; r += n; }
+    while (r >= n) { ++q; r -= n; }
+    return q;
+}
+__device__ __forceinline__ int64_t ceil_div(int64_t x, int64_t n, double inv) { return -floor_div(-x, n, inv); }
+
 constexpr int SIG_T = 512;
 
 __global__ void __launch_bounds__(SIG_T) k_sig_table(const SigArgs a) {
@@ -167,6 +178,7 @@ __global__ void __launch_bounds__(SIG_T) k_sig_table(const SigArgs a) {
     double* A = a.scratch + (int64_t)blockIdx.x * 2 * a.W_max;  // inclusive prefix sums of p(n_P)
     double* B = A + a.W_max;                                     // inclusive suffix sums of p(n_P)
     const int64_t num = (int64_t)*a.num;
+    const double invT = 1.0 / (double)a.N_T;
     for (int64_t m = a.m_begin + blockIdx.x; m < a.m_end; m += gridDim.x) {
         const unsigned long long h = a.hist[m];
         if (h == 0) {
@@ -204,21 +216,26 @@ __global__ void __launch_bounds__(SIG_T) k_sig_table(const SigArgs a) {
             tP = block_sum<SIG_T>(sP, red);
             tT = block_sum<SIG_T>(sT, red);
         }
-        for (int64_t i = threadIdx.x; i < W; i += SIG_T) {
-            const double v = exp(fP(aP + i));
-            A[i] = v;
-            B[i] = v;
-        }
-        __syncthreads();
-        block_scan<SIG_T, false>(A, W, red);
-        block_scan<SIG_T, true>(B, W, red);
         const int64_t eP = aP + W - 1;  // last n_P inside the window
+        // lo(n_T) and hi(n_T) increase with n_T: if the band covers the whole n_P window already at the ends of the
+        // n_T window, every tail below is exactly 0 and the pmf tables are not needed (the usual case when D is
+        // many standard deviations above the sampling noise)
+        const bool covered = ceil_div(bT * a.N_P - num, a.N_T, invT) <= aP && floor_div(aT * a.N_P + num, a.N_T, invT) >= eP;
+        if (!covered) {
+            for (int64_t i = threadIdx.x; i < W; i += SIG_T) {
+                const double v = exp(fP(aP + i));
+                A[i] = v;
+                B[i] = v;
+            }
+            __syncthreads();
+            block_scan<SIG_T, false>(A, W, red);
+            block_scan<SIG_T, true>(B, W, red);
+        }
         double acc = 0.0;
-        for (int64_t nT = aT + threadIdx.x; nT <= bT; nT += SIG_T) {
+        for (int64_t nT = aT + threadIdx.x; !covered && nT <= bT; nT += SIG_T) {
             // band of n_P with |n_P N_T - nT N_P| <= num: [lo, hi], exact int64
-            const int64_t x = nT * a.N_P - num;
-            const int64_t lo = x >= 0 ? (x + a.N_T - 1) / a.N_T : -((-x) / a.N_T);
-            const int64_t hi = (nT * a.N_P + num) / a.N_T;
+            const int64_t lo = ceil_div(nT * a.N_P - num, a.N_T, invT);
+            const int64_t hi = floor_div(nT * a.N_P + num, a.N_T, invT);
             const double left = lo <= aP ? 0.0 : A[(lo > eP + 1 ? eP + 1 : lo) - 1 - aP];   // sum_{n_P < lo}
             const double right = hi >= eP ? 0.0 : B[(hi < aP - 1 ? aP - 1 : hi) + 1 - aP];  // sum_{n_P > hi}
             const double tail = left + right;
