@@ -161,10 +161,8 @@ struct CountPlan {
 
 template <int D, bool SPLIT, bool GT, bool X0 = false>
 ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a, cudaStream_t st) {
-    using G = std::conditional_t<X0, ddks::GeoX0<D, SPLIT>, ddks::Geo<D, SPLIT>>;
-    void (*kern)(const ddks::CountArgs) = nullptr;
-    if constexpr (X0) kern = ddks::k_count_x0<D, SPLIT, GT>;
-    else kern = ddks::k_count<D, SPLIT, GT>;
+    using G = ddks::Geo<D, SPLIT>;
+    auto kern = ddks::k_count<D, SPLIT, GT, X0>;
     // function attributes are per device: remember which devices this instantiation was configured on
     static bool attr_done[kMaxDevices] = {};
     if (ctx->device >= kMaxDevices) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device index %d >= %d", ctx->device, kMaxDevices);
@@ -310,15 +308,13 @@ ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int6
     return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "d=%d", d);
 }
 
-// x0-ordered statistic (B == 1, 2 <= d <= 8): sort the packed points by x_0, build the sorted rows (coordinates + the
-// per-point increment / bin offset), count with bit-0 elision (k_count_x0), per-origin nums scattered back to pooled
-// order into per_origin[N] (zeroed here). Origins [o_begin, o_end) are positions in the SORTED order. split + hist:
-// SPLIT counters and the significance's M_T histogram (as run_count).
+// x0-ordered statistic (B == 1, 2 <= d <= 8): reorder the packed rows label-major by x_0, count with bit-0 elision
+// (k_count<X0>), per-origin nums scattered back to pooled order into per_origin[N] (zeroed here). Origins
+// [o_begin, o_end) are positions in the x0 order. split + hist: SPLIT counters and the significance's M_T histogram.
 template <int D>
 ddks_status run_count_x0_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int64_t n_Q, int64_t o_begin,
                            int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st, bool split,
                            unsigned long long* hist_out) {
-    constexpr int DPS = ddks::sorted_dim<D>();
     const int64_t N = n_P + n_Q;
     const int DP = pad_dim(D);
     const int tiles = (int)((N + ddks::RS_TILE - 1) / ddks::RS_TILE);
@@ -326,18 +322,18 @@ ddks_status run_count_x0_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     if ((s = ensure(ctx, ctx->x0_keys0, (size_t)N * 8))) return s;
     if ((s = ensure(ctx, ctx->x0_keys1, (size_t)N * 8))) return s;
     if ((s = ensure(ctx, ctx->x0_hist, (size_t)tiles * 256 * 4))) return s;
-    if ((s = ensure(ctx, ctx->x0_pts, (size_t)(N + 2) * DPS * 4))) return s;
+    if ((s = ensure(ctx, ctx->x0_pts, (size_t)(N + 4) * DP * 4))) return s;
     if ((s = ensure(ctx, ctx->x0_perm, (size_t)N * 4))) return s;
     uint64_t* k0 = (uint64_t*)ctx->x0_keys0.p;
     uint64_t* k1 = (uint64_t*)ctx->x0_keys1.p;
     uint32_t* hist = (uint32_t*)ctx->x0_hist.p;
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 16));
-    ddks::k_x0_keys<<<g, 256, 0, st>>>(packed, DP, N, k0);
+    ddks::k_x0_keys<<<g, 256, 0, st>>>(packed, DP, N, n_P, k0);
     CHECK_LAUNCH();
     ctx->launches++;
-    // stable LSD passes over the key's upper 32 bits only: ties in x_0 keep pooled-index order
+    // stable LSD passes over key bits 31..63 (x_0 key, then the label): ties keep pooled-index order
     uint64_t *src = k0, *dst = k1;
-    for (int shift = 32; shift < 64; shift += 8) {
+    for (int shift = 31; shift < 64; shift += 8) {
         ddks::k_rs_hist<<<tiles, ddks::RS_T, 0, st>>>(src, N, tiles, shift, hist);
         ddks::k_rs_scan<<<1, 256 * ddks::RS_SCAN_PARTS, 0, st>>>(hist, tiles);
         ddks::k_rs_scatter<<<tiles, ddks::RS_T, 0, st>>>(src, dst, N, tiles, shift, hist);
@@ -345,30 +341,19 @@ ddks_status run_count_x0_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
         ctx->launches += 3;
         std::swap(src, dst);
     }
-    const uint64_t gg = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
-    const uint32_t a_ = (uint32_t)((uint64_t)n_Q / gg), b_ = (uint32_t)((uint64_t)n_P / gg);
     float* spts = (float*)ctx->x0_pts.p;
-    uint32_t vP, vP2, vQ, vQ2;
-    if (split) {  // bin-block byte offset as a float: P -> 0, Q -> 4 * NQ * WPB
-        using G = ddks::GeoX0<D, true>;
-        const float off = (float)(4 * G::NQ * G::WPB);
-        uint32_t ob;
-        memcpy(&ob, &off, 4);
-        vP = 0u, vP2 = 0u, vQ = ob, vQ2 = 0u;
-    } else {      // DIFF increments for low / high 16-bit halves
-        vP = a_, vP2 = a_ << 16, vQ = 0u - b_, vQ2 = (0u - b_) << 16;
-    }
-    ddks::k_permute_sorted<<<g, 256, 0, st>>>(packed, DP, DPS, D, N, n_P, src, vP, vP2, vQ, vQ2, spts,
-                                              (int32_t*)ctx->x0_perm.p);
+    ddks::k_permute_rows<<<g, 256, 0, st>>>(packed, DP, N, src, spts, (int32_t*)ctx->x0_perm.p);
     CHECK_LAUNCH();
     ctx->launches++;
-    CU(cudaMemsetAsync(spts + N * DPS, 0, 2 * DPS * 4, st));  // the prefetch past the last point reads zeros
+    CU(cudaMemsetAsync(spts + N * DP, 0, 4 * DP * 4, st));  // the prefetch past the last row reads zeros
     CU(cudaMemsetAsync(per_origin, 0, (size_t)N * 8, st));
+    const uint64_t gg = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
+    const uint32_t a_ = (uint32_t)((uint64_t)n_Q / gg), b_ = (uint32_t)((uint64_t)n_P / gg);
     CountPlan pl{1, (int32_t)N, (int32_t)n_P, (int32_t)o_begin, (int32_t)o_end, n_P, n_Q, split,
                  split ? 32767 : (int64_t)(32767 / std::max(a_, b_))};
     ddks::CountArgs a{};
     a.pts = spts;
-    a.item_stride = N * DPS;
+    a.item_stride = N * DP;
     a.N = (int32_t)N;
     a.n_P = (int32_t)n_P;
     a.o_begin = (int32_t)o_begin;

@@ -256,22 +256,23 @@ __device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
 
 // Float-encoded counter address of the pair (origin o, point x): base + sum_k [x_k >= o_k] * 4 * 2^k * WPB, as d
 // FSET.BF (ALU pipe) + d FFMA-immediate (FMA pipe); exact, every partial sum is an integer < 2^24.
-template <int D, bool GT, int WPB, bool SPLIT_CHAIN = (D >= 6)>
+// Dims [FIRST, D) only: FIRST == 1 when bit 0 was decided for the whole tile (x0 ordering) and folded into base.
+template <int D, bool GT, int WPB, int FIRST = 0, bool SPLIT_CHAIN = (D >= 6)>
 __device__ __forceinline__ float code_addr(const float (&x)[D], const float (&o)[D], float base) {
     if constexpr (SPLIT_CHAIN) {
         // two half-length FFMA chains shorten the dependency chain when few warps are resident (d >= 6 keeps 256+
         // counters per origin in SMEM)
-        constexpr int H = D / 2;
+        constexpr int H = (D + FIRST) / 2;
         float f0 = base, f1 = 0.0f;
 #pragma unroll
-        for (int k = 0; k < H; ++k) f0 = fmaf(cmp_bit<GT>(x[k], o[k]), (float)(4 * (1 << k) * WPB), f0);
+        for (int k = FIRST; k < H; ++k) f0 = fmaf(cmp_bit<GT>(x[k], o[k]), (float)(4 * (1 << k) * WPB), f0);
 #pragma unroll
         for (int k = H; k < D; ++k) f1 = fmaf(cmp_bit<GT>(x[k], o[k]), (float)(4 * (1 << k) * WPB), f1);
         return f0 + f1;
     } else {
         float f = base;
 #pragma unroll
-        for (int k = 0; k < D; ++k) f = fmaf(cmp_bit<GT>(x[k], o[k]), (float)(4 * (1 << k) * WPB), f);
+        for (int k = FIRST; k < D; ++k) f = fmaf(cmp_bit<GT>(x[k], o[k]), (float)(4 * (1 << k) * WPB), f);
         return f;
     }
 }
@@ -281,7 +282,7 @@ __device__ __forceinline__ float code_addr(const float (&x)[D], const float (&o)
 // base[r % NB_] is the float-encoded address of origin slot r's bin-0 word; weights 4 * 2^k * WPB. inc_lo / inc_hi:
 // the increment for low-half / high-half origins (R == 1: the caller passes this thread's increment in both).
 // With R <= 2 origins per thread two points are classified per step, so a warp has 2R independent chains in flight.
-template <int D, bool GT, int R, int RP, int NB_, int WPB, int DP>
+template <int D, bool GT, int R, int RP, int NB_, int WPB, int DP, int FIRST = 0>
 __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, const float (&o)[R][D],
                                              const float (&base)[NB_], uint32_t ubase, uint32_t inc_lo,
                                              uint32_t inc_hi) {
@@ -304,8 +305,8 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 // two points in flight already give 2R independent chains: no chain split
-                fa[r] = code_addr<D, GT, WPB, false>(xa, o[r], base[r % NB_]);
-                fb[r] = code_addr<D, GT, WPB, false>(xb, o[r], base[r % NB_]);
+                fa[r] = code_addr<D, GT, WPB, FIRST, false>(xa, o[r], base[r % NB_]);
+                fb[r] = code_addr<D, GT, WPB, FIRST, false>(xb, o[r], base[r % NB_]);
             }
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -317,7 +318,7 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
         if (p < hi) {
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                red_add_shared(__float_as_uint(code_addr<D, GT, WPB>(na, o[r], base[r % NB_])) + ubase,
+                red_add_shared(__float_as_uint(code_addr<D, GT, WPB, FIRST>(na, o[r], base[r % NB_])) + ubase,
                                (R >= 2 && r < RP) ? inc_lo : inc_hi);
         }
         return;
@@ -332,12 +333,15 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
         load_point<D>(tile + (p + 1) * DP, xn);
 #pragma unroll
         for (int r = 0; r < R; ++r)
-            red_add_shared(__float_as_uint(code_addr<D, GT, WPB>(x, o[r], base[r % NB_])) + ubase,
+            red_add_shared(__float_as_uint(code_addr<D, GT, WPB, FIRST>(x, o[r], base[r % NB_])) + ubase,
                            (R >= 2 && r < RP) ? inc_lo : inc_hi);
     }
 }
 
-template <int D, bool SPLIT, bool GT>
+// X0: the rows are in x0 order (label-major: P rows sorted by x_0, then Q rows sorted by x_0; a.perm maps a row back
+// to its pooled index), and bit 0 is decided per tile when the tile's x_0 range does not interleave with the CTA's
+// origins' (DESIGN.md §7 "x0 ordering").
+template <int D, bool SPLIT, bool GT, bool X0 = false>
 __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a) {
     using G = Geo<D, SPLIT>;
     constexpr int R = G::R, RP = G::RP, T = G::T, DP = G::DP, TILE = G::TILE, S = G::S, NBASE = G::NBASE,
@@ -398,6 +402,23 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
     // R == 1: this thread's single origin is a low or a high half for its whole life
     const uint32_t incP_lo = (R == 1 && G::high(0, t)) ? incP_hi : a.incP;
     const uint32_t incQ_lo = (R == 1 && G::high(0, t)) ? incQ_hi : a.incQ;
+    // X0: the x_0 range of this CTA's origins (each label run is ascending) and the bases with bit 0's weight added
+    float o_lo = 0.0f, o_hi = 0.0f;
+    float baseP1[NBASE], baseQ1[NBASE];
+    if constexpr (X0) {
+        const int32_t b0 = blk_o0, b1 = min(a.o_end, blk_o0 + G::ORIGINS) - 1;
+        o_lo = __ldg(pts + (int64_t)b0 * DP);
+        o_hi = __ldg(pts + (int64_t)b1 * DP);
+        if (b0 < a.n_P && b1 >= a.n_P) {  // the block spans the P / Q boundary: two ascending runs
+            o_lo = fminf(o_lo, __ldg(pts + (int64_t)a.n_P * DP));
+            o_hi = fmaxf(o_hi, __ldg(pts + (int64_t)(a.n_P - 1) * DP));
+        }
+#pragma unroll
+        for (int b = 0; b < NBASE; ++b) {
+            baseP1[b] = baseP[b] + (float)(4 * WPB);  // exact: integers < 2^24
+            baseQ1[b] = baseQ[b] + (float)(4 * WPB);
+        }
+    }
 
     for (int it = 0; it < n_tiles; ++it) {
         const int s = it % S;
@@ -408,8 +429,27 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
         // sample-homogeneous sub-ranges: [p0, n_P) are P points, [n_P, ...) are Q points
         int32_t split = a.n_P - p0;
         split = split < 0 ? 0 : (split > cnt ? cnt : split);
-        count_points<D, GT, R, RP, NBASE, WPB, DP>(tile, 0, split, o, baseP, ubase, incP_lo, R == 1 ? incP_lo : incP_hi);
-        count_points<D, GT, R, RP, NBASE, WPB, DP>(tile, split, cnt, o, baseQ, ubase, incQ_lo, R == 1 ? incQ_lo : incQ_hi);
+        int mode = 2;  // 0: bit 0 = 0 for the whole tile, 1: bit 0 = 1, 2: compare all d dims
+        if constexpr (X0) {
+            // the tile's x_0 range (two ascending runs if it holds the P / Q boundary)
+            float t_lo = tile[0], t_hi = tile[(cnt - 1) * DP];
+            if (split > 0 && split < cnt) {
+                t_lo = fminf(t_lo, tile[split * DP]);
+                t_hi = fmaxf(t_hi, tile[(split - 1) * DP]);
+            }
+            // bit 0 = [x_0 >= o_0] (GT: >) is uniform over tile x origins when the ranges do not interleave
+            if (GT ? (t_hi <= o_lo) : (t_hi < o_lo)) mode = 0;
+            else if (GT ? (t_lo > o_hi) : (t_lo >= o_hi)) mode = 1;
+        }
+        if (mode == 2) {
+            count_points<D, GT, R, RP, NBASE, WPB, DP>(tile, 0, split, o, baseP, ubase, incP_lo, R == 1 ? incP_lo : incP_hi);
+            count_points<D, GT, R, RP, NBASE, WPB, DP>(tile, split, cnt, o, baseQ, ubase, incQ_lo, R == 1 ? incQ_lo : incQ_hi);
+        } else if constexpr (X0) {
+            count_points<D, GT, R, RP, NBASE, WPB, DP, 1>(tile, 0, split, o, mode ? baseP1 : baseP, ubase, incP_lo,
+                                                          R == 1 ? incP_lo : incP_hi);
+            count_points<D, GT, R, RP, NBASE, WPB, DP, 1>(tile, split, cnt, o, mode ? baseQ1 : baseQ, ubase, incQ_lo,
+                                                          R == 1 ? incQ_lo : incQ_hi);
+        }
         __syncthreads();  // every thread is done with stage s
         if (t == 0 && it + S < n_tiles) {
             fence_proxy_async();
@@ -461,197 +501,29 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
     }
 }
 
-// ----------------------------------------------------------------------------------------------- x0-ordered count
-// Bit-0 elision (DESIGN.md §7 "x0 ordering"). The pooled points are reordered by x_0 (a 4-pass radix sort of
-// (key(x_0), index)); a CTA's origins are then R*T consecutive points of that order, so their x_0 values lie in
-// [o_lo, o_hi], and a whole tile of points with max x_0 < o_lo (or min x_0 >= o_hi) has the same bit 0 for every
-// pair of the CTA: bit 0 is decided once per tile and only dims 1..d-1 are compared. Tiles that overlap [o_lo, o_hi]
-// (about (R*T + 2*TILE)/N of them) take the full d compares. The counts are exactly those of k_count.
-// Sorted row layout [N][DPS] (the label no longer follows from the position, so each row carries it):
-//   DIFF:  x_0..x_{d-1}, increment for low-half counters (P -> +a, Q -> -b), the same for high halves (<< 16);
-//   SPLIT: x_0..x_{d-1}, the byte offset of the point's bin block as a float (0 for P, 4*NQ*WPB for Q).
-template <int D> __host__ __device__ constexpr int sorted_dim() { return (D + 2 + 3) / 4 * 4; }
-
-__global__ void k_x0_keys(const float* __restrict__ pts, int DP, int64_t N, uint64_t* __restrict__ keys) {
+// ----------------------------------------------------------------------------------------------- x0 ordering
+// Bit-0 elision (DESIGN.md §7 "x0 ordering"): the pooled rows are reordered label-major by x_0 (P rows sorted by x_0,
+// then Q rows sorted by x_0; a 5-pass stable radix sort of (label, key(x_0), index)), so tiles stay
+// sample-homogeneous and a CTA's origins are R*T consecutive rows whose x_0 values span [o_lo, o_hi]. k_count<X0>
+// then decides bit 0 once per tile when the tile's x_0 range does not interleave with that span.
+__global__ void k_x0_keys(const float* __restrict__ pts, int DP, int64_t N, int64_t n_P, uint64_t* __restrict__ keys) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
-        keys[i] = ((uint64_t)f32_key(pts[i * DP]) << 32) | (uint64_t)i;
+        keys[i] = ((uint64_t)(i >= n_P) << 63) | ((uint64_t)f32_key(pts[i * DP]) << 31) | (uint64_t)i;
 }
 
-// slot d / d+1 of every row: (valP, valP2) for P points, (valQ, valQ2) for Q points (bit patterns)
-__global__ void k_permute_sorted(const float* __restrict__ pts, int DP, int DPS, int d, int64_t N, int64_t n_P,
-                                 const uint64_t* __restrict__ keys, uint32_t valP, uint32_t valP2, uint32_t valQ,
-                                 uint32_t valQ2, float* __restrict__ out, int32_t* __restrict__ perm) {
+// out[j] = pts[idx_j] (whole padded rows), perm[j] = idx_j (the pooled index, < 2^31)
+__global__ void k_permute_rows(const float* __restrict__ pts, int DP, int64_t N, const uint64_t* __restrict__ keys,
+                               float* __restrict__ out, int32_t* __restrict__ perm) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t idx = (int64_t)(uint32_t)keys[j];
-        const bool isP = idx < n_P;
-        for (int k = 0; k < DPS; ++k) {
-            float v = 0.0f;
-            if (k < d) v = pts[idx * DP + k];
-            else if (k == d) v = __uint_as_float(isP ? valP : valQ);
-            else if (k == d + 1) v = __uint_as_float(isP ? valP2 : valQ2);
-            out[j * DPS + k] = v;
-        }
+        const int64_t idx = (int64_t)(keys[j] & 0x7fffffffull);
+        const float4* src = reinterpret_cast<const float4*>(pts + idx * DP);
+        float4* dst = reinterpret_cast<float4*>(out + j * DP);
+        dst[0] = src[0];
+        if (DP == 8) dst[1] = src[1];
         perm[j] = (int32_t)idx;
     }
 }
 
-template <int D, int DPS>
-__device__ __forceinline__ void load_sorted(const float* sp, float (&x)[D], uint32_t& e0, uint32_t& e1) {
-    float v[DPS];
-#pragma unroll
-    for (int i = 0; i < DPS; i += 4) {
-        const float4 a = *reinterpret_cast<const float4*>(sp + i);
-        v[i] = a.x, v[i + 1] = a.y, v[i + 2] = a.z, v[i + 3] = a.w;
-    }
-#pragma unroll
-    for (int k = 0; k < D; ++k) x[k] = v[k];
-    e0 = __float_as_uint(v[D]);
-    e1 = __float_as_uint(v[D + 1]);
-}
-
-// dims [FIRST, D) of every point in [0, n) against this thread's R origins; base already holds bit 0's weight.
-// DIFF: the increment comes with the point (e0 for low halves, e1 for high halves; R == 1: HI picks this thread's).
-// SPLIT: the point's bin-block offset e0 is added to the base, the increment is 1 (low half) or 1 << 16 (high).
-template <int D, bool SPLIT, bool GT, int FIRST, int R, int RP, int NB_, int WPB, int DPS>
-__device__ __forceinline__ void count_sorted(const float* tile, int n, const float (&o)[R][D], const float (&base)[NB_],
-                                             uint32_t ubase, bool hi1) {
-    float xn[D];
-    uint32_t e0n, e1n;
-    load_sorted<D, DPS>(tile, xn, e0n, e1n);
-#pragma unroll 4
-    for (int p = 0; p < n; ++p) {
-        float x[D];
-#pragma unroll
-        for (int k = 0; k < D; ++k) x[k] = xn[k];
-        const uint32_t e0 = e0n, e1 = e1n;
-        load_sorted<D, DPS>(tile + (p + 1) * DPS, xn, e0n, e1n);  // index n <= TILE: inside the allocation, unused
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const bool high = R >= 2 ? (r >= RP) : hi1;
-            float f = SPLIT ? base[r % NB_] + __uint_as_float(e0) : base[r % NB_];
-#pragma unroll
-            for (int k = FIRST; k < D; ++k) f = fmaf(cmp_bit<GT>(x[k], o[r][k]), (float)(4 * (1 << k) * WPB), f);
-            const uint32_t inc = SPLIT ? (high ? (1u << 16) : 1u) : (high ? e1 : e0);
-            red_add_shared(__float_as_uint(f) + ubase, inc);
-        }
-    }
-}
-
-template <int D, bool SPLIT>
-using GeoX0 = Geo<D, SPLIT, sorted_dim<D>()>;
-
-template <int D, bool SPLIT, bool GT>
-__global__ void __launch_bounds__(GeoX0<D, SPLIT>::T, 1) k_count_x0(const CountArgs a) {
-    using G = GeoX0<D, SPLIT>;
-    constexpr int R = G::R, RP = G::RP, T = G::T, DPS = G::DP, TILE = G::TILE, S = G::S, NBASE = G::NBASE,
-                  WPB = G::WPB;
-    extern __shared__ __align__(128) uint8_t smem[];
-    float* tiles = reinterpret_cast<float*>(smem);
-    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + S * G::TILE_BYTES);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * G::TILE_BYTES + G::HIST_WORDS * 4);
-    const int t = threadIdx.x;
-    const float* pts = a.pts;
-    const int32_t blk_o0 = a.o_begin + (int32_t)blockIdx.y * G::ORIGINS;
-    const int32_t blk_o1 = min(a.o_end, blk_o0 + G::ORIGINS);
-    const int32_t seg0 = (int32_t)blockIdx.x * a.seg_points;
-    const int32_t seg1 = min(a.N, seg0 + a.seg_points);
-    const int n_tiles = (seg1 - seg0 + TILE - 1) / TILE;
-    if (t == 0) {
-#pragma unroll
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    for (int i = t; i < G::HIST_WORDS; i += T) hist[i] = 0u;
-    __syncthreads();
-    if (t == 0) {
-        for (int s = 0; s < S && s < n_tiles; ++s) {
-            const int32_t p0 = seg0 + s * TILE;
-            const uint32_t bytes = (uint32_t)(min(TILE, seg1 - p0) * DPS * 4);
-            mbar_expect_tx(&bars[s], bytes);
-            bulk_g2s(tiles + s * TILE * DPS, pts + (int64_t)p0 * DPS, bytes, &bars[s]);
-        }
-    }
-    float o[R][D];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        int32_t oi = blk_o0 + r * T + t;
-        oi = oi < a.o_end ? oi : a.o_end - 1;
-#pragma unroll
-        for (int k = 0; k < D; ++k) o[r][k] = __ldg(pts + (int64_t)oi * DPS + k);
-    }
-    // x_0 range of this CTA's origins (sorted order: first and last)
-    const float o_lo = __ldg(pts + (int64_t)blk_o0 * DPS), o_hi = __ldg(pts + (int64_t)(blk_o1 - 1) * DPS);
-    const uint32_t ubase = smem_u32(hist) - 0x4B000000u;
-    float base0[NBASE], base1[NBASE];
-#pragma unroll
-    for (int b = 0; b < NBASE; ++b) {
-        base0[b] = __uint_as_float(0x4B000000u + 4u * (uint32_t)G::slot(b, t));
-        base1[b] = base0[b] + (float)(4 * WPB);  // + bit 0's weight (exact: integers < 2^24)
-    }
-    const bool hi1 = G::high(0, t);  // R == 1: this thread's origin is a high half
-    for (int it = 0; it < n_tiles; ++it) {
-        const int s = it % S;
-        mbar_wait(&bars[s], (uint32_t)((it / S) & 1));
-        const float* tile = tiles + s * TILE * DPS;
-        const int32_t p0 = seg0 + it * TILE;
-        const int cnt = min(TILE, seg1 - p0);
-        const float t_lo = tile[0], t_hi = tile[(cnt - 1) * DPS];
-        // bit 0 = [x_0 >= o_0] (GT: >) is uniform over the tile x origins when the value ranges do not interleave
-        const bool all0 = GT ? (t_hi <= o_lo) : (t_hi < o_lo);
-        const bool all1 = GT ? (t_lo > o_hi) : (t_lo >= o_hi);
-        if (all0)      count_sorted<D, SPLIT, GT, 1, R, RP, NBASE, WPB, DPS>(tile, cnt, o, base0, ubase, hi1);
-        else if (all1) count_sorted<D, SPLIT, GT, 1, R, RP, NBASE, WPB, DPS>(tile, cnt, o, base1, ubase, hi1);
-        else           count_sorted<D, SPLIT, GT, 0, R, RP, NBASE, WPB, DPS>(tile, cnt, o, base0, ubase, hi1);
-        __syncthreads();
-        if (t == 0 && it + S < n_tiles) {
-            fence_proxy_async();
-            const int32_t q0 = seg0 + (it + S) * TILE;
-            const uint32_t bytes = (uint32_t)(min(TILE, seg1 - q0) * DPS * 4);
-            mbar_expect_tx(&bars[s], bytes);
-            bulk_g2s(tiles + s * TILE * DPS, pts + (int64_t)q0 * DPS, bytes, &bars[s]);
-        }
-    }
-    __syncthreads();
-    const int32_t n_orig = a.o_end - a.o_begin;
-    if (a.accum != nullptr) {
-        int32_t* acc = a.accum;
-#pragma unroll 1
-        for (int r = 0; r < R; ++r) {
-            const int32_t oi = blk_o0 + r * T + t;
-            if (oi >= a.o_end) continue;
-            const int sl = G::slot(r, t);
-            const bool hiw = G::high(r, t);
-#pragma unroll 4
-            for (int q = 0; q < G::NB; ++q) {
-                int32_t lo, hi;
-                split16(hist[q * WPB + sl], lo, hi);
-                const int32_t v = hiw ? hi : lo;
-                if (v) atomicAdd(&acc[(int64_t)q * n_orig + (oi - a.o_begin)], v);
-            }
-        }
-        return;
-    }
-    uint64_t best = 0;
-#pragma unroll 1
-    for (int r = 0; r < R; ++r) {
-        const int32_t oi = blk_o0 + r * T + t;
-        if (oi >= a.o_end) continue;
-        const uint64_t m = origin_num<D, SPLIT>(hist, r, t, a);
-        if (a.per_origin) a.per_origin[a.perm[oi]] = m;
-        best = m > best ? m : best;
-    }
-    best = warp_max_u64(best);
-    __shared__ uint64_t wmax[32];
-    if ((t & 31) == 0) wmax[t >> 5] = best;
-    __syncthreads();
-    if (t == 0) {
-        uint64_t m = 0;
-        for (int w = 0; w < T / 32; ++w) m = wmax[w] > m ? wmax[w] : m;
-        atomicMax(reinterpret_cast<unsigned long long*>(&a.item_num[0]), (unsigned long long)m);
-    }
-}
-
-// Finalise accumulate mode: one thread per (item, origin).
 // SPLIT with a.hist (significance): M_T values below HS are histogrammed in a block-private SMEM histogram first and
 // flushed once per block; larger values (rare) go straight to global memory.
 constexpr int HS = 2048;
