@@ -325,7 +325,7 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
     }
     float xn[D];
     load_point<D>(tile + p * DP, xn);
-#pragma unroll 4
+#pragma unroll 8
     for (; p < hi; ++p) {
         float x[D];
 #pragma unroll
