@@ -294,7 +294,7 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
         float na[D], nb[D];
         load_point<D>(tile + p * DP, na);
         load_point<D>(tile + (p + 1) * DP, nb);
-#pragma unroll 2
+#pragma unroll 4
         for (; p + 1 < hi; p += 2) {
             float xa[D], xb[D];
 #pragma unroll
@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(PermGeo<D>::T, 1) k_perm_count(const PermArgs 
         const float* sp = reinterpret_cast<const float*>(stages + s * G::STAGE_BYTES);
         const uint32_t* sl = reinterpret_cast<const uint32_t*>(stages + s * G::STAGE_BYTES + TILE * DP * 4);
         const int n = min(TILE, a.N - it * TILE);
-#pragma unroll 2
+#pragma unroll 4
         for (int p = 0; p < n; ++p) {
             float x[D];
             load_point<D>(sp + p * DP, x);
