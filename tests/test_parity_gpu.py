@@ -324,3 +324,28 @@ def test_x0_ordered_ties_gt(ctx_x0_gt, d):
     want = O.ddks(P, Q, ties_gt=True)
     got = ctx_x0_gt.stat(dev(P), dev(Q))
     assert (got.num, got.den, got.argmax_origin) == (want[0], want[1], want[3])
+
+
+# ----------------------------------------------------------------------------------- launch-limit edge paths
+
+def test_batch_beyond_grid_z_limit(ctx):
+    # B > 65535 items: the library runs the items in grid.z chunks of 65535
+    rng = np.random.default_rng(17)
+    B = 70_001
+    P = rng.integers(0, 3, (B, 4, 2)).astype(np.float32)
+    Q = rng.integers(0, 3, (B, 3, 2)).astype(np.float32)
+    got = ctx.stat_batch(dev(P), dev(Q))
+    want = O.batch(P, Q)
+    assert np.array_equal(got.num, want) and np.all(got.den == 12)
+
+
+def test_permutation_null_beyond_label_path(ctx):
+    # N > 65535 pooled points: the label-invariant kernel's 16-bit counters do not apply, so the library gathers
+    # each relabelled sample and re-runs the full classification (x0 / position-ordered count)
+    rng = np.random.default_rng(19)
+    n_P, n_Q = 33_000, 33_001
+    pooled = np.round(rng.standard_normal((n_P + n_Q, 1)) * 50).astype(np.float32)  # d = 1, tie-heavy
+    perms = np.stack([np.arange(n_P + n_Q), rng.permutation(n_P + n_Q)]).astype(np.int32)
+    null, obs, p = ctx.permutation_null(dev(pooled), n_P, dev(perms))
+    o_null, o_obs, o_pnum, o_p = O.permutation_null(pooled, n_P, perms)
+    assert np.array_equal(null, o_null) and obs.num == o_obs and p == o_p
