@@ -277,10 +277,13 @@ class Step:
             what = "whole vdKS step (pack, voxel histogram, prefix passes, orthant sums)"
         else:
             keys = (d + 1) * N * 8
-            # input read, f64 x' write + read, key write, 8 radix passes x (hist read + scatter read + write),
-            # count + sweep reads (DESIGN.md §7 rdKS)
-            byts = N * d * 4 + 2 * N * d * 8 + keys + 8 * 3 * keys + 2 * keys
-            what = "whole rdKS step (normalise, distance keys, 8-pass radix sort, sweep)"
+            nbk = 256
+            while nbk < N // 4 and nbk < (1 << 20):
+                nbk <<= 1
+            # input read, f64 x' write + read, key write, two key reads (bucket count, candidate compaction), and per
+            # bucket: count atomics, two scan reads, start-count write, candidate read + offset write
+            byts = N * d * 4 + 2 * N * d * 8 + 3 * keys + (d + 1) * nbk * 52
+            what = "whole rdKS step (normalise, distance keys, bucket-pruned sweep)"
         achieved = byts / (step_ms / 1e3) / 1e9
         peak = float(peaks_.get("hbm_gbs", 6536.7))
         return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -71,6 +71,8 @@ typedef enum {
 #define DDKS_FLAG_NO_X0 32u        /* TEST ONLY: never use the x0-ordered count (ddks_stat sorts the pooled points by x_0 when
                                       2 <= d <= 6 and N >= 200000, so whole tiles share bit 0; identical results)   */
 #define DDKS_FLAG_FORCE_X0 64u     /* TEST ONLY: use the x0-ordered count for any N (2 <= d <= 6, DIFF counters)      */
+#define DDKS_FLAG_RDKS_FULL_SORT 128u /* TEST ONLY: ddks_rdks sorts every key (8-pass radix sort) instead of the bucket-pruned
+                                         sweep that sorts only the buckets able to hold the maximum; identical results */
 #define DDKS_FLAG_PROFILE 8u      /* record CUDA events around every count-kernel launch (see ddks_profile_read) */
 
 typedef struct {

@@ -47,6 +47,7 @@ struct ddks_ctx {
     DevBuf vox_keys, vox_cnt, vox_S;                                           // ddks_vdks workspace
     DevBuf rd_keys, rd_xn, rd_k0, rd_k1, rd_hist, rd_tcnt, rd_cnum;              // ddks_rdks workspace
     DevBuf x0_keys0, x0_keys1, x0_hist, x0_pts, x0_perm;                        // x0-ordered count workspace
+    DevBuf rdb_cnt, rdb_pst, rdb_coff, rdb_fill, rdb_clist, rdb_csum;            // rdKS bucket-pruned sweep
     void* host_pinned = nullptr;  // DevResult + scratch
     size_t host_pinned_bytes = 0;
     int64_t launches = 0;
@@ -590,7 +591,7 @@ ddks_status ddks_create(ddks_ctx** out, int device, int world, int rank, const v
     if (world < 1 || rank < 0 || rank >= world) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad world/rank");
     if ((world == 1) != (nccl_id == nullptr))
         return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "nccl_id must be NULL iff world == 1");
-    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT | DDKS_FLAG_PROFILE | DDKS_FLAG_PERM_GATHER | DDKS_FLAG_NO_X0 | DDKS_FLAG_FORCE_X0)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
+    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT | DDKS_FLAG_PROFILE | DDKS_FLAG_PERM_GATHER | DDKS_FLAG_NO_X0 | DDKS_FLAG_FORCE_X0 | DDKS_FLAG_RDKS_FULL_SORT)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
     int ndev = 0;
     CU(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device %d of %d", device, ndev);
@@ -635,7 +636,8 @@ ddks_status ddks_destroy(ddks_ctx* ctx) {
                       &ctx->sig_lf, &ctx->sig_scratch, &ctx->sig_table, &ctx->sig_contrib, &ctx->sig_part,
                       &ctx->vox_keys, &ctx->vox_cnt, &ctx->vox_S, &ctx->rd_keys, &ctx->rd_xn, &ctx->rd_k0,
                       &ctx->rd_k1, &ctx->rd_hist, &ctx->rd_tcnt, &ctx->rd_cnum, &ctx->x0_keys0,
-                      &ctx->x0_keys1, &ctx->x0_hist, &ctx->x0_pts, &ctx->x0_perm})
+                      &ctx->x0_keys1, &ctx->x0_hist, &ctx->x0_pts, &ctx->x0_perm, &ctx->rdb_cnt,
+                      &ctx->rdb_pst, &ctx->rdb_coff, &ctx->rdb_fill, &ctx->rdb_clist, &ctx->rdb_csum})
         if (b->p) cudaFree(b->p);
     if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
     delete ctx;
@@ -1185,12 +1187,11 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     ddks::k_rd_normalize<<<grid_for(N * d), 256, 0, st>>>((const float*)dP, n_P, (const float*)dQ, n_Q, d, keys, xn);
     CHECK_LAUNCH();
     ctx->launches++;
-    if (nc > 0) {
-        ddks::k_rd_keys<<<grid_for(N * nc), 256, 0, st>>>(xn, N, n_P, d, (int)cb, (int)ce, k0);
-        CHECK_LAUNCH();
-        ctx->launches++;
+    // full path: segmented 8-pass LSD radix sort of every corner's keys, then the tie-complete sweep
+    auto full_sort = [&]() -> ddks_status {
         const int blocks = nc * tiles;
         uint64_t *src = k0, *dst = k1;
+        CU(cudaMemsetAsync(cnum, 0, (size_t)(d + 1) * 8, st));
         for (int shift = 0; shift < 64; shift += 8) {
             ddks::k_rs_hist<<<blocks, ddks::RS_T, 0, st>>>(src, N, tiles, shift, hist);
             ddks::k_rs_scan<<<nc, 256 * ddks::RS_SCAN_PARTS, 0, st>>>(hist, tiles);
@@ -1203,6 +1204,50 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
         ddks::k_rd_sweep<<<blocks, ddks::RS_T, 0, st>>>(src, N, tiles, n_P, n_Q, tcnt, cnum);
         CHECK_LAUNCH();
         ctx->launches += 2;
+        return DDKS_OK;
+    };
+    const bool pruned = !(ctx->flags & DDKS_FLAG_RDKS_FULL_SORT);
+    if (nc > 0) {
+        ddks::k_rd_keys<<<grid_for(N * nc), 256, 0, st>>>(xn, N, n_P, d, (int)cb, (int)ce, k0);
+        CHECK_LAUNCH();
+        ctx->launches++;
+        if (pruned) {
+            // bucket-pruned sweep: bucket counts, exact bucket-end values, sort only the buckets that can beat them
+            int nbk = 256;
+            while (nbk < N / 4 && nbk < (1 << 20)) nbk <<= 1;
+            const double scale = (double)nbk / (std::sqrt((double)d) * (1.0 + 1e-9));
+            const size_t nb = (size_t)nc * nbk;
+            if ((s = ensure(ctx, ctx->rdb_cnt, nb * 8))) return s;
+            if ((s = ensure(ctx, ctx->rdb_pst, nb * 8))) return s;
+            if ((s = ensure(ctx, ctx->rdb_coff, nb * 4))) return s;
+            if ((s = ensure(ctx, ctx->rdb_fill, nb * 4))) return s;
+            if ((s = ensure(ctx, ctx->rdb_clist, nb * 4))) return s;
+            if ((s = ensure(ctx, ctx->rdb_csum, ((size_t)nc * ((nbk + ddks::RDB_CH - 1) / ddks::RDB_CH) + nc) * 8))) return s;
+            uint32_t* bcnt = (uint32_t*)ctx->rdb_cnt.p;
+            int32_t* clist = (int32_t*)ctx->rdb_clist.p;
+            CU(cudaMemsetAsync(bcnt, 0, nb * 8, st));
+            CU(cudaMemsetAsync(ctx->rdb_fill.p, 0, nb * 4, st));
+            ddks::k_rdb_count<<<grid_for(N * nc), 256, 0, st>>>(k0, N, nc, nbk, scale, bcnt);
+            const int nch = (nbk + ddks::RDB_CH - 1) / ddks::RDB_CH;
+            uint64_t* csum = (uint64_t*)ctx->rdb_csum.p;
+            uint32_t* segc = (uint32_t*)(csum + (size_t)nc * nch);
+            CU(cudaMemsetAsync(segc, 0, (size_t)nc * 8, st));
+            CU(cudaMemsetAsync(cnum, 0, (size_t)(d + 1) * 8, st));
+            ddks::k_rdb_reduce<<<dim3(nch, nc), 256, 0, st>>>(bcnt, nbk, csum);
+            ddks::k_rdb_chunk_scan<<<nc, 256, 0, st>>>(csum, nch);
+            ddks::k_rdb_down<<<dim3(nch, nc), 256, 0, st>>>(bcnt, nbk, csum, n_P, n_Q, (uint2*)ctx->rdb_pst.p, cnum);
+            ddks::k_rdb_cand<<<grid_for((int64_t)nb), 256, 0, st>>>(bcnt, (const uint2*)ctx->rdb_pst.p, nc, nbk, n_P,
+                                                                    n_Q, cnum, (uint32_t*)ctx->rdb_coff.p, clist, segc);
+            ddks::k_rdb_compact<<<grid_for(N * nc), 256, 0, st>>>(k0, N, nc, nbk, scale, (const uint32_t*)ctx->rdb_coff.p,
+                                                                  (uint32_t*)ctx->rdb_fill.p, k1);
+            ddks::k_rdb_finish<<<dim3(std::max(1, std::min(1024, (148 * 4 + nc - 1) / nc)), nc), 256, 0, st>>>(
+                k1, N, nbk, bcnt, (const uint2*)ctx->rdb_pst.p, (const uint32_t*)ctx->rdb_coff.p, clist, segc, n_P,
+                n_Q, cnum, &dres->flag);
+            CHECK_LAUNCH();
+            ctx->launches += 7;
+        } else if ((s = full_sort())) {
+            return s;
+        }
     }
     if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)(d + 1) * 8))) return s;
     DevResult* hres = (DevResult*)ctx->host_pinned;
@@ -1210,6 +1255,11 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(hc, cnum, (size_t)std::max(nc, 0) * 8, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    if (nc > 0 && pruned && (hres->flag & 256u)) {  // a candidate bucket too large for SMEM: sort everything
+        if ((s = full_sort())) return s;
+        CU(cudaMemcpyAsync(hc, cnum, (size_t)nc * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+    }
     if (ctx->world > 1) {
         NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
         CU(cudaMemcpyAsync(&hres->flag, &dres->flag, 4, cudaMemcpyDeviceToHost, st));

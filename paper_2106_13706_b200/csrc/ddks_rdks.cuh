@@ -329,3 +329,251 @@ __global__ void __launch_bounds__(RS_T) k_rd_sweep(const uint64_t* __restrict__ 
 }
 
 }  // namespace ddks
+
+namespace ddks {
+
+// ------------------------------------------------------------------------------------ bucket-pruned sweep
+// GetDFromCornerLists without sorting every key (DESIGN.md §7 "rdKS"). Distances are bucketed by a monotone map
+// b = min(NBK - 1, floor(dist * scale)) (equal distances share a bucket, so every bucket end is a tie-group end).
+// Per bucket: counts (cP, cQ) and the min / max distance bits. A prefix over the buckets gives the exact ECDF pair at
+// every bucket end; inside bucket b the statistic t = i_P n_Q - i_Q n_P stays within
+// [t_start - cQ n_P, t_start + cP n_Q], so only buckets whose bound beats the best bucket-end value and that hold two
+// distinct distances can hide a larger value: their keys are compacted and sorted in SMEM (bitonic) and swept exactly.
+// A candidate bucket with more than RDB_CAPK keys and two distinct distances sets *flag bit 8 (as does a candidate
+// set larger than N/2), and the caller falls back to the full radix sort.
+constexpr int RDB_CAPK = 4096;
+
+__device__ __forceinline__ int rdb_bucket(uint64_t key, double scale, int nbk) {
+    const double dist = __longlong_as_double((long long)(key >> 1));
+    const double v = __dmul_rn(dist, scale);
+    const int b = v >= (double)(nbk - 1) ? nbk - 1 : (int)v;
+    return b < 0 ? 0 : b;
+}
+
+// cnt[(s * nbk + b) * 2 + label] += 1
+__global__ void k_rdb_count(const uint64_t* __restrict__ key, int64_t N, int nseg, int nbk, double scale,
+                            uint32_t* __restrict__ cnt) {
+    const int64_t total = N * nseg;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = e / N;
+        const uint64_t k = key[e];
+        atomicAdd(&cnt[2 * (s * nbk + rdb_bucket(k, scale, nbk)) + (k & 1ull)], 1u);
+    }
+}
+
+// Bucket prefix sums, many CTAs: a chunk is RDB_CH consecutive buckets of one segment (256 threads x 4 buckets).
+// (cP, cQ) travel packed as cP << 32 | cQ (each < 2^31, so the halves never carry into each other).
+constexpr int RDB_CH = 1024;
+
+__device__ __forceinline__ uint64_t block_excl_scan256_u64(uint64_t v, uint64_t* total = nullptr) {
+    __shared__ uint64_t wsum64[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    __syncthreads();
+    if (lane == 31) wsum64[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint64_t t = lane < 8 ? wsum64[lane] : 0ull;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < 8) wsum64[lane] = t;
+    }
+    __syncthreads();
+    if (total) *total = wsum64[7];
+    return x - v + (w ? wsum64[w - 1] : 0ull);
+}
+
+__device__ __forceinline__ uint64_t rdb_pair(const uint32_t* cnt, int64_t i) {
+    return ((uint64_t)cnt[2 * i] << 32) | cnt[2 * i + 1];
+}
+
+// csum[s * nch + c] = packed (cP, cQ) total of chunk c of segment s. grid (nch, nseg), 256 threads.
+__global__ void __launch_bounds__(256) k_rdb_reduce(const uint32_t* __restrict__ cnt, int nbk,
+                                                    uint64_t* __restrict__ csum) {
+    const int s = blockIdx.y, c = blockIdx.x, nch = gridDim.x;
+    uint64_t v = 0;
+#pragma unroll
+    for (int j = 0; j < RDB_CH / 256; ++j) {
+        const int b = c * RDB_CH + threadIdx.x * (RDB_CH / 256) + j;
+        if (b < nbk) v += rdb_pair(cnt, (int64_t)s * nbk + b);
+    }
+    uint64_t tot;
+    block_excl_scan256_u64(v, &tot);
+    if (threadIdx.x == 0) csum[(int64_t)s * nch + c] = tot;
+}
+
+// exclusive scan of the chunk totals of each segment (one CTA per segment; nch <= 1024 * 4)
+__global__ void __launch_bounds__(256) k_rdb_chunk_scan(uint64_t* __restrict__ csum, int nch) {
+    uint64_t* c = csum + (int64_t)blockIdx.x * nch;
+    const int per = (nch + 255) / 256;
+    uint64_t v = 0;
+    for (int j = 0; j < per; ++j) {
+        const int k = threadIdx.x * per + j;
+        if (k < nch) v += c[k];
+    }
+    uint64_t run = block_excl_scan256_u64(v);
+    for (int j = 0; j < per; ++j) {
+        const int k = threadIdx.x * per + j;
+        if (k < nch) {
+            const uint64_t x = c[k];
+            c[k] = run;
+            run += x;
+        }
+    }
+}
+
+// pst[b] = (P, Q) keys before bucket b; cnum[s] = max over bucket ends of |i_P n_Q - i_Q n_P| (atomicMax; init 0)
+__global__ void __launch_bounds__(256) k_rdb_down(const uint32_t* __restrict__ cnt, int nbk,
+                                                  const uint64_t* __restrict__ csum, int64_t n_P, int64_t n_Q,
+                                                  uint2* __restrict__ pst, unsigned long long* __restrict__ cnum) {
+    const int s = blockIdx.y, c = blockIdx.x, nch = gridDim.x;
+    constexpr int J = RDB_CH / 256;
+    uint64_t v[J], sum = 0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const int b = c * RDB_CH + threadIdx.x * J + j;
+        v[j] = b < nbk ? rdb_pair(cnt, (int64_t)s * nbk + b) : 0ull;
+        sum += v[j];
+    }
+    uint64_t run = csum[(int64_t)s * nch + c] + block_excl_scan256_u64(sum);
+    uint64_t best = 0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const int b = c * RDB_CH + threadIdx.x * J + j;
+        if (b >= nbk) break;
+        pst[(int64_t)s * nbk + b] = make_uint2((uint32_t)(run >> 32), (uint32_t)run);
+        run += v[j];
+        const int64_t t = (int64_t)(run >> 32) * n_Q - (int64_t)(uint32_t)run * n_P;
+        const uint64_t a = (uint64_t)(t < 0 ? -t : t);
+        best = a > best ? a : best;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t w = __shfl_xor_sync(0xffffffffu, best, o);
+        best = w > best ? w : best;
+    }
+    if ((threadIdx.x & 31) == 0 && best) atomicMax(&cnum[s], (unsigned long long)best);
+}
+
+// Candidates: at least two keys inside, and the reachable extreme beats the best bucket end (cnum[s] after
+// k_rdb_down). Each gets a slot in the segment's candidate buffer (coff) and list (clist) by atomics on the
+// segment's counters seg[2 * s] (keys) and seg[2 * s + 1] (buckets); non-candidates get coff = ~0u.
+__global__ void k_rdb_cand(const uint32_t* __restrict__ cnt, const uint2* __restrict__ pst, int nseg,
+                           int nbk, int64_t n_P, int64_t n_Q, const unsigned long long* __restrict__ cnum,
+                           uint32_t* __restrict__ coff, int32_t* __restrict__ clist, uint32_t* __restrict__ seg) {
+    const int64_t total = (int64_t)nseg * nbk;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int s = (int)(i / nbk);
+        const uint2 st = pst[i];
+        const int64_t cp = cnt[2 * i], cq = cnt[2 * i + 1];
+        const int64_t t0 = (int64_t)st.x * n_Q - (int64_t)st.y * n_P;
+        const int64_t hi = t0 + cp * n_Q, lo = t0 - cq * n_P;
+        const uint64_t bound = (uint64_t)max(hi < 0 ? -hi : hi, lo < 0 ? -lo : lo);
+        if (cp + cq >= 2 && bound > cnum[s]) {
+            coff[i] = atomicAdd(&seg[2 * s], (uint32_t)(cp + cq));
+            clist[(int64_t)s * nbk + atomicAdd(&seg[2 * s + 1], 1u)] = (int32_t)(i - (int64_t)s * nbk);
+        } else {
+            coff[i] = ~0u;
+        }
+    }
+}
+
+// candidate keys, grouped by bucket (order inside a bucket arbitrary): ck[s * N + coff[b] + k]
+__global__ void k_rdb_compact(const uint64_t* __restrict__ key, int64_t N, int nseg, int nbk, double scale,
+                              const uint32_t* __restrict__ coff, uint32_t* __restrict__ fill,
+                              uint64_t* __restrict__ ck) {
+    const int64_t total = N * nseg;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = e / N;
+        const uint64_t k = key[e];
+        const int64_t b = s * nbk + rdb_bucket(k, scale, nbk);
+        const uint32_t o = coff[b];
+        if (o != ~0u) ck[s * N + o + atomicAdd(&fill[b], 1u)] = k;
+    }
+}
+
+// One CTA per candidate bucket (grid-stride over the segment's list): bitonic sort of its <= RDB_CAPK keys in SMEM,
+// then the exact sweep from the bucket's start counts; atomicMax into cnum[s].
+__global__ void __launch_bounds__(256) k_rdb_finish(const uint64_t* __restrict__ ck, int64_t N, int nbk,
+                                                    const uint32_t* __restrict__ cnt, const uint2* __restrict__ pst,
+                                                    const uint32_t* __restrict__ coff,
+                                                    const int32_t* __restrict__ clist,
+                                                    const uint32_t* __restrict__ seg, int64_t n_P, int64_t n_Q,
+                                                    unsigned long long* __restrict__ cnum, uint32_t* flag) {
+    __shared__ uint64_t sk[RDB_CAPK];
+    const int s = blockIdx.y;
+    // too many candidate keys (e.g. nearly identical samples): cheaper to sort everything, the caller falls back
+    if (seg[2 * s] > (uint32_t)(N / 2)) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) atomicOr(flag, 256u);
+        return;
+    }
+    for (int k = blockIdx.x; k < (int)seg[2 * s + 1]; k += gridDim.x) {
+        const int b = clist[(int64_t)s * nbk + k];
+        const int64_t i = (int64_t)s * nbk + b;
+        const int n = (int)(cnt[2 * i] + cnt[2 * i + 1]);
+        if (n > RDB_CAPK) {
+            // too large for SMEM: harmless if every key has the same distance (no tie-group end inside), else the
+            // caller re-runs the full sort
+            const uint64_t* src = ck + (int64_t)s * N + coff[i];
+            uint64_t mn = ~0ull, mx = 0;
+            for (int j = threadIdx.x; j < n; j += blockDim.x) mn = min(mn, src[j] >> 1), mx = max(mx, src[j] >> 1);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                mn = min(mn, (uint64_t)__shfl_xor_sync(0xffffffffu, mn, o));
+                mx = max(mx, (uint64_t)__shfl_xor_sync(0xffffffffu, mx, o));
+            }
+            if ((threadIdx.x & 31) == 0 && mn != mx) atomicOr(flag, 256u);
+            continue;
+        }
+        int np2 = 1;
+        while (np2 < n) np2 <<= 1;
+        const uint64_t* src = ck + (int64_t)s * N + coff[i];
+        for (int j = threadIdx.x; j < np2; j += blockDim.x) sk[j] = j < n ? src[j] : ~0ull;
+        __syncthreads();
+        for (int size = 2; size <= np2; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int j = threadIdx.x; j < np2; j += blockDim.x) {
+                    const int p = j ^ stride;
+                    if (p > j) {
+                        const bool up = (j & size) == 0;
+                        const uint64_t a = sk[j], c = sk[p];
+                        if ((a > c) == up) sk[j] = c, sk[p] = a;
+                    }
+                }
+                __syncthreads();
+            }
+        // sweep: blocked arrangement, 16 keys per thread (256 x 16 = RDB_CAPK)
+        const uint2 st = pst[i];
+        uint32_t mine = 0;
+        const int j0 = threadIdx.x * (RDB_CAPK / 256);
+        for (int j = j0; j < j0 + RDB_CAPK / 256 && j < n; ++j) mine += (uint32_t)((sk[j] & 1ull) == 0);
+        uint32_t before = block_excl_scan256(mine);
+        int64_t iP = (int64_t)st.x + before;
+        uint64_t best = 0;
+        for (int j = j0; j < j0 + RDB_CAPK / 256 && j < n; ++j) {
+            iP += (int64_t)((sk[j] & 1ull) == 0);
+            if (j + 1 < n && (sk[j + 1] >> 1) == (sk[j] >> 1)) continue;  // not a tie-group end
+            const int64_t iQ = (int64_t)st.x + st.y + j + 1 - iP;
+            const int64_t t = iP * n_Q - iQ * n_P;
+            const uint64_t a = (uint64_t)(t < 0 ? -t : t);
+            best = a > best ? a : best;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t v = __shfl_xor_sync(0xffffffffu, best, o);
+            best = v > best ? v : best;
+        }
+        if ((threadIdx.x & 31) == 0 && best) atomicMax(&cnum[s], (unsigned long long)best);
+        __syncthreads();  // sk is reused by the next bucket
+    }
+}
+
+}  // namespace ddks

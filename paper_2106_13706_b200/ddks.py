@@ -27,6 +27,7 @@ DDKS_FLAG_PROFILE = 8
 DDKS_FLAG_PERM_GATHER = 16
 DDKS_FLAG_NO_X0 = 32
 DDKS_FLAG_FORCE_X0 = 64
+DDKS_FLAG_RDKS_FULL_SORT = 128
 DDKS_SIG_POISSON = 1
 
 

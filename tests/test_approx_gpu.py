@@ -123,3 +123,20 @@ def test_rdks_configs_full(ctx, name):
     want = O.rdks(P, Q)
     got = ctx.rdks(dev(P), dev(Q))
     assert (got.num, got.den, got.argmax_origin) == (want[0], want[1], want[3])
+
+
+def test_rdks_pruned_equals_full_sort_and_fallback(ctx):
+    # the bucket-pruned sweep (default) against the full radix sort path, and a workload whose maximum sits in a
+    # bucket with more than 4096 keys and several distinct distances (forces the in-call fallback to the full sort)
+    with K.Context(flags=K.DDKS_FLAG_RDKS_FULL_SORT) as cf:
+        for seed, (n_P, n_Q, d, kind) in enumerate([(3000, 2000, 3, "normal"), (700, 900, 2, "grid"),
+                                                    (5000, 5000, 5, "mixed"), (100, 100, 300, "dup")]):
+            P, Q = I.random_pair(7700 + seed, n_P, n_Q, d, kind)
+            assert ctx.rdks(dev(P), dev(Q)) == cf.rdks(dev(P), dev(Q))
+        rng = np.random.default_rng(7)
+        P = np.concatenate([rng.random((200, 2)), 0.5 + 1e-4 * rng.random((10000, 2))]).astype(np.float32)
+        Q = np.concatenate([rng.random((300, 2)), 0.5 + 1e-4 * rng.random((9000, 2)) + 2e-5]).astype(np.float32)
+        P[0], Q[0] = 0.0, 1.0
+        want = O.rdks(P, Q)
+        got = ctx.rdks(dev(P), dev(Q))
+        assert (got.num, got.argmax_origin) == (want[0], want[3]) and got == cf.rdks(dev(P), dev(Q))
