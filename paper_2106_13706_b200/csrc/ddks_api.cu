@@ -1096,12 +1096,9 @@ ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
         NC(ncclAllReduce(cnt, cnt, (size_t)V * 2, ncclUint32, ncclSum, ctx->comm, st));
         NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
     }
-    ddks::k_vox_diff<<<grid_for(V), blk, 0, st>>>(cnt, V, n_P, n_Q, S);
-    CHECK_LAUNCH();
-    ctx->launches++;
     int64_t stride = 1;
     for (int m = 0; m < d; ++m, stride *= k) {
-        ddks::k_prefix_line<<<grid_for(V / k), blk, 0, st>>>(S, V, k, stride);
+        ddks::k_prefix_line<<<grid_for(V / k), blk, 0, st>>>(S, V, k, stride, m == 0 ? cnt : nullptr, n_P, n_Q);
         CHECK_LAUNCH();
         ctx->launches++;
     }

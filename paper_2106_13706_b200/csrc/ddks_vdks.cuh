@@ -10,7 +10,8 @@
 //   * k_minmax: per-dimension min/max as order-preserving uint32 keys (one atomic per warp);
 //   * k_vox_hist: one thread per point; the voxel decision is taken in f64 with explicit _rn intrinsics (no FMA
 //     contraction), the same arithmetic as the oracle, so cells are bit-identical; counts by global atomics;
-//   * k_vox_diff + k_prefix_line (d passes): the inclusive d-dimensional prefix sum S of diff (int64, exact);
+//   * k_prefix_line (d passes, the first one reading the counts): the inclusive d-dimensional prefix sum S of
+//     diff (int64, exact);
 //   * k_vox_orthants: one thread per filled voxel gathers the 2^d box sums G[b] = S[corner(b)] with corner_m = k-1
 //     (bit m set) or c_m - 1, and a subset Moebius transform (d x 2^(d-1) subtractions) turns them into the 2^d
 //     orthant sums: O[q] = sum_{b subset of q} (-1)^{|q|-|b|} G[b]. Cost O(k^d d + F 2^d d) instead of the
@@ -87,22 +88,30 @@ __global__ void k_vox_hist(const float* __restrict__ pts, int64_t p_begin, int64
     }
 }
 
-__global__ void k_vox_diff(const uint32_t* __restrict__ cnt, int64_t V, int64_t n_P, int64_t n_Q,
-                           int64_t* __restrict__ S) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x)
-        S[v] = (int64_t)cnt[2 * v + 1] * n_P - (int64_t)cnt[2 * v] * n_Q;
-}
-
-// Inclusive scan of S along dimension j (stride k^j), one thread per line of k cells.
-__global__ void k_prefix_line(int64_t* __restrict__ S, int64_t V, int64_t k, int64_t stride) {
+// Inclusive scan of S along dimension j (stride k^j), one thread per line of k cells. Loads of a 16-cell chunk are
+// issued before its adds and stores, so they overlap (the stores may alias later loads of the same line only).
+// from_cnt (dimension 0 only): the line's values are first computed from the voxel counts, S = cQ n_P - cP n_Q.
+__global__ void k_prefix_line(int64_t* __restrict__ S, int64_t V, int64_t k, int64_t stride,
+                              const uint32_t* __restrict__ cnt, int64_t n_P, int64_t n_Q) {
+    constexpr int C = 16;
     const int64_t lines = V / k;
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < lines; l += (int64_t)gridDim.x * blockDim.x) {
         const int64_t lo = l % stride, hi = l / stride;
-        int64_t* p = S + hi * stride * k + lo;
+        const int64_t base = hi * stride * k + lo;
         int64_t run = 0;
-        for (int64_t c = 0; c < k; ++c) {
-            run += p[c * stride];
-            p[c * stride] = run;
+        for (int64_t c0 = 0; c0 < k; c0 += C) {
+            int64_t v[C];
+#pragma unroll
+            for (int j = 0; j < C; ++j) {
+                const int64_t idx = base + (c0 + j) * stride;
+                if (c0 + j < k) v[j] = cnt ? (int64_t)cnt[2 * idx + 1] * n_P - (int64_t)cnt[2 * idx] * n_Q : S[idx];
+            }
+#pragma unroll
+            for (int j = 0; j < C; ++j)
+                if (c0 + j < k) {
+                    run += v[j];
+                    S[base + (c0 + j) * stride] = run;
+                }
         }
     }
 }
