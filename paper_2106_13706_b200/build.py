@@ -13,8 +13,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libddks.so")
-SOURCES = [os.path.join(HERE, "csrc", "ddks_api.cu")]
-DEPS = SOURCES + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "ddks.h")]
+SOURCES = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))  # one translation unit per C-ABI area
+DEPS = SOURCES + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + glob.glob(os.path.join(HERE, "csrc", "*.h")) + \
+    [os.path.join(ROOT, "include", "ddks.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -38,14 +39,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return SO
     nd = nccl_dir()
+    common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
+              "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(nd, "include"), "-I", os.path.join(ROOT, "include")]
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    objs, procs = [], []
+    for src in SOURCES:  # the translation units compile in parallel
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + f".{os.getpid()}.o")
+        objs.append(obj)
+        procs.append(subprocess.Popen(common + ["-c", src, "-o", obj]))
+    rcs = [p.wait() for p in procs]
+    if any(rcs):
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
+        raise subprocess.CalledProcessError(max(rcs), "nvcc -c")
     tmp = SO + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-fvisibility=hidden",
-           "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(nd, "include"), "-I", os.path.join(ROOT, "include"),
-           "-o", tmp, *SOURCES,
-           "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", f"-Xlinker=-rpath={os.path.join(nd, 'lib')}",
-           "-lcudart"]
-    subprocess.check_call(cmd)
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
+                           f"-Xlinker=-rpath={os.path.join(nd, 'lib')}", "-lcudart"])
+    for o in objs:
+        os.remove(o)
     os.replace(tmp, SO)
     return SO
 

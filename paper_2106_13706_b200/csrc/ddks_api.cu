@@ -16,53 +16,15 @@
 #include <string>
 #include <vector>
 
-#include "../../include/ddks.h"
 #include "ddks_kernels.cuh"
-#include "ddks_significance.cuh"
-#include "ddks_vdks.cuh"
-#include "ddks_rdks.cuh"
+#include "ddks_radix.cuh"
+#include "ddks_internal.h"
 
 #define DDKS_VERSION "0.1.0-sm100a"
 
-constexpr int kMaxDevices = 64;  // per-device, per-kernel launch attributes are cached for this many devices
+thread_local std::string g_create_err;
 
-struct DevBuf {
-    void* p = nullptr;
-    size_t bytes = 0;
-};
-
-struct DevResult {  // device-side result block (one D2H per call)
-    unsigned long long num;
-    unsigned long long arg;
-    uint32_t flag;
-    uint32_t pad;
-};
-
-struct ddks_ctx {
-    int device = 0, world = 1, rank = 0;
-    uint32_t flags = 0;
-    ncclComm_t comm = nullptr;
-    DevBuf raw_a, raw_b, raw_perm, packed, packed2, pool_packed, per_origin, accum, item_num, bitmap, labels, res;
-    DevBuf sig_hist, sig_lf, sig_scratch, sig_table, sig_contrib, sig_part;  // ddks_significance workspace
-    DevBuf vox_keys, vox_cnt, vox_S;                                           // ddks_vdks workspace
-    DevBuf rd_keys, rd_xn, rd_k0, rd_k1, rd_hist, rd_tcnt, rd_cnum;              // ddks_rdks workspace
-    DevBuf x0_keys0, x0_keys1, x0_hist, x0_pts, x0_perm;                        // x0-ordered count workspace
-    DevBuf rdb_cnt, rdb_pst, rdb_coff, rdb_fill, rdb_clist, rdb_csum;            // rdKS bucket-pruned sweep
-    void* host_pinned = nullptr;  // DevResult + scratch
-    size_t host_pinned_bytes = 0;
-    int64_t launches = 0;
-    std::string err;
-    // profiling (DDKS_FLAG_PROFILE)
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending, ev_free;
-    std::vector<uint64_t> ev_pairs;
-    double prof_ms = 0.0;
-    int64_t prof_launches = 0;
-    uint64_t prof_pairs = 0;
-};
-
-static thread_local std::string g_create_err;
-
-namespace {
+namespace ddks_host {
 
 ddks_status fail(ddks_ctx* c, ddks_status s, const char* fmt, ...) {
     char buf[512];
@@ -74,23 +36,6 @@ ddks_status fail(ddks_ctx* c, ddks_status s, const char* fmt, ...) {
     else g_create_err = buf;
     return s;
 }
-
-#define CU(call)                                                                                     \
-    do {                                                                                             \
-        cudaError_t e_ = (call);                                                                     \
-        if (e_ != cudaSuccess)                                                                       \
-            return fail(ctx, e_ == cudaErrorMemoryAllocation ? DDKS_ERR_OOM : DDKS_ERR_CUDA, "%s: %s (%s:%d)", \
-                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                          \
-    } while (0)
-
-#define NC(call)                                                                                         \
-    do {                                                                                                 \
-        ncclResult_t r_ = (call);                                                                        \
-        if (r_ != ncclSuccess)                                                                           \
-            return fail(ctx, DDKS_ERR_NCCL, "%s: %s (%s:%d)", #call, ncclGetErrorString(r_), __FILE__, __LINE__); \
-    } while (0)
-
-#define CHECK_LAUNCH() CU(cudaGetLastError())
 
 ddks_status ensure(ddks_ctx* ctx, DevBuf& b, size_t bytes) {
     if (bytes <= b.bytes) return DDKS_OK;
@@ -309,6 +254,23 @@ ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int6
     return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "d=%d", d);
 }
 
+// Stable LSD radix sort of nseg segments of N 64-bit keys each, 8-bit digits from shift_begin up to bit 63;
+// src and dst ping-pong; *sorted receives the buffer holding the result. hist: nseg * tiles * 256 uint32.
+ddks_status radix_sort_keys(ddks_ctx* ctx, uint64_t* src, uint64_t* dst, int64_t N, int nseg, int shift_begin,
+                            uint32_t* hist, cudaStream_t st, uint64_t** sorted) {
+    const int tiles = (int)((N + ddks::RS_TILE - 1) / ddks::RS_TILE);
+    for (int shift = shift_begin; shift < 64; shift += 8) {
+        ddks::k_rs_hist<<<nseg * tiles, ddks::RS_T, 0, st>>>(src, N, tiles, shift, hist);
+        ddks::k_rs_scan<<<nseg, 256 * ddks::RS_SCAN_PARTS, 0, st>>>(hist, tiles);
+        ddks::k_rs_scatter<<<nseg * tiles, ddks::RS_T, 0, st>>>(src, dst, N, tiles, shift, hist);
+        CHECK_LAUNCH();
+        ctx->launches += 3;
+        std::swap(src, dst);
+    }
+    *sorted = src;
+    return DDKS_OK;
+}
+
 // x0-ordered statistic (B == 1, 2 <= d <= 8): reorder the packed rows label-major by x_0, count with bit-0 elision
 // (k_count<X0>), per-origin nums scattered back to pooled order into per_origin[N] (zeroed here). Origins
 // [o_begin, o_end) are positions in the x0 order. split + hist: SPLIT counters and the significance's M_T histogram.
@@ -333,15 +295,8 @@ ddks_status run_count_x0_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     CHECK_LAUNCH();
     ctx->launches++;
     // stable LSD passes over key bits 31..63 (x_0 key, then the label): ties keep pooled-index order
-    uint64_t *src = k0, *dst = k1;
-    for (int shift = 31; shift < 64; shift += 8) {
-        ddks::k_rs_hist<<<tiles, ddks::RS_T, 0, st>>>(src, N, tiles, shift, hist);
-        ddks::k_rs_scan<<<1, 256 * ddks::RS_SCAN_PARTS, 0, st>>>(hist, tiles);
-        ddks::k_rs_scatter<<<tiles, ddks::RS_T, 0, st>>>(src, dst, N, tiles, shift, hist);
-        CHECK_LAUNCH();
-        ctx->launches += 3;
-        std::swap(src, dst);
-    }
+    uint64_t* src = nullptr;
+    if ((s = radix_sort_keys(ctx, k0, k1, N, 1, 31, hist, st, &src))) return s;
     float* spts = (float*)ctx->x0_pts.p;
     ddks::k_permute_rows<<<g, 256, 0, st>>>(packed, DP, N, src, spts, (int32_t*)ctx->x0_perm.p);
     CHECK_LAUNCH();
@@ -559,7 +514,9 @@ ddks_status bind_device(ddks_ctx* ctx) {
     return DDKS_OK;
 }
 
-}  // namespace
+}  // namespace ddks_host
+
+using namespace ddks_host;
 
 // ===================================================================================================== C ABI
 extern "C" {
@@ -898,396 +855,6 @@ ddks_status ddks_permutation_null(ddks_ctx* ctx, const float* pooled, int64_t n_
         observed->argmax_origin = -1;
     }
     if (p_value) *p_value = (double)(1 + ge) / (double)(1 + n_perm);
-    return DDKS_OK;
-}
-
-// ------------------------------------------------------------------------------------- analytic significance
-// PAPER.md §3, SURVEY §8f NEXT-1. One SPLIT classify+count pass gives num (as ddks_stat) and the
-// histogram of the Q-counts M_T over the 2^d x N cells; the per-cell factor log p(d <= D | lambda) depends only on
-// M_T, so it is tabulated for the distinct values (k_sig_table) and summed with the histogram as weights.
-ddks_status ddks_significance(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
-                              uint32_t sig_flags, void* stream, ddks_significance_result* out, uint64_t* mt_hist,
-                              double* log_p_table) {
-    if (!ctx) return DDKS_ERR_INVALID_ARGUMENT;
-    ctx->err.clear();
-    if (!out) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "null out");
-    if (sig_flags & ~DDKS_SIG_POISSON) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad sig_flags");
-    ddks_status s = check_sizes(ctx, n_P, n_Q, d);
-    if (s) return s;
-    if (!P || !Q) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "null argument");
-    if ((s = bind_device(ctx))) return s;
-    cudaStream_t st = (cudaStream_t)stream;
-    const int64_t N = n_P + n_Q;
-    const int DP = pad_dim(d);
-    int64_t ob, oe;
-    ddks_shard_range(N, ctx->world, ctx->rank, &ob, &oe);
-    const void *dP, *dQ;
-    if ((s = stage_input(ctx, P, (size_t)n_P * d * 4, ctx->raw_a, st, &dP))) return s;
-    if ((s = stage_input(ctx, Q, (size_t)n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
-    if ((s = ensure(ctx, ctx->packed, (size_t)N * DP * 4))) return s;
-    if ((s = ensure(ctx, ctx->per_origin, (size_t)std::max<int64_t>(oe - ob, 1) * 8))) return s;
-    const int64_t nm = n_Q + 1;  // M_T in 0..n_Q
-    const int64_t n_max = std::max(n_P, n_Q);
-    // log n! for n <= n_max, plus room for the Poisson mass beyond N (mean < N, ~14 sd above it is below e^-100)
-    const int64_t n_lf = n_max + 1 + ((sig_flags & DDKS_SIG_POISSON) ? (int64_t)(32.0 * std::sqrt((double)n_max)) + 2048 : 0);
-    if ((s = ensure(ctx, ctx->sig_hist, (size_t)nm * 8))) return s;
-    if ((s = ensure(ctx, ctx->sig_lf, (size_t)n_lf * 8))) return s;
-    if ((s = ensure(ctx, ctx->sig_table, (size_t)nm * 8))) return s;
-    if ((s = ensure(ctx, ctx->sig_contrib, (size_t)nm * 8))) return s;
-    if ((s = ensure(ctx, ctx->sig_part, (size_t)ctx->world * 8 + 8))) return s;
-    unsigned long long* hist = (unsigned long long*)ctx->sig_hist.p;
-    double* LF = (double*)ctx->sig_lf.p;
-    double* table = (double*)ctx->sig_table.p;
-    double* contrib = (double*)ctx->sig_contrib.p;
-    double* part = (double*)ctx->sig_part.p;  // [0] = this rank's partial sum, [1 + r] = gathered partials
-    CU(cudaMemsetAsync(hist, 0, (size_t)nm * 8, st));
-    CU(cudaMemsetAsync(table, 0, (size_t)nm * 8, st));
-    CU(cudaMemsetAsync(contrib, 0, (size_t)nm * 8, st));
-    DevResult* dres = (DevResult*)ctx->res.p;
-    DevResult* hres = (DevResult*)ctx->host_pinned;
-    *hres = DevResult{0ull, ~0ull, 0u, 0u};
-    CU(cudaMemcpyAsync(dres, hres, sizeof(DevResult), cudaMemcpyHostToDevice, st));
-    float* packed = (float*)ctx->packed.p;
-    if ((s = launch_pack(ctx, (const float*)dP, n_P, (const float*)dQ, n_Q, d, 1, packed, &dres->flag, st))) return s;
-    uint64_t* per = nullptr;
-    if ((s = count_statistic(ctx, packed, d, n_P, n_Q, ob, oe, dres, false, true, hist, st, &per))) return s;
-    if (ctx->world > 1) {
-        NC(ncclAllReduce(&dres->arg, &dres->arg, 1, ncclUint64, ncclMin, ctx->comm, st));
-        NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
-        NC(ncclAllReduce(hist, hist, (size_t)nm, ncclUint64, ncclSum, ctx->comm, st));
-    }
-    ddks::k_logfact<<<(int)std::min<int64_t>((n_lf + 255) / 256, 148 * 8), 256, 0, st>>>(LF, n_lf - 1);
-    CHECK_LAUNCH();
-    ctx->launches++;
-    // table entries [mb, me) on this rank
-    int64_t mb, me;
-    ddks_shard_range(nm, ctx->world, ctx->rank, &mb, &me);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(me - mb, 148 * 2));
-    // window bound: ~2 x sqrt(2 x 100) standard deviations (+ slack for skewed small-rate pmfs); a kernel that
-    // finds a wider window flags it and the table is recomputed with twice the scratch
-    const double var = (sig_flags & DDKS_SIG_POISSON) ? (double)n_max : (double)n_max / 4.0;
-    int64_t W_max = std::min<int64_t>(n_max + 1, (int64_t)(32.0 * std::sqrt(var)) + 512);
-    const uint64_t host_part_off = sizeof(DevResult);
-    if ((s = ensure_host(ctx, host_part_off + (size_t)(ctx->world + 1) * 8))) return s;
-    hres = (DevResult*)ctx->host_pinned;
-    double* hpart = (double*)((char*)ctx->host_pinned + host_part_off);
-    for (int attempt = 0;; ++attempt) {
-        if ((s = ensure(ctx, ctx->sig_scratch, (size_t)grid * 2 * W_max * 8))) return s;
-        ddks::SigArgs sa{};
-        sa.LF = LF;
-        sa.lf_max = n_lf - 1;
-        sa.hist = hist;
-        sa.num = (const unsigned long long*)&dres->num;
-        sa.N_P = n_P;
-        sa.N_T = n_Q;
-        sa.m_begin = mb;
-        sa.m_end = me;
-        sa.poisson = (sig_flags & DDKS_SIG_POISSON) ? 1 : 0;
-        sa.scratch = (double*)ctx->sig_scratch.p;
-        sa.W_max = W_max;
-        sa.table = table;
-        sa.contrib = contrib;
-        sa.flag = &dres->flag;
-        if (me > mb) {
-            ddks::k_sig_table<<<grid, ddks::SIG_T, 0, st>>>(sa);
-            CHECK_LAUNCH();
-            ctx->launches++;
-        }
-        ddks::k_sig_sum<<<1, ddks::SIG_T, 0, st>>>(contrib, mb, me, part);
-        CHECK_LAUNCH();
-        ctx->launches++;
-        if (ctx->world > 1) {
-            NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
-            NC(ncclAllGather(part, part + 1, 1, ncclFloat64, ctx->comm, st));
-        } else {
-            CU(cudaMemcpyAsync(part + 1, part, 8, cudaMemcpyDeviceToDevice, st));
-        }
-        CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
-        CU(cudaMemcpyAsync(hpart, part + 1, (size_t)ctx->world * 8, cudaMemcpyDeviceToHost, st));
-        CU(cudaStreamSynchronize(st));
-        if ((s = collect_profile(ctx))) return s;
-        if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
-        if (!(hres->flag & 4u)) break;
-        if (attempt >= 3 || W_max >= n_max + 1) return fail(ctx, DDKS_ERR_CUDA, "significance window exceeds scratch");
-        W_max = std::min<int64_t>(n_max + 1, 2 * W_max);
-        const uint32_t zero = 0;
-        CU(cudaMemcpyAsync(&dres->flag, &zero, 4, cudaMemcpyHostToDevice, st));
-    }
-    double log_prod = 0.0;
-    for (int r = 0; r < ctx->world; ++r) log_prod += hpart[r];  // rank order: deterministic
-    if (mt_hist) {
-        CU(cudaMemcpyAsync(mt_hist, hist, (size_t)nm * 8, cudaMemcpyDefault, st));
-    }
-    if (log_p_table) {
-        if (ctx->world > 1) NC(ncclAllReduce(table, table, (size_t)nm, ncclFloat64, ncclSum, ctx->comm, st));
-        CU(cudaMemcpyAsync(log_p_table, table, (size_t)nm * 8, cudaMemcpyDefault, st));
-    }
-    CU(cudaStreamSynchronize(st));
-    out->stat.num = hres->num;
-    out->stat.den = (uint64_t)n_P * (uint64_t)n_Q;
-    out->stat.D = (double)out->stat.num / (double)out->stat.den;
-    out->stat.argmax_origin = hres->arg == ~0ull ? -1 : (int64_t)hres->arg;
-    out->log_prod = log_prod;
-    out->S = 0.0 - std::expm1(log_prod);  // (0.0 - x: no negative zero when log_prod == 0)
-    out->cells = ((int64_t)1 << d) * N;
-    return DDKS_OK;
-}
-
-// ------------------------------------------------------------------------------------- vdKS (Alg. 1)
-// Points sharded across ranks for the voxel histogram (NCCL all-reduce(sum) of the grid counts), voxels sharded
-// for the orthant sums (all-reduce(max)); min/max keys all-reduced (min / max) before voxelisation.
-ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d, int64_t k,
-                      void* stream, ddks_result* out) {
-    if (!ctx) return DDKS_ERR_INVALID_ARGUMENT;
-    ctx->err.clear();
-    if (!out) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "null out");
-    ddks_status s = check_sizes(ctx, n_P, n_Q, d);
-    if (s) return s;
-    if (!P || !Q) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "null argument");
-    if (k < 1) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "k=%lld < 1", (long long)k);
-    int64_t V = 1;
-    for (int m = 0; m < d; ++m) {
-        if (V > (int64_t(1) << 30) / k) return fail(ctx, DDKS_ERR_TOO_LARGE, "k^d > 2^30 voxels");
-        V *= k;
-    }
-    if ((s = bind_device(ctx))) return s;
-    cudaStream_t st = (cudaStream_t)stream;
-    const int64_t N = n_P + n_Q;
-    const int DP = pad_dim(d);
-    const void *dP, *dQ;
-    if ((s = stage_input(ctx, P, (size_t)n_P * d * 4, ctx->raw_a, st, &dP))) return s;
-    if ((s = stage_input(ctx, Q, (size_t)n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
-    if ((s = ensure(ctx, ctx->packed, (size_t)N * DP * 4))) return s;
-    if ((s = ensure(ctx, ctx->vox_keys, 16 * 4))) return s;
-    if ((s = ensure(ctx, ctx->vox_cnt, (size_t)V * 8))) return s;
-    if ((s = ensure(ctx, ctx->vox_S, (size_t)V * 8))) return s;
-    uint32_t* keys = (uint32_t*)ctx->vox_keys.p;
-    uint32_t* cnt = (uint32_t*)ctx->vox_cnt.p;
-    int64_t* S = (int64_t*)ctx->vox_S.p;
-    DevResult* dres = (DevResult*)ctx->res.p;
-    DevResult* hres = (DevResult*)ctx->host_pinned;
-    *hres = DevResult{0ull, ~0ull, 0u, 0u};
-    CU(cudaMemcpyAsync(dres, hres, sizeof(DevResult), cudaMemcpyHostToDevice, st));
-    CU(cudaMemsetAsync(keys, 0xff, 8 * 4, st));
-    CU(cudaMemsetAsync(keys + 8, 0, 8 * 4, st));
-    CU(cudaMemsetAsync(cnt, 0, (size_t)V * 8, st));
-    float* packed = (float*)ctx->packed.p;
-    if ((s = launch_pack(ctx, (const float*)dP, n_P, (const float*)dQ, n_Q, d, 1, packed, &dres->flag, st))) return s;
-    int64_t pb, pe;
-    ddks_shard_range(N, ctx->world, ctx->rank, &pb, &pe);
-    const int blk = 256;
-    auto grid_for = [](int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); };
-    if (pe > pb) {
-        ddks::k_minmax<<<(int)std::max<int64_t>(1, std::min<int64_t>((pe - pb + 1023) / 1024, 148 * 2)), blk, 0, st>>>(
-            packed + pb * DP, pe - pb, d, DP, keys);
-        CHECK_LAUNCH();
-        ctx->launches++;
-    }
-    if (ctx->world > 1) {
-        NC(ncclAllReduce(keys, keys, 8, ncclUint32, ncclMin, ctx->comm, st));
-        NC(ncclAllReduce(keys + 8, keys + 8, 8, ncclUint32, ncclMax, ctx->comm, st));
-    }
-    if (pe > pb) {
-        ddks::k_vox_hist<<<grid_for(pe - pb), blk, 0, st>>>(packed, pb, pe, n_P, d, DP, keys, k, cnt);
-        CHECK_LAUNCH();
-        ctx->launches++;
-    }
-    if (ctx->world > 1) {
-        NC(ncclAllReduce(cnt, cnt, (size_t)V * 2, ncclUint32, ncclSum, ctx->comm, st));
-        NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
-    }
-    int64_t stride = 1;
-    for (int m = 0; m < d; ++m, stride *= k) {
-        ddks::k_prefix_line<<<grid_for(V / k), blk, 0, st>>>(S, V, k, stride, m == 0 ? cnt : nullptr, n_P, n_Q);
-        CHECK_LAUNCH();
-        ctx->launches++;
-    }
-    int64_t vb, ve;
-    ddks_shard_range(V, ctx->world, ctx->rank, &vb, &ve);
-    if (ve > vb) {
-        unsigned long long* num = &dres->num;
-        const int g = grid_for(ve - vb);
-        switch (d) {
-            case 1: ddks::k_vox_orthants<1><<<g, blk, 0, st>>>(cnt, S, vb, ve, k, num); break;
-            case 2: ddks::k_vox_orthants<2><<<g, blk, 0, st>>>(cnt, S, vb, ve, k, num); break;
-            case 3: ddks::k_vox_orthants<3><<<g, blk, 0, st>>>(cnt, S, vb, ve, k, num); break;
-            case 4: ddks::k_vox_orthants<4><<<g, blk, 0, st>>>(cnt, S, vb, ve, k, num); break;
-            case 5: ddks::k_vox_orthants<5><<<g, blk, 0, st>>>(cnt, S, vb, ve, k, num); break;
-            case 6: ddks::k_vox_orthants<6><<<g, blk, 0, st>>>(cnt, S, vb, ve, k, num); break;
-            case 7: ddks::k_vox_orthants<7><<<g, blk, 0, st>>>(cnt, S, vb, ve, k, num); break;
-            case 8: ddks::k_vox_orthants<8><<<g, blk, 0, st>>>(cnt, S, vb, ve, k, num); break;
-        }
-        CHECK_LAUNCH();
-        ctx->launches++;
-    }
-    if (ctx->world > 1) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
-    CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
-    out->num = hres->num;
-    out->den = (uint64_t)n_P * (uint64_t)n_Q;
-    out->D = (double)out->num / (double)out->den;
-    out->argmax_origin = -1;
-    return DDKS_OK;
-}
-
-// ------------------------------------------------------------------------------------- rdKS (Alg. 2)
-// Corners sharded across ranks; the statistic is the max over corners (NCCL all-reduce max, then min of the first
-// attaining corner index).
-ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
-                      void* stream, ddks_result* out) {
-    if (!ctx) return DDKS_ERR_INVALID_ARGUMENT;
-    ctx->err.clear();
-    if (!out) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "null out");
-    if (n_P < 0 || n_Q < 0) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "negative sample size");
-    if (n_P == 0 || n_Q == 0) return fail(ctx, DDKS_ERR_EMPTY_SAMPLE, "empty sample");
-    if (d < 1) return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "d=%d < 1", d);
-    const int64_t N = n_P + n_Q;
-    if (N >= (int64_t(1) << 31) || (double)n_P * (double)n_Q >= 9007199254740992.0 ||
-        (double)N * (double)(d + 1) >= (double)(int64_t(1) << 34))
-        return fail(ctx, DDKS_ERR_TOO_LARGE, "rdKS problem too large (N=%lld, d=%d)", (long long)N, d);
-    if (!P || !Q) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "null argument");
-    ddks_status s;
-    if ((s = bind_device(ctx))) return s;
-    cudaStream_t st = (cudaStream_t)stream;
-    const void *dP, *dQ;
-    if ((s = stage_input(ctx, P, (size_t)n_P * d * 4, ctx->raw_a, st, &dP))) return s;
-    if ((s = stage_input(ctx, Q, (size_t)n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
-    int64_t cb, ce;
-    ddks_shard_range(d + 1, ctx->world, ctx->rank, &cb, &ce);
-    const int nc = (int)(ce - cb);
-    const int tiles = (int)((N + ddks::RS_TILE - 1) / ddks::RS_TILE);
-    if ((s = ensure(ctx, ctx->rd_keys, (size_t)2 * d * 4))) return s;
-    if ((s = ensure(ctx, ctx->rd_xn, (size_t)N * d * 8))) return s;
-    if ((s = ensure(ctx, ctx->rd_k0, (size_t)std::max(nc, 1) * N * 8))) return s;
-    if ((s = ensure(ctx, ctx->rd_k1, (size_t)std::max(nc, 1) * N * 8))) return s;
-    if ((s = ensure(ctx, ctx->rd_hist, (size_t)std::max(nc, 1) * tiles * 256 * 4))) return s;
-    if ((s = ensure(ctx, ctx->rd_tcnt, (size_t)std::max(nc, 1) * tiles * 4))) return s;
-    if ((s = ensure(ctx, ctx->rd_cnum, (size_t)(d + 1) * 8))) return s;
-    uint32_t* keys = (uint32_t*)ctx->rd_keys.p;
-    double* xn = (double*)ctx->rd_xn.p;
-    uint64_t* k0 = (uint64_t*)ctx->rd_k0.p;
-    uint64_t* k1 = (uint64_t*)ctx->rd_k1.p;
-    uint32_t* hist = (uint32_t*)ctx->rd_hist.p;
-    uint32_t* tcnt = (uint32_t*)ctx->rd_tcnt.p;
-    unsigned long long* cnum = (unsigned long long*)ctx->rd_cnum.p;
-    DevResult* dres = (DevResult*)ctx->res.p;
-    CU(cudaMemsetAsync(dres, 0, sizeof(DevResult), st));
-    CU(cudaMemsetAsync(keys, 0xff, (size_t)d * 4, st));
-    CU(cudaMemsetAsync(keys + d, 0, (size_t)d * 4, st));
-    CU(cudaMemsetAsync(cnum, 0, (size_t)(d + 1) * 8, st));
-    ddks::k_rd_minmax<<<(int)std::max<int64_t>(1, std::min<int64_t>((N + 1023) / 1024, 148 * 2)), 256, 0, st>>>(
-        (const float*)dP, n_P, (const float*)dQ, n_Q, d, keys, &dres->flag);
-    CHECK_LAUNCH();
-    ctx->launches++;
-    auto grid_for = [](int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); };
-    ddks::k_rd_normalize<<<grid_for(N * d), 256, 0, st>>>((const float*)dP, n_P, (const float*)dQ, n_Q, d, keys, xn);
-    CHECK_LAUNCH();
-    ctx->launches++;
-    // full path: segmented 8-pass LSD radix sort of every corner's keys, then the tie-complete sweep
-    auto full_sort = [&]() -> ddks_status {
-        const int blocks = nc * tiles;
-        uint64_t *src = k0, *dst = k1;
-        CU(cudaMemsetAsync(cnum, 0, (size_t)(d + 1) * 8, st));
-        for (int shift = 0; shift < 64; shift += 8) {
-            ddks::k_rs_hist<<<blocks, ddks::RS_T, 0, st>>>(src, N, tiles, shift, hist);
-            ddks::k_rs_scan<<<nc, 256 * ddks::RS_SCAN_PARTS, 0, st>>>(hist, tiles);
-            ddks::k_rs_scatter<<<blocks, ddks::RS_T, 0, st>>>(src, dst, N, tiles, shift, hist);
-            CHECK_LAUNCH();
-            ctx->launches += 3;
-            std::swap(src, dst);
-        }
-        ddks::k_rd_count<<<blocks, ddks::RS_T, 0, st>>>(src, N, tiles, tcnt);
-        ddks::k_rd_sweep<<<blocks, ddks::RS_T, 0, st>>>(src, N, tiles, n_P, n_Q, tcnt, cnum);
-        CHECK_LAUNCH();
-        ctx->launches += 2;
-        return DDKS_OK;
-    };
-    const bool pruned = !(ctx->flags & DDKS_FLAG_RDKS_FULL_SORT);
-    if (nc > 0) {
-        ddks::k_rd_keys<<<grid_for(N * nc), 256, 0, st>>>(xn, N, n_P, d, (int)cb, (int)ce, k0);
-        CHECK_LAUNCH();
-        ctx->launches++;
-        if (pruned) {
-            // bucket-pruned sweep: bucket counts, exact bucket-end values, sort only the buckets that can beat them
-            int nbk = 256;
-            while (nbk < N / 4 && nbk < (1 << 20)) nbk <<= 1;
-            const double scale = (double)nbk / (std::sqrt((double)d) * (1.0 + 1e-9));
-            const size_t nb = (size_t)nc * nbk;
-            if ((s = ensure(ctx, ctx->rdb_cnt, nb * 8))) return s;
-            if ((s = ensure(ctx, ctx->rdb_pst, nb * 8))) return s;
-            if ((s = ensure(ctx, ctx->rdb_coff, nb * 4))) return s;
-            if ((s = ensure(ctx, ctx->rdb_fill, nb * 4))) return s;
-            if ((s = ensure(ctx, ctx->rdb_clist, nb * 4))) return s;
-            if ((s = ensure(ctx, ctx->rdb_csum, ((size_t)nc * ((nbk + ddks::RDB_CH - 1) / ddks::RDB_CH) + nc) * 8))) return s;
-            uint32_t* bcnt = (uint32_t*)ctx->rdb_cnt.p;
-            int32_t* clist = (int32_t*)ctx->rdb_clist.p;
-            CU(cudaMemsetAsync(bcnt, 0, nb * 8, st));
-            CU(cudaMemsetAsync(ctx->rdb_fill.p, 0, nb * 4, st));
-            ddks::k_rdb_count<<<grid_for(N * nc), 256, 0, st>>>(k0, N, nc, nbk, scale, bcnt);
-            const int nch = (nbk + ddks::RDB_CH - 1) / ddks::RDB_CH;
-            uint64_t* csum = (uint64_t*)ctx->rdb_csum.p;
-            uint32_t* segc = (uint32_t*)(csum + (size_t)nc * nch);
-            CU(cudaMemsetAsync(segc, 0, (size_t)nc * 8, st));
-            CU(cudaMemsetAsync(cnum, 0, (size_t)(d + 1) * 8, st));
-            ddks::k_rdb_reduce<<<dim3(nch, nc), 256, 0, st>>>(bcnt, nbk, csum);
-            ddks::k_rdb_chunk_scan<<<nc, 256, 0, st>>>(csum, nch);
-            ddks::k_rdb_down<<<dim3(nch, nc), 256, 0, st>>>(bcnt, nbk, csum, n_P, n_Q, (uint2*)ctx->rdb_pst.p, cnum);
-            ddks::k_rdb_cand<<<grid_for((int64_t)nb), 256, 0, st>>>(bcnt, (const uint2*)ctx->rdb_pst.p, nc, nbk, n_P,
-                                                                    n_Q, cnum, (uint32_t*)ctx->rdb_coff.p, clist, segc);
-            ddks::k_rdb_compact<<<grid_for(N * nc), 256, 0, st>>>(k0, N, nc, nbk, scale, (const uint32_t*)ctx->rdb_coff.p,
-                                                                  (uint32_t*)ctx->rdb_fill.p, k1);
-            ddks::k_rdb_finish<<<dim3(std::max(1, std::min(1024, (148 * 4 + nc - 1) / nc)), nc), 256, 0, st>>>(
-                k1, N, nbk, bcnt, (const uint2*)ctx->rdb_pst.p, (const uint32_t*)ctx->rdb_coff.p, clist, segc, n_P,
-                n_Q, cnum, &dres->flag);
-            CHECK_LAUNCH();
-            ctx->launches += 7;
-        } else if ((s = full_sort())) {
-            return s;
-        }
-    }
-    if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)(d + 1) * 8))) return s;
-    DevResult* hres = (DevResult*)ctx->host_pinned;
-    uint64_t* hc = (uint64_t*)((char*)ctx->host_pinned + sizeof(DevResult));
-    CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(hc, cnum, (size_t)std::max(nc, 0) * 8, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    if (nc > 0 && pruned && (hres->flag & 256u)) {  // a candidate bucket too large for SMEM: sort everything
-        if ((s = full_sort())) return s;
-        CU(cudaMemcpyAsync(hc, cnum, (size_t)nc * 8, cudaMemcpyDeviceToHost, st));
-        CU(cudaStreamSynchronize(st));
-    }
-    if (ctx->world > 1) {
-        NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
-        CU(cudaMemcpyAsync(&hres->flag, &dres->flag, 4, cudaMemcpyDeviceToHost, st));
-        CU(cudaStreamSynchronize(st));
-    }
-    if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
-    uint64_t best = 0;
-    for (int c = 0; c < nc; ++c) best = std::max<uint64_t>(best, hc[c]);
-    uint64_t arg = ~0ull;
-    if (ctx->world > 1) {
-        hres->num = best;
-        CU(cudaMemcpyAsync(&dres->num, &hres->num, 8, cudaMemcpyHostToDevice, st));
-        NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
-        CU(cudaMemcpyAsync(&hres->num, &dres->num, 8, cudaMemcpyDeviceToHost, st));
-        CU(cudaStreamSynchronize(st));
-        best = hres->num;
-    }
-    for (int c = 0; c < nc; ++c)
-        if (hc[c] == best) { arg = (uint64_t)(cb + c); break; }
-    if (ctx->world > 1) {
-        hres->arg = arg;
-        CU(cudaMemcpyAsync(&dres->arg, &hres->arg, 8, cudaMemcpyHostToDevice, st));
-        NC(ncclAllReduce(&dres->arg, &dres->arg, 1, ncclUint64, ncclMin, ctx->comm, st));
-        CU(cudaMemcpyAsync(&hres->arg, &dres->arg, 8, cudaMemcpyDeviceToHost, st));
-        CU(cudaStreamSynchronize(st));
-        arg = hres->arg;
-    }
-    out->num = best;
-    out->den = (uint64_t)n_P * (uint64_t)n_Q;
-    out->D = (double)best / (double)out->den;
-    out->argmax_origin = (int64_t)arg;
     return DDKS_OK;
 }
 

@@ -1,0 +1,94 @@
+// ddks_internal.h — host-side internals shared by the translation units of libddks.so (NOT part of the C ABI):
+// the context, device workspace buffers, error macros and the helpers the C-ABI entry points are built from.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/ddks.h"
+#include "ddks_common.cuh"
+
+constexpr int kMaxDevices = 64;  // per-device, per-kernel launch attributes are cached for this many devices
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+struct DevResult {  // device-side result block (one D2H per call)
+    unsigned long long num;
+    unsigned long long arg;
+    uint32_t flag;
+    uint32_t pad;
+};
+
+struct ddks_ctx {
+    int device = 0, world = 1, rank = 0;
+    uint32_t flags = 0;
+    ncclComm_t comm = nullptr;
+    DevBuf raw_a, raw_b, raw_perm, packed, packed2, pool_packed, per_origin, accum, item_num, bitmap, labels, res;
+    DevBuf sig_hist, sig_lf, sig_scratch, sig_table, sig_contrib, sig_part;  // ddks_significance workspace
+    DevBuf vox_keys, vox_cnt, vox_S;                                           // ddks_vdks workspace
+    DevBuf rd_keys, rd_xn, rd_k0, rd_k1, rd_hist, rd_tcnt, rd_cnum;              // ddks_rdks workspace
+    DevBuf x0_keys0, x0_keys1, x0_hist, x0_pts, x0_perm;                        // x0-ordered count workspace
+    DevBuf rdb_cnt, rdb_pst, rdb_coff, rdb_fill, rdb_clist, rdb_csum;            // rdKS bucket-pruned sweep
+    void* host_pinned = nullptr;  // DevResult + scratch
+    size_t host_pinned_bytes = 0;
+    int64_t launches = 0;
+    std::string err;
+    // profiling (DDKS_FLAG_PROFILE)
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending, ev_free;
+    std::vector<uint64_t> ev_pairs;
+    double prof_ms = 0.0;
+    int64_t prof_launches = 0;
+    uint64_t prof_pairs = 0;
+};
+
+extern thread_local std::string g_create_err;
+
+namespace ddks_host {
+
+ddks_status fail(ddks_ctx* c, ddks_status s, const char* fmt, ...);
+
+#define CU(call)                                                                                     \
+    do {                                                                                             \
+        cudaError_t e_ = (call);                                                                     \
+        if (e_ != cudaSuccess)                                                                       \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? DDKS_ERR_OOM : DDKS_ERR_CUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                          \
+    } while (0)
+
+#define NC(call)                                                                                         \
+    do {                                                                                                 \
+        ncclResult_t r_ = (call);                                                                        \
+        if (r_ != ncclSuccess)                                                                           \
+            return fail(ctx, DDKS_ERR_NCCL, "%s: %s (%s:%d)", #call, ncclGetErrorString(r_), __FILE__, __LINE__); \
+    } while (0)
+
+#define CHECK_LAUNCH() CU(cudaGetLastError())
+
+// grow-only device workspace; host (pinned) scratch
+ddks_status ensure(ddks_ctx* ctx, DevBuf& b, size_t bytes);
+ddks_status ensure_host(ddks_ctx* ctx, size_t bytes);
+// device pointers are used in place, host pointers copied on st into buf
+ddks_status stage_input(ddks_ctx* ctx, const void* src, size_t bytes, DevBuf& buf, cudaStream_t st, const void** out);
+uint64_t gcd_u64(uint64_t a, uint64_t b);
+ddks_status check_sizes(ddks_ctx* ctx, int64_t n_P, int64_t n_Q, int32_t d);
+int pad_dim(int d);
+ddks_status bind_device(ddks_ctx* ctx);
+ddks_status collect_profile(ddks_ctx* ctx);
+// validate (NaN/Inf -> *flag |= 1) and pack P then Q into [B][N][pad_dim(d)] rows
+ddks_status launch_pack(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d, int64_t B,
+                        float* dst, uint32_t* flag, cudaStream_t st);
+// one statistic over the origin shard [ob, oe): count, NCCL max of num, this rank's argmax candidate (see ddks_api.cu)
+ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n_P, int64_t n_Q, int64_t ob,
+                            int64_t oe, DevResult* dres, bool export_per, bool split, unsigned long long* hist,
+                            cudaStream_t st, uint64_t** per_out);
+ddks_status radix_sort_keys(ddks_ctx* ctx, uint64_t* src, uint64_t* dst, int64_t N, int nseg, int shift_begin,
+                            uint32_t* hist, cudaStream_t st, uint64_t** sorted);
+
+}  // namespace ddks_host

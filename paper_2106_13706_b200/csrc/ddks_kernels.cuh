@@ -22,6 +22,8 @@
 #include <utility>
 #include <cuda_runtime.h>
 
+#include "ddks_common.cuh"
+
 namespace ddks {
 
 // ----------------------------------------------------------------------------------------------- config
@@ -43,7 +45,6 @@ template <> struct Cfg<6> { static constexpr int R = 4, T = 384, TILE = 256, S =
 template <> struct Cfg<7> { static constexpr int R = 2, T = 384, TILE = 256, S = 3; };
 template <> struct Cfg<8> { static constexpr int R = 1, T = 384, TILE = 256, S = 3; };
 
-template <int D> __host__ __device__ constexpr int padded_dim() { return D <= 4 ? 4 : 8; }
 
 template <int D, bool SPLIT, int DPX = padded_dim<D>()> struct Geo {
     // SPLIT doubles the bins: halve R (keeping it even or 1), or T when R is already <= 2
@@ -67,55 +68,6 @@ template <int D, bool SPLIT, int DPX = padded_dim<D>()> struct Geo {
     __host__ __device__ static constexpr int slot(int r, int t) { return (r * T + t) % WPB; }
     __host__ __device__ static constexpr bool high(int r, int t) { return r * T + t >= WPB; }
 };
-
-// order-preserving uint32 key of a float (after -0 -> +0 canonicalisation) and its inverse
-__device__ __forceinline__ uint32_t f32_key(float f) {
-    const uint32_t b = __float_as_uint(f);
-    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
-__device__ __forceinline__ float key_f32(uint32_t k) {
-    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
-}
-
-// ----------------------------------------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "DDKS_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra DDKS_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// 1-D bulk copy global -> shared through the TMA engine, completion counted on an mbarrier (bytes % 16 == 0).
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-// FP32 ordered compare -> 1.0f / 0.0f (SASS FSET.BF). No .ftz: denormals compare exactly (R6).
-template <bool GT> __device__ __forceinline__ float cmp_bit(float x, float o) {
-    float r;
-    if constexpr (GT) asm("set.gt.f32.f32 %0, %1, %2;" : "=f"(r) : "f"(x), "f"(o));
-    else              asm("set.ge.f32.f32 %0, %1, %2;" : "=f"(r) : "f"(x), "f"(o));
-    return r;
-}
-// No "memory" clobber: the counters are only read after a __syncthreads() (a compiler and hardware fence), and the
-// point tiles the hot loop loads are disjoint from them, so ptxas may hoist the next point's LDS above these REDs.
-__device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v));
-}
 
 template <int D> __device__ __forceinline__ void load_point(const float* sp, float (&x)[D]) {
     const float4 a = *reinterpret_cast<const float4*>(sp);
@@ -243,15 +195,6 @@ __device__ __forceinline__ uint64_t origin_num(const uint32_t* hist, int r, int 
         }
     }
     return best;
-}
-
-__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
-        v = w > v ? w : v;
-    }
-    return v;
 }
 
 // Float-encoded counter address of the pair (origin o, point x): base + sum_k [x_k >= o_k] * 4 * 2^k * WPB, as d

@@ -20,7 +20,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-#include "ddks_kernels.cuh"  // f32_key / key_f32
+#include "ddks_common.cuh"
 
 namespace ddks {
 
