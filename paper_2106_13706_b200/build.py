@@ -44,21 +44,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     objs, procs = [], []
-    for src in SOURCES:  # the translation units compile in parallel
-        obj = os.path.join(objdir, os.path.basename(src)[:-3] + f".{os.getpid()}.o")
-        objs.append(obj)
-        procs.append(subprocess.Popen(common + ["-c", src, "-o", obj]))
-    rcs = [p.wait() for p in procs]
-    if any(rcs):
+    tmp = SO + f".tmp{os.getpid()}"
+    try:
+        for src in SOURCES:  # the translation units compile in parallel
+            obj = os.path.join(objdir, os.path.basename(src)[:-3] + f".{os.getpid()}.o")
+            objs.append(obj)
+            procs.append(subprocess.Popen(common + ["-c", src, "-o", obj]))
+        rcs = [p.wait() for p in procs]
+        if any(rcs):
+            raise subprocess.CalledProcessError(max(rcs), "nvcc -c")
+        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L", os.path.join(nd, "lib"),
+                               "-l:libnccl.so.2", f"-Xlinker=-rpath={os.path.join(nd, 'lib')}", "-lcudart"])
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
         for o in objs:
             if os.path.exists(o):
                 os.remove(o)
-        raise subprocess.CalledProcessError(max(rcs), "nvcc -c")
-    tmp = SO + f".tmp{os.getpid()}"
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
-                           f"-Xlinker=-rpath={os.path.join(nd, 'lib')}", "-lcudart"])
-    for o in objs:
-        os.remove(o)
     os.replace(tmp, SO)
     return SO
 
