@@ -545,7 +545,7 @@ template <int D> struct PermCfg;
 template <> struct PermCfg<1> { static constexpr int J = 16, T = 256; };
 template <> struct PermCfg<2> { static constexpr int J = 16, T = 256; };
 template <> struct PermCfg<3> { static constexpr int J = 16, T = 256; };
-template <> struct PermCfg<4> { static constexpr int J = 16, T = 256; };
+template <> struct PermCfg<4> { static constexpr int J = 8, T = 256; };
 template <> struct PermCfg<5> { static constexpr int J = 16, T = 160; };
 template <> struct PermCfg<6> { static constexpr int J = 8, T = 128; };
 template <> struct PermCfg<7> { static constexpr int J = 4, T = 128; };
