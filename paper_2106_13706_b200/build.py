@@ -39,7 +39,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return SO
     nd = nccl_dir()
-    common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
+    debug = ["-DDDKS_DEBUG"] if os.environ.get("DDKS_DEBUG") else []  # device-side bounds asserts (ddks_common.cuh)
+    common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", *debug, "-Xcompiler", "-fPIC,-fvisibility=hidden",
               "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(nd, "include"), "-I", os.path.join(ROOT, "include")]
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)

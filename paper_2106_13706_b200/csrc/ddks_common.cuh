@@ -5,6 +5,15 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Device-side bounds checks, compiled in with -DDDKS_DEBUG (build.py: DDKS_DEBUG=1). compute-sanitizer is not
+// available on the GPU pool, so the debug build's asserts (run under the whole GPU test suite) stand in for memcheck.
+#ifdef DDKS_DEBUG
+#include <cassert>
+#define DDKS_ASSERT(c) assert(c)
+#else
+#define DDKS_ASSERT(c) ((void)0)
+#endif
+
 namespace ddks {
 
 template <int D> __host__ __device__ constexpr int padded_dim() { return D <= 4 ? 4 : 8; }

@@ -225,10 +225,17 @@ __device__ __forceinline__ float code_addr(const float (&x)[D], const float (&o)
 // base[r % NB_] is the float-encoded address of origin slot r's bin-0 word; weights 4 * 2^k * WPB. inc_lo / inc_hi:
 // the increment for low-half / high-half origins (R == 1: the caller passes this thread's increment in both).
 // With R <= 2 origins per thread two points are classified per step, so a warp has 2R independent chains in flight.
+// SMEM counter increment at the float-encoded byte offset f (debug builds check it lies inside the counters)
+__device__ __forceinline__ void red_counter(float f, uint32_t ubase, uint32_t inc, uint32_t hbytes) {
+    DDKS_ASSERT(__float_as_uint(f) - 0x4B000000u < hbytes);
+    (void)hbytes;
+    red_add_shared(__float_as_uint(f) + ubase, inc);
+}
+
 template <int D, bool GT, int R, int RP, int NB_, int WPB, int DP, int FIRST = 0>
 __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, const float (&o)[R][D],
                                              const float (&base)[NB_], uint32_t ubase, uint32_t inc_lo,
-                                             uint32_t inc_hi) {
+                                             uint32_t inc_hi, uint32_t hbytes) {
     if (lo >= hi) return;
     int p = lo;
     // prefetches read at most two points past hi <= TILE: still inside the SMEM allocation (the next stage or the
@@ -254,15 +261,15 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const uint32_t inc = (R >= 2 && r < RP) ? inc_lo : inc_hi;
-                red_add_shared(__float_as_uint(fa[r]) + ubase, inc);
-                red_add_shared(__float_as_uint(fb[r]) + ubase, inc);
+                red_counter(fa[r], ubase, inc, hbytes);
+                red_counter(fb[r], ubase, inc, hbytes);
             }
         }
         if (p < hi) {
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                red_add_shared(__float_as_uint(code_addr<D, GT, WPB, FIRST>(na, o[r], base[r % NB_])) + ubase,
-                               (R >= 2 && r < RP) ? inc_lo : inc_hi);
+                red_counter(code_addr<D, GT, WPB, FIRST>(na, o[r], base[r % NB_]), ubase,
+                            (R >= 2 && r < RP) ? inc_lo : inc_hi, hbytes);
         }
         return;
     }
@@ -276,8 +283,8 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
         load_point<D>(tile + (p + 1) * DP, xn);
 #pragma unroll
         for (int r = 0; r < R; ++r)
-            red_add_shared(__float_as_uint(code_addr<D, GT, WPB, FIRST>(x, o[r], base[r % NB_])) + ubase,
-                           (R >= 2 && r < RP) ? inc_lo : inc_hi);
+            red_counter(code_addr<D, GT, WPB, FIRST>(x, o[r], base[r % NB_]), ubase,
+                        (R >= 2 && r < RP) ? inc_lo : inc_hi, hbytes);
     }
 }
 
@@ -385,13 +392,13 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
             else if (GT ? (t_lo > o_hi) : (t_lo >= o_hi)) mode = 1;
         }
         if (mode == 2) {
-            count_points<D, GT, R, RP, NBASE, WPB, DP>(tile, 0, split, o, baseP, ubase, incP_lo, R == 1 ? incP_lo : incP_hi);
-            count_points<D, GT, R, RP, NBASE, WPB, DP>(tile, split, cnt, o, baseQ, ubase, incQ_lo, R == 1 ? incQ_lo : incQ_hi);
+            count_points<D, GT, R, RP, NBASE, WPB, DP>(tile, 0, split, o, baseP, ubase, incP_lo, R == 1 ? incP_lo : incP_hi, G::HIST_WORDS * 4u);
+            count_points<D, GT, R, RP, NBASE, WPB, DP>(tile, split, cnt, o, baseQ, ubase, incQ_lo, R == 1 ? incQ_lo : incQ_hi, G::HIST_WORDS * 4u);
         } else if constexpr (X0) {
             count_points<D, GT, R, RP, NBASE, WPB, DP, 1>(tile, 0, split, o, mode ? baseP1 : baseP, ubase, incP_lo,
-                                                          R == 1 ? incP_lo : incP_hi);
+                                                          R == 1 ? incP_lo : incP_hi, G::HIST_WORDS * 4u);
             count_points<D, GT, R, RP, NBASE, WPB, DP, 1>(tile, split, cnt, o, mode ? baseQ1 : baseQ, ubase, incQ_lo,
-                                                          R == 1 ? incQ_lo : incQ_hi);
+                                                          R == 1 ? incQ_lo : incQ_hi, G::HIST_WORDS * 4u);
         }
         __syncthreads();  // every thread is done with stage s
         if (t == 0 && it + S < n_tiles) {
@@ -419,6 +426,7 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
                 int32_t lo, hi;
                 split16(hist[q * WPB + sl], lo, hi);
                 const int32_t v = hiw ? hi : lo;
+                DDKS_ASSERT(oi - a.o_begin < n_orig && oi >= a.o_begin);
                 if (v) atomicAdd(&acc[(int64_t)q * n_orig + (oi - a.o_begin)], v);
             }
         }
@@ -459,6 +467,7 @@ __global__ void k_permute_rows(const float* __restrict__ pts, int DP, int64_t N,
                                float* __restrict__ out, int32_t* __restrict__ perm) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t idx = (int64_t)(keys[j] & 0x7fffffffull);
+        DDKS_ASSERT(idx < N);
         const float4* src = reinterpret_cast<const float4*>(pts + idx * DP);
         float4* dst = reinterpret_cast<float4*>(out + j * DP);
         dst[0] = src[0];
@@ -652,6 +661,7 @@ __global__ void __launch_bounds__(PermGeo<D>::T, 1) k_perm_count(const PermArgs 
 #pragma unroll
             for (int k = 0; k < D; ++k) f = fmaf(cmp_bit<GT>(x[k], o[k]), (float)(4 * (1 << k) * (JP + 1) * T), f);
             const uint32_t addr = __float_as_uint(f) + ubase;
+            DDKS_ASSERT(__float_as_uint(f) - 0x4B000000u + JP * SLOT < (uint32_t)G::CNT_WORDS * 4u);
             red_add_shared(addr + JP * SLOT, 1u);  // T[q]
             const uint32_t* lw = sl + p * JP;
             if constexpr (JP % 4 == 0) {

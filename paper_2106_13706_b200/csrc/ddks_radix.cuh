@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(RS_T) k_rs_scatter(const uint64_t* __restrict_
     for (int i = threadIdx.x; i < n; i += RS_T) {
         const uint64_t key = stage[i];
         const uint32_t dig = (uint32_t)(key >> shift) & 255u;
+        DDKS_ASSERT((int64_t)o[dig] + i - dbase[dig] < N);
         out[sbase + o[dig] + (uint32_t)i - dbase[dig]] = key;
     }
 }

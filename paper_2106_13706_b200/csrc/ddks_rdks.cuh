@@ -304,7 +304,11 @@ __global__ void k_rdb_compact(const uint64_t* __restrict__ key, int64_t N, int n
         const uint64_t k = key[e];
         const int64_t b = s * nbk + rdb_bucket(k, scale, nbk);
         const uint32_t o = coff[b];
-        if (o != ~0u) ck[s * N + o + atomicAdd(&fill[b], 1u)] = k;
+        if (o != ~0u) {
+            const uint32_t pos = o + atomicAdd(&fill[b], 1u);
+            DDKS_ASSERT(pos < N);
+            ck[s * N + pos] = k;
+        }
     }
 }
 
@@ -344,6 +348,7 @@ __global__ void __launch_bounds__(256) k_rdb_finish(const uint64_t* __restrict__
         int np2 = 1;
         while (np2 < n) np2 <<= 1;
         const uint64_t* src = ck + (int64_t)s * N + coff[i];
+        DDKS_ASSERT(coff[i] + (int64_t)n <= N && np2 <= RDB_CAPK);
         for (int j = threadIdx.x; j < np2; j += blockDim.x) sk[j] = j < n ? src[j] : ~0ull;
         __syncthreads();
         for (int size = 2; size <= np2; size <<= 1)

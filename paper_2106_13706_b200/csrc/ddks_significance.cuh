@@ -21,6 +21,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "ddks_common.cuh"
+
 namespace ddks {
 
 __global__ void k_logfact(double* __restrict__ LF, int64_t n_max) {
@@ -59,6 +61,7 @@ struct LogPmf {
         logmu = log(mu);
     }
     __device__ __forceinline__ double operator()(int64_t n) const {
+        DDKS_ASSERT(n >= 0);
         if (poisson) return -mu + (double)n * logmu - LF[n];
         return LF[m] - LF[n] - LF[m - n] + (double)n * loglam + (double)(m - n) * log1m;
     }
@@ -236,6 +239,8 @@ __global__ void __launch_bounds__(SIG_T) k_sig_table(const SigArgs a) {
             // band of n_P with |n_P N_T - nT N_P| <= num: [lo, hi], exact int64
             const int64_t lo = ceil_div(nT * a.N_P - num, a.N_T, invT);
             const int64_t hi = floor_div(nT * a.N_P + num, a.N_T, invT);
+            DDKS_ASSERT(lo <= aP || (lo > eP + 1 ? eP + 1 : lo) - 1 - aP < W);
+            DDKS_ASSERT(hi >= eP || (hi < aP - 1 ? aP - 1 : hi) + 1 - aP >= 0);
             const double left = lo <= aP ? 0.0 : A[(lo > eP + 1 ? eP + 1 : lo) - 1 - aP];   // sum_{n_P < lo}
             const double right = hi >= eP ? 0.0 : B[(hi < aP - 1 ? aP - 1 : hi) + 1 - aP];  // sum_{n_P > hi}
             const double tail = left + right;

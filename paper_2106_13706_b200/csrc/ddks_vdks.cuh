@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(256) k_vox_orthants(const uint32_t* __restrict
 #pragma unroll
             for (int m = 0; m < D; ++m) {
                 const int64_t cm = ((b >> m) & 1) ? k - 1 : c[m] - 1;
+                DDKS_ASSERT(cm < k);
                 empty |= cm < 0;
                 idx += cm * stride[m];
             }
