@@ -46,14 +46,19 @@ template <> struct Cfg<7> { static constexpr int R = 2, T = 384, TILE = 256, S =
 template <> struct Cfg<8> { static constexpr int R = 1, T = 384, TILE = 256, S = 3; };
 
 
+// SPLIT (c_P and c_Q kept apart) doubles the bins: halve R (keeping it even or 1), or T when R is already <= 2
+template <int D> struct CfgSplit {
+    static constexpr int R = Cfg<D>::R > 2 ? Cfg<D>::R / 2 : Cfg<D>::R;
+    static constexpr int T = Cfg<D>::R <= 2 ? Cfg<D>::T / 2 : Cfg<D>::T;
+};
+
 template <int D, bool SPLIT, int DPX = padded_dim<D>()> struct Geo {
-    // SPLIT doubles the bins: halve R (keeping it even or 1), or T when R is already <= 2
-    static constexpr int R = (SPLIT && Cfg<D>::R > 2) ? Cfg<D>::R / 2 : Cfg<D>::R;
-    static constexpr int T = (SPLIT && Cfg<D>::R <= 2) ? Cfg<D>::T / 2 : Cfg<D>::T;
+    static constexpr int R = SPLIT ? CfgSplit<D>::R : Cfg<D>::R;
+    static constexpr int T = SPLIT ? CfgSplit<D>::T : Cfg<D>::T;
     static constexpr int RP = R / 2;                            // counter words per (bin, thread) when R >= 2
     static constexpr int NBASE = R >= 2 ? RP : 1;               // distinct counter base addresses per thread
     static constexpr int WPB = R * T / 2;                       // counter words per bin
-    static constexpr int TILE = DPX > 8 ? Cfg<D>::TILE / 2 : Cfg<D>::TILE;  // 48-byte x0 rows: half the points
+    static constexpr int TILE = Cfg<D>::TILE;
     static constexpr int S = Cfg<D>::S;
     static constexpr int DP = DPX;
     static constexpr int NQ = 1 << D;
