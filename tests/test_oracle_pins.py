@@ -467,3 +467,18 @@ def test_rdks_pins():
     assert a[0] == b[0] and 0 <= a[0] <= a[1]
     s = np.array([2.0, 0.25, 4.0, 1.0], np.float32)
     assert O.rdks(P * s, Q * s)[:2] == a[:2]
+
+
+def test_stored_c5_oracle_matches_inputs_and_oracle_source():
+    # the stored full-C5 oracle result (tests/golden/make_c5_oracle.py) belongs to these input bytes and this oracle
+    import hashlib
+    path = os.path.join(os.path.dirname(__file__), "golden", "c5_oracle.json")
+    if not os.path.exists(path):
+        pytest.skip("tests/golden/c5_oracle.json not generated yet")
+    g = json.load(open(path))
+    assert g["input_sha256"] == I.SURVEY_SHA256["C5"]
+    src = open(os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "ddks_oracle.c"), "rb").read()
+    assert g["oracle_c_sha256"] == hashlib.sha256(src).hexdigest()
+    assert g["den"] == 10**12 and 0 < g["num"] <= g["den"] and float.fromhex(g["D_hex"]) == g["num"] / g["den"]
+    # the survey's independent per-origin spot values bound it from below
+    assert g["num"] >= 42316 * 10**6

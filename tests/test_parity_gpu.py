@@ -349,3 +349,19 @@ def test_permutation_null_beyond_label_path(ctx):
     null, obs, p = ctx.permutation_null(dev(pooled), n_P, dev(perms))
     o_null, o_obs, o_pnum, o_p = O.permutation_null(pooled, n_P, perms)
     assert np.array_equal(null, o_null) and obs.num == o_obs and p == o_p
+
+
+def test_config_c5_full_vs_stored_oracle(ctx):
+    # the whole C5 statistic against the oracle's own full run (tests/golden/make_c5_oracle.py; hours of CPU, so
+    # stored): num, den, D bits and argmax, bit for bit
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "c5_oracle.json")
+    if not os.path.exists(path):
+        pytest.skip("tests/golden/c5_oracle.json not generated yet")
+    g = json.load(open(path))
+    P, Q = I.config("C5")
+    assert I.sha256_pq(P, Q) == g["input_sha256"]
+    r = ctx.stat(dev(P), dev(Q))
+    assert (r.num, r.den, r.argmax_origin) == (g["num"], g["den"], g["argmax_origin"])
+    assert float.hex(r.D) == g["D_hex"]
