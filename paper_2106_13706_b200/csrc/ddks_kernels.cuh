@@ -35,12 +35,13 @@ namespace ddks {
 // global accumulators; if the whole point set fits one segment it finalises in-kernel instead.
 template <int D> struct Cfg;
 // R origins per thread (1 or even), T threads per CTA (multiple of 64 when R == 1), TILE points per SMEM stage,
-// S stages (DIFF mode). T is a multiple of 128 so every SMSP gets the same number of warps.
+// S stages (DIFF mode). T is a multiple of 128 so every SMSP gets the same number of warps (d=5: R=12 x 8 warps
+// measured 0.8% faster than R=8 x 12 warps on the x0-ordered C5 kernel).
 template <> struct Cfg<1> { static constexpr int R = 8, T = 256, TILE = 512, S = 3; };
 template <> struct Cfg<2> { static constexpr int R = 8, T = 256, TILE = 512, S = 3; };
 template <> struct Cfg<3> { static constexpr int R = 8, T = 256, TILE = 512, S = 3; };
 template <> struct Cfg<4> { static constexpr int R = 4, T = 256, TILE = 512, S = 3; };
-template <> struct Cfg<5> { static constexpr int R = 8, T = 384, TILE = 256, S = 3; };
+template <> struct Cfg<5> { static constexpr int R = 12, T = 256, TILE = 256, S = 3; };
 template <> struct Cfg<6> { static constexpr int R = 4, T = 384, TILE = 256, S = 3; };
 template <> struct Cfg<7> { static constexpr int R = 2, T = 384, TILE = 256, S = 3; };
 template <> struct Cfg<8> { static constexpr int R = 1, T = 384, TILE = 256, S = 3; };
@@ -51,6 +52,7 @@ template <int D> struct CfgSplit {
     static constexpr int R = Cfg<D>::R > 2 ? Cfg<D>::R / 2 : Cfg<D>::R;
     static constexpr int T = Cfg<D>::R <= 2 ? Cfg<D>::T / 2 : Cfg<D>::T;
 };
+template <> struct CfgSplit<5> { static constexpr int R = 4, T = 384; };  // A/B: 12 warps beat R=6 x 8 warps
 
 template <int D, bool SPLIT, int DPX = padded_dim<D>()> struct Geo {
     static constexpr int R = SPLIT ? CfgSplit<D>::R : Cfg<D>::R;
