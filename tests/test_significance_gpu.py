@@ -162,3 +162,17 @@ def test_significance_x0_c2(ctx):
         a = cx.significance(dev(P), dev(Q), detail=True)
     b = ctx.significance(dev(P), dev(Q), detail=True)
     assert a.stat == b.stat and np.array_equal(a.mt_hist, b.mt_hist) and a.log_prod == b.log_prod
+
+
+@pytest.mark.parametrize("n_P,n_Q,d", [(40, 30, 2), (35, 45, 4), (30, 26, 6)])
+def test_significance_ties_gt(n_P, n_Q, d):
+    # the '>' convention (DDKS_FLAG_TIES_GT, test only) through both the position- and the x0-ordered SPLIT kernels
+    P, Q = I.random_pair(1500 + n_P + d, n_P, n_Q, d, "grid")
+    S_o, lp_o, num_o = O.significance(P, Q, ties_gt=True)
+    MT = O.membership(Q, np.concatenate([P, Q]), ties_gt=True)
+    h_o = np.bincount(MT.ravel(), minlength=n_Q + 1).astype(np.uint64)
+    for fl in (K.DDKS_FLAG_TIES_GT, K.DDKS_FLAG_TIES_GT | K.DDKS_FLAG_FORCE_X0):
+        with K.Context(flags=fl) as c:
+            g = c.significance(dev(P), dev(Q), detail=True)
+        assert g.stat.num == num_o and np.array_equal(g.mt_hist, h_o)
+        assert abs(g.log_prod - lp_o) <= g.cells * tol_entry(n_P, n_Q) + 1e-12 * abs(lp_o)
