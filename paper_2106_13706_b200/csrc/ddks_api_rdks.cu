@@ -58,7 +58,9 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     CU(cudaMemsetAsync(keys, 0xff, (size_t)d * 4, st));
     CU(cudaMemsetAsync(keys + d, 0, (size_t)d * 4, st));
     CU(cudaMemsetAsync(cnum, 0, (size_t)(d + 1) * 8, st));
-    ddks::k_rd_minmax<<<(int)std::max<int64_t>(1, std::min<int64_t>((N + 1023) / 1024, 148 * 2)), 256, 0, st>>>(
+    const int gy = std::min(d, 1024);
+    const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((N + 1023) / 1024, std::max(1, 296 / gy)));
+    ddks::k_rd_minmax<<<dim3(gx, gy), 256, 0, st>>>(
         (const float*)dP, n_P, (const float*)dQ, n_Q, d, keys, &dres->flag);
     CHECK_LAUNCH();
     ctx->launches++;

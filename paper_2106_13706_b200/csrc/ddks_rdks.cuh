@@ -21,15 +21,15 @@
 namespace ddks {
 
 // keys[0..d) = min keys (init 0xffffffff), keys[d..2d) = max keys (init 0), as order-preserving uint32.
-// Grid-stride over points inside each dimension, block reduction, one atomic pair per (block, dimension);
-// non-finite -> *flag |= 1.
+// grid.y strides over dimensions, grid.x over point chunks (so d = 1000 with 200 points is 1000 CTAs, and d = 5 with
+// 2M points is 5 x 60); block reduction, one atomic pair per (block, dimension); non-finite -> *flag |= 1.
 __global__ void __launch_bounds__(256) k_rd_minmax(const float* __restrict__ P, int64_t n_P,
                                                    const float* __restrict__ Q, int64_t n_Q, int d, uint32_t* keys,
                                                    uint32_t* flag) {
     __shared__ uint32_t sa[8], sb[8];
     const int64_t N = n_P + n_Q;
     bool bad = false;
-    for (int m = 0; m < d; ++m) {
+    for (int m = blockIdx.y; m < d; m += gridDim.y) {
         uint32_t a = 0xffffffffu, b = 0u;
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
             float x = i < n_P ? P[i * d + m] : Q[(i - n_P) * d + m];
@@ -81,6 +81,7 @@ __global__ void k_rd_keys(const double* __restrict__ xn, int64_t N, int64_t n_P,
         const int c = (int)(e - i * nc) + c_begin;
         const double* row = xn + i * d;
         double s = 0.0;
+#pragma unroll 8
         for (int m = 0; m < d; ++m) {
             const double t = __dsub_rn(row[m], (c >= 1 && m == c - 1) ? 1.0 : 0.0);
             s = __dadd_rn(s, __dmul_rn(t, t));
