@@ -15,8 +15,12 @@
 //     fire-and-forget ATOMS.ADD to a thread-private, bank-conflict-free SMEM counter;
 //   * DIFF mode keeps one signed counter per orthant: c_P*a - c_Q*b with a = n_Q/g, b = n_P/g
 //     (g = gcd(n_P, n_Q)), so |counter| * g is exactly |c_P n_Q - c_Q n_P| (P:L238 cross-multiplied);
-//     SPLIT mode (only when n_P n_Q / g >= 2^31) keeps c_P and c_Q separately;
-//   * finalisation is exact integer arithmetic; the max is a warp-shuffle + CTA + atomicMax(u64) reduction.
+//     SPLIT mode (when DIFF would overflow, and for the significance, which needs c_Q) keeps c_P and c_Q apart;
+//   * X0 (large N): rows pre-sorted label-major by x_0, so bit 0 is decided once per tile for most tiles and only
+//     dims 1..d-1 are compared (DESIGN.md §7 "x0 ordering");
+//   * finalisation is exact integer arithmetic; the max is a warp-shuffle + CTA + atomicMax(u64) reduction;
+//   * the label-invariant permutation null (k_labels / k_perm_count) classifies each pair once per chunk of
+//     permutations.
 #pragma once
 #include <cstdint>
 #include <utility>
