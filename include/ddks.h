@@ -22,13 +22,17 @@
  *     unspecified and ddks_last_error(ctx) holds a one-line message.
  *   - A context is bound to one device and one host thread; it is not thread-safe.
  *   - Multi-GPU (world > 1): every rank makes the same call with the same (replicated) inputs.
- *       ddks_stat                shards the pooled ORIGINS into `world` contiguous ranges and combines the
+ *       ddks_stat /              shard the pooled ORIGINS into `world` contiguous ranges (of the pooled order, or of the
+ *       ddks_significance        x_0 order when the x0-ordered kernel runs: N >= 200000, 2 <= d <= 8) and combine the
  *                                per-rank maxima with one NCCL all-reduce(max) of a uint64 (+ one all-reduce(min)
- *                                for the argmax).
+ *                                for the argmax); the significance also all-reduces its M_T histogram.
  *       ddks_stat_batch /
  *       ddks_permutation_null    shard ITEMS (pairs / permutations) contiguously and all-gather the per-item nums,
  *                                so every rank returns the full result.
- *   - Limits: 1 <= d <= 8; n_P, n_Q >= 1; n_P + n_Q < 2^31; n_P*n_Q < 2^53 (so D is one exact IEEE division).
+ *       ddks_vdks / ddks_rdks    shard points + voxels / corners (see each call).
+ *   - Limits: 1 <= d <= 8 (ddks_rdks: any d >= 1); n_P, n_Q >= 1; n_P + n_Q < 2^31; n_P*n_Q < 2^53 (so D is one
+ *     exact IEEE division).
+ *   - Results do not depend on the world size, the stream, the flags marked TEST ONLY, or which internal kernel ran.
  */
 #ifndef DDKS_H_
 #define DDKS_H_
