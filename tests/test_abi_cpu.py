@@ -75,3 +75,17 @@ def test_version_and_create_without_gpu(lib):
     with pytest.raises(lib.DDKSError) as e:
         lib.ddks_create(world=2, rank=0, nccl_id=None)
     assert e.value.status == 1
+
+
+def test_null_context_is_an_argument_error_not_a_crash(lib):
+    # every compute entry point rejects a NULL context with DDKS_ERR_INVALID_ARGUMENT before touching the device
+    L, NULL = lib.LIB, None
+    assert L.ddks_stat(NULL, NULL, 1, NULL, 1, 2, NULL, NULL) == 1
+    assert L.ddks_stat_batch(NULL, NULL, NULL, 1, 1, 1, 2, NULL, NULL) == 1
+    assert L.ddks_permutation_null(NULL, NULL, 1, 1, 2, NULL, 0, NULL, NULL, NULL, NULL) == 1
+    assert L.ddks_stat_per_origin(NULL, NULL, 1, NULL, 1, 2, 0, 1, NULL, NULL) == 1
+    assert L.ddks_significance(NULL, NULL, 1, NULL, 1, 2, 0, NULL, NULL, NULL, NULL) == 1
+    assert L.ddks_vdks(NULL, NULL, 1, NULL, 1, 2, 4, NULL, NULL) == 1
+    assert L.ddks_rdks(NULL, NULL, 1, NULL, 1, 2, NULL, NULL) == 1
+    assert L.ddks_profile_read(NULL, NULL, NULL, NULL) == 1
+    assert L.ddks_destroy(NULL) == 0 and L.ddks_launch_count(NULL) == 0
