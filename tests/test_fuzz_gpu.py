@@ -1,6 +1,8 @@
 """Seeded fuzz of every GPU path against the oracle at sizes that straddle the kernels' internal boundaries: tile
 sizes (256/512 points), the int16 flush window (32767 points), origin blocks (R*T), radix tiles (4096 keys), warp
 and CTA edges, plus degenerate shapes (single points, one-sided samples, constant or duplicated coordinates)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -44,7 +46,7 @@ def ctxs():
         c.close()
 
 
-@pytest.mark.parametrize("n_P,n_Q,d,kind,seed", cases(2024, 36))
+@pytest.mark.parametrize("n_P,n_Q,d,kind,seed", cases(2024, int(os.environ.get("DDKS_FUZZ_CASES", "36"))))
 def test_fuzz_exact_and_approx(ctxs, n_P, n_Q, d, kind, seed):
     P, Q = I.random_pair(seed, n_P, n_Q, d, kind)
     want = O.ddks(P, Q)
