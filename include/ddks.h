@@ -166,6 +166,14 @@ DDKS_API ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const
 DDKS_API ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
                                void* stream, ddks_result* out);
 
+/* Multi-GPU rehearsal on one device (scaling projections and shard-logic tests): ddks_stat restricted to the origin
+ * shard that rank `rank` of `world` would own (same kernels, same shard — of the x_0 order when the x0-ordered
+ * kernel runs — and no collective). out->num is the shard's maximum and out->argmax_origin the smallest pooled origin
+ * attaining it; the max of the `world` nums, and the smallest argmax among the shards attaining that max, are
+ * ddks_stat's result. ctx must be single-rank (world == 1 at ddks_create). */
+DDKS_API ddks_status ddks_stat_shard(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
+                                     int world, int rank, void* stream, ddks_result* out);
+
 /* Host-only helper (no GPU needed): the contiguous origin / item range [*begin, *end) that `rank` of `world`
  * owns out of `total` units. Ranges are balanced to within one unit and cover 0..total exactly. */
 DDKS_API ddks_status ddks_shard_range(int64_t total, int world, int rank, int64_t* begin, int64_t* end);

@@ -619,9 +619,10 @@ ddks_status ddks_profile_read(ddks_ctx* ctx, double* count_ms, int64_t* launches
 }
 
 // a1-a7 for one pair, origins sharded across ranks; optional per-origin export (debug path, single rank).
+// shard_world > 0: compute only the origin shard that rank shard_rank of shard_world would own (ddks_stat_shard)
 static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
                              void* stream, ddks_result* out, int64_t o_begin_req, int64_t o_end_req,
-                             uint64_t* per_origin_out) {
+                             uint64_t* per_origin_out, int shard_world = 0, int shard_rank = 0) {
     ctx->err.clear();
     ddks_status s = check_sizes(ctx, n_P, n_Q, d);
     if (s) return s;
@@ -636,6 +637,8 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
     if (export_mode) {
         ob = o_begin_req;
         oe = o_end_req;
+    } else if (shard_world > 0) {
+        ddks_shard_range(N, shard_world, shard_rank, &ob, &oe);
     } else {
         ddks_shard_range(N, ctx->world, ctx->rank, &ob, &oe);
     }
@@ -678,6 +681,15 @@ ddks_status ddks_stat(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     if (!ctx) return DDKS_ERR_INVALID_ARGUMENT;
     if (!out) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "null out");
     return stat_impl(ctx, P, n_P, Q, n_Q, d, stream, out, 0, 0, nullptr);
+}
+
+ddks_status ddks_stat_shard(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
+                            int world, int rank, void* stream, ddks_result* out) {
+    if (!ctx) return DDKS_ERR_INVALID_ARGUMENT;
+    if (!out) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "null out");
+    if (ctx->world != 1) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "ddks_stat_shard needs a single-rank context");
+    if (world < 1 || rank < 0 || rank >= world) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad world/rank");
+    return stat_impl(ctx, P, n_P, Q, n_Q, d, stream, out, 0, 0, nullptr, world, rank);
 }
 
 ddks_status ddks_stat_per_origin(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,

@@ -75,6 +75,8 @@ def _load() -> ctypes.CDLL:
         "ddks_stat_batch": ([vp, vp, vp, i64, i64, i64, i32, vp, ctypes.POINTER(ddks_result)], ctypes.c_int),
         "ddks_permutation_null": ([vp, vp, i64, i64, i32, vp, i64, vp, vp, ctypes.POINTER(ddks_result),
                                    ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+        "ddks_stat_shard": ([vp, vp, i64, vp, i64, i32, ctypes.c_int, ctypes.c_int, vp, ctypes.POINTER(ddks_result)],
+                            ctypes.c_int),
         "ddks_stat_per_origin": ([vp, vp, i64, vp, i64, i32, i64, i64, vp, vp], ctypes.c_int),
         "ddks_significance": ([vp, vp, i64, vp, i64, i32, u32, vp, ctypes.POINTER(ddks_significance_result), vp, vp],
                               ctypes.c_int),
@@ -97,7 +99,7 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 EXPORTED = ("ddks_get_nccl_id", "ddks_create", "ddks_stat", "ddks_stat_batch", "ddks_permutation_null",
-            "ddks_stat_per_origin", "ddks_significance", "ddks_vdks", "ddks_rdks", "ddks_shard_range", "ddks_launch_count", "ddks_profile_read", "ddks_destroy",
+            "ddks_stat_per_origin", "ddks_stat_shard", "ddks_significance", "ddks_vdks", "ddks_rdks", "ddks_shard_range", "ddks_launch_count", "ddks_profile_read", "ddks_destroy",
             "ddks_last_error", "ddks_version")
 
 
@@ -235,6 +237,15 @@ def ddks_permutation_null(ctx, pooled, n_P: int, perms, stream=None):
     return null, Result(obs.num, obs.den, obs.D, obs.argmax_origin), pv.value
 
 
+def ddks_stat_shard(ctx, P, Q, world: int, rank: int, stream=None) -> Result:
+    """ddks_stat restricted to the origin shard rank `rank` of `world` would own (no collective)."""
+    p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
+    r = ddks_result()
+    _check(LIB.ddks_stat_shard(ctx, p.ptr, p.shape[0], q.ptr, q.shape[0], p.shape[1], world, rank, _stream(stream),
+                               ctypes.byref(r)), ctx)
+    return Result(r.num, r.den, r.D, r.argmax_origin)
+
+
 def ddks_stat_per_origin(ctx, P, Q, o_begin: int, o_end: int, stream=None) -> np.ndarray:
     p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
     out = np.zeros(max(o_end - o_begin, 0), dtype=np.uint64)
@@ -305,6 +316,9 @@ class Context:
 
     def permutation_null(self, pooled, n_P, perms, stream=None):
         return ddks_permutation_null(self.ctx, pooled, n_P, perms, stream)
+
+    def stat_shard(self, P, Q, world, rank, stream=None) -> Result:
+        return ddks_stat_shard(self.ctx, P, Q, world, rank, stream)
 
     def stat_per_origin(self, P, Q, o_begin, o_end, stream=None):
         return ddks_stat_per_origin(self.ctx, P, Q, o_begin, o_end, stream)

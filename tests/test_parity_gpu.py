@@ -365,3 +365,20 @@ def test_config_c5_full_vs_stored_oracle(ctx):
     r = ctx.stat(dev(P), dev(Q))
     assert (r.num, r.den, r.argmax_origin) == (g["num"], g["den"], g["argmax_origin"])
     assert float.hex(r.D) == g["D_hex"]
+
+
+@pytest.mark.parametrize("flags,n_P,n_Q,d", [(0, 3000, 2500, 3), (64, 3000, 2500, 3), (64, 9000, 7000, 5),
+                                               (0, 1200, 1300, 8), (64, 150, 170, 2)])
+def test_shard_rehearsal_combines_to_the_statistic(flags, n_P, n_Q, d):
+    # ddks_stat_shard runs the exact kernels on the origin shard a rank would own (x0 order when FORCE_X0 = 64);
+    # max over shards and the smallest attaining argmax must reproduce ddks_stat and the oracle for any world size
+    P, Q = I.random_pair(9900 + n_P + d, n_P, n_Q, d, "mixed")
+    want = O.ddks(P, Q)
+    with K.Context(flags=flags) as c:
+        full = c.stat(dev(P), dev(Q))
+        assert (full.num, full.argmax_origin) == (want[0], want[3])
+        for world in (2, 3, 8):
+            parts = [c.stat_shard(dev(P), dev(Q), world, r) for r in range(world)]
+            num = max(p.num for p in parts)
+            arg = min(p.argmax_origin for p in parts if p.num == num)
+            assert (num, arg) == (want[0], want[3]), (world, parts)
