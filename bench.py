@@ -64,29 +64,36 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons every 50 ms. Started at the top of main() (nvidia-smi needs ~0.1 s to
+    produce its first row); mark()/stop() bracket the timed region and only rows inside it are reported — unless the
+    region is shorter than the sampling period, in which case every row up to the end of the timed region is used
+    and `window` says so."""
     FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
               "clocks_event_reasons.sw_power_cap"]
 
     def __init__(self, gpu: int):
-        self.gpu, self.rows, self.proc = gpu, [], None
+        self.gpu, self.rows, self.proc, self.t0 = gpu, [], None, None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={','.join(self.FIELDS)}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
             self.proc = None
 
+    def mark(self):
+        self.t0 = time.perf_counter()
+
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
 
     def stop(self):
+        t1 = time.perf_counter()
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -95,12 +102,17 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         self.t.join(timeout=2)
-        sm = [float(r[0]) for r in self.rows if len(r) == 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) == 7 and r[1].replace(".", "").isdigit()]
+        rows = [r for t, r in self.rows if len(r) == 7 and self.t0 is not None and self.t0 <= t <= t1]
+        window = "timed region"
+        if not rows:
+            rows = [r for t, r in self.rows if len(r) == 7 and t <= t1]
+            window = "whole run up to the end of the timed region (timed region shorter than the 50 ms period)"
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows if len(r) == 7 for i in range(4) if r[3 + i] == "Active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(sm)}
+                "reasons": reasons, "samples": len(sm), "window": window}
 
 
 def workload(name):
@@ -304,6 +316,8 @@ def main():
     if world != args.gpus:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
     torch.cuda.set_device(local)
+    clocks = ClockSampler(local)  # started early: nvidia-smi takes ~0.1 s to produce its first row
+    clocks.start()
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2106_13706_b200 import ddks as K
@@ -338,8 +352,7 @@ def main():
         res = step.call(*step.dev)
     ctx.profile_read()  # discard warm-up profile
     barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks.mark()
     launches0 = ctx.launch_count
     step_ms = []
     t_wall0 = time.perf_counter()
