@@ -145,6 +145,13 @@ DDKS_API ddks_status ddks_significance(ddks_ctx* ctx, const float* P, int64_t n_
                               uint32_t sig_flags, void* stream, ddks_significance_result* out, uint64_t* mt_hist,
                               double* log_p_table);
 
+/* Batched significance: B independent pairs P[B][n_P][d], Q[B][n_Q][d] (device or host), each exactly as
+ * ddks_significance (no histogram/table outputs); out: host [B], stat.argmax_origin = -1. Multi-GPU: items sharded,
+ * every rank returns all B results. For the paper's repeated small tests (power analyses). */
+DDKS_API ddks_status ddks_significance_batch(ddks_ctx* ctx, const float* P, const float* Q, int64_t B, int64_t n_P,
+                                             int64_t n_Q, int32_t d, uint32_t sig_flags, void* stream,
+                                             ddks_significance_result* out);
+
 /* ---- vdKS: voxel approximation (§2.2.2, Alg. 1) -------------------
  * NormalizeData: per dimension over the pooled points, x' = (x - min)/(max - min) in double (a constant dimension
  * maps to 0.5; R15); IndexFromPoint: cell c_m = min(floor(x'_m k), k-1), k voxels per dimension;

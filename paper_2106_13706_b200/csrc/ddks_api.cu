@@ -207,7 +207,7 @@ ddks_status launch_count_d(ddks_ctx* ctx, const CountPlan& pl, const ddks::Count
 // force_split + hist (significance): SPLIT counters, and the finaliser histograms c_Q into hist[n_Q + 1].
 ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int64_t n_P, int64_t n_Q,
                       int64_t o_begin, int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st,
-                      bool force_split = false, unsigned long long* hist = nullptr) {
+                      bool force_split, unsigned long long* hist) {
     const int64_t N = n_P + n_Q;
     const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
     const uint64_t a_ = (uint64_t)n_Q / g, b_ = (uint64_t)n_P / g;
@@ -232,11 +232,12 @@ ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int6
     a.item_num = item_num;
     a.per_origin = per_origin;
     a.hist = split ? hist : nullptr;
+    a.hist_stride = n_Q + 1;
     if (B > 65535) {  // grid.z limit: run the items in chunks
         for (int64_t b0 = 0; b0 < B; b0 += 65535) {
             const int64_t nb = std::min<int64_t>(65535, B - b0);
             ddks_status s = run_count(ctx, packed + b0 * N * pad_dim(d), d, nb, n_P, n_Q, o_begin, o_end,
-                                      item_num + b0, nullptr, st);
+                                      item_num + b0, nullptr, st, force_split, hist ? hist + b0 * (n_Q + 1) : nullptr);
             if (s) return s;
         }
         return DDKS_OK;
@@ -323,6 +324,7 @@ ddks_status run_count_x0_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     a.per_origin = per_origin;
     a.perm = (const int32_t*)ctx->x0_perm.p;
     a.hist = split ? hist_out : nullptr;
+    a.hist_stride = n_Q + 1;
     const bool gt = (ctx->flags & DDKS_FLAG_TIES_GT) != 0;
     if (split)
         return gt ? launch_count_t<D, true, true, true>(ctx, pl, a, st) : launch_count_t<D, true, false, true>(ctx, pl, a, st);
@@ -511,6 +513,28 @@ ddks_status collect_profile(ddks_ctx* ctx) {
 
 ddks_status bind_device(ddks_ctx* ctx) {
     CU(cudaSetDevice(ctx->device));
+    return DDKS_OK;
+}
+
+// Items [i0, i1) of an already-packed batch -> nums into dev item_num[i0..i1).
+ddks_status all_gather_items(ddks_ctx* ctx, uint64_t* dev_nums, int64_t total, cudaStream_t st) {
+    // every rank owns a contiguous shard; NCCL all-gather needs equal counts -> pad to the largest shard
+    int64_t b0, b1;
+    ddks_shard_range(total, ctx->world, 0, &b0, &b1);
+    const int64_t chunk = b1 - b0;  // rank 0 holds the largest shard
+    ddks_status s = ensure(ctx, ctx->packed2, (size_t)chunk * ctx->world * 8);
+    if (s) return s;
+    int64_t mb, me;
+    ddks_shard_range(total, ctx->world, ctx->rank, &mb, &me);
+    uint64_t* gathered = (uint64_t*)ctx->packed2.p;
+    NC(ncclAllGather(dev_nums + mb, gathered, (size_t)chunk, ncclUint64, ctx->comm, st));
+    for (int r = 0; r < ctx->world; ++r) {
+        int64_t rb, re;
+        ddks_shard_range(total, ctx->world, r, &rb, &re);
+        if (re > rb)
+            CU(cudaMemcpyAsync(dev_nums + rb, gathered + (int64_t)r * chunk, (size_t)(re - rb) * 8,
+                               cudaMemcpyDeviceToDevice, st));
+    }
     return DDKS_OK;
 }
 
@@ -703,28 +727,6 @@ ddks_status ddks_stat_per_origin(ddks_ctx* ctx, const float* P, int64_t n_P, con
         return s;
     }
     return stat_impl(ctx, P, n_P, Q, n_Q, d, stream, nullptr, o_begin, o_end, num_out);
-}
-
-// Items [i0, i1) of an already-packed batch -> nums into dev item_num[i0..i1).
-static ddks_status all_gather_items(ddks_ctx* ctx, uint64_t* dev_nums, int64_t total, cudaStream_t st) {
-    // every rank owns a contiguous shard; NCCL all-gather needs equal counts -> pad to the largest shard
-    int64_t b0, b1;
-    ddks_shard_range(total, ctx->world, 0, &b0, &b1);
-    const int64_t chunk = b1 - b0;  // rank 0 holds the largest shard
-    ddks_status s = ensure(ctx, ctx->packed2, (size_t)chunk * ctx->world * 8);
-    if (s) return s;
-    int64_t mb, me;
-    ddks_shard_range(total, ctx->world, ctx->rank, &mb, &me);
-    uint64_t* gathered = (uint64_t*)ctx->packed2.p;
-    NC(ncclAllGather(dev_nums + mb, gathered, (size_t)chunk, ncclUint64, ctx->comm, st));
-    for (int r = 0; r < ctx->world; ++r) {
-        int64_t rb, re;
-        ddks_shard_range(total, ctx->world, r, &rb, &re);
-        if (re > rb)
-            CU(cudaMemcpyAsync(dev_nums + rb, gathered + (int64_t)r * chunk, (size_t)(re - rb) * 8,
-                               cudaMemcpyDeviceToDevice, st));
-    }
-    return DDKS_OK;
 }
 
 ddks_status ddks_stat_batch(ddks_ctx* ctx, const float* P, const float* Q, int64_t B, int64_t n_P, int64_t n_Q,

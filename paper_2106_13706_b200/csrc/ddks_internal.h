@@ -88,6 +88,13 @@ ddks_status launch_pack(ddks_ctx* ctx, const float* P, int64_t n_P, const float*
 ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n_P, int64_t n_Q, int64_t ob,
                             int64_t oe, DevResult* dres, bool export_per, bool split, unsigned long long* hist,
                             cudaStream_t st, uint64_t** per_out);
+// B items of N packed points: classify + count (+ finalise); force_split + hist: SPLIT counters and per-item M_T
+// histograms hist[B][n_Q + 1] (significance)
+ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int64_t n_P, int64_t n_Q,
+                      int64_t o_begin, int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st,
+                      bool force_split = false, unsigned long long* hist = nullptr);
+// items sharded contiguously over ranks: all-gather every rank's slice of dev_nums[total] (8-byte elements)
+ddks_status all_gather_items(ddks_ctx* ctx, uint64_t* dev_nums, int64_t total, cudaStream_t st);
 ddks_status radix_sort_keys(ddks_ctx* ctx, uint64_t* src, uint64_t* dst, int64_t N, int nseg, int shift_begin,
                             uint32_t* hist, cudaStream_t st, uint64_t** sorted);
 

@@ -163,8 +163,9 @@ struct CountArgs {
     int32_t* accum;          // accumulate mode: [B][NB][n_orig] int32 counters, else nullptr (direct mode)
     const int32_t* perm;     // x0-ordered mode: perm[j] = pooled index of sorted origin j; per_origin is then a
                              // full [N] array in pooled order (else nullptr: per_origin indexed o - o_begin)
-    unsigned long long* hist;  // SPLIT only, or nullptr: hist[c_Q] += 1 for every (origin, orthant) cell (the M_T
-                               // histogram of the analytic significance, ddks_significance.cuh)
+    unsigned long long* hist;  // SPLIT only, or nullptr: hist[item * hist_stride + c_Q] += 1 for every (origin,
+                               // orthant) cell (the M_T histogram of the analytic significance, ddks_significance.cuh)
+    int64_t hist_stride;       // n_Q + 1 (one histogram per batch item)
 };
 
 // decode the two signed 16-bit halves of a counter word (value = lo + 65536 * hi, both in int16 range)
@@ -183,7 +184,7 @@ __device__ __forceinline__ void hist_add_aggregated(unsigned long long* hist, in
 
 // num(o) of origin r of thread t from the SMEM counters (direct mode)
 template <int D, bool SPLIT>
-__device__ __forceinline__ uint64_t origin_num(const uint32_t* hist, int r, int t, const CountArgs& a) {
+__device__ __forceinline__ uint64_t origin_num(const uint32_t* hist, int r, int t, const CountArgs& a, int64_t item) {
     using G = Geo<D, SPLIT>;
     constexpr int NQ = G::NQ;
     const int sl = G::slot(r, t);
@@ -200,7 +201,7 @@ __device__ __forceinline__ uint64_t origin_num(const uint32_t* hist, int r, int 
             int32_t lo2, hi2;
             split16(hist[(NQ + q) * G::WPB + sl], lo2, hi2);
             const int64_t cQ = high ? hi2 : lo2;
-            if (a.hist) hist_add_aggregated(a.hist, cQ);
+            if (a.hist) hist_add_aggregated(a.hist, item * a.hist_stride + cQ);
             const int64_t df = (int64_t)v * a.nQ - cQ * a.nP;
             const uint64_t av = (uint64_t)(df < 0 ? -df : df);
             best = av > best ? av : best;
@@ -449,7 +450,7 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
     for (int r = 0; r < R; ++r) {
         const int32_t oi = blk_o0 + r * T + t;
         if (oi >= a.o_end) continue;
-        const uint64_t m = origin_num<D, SPLIT>(hist, r, t, a);
+        const uint64_t m = origin_num<D, SPLIT>(hist, r, t, a, item);
         if (a.per_origin) a.per_origin[a.perm ? a.perm[oi] : oi - a.o_begin] = m;
         best = m > best ? m : best;
     }
@@ -498,8 +499,9 @@ __global__ void k_finalize(const CountArgs a, int64_t B) {
     constexpr int NB = Geo<D, SPLIT>::NB;
     const int32_t n_orig = a.o_end - a.o_begin;
     __shared__ uint32_t sh_hist[SPLIT ? HS : 1];
+    const bool priv = SPLIT && a.hist && B == 1;  // a block-private histogram only when every cell is one item's
     if constexpr (SPLIT) {
-        if (a.hist) {
+        if (priv) {
             for (int i = threadIdx.x; i < HS; i += blockDim.x) sh_hist[i] = 0u;
             __syncthreads();
         }
@@ -524,8 +526,8 @@ __global__ void k_finalize(const CountArgs a, int64_t B) {
                 const int64_t cP = (int64_t)acc[(int64_t)q * n_orig];
                 const int64_t cQ = (int64_t)acc[(int64_t)(NQ + q) * n_orig];
                 if (a.hist) {
-                    if (cQ < HS) atomicAdd(&sh_hist[cQ], 1u);
-                    else hist_add_aggregated(a.hist, cQ);
+                    if (priv && cQ < HS) atomicAdd(&sh_hist[cQ], 1u);
+                    else hist_add_aggregated(a.hist, item * a.hist_stride + cQ);
                 }
                 const int64_t df = cP * a.nQ - cQ * a.nP;
                 const uint64_t av = (uint64_t)(df < 0 ? -df : df);
@@ -546,7 +548,7 @@ __global__ void k_finalize(const CountArgs a, int64_t B) {
             atomicMax(reinterpret_cast<unsigned long long*>(&a.item_num[0]), (unsigned long long)best);
     }
     if constexpr (SPLIT) {
-        if (a.hist) {
+        if (priv) {
             __syncthreads();
             for (int i = threadIdx.x; i < HS; i += blockDim.x)
                 if (sh_hist[i]) atomicAdd(&a.hist[i], (unsigned long long)sh_hist[i]);

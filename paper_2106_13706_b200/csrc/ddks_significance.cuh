@@ -33,15 +33,15 @@ __global__ void k_logfact(double* __restrict__ LF, int64_t n_max) {
 struct SigArgs {
     const double* LF;                    // [lf_max + 1] log n!
     int64_t lf_max;                      // >= max(N_P, N_T); Poisson: room for the pmf mass beyond N
-    const unsigned long long* hist;      // [N_T + 1] cells with M_T = m (all ranks' cells)
-    const unsigned long long* num;       // device: the global statistic numerator (after the all-reduce)
+    const unsigned long long* hist;      // [B][N_T + 1] cells with M_T = m (all ranks' cells), per item
+    const unsigned long long* num;       // device [B]: the items' statistic numerators (after any all-reduce)
     int64_t N_P, N_T;
-    int64_t m_begin, m_end;              // table entries this rank evaluates
+    int64_t m_begin, m_end;              // flat table entries e = item * (N_T + 1) + m this rank evaluates
     int poisson;
     double* scratch;                     // [gridDim.x][2][W_max]
     int64_t W_max;
-    double* table;                       // [N_T + 1] log p(d <= D | lambda_m); 0 where hist[m] == 0
-    double* contrib;                     // [N_T + 1] hist[m] * table[m]
+    double* table;                       // [B][N_T + 1] log p(d <= D | lambda_m); 0 where hist[m] == 0
+    double* contrib;                     // [B][N_T + 1] hist[m] * table[m]
     uint32_t* flag;                      // |= 4 if a window exceeded W_max (host retries with a larger W_max)
 };
 
@@ -180,12 +180,13 @@ __global__ void __launch_bounds__(SIG_T) k_sig_table(const SigArgs a) {
     __shared__ int64_t win[8];
     double* A = a.scratch + (int64_t)blockIdx.x * 2 * a.W_max;  // inclusive prefix sums of p(n_P)
     double* B = A + a.W_max;                                     // inclusive suffix sums of p(n_P)
-    const int64_t num = (int64_t)*a.num;
     const double invT = 1.0 / (double)a.N_T;
-    for (int64_t m = a.m_begin + blockIdx.x; m < a.m_end; m += gridDim.x) {
-        const unsigned long long h = a.hist[m];
+    for (int64_t e = a.m_begin + blockIdx.x; e < a.m_end; e += gridDim.x) {
+        const int64_t item = e / (a.N_T + 1), m = e - item * (a.N_T + 1);
+        const int64_t num = (int64_t)a.num[item];
+        const unsigned long long h = a.hist[e];
         if (h == 0) {
-            if (threadIdx.x == 0) a.table[m] = 0.0, a.contrib[m] = 0.0;
+            if (threadIdx.x == 0) a.table[e] = 0.0, a.contrib[e] = 0.0;
             continue;
         }
         const double lam = ((double)m + 1.0) / ((double)a.N_T + 2.0);
@@ -249,17 +250,19 @@ __global__ void __launch_bounds__(SIG_T) k_sig_table(const SigArgs a) {
         const double q = block_sum<SIG_T>(acc, red) + (tP + tT - tP * tT);
         if (threadIdx.x == 0) {
             const double lp = log1p(-q);
-            a.table[m] = lp;
-            a.contrib[m] = (double)h * lp;
+            a.table[e] = lp;
+            a.contrib[e] = (double)h * lp;
         }
         __syncthreads();  // scratch and win reused by the next entry
     }
 }
 
-// Fixed-order sum of contrib[b..e) -> *out (one CTA).
+// Fixed-order sum of contrib[b..e) -> *out (one CTA); batch: CTA i sums [b + i*stride, e + i*stride) -> out[i].
 __global__ void __launch_bounds__(SIG_T) k_sig_sum(const double* __restrict__ contrib, int64_t b, int64_t e,
-                                                   double* out) {
+                                                   double* out, int64_t stride = 0) {
     __shared__ double red[SIG_T];
+    contrib += blockIdx.x * stride;
+    out += blockIdx.x;
     const int64_t n = e - b;
     const int64_t C = (n + SIG_T - 1) / SIG_T;
     const int64_t lo = b + threadIdx.x * C, hi = lo + C < e ? lo + C : e;

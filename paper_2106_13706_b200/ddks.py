@@ -80,6 +80,7 @@ def _load() -> ctypes.CDLL:
         "ddks_stat_per_origin": ([vp, vp, i64, vp, i64, i32, i64, i64, vp, vp], ctypes.c_int),
         "ddks_significance": ([vp, vp, i64, vp, i64, i32, u32, vp, ctypes.POINTER(ddks_significance_result), vp, vp],
                               ctypes.c_int),
+        "ddks_significance_batch": ([vp, vp, vp, i64, i64, i64, i32, u32, vp, vp], ctypes.c_int),
         "ddks_vdks": ([vp, vp, i64, vp, i64, i32, i64, vp, ctypes.POINTER(ddks_result)], ctypes.c_int),
         "ddks_rdks": ([vp, vp, i64, vp, i64, i32, vp, ctypes.POINTER(ddks_result)], ctypes.c_int),
         "ddks_shard_range": ([i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)], ctypes.c_int),
@@ -99,7 +100,7 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 EXPORTED = ("ddks_get_nccl_id", "ddks_create", "ddks_stat", "ddks_stat_batch", "ddks_permutation_null",
-            "ddks_stat_per_origin", "ddks_stat_shard", "ddks_significance", "ddks_vdks", "ddks_rdks", "ddks_shard_range", "ddks_launch_count", "ddks_profile_read", "ddks_destroy",
+            "ddks_stat_per_origin", "ddks_stat_shard", "ddks_significance", "ddks_significance_batch", "ddks_vdks", "ddks_rdks", "ddks_shard_range", "ddks_launch_count", "ddks_profile_read", "ddks_destroy",
             "ddks_last_error", "ddks_version")
 
 
@@ -269,6 +270,19 @@ def ddks_significance(ctx, P, Q, poisson: bool = False, detail: bool = False, st
     return Significance(Result(st.num, st.den, st.D, st.argmax_origin), r.S, r.log_prod, r.cells, hist, table)
 
 
+def ddks_significance_batch(ctx, P, Q, poisson: bool = False, stream=None) -> list[Significance]:
+    """B independent pairs P [B, n_P, d], Q [B, n_Q, d] -> one Significance per pair (no histogram/table)."""
+    p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
+    if len(p.shape) != 3 or len(q.shape) != 3 or p.shape[0] != q.shape[0] or p.shape[2] != q.shape[2]:
+        raise ValueError(f"P {p.shape} and Q {q.shape} must be [B, n, d] with the same B and d")
+    B = p.shape[0]
+    out = (ddks_significance_result * B)()
+    _check(LIB.ddks_significance_batch(ctx, p.ptr, q.ptr, B, p.shape[1], q.shape[1], p.shape[2],
+                                       DDKS_SIG_POISSON if poisson else 0, _stream(stream), out), ctx)
+    return [Significance(Result(o.stat.num, o.stat.den, o.stat.D, o.stat.argmax_origin), o.S, o.log_prod, o.cells,
+                         None, None) for o in out]
+
+
 def ddks_vdks(ctx, P, Q, k: int, stream=None) -> Result:
     """vdKS (Alg. 1) with k voxels per dimension."""
     p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
@@ -325,6 +339,9 @@ class Context:
 
     def significance(self, P, Q, poisson=False, detail=False, stream=None) -> Significance:
         return ddks_significance(self.ctx, P, Q, poisson, detail, stream)
+
+    def significance_batch(self, P, Q, poisson=False, stream=None) -> list[Significance]:
+        return ddks_significance_batch(self.ctx, P, Q, poisson, stream)
 
     def vdks(self, P, Q, k: int, stream=None) -> Result:
         return ddks_vdks(self.ctx, P, Q, k, stream)

@@ -85,6 +85,7 @@ def test_null_context_is_an_argument_error_not_a_crash(lib):
     assert L.ddks_permutation_null(NULL, NULL, 1, 1, 2, NULL, 0, NULL, NULL, NULL, NULL) == 1
     assert L.ddks_stat_per_origin(NULL, NULL, 1, NULL, 1, 2, 0, 1, NULL, NULL) == 1
     assert L.ddks_significance(NULL, NULL, 1, NULL, 1, 2, 0, NULL, NULL, NULL, NULL) == 1
+    assert L.ddks_significance_batch(NULL, NULL, NULL, 1, 1, 1, 2, 0, NULL, NULL) == 1
     assert L.ddks_vdks(NULL, NULL, 1, NULL, 1, 2, 4, NULL, NULL) == 1
     assert L.ddks_rdks(NULL, NULL, 1, NULL, 1, 2, NULL, NULL) == 1
     assert L.ddks_profile_read(NULL, NULL, NULL, NULL) == 1

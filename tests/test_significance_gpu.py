@@ -176,3 +176,35 @@ def test_significance_ties_gt(n_P, n_Q, d):
             g = c.significance(dev(P), dev(Q), detail=True)
         assert g.stat.num == num_o and np.array_equal(g.mt_hist, h_o)
         assert abs(g.log_prod - lp_o) <= g.cells * tol_entry(n_P, n_Q) + 1e-12 * abs(lp_o)
+
+
+@pytest.mark.parametrize("B,n_P,n_Q,d,poisson", [(7, 40, 30, 2, False), (5, 50, 50, 3, True), (3, 33, 41, 5, False),
+                                                 (4, 30, 26, 8, False)])
+def test_significance_batch(ctx, B, n_P, n_Q, d, poisson):
+    # B independent pairs in one call: each item against the oracle, and bit-identical to the single-pair call
+    Pb, Qb = I.random_pair(2000 + B + d, B * n_P, B * n_Q, d, "mixed")
+    Pb, Qb = Pb.reshape(B, n_P, d), Qb.reshape(B, n_Q, d)
+    got = ctx.significance_batch(dev(Pb), dev(Qb), poisson=poisson)
+    te = tol_entry(n_P, n_Q)
+    for b in range(B):
+        S_o, lp_o, num_o = O.significance(Pb[b], Qb[b], poisson=poisson)
+        g = got[b]
+        assert g.stat.num == num_o and g.stat.den == n_P * n_Q and g.cells == (1 << d) * (n_P + n_Q)
+        assert abs(g.log_prod - lp_o) <= g.cells * te + 1e-12 * abs(lp_o), (b, g.log_prod, lp_o)
+        one = ctx.significance(dev(Pb[b]), dev(Qb[b]), poisson=poisson)
+        assert one.stat.num == g.stat.num and one.log_prod == g.log_prod and one.S == g.S
+
+
+def test_significance_batch_many_small(ctx):
+    # the paper's power-analysis shape: many 50 + 50 tests in 3-D; spot-check items against the oracle
+    rng = np.random.default_rng(77)
+    B = 512
+    Pb = rng.random((B, 50, 3)).astype(np.float32)
+    Qb = rng.random((B, 50, 3)).astype(np.float32)
+    Qb[B // 2:] = Qb[B // 2:] ** 1.5
+    got = ctx.significance_batch(dev(Pb), dev(Qb))
+    for b in (0, 1, 255, 256, 511):
+        S_o, lp_o, num_o = O.significance(Pb[b], Qb[b])
+        assert got[b].stat.num == num_o
+        assert abs(got[b].log_prod - lp_o) <= got[b].cells * tol_entry(50, 50) + 1e-12 * abs(lp_o)
+    assert all(0.0 <= g.S <= 1.0 for g in got)
