@@ -72,9 +72,12 @@ typedef enum {
 #define DDKS_FLAG_PERM_GATHER 16u /* TEST ONLY: permutation null by gathering each relabelled sample and re-running the
                                       full classification (the default label-invariant path classifies each pair once
                                       for a chunk of permutations; both give identical results)                    */
-#define DDKS_FLAG_NO_X0 32u        /* TEST ONLY: never use the x0-ordered count (ddks_stat sorts the pooled points by x_0 when
-                                      2 <= d <= 6 and N >= 200000, so whole tiles share bit 0; identical results)   */
-#define DDKS_FLAG_FORCE_X0 64u     /* TEST ONLY: use the x0-ordered count for any N (2 <= d <= 6, DIFF counters)      */
+#define DDKS_FLAG_NO_X0 32u        /* TEST ONLY: never use the kd-ordered count (ddks_stat / ddks_significance reorder the
+                                      pooled points hierarchically by x_0 .. x_{K-1} when 2 <= d <= 8 and N >= 200000,
+                                      so whole tiles share those bits; identical results)                          */
+#define DDKS_FLAG_FORCE_X0 64u     /* TEST ONLY: use the kd-ordered count for any N (2 <= d <= 8)                      */
+#define DDKS_FLAG_KD_SHIFT 9u      /* TEST ONLY: bits 9..10 = K in 1..3 force the number of kd levels (0: cost model) */
+#define DDKS_FLAG_KD_LEVELS(k) ((unsigned)(k) << DDKS_FLAG_KD_SHIFT)
 #define DDKS_FLAG_RDKS_FULL_SORT 128u /* TEST ONLY: ddks_rdks sorts every key (8-pass radix sort) instead of the bucket-pruned
                                          sweep that sorts only the buckets able to hold the maximum; identical results */
 #define DDKS_FLAG_PROFILE 8u      /* record CUDA events around every count-kernel launch (see ddks_profile_read) */
@@ -187,6 +190,10 @@ DDKS_API ddks_status ddks_shard_range(int64_t total, int world, int rank, int64_
 
 /* Number of kernels the library launched on this context since creation (for the bench's gpu_launches). */
 DDKS_API int64_t ddks_launch_count(const ddks_ctx* ctx);
+
+/* Levels K of the kd ordering used by the last count on this context (0: position order, no bit elision;
+ * K >= 1: bits 0..K-1 decided per tile where possible). Host-only, for tests and the bench line. */
+DDKS_API int32_t ddks_kd_levels(const ddks_ctx* ctx);
 
 /* Profiling (context created with DDKS_FLAG_PROFILE): totals since the last read, then reset.
  * count_ms: summed device time of the classify+count kernel launches (CUDA events on the call's stream);

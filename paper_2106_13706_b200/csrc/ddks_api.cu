@@ -19,6 +19,7 @@
 #include "ddks_kernels.cuh"
 #include "ddks_radix.cuh"
 #include "ddks_internal.h"
+#include "ddks_launch.cuh"
 
 #define DDKS_VERSION "0.1.0-sm100a"
 
@@ -97,105 +98,6 @@ ddks_status check_sizes(ddks_ctx* ctx, int64_t n_P, int64_t n_Q, int32_t d) {
 int pad_dim(int d) { return d <= 4 ? 4 : 8; }
 
 // ------------------------------------------------------------------------------------- count dispatch
-struct CountPlan {
-    int64_t B;
-    int32_t N, n_P, o_begin, o_end;
-    int64_t nP, nQ;
-    bool split;      // SPLIT counters (c_P, c_Q separately)
-    int64_t window;  // max points per segment so no 16-bit counter half leaves int16
-};
-
-template <int D, bool SPLIT, bool GT, bool X0 = false>
-ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a, cudaStream_t st) {
-    using G = ddks::Geo<D, SPLIT>;
-    auto kern = ddks::k_count<D, SPLIT, GT, X0>;
-    // function attributes are per device: remember which devices this instantiation was configured on
-    static bool attr_done[kMaxDevices] = {};
-    if (ctx->device >= kMaxDevices) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device index %d >= %d", ctx->device, kMaxDevices);
-    if (!attr_done[ctx->device]) {
-        CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES));
-        attr_done[ctx->device] = true;
-    }
-    const int n_orig = pl.o_end - pl.o_begin;
-    const int blocks_o = (n_orig + G::ORIGINS - 1) / G::ORIGINS;
-    const int n_tiles = (pl.N + G::TILE - 1) / G::TILE;
-    // segment length: at most the int16 flush window. Among the segment counts that respect it, pick the one with
-    // the least modelled time: waves x per-CTA cost, where a CTA costs its segment's points (x its origins) plus the
-    // flush of NB int32 partials per origin (global atomics; ~FLUSH_COST point-equivalents each) and the setup.
-    static int per_sm_dev[kMaxDevices] = {};
-    int& per_sm = per_sm_dev[ctx->device];
-    if (!per_sm) {
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::T, G::SMEM_BYTES));
-        per_sm = std::max(per_sm, 1);
-    }
-    int nsm = 148;
-    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
-    const int64_t slots = (int64_t)nsm * per_sm;
-    const int w_tiles = std::max(1, (int)(pl.window / G::TILE));
-    const int min_segs = (n_tiles + w_tiles - 1) / w_tiles;
-    const int64_t base_ctas = pl.B * blocks_o;
-    int segs = min_segs;
-    if (!(ctx->flags & DDKS_FLAG_FORCE_DIRECT)) {
-        constexpr double FLUSH_COST = 2.0, SETUP_COST = 2.0 * G::TILE;  // calibrated on C3 (segs 2..16 sweep)
-        double best = 1e300;
-        const int max_segs = (int)std::min<int64_t>(n_tiles, std::max<int64_t>(min_segs, (16 * slots + base_ctas - 1) / base_ctas));
-        for (int sg = min_segs; sg <= max_segs; ++sg) {
-            const int tps = (n_tiles + sg - 1) / sg;
-            const int real = (n_tiles + tps - 1) / tps;
-            if (real != sg) continue;
-            const int64_t ctas = base_ctas * sg;
-            const int64_t waves = (ctas + slots - 1) / slots;
-            const double cta = (double)tps * G::TILE + SETUP_COST + (sg > 1 ? FLUSH_COST * G::NB : 0.0);
-            const double cost = (double)waves * cta;
-            if (cost < best * (1.0 - 1e-9)) { best = cost; segs = sg; }
-        }
-        if (const char* e = getenv("DDKS_SEGS")) segs = std::max(min_segs, std::min(n_tiles, atoi(e)));  // tuning override
-    }
-    const int tiles_per_seg = (n_tiles + segs - 1) / segs;
-    segs = (n_tiles + tiles_per_seg - 1) / tiles_per_seg;
-    a.seg_points = tiles_per_seg * G::TILE;
-    if (segs > 65535) return fail(ctx, DDKS_ERR_TOO_LARGE, "too many point segments");
-    if (segs > 1) {
-        const size_t acc_bytes = (size_t)pl.B * G::NB * (size_t)n_orig * 4;
-        ddks_status s = ensure(ctx, ctx->accum, acc_bytes);
-        if (s) return s;
-        CU(cudaMemsetAsync(ctx->accum.p, 0, acc_bytes, st));
-        a.accum = (int32_t*)ctx->accum.p;
-    } else {
-        a.accum = nullptr;
-    }
-    if (pl.B > 65535 || blocks_o > 65535) return fail(ctx, DDKS_ERR_TOO_LARGE, "grid too large");
-    dim3 grid((unsigned)segs, (unsigned)blocks_o, (unsigned)pl.B);
-    std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
-    if (ctx->flags & DDKS_FLAG_PROFILE) {
-        if (!ctx->ev_free.empty()) {
-            ev = ctx->ev_free.back();
-            ctx->ev_free.pop_back();
-        } else {
-            CU(cudaEventCreate(&ev.first));
-            CU(cudaEventCreate(&ev.second));
-        }
-        CU(cudaEventRecord(ev.first, st));
-    }
-    kern<<<grid, G::T, G::SMEM_BYTES, st>>>(a);
-    CHECK_LAUNCH();
-    ctx->launches++;
-    if (ev.first) {
-        CU(cudaEventRecord(ev.second, st));
-        ctx->ev_pending.push_back(ev);
-        ctx->ev_pairs.push_back((uint64_t)pl.B * (uint64_t)n_orig * (uint64_t)pl.N);
-    }
-    if (segs > 1) {
-        const int64_t total = pl.B * n_orig;
-        const int threads = 256;
-        const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 16);
-        ddks::k_finalize<D, SPLIT><<<blocks, threads, 0, st>>>(a, pl.B);
-        CHECK_LAUNCH();
-        ctx->launches++;
-    }
-    return DDKS_OK;
-}
-
 template <int D>
 ddks_status launch_count_d(ddks_ctx* ctx, const CountPlan& pl, const ddks::CountArgs& a, cudaStream_t st) {
     const bool gt = (ctx->flags & DDKS_FLAG_TIES_GT) != 0;
@@ -272,65 +174,6 @@ ddks_status radix_sort_keys(ddks_ctx* ctx, uint64_t* src, uint64_t* dst, int64_t
     return DDKS_OK;
 }
 
-// x0-ordered statistic (B == 1, 2 <= d <= 8): reorder the packed rows label-major by x_0, count with bit-0 elision
-// (k_count<X0>), per-origin nums scattered back to pooled order into per_origin[N] (zeroed here). Origins
-// [o_begin, o_end) are positions in the x0 order. split + hist: SPLIT counters and the significance's M_T histogram.
-template <int D>
-ddks_status run_count_x0_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int64_t n_Q, int64_t o_begin,
-                           int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st, bool split,
-                           unsigned long long* hist_out) {
-    const int64_t N = n_P + n_Q;
-    const int DP = pad_dim(D);
-    const int tiles = (int)((N + ddks::RS_TILE - 1) / ddks::RS_TILE);
-    ddks_status s;
-    if ((s = ensure(ctx, ctx->x0_keys0, (size_t)N * 8))) return s;
-    if ((s = ensure(ctx, ctx->x0_keys1, (size_t)N * 8))) return s;
-    if ((s = ensure(ctx, ctx->x0_hist, (size_t)tiles * 256 * 4))) return s;
-    if ((s = ensure(ctx, ctx->x0_pts, (size_t)(N + 4) * DP * 4))) return s;
-    if ((s = ensure(ctx, ctx->x0_perm, (size_t)N * 4))) return s;
-    uint64_t* k0 = (uint64_t*)ctx->x0_keys0.p;
-    uint64_t* k1 = (uint64_t*)ctx->x0_keys1.p;
-    uint32_t* hist = (uint32_t*)ctx->x0_hist.p;
-    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 16));
-    ddks::k_x0_keys<<<g, 256, 0, st>>>(packed, DP, N, n_P, k0);
-    CHECK_LAUNCH();
-    ctx->launches++;
-    // stable LSD passes over key bits 31..63 (x_0 key, then the label): ties keep pooled-index order
-    uint64_t* src = nullptr;
-    if ((s = radix_sort_keys(ctx, k0, k1, N, 1, 31, hist, st, &src))) return s;
-    float* spts = (float*)ctx->x0_pts.p;
-    ddks::k_permute_rows<<<g, 256, 0, st>>>(packed, DP, N, src, spts, (int32_t*)ctx->x0_perm.p);
-    CHECK_LAUNCH();
-    ctx->launches++;
-    CU(cudaMemsetAsync(spts + N * DP, 0, 4 * DP * 4, st));  // the prefetch past the last row reads zeros
-    CU(cudaMemsetAsync(per_origin, 0, (size_t)N * 8, st));
-    const uint64_t gg = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
-    const uint32_t a_ = (uint32_t)((uint64_t)n_Q / gg), b_ = (uint32_t)((uint64_t)n_P / gg);
-    CountPlan pl{1, (int32_t)N, (int32_t)n_P, (int32_t)o_begin, (int32_t)o_end, n_P, n_Q, split,
-                 split ? 32767 : (int64_t)(32767 / std::max(a_, b_))};
-    ddks::CountArgs a{};
-    a.pts = spts;
-    a.item_stride = N * DP;
-    a.N = (int32_t)N;
-    a.n_P = (int32_t)n_P;
-    a.o_begin = (int32_t)o_begin;
-    a.o_end = (int32_t)o_end;
-    a.incP = split ? 1u : a_;
-    a.incQ = split ? 1u : 0u - b_;
-    a.g = split ? 1 : gg;
-    a.nP = n_P;
-    a.nQ = n_Q;
-    a.item_num = item_num;
-    a.per_origin = per_origin;
-    a.perm = (const int32_t*)ctx->x0_perm.p;
-    a.hist = split ? hist_out : nullptr;
-    a.hist_stride = n_Q + 1;
-    const bool gt = (ctx->flags & DDKS_FLAG_TIES_GT) != 0;
-    if (split)
-        return gt ? launch_count_t<D, true, true, true>(ctx, pl, a, st) : launch_count_t<D, true, false, true>(ctx, pl, a, st);
-    return gt ? launch_count_t<D, false, true, true>(ctx, pl, a, st) : launch_count_t<D, false, false, true>(ctx, pl, a, st);
-}
-
 // DIFF counters fit (|c_P a - c_Q b| stays in int32 and the int16 window is >= 4096 points); else SPLIT
 bool diff_counters_ok(int64_t n_P, int64_t n_Q) {
     const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
@@ -345,15 +188,15 @@ bool x0_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q) {
     return d >= 2 && d <= 8 && n_P + n_Q >= min_n;
 }
 
-ddks_status run_count_x0(ddks_ctx* ctx, const float* packed, int d, int64_t n_P, int64_t n_Q, int64_t o_begin,
+ddks_status run_count_kd(ddks_ctx* ctx, const float* packed, int d, int64_t n_P, int64_t n_Q, int64_t o_begin,
                          int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st, bool split,
                          unsigned long long* hist) {
     switch (d) {
-#define X0_CASE(D) case D: return run_count_x0_d<D>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st, split, hist);
-        X0_CASE(2) X0_CASE(3) X0_CASE(4) X0_CASE(5) X0_CASE(6) X0_CASE(7) X0_CASE(8)
-#undef X0_CASE
+#define KD_CASE(D) case D: return run_count_kd_d<D>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st, split, hist);
+        KD_CASE(2) KD_CASE(3) KD_CASE(4) KD_CASE(5) KD_CASE(6) KD_CASE(7) KD_CASE(8)
+#undef KD_CASE
     }
-    return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "x0 mode d=%d", d);
+    return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "kd mode d=%d", d);
 }
 
 // One statistic (B == 1) over the origin shard [ob, oe) of this rank: count (x0-ordered when it applies, else
@@ -364,14 +207,16 @@ ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n
                             cudaStream_t st, uint64_t** per_out) {
     const int64_t N = n_P + n_Q;
     ddks_status s;
-    const bool x0 = !export_per && x0_applicable(ctx, d, n_P, n_Q) && (split || diff_counters_ok(n_P, n_Q));
+    const bool x0 = !export_per && x0_applicable(ctx, d, n_P, n_Q);
     if (x0) {
         // origins are positions of the x_0 order; per-origin nums land in pooled order in per[N] (zeros elsewhere)
         if ((s = ensure(ctx, ctx->per_origin, (size_t)N * 8))) return s;
         uint64_t* per = (uint64_t*)ctx->per_origin.p;
         *per_out = per;
         if (oe > ob) {
-            if ((s = run_count_x0(ctx, packed, d, n_P, n_Q, ob, oe, (uint64_t*)&dres->num, per, st, split, hist))) return s;
+            // SPLIT counters when the significance needs c_Q or DIFF counters would overflow (as in run_count)
+            const bool sp = split || !diff_counters_ok(n_P, n_Q);
+            if ((s = run_count_kd(ctx, packed, d, n_P, n_Q, ob, oe, (uint64_t*)&dres->num, per, st, sp, hist))) return s;
         } else {
             CU(cudaMemsetAsync(per, 0, (size_t)N * 8, st));
         }
@@ -382,6 +227,7 @@ ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n
         ctx->launches++;
         return DDKS_OK;
     }
+    ctx->kd_levels = 0;
     if ((s = ensure(ctx, ctx->per_origin, (size_t)std::max<int64_t>(oe - ob, 1) * 8))) return s;
     uint64_t* per = (uint64_t*)ctx->per_origin.p;
     *per_out = per;
@@ -572,7 +418,7 @@ ddks_status ddks_create(ddks_ctx** out, int device, int world, int rank, const v
     if (world < 1 || rank < 0 || rank >= world) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad world/rank");
     if ((world == 1) != (nccl_id == nullptr))
         return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "nccl_id must be NULL iff world == 1");
-    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT | DDKS_FLAG_PROFILE | DDKS_FLAG_PERM_GATHER | DDKS_FLAG_NO_X0 | DDKS_FLAG_FORCE_X0 | DDKS_FLAG_RDKS_FULL_SORT)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
+    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT | DDKS_FLAG_PROFILE | DDKS_FLAG_PERM_GATHER | DDKS_FLAG_NO_X0 | DDKS_FLAG_FORCE_X0 | DDKS_FLAG_RDKS_FULL_SORT | DDKS_FLAG_KD_LEVELS(3))) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
     int ndev = 0;
     CU(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device %d of %d", device, ndev);
@@ -628,6 +474,8 @@ ddks_status ddks_destroy(ddks_ctx* ctx) {
 const char* ddks_last_error(const ddks_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
 
 int64_t ddks_launch_count(const ddks_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int32_t ddks_kd_levels(const ddks_ctx* ctx) { return ctx ? ctx->kd_levels : 0; }
 
 ddks_status ddks_profile_read(ddks_ctx* ctx, double* count_ms, int64_t* launches, uint64_t* pairs) {
     if (!ctx) return DDKS_ERR_INVALID_ARGUMENT;

@@ -1,0 +1,12 @@
+// ddks_api_kd_a.cu — kd-ordered count instantiations (see ddks_kd.cuh); one translation unit per group of d so
+// the builds run in parallel.
+#include "ddks_kd.cuh"
+
+namespace ddks_host {
+template ddks_status run_count_kd_d<2>(ddks_ctx*, const float*, int64_t, int64_t, int64_t, int64_t, uint64_t*, uint64_t*,
+                                         cudaStream_t, bool, unsigned long long*);
+template ddks_status run_count_kd_d<3>(ddks_ctx*, const float*, int64_t, int64_t, int64_t, int64_t, uint64_t*, uint64_t*,
+                                         cudaStream_t, bool, unsigned long long*);
+template ddks_status run_count_kd_d<4>(ddks_ctx*, const float*, int64_t, int64_t, int64_t, int64_t, uint64_t*, uint64_t*,
+                                         cudaStream_t, bool, unsigned long long*);
+}  // namespace ddks_host

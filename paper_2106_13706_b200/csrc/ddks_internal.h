@@ -34,11 +34,12 @@ struct ddks_ctx {
     DevBuf sig_hist, sig_lf, sig_scratch, sig_table, sig_contrib, sig_part;  // ddks_significance workspace
     DevBuf vox_keys, vox_cnt, vox_S;                                           // ddks_vdks workspace
     DevBuf rd_keys, rd_xn, rd_k0, rd_k1, rd_hist, rd_tcnt, rd_cnum;              // ddks_rdks workspace
-    DevBuf x0_keys0, x0_keys1, x0_hist, x0_pts, x0_perm;                        // x0-ordered count workspace
+    DevBuf x0_keys0, x0_keys1, x0_hist, x0_pts, x0_perm, x0_pts2, x0_perm2, x0_boxes;  // kd-ordered count workspace
     DevBuf rdb_cnt, rdb_pst, rdb_coff, rdb_fill, rdb_clist, rdb_csum;            // rdKS bucket-pruned sweep
     void* host_pinned = nullptr;  // DevResult + scratch
     size_t host_pinned_bytes = 0;
     int64_t launches = 0;
+    int kd_levels = 0;  // levels of the last kd-ordered count (0: position order)
     std::string err;
     // profiling (DDKS_FLAG_PROFILE)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending, ev_free;
@@ -95,6 +96,11 @@ ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int6
                       bool force_split = false, unsigned long long* hist = nullptr);
 // items sharded contiguously over ranks: all-gather every rank's slice of dev_nums[total] (8-byte elements)
 ddks_status all_gather_items(ddks_ctx* ctx, uint64_t* dev_nums, int64_t total, cudaStream_t st);
+// kd-ordered count of one statistic (B == 1, 2 <= D <= 8; ddks_kd.cuh, instantiated in ddks_api_kd_*.cu)
+template <int D>
+ddks_status run_count_kd_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int64_t n_Q, int64_t o_begin,
+                           int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st, bool split,
+                           unsigned long long* hist);
 ddks_status radix_sort_keys(ddks_ctx* ctx, uint64_t* src, uint64_t* dst, int64_t N, int nseg, int shift_begin,
                             uint32_t* hist, cudaStream_t st, uint64_t** sorted);
 

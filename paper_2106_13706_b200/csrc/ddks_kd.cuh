@@ -1,0 +1,165 @@
+// ddks_kd.cuh — host side of the kd-ordered count (bit elision, DESIGN.md §7 "kd ordering"): reorder the packed
+// rows label-major and hierarchically by x_0 .. x_{K-1} (K stable radix sorts), build the per-tile boxes, count with
+// k_count<D, SPLIT, GT, K>. Instantiated per d in ddks_api_kd_*.cu (parallel compilation).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "ddks_kernels.cuh"
+#include "ddks_internal.h"
+#include "ddks_launch.cuh"
+
+namespace ddks_host {
+
+struct KdChoice {
+    int K;
+    int64_t G0, G1;
+};
+
+inline int64_t lcm_i64(int64_t a, int64_t b) { return a / (int64_t)gcd_u64((uint64_t)a, (uint64_t)b) * b; }
+inline int bits_for(uint64_t v) { int b = 0; while (v) { ++b; v >>= 1; } return b; }  // bits to hold 0..v
+
+// Levels and cuts from a cost model of the compares per pair: D - K compared dims always, plus the expected
+// undecided bits: a tile in the same slab (or, across labels, the neighbouring one) leaves bit 0 open
+// (~1.5 / G0), likewise bit 1 (~1.5 / G1), and the last sorted dim interleaves for (origins per CTA + TILE) /
+// cell rows of the tiles. Cells must keep at least 2 A rows. forced_k (1..3) fixes K (tests); kmax caps it.
+inline KdChoice kd_choose(int D, int64_t n_lab, int64_t RT, int64_t TILE, int64_t A, int forced_k, int kmax) {
+    KdChoice best{1, 1, 1};
+    double best_cost = 1e300;
+    const double c = (double)(RT + TILE) / (double)std::max<int64_t>(n_lab, 1);
+    for (int K = 1; K <= std::min(3, std::min(D, kmax)); ++K) {
+        if (forced_k && K != forced_k) continue;
+        for (int64_t g0 = 1; g0 <= (K >= 2 ? 256 : 1); ++g0) {
+            for (int64_t g1 = 1; g1 <= (K >= 3 ? 64 : 1); ++g1) {
+                if (g0 * g1 > 1 && n_lab / (g0 * g1) < 2 * A) continue;
+                double cost = (double)(D - K) + c * (double)(g0 * g1);
+                if (K >= 2) cost += 1.5 / (double)g0;
+                if (K >= 3) cost += 1.5 / (double)g1;
+                if (cost < best_cost - 1e-12) { best_cost = cost; best = {K, g0, g1}; }
+            }
+        }
+    }
+    if (const char* e = getenv("DDKS_KD")) {  // tuning override: "K[,G0[,G1]]"
+        int k = 1;
+        long long g0 = best.G0, g1 = best.G1;
+        const int n = sscanf(e, "%d,%lld,%lld", &k, &g0, &g1);
+        if (n >= 1 && k >= 1 && k <= std::min(3, std::min(D, kmax))) {
+            best.K = k;
+            best.G0 = n >= 2 ? std::max<long long>(1, g0) : (k >= 2 ? best.G0 : 1);
+            best.G1 = n >= 3 ? std::max<long long>(1, g1) : (k >= 3 ? best.G1 : 1);
+        }
+    }
+    if (best.K < 2) best.G0 = 1;
+    if (best.K < 3) best.G1 = 1;
+    return best;
+}
+
+template <int D, bool SPLIT, bool GT, int K>
+ddks_status launch_kd(ddks_ctx* ctx, const CountPlan& pl, const ddks::CountArgs& a, cudaStream_t st) {
+    return launch_count_t<D, SPLIT, GT, K>(ctx, pl, a, st);
+}
+
+template <int D, bool SPLIT>
+ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int64_t n_Q, int64_t o_begin,
+                           int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st,
+                           unsigned long long* hist_out) {
+    using G = ddks::Geo<D, SPLIT>;
+    const int64_t N = n_P + n_Q;
+    const int DP = pad_dim(D);
+    const bool gt = (ctx->flags & DDKS_FLAG_TIES_GT) != 0;
+    const int64_t A = lcm_i64(G::ORIGINS, G::TILE);
+    const int forced = (int)((ctx->flags >> DDKS_FLAG_KD_SHIFT) & 3u);
+    // the tie-convention test variant (GT) is instantiated with one level only
+    const KdChoice kc = kd_choose(D, std::min(n_P, n_Q), G::ORIGINS, G::TILE, A, gt ? 1 : forced, gt ? 1 : 3);
+    const int K = kc.K;
+    const int ib = std::max(1, bits_for((uint64_t)(N - 1)));
+    const int tiles_rs = (int)((N + ddks::RS_TILE - 1) / ddks::RS_TILE);
+    const int64_t n_tiles = (N + G::TILE - 1) / G::TILE;
+    ddks_status s;
+    if ((s = ensure(ctx, ctx->x0_keys0, (size_t)N * 8))) return s;
+    if ((s = ensure(ctx, ctx->x0_keys1, (size_t)N * 8))) return s;
+    if ((s = ensure(ctx, ctx->x0_hist, (size_t)tiles_rs * 256 * 4))) return s;
+    if ((s = ensure(ctx, ctx->x0_pts, (size_t)(N + 4) * DP * 4))) return s;
+    if ((s = ensure(ctx, ctx->x0_perm, (size_t)N * 4))) return s;
+    if ((s = ensure(ctx, ctx->x0_boxes, (size_t)n_tiles * K * 2 * 4))) return s;
+    if (K > 1) {
+        if ((s = ensure(ctx, ctx->x0_pts2, (size_t)N * DP * 4))) return s;
+        if ((s = ensure(ctx, ctx->x0_perm2, (size_t)N * 4))) return s;
+    }
+    uint64_t* k0 = (uint64_t*)ctx->x0_keys0.p;
+    uint64_t* k1 = (uint64_t*)ctx->x0_keys1.p;
+    uint32_t* hist = (uint32_t*)ctx->x0_hist.p;
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 16));
+    const float* src_pts = packed;
+    const int32_t* src_perm = nullptr;
+    for (int level = 0; level < K; ++level) {
+        const int64_t cells = level == 0 ? 1 : (level == 1 ? kc.G0 : kc.G0 * kc.G1);
+        const int cb = cells > 1 ? bits_for((uint64_t)(cells - 1)) : 0;
+        ddks::k_kd_keys<<<g, 256, 0, st>>>(src_pts, DP, N, n_P, level, kc.G0, kc.G1, A, ib, cb, k0);
+        CHECK_LAUNCH();
+        ctx->launches++;
+        uint64_t* sorted = nullptr;
+        if ((s = radix_sort_keys(ctx, k0, k1, N, 1, ib, hist, st, &sorted))) return s;
+        // the last level lands in x0_pts / x0_perm; earlier ones alternate with x0_pts2 / x0_perm2
+        const bool fin = ((K - 1 - level) % 2) == 0;
+        float* dst_pts = (float*)(fin ? ctx->x0_pts.p : ctx->x0_pts2.p);
+        int32_t* dst_perm = (int32_t*)(fin ? ctx->x0_perm.p : ctx->x0_perm2.p);
+        ddks::k_permute_rows<<<g, 256, 0, st>>>(src_pts, DP, N, sorted, ib, src_perm, dst_pts, dst_perm);
+        CHECK_LAUNCH();
+        ctx->launches++;
+        src_pts = dst_pts;
+        src_perm = dst_perm;
+    }
+    float* spts = (float*)ctx->x0_pts.p;
+    CU(cudaMemsetAsync(spts + N * DP, 0, 4 * DP * 4, st));  // the prefetch past the last row reads zeros
+    ddks::k_tile_boxes<<<(int)std::max<int64_t>(1, std::min<int64_t>((n_tiles + 7) / 8, 148 * 16)), 256, 0, st>>>(
+        spts, DP, N, G::TILE, K, (float*)ctx->x0_boxes.p);
+    CHECK_LAUNCH();
+    ctx->launches++;
+    CU(cudaMemsetAsync(per_origin, 0, (size_t)N * 8, st));
+    const uint64_t gg = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
+    const uint32_t a_ = (uint32_t)((uint64_t)n_Q / gg), b_ = (uint32_t)((uint64_t)n_P / gg);
+    CountPlan pl{1, (int32_t)N, (int32_t)n_P, (int32_t)o_begin, (int32_t)o_end, n_P, n_Q, SPLIT,
+                 SPLIT ? 32767 : (int64_t)(32767 / std::max(a_, b_))};
+    ddks::CountArgs a{};
+    a.pts = spts;
+    a.item_stride = N * DP;
+    a.N = (int32_t)N;
+    a.n_P = (int32_t)n_P;
+    a.o_begin = (int32_t)o_begin;
+    a.o_end = (int32_t)o_end;
+    a.incP = SPLIT ? 1u : a_;
+    a.incQ = SPLIT ? 1u : 0u - b_;
+    a.g = SPLIT ? 1 : gg;
+    a.nP = n_P;
+    a.nQ = n_Q;
+    a.item_num = item_num;
+    a.per_origin = per_origin;
+    a.perm = (const int32_t*)ctx->x0_perm.p;
+    a.boxes = (const float*)ctx->x0_boxes.p;
+    a.hist = SPLIT ? hist_out : nullptr;
+    a.hist_stride = n_Q + 1;
+    ctx->kd_levels = K;
+    if (gt) return launch_kd<D, SPLIT, true, 1>(ctx, pl, a, st);
+    if (K == 1) return launch_kd<D, SPLIT, false, 1>(ctx, pl, a, st);
+    if constexpr (D >= 2) {
+        if (K == 2) return launch_kd<D, SPLIT, false, 2>(ctx, pl, a, st);
+    }
+    if constexpr (D >= 3) {
+        if (K == 3) return launch_kd<D, SPLIT, false, 3>(ctx, pl, a, st);
+    }
+    return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "kd levels %d for d=%d", K, D);
+}
+
+template <int D>
+ddks_status run_count_kd_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int64_t n_Q, int64_t o_begin,
+                           int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st, bool split,
+                           unsigned long long* hist) {
+    return split ? run_count_kd_t<D, true>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st, hist)
+                 : run_count_kd_t<D, false>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st, hist);
+}
+
+}  // namespace ddks_host

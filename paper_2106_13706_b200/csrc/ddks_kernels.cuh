@@ -16,8 +16,8 @@
 //   * DIFF mode keeps one signed counter per orthant: c_P*a - c_Q*b with a = n_Q/g, b = n_P/g
 //     (g = gcd(n_P, n_Q)), so |counter| * g is exactly |c_P n_Q - c_Q n_P| (P:L238 cross-multiplied);
 //     SPLIT mode (when DIFF would overflow, and for the significance, which needs c_Q) keeps c_P and c_Q apart;
-//   * X0 (large N): rows pre-sorted label-major by x_0, so bit 0 is decided once per tile for most tiles and only
-//     dims 1..d-1 are compared (DESIGN.md §7 "x0 ordering");
+//   * kd ordering (large N): rows pre-sorted label-major and hierarchically by x_0 .. x_{KX-1}, so for most tiles the
+//     bits of those dims are decided once per tile and only the other dims are compared (DESIGN.md §7 "kd ordering");
 //   * finalisation is exact integer arithmetic; the max is a warp-shuffle + CTA + atomicMax(u64) reduction;
 //   * the label-invariant permutation null (k_labels / k_perm_count) classifies each pair once per chunk of
 //     permutations.
@@ -29,6 +29,7 @@
 #include "ddks_common.cuh"
 
 namespace ddks {
+namespace {  // internal linkage: several translation units include these kernels
 
 // ----------------------------------------------------------------------------------------------- config
 // Counters are 16-bit halves of 32-bit SMEM words. A CTA owns R*T origins; origin j = r*T + t (slot r of thread t)
@@ -161,7 +162,8 @@ struct CountArgs {
     uint64_t* item_num;      // [B] atomicMax target (direct mode)
     uint64_t* per_origin;    // [o_end - o_begin] or nullptr (direct mode, B == 1)
     int32_t* accum;          // accumulate mode: [B][NB][n_orig] int32 counters, else nullptr (direct mode)
-    const int32_t* perm;     // x0-ordered mode: perm[j] = pooled index of sorted origin j; per_origin is then a
+    const float* boxes;      // kd-ordered mode: [n_tiles][KX][2] min / max of dims < KX per TILE rows, else nullptr
+    const int32_t* perm;     // kd-ordered mode: perm[j] = pooled index of sorted origin j; per_origin is then a
                              // full [N] array in pooled order (else nullptr: per_origin indexed o - o_begin)
     unsigned long long* hist;  // SPLIT only, or nullptr: hist[item * hist_stride + c_Q] += 1 for every (origin,
                                // orthant) cell (the M_T histogram of the analytic significance, ddks_significance.cuh)
@@ -212,23 +214,37 @@ __device__ __forceinline__ uint64_t origin_num(const uint32_t* hist, int r, int 
 
 // Float-encoded counter address of the pair (origin o, point x): base + sum_k [x_k >= o_k] * 4 * 2^k * WPB, as d
 // FSET.BF (ALU pipe) + d FFMA-immediate (FMA pipe); exact, every partial sum is an integer < 2^24.
-// Dims [FIRST, D) only: FIRST == 1 when bit 0 was decided for the whole tile (x0 ordering) and folded into base.
-template <int D, bool GT, int WPB, int FIRST = 0, bool SPLIT_CHAIN = (D >= 6)>
+// kd ordering (KX > 0): dims k < KX whose bit was decided for the whole tile (bit k of UM clear) are not compared;
+// their weight is folded into base by the caller. Dims k >= KX are always compared.
+template <int KX, int UM> __host__ __device__ constexpr bool cmp_dim(int k) { return k >= KX || ((UM >> k) & 1); }
+template <int D, int KX, int UM> __host__ __device__ constexpr int n_cmp() {
+    int c = 0;
+    for (int k = 0; k < D; ++k) c += cmp_dim<KX, UM>(k) ? 1 : 0;
+    return c;
+}
+
+template <int D, bool GT, int WPB, int KX = 0, int UM = 0, bool SPLIT_CHAIN = (D >= 6)>
 __device__ __forceinline__ float code_addr(const float (&x)[D], const float (&o)[D], float base) {
-    if constexpr (SPLIT_CHAIN) {
+    constexpr int NC = n_cmp<D, KX, UM>();
+    if constexpr (SPLIT_CHAIN && NC >= 4) {
         // two half-length FFMA chains shorten the dependency chain when few warps are resident (d >= 6 keeps 256+
         // counters per origin in SMEM)
-        constexpr int H = (D + FIRST) / 2;
         float f0 = base, f1 = 0.0f;
+        int c = 0;
 #pragma unroll
-        for (int k = FIRST; k < H; ++k) f0 = fmaf(cmp_bit<GT>(x[k], o[k]), (float)(4 * (1 << k) * WPB), f0);
-#pragma unroll
-        for (int k = H; k < D; ++k) f1 = fmaf(cmp_bit<GT>(x[k], o[k]), (float)(4 * (1 << k) * WPB), f1);
+        for (int k = 0; k < D; ++k) {
+            if (!cmp_dim<KX, UM>(k)) continue;
+            const float w = (float)(4 * (1 << k) * WPB);
+            if (c < NC / 2) f0 = fmaf(cmp_bit<GT>(x[k], o[k]), w, f0);
+            else            f1 = fmaf(cmp_bit<GT>(x[k], o[k]), w, f1);
+            ++c;
+        }
         return f0 + f1;
     } else {
         float f = base;
 #pragma unroll
-        for (int k = FIRST; k < D; ++k) f = fmaf(cmp_bit<GT>(x[k], o[k]), (float)(4 * (1 << k) * WPB), f);
+        for (int k = 0; k < D; ++k)
+            if (cmp_dim<KX, UM>(k)) f = fmaf(cmp_bit<GT>(x[k], o[k]), (float)(4 * (1 << k) * WPB), f);
         return f;
     }
 }
@@ -245,7 +261,7 @@ __device__ __forceinline__ void red_counter(float f, uint32_t ubase, uint32_t in
     red_add_shared(__float_as_uint(f) + ubase, inc);
 }
 
-template <int D, bool GT, int R, int RP, int NB_, int WPB, int DP, int FIRST = 0>
+template <int D, bool GT, int R, int RP, int NB_, int WPB, int DP, int KX = 0, int UM = 0>
 __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, const float (&o)[R][D],
                                              const float (&base)[NB_], uint32_t ubase, uint32_t inc_lo,
                                              uint32_t inc_hi, uint32_t hbytes) {
@@ -268,8 +284,8 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 // two points in flight already give 2R independent chains: no chain split
-                fa[r] = code_addr<D, GT, WPB, FIRST, false>(xa, o[r], base[r % NB_]);
-                fb[r] = code_addr<D, GT, WPB, FIRST, false>(xb, o[r], base[r % NB_]);
+                fa[r] = code_addr<D, GT, WPB, KX, UM, false>(xa, o[r], base[r % NB_]);
+                fb[r] = code_addr<D, GT, WPB, KX, UM, false>(xb, o[r], base[r % NB_]);
             }
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -281,7 +297,7 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
         if (p < hi) {
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                red_counter(code_addr<D, GT, WPB, FIRST>(na, o[r], base[r % NB_]), ubase,
+                red_counter(code_addr<D, GT, WPB, KX, UM>(na, o[r], base[r % NB_]), ubase,
                             (R >= 2 && r < RP) ? inc_lo : inc_hi, hbytes);
         }
         return;
@@ -296,15 +312,29 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
         load_point<D>(tile + (p + 1) * DP, xn);
 #pragma unroll
         for (int r = 0; r < R; ++r)
-            red_counter(code_addr<D, GT, WPB, FIRST>(x, o[r], base[r % NB_]), ubase,
+            red_counter(code_addr<D, GT, WPB, KX, UM>(x, o[r], base[r % NB_]), ubase,
                         (R >= 2 && r < RP) ? inc_lo : inc_hi, hbytes);
     }
 }
 
-// X0: the rows are in x0 order (label-major: P rows sorted by x_0, then Q rows sorted by x_0; a.perm maps a row back
-// to its pooled index), and bit 0 is decided per tile when the tile's x_0 range does not interleave with the CTA's
-// origins' (DESIGN.md §7 "x0 ordering").
-template <int D, bool SPLIT, bool GT, bool X0 = false>
+// count_points for the undecided-dims mask um (one instantiation per mask; um is uniform over the CTA)
+template <int D, bool GT, int R, int RP, int NB_, int WPB, int DP, int KX, int UM = (1 << KX) - 1>
+__device__ __forceinline__ void count_points_um(int um, const float* tile, int lo, int hi, const float (&o)[R][D],
+                                                const float (&base)[NB_], uint32_t ubase, uint32_t inc_lo,
+                                                uint32_t inc_hi, uint32_t hbytes) {
+    if constexpr (UM == 0) {
+        count_points<D, GT, R, RP, NB_, WPB, DP, KX, 0>(tile, lo, hi, o, base, ubase, inc_lo, inc_hi, hbytes);
+    } else {
+        if (um == UM) count_points<D, GT, R, RP, NB_, WPB, DP, KX, UM>(tile, lo, hi, o, base, ubase, inc_lo, inc_hi, hbytes);
+        else count_points_um<D, GT, R, RP, NB_, WPB, DP, KX, UM - 1>(um, tile, lo, hi, o, base, ubase, inc_lo, inc_hi, hbytes);
+    }
+}
+
+// KX > 0 (kd ordering): the rows are in kd order (label-major, hierarchically sorted by x_0 .. x_{KX-1}, see k_kd_keys;
+// a.perm maps a row back to its pooled index) and a.boxes holds every tile's [min, max] of dims < KX. Bit k < KX is
+// decided for a whole tile when the tile's x_k range does not interleave with the CTA's origins' (DESIGN.md §7
+// "kd ordering"); only the undecided dims are compared.
+template <int D, bool SPLIT, bool GT, int KX = 0>
 __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a) {
     using G = Geo<D, SPLIT>;
     constexpr int R = G::R, RP = G::RP, T = G::T, DP = G::DP, TILE = G::TILE, S = G::S, NBASE = G::NBASE,
@@ -365,22 +395,36 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
     // R == 1: this thread's single origin is a low or a high half for its whole life
     const uint32_t incP_lo = (R == 1 && G::high(0, t)) ? incP_hi : a.incP;
     const uint32_t incQ_lo = (R == 1 && G::high(0, t)) ? incQ_hi : a.incQ;
-    // X0: the x_0 range of this CTA's origins (each label run is ascending) and the bases with bit 0's weight added
-    float o_lo = 0.0f, o_hi = 0.0f;
-    float baseP1[NBASE], baseQ1[NBASE];
-    if constexpr (X0) {
-        const int32_t b0 = blk_o0, b1 = min(a.o_end, blk_o0 + G::ORIGINS) - 1;
-        o_lo = __ldg(pts + (int64_t)b0 * DP);
-        o_hi = __ldg(pts + (int64_t)b1 * DP);
-        if (b0 < a.n_P && b1 >= a.n_P) {  // the block spans the P / Q boundary: two ascending runs
-            o_lo = fminf(o_lo, __ldg(pts + (int64_t)a.n_P * DP));
-            o_hi = fmaxf(o_hi, __ldg(pts + (int64_t)(a.n_P - 1) * DP));
-        }
+    // KX > 0: the box [cmin, cmax] of dims < KX over this CTA's origins (clamped slots repeat o_end - 1, which is in
+    // the last block), block-reduced once
+    constexpr int KB = KX > 0 ? KX : 1;
+    float cmin[KB], cmax[KB];
+    if constexpr (KX > 0) {
+        __shared__ float sbox[32][2 * KB];
 #pragma unroll
-        for (int b = 0; b < NBASE; ++b) {
-            baseP1[b] = baseP[b] + (float)(4 * WPB);  // exact: integers < 2^24
-            baseQ1[b] = baseQ[b] + (float)(4 * WPB);
+        for (int k = 0; k < KX; ++k) {
+            float lo = o[0][k], hi = o[0][k];
+#pragma unroll
+            for (int r = 1; r < R; ++r) lo = fminf(lo, o[r][k]), hi = fmaxf(hi, o[r][k]);
+#pragma unroll
+            for (int sh = 16; sh; sh >>= 1) {
+                lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, sh));
+                hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, sh));
+            }
+            if ((t & 31) == 0) sbox[t >> 5][2 * k] = lo, sbox[t >> 5][2 * k + 1] = hi;
         }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < KX; ++k) {
+            cmin[k] = sbox[0][2 * k], cmax[k] = sbox[0][2 * k + 1];
+            for (int w = 1; w < T / 32; ++w) cmin[k] = fminf(cmin[k], sbox[w][2 * k]), cmax[k] = fmaxf(cmax[k], sbox[w][2 * k + 1]);
+        }
+    }
+    // the tile box of the next tile is loaded one iteration ahead (tiles are TILE-aligned from row 0)
+    float bnext[2 * KB];
+    if constexpr (KX > 0) {
+#pragma unroll
+        for (int k = 0; k < 2 * KX; ++k) bnext[k] = __ldg(a.boxes + (int64_t)(seg0 / TILE) * 2 * KX + k);
     }
 
     for (int it = 0; it < n_tiles; ++it) {
@@ -392,26 +436,38 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
         // sample-homogeneous sub-ranges: [p0, n_P) are P points, [n_P, ...) are Q points
         int32_t split = a.n_P - p0;
         split = split < 0 ? 0 : (split > cnt ? cnt : split);
-        int mode = 2;  // 0: bit 0 = 0 for the whole tile, 1: bit 0 = 1, 2: compare all d dims
-        if constexpr (X0) {
-            // the tile's x_0 range (two ascending runs if it holds the P / Q boundary)
-            float t_lo = tile[0], t_hi = tile[(cnt - 1) * DP];
-            if (split > 0 && split < cnt) {
-                t_lo = fminf(t_lo, tile[split * DP]);
-                t_hi = fmaxf(t_hi, tile[(split - 1) * DP]);
+        // undecided dims among the first KX (bit k of um) and the weight of the bits decided as 1
+        int um = (1 << KX) - 1;
+        float add = 0.0f;
+        if constexpr (KX > 0) {
+            float bx[2 * KX];
+#pragma unroll
+            for (int k = 0; k < 2 * KX; ++k) bx[k] = bnext[k];
+            if (it + 1 < n_tiles) {
+#pragma unroll
+                for (int k = 0; k < 2 * KX; ++k) bnext[k] = __ldg(a.boxes + (int64_t)(p0 / TILE + 1) * 2 * KX + k);
             }
-            // bit 0 = [x_0 >= o_0] (GT: >) is uniform over tile x origins when the ranges do not interleave
-            if (GT ? (t_hi <= o_lo) : (t_hi < o_lo)) mode = 0;
-            else if (GT ? (t_lo > o_hi) : (t_lo >= o_hi)) mode = 1;
+#pragma unroll
+            for (int k = 0; k < KX; ++k) {
+                // bit k = [x_k >= o_k] (GT: >) is uniform over tile x origins when the ranges do not interleave
+                if (GT ? (bx[2 * k + 1] <= cmin[k]) : (bx[2 * k + 1] < cmin[k])) {
+                    um &= ~(1 << k);
+                } else if (GT ? (bx[2 * k] > cmax[k]) : (bx[2 * k] >= cmax[k])) {
+                    um &= ~(1 << k);
+                    add += (float)(4 * (1 << k) * WPB);  // exact: integers < 2^24
+                }
+            }
         }
-        if (mode == 2) {
-            count_points<D, GT, R, RP, NBASE, WPB, DP>(tile, 0, split, o, baseP, ubase, incP_lo, R == 1 ? incP_lo : incP_hi, G::HIST_WORDS * 4u);
-            count_points<D, GT, R, RP, NBASE, WPB, DP>(tile, split, cnt, o, baseQ, ubase, incQ_lo, R == 1 ? incQ_lo : incQ_hi, G::HIST_WORDS * 4u);
-        } else if constexpr (X0) {
-            count_points<D, GT, R, RP, NBASE, WPB, DP, 1>(tile, 0, split, o, mode ? baseP1 : baseP, ubase, incP_lo,
-                                                          R == 1 ? incP_lo : incP_hi, G::HIST_WORDS * 4u);
-            count_points<D, GT, R, RP, NBASE, WPB, DP, 1>(tile, split, cnt, o, mode ? baseQ1 : baseQ, ubase, incQ_lo,
-                                                          R == 1 ? incQ_lo : incQ_hi, G::HIST_WORDS * 4u);
+#pragma unroll 1
+        for (int part = 0; part < 2; ++part) {
+            const int lo = part ? split : 0, hi = part ? cnt : split;
+            if (lo >= hi) continue;
+            float bb[NBASE];
+#pragma unroll
+            for (int b = 0; b < NBASE; ++b) bb[b] = (part ? baseQ[b] : baseP[b]) + add;
+            const uint32_t il = part ? incQ_lo : incP_lo;
+            const uint32_t ih = R == 1 ? il : (part ? incQ_hi : incP_hi);
+            count_points_um<D, GT, R, RP, NBASE, WPB, DP, KX>(um, tile, lo, hi, o, bb, ubase, il, ih, G::HIST_WORDS * 4u);
         }
         __syncthreads();  // every thread is done with stage s
         if (t == 0 && it + S < n_tiles) {
@@ -465,27 +521,94 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
     }
 }
 
-// ----------------------------------------------------------------------------------------------- x0 ordering
-// Bit-0 elision (DESIGN.md §7 "x0 ordering"): the pooled rows are reordered label-major by x_0 (P rows sorted by x_0,
-// then Q rows sorted by x_0; a 5-pass stable radix sort of (label, key(x_0), index)), so tiles stay
-// sample-homogeneous and a CTA's origins are R*T consecutive rows whose x_0 values span [o_lo, o_hi]. k_count<X0>
-// then decides bit 0 once per tile when the tile's x_0 range does not interleave with that span.
-__global__ void k_x0_keys(const float* __restrict__ pts, int DP, int64_t N, int64_t n_P, uint64_t* __restrict__ keys) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
-        keys[i] = ((uint64_t)(i >= n_P) << 63) | ((uint64_t)f32_key(pts[i * DP]) << 31) | (uint64_t)i;
+// ----------------------------------------------------------------------------------------------- kd ordering
+// Bit elision (DESIGN.md §7 "kd ordering"). The pooled rows are reordered label-major (P rows, then Q rows, so tiles
+// stay sample-homogeneous) and, within each label run, hierarchically: level 0 sorts the run by x_0 and cuts it into
+// G0 slabs, level 1 sorts every slab by x_1 and cuts it into G1 cells, level 2 sorts every cell by x_2 (KX levels in
+// all). Cut points are rounded to multiples of A = lcm(origins per CTA, TILE), so a CTA's origins and a tile lie in one
+// cell. A CTA's origins then span a narrow range of the last sorted dim and one slab / cell range of the others,
+// and k_count<KX> decides bit k for a whole tile whenever the tile's x_k range does not interleave with it.
+// The order only affects speed: every decision is taken from the actual per-tile and per-CTA min / max.
+
+// cut point i of the run [s, e) into G parts, rounded to a multiple of A (monotone in i; cut 0 = s, cut G = e)
+__device__ __forceinline__ int64_t kd_cut(int64_t s, int64_t e, int64_t G, int64_t i, int64_t A) {
+    if (i <= 0) return s;
+    if (i >= G) return e;
+    const int64_t x = s + (e - s) * i / G;
+    const int64_t r = (x + A / 2) / A * A;
+    return r < s ? s : (r > e ? e : r);
+}
+// the part of [s, e) holding row j: the largest i < G with kd_cut(i) <= j
+__device__ __forceinline__ int64_t kd_part(int64_t j, int64_t s, int64_t e, int64_t G, int64_t A) {
+    int64_t i = e > s ? (j - s) * G / (e - s) : 0;
+    i = i < 0 ? 0 : (i >= G ? G - 1 : i);
+    while (i + 1 < G && kd_cut(s, e, G, i + 1, A) <= j) ++i;
+    while (i > 0 && kd_cut(s, e, G, i, A) > j) --i;
+    return i;
 }
 
-// out[j] = pts[idx_j] (whole padded rows), perm[j] = idx_j (the pooled index, < 2^31)
-__global__ void k_permute_rows(const float* __restrict__ pts, int DP, int64_t N, const uint64_t* __restrict__ keys,
-                               float* __restrict__ out, int32_t* __restrict__ perm) {
+// keys of level `level` (0 <= level < 3) for rows already in the order of the previous level:
+// key = label (1 bit) | cell of the previous levels (cb bits) | order key of x_level (the top 63 - cb - ib bits of
+// f32_key) | row index (ib bits). A stable LSD sort of bits [ib, 64) gives the level's order.
+__global__ void k_kd_keys(const float* __restrict__ pts, int DP, int64_t N, int64_t n_P, int level, int64_t G0,
+                          int64_t G1, int64_t A, int ib, int cb, uint64_t* __restrict__ keys) {
+    const int kb = 63 - cb - ib;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t idx = (int64_t)(keys[j] & 0x7fffffffull);
+        const bool lab = j >= n_P;
+        const int64_t s = lab ? n_P : 0, e = lab ? N : n_P;
+        uint64_t cell = 0;
+        if (level >= 1) {
+            const int64_t i0 = kd_part(j, s, e, G0, A);
+            cell = (uint64_t)i0;
+            if (level >= 2) {
+                const int64_t s1 = kd_cut(s, e, G0, i0, A), e1 = kd_cut(s, e, G0, i0 + 1, A);
+                cell = (uint64_t)(i0 * G1 + kd_part(j, s1, e1, G1, A));
+            }
+        }
+        uint64_t k = f32_key(pts[j * DP + level]);
+        if (kb < 32) k >>= (32 - kb);
+        keys[j] = ((uint64_t)lab << 63) | (cb ? cell << (63 - cb) : 0ull) | (k << ib) | (uint64_t)j;
+    }
+}
+
+// out[j] = pts[idx_j] (whole padded rows), perm_out[j] = perm_in[idx_j] (perm_in == nullptr: idx_j), idx_j = the low
+// ib bits of the sorted key j (pooled indices < 2^31)
+__global__ void k_permute_rows(const float* __restrict__ pts, int DP, int64_t N, const uint64_t* __restrict__ keys,
+                               int ib, const int32_t* __restrict__ perm_in, float* __restrict__ out,
+                               int32_t* __restrict__ perm_out) {
+    const uint64_t mask = (ib >= 64) ? ~0ull : ((1ull << ib) - 1);
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t idx = (int64_t)(keys[j] & mask);
         DDKS_ASSERT(idx < N);
         const float4* src = reinterpret_cast<const float4*>(pts + idx * DP);
         float4* dst = reinterpret_cast<float4*>(out + j * DP);
         dst[0] = src[0];
         if (DP == 8) dst[1] = src[1];
-        perm[j] = (int32_t)idx;
+        perm_out[j] = perm_in ? perm_in[idx] : (int32_t)idx;
+    }
+}
+
+// boxes[t][k] = {min, max} of x_k over rows [t*TILE, min(N, (t+1)*TILE)), k < KX: one warp per tile
+__global__ void k_tile_boxes(const float* __restrict__ pts, int DP, int64_t N, int TILE, int KX,
+                             float* __restrict__ boxes) {
+    const int64_t n_tiles = (N + TILE - 1) / TILE;
+    const int lane = threadIdx.x & 31;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < n_tiles;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t r0 = w * TILE, r1 = min(N, r0 + TILE);
+        for (int k = 0; k < KX; ++k) {
+            float lo = INFINITY, hi = -INFINITY;
+            for (int64_t r = r0 + lane; r < r1; r += 32) {
+                const float v = pts[r * DP + k];
+                lo = fminf(lo, v), hi = fmaxf(hi, v);
+            }
+#pragma unroll
+            for (int sh = 16; sh; sh >>= 1) {
+                lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, sh));
+                hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, sh));
+            }
+            if (lane == 0) boxes[(w * KX + k) * 2] = lo, boxes[(w * KX + k) * 2 + 1] = hi;
+        }
     }
 }
 
@@ -734,4 +857,5 @@ __global__ void k_argmax(const uint64_t* __restrict__ per_origin, int64_t n, int
         if (per_origin[i] == target) atomicMin(arg, (unsigned long long)(o_begin + i));
 }
 
+}  // namespace
 }  // namespace ddks

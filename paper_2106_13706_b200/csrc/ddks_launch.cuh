@@ -1,0 +1,114 @@
+// ddks_launch.cuh — host-side launch of the count kernel (segment planning, accumulators, finaliser), shared by the
+// translation units that instantiate k_count (ddks_api.cu: position order; ddks_api_kd*.cu: kd order).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <utility>
+
+#include "ddks_kernels.cuh"
+#include "ddks_internal.h"
+
+namespace ddks_host {
+
+struct CountPlan {
+    int64_t B;
+    int32_t N, n_P, o_begin, o_end;
+    int64_t nP, nQ;
+    bool split;      // SPLIT counters (c_P, c_Q separately)
+    int64_t window;  // max points per segment so no 16-bit counter half leaves int16
+};
+
+template <int D, bool SPLIT, bool GT, int KX = 0>
+ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a, cudaStream_t st) {
+    using G = ddks::Geo<D, SPLIT>;
+    auto kern = ddks::k_count<D, SPLIT, GT, KX>;
+    // function attributes are per device: remember which devices this instantiation was configured on
+    static bool attr_done[kMaxDevices] = {};
+    if (ctx->device >= kMaxDevices) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device index %d >= %d", ctx->device, kMaxDevices);
+    if (!attr_done[ctx->device]) {
+        CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES));
+        attr_done[ctx->device] = true;
+    }
+    const int n_orig = pl.o_end - pl.o_begin;
+    const int blocks_o = (n_orig + G::ORIGINS - 1) / G::ORIGINS;
+    const int n_tiles = (pl.N + G::TILE - 1) / G::TILE;
+    // segment length: at most the int16 flush window. Among the segment counts that respect it, pick the one with
+    // the least modelled time: waves x per-CTA cost, where a CTA costs its segment's points (x its origins) plus the
+    // flush of NB int32 partials per origin (global atomics; ~FLUSH_COST point-equivalents each) and the setup.
+    static int per_sm_dev[kMaxDevices] = {};
+    int& per_sm = per_sm_dev[ctx->device];
+    if (!per_sm) {
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::T, G::SMEM_BYTES));
+        per_sm = std::max(per_sm, 1);
+    }
+    int nsm = 148;
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
+    const int64_t slots = (int64_t)nsm * per_sm;
+    const int w_tiles = std::max(1, (int)(pl.window / G::TILE));
+    const int min_segs = (n_tiles + w_tiles - 1) / w_tiles;
+    const int64_t base_ctas = pl.B * blocks_o;
+    int segs = min_segs;
+    if (!(ctx->flags & DDKS_FLAG_FORCE_DIRECT)) {
+        constexpr double FLUSH_COST = 2.0, SETUP_COST = 2.0 * G::TILE;  // calibrated on C3 (segs 2..16 sweep)
+        double best = 1e300;
+        const int max_segs = (int)std::min<int64_t>(n_tiles, std::max<int64_t>(min_segs, (16 * slots + base_ctas - 1) / base_ctas));
+        for (int sg = min_segs; sg <= max_segs; ++sg) {
+            const int tps = (n_tiles + sg - 1) / sg;
+            const int real = (n_tiles + tps - 1) / tps;
+            if (real != sg) continue;
+            const int64_t ctas = base_ctas * sg;
+            const int64_t waves = (ctas + slots - 1) / slots;
+            const double cta = (double)tps * G::TILE + SETUP_COST + (sg > 1 ? FLUSH_COST * G::NB : 0.0);
+            const double cost = (double)waves * cta;
+            if (cost < best * (1.0 - 1e-9)) { best = cost; segs = sg; }
+        }
+        if (const char* e = getenv("DDKS_SEGS")) segs = std::max(min_segs, std::min(n_tiles, atoi(e)));  // tuning override
+    }
+    const int tiles_per_seg = (n_tiles + segs - 1) / segs;
+    segs = (n_tiles + tiles_per_seg - 1) / tiles_per_seg;
+    a.seg_points = tiles_per_seg * G::TILE;
+    if (segs > 65535) return fail(ctx, DDKS_ERR_TOO_LARGE, "too many point segments");
+    if (segs > 1) {
+        const size_t acc_bytes = (size_t)pl.B * G::NB * (size_t)n_orig * 4;
+        ddks_status s = ensure(ctx, ctx->accum, acc_bytes);
+        if (s) return s;
+        CU(cudaMemsetAsync(ctx->accum.p, 0, acc_bytes, st));
+        a.accum = (int32_t*)ctx->accum.p;
+    } else {
+        a.accum = nullptr;
+    }
+    if (pl.B > 65535 || blocks_o > 65535) return fail(ctx, DDKS_ERR_TOO_LARGE, "grid too large");
+    dim3 grid((unsigned)segs, (unsigned)blocks_o, (unsigned)pl.B);
+    std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+    if (ctx->flags & DDKS_FLAG_PROFILE) {
+        if (!ctx->ev_free.empty()) {
+            ev = ctx->ev_free.back();
+            ctx->ev_free.pop_back();
+        } else {
+            CU(cudaEventCreate(&ev.first));
+            CU(cudaEventCreate(&ev.second));
+        }
+        CU(cudaEventRecord(ev.first, st));
+    }
+    kern<<<grid, G::T, G::SMEM_BYTES, st>>>(a);
+    CHECK_LAUNCH();
+    ctx->launches++;
+    if (ev.first) {
+        CU(cudaEventRecord(ev.second, st));
+        ctx->ev_pending.push_back(ev);
+        ctx->ev_pairs.push_back((uint64_t)pl.B * (uint64_t)n_orig * (uint64_t)pl.N);
+    }
+    if (segs > 1) {
+        const int64_t total = pl.B * n_orig;
+        const int threads = 256;
+        const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 16);
+        ddks::k_finalize<D, SPLIT><<<blocks, threads, 0, st>>>(a, pl.B);
+        CHECK_LAUNCH();
+        ctx->launches++;
+    }
+    return DDKS_OK;
+}
+
+}  // namespace ddks_host

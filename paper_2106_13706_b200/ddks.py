@@ -28,6 +28,12 @@ DDKS_FLAG_PERM_GATHER = 16
 DDKS_FLAG_NO_X0 = 32
 DDKS_FLAG_FORCE_X0 = 64
 DDKS_FLAG_RDKS_FULL_SORT = 128
+DDKS_FLAG_KD_SHIFT = 9
+
+
+def DDKS_FLAG_KD_LEVELS(k: int) -> int:
+    """TEST ONLY: force k (1..3) levels of kd ordering (include/ddks.h)."""
+    return (k & 3) << DDKS_FLAG_KD_SHIFT
 DDKS_SIG_POISSON = 1
 
 
@@ -85,6 +91,7 @@ def _load() -> ctypes.CDLL:
         "ddks_rdks": ([vp, vp, i64, vp, i64, i32, vp, ctypes.POINTER(ddks_result)], ctypes.c_int),
         "ddks_shard_range": ([i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)], ctypes.c_int),
         "ddks_launch_count": ([vp], i64),
+        "ddks_kd_levels": ([vp], i32),
         "ddks_profile_read": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_uint64)],
                               ctypes.c_int),
         "ddks_destroy": ([vp], ctypes.c_int),
@@ -100,7 +107,7 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 EXPORTED = ("ddks_get_nccl_id", "ddks_create", "ddks_stat", "ddks_stat_batch", "ddks_permutation_null",
-            "ddks_stat_per_origin", "ddks_stat_shard", "ddks_significance", "ddks_significance_batch", "ddks_vdks", "ddks_rdks", "ddks_shard_range", "ddks_launch_count", "ddks_profile_read", "ddks_destroy",
+            "ddks_stat_per_origin", "ddks_stat_shard", "ddks_significance", "ddks_significance_batch", "ddks_vdks", "ddks_rdks", "ddks_shard_range", "ddks_launch_count", "ddks_kd_levels", "ddks_profile_read", "ddks_destroy",
             "ddks_last_error", "ddks_version")
 
 
@@ -308,6 +315,11 @@ def ddks_launch_count(ctx) -> int:
     return int(LIB.ddks_launch_count(ctx))
 
 
+def ddks_kd_levels(ctx) -> int:
+    """Levels of the kd ordering used by the last count (0: position order)."""
+    return int(LIB.ddks_kd_levels(ctx))
+
+
 def ddks_profile_read(ctx):
     """-> (count_kernel_ms, count_launches, pairs) since the last read (context needs DDKS_FLAG_PROFILE)."""
     ms, n, pairs = ctypes.c_double(), ctypes.c_int64(), ctypes.c_uint64()
@@ -355,6 +367,10 @@ class Context:
     @property
     def launch_count(self) -> int:
         return ddks_launch_count(self.ctx)
+
+    @property
+    def kd_levels(self) -> int:
+        return ddks_kd_levels(self.ctx)
 
     def close(self):
         if self.ctx is not None:

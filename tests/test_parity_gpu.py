@@ -326,6 +326,58 @@ def test_x0_ordered_ties_gt(ctx_x0_gt, d):
     assert (got.num, got.den, got.argmax_origin) == (want[0], want[1], want[3])
 
 
+# ----------------------------------------------------------------------------------- kd-ordered count (K levels)
+
+KD_CASES = [(2, "2,5,1", 9000, 7000, 2, "normal"), (2, "2,3,1", 6000, 6000, 3, "grid"), (3, "3,3,2", 12000, 9000, 3, "mixed"),
+            (3, "3,2,2", 8000, 8000, 4, "grid"), (3, "3,3,3", 16000, 14000, 5, "mixed"), (2, "2,7,1", 20000, 17001, 5, "dup"),
+            (3, "3,2,3", 9000, 9000, 6, "normal"), (3, "3,3,3", 7000, 6000, 7, "grid"), (2, "2,4,1", 5000, 5400, 8, "mixed"),
+            (3, "3,9,9", 4000, 3000, 5, "normal"), (3, "3,3,3", 3, 12000, 5, "grid"), (2, "2,2,1", 20000, 1, 3, "normal"),
+            (2, "2,1,1", 9000, 7000, 2, "grid"), (3, None, 11000, 9000, 5, "mixed")]
+
+
+@pytest.mark.parametrize("K_,env,n_P,n_Q,d,kind", KD_CASES)
+def test_kd_ordered_parity(monkeypatch, ctx_nox0, K_, env, n_P, n_Q, d, kind):
+    # K levels of kd ordering (bits 0..K-1 decided per tile where the tile's box does not interleave with the CTA's
+    # origins'); DDKS_KD fixes the slab / cell counts so small inputs still get several cells (and empty ones: 3,9,9)
+    if env is None:
+        monkeypatch.delenv("DDKS_KD", raising=False)
+    else:
+        monkeypatch.setenv("DDKS_KD", env)
+    P, Q = I.random_pair(9500 + n_P + 3 * d, n_P, n_Q, d, kind)
+    if kind == "grid":
+        P[:, :3] = np.round(P[:, :3] * 3) / 3
+    with K.Context(flags=K.DDKS_FLAG_FORCE_X0 | K.DDKS_FLAG_KD_LEVELS(K_)) as c:
+        got = check_pair(c, P, Q)
+        assert c.kd_levels == K_
+    assert ctx_nox0.stat(dev(P), dev(Q)) == got
+
+
+def test_kd_ties_gt_uses_one_level(monkeypatch):
+    # the '>' test convention is instantiated with one level: a forced K falls back to 1, still exact
+    monkeypatch.setenv("DDKS_KD", "3,3,3")
+    P, Q = I.random_pair(9400, 7000, 6000, 5, "grid")
+    want = O.ddks(P, Q, ties_gt=True)
+    with K.Context(flags=K.DDKS_FLAG_FORCE_X0 | K.DDKS_FLAG_TIES_GT | K.DDKS_FLAG_KD_LEVELS(3)) as c:
+        got = c.stat(dev(P), dev(Q))
+        assert c.kd_levels == 1
+    assert (got.num, got.den, got.argmax_origin) == (want[0], want[1], want[3])
+
+
+@pytest.mark.parametrize("K_,env", [(2, "2,4,1"), (3, "3,3,2")])
+def test_kd_shard_rehearsal(monkeypatch, K_, env):
+    # origin shards are positions of the kd order: max over shards and the smallest attaining argmax reproduce the
+    # oracle for any world size
+    monkeypatch.setenv("DDKS_KD", env)
+    P, Q = I.random_pair(9950 + K_, 15000, 13000, 5, "mixed")
+    want = O.ddks(P, Q)
+    with K.Context(flags=K.DDKS_FLAG_FORCE_X0 | K.DDKS_FLAG_KD_LEVELS(K_)) as c:
+        for world in (2, 3, 8):
+            parts = [c.stat_shard(dev(P), dev(Q), world, r) for r in range(world)]
+            num = max(p.num for p in parts)
+            arg = min(p.argmax_origin for p in parts if p.num == num)
+            assert (num, arg) == (want[0], want[3]), (world, parts)
+
+
 # ----------------------------------------------------------------------------------- launch-limit edge paths
 
 def test_batch_beyond_grid_z_limit(ctx):

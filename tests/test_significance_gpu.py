@@ -156,6 +156,22 @@ def test_significance_x0_ordered(n_P, n_Q, d, kind):
     assert (a.stat.num, a.stat.argmax_origin) == (want[0], want[3])
 
 
+@pytest.mark.parametrize("K_,env,n_P,n_Q,d", [(2, "2,3,1", 3000, 2600, 3), (3, "3,3,2", 4000, 3500, 5),
+                                               (3, "3,2,2", 2500, 2500, 8)])
+def test_significance_kd_ordered(monkeypatch, K_, env, n_P, n_Q, d):
+    # the kd-ordered SPLIT kernel with several slabs / cells: identical M_T histogram, statistic and log_prod
+    monkeypatch.setenv("DDKS_KD", env)
+    P, Q = I.random_pair(1300 + n_P + d, n_P, n_Q, d, "mixed")
+    with K.Context(flags=K.DDKS_FLAG_FORCE_X0 | K.DDKS_FLAG_KD_LEVELS(K_)) as cx, \
+            K.Context(flags=K.DDKS_FLAG_NO_X0) as cn:
+        a = cx.significance(dev(P), dev(Q), detail=True)
+        assert cx.kd_levels == K_
+        b = cn.significance(dev(P), dev(Q), detail=True)
+    assert a.stat == b.stat and np.array_equal(a.mt_hist, b.mt_hist) and a.log_prod == b.log_prod
+    want = O.ddks(P, Q)
+    assert (a.stat.num, a.stat.argmax_origin) == (want[0], want[3])
+
+
 def test_significance_x0_c2(ctx):
     P, Q = I.config("C2")
     with K.Context(flags=K.DDKS_FLAG_FORCE_X0) as cx:
