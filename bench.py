@@ -14,7 +14,8 @@ CUDA events on the launching stream; L2 flushed (512 MiB write) between steps, o
 reported time is the MAX over ranks. `value` = K * N^2 / that time. `e2e` repeats the step through the
 C-ABI with PINNED HOST input buffers (H2D inside the timed call) and the host result read.
 `roofline`: the classify+count kernel's FP32 compares/s (d per pair) vs the ALU-pipe compare peak
-148 SMs x 64 lanes/clk (FSET.BF, measured by microbench/pipes.cu) x sm_max_mhz (MEASURED_PEAKS.json).
+148 SMs x 64 lanes/clk (FSET.BF, measured by microbench/pipes.cu) x sm_max_mhz (MEASURED_PEAKS.json). With the kd
+ordering (N >= 200000) most tiles decide up to 3 of the d bits once per tile, so frac can exceed 1.
 `cpu_baseline`: the CPU oracle (oracle/ddks_oracle.c, as it stands) on this host's cores over a bounded
 sample of origins of the same workload (rank 0, N = 1 only).
 """
@@ -401,6 +402,11 @@ def main():
     roof = step.roofline(kern_ms, kern_launches, kern_pairs, total_ms / args.steps, pk)
     if args.method in ("exact", "significance"):
         roof["kernel_share_of_step"] = kern_ms_max / total_ms if total_ms else None
+        roof["kd_levels"] = ctx.kd_levels
+        if ctx.kd_levels:
+            roof["note"] = (f"kd ordering: bits 0..{ctx.kd_levels - 1} are decided once per tile for most tiles, so fewer "
+                            "than d compares are executed per pair and frac (algorithmic d compares per pair) can "
+                            "exceed 1; DESIGN.md §7 'kd ordering'")
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp) and args.method == "exact":

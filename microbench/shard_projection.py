@@ -1,5 +1,5 @@
 """One-GPU rehearsal of the multi-GPU C5 statistic: for world = 1, 2, 4, 8, time on this device the
-origin shard every rank would own (ddks_stat_shard: the same kernels, shard of the x_0 order, no collective),
+origin shard every rank would own (ddks_stat_shard: the same kernels, shard of the kd order, no collective),
 combine the shard results as NCCL would, and report the projected per-world time = max over ranks. This is a
 projection from one B200, not a multi-GPU measurement (the NCCL all-reduce of one uint64 is not included)."""
 import json, os, sys

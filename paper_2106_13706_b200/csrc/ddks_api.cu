@@ -188,11 +188,11 @@ bool x0_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q) {
     return d >= 2 && d <= 8 && n_P + n_Q >= min_n;
 }
 
-ddks_status run_count_kd(ddks_ctx* ctx, const float* packed, int d, int64_t n_P, int64_t n_Q, int64_t o_begin,
-                         int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st, bool split,
+ddks_status run_count_kd(ddks_ctx* ctx, const float* packed, int d, int64_t n_P, int64_t n_Q, int sw, int sr,
+                         uint64_t* item_num, uint64_t* per_origin, cudaStream_t st, bool split,
                          unsigned long long* hist) {
     switch (d) {
-#define KD_CASE(D) case D: return run_count_kd_d<D>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st, split, hist);
+#define KD_CASE(D) case D: return run_count_kd_d<D>(ctx, packed, n_P, n_Q, sw, sr, item_num, per_origin, st, split, hist);
         KD_CASE(2) KD_CASE(3) KD_CASE(4) KD_CASE(5) KD_CASE(6) KD_CASE(7) KD_CASE(8)
 #undef KD_CASE
     }
@@ -203,8 +203,8 @@ ddks_status run_count_kd(ddks_ctx* ctx, const float* packed, int d, int64_t n_P,
 // position-ordered), then -- unless export_per (debug export of per-origin nums for [ob, oe)) -- the NCCL max of
 // num and this rank's argmax candidate into dres->arg (min-combined by the caller). split/hist: significance.
 ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n_P, int64_t n_Q, int64_t ob,
-                            int64_t oe, DevResult* dres, bool export_per, bool split, unsigned long long* hist,
-                            cudaStream_t st, uint64_t** per_out) {
+                            int64_t oe, int sw, int sr, DevResult* dres, bool export_per, bool split,
+                            unsigned long long* hist, cudaStream_t st, uint64_t** per_out) {
     const int64_t N = n_P + n_Q;
     ddks_status s;
     const bool x0 = !export_per && x0_applicable(ctx, d, n_P, n_Q);
@@ -213,13 +213,9 @@ ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n
         if ((s = ensure(ctx, ctx->per_origin, (size_t)N * 8))) return s;
         uint64_t* per = (uint64_t*)ctx->per_origin.p;
         *per_out = per;
-        if (oe > ob) {
-            // SPLIT counters when the significance needs c_Q or DIFF counters would overflow (as in run_count)
-            const bool sp = split || !diff_counters_ok(n_P, n_Q);
-            if ((s = run_count_kd(ctx, packed, d, n_P, n_Q, ob, oe, (uint64_t*)&dres->num, per, st, sp, hist))) return s;
-        } else {
-            CU(cudaMemsetAsync(per, 0, (size_t)N * 8, st));
-        }
+        // SPLIT counters when the significance needs c_Q or DIFF counters would overflow (as in run_count)
+        const bool sp = split || !diff_counters_ok(n_P, n_Q);
+        if ((s = run_count_kd(ctx, packed, d, n_P, n_Q, sw, sr, (uint64_t*)&dres->num, per, st, sp, hist))) return s;
         if (ctx->world > 1) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
         ddks::k_argmax<<<(int)std::min<int64_t>((N + 255) / 256, 148 * 4), 256, 0, st>>>(
             per, N, 0, (const uint64_t*)&dres->num, &dres->arg);
@@ -527,7 +523,8 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
     float* packed = (float*)ctx->packed.p;
     if ((s = launch_pack(ctx, (const float*)dP, n_P, (const float*)dQ, n_Q, d, 1, packed, &dres->flag, st))) return s;
     uint64_t* per = nullptr;
-    if ((s = count_statistic(ctx, packed, d, n_P, n_Q, ob, oe, dres, export_mode, false, nullptr, st, &per))) return s;
+    const int sw = shard_world > 0 ? shard_world : ctx->world, sr = shard_world > 0 ? shard_rank : ctx->rank;
+    if ((s = count_statistic(ctx, packed, d, n_P, n_Q, ob, oe, sw, sr, dres, export_mode, false, nullptr, st, &per))) return s;
     if (ctx->world > 1 && !export_mode) {
         NC(ncclAllReduce(&dres->arg, &dres->arg, 1, ncclUint64, ncclMin, ctx->comm, st));
         NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));

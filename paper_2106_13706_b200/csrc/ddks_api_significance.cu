@@ -62,7 +62,7 @@ ddks_status ddks_significance(ddks_ctx* ctx, const float* P, int64_t n_P, const 
     float* packed = (float*)ctx->packed.p;
     if ((s = launch_pack(ctx, (const float*)dP, n_P, (const float*)dQ, n_Q, d, 1, packed, &dres->flag, st))) return s;
     uint64_t* per = nullptr;
-    if ((s = count_statistic(ctx, packed, d, n_P, n_Q, ob, oe, dres, false, true, hist, st, &per))) return s;
+    if ((s = count_statistic(ctx, packed, d, n_P, n_Q, ob, oe, ctx->world, ctx->rank, dres, false, true, hist, st, &per))) return s;
     if (ctx->world > 1) {
         NC(ncclAllReduce(&dres->arg, &dres->arg, 1, ncclUint64, ncclMin, ctx->comm, st));
         NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));

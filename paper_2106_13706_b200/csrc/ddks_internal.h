@@ -86,9 +86,10 @@ ddks_status collect_profile(ddks_ctx* ctx);
 ddks_status launch_pack(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d, int64_t B,
                         float* dst, uint32_t* flag, cudaStream_t st);
 // one statistic over the origin shard [ob, oe): count, NCCL max of num, this rank's argmax candidate (see ddks_api.cu)
+// (kd order: the strided origin blocks of shard sr of sw instead of [ob, oe))
 ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n_P, int64_t n_Q, int64_t ob,
-                            int64_t oe, DevResult* dres, bool export_per, bool split, unsigned long long* hist,
-                            cudaStream_t st, uint64_t** per_out);
+                            int64_t oe, int sw, int sr, DevResult* dres, bool export_per, bool split,
+                            unsigned long long* hist, cudaStream_t st, uint64_t** per_out);
 // B items of N packed points: classify + count (+ finalise); force_split + hist: SPLIT counters and per-item M_T
 // histograms hist[B][n_Q + 1] (significance)
 ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int64_t n_P, int64_t n_Q,
@@ -96,10 +97,11 @@ ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int6
                       bool force_split = false, unsigned long long* hist = nullptr);
 // items sharded contiguously over ranks: all-gather every rank's slice of dev_nums[total] (8-byte elements)
 ddks_status all_gather_items(ddks_ctx* ctx, uint64_t* dev_nums, int64_t total, cudaStream_t st);
-// kd-ordered count of one statistic (B == 1, 2 <= D <= 8; ddks_kd.cuh, instantiated in ddks_api_kd_*.cu)
+// kd-ordered count of one statistic (B == 1, 2 <= D <= 8; ddks_kd.cuh, instantiated in ddks_api_kd_*.cu): the origin
+// blocks shard_rank, shard_rank + shard_world, ... of the kd order
 template <int D>
-ddks_status run_count_kd_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int64_t n_Q, int64_t o_begin,
-                           int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st, bool split,
+ddks_status run_count_kd_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int64_t n_Q, int shard_world,
+                           int shard_rank, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st, bool split,
                            unsigned long long* hist);
 ddks_status radix_sort_keys(ddks_ctx* ctx, uint64_t* src, uint64_t* dst, int64_t N, int nseg, int shift_begin,
                             uint32_t* hist, cudaStream_t st, uint64_t** sorted);

@@ -63,8 +63,8 @@ ddks_status launch_kd(ddks_ctx* ctx, const CountPlan& pl, const ddks::CountArgs&
 }
 
 template <int D, bool SPLIT>
-ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int64_t n_Q, int64_t o_begin,
-                           int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st,
+ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int64_t n_Q, int shard_world,
+                           int shard_rank, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st,
                            unsigned long long* hist_out) {
     using G = ddks::Geo<D, SPLIT>;
     const int64_t N = n_P + n_Q;
@@ -122,15 +122,17 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     CU(cudaMemsetAsync(per_origin, 0, (size_t)N * 8, st));
     const uint64_t gg = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
     const uint32_t a_ = (uint32_t)((uint64_t)n_Q / gg), b_ = (uint32_t)((uint64_t)n_P / gg);
-    CountPlan pl{1, (int32_t)N, (int32_t)n_P, (int32_t)o_begin, (int32_t)o_end, n_P, n_Q, SPLIT,
-                 SPLIT ? 32767 : (int64_t)(32767 / std::max(a_, b_))};
+    // all N origins (positions of the kd order); shard r of W takes origin blocks r, r + W, r + 2W, ... so every
+    // rank gets the same mix of cells (contiguous shards differ by ~10 % in decided bits at C5)
+    CountPlan pl{1, (int32_t)N, (int32_t)n_P, 0, (int32_t)N, n_P, n_Q, SPLIT,
+                 SPLIT ? 32767 : (int64_t)(32767 / std::max(a_, b_)), shard_world, shard_rank};
     ddks::CountArgs a{};
     a.pts = spts;
     a.item_stride = N * DP;
     a.N = (int32_t)N;
     a.n_P = (int32_t)n_P;
-    a.o_begin = (int32_t)o_begin;
-    a.o_end = (int32_t)o_end;
+    a.o_begin = 0;
+    a.o_end = (int32_t)N;
     a.incP = SPLIT ? 1u : a_;
     a.incQ = SPLIT ? 1u : 0u - b_;
     a.g = SPLIT ? 1 : gg;
@@ -155,11 +157,11 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
 }
 
 template <int D>
-ddks_status run_count_kd_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int64_t n_Q, int64_t o_begin,
-                           int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st, bool split,
+ddks_status run_count_kd_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int64_t n_Q, int shard_world,
+                           int shard_rank, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st, bool split,
                            unsigned long long* hist) {
-    return split ? run_count_kd_t<D, true>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st, hist)
-                 : run_count_kd_t<D, false>(ctx, packed, n_P, n_Q, o_begin, o_end, item_num, per_origin, st, hist);
+    return split ? run_count_kd_t<D, true>(ctx, packed, n_P, n_Q, shard_world, shard_rank, item_num, per_origin, st, hist)
+                 : run_count_kd_t<D, false>(ctx, packed, n_P, n_Q, shard_world, shard_rank, item_num, per_origin, st, hist);
 }
 
 }  // namespace ddks_host

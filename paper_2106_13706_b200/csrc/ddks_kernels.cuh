@@ -155,13 +155,17 @@ struct CountArgs {
     int64_t item_stride;     // floats per item = N * DP
     int32_t N, n_P;          // pooled points per item; the first n_P are P
     int32_t o_begin, o_end;  // origin range (pooled indices) this launch owns, per item
+    // origin blocks of R*T: CTA y takes block y * blk_stride + blk_off of [o_begin, o_end) (kd-ordered shards stride
+    // over the blocks so every rank gets the same mix of cells); accumulator slot li = y * R*T + r*T + t, acc_stride
+    // slots per item (stride 1: li = o - o_begin)
+    int32_t blk_stride = 1, blk_off = 0, acc_stride = 0;
     int32_t seg_points;      // points per grid.z segment (multiple of TILE, <= the int16 flush window)
     uint32_t incP, incQ;     // DIFF: +a and -b (two's complement); SPLIT: 1 and 1
     uint64_t g;              // DIFF: gcd(n_P, n_Q) multiplier
     int64_t nP, nQ;          // SPLIT finalisation
     uint64_t* item_num;      // [B] atomicMax target (direct mode)
     uint64_t* per_origin;    // [o_end - o_begin] or nullptr (direct mode, B == 1)
-    int32_t* accum;          // accumulate mode: [B][NB][n_orig] int32 counters, else nullptr (direct mode)
+    int32_t* accum;          // accumulate mode: [B][NB][acc_stride] int32 counters, else nullptr (direct mode)
     const float* boxes;      // kd-ordered mode: [n_tiles][KX][2] min / max of dims < KX per TILE rows, else nullptr
     const int32_t* perm;     // kd-ordered mode: perm[j] = pooled index of sorted origin j; per_origin is then a
                              // full [N] array in pooled order (else nullptr: per_origin indexed o - o_begin)
@@ -349,7 +353,8 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
     const int t = threadIdx.x;
     const int64_t item = blockIdx.z;
     const float* pts = a.pts + item * a.item_stride;
-    const int32_t blk_o0 = a.o_begin + (int32_t)blockIdx.y * G::ORIGINS;
+    const int32_t blk_o0 = a.o_begin + ((int32_t)blockIdx.y * a.blk_stride + a.blk_off) * G::ORIGINS;
+    const int32_t li0 = (int32_t)blockIdx.y * G::ORIGINS;  // this CTA's first accumulator slot
     const int32_t seg0 = (int32_t)blockIdx.x * a.seg_points;
     const int32_t seg1 = min(a.N, seg0 + a.seg_points);
     const int n_tiles = (seg1 - seg0 + TILE - 1) / TILE;
@@ -480,10 +485,9 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
     }
     __syncthreads();  // all red.shared retired before reading the counters
 
-    const int32_t n_orig = a.o_end - a.o_begin;
     if (a.accum != nullptr) {
         // flush: exact int32 partial counters -> global (red.global.add), finalised by k_finalize
-        int32_t* acc = a.accum + item * (int64_t)G::NB * n_orig;
+        int32_t* acc = a.accum + item * (int64_t)G::NB * a.acc_stride;
 #pragma unroll 1
         for (int r = 0; r < R; ++r) {
             const int32_t oi = blk_o0 + r * T + t;
@@ -495,8 +499,8 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
                 int32_t lo, hi;
                 split16(hist[q * WPB + sl], lo, hi);
                 const int32_t v = hiw ? hi : lo;
-                DDKS_ASSERT(oi - a.o_begin < n_orig && oi >= a.o_begin);
-                if (v) atomicAdd(&acc[(int64_t)q * n_orig + (oi - a.o_begin)], v);
+                DDKS_ASSERT(li0 + r * T + t < a.acc_stride && oi >= a.o_begin);
+                if (v) atomicAdd(&acc[(int64_t)q * a.acc_stride + (li0 + r * T + t)], v);
             }
         }
         return;
@@ -629,25 +633,30 @@ __global__ void k_finalize(const CountArgs a, int64_t B) {
             __syncthreads();
         }
     }
-    const int64_t total = B * (int64_t)n_orig;
+    constexpr int ORIG = Geo<D, SPLIT>::ORIGINS;
+    const int64_t ns = a.acc_stride;  // accumulator slots per item
+    const int64_t total = B * ns;
     uint64_t best = 0;
-    int64_t item_of_best = -1;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t item = i / n_orig, oi = i - item * n_orig;
-        const int32_t* acc = a.accum + item * (int64_t)NB * n_orig + oi;
+        const int64_t item = i / ns, li = i - item * ns;
+        // slot li -> origin offset oi in [0, n_orig) (block li / ORIG of this launch is block
+        // (li / ORIG) * blk_stride + blk_off of the range); slots past the range hold no origin
+        const int64_t oi = ((li / ORIG) * a.blk_stride + a.blk_off) * ORIG + li % ORIG;
+        if (oi >= n_orig) continue;
+        const int32_t* acc = a.accum + item * (int64_t)NB * ns + li;
         uint64_t m = 0;
         if constexpr (!SPLIT) {
             uint32_t mm = 0;
             for (int q = 0; q < NQ; ++q) {
-                const int32_t v = (int32_t)acc[(int64_t)q * n_orig];
+                const int32_t v = (int32_t)acc[(int64_t)q * ns];
                 const uint32_t av = (uint32_t)(v < 0 ? -v : v);
                 mm = av > mm ? av : mm;
             }
             m = (uint64_t)mm * a.g;
         } else {
             for (int q = 0; q < NQ; ++q) {
-                const int64_t cP = (int64_t)acc[(int64_t)q * n_orig];
-                const int64_t cQ = (int64_t)acc[(int64_t)(NQ + q) * n_orig];
+                const int64_t cP = (int64_t)acc[(int64_t)q * ns];
+                const int64_t cQ = (int64_t)acc[(int64_t)(NQ + q) * ns];
                 if (a.hist) {
                     if (priv && cQ < HS) atomicAdd(&sh_hist[cQ], 1u);
                     else hist_add_aggregated(a.hist, item * a.hist_stride + cQ);
@@ -663,7 +672,6 @@ __global__ void k_finalize(const CountArgs a, int64_t B) {
         } else {
             atomicMax(reinterpret_cast<unsigned long long*>(&a.item_num[item]), (unsigned long long)m);
         }
-        (void)item_of_best;
     }
     if (B == 1) {
         best = warp_max_u64(best);

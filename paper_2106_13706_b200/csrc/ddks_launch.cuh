@@ -18,6 +18,7 @@ struct CountPlan {
     int64_t nP, nQ;
     bool split;      // SPLIT counters (c_P, c_Q separately)
     int64_t window;  // max points per segment so no 16-bit counter half leaves int16
+    int32_t blk_stride = 1, blk_off = 0;  // this launch takes origin blocks blk_off, blk_off + blk_stride, ...
 };
 
 template <int D, bool SPLIT, bool GT, int KX = 0>
@@ -32,7 +33,12 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
         attr_done[ctx->device] = true;
     }
     const int n_orig = pl.o_end - pl.o_begin;
-    const int blocks_o = (n_orig + G::ORIGINS - 1) / G::ORIGINS;
+    const int blocks_all = (n_orig + G::ORIGINS - 1) / G::ORIGINS;
+    const int blocks_o = blocks_all > pl.blk_off ? (blocks_all - pl.blk_off + pl.blk_stride - 1) / pl.blk_stride : 0;
+    if (blocks_o == 0) return DDKS_OK;  // no origin block falls to this shard
+    a.blk_stride = pl.blk_stride;
+    a.blk_off = pl.blk_off;
+    a.acc_stride = pl.blk_stride == 1 ? n_orig : blocks_o * G::ORIGINS;
     const int n_tiles = (pl.N + G::TILE - 1) / G::TILE;
     // segment length: at most the int16 flush window. Among the segment counts that respect it, pick the one with
     // the least modelled time: waves x per-CTA cost, where a CTA costs its segment's points (x its origins) plus the
@@ -71,7 +77,7 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
     a.seg_points = tiles_per_seg * G::TILE;
     if (segs > 65535) return fail(ctx, DDKS_ERR_TOO_LARGE, "too many point segments");
     if (segs > 1) {
-        const size_t acc_bytes = (size_t)pl.B * G::NB * (size_t)n_orig * 4;
+        const size_t acc_bytes = (size_t)pl.B * G::NB * (size_t)a.acc_stride * 4;
         ddks_status s = ensure(ctx, ctx->accum, acc_bytes);
         if (s) return s;
         CU(cudaMemsetAsync(ctx->accum.p, 0, acc_bytes, st));
@@ -98,10 +104,13 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
     if (ev.first) {
         CU(cudaEventRecord(ev.second, st));
         ctx->ev_pending.push_back(ev);
-        ctx->ev_pairs.push_back((uint64_t)pl.B * (uint64_t)n_orig * (uint64_t)pl.N);
+        // origins of this launch: its blocks, less the missing tail of the last block when that block is its own
+        const bool last_own = (blocks_all - 1 - pl.blk_off) % pl.blk_stride == 0;
+        const uint64_t own = (uint64_t)blocks_o * G::ORIGINS - (last_own ? (uint64_t)blocks_all * G::ORIGINS - n_orig : 0);
+        ctx->ev_pairs.push_back((uint64_t)pl.B * own * (uint64_t)pl.N);
     }
     if (segs > 1) {
-        const int64_t total = pl.B * n_orig;
+        const int64_t total = pl.B * a.acc_stride;
         const int threads = 256;
         const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 16);
         ddks::k_finalize<D, SPLIT><<<blocks, threads, 0, st>>>(a, pl.B);

@@ -5,8 +5,9 @@ configuration on an origin subset via ddks_stat_per_origin, or a whole small con
     python profiles/profile_run.py C5 <o_begin> <o_end>   # C5 origin subset (same kernel, same segments)
     python profiles/profile_run.py C3|C2|C1               # full statistic
     python profiles/profile_run.py C4                     # full 4096-pair batch
-    python profiles/profile_run.py C5x0 <n>               # first n + n points of C5 through the x0-ordered kernel
-                                                          # (same k_count_x0<5> instantiation and CTA shape)
+    python profiles/profile_run.py C5kd <n>               # first n + n points of C5 through the kd-ordered kernel
+                                                          # (same k_count<5, ., ., K> kernel and CTA shape; the cost
+                                                          # model picks the cuts for n, so K / cells differ from C5)
 """
 import os
 import sys
@@ -19,7 +20,7 @@ from paper_2106_13706_b200 import inputs as I  # noqa: E402
 
 name = sys.argv[1]
 flags = 0
-if name == "C5x0":
+if name in ("C5x0", "C5kd"):
     P, Q = I.config("C5")
     n = int(sys.argv[2])
     P, Q = P[:n].copy(), Q[:n].copy()
