@@ -40,6 +40,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return SO
     nd = nccl_dir()
     debug = ["-DDDKS_DEBUG"] if os.environ.get("DDKS_DEBUG") else []  # device-side bounds asserts (ddks_common.cuh)
+    debug += os.environ.get("DDKS_NVCC_EXTRA", "").split()  # experiments only (e.g. -DDDKS_CFG5=8,384,256,3)
     common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", *debug, "-Xcompiler", "-fPIC,-fvisibility=hidden",
               "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(nd, "include"), "-I", os.path.join(ROOT, "include")]
     objdir = os.path.join(HERE, "build")

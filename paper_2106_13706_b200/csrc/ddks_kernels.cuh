@@ -39,6 +39,13 @@ namespace {  // internal linkage: several translation units include these kernel
 // points per launch segment (W chosen by the host so no half can leave int16), then flushes its counters to int32
 // global accumulators; if the whole point set fits one segment it finalises in-kernel instead.
 template <int D> struct Cfg;
+#ifndef DDKS_UNROLL  // experiments: points per unrolled step of the R > 2 inner loop
+#define DDKS_UNROLL 8
+#endif
+constexpr int kUnrollPts = DDKS_UNROLL;
+#ifndef DDKS_UNROLL_PARTIAL  // the same for the kd variants that compare some of the first KX dims (colder code)
+#define DDKS_UNROLL_PARTIAL DDKS_UNROLL
+#endif
 // R origins per thread (1 or even), T threads per CTA (multiple of 64 when R == 1), TILE points per SMEM stage,
 // S stages (DIFF mode). T is a multiple of 128 so every SMSP gets the same number of warps (d=5: R=12 x 8 warps
 // measured 0.8% faster than R=8 x 12 warps on the x0-ordered C5 kernel).
@@ -46,7 +53,13 @@ template <> struct Cfg<1> { static constexpr int R = 8, T = 256, TILE = 512, S =
 template <> struct Cfg<2> { static constexpr int R = 8, T = 256, TILE = 512, S = 3; };
 template <> struct Cfg<3> { static constexpr int R = 8, T = 256, TILE = 512, S = 3; };
 template <> struct Cfg<4> { static constexpr int R = 4, T = 256, TILE = 512, S = 3; };
-template <> struct Cfg<5> { static constexpr int R = 12, T = 256, TILE = 256, S = 3; };
+#ifndef DDKS_C5R  // geometry experiments: -DDDKS_C5R=.. -DDDKS_C5T=.. -DDDKS_C5TILE=.. -DDDKS_C5S=..
+#define DDKS_C5R 12
+#define DDKS_C5T 256
+#define DDKS_C5TILE 256
+#define DDKS_C5S 3
+#endif
+template <> struct Cfg<5> { static constexpr int R = DDKS_C5R, T = DDKS_C5T, TILE = DDKS_C5TILE, S = DDKS_C5S; };
 template <> struct Cfg<6> { static constexpr int R = 4, T = 384, TILE = 256, S = 3; };
 template <> struct Cfg<7> { static constexpr int R = 2, T = 384, TILE = 256, S = 3; };
 template <> struct Cfg<8> { static constexpr int R = 1, T = 384, TILE = 256, S = 3; };
@@ -308,7 +321,8 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
     }
     float xn[D];
     load_point<D>(tile + p * DP, xn);
-#pragma unroll 8
+    constexpr int UNR = (KX > 0 && UM != 0) ? DDKS_UNROLL_PARTIAL : kUnrollPts;
+#pragma unroll UNR
     for (; p < hi; ++p) {
         float x[D];
 #pragma unroll
