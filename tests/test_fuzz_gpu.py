@@ -40,19 +40,27 @@ def ctxs():
     cs = {name: K.Context(flags=f) for name, f in [("default", 0), ("x0", K.DDKS_FLAG_FORCE_X0),
                                                     ("direct", K.DDKS_FLAG_FORCE_DIRECT),
                                                     ("x0gt", K.DDKS_FLAG_FORCE_X0 | K.DDKS_FLAG_TIES_GT),
-                                                    ("full", K.DDKS_FLAG_RDKS_FULL_SORT)]}
+                                                    ("full", K.DDKS_FLAG_RDKS_FULL_SORT),
+                                                    ("kd2", K.DDKS_FLAG_FORCE_X0 | K.DDKS_FLAG_KD_LEVELS(2)),
+                                                    ("kd3", K.DDKS_FLAG_FORCE_X0 | K.DDKS_FLAG_KD_LEVELS(3))]}
     yield cs
     for c in cs.values():
         c.close()
 
 
 @pytest.mark.parametrize("n_P,n_Q,d,kind,seed", cases(2024, int(os.environ.get("DDKS_FUZZ_CASES", "36"))))
-def test_fuzz_exact_and_approx(ctxs, n_P, n_Q, d, kind, seed):
+def test_fuzz_exact_and_approx(monkeypatch, ctxs, n_P, n_Q, d, kind, seed):
     P, Q = I.random_pair(seed, n_P, n_Q, d, kind)
     want = O.ddks(P, Q)
     for name in ("default", "x0", "direct"):
         r = ctxs[name].stat(dev(P), dev(Q))
         assert (r.num, r.den, r.argmax_origin) == (want[0], want[1], want[3]), name
+    # kd levels 2 and 3 with seeded slab / cell counts (many empty or single-tile cells at these sizes)
+    for K_ in (2, 3):
+        monkeypatch.setenv("DDKS_KD", f"{K_},{1 + seed % 6},{1 + (seed // 6) % 5}")
+        r = ctxs[f"kd{K_}"].stat(dev(P), dev(Q))
+        assert (r.num, r.den, r.argmax_origin) == (want[0], want[1], want[3]), (K_, os.environ["DDKS_KD"])
+    monkeypatch.delenv("DDKS_KD")
     gt = O.ddks(P, Q, ties_gt=True)
     r = ctxs["x0gt"].stat(dev(P), dev(Q))
     assert (r.num, r.argmax_origin) == (gt[0], gt[3])
