@@ -103,6 +103,62 @@ __global__ void k_imad(Rec* r, uint32_t* out, float seed){
   uint32_t s=0; for (int i=0;i<CH;i++) s += a[i];
   rec_end(r,c,t,s,out);
 }
+// 9) FSETP.GE feeding a select (the predicate form of the compare; FSEL consumes it)
+__global__ void k_fsetp(Rec* r, uint32_t* out, float seed){
+  float a[CH]; for (int i=0;i<CH;i++) a[i] = seed + threadIdx.x + i;
+  unsigned long long c,t; rec_begin(r,c,t);
+  for (int it=0; it<ITERS; it++){
+    #pragma unroll
+    for (int i=0;i<CH;i++) asm volatile("{ .reg .pred p; setp.ge.f32 p, %0, 0f3F000000; selp.f32 %0, 0f3F800000, 0f3E800000, p; }" : "+f"(a[i]));
+  }
+  uint32_t s=0; for (int i=0;i<CH;i++) s += __float_as_uint(a[i]);
+  rec_end(r,c,t,s,out);
+}
+// 10) SHF.L.W (funnel shift, wrap)
+__global__ void k_shf(Rec* r, uint32_t* out, float seed){
+  uint32_t a[CH]; for (int i=0;i<CH;i++) a[i] = threadIdx.x*(i+3) + 1;
+  unsigned long long c,t; rec_begin(r,c,t);
+  for (int it=0; it<ITERS; it++){
+    #pragma unroll
+    for (int i=0;i<CH;i++) asm volatile("shf.l.wrap.b32 %0, %0, %0, %1;" : "+r"(a[i]) : "r"(it));
+  }
+  uint32_t s=0; for (int i=0;i<CH;i++) s += a[i];
+  rec_end(r,c,t,s,out);
+}
+// 11) IADD3 (three-input integer add)
+__global__ void k_iadd3(Rec* r, uint32_t* out, float seed){
+  uint32_t a[CH]; for (int i=0;i<CH;i++) a[i] = threadIdx.x*(i+3);
+  const uint32_t b = threadIdx.x ^ 0x55u;
+  unsigned long long c,t; rec_begin(r,c,t);
+  for (int it=0; it<ITERS; it++){
+    #pragma unroll
+    for (int i=0;i<CH;i++) asm volatile("{ .reg .u32 q; add.u32 q, %0, %1; add.u32 %0, q, %2; }" : "+r"(a[i]) : "r"(b), "r"(it));
+  }
+  uint32_t s=0; for (int i=0;i<CH;i++) s += a[i];
+  rec_end(r,c,t,s,out);
+}
+// 12) MATCH.ANY (warp-wide value match; the per-warp histogram aggregation of the north_star sketch)
+__global__ void k_match(Rec* r, uint32_t* out, float seed){
+  uint32_t a[CH], acc[CH]; for (int i=0;i<CH;i++) { a[i] = (threadIdx.x * (i + 3)) & 7u; acc[i] = 0; }
+  unsigned long long c,t; rec_begin(r,c,t);
+  for (int it=0; it<ITERS / 8; it++){
+    #pragma unroll
+    for (int i=0;i<CH;i++) { uint32_t m; asm volatile("match.any.sync.b32 %0, %1, 0xffffffff;" : "=r"(m) : "r"(a[i])); acc[i] += m; a[i] = (m + it) & 7u; }
+  }
+  uint32_t s=0; for (int i=0;i<CH;i++) s += acc[i];
+  rec_end(r,c,t,s,out);
+}
+// 13) VOTE.ANY
+__global__ void k_vote(Rec* r, uint32_t* out, float seed){
+  uint32_t a[CH]; for (int i=0;i<CH;i++) a[i] = (threadIdx.x * (i + 3)) & 1u;
+  unsigned long long c,t; rec_begin(r,c,t);
+  for (int it=0; it<ITERS; it++){
+    #pragma unroll
+    for (int i=0;i<CH;i++) { uint32_t v; asm volatile("{ .reg .pred p, q; setp.ne.u32 p, %1, 0; vote.sync.any.pred q, p, 0xffffffff; selp.u32 %0, 0, 1, q; }" : "=r"(v) : "r"(a[i])); a[i] = v; }
+  }
+  uint32_t s=0; for (int i=0;i<CH;i++) s += a[i];
+  rec_end(r,c,t,s,out);
+}
 // 8) The ddKS d=5 inner loop shape: 5 FSET.BF + 5 FFMA(imm) + 1 ATOMS per pair, R=8 origins per thread,
 //    points broadcast from SMEM (2 LDS per point, amortised over R origins).
 template<int R>
@@ -163,6 +219,11 @@ int main(){
   run("LOP3", [](Rec* r, uint32_t* o){ k_lop3<<<148,512>>>(r,o,1.f); }, d_r, d_o, nsm, (double)ITERS*CH, T);
   run("POPC", [](Rec* r, uint32_t* o){ k_popc<<<148,512>>>(r,o,1.f); }, d_r, d_o, nsm, (double)ITERS*CH*2, T);
   run("IMAD", [](Rec* r, uint32_t* o){ k_imad<<<148,512>>>(r,o,1.f); }, d_r, d_o, nsm, (double)ITERS*CH, T);
+  run("FSETP.GE (+FSEL consumer)", [](Rec* r, uint32_t* o){ k_fsetp<<<148,512>>>(r,o,1.f); }, d_r, d_o, nsm, (double)ITERS*CH, T);
+  run("SHF.L.W", [](Rec* r, uint32_t* o){ k_shf<<<148,512>>>(r,o,1.f); }, d_r, d_o, nsm, (double)ITERS*CH, T);
+  run("IADD3", [](Rec* r, uint32_t* o){ k_iadd3<<<148,512>>>(r,o,1.f); }, d_r, d_o, nsm, (double)ITERS*CH, T);
+  run("MATCH.ANY", [](Rec* r, uint32_t* o){ k_match<<<148,512>>>(r,o,1.f); }, d_r, d_o, nsm, (double)(ITERS/8)*CH, T);
+  run("VOTE.ANY (+ISETP/SEL)", [](Rec* r, uint32_t* o){ k_vote<<<148,512>>>(r,o,1.f); }, d_r, d_o, nsm, (double)ITERS*CH, T);
   // inner loop: report pairs/clk/SM (laneops = pairs)
   const int NP = 1024;
   float* d_p; cudaMalloc(&d_p, NP*8*4);
