@@ -352,6 +352,7 @@ def main():
     for _ in range(max(3, args.warmup)):
         res = step.call(*step.dev)
     ctx.profile_read()  # discard warm-up profile
+    ctx.profile_clock()
     barrier()
     clocks.mark()
     launches0 = ctx.launch_count
@@ -372,6 +373,9 @@ def main():
     launches = ctx.launch_count - launches0
     kern_ms, kern_launches, kern_pairs = ctx.profile_read()
     clk = clocks.stop()
+    if args.method in ("exact", "significance"):
+        # the SM clock the count kernel actually ran at (one clock64 / %globaltimer probe per CTA)
+        clk["sm_mhz_in_kernel"] = round(ctx.profile_clock(), 1)
     total_ms = max_over_ranks(float(sum(step_ms)))
     value = args.steps * step.units / (total_ms / 1e3)
 

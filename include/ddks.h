@@ -202,6 +202,11 @@ DDKS_API int32_t ddks_kd_levels(const ddks_ctx* ctx);
  * permutations it serves); any pointer may be NULL. */
 DDKS_API ddks_status ddks_profile_read(ddks_ctx* ctx, double* count_ms, int64_t* launches, uint64_t* pairs);
 
+/* In-kernel clock probe (context created with DDKS_FLAG_PROFILE): one lane per count-kernel CTA reads clock64 and
+ * %globaltimer around its classify+count loop; *sm_mhz = summed SM cycles / summed ns over those CTAs since the last
+ * read (0 if none), i.e. the SM clock the counting actually ran at. Resets the totals. */
+DDKS_API ddks_status ddks_profile_clock(ddks_ctx* ctx, double* sm_mhz);
+
 /* Destroy a context (NULL-safe). Frees workspace and the NCCL communicator. */
 DDKS_API ddks_status ddks_destroy(ddks_ctx* ctx);
 

@@ -36,6 +36,7 @@ struct ddks_ctx {
     DevBuf rd_keys, rd_xn, rd_k0, rd_k1, rd_hist, rd_tcnt, rd_cnum;              // ddks_rdks workspace
     DevBuf x0_keys0, x0_keys1, x0_hist, x0_pts, x0_perm, x0_pts2, x0_perm2, x0_boxes;  // kd-ordered count workspace
     DevBuf rdb_cnt, rdb_pst, rdb_coff, rdb_fill, rdb_clist, rdb_csum;            // rdKS bucket-pruned sweep
+    DevBuf prof_clk;  // [2] u64: SM cycles, globaltimer ns summed over count CTAs (DDKS_FLAG_PROFILE)
     void* host_pinned = nullptr;  // DevResult + scratch
     size_t host_pinned_bytes = 0;
     int64_t launches = 0;
@@ -47,6 +48,7 @@ struct ddks_ctx {
     double prof_ms = 0.0;
     int64_t prof_launches = 0;
     uint64_t prof_pairs = 0;
+    double prof_cycles = 0.0, prof_ns = 0.0;  // in-kernel clock probe totals since the last ddks_profile_clock
 };
 
 extern thread_local std::string g_create_err;

@@ -185,6 +185,7 @@ struct CountArgs {
     unsigned long long* hist;  // SPLIT only, or nullptr: hist[item * hist_stride + c_Q] += 1 for every (origin,
                                // orthant) cell (the M_T histogram of the analytic significance, ddks_significance.cuh)
     int64_t hist_stride;       // n_Q + 1 (one histogram per batch item)
+    unsigned long long* clk = nullptr;  // profiling: += SM cycles and globaltimer ns of every CTA's count loop
 };
 
 // decode the two signed 16-bit halves of a counter word (value = lo + 65536 * hi, both in int16 range)
@@ -446,6 +447,10 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
         for (int k = 0; k < 2 * KX; ++k) bnext[k] = __ldg(a.boxes + (int64_t)(seg0 / TILE) * 2 * KX + k);
     }
 
+    // in-kernel clock probe (one lane per CTA, profiling only): the SM clock this launch actually ran at
+    unsigned long long clk0 = 0, ns0 = 0;
+    if (a.clk && t == 0) clk0 = clock64(), ns0 = globaltimer_ns();
+
     for (int it = 0; it < n_tiles; ++it) {
         const int s = it % S;
         mbar_wait(&bars[s], (uint32_t)((it / S) & 1));
@@ -498,6 +503,10 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
         }
     }
     __syncthreads();  // all red.shared retired before reading the counters
+    if (a.clk && t == 0) {
+        atomicAdd(&a.clk[0], (unsigned long long)(clock64() - clk0));
+        atomicAdd(&a.clk[1], globaltimer_ns() - ns0);
+    }
 
     if (a.accum != nullptr) {
         // flush: exact int32 partial counters -> global (red.global.add), finalised by k_finalize

@@ -97,6 +97,12 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
             CU(cudaEventCreate(&ev.second));
         }
         CU(cudaEventRecord(ev.first, st));
+        if (!ctx->prof_clk.p) {
+            ddks_status s = ensure(ctx, ctx->prof_clk, 16);
+            if (s) return s;
+            CU(cudaMemset(ctx->prof_clk.p, 0, 16));
+        }
+        a.clk = (unsigned long long*)ctx->prof_clk.p;
     }
     kern<<<grid, G::T, G::SMEM_BYTES, st>>>(a);
     CHECK_LAUNCH();

@@ -92,6 +92,7 @@ def _load() -> ctypes.CDLL:
         "ddks_shard_range": ([i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)], ctypes.c_int),
         "ddks_launch_count": ([vp], i64),
         "ddks_kd_levels": ([vp], i32),
+        "ddks_profile_clock": ([vp, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
         "ddks_profile_read": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_uint64)],
                               ctypes.c_int),
         "ddks_destroy": ([vp], ctypes.c_int),
@@ -107,7 +108,7 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 EXPORTED = ("ddks_get_nccl_id", "ddks_create", "ddks_stat", "ddks_stat_batch", "ddks_permutation_null",
-            "ddks_stat_per_origin", "ddks_stat_shard", "ddks_significance", "ddks_significance_batch", "ddks_vdks", "ddks_rdks", "ddks_shard_range", "ddks_launch_count", "ddks_kd_levels", "ddks_profile_read", "ddks_destroy",
+            "ddks_stat_per_origin", "ddks_stat_shard", "ddks_significance", "ddks_significance_batch", "ddks_vdks", "ddks_rdks", "ddks_shard_range", "ddks_launch_count", "ddks_kd_levels", "ddks_profile_clock", "ddks_profile_read", "ddks_destroy",
             "ddks_last_error", "ddks_version")
 
 
@@ -315,6 +316,13 @@ def ddks_launch_count(ctx) -> int:
     return int(LIB.ddks_launch_count(ctx))
 
 
+def ddks_profile_clock(ctx) -> float:
+    """Mean SM MHz of the count kernels' CTAs since the last read (in-kernel clock64 / globaltimer probe)."""
+    v = ctypes.c_double()
+    _check(LIB.ddks_profile_clock(ctx, ctypes.byref(v)), ctx)
+    return float(v.value)
+
+
 def ddks_kd_levels(ctx) -> int:
     """Levels of the kd ordering used by the last count (0: position order)."""
     return int(LIB.ddks_kd_levels(ctx))
@@ -367,6 +375,9 @@ class Context:
     @property
     def launch_count(self) -> int:
         return ddks_launch_count(self.ctx)
+
+    def profile_clock(self) -> float:
+        return ddks_profile_clock(self.ctx)
 
     @property
     def kd_levels(self) -> int:

@@ -434,3 +434,16 @@ def test_shard_rehearsal_combines_to_the_statistic(flags, n_P, n_Q, d):
             num = max(p.num for p in parts)
             arg = min(p.argmax_origin for p in parts if p.num == num)
             assert (num, arg) == (want[0], want[3]), (world, parts)
+
+
+def test_profile_clock_probe():
+    # DDKS_FLAG_PROFILE: the count kernel's per-CTA clock64 / %globaltimer probe yields the SM clock it ran at
+    P, Q = I.random_pair(77, 20000, 20000, 5, "normal")
+    with K.Context(flags=K.DDKS_FLAG_PROFILE) as c:
+        c.stat(dev(P), dev(Q))
+        mhz = c.profile_clock()
+        assert 300.0 < mhz < 3000.0, mhz
+        assert c.profile_clock() == 0.0  # reset by the read
+    with K.Context() as c:
+        c.stat(dev(P), dev(Q))
+        assert c.profile_clock() == 0.0  # no probe without the flag
