@@ -415,7 +415,20 @@ def main():
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp) and args.method == "exact":
         try:
-            traffic = json.load(open(tp)).get(args.workload)
+            tj = json.load(open(tp))
+            traffic = tj.get(args.workload)
+            ipp = tj.get(f"{args.workload}_detail", {}).get("per_pair", {}).get("thread_instructions")
+            if ipp and kern_ms:
+                # issue-side view of the same kernel: live pair rate x ncu-measured instructions per pair vs the SM
+                # issue peak (4 warp-instructions / clk / SM)
+                sm_max = float(pk.get("sm_max_mhz", 1965.0))
+                rate = kern_pairs / (kern_ms / 1e3)
+                ach = rate * ipp / 32.0
+                peak_i = N_SM * 4 * sm_max * 1e6
+                roof["issue"] = {"instr_per_pair": round(ipp, 3), "achieved_warp_inst_per_s": ach,
+                                 "peak_warp_inst_per_s": peak_i, "frac": ach / peak_i,
+                                 "source": "thread instructions per pair from ncu smsp__inst_executed.sum of one "
+                                           "full-size launch (profiles/traffic.json); pair rate measured live"}
         except Exception:
             traffic = None
     roof = dict({k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac")}, traffic=traffic,

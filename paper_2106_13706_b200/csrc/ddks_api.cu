@@ -1,6 +1,6 @@
 // ddks_api.cu — host side of libddks.so: the C ABI declared in include/ddks.h.
 //
-// Context = device + grow-only workspace + (world > 1) an NCCL communicator (NCCL 2.28.9, the copy torch
+// Context = device + grow-only workspace + (world > 1, or the NCCL_SELF test flag) an NCCL communicator (NCCL 2.28.9, the copy torch
 // bundles). Each public call: argument checks -> optional H2D of host inputs -> k_pack (validate + pack) ->
 // k_count (classify + count + per-origin max) [-> k_finalize] -> k_argmax -> NCCL combine -> one D2H -> sync.
 #include <cuda_runtime.h>
@@ -216,7 +216,7 @@ ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n
         // SPLIT counters when the significance needs c_Q or DIFF counters would overflow (as in run_count)
         const bool sp = split || !diff_counters_ok(n_P, n_Q);
         if ((s = run_count_kd(ctx, packed, d, n_P, n_Q, sw, sr, (uint64_t*)&dres->num, per, st, sp, hist))) return s;
-        if (ctx->world > 1) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
+        if (ctx->comm) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
         ddks::k_argmax<<<(int)std::min<int64_t>((N + 255) / 256, 148 * 4), 256, 0, st>>>(
             per, N, 0, (const uint64_t*)&dres->num, &dres->arg);
         CHECK_LAUNCH();
@@ -230,7 +230,7 @@ ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n
     if (oe > ob && (s = run_count(ctx, packed, d, 1, n_P, n_Q, ob, oe, (uint64_t*)&dres->num, per, st, split, hist)))
         return s;
     if (export_per) return DDKS_OK;
-    if (ctx->world > 1) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
+    if (ctx->comm) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
     if (oe > ob) {
         ddks::k_argmax<<<(int)std::min<int64_t>((oe - ob + 255) / 256, 148 * 4), 256, 0, st>>>(
             per, oe - ob, ob, (const uint64_t*)&dres->num, &dres->arg);
@@ -421,7 +421,7 @@ ddks_status ddks_create(ddks_ctx** out, int device, int world, int rank, const v
     if (world < 1 || rank < 0 || rank >= world) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad world/rank");
     if ((world == 1) != (nccl_id == nullptr))
         return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "nccl_id must be NULL iff world == 1");
-    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT | DDKS_FLAG_PROFILE | DDKS_FLAG_PERM_GATHER | DDKS_FLAG_NO_X0 | DDKS_FLAG_FORCE_X0 | DDKS_FLAG_RDKS_FULL_SORT | DDKS_FLAG_KD_LEVELS(3))) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
+    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT | DDKS_FLAG_PROFILE | DDKS_FLAG_PERM_GATHER | DDKS_FLAG_NO_X0 | DDKS_FLAG_FORCE_X0 | DDKS_FLAG_RDKS_FULL_SORT | DDKS_FLAG_KD_LEVELS(3) | DDKS_FLAG_NCCL_SELF)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
     int ndev = 0;
     CU(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device %d of %d", device, ndev);
@@ -431,9 +431,20 @@ ddks_status ddks_create(ddks_ctx** out, int device, int world, int rank, const v
     ctx->world = world;
     ctx->rank = rank;
     ctx->flags = flags;
-    if (world > 1) {
+    if (world > 1 || (flags & DDKS_FLAG_NCCL_SELF)) {
+        // world > 1: the harness's id; NCCL_SELF (tests): a one-rank communicator of our own, so every collective
+        // of the multi-GPU path runs through NCCL on a single device
         ncclUniqueId id;
-        memcpy(&id, nccl_id, sizeof id);
+        if (world > 1) {
+            memcpy(&id, nccl_id, sizeof id);
+        } else {
+            ncclResult_t g = ncclGetUniqueId(&id);
+            if (g != ncclSuccess) {
+                fail(nullptr, DDKS_ERR_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(g));
+                delete ctx;
+                return DDKS_ERR_NCCL;
+            }
+        }
         ncclResult_t r = ncclCommInitRank(&ctx->comm, world, id, rank);
         if (r != ncclSuccess) {
             fail(nullptr, DDKS_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
@@ -541,7 +552,7 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
     uint64_t* per = nullptr;
     const int sw = shard_world > 0 ? shard_world : ctx->world, sr = shard_world > 0 ? shard_rank : ctx->rank;
     if ((s = count_statistic(ctx, packed, d, n_P, n_Q, ob, oe, sw, sr, dres, export_mode, false, nullptr, st, &per))) return s;
-    if (ctx->world > 1 && !export_mode) {
+    if (ctx->comm && !export_mode) {
         NC(ncclAllReduce(&dres->arg, &dres->arg, 1, ncclUint64, ncclMin, ctx->comm, st));
         NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
     }
@@ -621,7 +632,7 @@ ddks_status ddks_stat_batch(ddks_ctx* ctx, const float* P, const float* Q, int64
             return s;
         if ((s = run_count(ctx, packed, d, nb, n_P, n_Q, 0, N, nums + ib, nullptr, st))) return s;
     }
-    if (ctx->world > 1) {
+    if (ctx->comm) {
         if ((s = all_gather_items(ctx, nums, B, st))) return s;
         NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
     }
@@ -704,7 +715,7 @@ ddks_status ddks_permutation_null(ddks_ctx* ctx, const float* pooled, int64_t n_
                 return s;
         }
     }
-    if (ctx->world > 1) {
+    if (ctx->comm) {
         if ((s = all_gather_items(ctx, nums + 1, n_perm, st))) return s;
         NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
     }

@@ -135,7 +135,7 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
         CU(cudaMemcpyAsync(hc, cnum, (size_t)nc * 8, cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
     }
-    if (ctx->world > 1) {
+    if (ctx->comm) {
         NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
         CU(cudaMemcpyAsync(&hres->flag, &dres->flag, 4, cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
@@ -144,7 +144,7 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     uint64_t best = 0;
     for (int c = 0; c < nc; ++c) best = std::max<uint64_t>(best, hc[c]);
     uint64_t arg = ~0ull;
-    if (ctx->world > 1) {
+    if (ctx->comm) {
         hres->num = best;
         CU(cudaMemcpyAsync(&dres->num, &hres->num, 8, cudaMemcpyHostToDevice, st));
         NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
@@ -154,7 +154,7 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     }
     for (int c = 0; c < nc; ++c)
         if (hc[c] == best) { arg = (uint64_t)(cb + c); break; }
-    if (ctx->world > 1) {
+    if (ctx->comm) {
         hres->arg = arg;
         CU(cudaMemcpyAsync(&dres->arg, &hres->arg, 8, cudaMemcpyHostToDevice, st));
         NC(ncclAllReduce(&dres->arg, &dres->arg, 1, ncclUint64, ncclMin, ctx->comm, st));

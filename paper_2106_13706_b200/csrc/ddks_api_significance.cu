@@ -63,7 +63,7 @@ ddks_status ddks_significance(ddks_ctx* ctx, const float* P, int64_t n_P, const 
     if ((s = launch_pack(ctx, (const float*)dP, n_P, (const float*)dQ, n_Q, d, 1, packed, &dres->flag, st))) return s;
     uint64_t* per = nullptr;
     if ((s = count_statistic(ctx, packed, d, n_P, n_Q, ob, oe, ctx->world, ctx->rank, dres, false, true, hist, st, &per))) return s;
-    if (ctx->world > 1) {
+    if (ctx->comm) {
         NC(ncclAllReduce(&dres->arg, &dres->arg, 1, ncclUint64, ncclMin, ctx->comm, st));
         NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
         NC(ncclAllReduce(hist, hist, (size_t)nm, ncclUint64, ncclSum, ctx->comm, st));
@@ -108,7 +108,7 @@ ddks_status ddks_significance(ddks_ctx* ctx, const float* P, int64_t n_P, const 
         ddks::k_sig_sum<<<1, ddks::SIG_T, 0, st>>>(contrib, mb, me, part);
         CHECK_LAUNCH();
         ctx->launches++;
-        if (ctx->world > 1) {
+        if (ctx->comm) {
             NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
             NC(ncclAllGather(part, part + 1, 1, ncclFloat64, ctx->comm, st));
         } else {
@@ -131,7 +131,7 @@ ddks_status ddks_significance(ddks_ctx* ctx, const float* P, int64_t n_P, const 
         CU(cudaMemcpyAsync(mt_hist, hist, (size_t)nm * 8, cudaMemcpyDefault, st));
     }
     if (log_p_table) {
-        if (ctx->world > 1) NC(ncclAllReduce(table, table, (size_t)nm, ncclFloat64, ncclSum, ctx->comm, st));
+        if (ctx->comm) NC(ncclAllReduce(table, table, (size_t)nm, ncclFloat64, ncclSum, ctx->comm, st));
         CU(cudaMemcpyAsync(log_p_table, table, (size_t)nm * 8, cudaMemcpyDefault, st));
     }
     CU(cudaStreamSynchronize(st));
@@ -234,7 +234,7 @@ ddks_status ddks_significance_batch(ddks_ctx* ctx, const float* P, const float* 
             CU(cudaMemsetAsync(&dres->flag, 0, 4, st));
         }
     }
-    if (ctx->world > 1) {
+    if (ctx->comm) {
         if ((s = all_gather_items(ctx, nums, B, st))) return s;
         if ((s = all_gather_items(ctx, (uint64_t*)parts, B, st))) return s;
         NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));

@@ -63,7 +63,7 @@ ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
         CHECK_LAUNCH();
         ctx->launches++;
     }
-    if (ctx->world > 1) {
+    if (ctx->comm) {
         NC(ncclAllReduce(keys, keys, 8, ncclUint32, ncclMin, ctx->comm, st));
         NC(ncclAllReduce(keys + 8, keys + 8, 8, ncclUint32, ncclMax, ctx->comm, st));
     }
@@ -72,7 +72,7 @@ ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
         CHECK_LAUNCH();
         ctx->launches++;
     }
-    if (ctx->world > 1) {
+    if (ctx->comm) {
         NC(ncclAllReduce(cnt, cnt, (size_t)V * 2, ncclUint32, ncclSum, ctx->comm, st));
         NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
     }
@@ -100,7 +100,7 @@ ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
         CHECK_LAUNCH();
         ctx->launches++;
     }
-    if (ctx->world > 1) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
+    if (ctx->comm) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
     CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");

@@ -29,6 +29,7 @@ DDKS_FLAG_NO_X0 = 32
 DDKS_FLAG_FORCE_X0 = 64
 DDKS_FLAG_RDKS_FULL_SORT = 128
 DDKS_FLAG_KD_SHIFT = 9
+DDKS_FLAG_NCCL_SELF = 2048
 
 
 def DDKS_FLAG_KD_LEVELS(k: int) -> int:
