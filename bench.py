@@ -284,18 +284,20 @@ class Step:
         N = self.N
         if self.args.method == "vdks":
             V = self.args.vdks_k ** d
-            # input read + pack write/read, voxel counts, diff, d prefix passes (read + write), one read in the
-            # orthant pass (DESIGN.md §7 vdKS)
-            byts = N * d * 4 + 2 * N * (4 if d <= 4 else 8) * 4 + V * 8 * 2 + V * 8 + 2 * d * V * 8 + V * 8
+            # input read twice in place (min/max, voxelise), voxel counts (zero + read), d prefix passes over the
+            # int64 sums (read + write; the first reads the counts), one read of counts and sums in the orthant pass
+            # (DESIGN.md §7 vdKS)
+            byts = 2 * N * d * 4 + 2 * V * 8 + 2 * d * V * 8 + 2 * V * 8
             what = "whole vdKS step (pack, voxel histogram, prefix passes, orthant sums)"
         else:
             keys = (d + 1) * N * 8
             nbk = 256
             while nbk < N // 4 and nbk < (1 << 20):
                 nbk <<= 1
-            # input read, f64 x' write + read, key write, two key reads (bucket count, candidate compaction), and per
-            # bucket: count atomics, two scan reads, start-count write, candidate read + offset write
-            byts = N * d * 4 + 2 * N * d * 8 + 3 * keys + (d + 1) * nbk * 52
+            # input read twice in place (min/max; distance keys with NormalizeData fused), key write, one key read
+            # (candidate compaction), and per bucket: count atomics, two scan reads, start-count write, candidate
+            # read + offset write
+            byts = 2 * N * d * 4 + 2 * keys + (d + 1) * nbk * 52
             what = "whole rdKS step (normalise, distance keys, bucket-pruned sweep)"
         achieved = byts / (step_ms / 1e3) / 1e9
         peak = float(peaks_.get("hbm_gbs", 6536.7))

@@ -40,14 +40,12 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     const int nc = (int)(ce - cb);
     const int tiles = (int)((N + ddks::RS_TILE - 1) / ddks::RS_TILE);
     if ((s = ensure(ctx, ctx->rd_keys, (size_t)2 * d * 4))) return s;
-    if ((s = ensure(ctx, ctx->rd_xn, (size_t)N * d * 8))) return s;
     if ((s = ensure(ctx, ctx->rd_k0, (size_t)std::max(nc, 1) * N * 8))) return s;
     if ((s = ensure(ctx, ctx->rd_k1, (size_t)std::max(nc, 1) * N * 8))) return s;
     if ((s = ensure(ctx, ctx->rd_hist, (size_t)std::max(nc, 1) * tiles * 256 * 4))) return s;
     if ((s = ensure(ctx, ctx->rd_tcnt, (size_t)std::max(nc, 1) * tiles * 4))) return s;
     if ((s = ensure(ctx, ctx->rd_cnum, (size_t)(d + 1) * 8))) return s;
     uint32_t* keys = (uint32_t*)ctx->rd_keys.p;
-    double* xn = (double*)ctx->rd_xn.p;
     uint64_t* k0 = (uint64_t*)ctx->rd_k0.p;
     uint64_t* k1 = (uint64_t*)ctx->rd_k1.p;
     uint32_t* hist = (uint32_t*)ctx->rd_hist.p;
@@ -65,9 +63,17 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     CHECK_LAUNCH();
     ctx->launches++;
     auto grid_for = [](int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); };
-    ddks::k_rd_normalize<<<grid_for(N * d), 256, 0, st>>>((const float*)dP, n_P, (const float*)dQ, n_Q, d, keys, xn);
-    CHECK_LAUNCH();
-    ctx->launches++;
+    // small d: NormalizeData is fused into the key kernel (x' recomputed per corner, no N x d f64 round trip);
+    // large d (the paper's d = 1000 shape): normalise once, the key kernel reads x'
+    const double* xn = nullptr;
+    if (d > 16 && nc > 0) {
+        if ((s = ensure(ctx, ctx->rd_xn, (size_t)N * d * 8))) return s;
+        ddks::k_rd_normalize<<<grid_for(N * d), 256, 0, st>>>((const float*)dP, n_P, (const float*)dQ, n_Q, d, keys,
+                                                              (double*)ctx->rd_xn.p);
+        CHECK_LAUNCH();
+        ctx->launches++;
+        xn = (const double*)ctx->rd_xn.p;
+    }
     // full path: segmented 8-pass LSD radix sort of every corner's keys, then the tie-complete sweep
     auto full_sort = [&]() -> ddks_status {
         const int blocks = nc * tiles;
@@ -83,10 +89,13 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     };
     const bool pruned = !(ctx->flags & DDKS_FLAG_RDKS_FULL_SORT);
     if (nc > 0) {
-        ddks::k_rd_keys<<<grid_for(N * nc), 256, 0, st>>>(xn, N, n_P, d, (int)cb, (int)ce, k0);
-        CHECK_LAUNCH();
-        ctx->launches++;
-        if (pruned) {
+        if (!pruned) {
+            ddks::k_rd_keys<<<grid_for(N * nc), 256, 0, st>>>((const float*)dP, (const float*)dQ, xn, N, n_P, d, keys,
+                                                              (int)cb, (int)ce, k0, nullptr, 0, 0.0);
+            CHECK_LAUNCH();
+            ctx->launches++;
+            if ((s = full_sort())) return s;
+        } else {
             // bucket-pruned sweep: bucket counts, exact bucket-end values, sort only the buckets that can beat them
             int nbk = 256;
             while (nbk < N / 4 && nbk < (1 << 20)) nbk <<= 1;
@@ -102,7 +111,9 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
             int32_t* clist = (int32_t*)ctx->rdb_clist.p;
             CU(cudaMemsetAsync(bcnt, 0, nb * 8, st));
             CU(cudaMemsetAsync(ctx->rdb_fill.p, 0, nb * 4, st));
-            ddks::k_rdb_count<<<grid_for(N * nc), 256, 0, st>>>(k0, N, nc, nbk, scale, bcnt);
+            // distance keys and their bucket counts in one pass (NormalizeData fused)
+            ddks::k_rd_keys<<<grid_for(N * nc), 256, 0, st>>>((const float*)dP, (const float*)dQ, xn, N, n_P, d, keys,
+                                                              (int)cb, (int)ce, k0, bcnt, nbk, scale);
             const int nch = (nbk + ddks::RDB_CH - 1) / ddks::RDB_CH;
             uint64_t* csum = (uint64_t*)ctx->rdb_csum.p;
             uint32_t* segc = (uint32_t*)(csum + (size_t)nc * nch);
@@ -120,8 +131,6 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
                 n_Q, cnum, &dres->flag);
             CHECK_LAUNCH();
             ctx->launches += 7;
-        } else if ((s = full_sort())) {
-            return s;
         }
     }
     if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)(d + 1) * 8))) return s;

@@ -33,11 +33,9 @@ ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     if ((s = bind_device(ctx))) return s;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t N = n_P + n_Q;
-    const int DP = pad_dim(d);
     const void *dP, *dQ;
     if ((s = stage_input(ctx, P, (size_t)n_P * d * 4, ctx->raw_a, st, &dP))) return s;
     if ((s = stage_input(ctx, Q, (size_t)n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
-    if ((s = ensure(ctx, ctx->packed, (size_t)N * DP * 4))) return s;
     if ((s = ensure(ctx, ctx->vox_keys, 16 * 4))) return s;
     if ((s = ensure(ctx, ctx->vox_cnt, (size_t)V * 8))) return s;
     if ((s = ensure(ctx, ctx->vox_S, (size_t)V * 8))) return s;
@@ -51,15 +49,15 @@ ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     CU(cudaMemsetAsync(keys, 0xff, 8 * 4, st));
     CU(cudaMemsetAsync(keys + 8, 0, 8 * 4, st));
     CU(cudaMemsetAsync(cnt, 0, (size_t)V * 8, st));
-    float* packed = (float*)ctx->packed.p;
-    if ((s = launch_pack(ctx, (const float*)dP, n_P, (const float*)dQ, n_Q, d, 1, packed, &dres->flag, st))) return s;
+    // the points are read in place (no pack): k_minmax validates them and k_vox_hist voxelises them
     int64_t pb, pe;
     ddks_shard_range(N, ctx->world, ctx->rank, &pb, &pe);
     const int blk = 256;
     auto grid_for = [](int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); };
     if (pe > pb) {
-        ddks::k_minmax<<<(int)std::max<int64_t>(1, std::min<int64_t>((pe - pb + 1023) / 1024, 148 * 2)), blk, 0, st>>>(
-            packed + pb * DP, pe - pb, d, DP, keys);
+        ddks::k_minmax<<<(int)std::max<int64_t>(1, std::min<int64_t>((pe - pb + 255) / 256, 148 * 8)), blk, 0, st>>>(
+            (const float*)dP, (const float*)dQ, n_P, pb, pe, d, keys, !(ctx->flags & DDKS_FLAG_NO_VALIDATE),
+            &dres->flag);
         CHECK_LAUNCH();
         ctx->launches++;
     }
@@ -68,7 +66,8 @@ ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
         NC(ncclAllReduce(keys + 8, keys + 8, 8, ncclUint32, ncclMax, ctx->comm, st));
     }
     if (pe > pb) {
-        ddks::k_vox_hist<<<grid_for(pe - pb), blk, 0, st>>>(packed, pb, pe, n_P, d, DP, keys, k, cnt);
+        ddks::k_vox_hist<<<grid_for(pe - pb), blk, 0, st>>>((const float*)dP, (const float*)dQ, pb, pe, n_P, d, keys,
+                                                            k, cnt);
         CHECK_LAUNCH();
         ctx->launches++;
     }
@@ -78,7 +77,11 @@ ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     }
     int64_t stride = 1;
     for (int m = 0; m < d; ++m, stride *= k) {
-        ddks::k_prefix_line<<<grid_for(V / k), blk, 0, st>>>(S, V, k, stride, m == 0 ? cnt : nullptr, n_P, n_Q);
+        if (m == 0 && k <= 32 && (k & (k - 1)) == 0) {  // coalesced segmented warp scan of the k-voxel lines
+            ddks::k_prefix_first<<<grid_for(V), blk, 0, st>>>(S, V, (int)k, cnt, n_P, n_Q);
+        } else {
+            ddks::k_prefix_line<<<grid_for(V / k), blk, 0, st>>>(S, V, k, stride, m == 0 ? cnt : nullptr, n_P, n_Q);
+        }
         CHECK_LAUNCH();
         ctx->launches++;
     }

@@ -56,38 +56,52 @@ __global__ void __launch_bounds__(256) k_rd_minmax(const float* __restrict__ P, 
     if (bad) atomicOr(flag, 1u);
 }
 
-// xn[i][m] = (x - min_m) / (max_m - min_m) in f64 (0.5 for a constant dimension), pooled order P then Q.
+// x'_m = (x_m - min_m) / (max_m - min_m) in f64 (0.5 for a constant dimension; NormalizeData), read in place
+__device__ __forceinline__ double rd_norm(const float* row, int m, const uint32_t* __restrict__ keys, int d) {
+    const double mn = (double)key_f32(keys[m]);
+    const double rng = __dsub_rn((double)key_f32(keys[d + m]), mn);
+    return rng > 0.0 ? __ddiv_rn(__dsub_rn((double)row[m], mn), rng) : 0.5;
+}
+
+__device__ __forceinline__ int rdb_bucket(uint64_t key, double scale, int nbk);
+
+// xn[i][m] = x'_im for every pooled row (large d: normalise once instead of once per corner)
 __global__ void k_rd_normalize(const float* __restrict__ P, int64_t n_P, const float* __restrict__ Q, int64_t n_Q,
                                int d, const uint32_t* __restrict__ keys, double* __restrict__ xn) {
     const int64_t total = (n_P + n_Q) * d;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e / d;
         const int m = (int)(e - i * d);
-        const float x = i < n_P ? P[e] : Q[e - n_P * d];
-        const double mn = (double)key_f32(keys[m]);
-        const double rng = __dsub_rn((double)key_f32(keys[d + m]), mn);
-        xn[e] = rng > 0.0 ? __ddiv_rn(__dsub_rn((double)x, mn), rng) : 0.5;
+        xn[e] = rd_norm(i < n_P ? P + i * d : Q + (i - n_P) * d, m, keys, d);
     }
 }
 
 // key[c][i] = bits(|x'_i - corner_c|) << 1 | (i >= n_P) for corners c in [c_begin, c_end); corner 0 = origin,
-// corner c >= 1 = unit vector e_{c-1}. Threads: corner fastest, so the threads of one point share its row.
-__global__ void k_rd_keys(const double* __restrict__ xn, int64_t N, int64_t n_P, int d, int c_begin, int c_end,
-                          uint64_t* __restrict__ key) {
+// corner c >= 1 = unit vector e_{c-1}. x' comes from xn when given (large d), else it is formed on the fly from the
+// caller's rows (same f64 _rn arithmetic as the oracle either way, so the keys are bit-identical). Threads: corner
+// fastest, so the threads of one point share its row.
+// cnt != nullptr (bucket-pruned sweep): also counts the key into its distance bucket, cnt[(c * nbk + b) * 2 + label].
+__global__ void k_rd_keys(const float* __restrict__ P, const float* __restrict__ Q, const double* __restrict__ xn,
+                          int64_t N, int64_t n_P, int d,
+                          const uint32_t* __restrict__ keys, int c_begin, int c_end, uint64_t* __restrict__ key,
+                          uint32_t* __restrict__ cnt, int nbk, double scale) {
     const int nc = c_end - c_begin;
     const int64_t total = N * nc;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e / nc;
         const int c = (int)(e - i * nc) + c_begin;
-        const double* row = xn + i * d;
+        const float* row = i < n_P ? P + i * d : Q + (i - n_P) * d;
         double s = 0.0;
-#pragma unroll 8
+#pragma unroll 4
         for (int m = 0; m < d; ++m) {
-            const double t = __dsub_rn(row[m], (c >= 1 && m == c - 1) ? 1.0 : 0.0);
+            const double xm = xn ? xn[i * d + m] : rd_norm(row, m, keys, d);
+            const double t = __dsub_rn(xm, (c >= 1 && m == c - 1) ? 1.0 : 0.0);
             s = __dadd_rn(s, __dmul_rn(t, t));
         }
         const double dist = __dsqrt_rn(s);
-        key[(int64_t)(c - c_begin) * N + i] = ((uint64_t)__double_as_longlong(dist) << 1) | (uint64_t)(i >= n_P);
+        const uint64_t k = ((uint64_t)__double_as_longlong(dist) << 1) | (uint64_t)(i >= n_P);
+        key[(int64_t)(c - c_begin) * N + i] = k;
+        if (cnt) atomicAdd(&cnt[2 * ((int64_t)(c - c_begin) * nbk + rdb_bucket(k, scale, nbk)) + (k & 1ull)], 1u);
     }
 }
 
@@ -183,17 +197,6 @@ __device__ __forceinline__ int rdb_bucket(uint64_t key, double scale, int nbk) {
     const double v = __dmul_rn(dist, scale);
     const int b = v >= (double)(nbk - 1) ? nbk - 1 : (int)v;
     return b < 0 ? 0 : b;
-}
-
-// cnt[(s * nbk + b) * 2 + label] += 1
-__global__ void k_rdb_count(const uint64_t* __restrict__ key, int64_t N, int nseg, int nbk, double scale,
-                            uint32_t* __restrict__ cnt) {
-    const int64_t total = N * nseg;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t s = e / N;
-        const uint64_t k = key[e];
-        atomicAdd(&cnt[2 * (s * nbk + rdb_bucket(k, scale, nbk)) + (k & 1ull)], 1u);
-    }
 }
 
 // Bucket prefix sums, many CTAs: a chunk is RDB_CH consecutive buckets of one segment (256 threads x 4 buckets).

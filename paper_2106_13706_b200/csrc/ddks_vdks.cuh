@@ -24,22 +24,36 @@
 
 namespace ddks {
 
-// keys[0..d) = min keys (init 0xffffffff), keys[8..8+d) = max keys (init 0). pts: packed [N][DP].
+// Row i of the pooled set, read in place from the caller's arrays (P rows, then Q rows; row-major [n][d] f32).
+__device__ __forceinline__ const float* pooled_row(const float* P, const float* Q, int64_t n_P, int d, int64_t i) {
+    return i < n_P ? P + i * d : Q + (i - n_P) * d;
+}
+
+// keys[0..d) = min keys (init 0xffffffff), keys[8..8+d) = max keys (init 0) over pooled rows [i_begin, i_end), read
+// in place (no pack); -0 counts as +0. validate: a non-finite coordinate sets *flag |= 1 (SPEC NonFiniteValue).
 // Grid-stride per thread, block reduction in SMEM, one atomic pair per (block, dimension).
-__global__ void __launch_bounds__(256) k_minmax(const float* __restrict__ pts, int64_t n, int d, int DP, uint32_t* keys) {
+__global__ void __launch_bounds__(256) k_minmax(const float* __restrict__ P, const float* __restrict__ Q, int64_t n_P,
+                                                int64_t i_begin, int64_t i_end, int d, uint32_t* keys, int validate,
+                                                uint32_t* flag) {
     __shared__ uint32_t sa[8][8], sb[8][8];
     uint32_t mn[8], mx[8];
+    bool bad = false;
 #pragma unroll
     for (int m = 0; m < 8; ++m) mn[m] = 0xffffffffu, mx[m] = 0u;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = i_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < i_end;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float* x = pooled_row(P, Q, n_P, d, i);
 #pragma unroll
         for (int m = 0; m < 8; ++m)
             if (m < d) {
-                const uint32_t k = f32_key(pts[i * DP + m]);
+                const float v = x[m];
+                if (validate && !isfinite(v)) bad = true;
+                const uint32_t k = f32_key(v == 0.0f ? 0.0f : v);
                 mn[m] = k < mn[m] ? k : mn[m];
                 mx[m] = k > mx[m] ? k : mx[m];
             }
     }
+    if (bad) atomicOr(flag, 1u);
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
         uint32_t a = mn[m], b = mx[m];
@@ -73,9 +87,9 @@ __device__ __forceinline__ int64_t voxel_of(const float* x, int d, const double*
     return flat;
 }
 
-// cnt[2 v] = # P points in voxel v, cnt[2 v + 1] = # Q points. Points [p_begin, p_end) of the pooled packed set.
-__global__ void k_vox_hist(const float* __restrict__ pts, int64_t p_begin, int64_t p_end, int64_t n_P, int d, int DP,
-                           const uint32_t* __restrict__ keys, int64_t k, uint32_t* __restrict__ cnt) {
+// cnt[2 v] = # P points in voxel v, cnt[2 v + 1] = # Q points. Pooled rows [p_begin, p_end), read in place.
+__global__ void k_vox_hist(const float* __restrict__ P, const float* __restrict__ Q, int64_t p_begin, int64_t p_end,
+                           int64_t n_P, int d, const uint32_t* __restrict__ keys, int64_t k, uint32_t* __restrict__ cnt) {
     double mn[8], rng[8];
     for (int m = 0; m < d; ++m) {
         mn[m] = (double)key_f32(keys[m]);
@@ -83,7 +97,7 @@ __global__ void k_vox_hist(const float* __restrict__ pts, int64_t p_begin, int64
     }
     for (int64_t i = p_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p_end;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v = voxel_of(pts + i * DP, d, mn, rng, k);
+        const int64_t v = voxel_of(pooled_row(P, Q, n_P, d, i), d, mn, rng, k);
         atomicAdd(&cnt[2 * v + (i < n_P ? 0 : 1)], 1u);
     }
 }
@@ -113,6 +127,28 @@ __global__ void k_prefix_line(int64_t* __restrict__ S, int64_t V, int64_t k, int
                     S[base + (c0 + j) * stride] = run;
                 }
         }
+    }
+}
+
+// Dimension-0 pass for k in {2, 4, 8, 16, 32}: one thread per voxel (coalesced), S = cQ n_P - cP n_Q scanned along
+// each line of k consecutive voxels by a segmented warp scan (a line is k consecutive lanes; V is a multiple of k).
+__global__ void k_prefix_first(int64_t* __restrict__ S, int64_t V, int k, const uint32_t* __restrict__ cnt,
+                               int64_t n_P, int64_t n_Q) {
+    const int lane = threadIdx.x & 31, pos = lane & (k - 1);
+    for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < V;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = base + lane;
+        int64_t x = 0;
+        if (v < V) {
+            const uint2 c = *reinterpret_cast<const uint2*>(cnt + 2 * v);
+            x = (int64_t)c.y * n_P - (int64_t)c.x * n_Q;
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, x, off);
+            if (off < k && pos >= off) x += y;
+        }
+        if (v < V) S[v] = x;
     }
 }
 

@@ -140,3 +140,20 @@ def test_rdks_pruned_equals_full_sort_and_fallback(ctx):
         want = O.rdks(P, Q)
         got = ctx.rdks(dev(P), dev(Q))
         assert (got.num, got.argmax_origin) == (want[0], want[3]) and got == cf.rdks(dev(P), dev(Q))
+
+
+def test_vdks_validates_in_place(ctx):
+    # vdKS reads the caller's arrays in place (no pack): the min/max pass rejects NaN / Inf and treats -0 as +0
+    P, Q = I.random_pair(61, 500, 400, 3, "normal")
+    for bad in (np.nan, np.inf, -np.inf):
+        Pb = P.copy()
+        Pb[123, 1] = bad
+        with pytest.raises(K.DDKSError) as e:
+            ctx.vdks(dev(Pb), dev(Q), 8)
+        assert e.value.status == 4
+    Pz, Qz = P.copy(), Q.copy()
+    Pz[:50, 0] = -0.0
+    Qz[:50, 0] = 0.0
+    for k in (4, 7, 16):
+        assert ctx.vdks(dev(Pz), dev(Qz), k)[:2] == O.vdks(Pz, Qz, k)[:2]
+        assert ctx.vdks(Pz, Qz, k)[:2] == O.vdks(Pz, Qz, k)[:2]  # host inputs
