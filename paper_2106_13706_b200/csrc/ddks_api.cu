@@ -350,13 +350,6 @@ ddks_status collect_profile(ddks_ctx* ctx) {
     }
     ctx->ev_pending.clear();
     ctx->ev_pairs.clear();
-    if (ctx->prof_clk.p) {  // called after the call's stream sync: the probe totals are final
-        unsigned long long c[2];
-        CU(cudaMemcpy(c, ctx->prof_clk.p, 16, cudaMemcpyDeviceToHost));
-        CU(cudaMemset(ctx->prof_clk.p, 0, 16));
-        ctx->prof_cycles += (double)c[0];
-        ctx->prof_ns += (double)c[1];
-    }
     return DDKS_OK;
 }
 
@@ -506,10 +499,15 @@ ddks_status ddks_profile_read(ddks_ctx* ctx, double* count_ms, int64_t* launches
 
 ddks_status ddks_profile_clock(ddks_ctx* ctx, double* sm_mhz) {
     if (!ctx || !sm_mhz) return DDKS_ERR_INVALID_ARGUMENT;
-    ddks_status s = collect_profile(ctx);
-    if (s) return s;
-    *sm_mhz = ctx->prof_ns > 0 ? ctx->prof_cycles / ctx->prof_ns * 1e3 : 0.0;
-    ctx->prof_cycles = ctx->prof_ns = 0.0;
+    *sm_mhz = 0.0;
+    if (!ctx->prof_clk.p) return DDKS_OK;
+    // the probe totals accumulate on the device across calls (no per-call copy inside a timed region); read here
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaDeviceSynchronize());
+    unsigned long long c[2];
+    CU(cudaMemcpy(c, ctx->prof_clk.p, 16, cudaMemcpyDeviceToHost));
+    CU(cudaMemset(ctx->prof_clk.p, 0, 16));
+    *sm_mhz = c[1] > 0 ? (double)c[0] / (double)c[1] * 1e3 : 0.0;
     return DDKS_OK;
 }
 

@@ -48,7 +48,6 @@ struct ddks_ctx {
     double prof_ms = 0.0;
     int64_t prof_launches = 0;
     uint64_t prof_pairs = 0;
-    double prof_cycles = 0.0, prof_ns = 0.0;  // in-kernel clock probe totals since the last ddks_profile_clock
 };
 
 extern thread_local std::string g_create_err;
