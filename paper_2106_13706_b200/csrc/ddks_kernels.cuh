@@ -51,7 +51,12 @@ constexpr int kUnrollPts = DDKS_UNROLL;
 // measured 0.8% faster than R=8 x 12 warps on the x0-ordered C5 kernel).
 template <> struct Cfg<1> { static constexpr int R = 8, T = 256, TILE = 512, S = 3; };
 template <> struct Cfg<2> { static constexpr int R = 8, T = 256, TILE = 512, S = 3; };
-template <> struct Cfg<3> { static constexpr int R = 8, T = 256, TILE = 512, S = 3; };
+#ifndef DDKS_C3R  // geometry experiments (d = 3), as for d = 5 below
+#define DDKS_C3R 8
+#define DDKS_C3T 256
+#define DDKS_C3TILE 512
+#endif
+template <> struct Cfg<3> { static constexpr int R = DDKS_C3R, T = DDKS_C3T, TILE = DDKS_C3TILE, S = 3; };
 template <> struct Cfg<4> { static constexpr int R = 4, T = 256, TILE = 512, S = 3; };
 #ifndef DDKS_C5R  // geometry experiments: -DDDKS_C5R=.. -DDDKS_C5T=.. -DDDKS_C5TILE=.. -DDDKS_C5S=..
 #define DDKS_C5R 12
