@@ -78,6 +78,9 @@ typedef enum {
 #define DDKS_FLAG_FORCE_X0 64u     /* TEST ONLY: use the kd-ordered count for any N (2 <= d <= 8)                      */
 #define DDKS_FLAG_KD_SHIFT 9u      /* TEST ONLY: bits 9..10 = K in 1..3 force the number of kd levels (0: cost model) */
 #define DDKS_FLAG_KD_LEVELS(k) ((unsigned)(k) << DDKS_FLAG_KD_SHIFT)
+#define DDKS_FLAG_NO_GRAPH 4096u   /* never capture ddks_stat into a CUDA graph (by default the second identical call --
+                                      same input pointers, sizes and workspace -- is captured and later calls replay it
+                                      with one cudaGraphLaunch; identical results)                                     */
 #define DDKS_FLAG_NCCL_SELF 2048u  /* TEST ONLY (world == 1): create a one-rank NCCL communicator and run every collective
                                       of the multi-GPU path (all-reduce / all-gather) through it; identical results */
 #define DDKS_FLAG_RDKS_FULL_SORT 128u /* TEST ONLY: ddks_rdks sorts every key (8-pass radix sort) instead of the bucket-pruned

@@ -44,6 +44,7 @@ ddks_status ensure(ddks_ctx* ctx, DevBuf& b, size_t bytes) {
     b.p = nullptr;
     b.bytes = 0;
     size_t want = std::max(bytes, (size_t)256);
+    ctx->alloc_epoch++;  // invalidates captured graphs (they hold the old pointers)
     cudaError_t e = cudaMalloc(&b.p, want);
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -299,14 +300,15 @@ ddks_status launch_perm_d(ddks_ctx* ctx, const float* pooled_packed, const int32
     if (ctx->flags & DDKS_FLAG_PROFILE) {
         CU(cudaEventCreate(&ev.first));
         CU(cudaEventCreate(&ev.second));
-        CU(cudaEventRecord(ev.first, st));
+        CU(record_event(ev.first, st));
     }
     kern<<<grid, G::T, G::SMEM_BYTES, st>>>(pa);
     CHECK_LAUNCH();
     ctx->launches++;
     if (ev.first) {
-        CU(cudaEventRecord(ev.second, st));
+        CU(record_event(ev.second, st));
         ctx->ev_pending.push_back(ev);
+        ctx->ev_recycle.push_back(1);
         // classifications actually performed: each pair is classified once per chunk of J permutations
         ctx->ev_pairs.push_back((uint64_t)chunks * (uint64_t)N * (uint64_t)N);
     }
@@ -331,6 +333,7 @@ ddks_status launch_perm(ddks_ctx* ctx, int d, const float* pooled_packed, const 
 ddks_status ensure_host(ddks_ctx* ctx, size_t bytes) {
     if (bytes <= ctx->host_pinned_bytes) return DDKS_OK;
     if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
+    ctx->alloc_epoch++;
     ctx->host_pinned = nullptr;
     ctx->host_pinned_bytes = 0;
     CU(cudaMallocHost(&ctx->host_pinned, bytes));
@@ -346,10 +349,11 @@ ddks_status collect_profile(ddks_ctx* ctx) {
         ctx->prof_ms += ms;
         ctx->prof_launches += 1;
         ctx->prof_pairs += ctx->ev_pairs[i];
-        ctx->ev_free.push_back(ctx->ev_pending[i]);
+        if (i >= ctx->ev_recycle.size() || ctx->ev_recycle[i]) ctx->ev_free.push_back(ctx->ev_pending[i]);
     }
     ctx->ev_pending.clear();
     ctx->ev_pairs.clear();
+    ctx->ev_recycle.clear();
     return DDKS_OK;
 }
 
@@ -414,7 +418,7 @@ ddks_status ddks_create(ddks_ctx** out, int device, int world, int rank, const v
     if (world < 1 || rank < 0 || rank >= world) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad world/rank");
     if ((world == 1) != (nccl_id == nullptr))
         return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "nccl_id must be NULL iff world == 1");
-    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT | DDKS_FLAG_PROFILE | DDKS_FLAG_PERM_GATHER | DDKS_FLAG_NO_X0 | DDKS_FLAG_FORCE_X0 | DDKS_FLAG_RDKS_FULL_SORT | DDKS_FLAG_KD_LEVELS(3) | DDKS_FLAG_NCCL_SELF)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
+    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT | DDKS_FLAG_PROFILE | DDKS_FLAG_PERM_GATHER | DDKS_FLAG_NO_X0 | DDKS_FLAG_FORCE_X0 | DDKS_FLAG_RDKS_FULL_SORT | DDKS_FLAG_KD_LEVELS(3) | DDKS_FLAG_NCCL_SELF | DDKS_FLAG_NO_GRAPH)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
     int ndev = 0;
     CU(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device %d of %d", device, ndev);
@@ -460,17 +464,25 @@ ddks_status ddks_destroy(ddks_ctx* ctx) {
     if (!ctx) return DDKS_OK;
     cudaSetDevice(ctx->device);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
-    for (auto* v : {&ctx->ev_pending, &ctx->ev_free})
+    if (ctx->sg_exec) cudaGraphExecDestroy(ctx->sg_exec);
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+    for (auto* v : {&ctx->ev_free, &ctx->sg_evs})
         for (auto& e : *v) {
             cudaEventDestroy(e.first);
             cudaEventDestroy(e.second);
+        }
+    for (size_t i = 0; i < ctx->ev_pending.size(); ++i)  // left pending only by a failed call
+        if (i < ctx->ev_recycle.size() && ctx->ev_recycle[i]) {
+            cudaEventDestroy(ctx->ev_pending[i].first);
+            cudaEventDestroy(ctx->ev_pending[i].second);
         }
     for (DevBuf* b : {&ctx->raw_a, &ctx->raw_b, &ctx->raw_perm, &ctx->packed, &ctx->packed2, &ctx->pool_packed, &ctx->per_origin,
                       &ctx->accum, &ctx->item_num, &ctx->bitmap, &ctx->labels, &ctx->res, &ctx->sig_hist,
                       &ctx->sig_lf, &ctx->sig_scratch, &ctx->sig_table, &ctx->sig_contrib, &ctx->sig_part,
                       &ctx->vox_keys, &ctx->vox_cnt, &ctx->vox_S, &ctx->rd_keys, &ctx->rd_xn, &ctx->rd_k0,
                       &ctx->rd_k1, &ctx->rd_hist, &ctx->rd_tcnt, &ctx->rd_cnum, &ctx->x0_keys0,
-                      &ctx->x0_keys1, &ctx->x0_hist, &ctx->x0_pts, &ctx->x0_perm, &ctx->rdb_cnt,
+                      &ctx->x0_keys1, &ctx->x0_hist, &ctx->x0_pts, &ctx->x0_perm, &ctx->x0_pts2,
+                      &ctx->x0_perm2, &ctx->x0_boxes, &ctx->prof_clk, &ctx->rdb_cnt,
                       &ctx->rdb_pst, &ctx->rdb_coff, &ctx->rdb_fill, &ctx->rdb_clist, &ctx->rdb_csum})
         if (b->p) cudaFree(b->p);
     if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
@@ -511,8 +523,104 @@ ddks_status ddks_profile_clock(ddks_ctx* ctx, double* sm_mhz) {
     return DDKS_OK;
 }
 
+// Enqueue one statistic on st, ending with the D2H of the result block into host_pinned (no sync): staging of host
+// inputs, pack, count, finalise, argmax, collectives. Everything here is stream-ordered, so it can be captured.
+static ddks_status stat_enqueue(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
+                                cudaStream_t st, int64_t ob, int64_t oe, uint64_t* per_origin_out, int sw, int sr) {
+    ddks_status s;
+    const int64_t N = n_P + n_Q;
+    const int DP = pad_dim(d);
+    const bool export_mode = per_origin_out != nullptr;
+    const void *dP, *dQ;
+    if ((s = stage_input(ctx, P, (size_t)n_P * d * 4, ctx->raw_a, st, &dP))) return s;
+    if ((s = stage_input(ctx, Q, (size_t)n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
+    if ((s = ensure(ctx, ctx->packed, (size_t)N * DP * 4))) return s;
+    if ((s = ensure(ctx, ctx->per_origin, (size_t)std::max<int64_t>(oe - ob, 1) * 8))) return s;
+    DevResult* dres = (DevResult*)ctx->res.p;
+    DevResult* hres = (DevResult*)ctx->host_pinned;
+    *hres = DevResult{0ull, ~0ull, 0u, 0u};  // re-written by the host before every graph replay as well
+    CU(cudaMemcpyAsync(dres, hres, sizeof(DevResult), cudaMemcpyHostToDevice, st));
+    float* packed = (float*)ctx->packed.p;
+    if ((s = launch_pack(ctx, (const float*)dP, n_P, (const float*)dQ, n_Q, d, 1, packed, &dres->flag, st))) return s;
+    uint64_t* per = nullptr;
+    if ((s = count_statistic(ctx, packed, d, n_P, n_Q, ob, oe, sw, sr, dres, export_mode, false, nullptr, st, &per))) return s;
+    if (ctx->comm && !export_mode) {
+        NC(ncclAllReduce(&dres->arg, &dres->arg, 1, ncclUint64, ncclMin, ctx->comm, st));
+        NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
+    }
+    if (export_mode && oe > ob) {
+        CU(cudaMemcpyAsync(per_origin_out, per, (size_t)(oe - ob) * 8, cudaMemcpyDefault, st));
+    }
+    CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+    return DDKS_OK;
+}
+
+// a graph may read this input at replay time: device (or managed) memory, or page-locked host memory
+static bool graph_input_ok(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged || a.type == cudaMemoryTypeHost;
+}
+
+static void drop_stat_graph(ddks_ctx* ctx) {
+    if (ctx->sg_exec) cudaGraphExecDestroy(ctx->sg_exec);
+    ctx->sg_exec = nullptr;
+    ctx->sg_key = ddks_ctx::StatKey{};
+    // the graph's event pairs: no longer pending (every call collects before returning), so they are free again
+    for (auto& e : ctx->sg_evs) ctx->ev_free.push_back(e);
+    ctx->sg_evs.clear();
+    ctx->sg_ev_pairs.clear();
+}
+
+// Capture stat_enqueue on the context's capture stream into ctx->sg_exec. *ok = false (and no error) when the capture
+// or instantiation is refused or the workspace moved meanwhile; the caller then runs the call uncaptured.
+static ddks_status stat_capture(ddks_ctx* ctx, const ddks_ctx::StatKey& key, const float* P, int64_t n_P,
+                                const float* Q, int64_t n_Q, int32_t d, int64_t ob, int64_t oe, int sw, int sr,
+                                bool* ok) {
+    *ok = false;
+    drop_stat_graph(ctx);
+    if (!ctx->cap_stream) CU(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    const size_t ev0 = ctx->ev_pending.size();
+    const int64_t l0 = ctx->launches;
+    CU(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed));
+    const ddks_status s = stat_enqueue(ctx, P, n_P, Q, n_Q, d, ctx->cap_stream, ob, oe, nullptr, sw, sr);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &g);
+    // the events recorded during the capture are graph nodes (not executed yet): they belong to the graph
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs(ctx->ev_pending.begin() + ev0, ctx->ev_pending.end());
+    std::vector<uint64_t> pairs(ctx->ev_pairs.begin() + ev0, ctx->ev_pairs.end());
+    ctx->ev_pending.resize(ev0);
+    ctx->ev_pairs.resize(ev0);
+    ctx->ev_recycle.resize(ev0);
+    const int64_t nl = ctx->launches - l0;
+    ctx->launches = l0;
+    cudaGraphExec_t ex = nullptr;
+    const bool good = s == DDKS_OK && e == cudaSuccess && g && ctx->alloc_epoch == key.epoch &&
+                      cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    if (!good) {
+        cudaGetLastError();
+        for (auto& v : evs) ctx->ev_free.push_back(v);
+        ctx->err.clear();
+        return DDKS_OK;
+    }
+    ctx->sg_exec = ex;
+    ctx->sg_key = key;
+    ctx->sg_launches = nl;
+    ctx->sg_kd_levels = ctx->kd_levels;
+    ctx->sg_evs = evs;
+    ctx->sg_ev_pairs = pairs;
+    *ok = true;
+    return DDKS_OK;
+}
+
 // a1-a7 for one pair, origins sharded across ranks; optional per-origin export (debug path, single rank).
-// shard_world > 0: compute only the origin shard that rank shard_rank of shard_world would own (ddks_stat_shard)
+// shard_world > 0: compute only the origin shard that rank shard_rank of shard_world would own (ddks_stat_shard).
+// Repeated identical ddks_stat calls (same input pointers and sizes, same workspace) are captured into a CUDA graph
+// on the second call and replayed with one cudaGraphLaunch from then on (DDKS_FLAG_NO_GRAPH disables it).
 static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
                              void* stream, ddks_result* out, int64_t o_begin_req, int64_t o_end_req,
                              uint64_t* per_origin_out, int shard_world = 0, int shard_rank = 0) {
@@ -524,7 +632,6 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
     if (s) return s;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t N = n_P + n_Q;
-    const int DP = pad_dim(d);
     const bool export_mode = per_origin_out != nullptr;
     int64_t ob, oe;
     if (export_mode) {
@@ -535,29 +642,34 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
     } else {
         ddks_shard_range(N, ctx->world, ctx->rank, &ob, &oe);
     }
-    const void *dP, *dQ;
-    if ((s = stage_input(ctx, P, (size_t)n_P * d * 4, ctx->raw_a, st, &dP))) return s;
-    if ((s = stage_input(ctx, Q, (size_t)n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
-    if ((s = ensure(ctx, ctx->packed, (size_t)N * DP * 4))) return s;
-    if ((s = ensure(ctx, ctx->per_origin, (size_t)std::max<int64_t>(oe - ob, 1) * 8))) return s;
-    DevResult* dres = (DevResult*)ctx->res.p;
-    DevResult init{0ull, ~0ull, 0u, 0u};
-    DevResult* hres = (DevResult*)ctx->host_pinned;
-    *hres = init;
-    CU(cudaMemcpyAsync(dres, hres, sizeof init, cudaMemcpyHostToDevice, st));
-    float* packed = (float*)ctx->packed.p;
-    if ((s = launch_pack(ctx, (const float*)dP, n_P, (const float*)dQ, n_Q, d, 1, packed, &dres->flag, st))) return s;
-    uint64_t* per = nullptr;
     const int sw = shard_world > 0 ? shard_world : ctx->world, sr = shard_world > 0 ? shard_rank : ctx->rank;
-    if ((s = count_statistic(ctx, packed, d, n_P, n_Q, ob, oe, sw, sr, dres, export_mode, false, nullptr, st, &per))) return s;
-    if (ctx->comm && !export_mode) {
-        NC(ncclAllReduce(&dres->arg, &dres->arg, 1, ncclUint64, ncclMin, ctx->comm, st));
-        NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
+    const bool graphable = !export_mode && shard_world == 0 && !(ctx->flags & DDKS_FLAG_NO_GRAPH) &&
+                           graph_input_ok(P) && graph_input_ok(Q);
+    const ddks_ctx::StatKey key{P, Q, n_P, n_Q, d, ctx->alloc_epoch};
+    bool replay = graphable && ctx->sg_exec && ctx->sg_key == key;
+    if (graphable && !replay && ctx->sg_seen == key) {
+        if ((s = stat_capture(ctx, key, P, n_P, Q, n_Q, d, ob, oe, sw, sr, &replay))) return s;
     }
-    if (export_mode && oe > ob) {
-        CU(cudaMemcpyAsync(per_origin_out, per, (size_t)(oe - ob) * 8, cudaMemcpyDefault, st));
+    DevResult* hres;
+    if (replay) {
+        hres = (DevResult*)ctx->host_pinned;
+        *hres = DevResult{0ull, ~0ull, 0u, 0u};  // the graph's first node copies it to the device
+        CU(cudaGraphLaunch(ctx->sg_exec, st));
+        ctx->launches += ctx->sg_launches;
+        ctx->kd_levels = ctx->sg_kd_levels;
+        for (size_t i = 0; i < ctx->sg_evs.size(); ++i) {
+            ctx->ev_pending.push_back(ctx->sg_evs[i]);
+            ctx->ev_pairs.push_back(ctx->sg_ev_pairs[i]);
+            ctx->ev_recycle.push_back(0);
+        }
+    } else {
+        if ((s = stat_enqueue(ctx, P, n_P, Q, n_Q, d, st, ob, oe, per_origin_out, sw, sr))) return s;
+        hres = (DevResult*)ctx->host_pinned;
+        if (graphable) {  // a second identical call (same workspace) will be captured
+            ctx->sg_seen = key;
+            ctx->sg_seen.epoch = ctx->alloc_epoch;
+        }
     }
-    CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     if ((s = collect_profile(ctx))) return s;
     if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");

@@ -45,6 +45,26 @@ struct ddks_ctx {
     // profiling (DDKS_FLAG_PROFILE)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending, ev_free;
     std::vector<uint64_t> ev_pairs;
+    std::vector<char> ev_recycle;  // parallel to ev_pending: return the pair to ev_free (0: owned by a CUDA graph)
+    // ddks_stat CUDA graph (DESIGN.md §7 "graphs"): the whole call -- H2D of pinned inputs, pack, count, finalise,
+    // argmax, collectives, D2H -- captured on the second identical call and replayed by one cudaGraphLaunch after
+    uint64_t alloc_epoch = 0;  // bumped on every workspace (re)allocation: a captured graph holds raw pointers
+    struct StatKey {
+        const void *P = nullptr, *Q = nullptr;
+        int64_t n_P = -1, n_Q = -1;
+        int d = 0;
+        uint64_t epoch = ~0ull;
+        bool operator==(const StatKey& o) const {
+            return P == o.P && Q == o.Q && n_P == o.n_P && n_Q == o.n_Q && d == o.d && epoch == o.epoch;
+        }
+    };
+    StatKey sg_seen, sg_key;
+    cudaGraphExec_t sg_exec = nullptr;
+    cudaStream_t cap_stream = nullptr;
+    int64_t sg_launches = 0;
+    int sg_kd_levels = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> sg_evs;
+    std::vector<uint64_t> sg_ev_pairs;
     double prof_ms = 0.0;
     int64_t prof_launches = 0;
     uint64_t prof_pairs = 0;
@@ -72,6 +92,16 @@ ddks_status fail(ddks_ctx* c, ddks_status s, const char* fmt, ...);
     } while (0)
 
 #define CHECK_LAUNCH() CU(cudaGetLastError())
+
+// Profiling event record: under stream capture it must be an external record node (a plain record is only a
+// dependency marker there and cannot be timed); outside capture the external flag is refused.
+inline cudaError_t record_event(cudaEvent_t e, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaError_t r = cudaStreamIsCapturing(st, &cs);
+    if (r != cudaSuccess) return r;
+    return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal)
+                                               : cudaEventRecord(e, st);
+}
 
 // grow-only device workspace; host (pinned) scratch
 ddks_status ensure(ddks_ctx* ctx, DevBuf& b, size_t bytes);

@@ -96,7 +96,7 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
             CU(cudaEventCreate(&ev.first));
             CU(cudaEventCreate(&ev.second));
         }
-        CU(cudaEventRecord(ev.first, st));
+        CU(record_event(ev.first, st));
         if (!ctx->prof_clk.p) {
             ddks_status s = ensure(ctx, ctx->prof_clk, 16);
             if (s) return s;
@@ -108,8 +108,9 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
     CHECK_LAUNCH();
     ctx->launches++;
     if (ev.first) {
-        CU(cudaEventRecord(ev.second, st));
+        CU(record_event(ev.second, st));
         ctx->ev_pending.push_back(ev);
+        ctx->ev_recycle.push_back(1);
         // origins of this launch: its blocks, less the missing tail of the last block when that block is its own
         const bool last_own = (blocks_all - 1 - pl.blk_off) % pl.blk_stride == 0;
         const uint64_t own = (uint64_t)blocks_o * G::ORIGINS - (last_own ? (uint64_t)blocks_all * G::ORIGINS - n_orig : 0);

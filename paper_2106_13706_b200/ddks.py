@@ -30,6 +30,7 @@ DDKS_FLAG_FORCE_X0 = 64
 DDKS_FLAG_RDKS_FULL_SORT = 128
 DDKS_FLAG_KD_SHIFT = 9
 DDKS_FLAG_NCCL_SELF = 2048
+DDKS_FLAG_NO_GRAPH = 4096
 
 
 def DDKS_FLAG_KD_LEVELS(k: int) -> int:

@@ -1,0 +1,76 @@
+"""ddks_stat's CUDA graph: the second identical call (same input pointers, sizes, workspace) is captured and later
+calls replay it with one cudaGraphLaunch. Replays must track the buffers' current contents, survive a change of
+shape or flags, keep the profiling counters, and match the oracle / the uncaptured path bit for bit."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import oracle as O  # noqa: E402
+from paper_2106_13706_b200 import ddks as K  # noqa: E402
+from paper_2106_13706_b200 import inputs as I  # noqa: E402
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("n_P,n_Q,d,fl", [(200, 200, 3, 0), (3000, 2500, 5, 0), (150000, 150000, 4, 0),
+                                          (5000, 4000, 5, K.DDKS_FLAG_FORCE_X0 | K.DDKS_FLAG_KD_LEVELS(3)),
+                                          (4000, 4000, 8, K.DDKS_FLAG_PROFILE), (700, 900, 2, K.DDKS_FLAG_NCCL_SELF)])
+def test_graph_replay_tracks_buffer_contents(n_P, n_Q, d, fl):
+    P1, Q1 = I.random_pair(500 + d, n_P, n_Q, d, "mixed")
+    P2, Q2 = I.random_pair(600 + d, n_P, n_Q, d, "grid")
+    dP, dQ = dev(P1), dev(Q1)
+    small = n_P + n_Q <= 20000
+    with K.Context(flags=fl) as c, K.Context(flags=fl | K.DDKS_FLAG_NO_GRAPH) as ref:
+        r1 = [c.stat(dP, dQ) for _ in range(4)]  # plain, capture, replay, replay
+        assert all(r == r1[0] for r in r1) and r1[0] == ref.stat(dP, dQ)
+        if small:
+            w = O.ddks(P1, Q1)
+            assert (r1[0].num, r1[0].den, r1[0].D, r1[0].argmax_origin) == w
+        dP.copy_(dev(P2))  # same buffers, new contents: the replay reads them
+        dQ.copy_(dev(Q2))
+        r2 = c.stat(dP, dQ)
+        assert r2 == ref.stat(dP, dQ)
+        if small:
+            assert (r2.num, r2.den, r2.D, r2.argmax_origin) == O.ddks(P2, Q2)
+        # another shape on the same context, then back: still exact
+        r3 = c.stat(dP[: n_P // 2], dQ)
+        assert r3 == ref.stat(dP[: n_P // 2], dQ)
+        assert c.stat(dP, dQ) == r2 and c.stat(dP, dQ) == r2
+
+
+def test_graph_profile_and_launch_counts():
+    P, Q = I.random_pair(7, 20000, 20000, 5, "normal")
+    dP, dQ = dev(P), dev(Q)
+    with K.Context(flags=K.DDKS_FLAG_PROFILE) as c:
+        c.stat(dP, dQ)
+        c.profile_read()
+        l0 = c.launch_count
+        c.stat(dP, dQ)  # captured and launched
+        l1 = c.launch_count
+        c.stat(dP, dQ)  # replayed
+        l2 = c.launch_count
+        assert l1 - l0 == l2 - l1 > 0
+        ms, n, pairs = c.profile_read()
+        assert n == 2 and ms > 0 and pairs == 2 * 40000 ** 2
+        assert 300.0 < c.profile_clock() < 3000.0
+
+
+def test_graph_pinned_host_inputs():
+    P, Q = I.random_pair(8, 3000, 2000, 4, "normal")
+    hP, hQ = torch.from_numpy(P).pin_memory(), torch.from_numpy(Q).pin_memory()
+    w = O.ddks(P, Q)
+    with K.Context() as c:
+        for _ in range(4):
+            r = c.stat(hP, hQ)
+            assert (r.num, r.den, r.D, r.argmax_origin) == w
+        Pr = np.ascontiguousarray(P[::-1])
+        hP.copy_(torch.from_numpy(Pr))  # new contents of the same pinned buffer: the replay's H2D copy reads them
+        r = c.stat(hP, hQ)
+        assert (r.num, r.den, r.D, r.argmax_origin) == O.ddks(Pr, Q)
