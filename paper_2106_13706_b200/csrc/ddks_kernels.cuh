@@ -579,11 +579,11 @@ __device__ __forceinline__ int64_t kd_part(int64_t j, int64_t s, int64_t e, int6
     return i;
 }
 
-// keys of level `level` (0 <= level < 3) for rows already in the order of the previous level:
+// keys of level `level` (0 <= level < 4) for rows already in the order of the previous level:
 // key = label (1 bit) | cell of the previous levels (cb bits) | order key of x_level (the top 63 - cb - ib bits of
 // f32_key) | row index (ib bits). A stable LSD sort of bits [ib, 64) gives the level's order.
 __global__ void k_kd_keys(const float* __restrict__ pts, int DP, int64_t N, int64_t n_P, int level, int64_t G0,
-                          int64_t G1, int64_t A, int ib, int cb, uint64_t* __restrict__ keys) {
+                          int64_t G1, int64_t G2, int64_t A, int ib, int cb, uint64_t* __restrict__ keys) {
     const int kb = 63 - cb - ib;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
         const bool lab = j >= n_P;
@@ -594,7 +594,12 @@ __global__ void k_kd_keys(const float* __restrict__ pts, int DP, int64_t N, int6
             cell = (uint64_t)i0;
             if (level >= 2) {
                 const int64_t s1 = kd_cut(s, e, G0, i0, A), e1 = kd_cut(s, e, G0, i0 + 1, A);
-                cell = (uint64_t)(i0 * G1 + kd_part(j, s1, e1, G1, A));
+                const int64_t i1 = kd_part(j, s1, e1, G1, A);
+                cell = (uint64_t)(i0 * G1 + i1);
+                if (level >= 3) {
+                    const int64_t s2 = kd_cut(s1, e1, G1, i1, A), e2 = kd_cut(s1, e1, G1, i1 + 1, A);
+                    cell = cell * (uint64_t)G2 + (uint64_t)kd_part(j, s2, e2, G2, A);
+                }
             }
         }
         uint64_t k = f32_key(pts[j * DP + level]);

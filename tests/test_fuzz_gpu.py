@@ -42,7 +42,8 @@ def ctxs():
                                                     ("x0gt", K.DDKS_FLAG_FORCE_X0 | K.DDKS_FLAG_TIES_GT),
                                                     ("full", K.DDKS_FLAG_RDKS_FULL_SORT),
                                                     ("kd2", K.DDKS_FLAG_FORCE_X0 | K.DDKS_FLAG_KD_LEVELS(2)),
-                                                    ("kd3", K.DDKS_FLAG_FORCE_X0 | K.DDKS_FLAG_KD_LEVELS(3))]}
+                                                    ("kd3", K.DDKS_FLAG_FORCE_X0 | K.DDKS_FLAG_KD_LEVELS(3)),
+                                                    ("kd4", K.DDKS_FLAG_FORCE_X0)]}
     yield cs
     for c in cs.values():
         c.close()
@@ -55,9 +56,9 @@ def test_fuzz_exact_and_approx(monkeypatch, ctxs, n_P, n_Q, d, kind, seed):
     for name in ("default", "x0", "direct"):
         r = ctxs[name].stat(dev(P), dev(Q))
         assert (r.num, r.den, r.argmax_origin) == (want[0], want[1], want[3]), name
-    # kd levels 2 and 3 with seeded slab / cell counts (many empty or single-tile cells at these sizes)
-    for K_ in (2, 3):
-        monkeypatch.setenv("DDKS_KD", f"{K_},{1 + seed % 6},{1 + (seed // 6) % 5}")
+    # kd levels 2, 3 and 4 (capped at d) with seeded slab / cell counts (many empty or single-tile cells at these sizes)
+    for K_ in (2, 3, 4):
+        monkeypatch.setenv("DDKS_KD", f"{K_},{1 + seed % 6},{1 + (seed // 6) % 5},{1 + (seed // 30) % 4}")
         r = ctxs[f"kd{K_}"].stat(dev(P), dev(Q))
         assert (r.num, r.den, r.argmax_origin) == (want[0], want[1], want[3]), (K_, os.environ["DDKS_KD"])
     monkeypatch.delenv("DDKS_KD")

@@ -332,13 +332,17 @@ KD_CASES = [(2, "2,5,1", 9000, 7000, 2, "normal"), (2, "2,3,1", 6000, 6000, 3, "
             (3, "3,2,2", 8000, 8000, 4, "grid"), (3, "3,3,3", 16000, 14000, 5, "mixed"), (2, "2,7,1", 20000, 17001, 5, "dup"),
             (3, "3,2,3", 9000, 9000, 6, "normal"), (3, "3,3,3", 7000, 6000, 7, "grid"), (2, "2,4,1", 5000, 5400, 8, "mixed"),
             (3, "3,9,9", 4000, 3000, 5, "normal"), (3, "3,3,3", 3, 12000, 5, "grid"), (2, "2,2,1", 20000, 1, 3, "normal"),
-            (2, "2,1,1", 9000, 7000, 2, "grid"), (3, None, 11000, 9000, 5, "mixed")]
+            (2, "2,1,1", 9000, 7000, 2, "grid"), (3, None, 11000, 9000, 5, "mixed"),
+            (4, "4,2,2,2", 12000, 9000, 5, "mixed"), (4, "4,3,2,2", 9000, 8000, 4, "grid"),
+            (4, "4,2,3,2", 8000, 7000, 8, "normal"), (4, "4,5,5,5", 4000, 3000, 6, "normal"),
+            (4, "4,2,2,3", 3, 9000, 7, "grid")]
 
 
 @pytest.mark.parametrize("K_,env,n_P,n_Q,d,kind", KD_CASES)
 def test_kd_ordered_parity(monkeypatch, ctx_nox0, K_, env, n_P, n_Q, d, kind):
     # K levels of kd ordering (bits 0..K-1 decided per tile where the tile's box does not interleave with the CTA's
-    # origins'); DDKS_KD fixes the slab / cell counts so small inputs still get several cells (and empty ones: 3,9,9)
+    # origins'); DDKS_KD fixes the level and the slab / cell counts so small inputs still get several cells (and
+    # empty ones: 3,9,9 and 4,5,5,5); K = 4 is reached through DDKS_KD only (the test flag holds 1..3)
     if env is None:
         monkeypatch.delenv("DDKS_KD", raising=False)
     else:
@@ -363,7 +367,7 @@ def test_kd_ties_gt_uses_one_level(monkeypatch):
     assert (got.num, got.den, got.argmax_origin) == (want[0], want[1], want[3])
 
 
-@pytest.mark.parametrize("K_,env", [(2, "2,4,1"), (3, "3,3,2")])
+@pytest.mark.parametrize("K_,env", [(2, "2,4,1"), (3, "3,3,2"), (4, "4,2,2,2")])
 def test_kd_shard_rehearsal(monkeypatch, K_, env):
     # origin shards are positions of the kd order: max over shards and the smallest attaining argmax reproduce the
     # oracle for any world size

@@ -157,7 +157,7 @@ def test_significance_x0_ordered(n_P, n_Q, d, kind):
 
 
 @pytest.mark.parametrize("K_,env,n_P,n_Q,d", [(2, "2,3,1", 3000, 2600, 3), (3, "3,3,2", 4000, 3500, 5),
-                                               (3, "3,2,2", 2500, 2500, 8)])
+                                               (3, "3,2,2", 2500, 2500, 8), (4, "4,2,2,2", 4000, 3600, 6)])
 def test_significance_kd_ordered(monkeypatch, K_, env, n_P, n_Q, d):
     # the kd-ordered SPLIT kernel with several slabs / cells: identical M_T histogram, statistic and log_prod
     monkeypatch.setenv("DDKS_KD", env)
