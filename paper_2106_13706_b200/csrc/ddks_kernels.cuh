@@ -327,7 +327,10 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
     }
     float xn[D];
     load_point<D>(tile + p * DP, xn);
-    constexpr int UNR = (KX > 0 && UM != 0) ? DDKS_UNROLL_PARTIAL : kUnrollPts;
+    // K = 4 has 16 loop variants: with R >= 8 origins per thread (large bodies) the ones with undecided dims are
+    // unrolled 4 deep to relieve the instruction cache (C5: 840 -> 827 ms; K = 3, or R = 4 at d = 6, do better with
+    // the full unroll)
+    constexpr int UNR = (KX > 0 && UM != 0) ? ((KX >= 4 && R >= 8) ? 4 : DDKS_UNROLL_PARTIAL) : kUnrollPts;
 #pragma unroll UNR
     for (; p < hi; ++p) {
         float x[D];
