@@ -47,8 +47,7 @@ constexpr int kUnrollPts = DDKS_UNROLL;
 #define DDKS_UNROLL_PARTIAL DDKS_UNROLL
 #endif
 // R origins per thread (1 or even), T threads per CTA (multiple of 64 when R == 1), TILE points per SMEM stage,
-// S stages (DIFF mode). T is a multiple of 128 so every SMSP gets the same number of warps (d=5: R=12 x 8 warps
-// measured 0.8% faster than R=8 x 12 warps on the x0-ordered C5 kernel).
+// S stages (DIFF mode). T is a multiple of 128 so every SMSP gets the same number of warps.
 template <> struct Cfg<1> { static constexpr int R = 8, T = 256, TILE = 512, S = 3; };
 template <> struct Cfg<2> { static constexpr int R = 8, T = 256, TILE = 512, S = 3; };
 #ifndef DDKS_C3R  // geometry experiments (d = 3), as for d = 5 below
@@ -59,8 +58,11 @@ template <> struct Cfg<2> { static constexpr int R = 8, T = 256, TILE = 512, S =
 template <> struct Cfg<3> { static constexpr int R = DDKS_C3R, T = DDKS_C3T, TILE = DDKS_C3TILE, S = 3; };
 template <> struct Cfg<4> { static constexpr int R = 4, T = 256, TILE = 512, S = 3; };
 #ifndef DDKS_C5R  // geometry experiments: -DDDKS_C5R=.. -DDDKS_C5T=.. -DDDKS_C5TILE=.. -DDDKS_C5S=..
-#define DDKS_C5R 12
-#define DDKS_C5T 256
+// d = 5: R = 6 x 16 warps (same 3072 origins per CTA as R = 12 x 8 warps, which was best with bit-0 elision only):
+// with the 4-level kd ordering the deeper warp pool hides the instruction-fetch stalls of the 16 loop variants
+// (C5: 812 vs 830 ms, profiles/r1_c5_variants.txt)
+#define DDKS_C5R 6
+#define DDKS_C5T 512
 #define DDKS_C5TILE 256
 #define DDKS_C5S 3
 #endif
