@@ -386,6 +386,7 @@ def main():
     if not args.no_e2e:
         hosts = tuple(torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in step.host)
         step.call(*hosts)
+        step.call(*hosts)  # the second identical call is captured into the CUDA graph the timed calls replay
         ctx.profile_read()
         barrier()
         e2e_s = []
