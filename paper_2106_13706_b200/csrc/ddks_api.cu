@@ -100,8 +100,14 @@ int pad_dim(int d) { return d <= 4 ? 4 : 8; }
 
 // ------------------------------------------------------------------------------------- count dispatch
 template <int D>
-ddks_status launch_count_d(ddks_ctx* ctx, const CountPlan& pl, const ddks::CountArgs& a, cudaStream_t st) {
+ddks_status launch_count_d(ddks_ctx* ctx, const CountPlan& pl, const ddks::CountArgs& a, cudaStream_t st, bool wx) {
     const bool gt = (ctx->flags & DDKS_FLAG_TIES_GT) != 0;
+    if constexpr (D >= 2) {
+        // rows pre-sorted by x_0 inside every label run (k_pack_sorted) and one point segment: warp-level bit 0
+        if (wx && !gt && pl.N <= pl.window)
+            return pl.split ? launch_count_t<D, true, false, 0, true>(ctx, pl, a, st)
+                            : launch_count_t<D, false, false, 0, true>(ctx, pl, a, st);
+    }
     if (pl.split) return gt ? launch_count_t<D, true, true>(ctx, pl, a, st) : launch_count_t<D, true, false>(ctx, pl, a, st);
     return gt ? launch_count_t<D, false, true>(ctx, pl, a, st) : launch_count_t<D, false, false>(ctx, pl, a, st);
 }
@@ -110,7 +116,7 @@ ddks_status launch_count_d(ddks_ctx* ctx, const CountPlan& pl, const ddks::Count
 // force_split + hist (significance): SPLIT counters, and the finaliser histograms c_Q into hist[n_Q + 1].
 ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int64_t n_P, int64_t n_Q,
                       int64_t o_begin, int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st,
-                      bool force_split, unsigned long long* hist) {
+                      bool force_split, unsigned long long* hist, bool wx) {
     const int64_t N = n_P + n_Q;
     const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
     const uint64_t a_ = (uint64_t)n_Q / g, b_ = (uint64_t)n_P / g;
@@ -140,20 +146,21 @@ ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int6
         for (int64_t b0 = 0; b0 < B; b0 += 65535) {
             const int64_t nb = std::min<int64_t>(65535, B - b0);
             ddks_status s = run_count(ctx, packed + b0 * N * pad_dim(d), d, nb, n_P, n_Q, o_begin, o_end,
-                                      item_num + b0, nullptr, st, force_split, hist ? hist + b0 * (n_Q + 1) : nullptr);
+                                      item_num + b0, nullptr, st, force_split, hist ? hist + b0 * (n_Q + 1) : nullptr,
+                                      wx);
             if (s) return s;
         }
         return DDKS_OK;
     }
     switch (d) {
-        case 1: return launch_count_d<1>(ctx, pl, a, st);
-        case 2: return launch_count_d<2>(ctx, pl, a, st);
-        case 3: return launch_count_d<3>(ctx, pl, a, st);
-        case 4: return launch_count_d<4>(ctx, pl, a, st);
-        case 5: return launch_count_d<5>(ctx, pl, a, st);
-        case 6: return launch_count_d<6>(ctx, pl, a, st);
-        case 7: return launch_count_d<7>(ctx, pl, a, st);
-        case 8: return launch_count_d<8>(ctx, pl, a, st);
+        case 1: return launch_count_d<1>(ctx, pl, a, st, wx);
+        case 2: return launch_count_d<2>(ctx, pl, a, st, wx);
+        case 3: return launch_count_d<3>(ctx, pl, a, st, wx);
+        case 4: return launch_count_d<4>(ctx, pl, a, st, wx);
+        case 5: return launch_count_d<5>(ctx, pl, a, st, wx);
+        case 6: return launch_count_d<6>(ctx, pl, a, st, wx);
+        case 7: return launch_count_d<7>(ctx, pl, a, st, wx);
+        case 8: return launch_count_d<8>(ctx, pl, a, st, wx);
     }
     return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "d=%d", d);
 }
@@ -737,10 +744,20 @@ ddks_status ddks_stat_batch(ddks_ctx* ctx, const float* P, const float* Q, int64
     if (nb > 0) {
         if ((s = ensure(ctx, ctx->packed, (size_t)nb * N * DP * 4))) return s;
         float* packed = (float*)ctx->packed.p;
-        if ((s = launch_pack(ctx, (const float*)dP + ib * n_P * d, n_P, (const float*)dQ + ib * n_Q * d, n_Q, d, nb,
-                             packed, &dres->flag, st)))
+        // small items: rows sorted by x_0 inside every label run, so the count decides bit 0 per warp and sub-tile
+        const bool wx = d >= 2 && n_P <= 2 * ddks::KPS_T && n_Q <= 2 * ddks::KPS_T &&
+                        !(ctx->flags & (DDKS_FLAG_TIES_GT | DDKS_FLAG_NO_X0));
+        if (wx) {
+            ddks::k_pack_sorted<<<dim3((unsigned)nb, 2), ddks::KPS_T, 0, st>>>(
+                (const float*)dP + ib * n_P * d, n_P, (const float*)dQ + ib * n_Q * d, n_Q, d, packed, DP,
+                !(ctx->flags & DDKS_FLAG_NO_VALIDATE), &dres->flag);
+            CHECK_LAUNCH();
+            ctx->launches++;
+        } else if ((s = launch_pack(ctx, (const float*)dP + ib * n_P * d, n_P, (const float*)dQ + ib * n_Q * d, n_Q,
+                                    d, nb, packed, &dres->flag, st))) {
             return s;
-        if ((s = run_count(ctx, packed, d, nb, n_P, n_Q, 0, N, nums + ib, nullptr, st))) return s;
+        }
+        if ((s = run_count(ctx, packed, d, nb, n_P, n_Q, 0, N, nums + ib, nullptr, st, false, nullptr, wx))) return s;
     }
     if (ctx->comm) {
         if ((s = all_gather_items(ctx, nums, B, st))) return s;

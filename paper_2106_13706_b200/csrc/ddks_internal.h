@@ -125,7 +125,7 @@ ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n
 // histograms hist[B][n_Q + 1] (significance)
 ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int64_t n_P, int64_t n_Q,
                       int64_t o_begin, int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st,
-                      bool force_split = false, unsigned long long* hist = nullptr);
+                      bool force_split = false, unsigned long long* hist = nullptr, bool wx = false);
 // items sharded contiguously over ranks: all-gather every rank's slice of dev_nums[total] (8-byte elements)
 ddks_status all_gather_items(ddks_ctx* ctx, uint64_t* dev_nums, int64_t total, cudaStream_t st);
 // kd-ordered count of one statistic (B == 1, 2 <= D <= 8; ddks_kd.cuh, instantiated in ddks_api_kd_*.cu): the origin

@@ -146,6 +146,93 @@ __global__ void k_pack(const float* __restrict__ P, int64_t n_P, const float* __
     if (bad) atomicOr(flag, 1u);
 }
 
+// a1 for batches of small items, rows of every (item, label) run ordered by x_0 (for k_count<WX>): one CTA of KPS_T
+// threads per run of n <= 2 KPS_T rows. The order only has to be close to sorted (it changes speed, never counts):
+// a one-pass bucket sort into 256 equal-width x_0 buckets between the run's min and max (SMEM histogram, scan,
+// atomic slots), then the rows are written in bucket order (validated, -0 -> +0, pad dims = 0). Row order inside a
+// label run does not change the statistic.
+constexpr int KPS_T = 512;
+__global__ void __launch_bounds__(KPS_T) k_pack_sorted(const float* __restrict__ P, int64_t n_P,
+                                                       const float* __restrict__ Q, int64_t n_Q, int d,
+                                                       float* __restrict__ dst, int DP, int validate, uint32_t* flag) {
+    constexpr int NBK = 256;
+    __shared__ uint32_t cnt[NBK];
+    __shared__ float red[2][KPS_T / 32];
+    const int64_t b = blockIdx.x;
+    const bool lab = blockIdx.y != 0;
+    const int n = (int)(lab ? n_Q : n_P);
+    const float* src = lab ? Q + b * n_Q * d : P + b * n_P * d;
+    float* out = dst + (b * (n_P + n_Q) + (lab ? n_P : 0)) * DP;
+    const int t = threadIdx.x;
+    for (int i = t; i < NBK; i += KPS_T) cnt[i] = 0u;
+    // this thread's (up to two) rows: x_0 and the run's min / max (non-finite values are flagged below and excluded
+    // from the range so the bucket arithmetic stays finite)
+    float x[2];
+    float lo = INFINITY, hi = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int i = t + k * KPS_T;
+        x[k] = i < n ? src[(int64_t)i * d] : 0.0f;
+        if (i < n && isfinite(x[k])) lo = fminf(lo, x[k]), hi = fmaxf(hi, x[k]);
+    }
+#pragma unroll
+    for (int sh = 16; sh; sh >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, sh));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, sh));
+    }
+    if ((t & 31) == 0) red[0][t >> 5] = lo, red[1][t >> 5] = hi;
+    __syncthreads();
+    lo = red[0][0], hi = red[1][0];
+    for (int w = 1; w < KPS_T / 32; ++w) lo = fminf(lo, red[0][w]), hi = fmaxf(hi, red[1][w]);
+    const float scale = hi > lo ? (float)NBK / (hi - lo) : 0.0f;
+    int bk[2], rk[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int i = t + k * KPS_T;
+        if (i < n) {
+            const float v = isfinite(x[k]) ? (x[k] - lo) * scale : 0.0f;
+            bk[k] = v >= (float)(NBK - 1) ? NBK - 1 : (v > 0.0f ? (int)v : 0);
+            rk[k] = (int)atomicAdd(&cnt[bk[k]], 1u);
+        }
+    }
+    __syncthreads();
+    if (t < 32) {  // exclusive scan of the 256 bucket counts by one warp (8 per lane)
+        uint32_t v[NBK / 32], run = 0;
+#pragma unroll
+        for (int j = 0; j < NBK / 32; ++j) v[j] = cnt[t * (NBK / 32) + j], run += v[j];
+        uint32_t inc = run;
+#pragma unroll
+        for (int sh = 1; sh < 32; sh <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, sh);
+            if (t >= sh) inc += y;
+        }
+        uint32_t off = inc - run;
+#pragma unroll
+        for (int j = 0; j < NBK / 32; ++j) cnt[t * (NBK / 32) + j] = off, off += v[j];
+    }
+    __syncthreads();
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int i = t + k * KPS_T;
+        if (i >= n) continue;
+        const float* s = src + (int64_t)i * d;
+        float v[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const float u = (m < d) ? s[m] : 0.0f;
+            if (m < d && validate && !isfinite(u)) bad = true;
+            v[m] = (u == 0.0f) ? 0.0f : u;
+        }
+        const int dstrow = (int)cnt[bk[k]] + rk[k];
+        DDKS_ASSERT(dstrow < n);
+        float4* o = reinterpret_cast<float4*>(out + (int64_t)dstrow * DP);
+        o[0] = make_float4(v[0], v[1], v[2], v[3]);
+        if (DP == 8) o[1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
+    if (bad) atomicOr(flag, 1u);
+}
+
 // Permutation gather (a9): dst[j][i] = pooled[perm[j][i]]; checks every row is a permutation of 0..N-1
 // (range + no duplicates via a per-row bitmap), else *flag |= 2.
 template <int DP>
@@ -363,8 +450,13 @@ __device__ __forceinline__ void count_points_um(int um, const float* tile, int l
 // a.perm maps a row back to its pooled index) and a.boxes holds every tile's [min, max] of dims < KX. Bit k < KX is
 // decided for a whole tile when the tile's x_k range does not interleave with the CTA's origins' (DESIGN.md §7
 // "kd ordering"); only the undecided dims are compared.
-template <int D, bool SPLIT, bool GT, int KX = 0>
+//
+// WX (batches of small items, rows of every label run pre-sorted by x_0, see k_pack_sorted): each warp owns 32 R
+// consecutive origins of the sorted order, and bit 0 is decided per (warp, 32-point sub-tile) when the sub-tile's
+// x_0 range does not interleave with the warp's -- the kd idea at warp granularity inside one item.
+template <int D, bool SPLIT, bool GT, int KX = 0, bool WX = false>
 __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a) {
+    static_assert(!(WX && KX > 0), "WX and KX are exclusive");
     using G = Geo<D, SPLIT>;
     constexpr int R = G::R, RP = G::RP, T = G::T, DP = G::DP, TILE = G::TILE, S = G::S, NBASE = G::NBASE,
                   WPB = G::WPB;
@@ -401,11 +493,16 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
         }
     }
 
-    // origins of this thread: r -> o = blk_o0 + r*T + t (clamped to a valid origin; ignored at the end)
+    // origins of this thread: slot r -> o = blk_o0 + r*T + t (WX: blk_o0 + warp*32R + r*32 + lane, so a warp's
+    // origins are consecutive), clamped to a valid origin (ignored at the end); counters stay in slot (r, t)
+    const int lane = t & 31, warp = t >> 5;
+    auto origin_of = [&](int r) -> int32_t {
+        return WX ? blk_o0 + warp * (32 * R) + r * 32 + lane : blk_o0 + r * T + t;
+    };
     float o[R][D];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        int32_t oi = blk_o0 + r * T + t;
+        int32_t oi = origin_of(r);
         oi = oi < a.o_end ? oi : a.o_end - 1;
         const float* op = pts + (int64_t)oi * DP;
 #pragma unroll
@@ -448,6 +545,18 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
         for (int k = 0; k < KX; ++k) {
             cmin[k] = sbox[0][2 * k], cmax[k] = sbox[0][2 * k + 1];
             for (int w = 1; w < T / 32; ++w) cmin[k] = fminf(cmin[k], sbox[w][2 * k]), cmax[k] = fmaxf(cmax[k], sbox[w][2 * k + 1]);
+        }
+    }
+    // WX: the x_0 range of this warp's origins
+    float xw_lo = 0.0f, xw_hi = 0.0f;
+    if constexpr (WX) {
+        xw_lo = o[0][0], xw_hi = o[0][0];
+#pragma unroll
+        for (int r = 1; r < R; ++r) xw_lo = fminf(xw_lo, o[r][0]), xw_hi = fmaxf(xw_hi, o[r][0]);
+#pragma unroll
+        for (int sh = 16; sh; sh >>= 1) {
+            xw_lo = fminf(xw_lo, __shfl_xor_sync(0xffffffffu, xw_lo, sh));
+            xw_hi = fmaxf(xw_hi, __shfl_xor_sync(0xffffffffu, xw_hi, sh));
         }
     }
     // the tile box of the next tile is loaded one iteration ahead (tiles are TILE-aligned from row 0)
@@ -501,7 +610,34 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
             for (int b = 0; b < NBASE; ++b) bb[b] = (part ? baseQ[b] : baseP[b]) + add;
             const uint32_t il = part ? incQ_lo : incP_lo;
             const uint32_t ih = R == 1 ? il : (part ? incQ_hi : incP_hi);
-            count_points_um<D, GT, R, RP, NBASE, WPB, DP, KX>(um, tile, lo, hi, o, bb, ubase, il, ih, G::HIST_WORDS * 4u);
+            if constexpr (WX) {
+                // 32-point sub-tiles (x_0-sorted within the run): bit 0 decided per warp when the ranges do not meet
+                for (int sb = lo; sb < hi; sb += 32) {
+                    const int se = min(hi, sb + 32);
+                    float mn = tile[min(sb + lane, se - 1) * DP], mx = mn;
+#pragma unroll
+                    for (int sh = 16; sh; sh >>= 1) {
+                        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, sh));
+                        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, sh));
+                    }
+                    int wm = 1;
+                    float wadd = 0.0f;
+                    if (GT ? (mx <= xw_lo) : (mx < xw_lo)) {
+                        wm = 0;
+                    } else if (GT ? (mn > xw_hi) : (mn >= xw_hi)) {
+                        wm = 0;
+                        wadd = (float)(4 * WPB);
+                    }
+                    float wb[NBASE];
+#pragma unroll
+                    for (int b = 0; b < NBASE; ++b) wb[b] = bb[b] + wadd;
+                    count_points_um<D, GT, R, RP, NBASE, WPB, DP, 1>(wm, tile, sb, se, o, wb, ubase, il, ih,
+                                                                    G::HIST_WORDS * 4u);
+                }
+            } else {
+                count_points_um<D, GT, R, RP, NBASE, WPB, DP, KX>(um, tile, lo, hi, o, bb, ubase, il, ih,
+                                                                 G::HIST_WORDS * 4u);
+            }
         }
         __syncthreads();  // every thread is done with stage s
         if (t == 0 && it + S < n_tiles) {
@@ -523,7 +659,7 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
         int32_t* acc = a.accum + item * (int64_t)G::NB * a.acc_stride;
 #pragma unroll 1
         for (int r = 0; r < R; ++r) {
-            const int32_t oi = blk_o0 + r * T + t;
+            const int32_t oi = origin_of(r);
             if (oi >= a.o_end) continue;
             const int sl = G::slot(r, t);
             const bool hiw = G::high(r, t);
@@ -541,7 +677,7 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
     uint64_t best = 0;
 #pragma unroll 1
     for (int r = 0; r < R; ++r) {
-        const int32_t oi = blk_o0 + r * T + t;
+        const int32_t oi = origin_of(r);
         if (oi >= a.o_end) continue;
         const uint64_t m = origin_num<D, SPLIT>(hist, r, t, a, item);
         if (a.per_origin) a.per_origin[a.perm ? a.perm[oi] : oi - a.o_begin] = m;

@@ -21,10 +21,10 @@ struct CountPlan {
     int32_t blk_stride = 1, blk_off = 0;  // this launch takes origin blocks blk_off, blk_off + blk_stride, ...
 };
 
-template <int D, bool SPLIT, bool GT, int KX = 0>
+template <int D, bool SPLIT, bool GT, int KX = 0, bool WX = false>
 ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a, cudaStream_t st) {
     using G = ddks::Geo<D, SPLIT>;
-    auto kern = ddks::k_count<D, SPLIT, GT, KX>;
+    auto kern = ddks::k_count<D, SPLIT, GT, KX, WX>;
     // function attributes are per device: remember which devices this instantiation was configured on
     static bool attr_done[kMaxDevices] = {};
     if (ctx->device >= kMaxDevices) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device index %d >= %d", ctx->device, kMaxDevices);
@@ -56,7 +56,8 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
     const int min_segs = (n_tiles + w_tiles - 1) / w_tiles;
     const int64_t base_ctas = pl.B * blocks_o;
     int segs = min_segs;
-    if (!(ctx->flags & DDKS_FLAG_FORCE_DIRECT)) {
+    if (WX && min_segs > 1) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "warp-level x0 count needs one point segment");
+    if (!WX && !(ctx->flags & DDKS_FLAG_FORCE_DIRECT)) {
         constexpr double FLUSH_COST = 2.0, SETUP_COST = 2.0 * G::TILE;  // calibrated on C3 (segs 2..16 sweep)
         double best = 1e300;
         const int max_segs = (int)std::min<int64_t>(n_tiles, std::max<int64_t>(min_segs, (16 * slots + base_ctas - 1) / base_ctas));

@@ -382,6 +382,25 @@ def test_kd_shard_rehearsal(monkeypatch, K_, env):
             assert (num, arg) == (want[0], want[3]), (world, parts)
 
 
+# ----------------------------------------------------------------------------------- warp-level x0 batch count
+
+@pytest.mark.parametrize("B,n_P,n_Q,d,kind", [(37, 512, 512, 4, "normal"), (9, 700, 300, 3, "grid"), (5, 1024, 1024, 5, "mixed"),
+                                              (11, 33, 97, 8, "dup"), (6, 1, 200, 2, "grid"), (3, 1000, 17, 6, "normal"),
+                                              (4, 129, 257, 7, "grid")])
+def test_batch_warp_x0_parity(B, n_P, n_Q, d, kind):
+    # ddks_stat_batch on small items sorts every label run by x_0 (k_pack_sorted) and decides bit 0 per warp and
+    # 32-point sub-tile (k_count<WX>); against the oracle and the unsorted position-ordered path (DDKS_FLAG_NO_X0)
+    P, Q = I.random_pair(7100 + B + d, B * n_P, B * n_Q, d, kind)
+    if kind == "grid":
+        P[:, 0] = np.round(P[:, 0] * 2) / 2
+    P, Q = P.reshape(B, n_P, d), Q.reshape(B, n_Q, d)
+    want = O.batch(P, Q).tolist()
+    with K.Context() as c, K.Context(flags=K.DDKS_FLAG_NO_X0) as cn:
+        got = [r.num for r in c.stat_batch(dev(P), dev(Q))]
+        assert got == want
+        assert [r.num for r in cn.stat_batch(dev(P), dev(Q))] == want
+
+
 # ----------------------------------------------------------------------------------- launch-limit edge paths
 
 def test_batch_beyond_grid_z_limit(ctx):
