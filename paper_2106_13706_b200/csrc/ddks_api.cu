@@ -261,6 +261,20 @@ ddks_status launch_pack(ddks_ctx* ctx, const float* P, int64_t n_P, const float*
     return DDKS_OK;
 }
 
+// Batches of small items (n_P, n_Q <= 1024, d >= 2): pack every label run in near-x_0 order (k_pack_sorted) so the
+// count can decide bit 0 per warp (*wx = true); otherwise the plain pack.
+ddks_status launch_pack_batch(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d,
+                              int64_t B, float* dst, uint32_t* flag, cudaStream_t st, bool* wx) {
+    *wx = d >= 2 && n_P <= 2 * ddks::KPS_T && n_Q <= 2 * ddks::KPS_T && B <= 0x7fffffff &&
+          !(ctx->flags & (DDKS_FLAG_TIES_GT | DDKS_FLAG_NO_X0));
+    if (!*wx) return launch_pack(ctx, P, n_P, Q, n_Q, d, B, dst, flag, st);
+    ddks::k_pack_sorted<<<dim3((unsigned)B, 2), ddks::KPS_T, 0, st>>>(P, n_P, Q, n_Q, d, dst, pad_dim(d),
+                                                                      !(ctx->flags & DDKS_FLAG_NO_VALIDATE), flag);
+    CHECK_LAUNCH();
+    ctx->launches++;
+    return DDKS_OK;
+}
+
 // Label-invariant permutation null (NEXT-2): labels + validation, then one classification per pair for J perms.
 template <int D>
 ddks_status launch_perm_d(ddks_ctx* ctx, const float* pooled_packed, const int32_t* perms, int64_t n_perm,
@@ -744,19 +758,10 @@ ddks_status ddks_stat_batch(ddks_ctx* ctx, const float* P, const float* Q, int64
     if (nb > 0) {
         if ((s = ensure(ctx, ctx->packed, (size_t)nb * N * DP * 4))) return s;
         float* packed = (float*)ctx->packed.p;
-        // small items: rows sorted by x_0 inside every label run, so the count decides bit 0 per warp and sub-tile
-        const bool wx = d >= 2 && n_P <= 2 * ddks::KPS_T && n_Q <= 2 * ddks::KPS_T &&
-                        !(ctx->flags & (DDKS_FLAG_TIES_GT | DDKS_FLAG_NO_X0));
-        if (wx) {
-            ddks::k_pack_sorted<<<dim3((unsigned)nb, 2), ddks::KPS_T, 0, st>>>(
-                (const float*)dP + ib * n_P * d, n_P, (const float*)dQ + ib * n_Q * d, n_Q, d, packed, DP,
-                !(ctx->flags & DDKS_FLAG_NO_VALIDATE), &dres->flag);
-            CHECK_LAUNCH();
-            ctx->launches++;
-        } else if ((s = launch_pack(ctx, (const float*)dP + ib * n_P * d, n_P, (const float*)dQ + ib * n_Q * d, n_Q,
-                                    d, nb, packed, &dres->flag, st))) {
+        bool wx = false;
+        if ((s = launch_pack_batch(ctx, (const float*)dP + ib * n_P * d, n_P, (const float*)dQ + ib * n_Q * d, n_Q, d,
+                                   nb, packed, &dres->flag, st, &wx)))
             return s;
-        }
         if ((s = run_count(ctx, packed, d, nb, n_P, n_Q, 0, N, nums + ib, nullptr, st, false, nullptr, wx))) return s;
     }
     if (ctx->comm) {

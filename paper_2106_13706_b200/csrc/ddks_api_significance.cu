@@ -193,10 +193,11 @@ ddks_status ddks_significance_batch(ddks_ctx* ctx, const float* P, const float* 
     if (nb > 0) {
         if ((s = ensure(ctx, ctx->packed, (size_t)nb * N * DP * 4))) return s;
         float* packed = (float*)ctx->packed.p;
-        if ((s = launch_pack(ctx, (const float*)dP + ib * n_P * d, n_P, (const float*)dQ + ib * n_Q * d, n_Q, d, nb,
-                             packed, &dres->flag, st)))
+        bool wx = false;  // small items: near-x_0-sorted runs, warp-level bit 0 (the M_T histogram is order-free)
+        if ((s = launch_pack_batch(ctx, (const float*)dP + ib * n_P * d, n_P, (const float*)dQ + ib * n_Q * d, n_Q, d,
+                                   nb, packed, &dres->flag, st, &wx)))
             return s;
-        if ((s = run_count(ctx, packed, d, nb, n_P, n_Q, 0, N, nums + ib, nullptr, st, true, hist))) return s;
+        if ((s = run_count(ctx, packed, d, nb, n_P, n_Q, 0, N, nums + ib, nullptr, st, true, hist, wx))) return s;
         ddks::k_logfact<<<(int)std::min<int64_t>((n_lf + 255) / 256, 148 * 8), 256, 0, st>>>(LF, n_lf - 1);
         CHECK_LAUNCH();
         ctx->launches++;

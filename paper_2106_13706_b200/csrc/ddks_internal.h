@@ -116,6 +116,9 @@ ddks_status collect_profile(ddks_ctx* ctx);
 // validate (NaN/Inf -> *flag |= 1) and pack P then Q into [B][N][pad_dim(d)] rows
 ddks_status launch_pack(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d, int64_t B,
                         float* dst, uint32_t* flag, cudaStream_t st);
+// batches: near-x_0-sorted pack of every label run when the items are small (*wx: the count may use k_count<WX>)
+ddks_status launch_pack_batch(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d,
+                              int64_t B, float* dst, uint32_t* flag, cudaStream_t st, bool* wx);
 // one statistic over the origin shard [ob, oe): count, NCCL max of num, this rank's argmax candidate (see ddks_api.cu)
 // (kd order: the strided origin blocks of shard sr of sw instead of [ob, oe))
 ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n_P, int64_t n_Q, int64_t ob,
