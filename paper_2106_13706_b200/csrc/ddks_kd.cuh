@@ -30,7 +30,8 @@ inline int bits_for(uint64_t v) { int b = 0; while (v) { ++b; v >>= 1; } return 
 // undecided bits: a tile in the same slab (or, across labels, the neighbouring one) leaves bit 0 open
 // (~1.5 / G0), likewise bit 1 (~1.5 / G1), and the last sorted dim interleaves for (origins per CTA + TILE) /
 // cell rows of the tiles. Cells must keep at least 2 A rows. forced_k (1..3) fixes K (tests); kmax caps it.
-inline KdChoice kd_choose(int D, int64_t n_lab, int64_t RT, int64_t TILE, int64_t A, int forced_k, int kmax) {
+inline KdChoice kd_choose(int D, int64_t n_lab, int64_t RT, int64_t RW, int64_t TILE, int64_t A, int forced_k,
+                          int kmax) {
     // tuning override DDKS_KD = "K[,G0[,G1[,G2]]]": K replaces the forced level; cuts not given come from the model
     int env_k = 0, env_n = 0;
     long long env_g[3] = {0, 0, 0};
@@ -41,7 +42,9 @@ inline KdChoice kd_choose(int D, int64_t n_lab, int64_t RT, int64_t TILE, int64_
     }
     KdChoice best{1, 1, 1, 1};
     double best_cost = 1e300;
-    const double c = (double)(RT + TILE) / (double)std::max<int64_t>(n_lab, 1);
+    // the last sorted dim is decided per warp: its open fraction scales with the warp's RW origins, not the CTA's RT
+    (void)RT;
+    const double c = (double)(RW + TILE) / (double)std::max<int64_t>(n_lab, 1);
     const int kcap = std::min(DDKS_KD_MAX, std::min(D, kmax));
     for (int K = 1; K <= kcap; ++K) {
         if (forced_k && K != forced_k) continue;
@@ -83,7 +86,8 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     const int64_t A = lcm_i64(G::ORIGINS, G::TILE);
     const int forced = (int)((ctx->flags >> DDKS_FLAG_KD_SHIFT) & 3u);
     // the tie-convention test variant (GT) is instantiated with one level only
-    const KdChoice kc = kd_choose(D, std::min(n_P, n_Q), G::ORIGINS, G::TILE, A, gt ? 1 : forced, gt ? 1 : 4);
+    const KdChoice kc = kd_choose(D, std::min(n_P, n_Q), G::ORIGINS, 32 * G::R, G::TILE, A, gt ? 1 : forced,
+                                  gt ? 1 : 4);
     const int K = kc.K;
     const int ib = std::max(1, bits_for((uint64_t)(N - 1)));
     const int tiles_rs = (int)((N + ddks::RS_TILE - 1) / ddks::RS_TILE);

@@ -266,6 +266,8 @@ struct CountArgs {
     // over the blocks so every rank gets the same mix of cells); accumulator slot li = y * R*T + r*T + t, acc_stride
     // slots per item (stride 1: li = o - o_begin)
     int32_t blk_stride = 1, blk_off = 0, acc_stride = 0;
+    // slot (r, t) of a block holds origin r*T + t, or (warp_major: kd / WX counts) warp*32R + r*32 + lane
+    int32_t warp_major = 0;
     int32_t seg_points;      // points per grid.z segment (multiple of TILE, <= the int16 flush window)
     uint32_t incP, incQ;     // DIFF: +a and -b (two's complement); SPLIT: 1 and 1
     uint64_t g;              // DIFF: gcd(n_P, n_Q) multiplier
@@ -497,7 +499,7 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
     // origins are consecutive), clamped to a valid origin (ignored at the end); counters stay in slot (r, t)
     const int lane = t & 31, warp = t >> 5;
     auto origin_of = [&](int r) -> int32_t {
-        return WX ? blk_o0 + warp * (32 * R) + r * 32 + lane : blk_o0 + r * T + t;
+        return (WX || KX > 0) ? blk_o0 + warp * (32 * R) + r * 32 + lane : blk_o0 + r * T + t;
     };
     float o[R][D];
 #pragma unroll
@@ -547,12 +549,14 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
             for (int w = 1; w < T / 32; ++w) cmin[k] = fminf(cmin[k], sbox[w][2 * k]), cmax[k] = fmaxf(cmax[k], sbox[w][2 * k + 1]);
         }
     }
-    // WX: the x_0 range of this warp's origins
+    // WX: the x_0 range of this warp's origins; KX > 0: the range of the last sorted dim x_{KX-1}, in which a warp's
+    // 32 R consecutive origins are far narrower than the CTA's (the bit is then decided per warp and tile)
+    constexpr int WD = KX > 0 ? KX - 1 : 0;
     float xw_lo = 0.0f, xw_hi = 0.0f;
-    if constexpr (WX) {
-        xw_lo = o[0][0], xw_hi = o[0][0];
+    if constexpr (WX || KX > 0) {
+        xw_lo = o[0][WD], xw_hi = o[0][WD];
 #pragma unroll
-        for (int r = 1; r < R; ++r) xw_lo = fminf(xw_lo, o[r][0]), xw_hi = fmaxf(xw_hi, o[r][0]);
+        for (int r = 1; r < R; ++r) xw_lo = fminf(xw_lo, o[r][WD]), xw_hi = fmaxf(xw_hi, o[r][WD]);
 #pragma unroll
         for (int sh = 16; sh; sh >>= 1) {
             xw_lo = fminf(xw_lo, __shfl_xor_sync(0xffffffffu, xw_lo, sh));
@@ -598,6 +602,15 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
                 } else if (GT ? (bx[2 * k] > cmax[k]) : (bx[2 * k] >= cmax[k])) {
                     um &= ~(1 << k);
                     add += (float)(4 * (1 << k) * WPB);  // exact: integers < 2^24
+                }
+            }
+            // still open at CTA level: the last sorted dim against this warp's own (narrow) origin range
+            if ((um >> WD) & 1) {
+                if (GT ? (bx[2 * WD + 1] <= xw_lo) : (bx[2 * WD + 1] < xw_lo)) {
+                    um &= ~(1 << WD);
+                } else if (GT ? (bx[2 * WD] > xw_hi) : (bx[2 * WD] >= xw_hi)) {
+                    um &= ~(1 << WD);
+                    add += (float)(4 * (1 << WD) * WPB);
                 }
             }
         }
@@ -815,7 +828,14 @@ __global__ void k_finalize(const CountArgs a, int64_t B) {
         const int64_t item = i / ns, li = i - item * ns;
         // slot li -> origin offset oi in [0, n_orig) (block li / ORIG of this launch is block
         // (li / ORIG) * blk_stride + blk_off of the range); slots past the range hold no origin
-        const int64_t oi = ((li / ORIG) * a.blk_stride + a.blk_off) * ORIG + li % ORIG;
+        const int64_t sl = li % ORIG;  // slot r*T + t inside the block
+        int64_t off = sl;
+        if (a.warp_major) {
+            constexpr int TT = Geo<D, SPLIT>::T, RR = Geo<D, SPLIT>::R;
+            const int64_t r = sl / TT, tt = sl % TT;
+            off = (tt >> 5) * (32 * RR) + r * 32 + (tt & 31);
+        }
+        const int64_t oi = ((li / ORIG) * a.blk_stride + a.blk_off) * ORIG + off;
         if (oi >= n_orig) continue;
         const int32_t* acc = a.accum + item * (int64_t)NB * ns + li;
         uint64_t m = 0;

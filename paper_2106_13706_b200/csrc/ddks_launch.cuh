@@ -36,9 +36,12 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
     const int blocks_all = (n_orig + G::ORIGINS - 1) / G::ORIGINS;
     const int blocks_o = blocks_all > pl.blk_off ? (blocks_all - pl.blk_off + pl.blk_stride - 1) / pl.blk_stride : 0;
     if (blocks_o == 0) return DDKS_OK;  // no origin block falls to this shard
+    a.warp_major = (KX > 0 || WX) ? 1 : 0;  // must match k_count's origin_of
     a.blk_stride = pl.blk_stride;
     a.blk_off = pl.blk_off;
-    a.acc_stride = pl.blk_stride == 1 ? n_orig : blocks_o * G::ORIGINS;
+    // accumulator slots per item: the origin offsets themselves when slots and origins coincide (plain mapping, all
+    // blocks), else whole blocks of slots (strided shards; warp-major slots of kd / WX counts)
+    a.acc_stride = (pl.blk_stride == 1 && !a.warp_major) ? n_orig : blocks_o * G::ORIGINS;
     const int n_tiles = (pl.N + G::TILE - 1) / G::TILE;
     // segment length: at most the int16 flush window. Among the segment counts that respect it, pick the one with
     // the least modelled time: waves x per-CTA cost, where a CTA costs its segment's points (x its origins) plus the
