@@ -29,7 +29,7 @@ inline int bits_for(uint64_t v) { int b = 0; while (v) { ++b; v >>= 1; } return 
 // Levels and cuts from a cost model of the compares per pair: D - K compared dims always, plus the expected
 // undecided bits: a tile in the same slab (or, across labels, the neighbouring one) leaves bit 0 open
 // (~1.5 / G0), likewise bit 1 (~1.5 / G1), and the last sorted dim interleaves for (origins per CTA + TILE) /
-// cell rows of the tiles. Cells must keep at least 2 A rows. forced_k (1..3) fixes K (tests); kmax caps it.
+// cell rows of the tiles (per warp for the last dim). Cells must keep at least A rows on average. forced_k (1..3) fixes K (tests); kmax caps it.
 inline KdChoice kd_choose(int D, int64_t n_lab, int64_t RT, int64_t RW, int64_t TILE, int64_t A, int forced_k,
                           int kmax) {
     // tuning override DDKS_KD = "K[,G0[,G1[,G2]]]": K replaces the forced level; cuts not given come from the model
@@ -53,7 +53,7 @@ inline KdChoice kd_choose(int D, int64_t n_lab, int64_t RT, int64_t RW, int64_t 
             for (int64_t g1 = 1; g1 <= m1; ++g1)
                 for (int64_t g2 = 1; g2 <= m2; ++g2) {
                     const int64_t cells = g0 * g1 * g2;
-                    if (cells > 1 && n_lab / cells < 2 * A) break;
+                    if (cells > 1 && n_lab / cells < A) break;  // a cell holds >= one origin block on average
                     double cost = (double)(D - K) + c * (double)cells;
                     if (K >= 2) cost += 1.5 / (double)g0;
                     if (K >= 3) cost += 1.5 / (double)g1;
