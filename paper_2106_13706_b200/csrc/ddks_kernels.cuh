@@ -478,9 +478,10 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
     const int32_t seg1 = min(a.N, seg0 + a.seg_points);
     const int n_tiles = (seg1 - seg0 + TILE - 1) / TILE;
 
+    __shared__ uint32_t done_cnt[S];  // warps done with each stage (monotone over the rounds)
     if (t == 0) {
 #pragma unroll
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1), done_cnt[s] = 0u;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = t; i < G::HIST_WORDS; i += T) hist[i] = 0u;
@@ -652,13 +653,34 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
                                                                  G::HIST_WORDS * 4u);
             }
         }
-        __syncthreads();  // every thread is done with stage s
-        if (t == 0 && it + S < n_tiles) {
-            fence_proxy_async();
-            const int32_t q0 = seg0 + (it + S) * TILE;
-            const uint32_t bytes = (uint32_t)(min(TILE, seg1 - q0) * DP * 4);
-            mbar_expect_tx(&bars[s], bytes);
-            bulk_g2s(tiles + s * TILE * DP, pts + (int64_t)q0 * DP, bytes, &bars[s]);
+        // kd counts (per-warp loop variants): release stage s without a CTA barrier -- the last warp done with it
+        // refills it, so warps may drift up to S - 1 tiles apart instead of waiting at every tile. Measured (count
+        // kernel): C5 724 -> 711 ms, d = 7 / 8 at N = 4e5 -3 %, d = 6 +9 % and the position-ordered C2 / C3 +4 %
+        // (lockstep warps keep the full S - 1 tiles of TMA slack), so those keep the barrier.
+        constexpr bool WREL = KX > 0 && D != 6;
+        if constexpr (!WREL) {
+            __syncthreads();  // every thread is done with stage s
+            if (t == 0 && it + S < n_tiles) {
+                fence_proxy_async();
+                const int32_t q0 = seg0 + (it + S) * TILE;
+                const uint32_t bytes = (uint32_t)(min(TILE, seg1 - q0) * DP * 4);
+                mbar_expect_tx(&bars[s], bytes);
+                bulk_g2s(tiles + s * TILE * DP, pts + (int64_t)q0 * DP, bytes, &bars[s]);
+            }
+            continue;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            const uint32_t prev = atomicAdd(&done_cnt[s], 1u);  // monotone: round it / S ends at (round + 1) * warps
+            if (prev == (uint32_t)((it / S + 1) * (T / 32) - 1) && it + S < n_tiles) {
+                __threadfence_block();
+                fence_proxy_async();
+                const int32_t q0 = seg0 + (it + S) * TILE;
+                const uint32_t bytes = (uint32_t)(min(TILE, seg1 - q0) * DP * 4);
+                mbar_expect_tx(&bars[s], bytes);
+                bulk_g2s(tiles + s * TILE * DP, pts + (int64_t)q0 * DP, bytes, &bars[s]);
+            }
         }
     }
     __syncthreads();  // all red.shared retired before reading the counters
