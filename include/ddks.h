@@ -22,9 +22,10 @@
  *     unspecified and ddks_last_error(ctx) holds a one-line message.
  *   - A context is bound to one device and one host thread; it is not thread-safe.
  *   - Multi-GPU (world > 1): every rank makes the same call with the same (replicated) inputs.
- *       ddks_stat /              shard the pooled ORIGINS into `world` contiguous ranges (of the pooled order, or of the
- *       ddks_significance        x_0 order when the x0-ordered kernel runs: N >= 200000, 2 <= d <= 8) and combine the
- *                                per-rank maxima with one NCCL all-reduce(max) of a uint64 (+ one all-reduce(min)
+ *       ddks_stat /              shard the pooled ORIGINS -- `world` contiguous ranges of the pooled order, or, when
+ *       ddks_significance        the kd-ordered count runs (N >= 200000, 2 <= d <= 8), the origin blocks r, r + world,
+ *                                r + 2 world, ... of the kd order (every rank computes the same order) -- and combine
+ *                                the per-rank maxima with one NCCL all-reduce(max) of a uint64 (+ one all-reduce(min)
  *                                for the argmax); the significance also all-reduces its M_T histogram.
  *       ddks_stat_batch /
  *       ddks_permutation_null    shard ITEMS (pairs / permutations) contiguously and all-gather the per-item nums,
@@ -182,8 +183,8 @@ DDKS_API ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const
                                void* stream, ddks_result* out);
 
 /* Multi-GPU rehearsal on one device (scaling projections and shard-logic tests): ddks_stat restricted to the origin
- * shard that rank `rank` of `world` would own (same kernels, same shard — of the x_0 order when the x0-ordered
- * kernel runs — and no collective). out->num is the shard's maximum and out->argmax_origin the smallest pooled origin
+ * shard that rank `rank` of `world` would own (same kernels, same shard — the strided origin blocks of the kd order
+ * when the kd-ordered count runs — and no collective). out->num is the shard's maximum and out->argmax_origin the smallest pooled origin
  * attaining it; the max of the `world` nums, and the smallest argmax among the shards attaining that max, are
  * ddks_stat's result. ctx must be single-rank (world == 1 at ddks_create). */
 DDKS_API ddks_status ddks_stat_shard(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
