@@ -16,11 +16,11 @@ namespace ddks_host {
 
 struct KdChoice {
     int K;
-    int64_t G0, G1, G2;
+    int64_t G0, G1, G2, G3;
 };
 
-#ifndef DDKS_KD_MAX  // deepest kd level instantiated (bits 0..3 decided per tile at most)
-#define DDKS_KD_MAX 4
+#ifndef DDKS_KD_MAX  // deepest kd level instantiated: 4 (-DDDKS_KD_MAX=5 builds the 5-level variant, which measured
+#define DDKS_KD_MAX 4  // slower: C5 755 vs 709 ms, d = 6 / 8 at N = 4e5 +15 % / +10 %)
 #endif
 
 inline int64_t lcm_i64(int64_t a, int64_t b) { return a / (int64_t)gcd_u64((uint64_t)a, (uint64_t)b) * b; }
@@ -34,13 +34,13 @@ inline KdChoice kd_choose(int D, int64_t n_lab, int64_t RT, int64_t RW, int64_t 
                           int kmax) {
     // tuning override DDKS_KD = "K[,G0[,G1[,G2]]]": K replaces the forced level; cuts not given come from the model
     int env_k = 0, env_n = 0;
-    long long env_g[3] = {0, 0, 0};
+    long long env_g[4] = {0, 0, 0, 0};
     if (const char* e = getenv("DDKS_KD")) {
-        env_n = sscanf(e, "%d,%lld,%lld,%lld", &env_k, &env_g[0], &env_g[1], &env_g[2]);
+        env_n = sscanf(e, "%d,%lld,%lld,%lld,%lld", &env_k, &env_g[0], &env_g[1], &env_g[2], &env_g[3]);
         if (env_n >= 1 && env_k >= 1 && env_k <= std::min(DDKS_KD_MAX, std::min(D, kmax))) forced_k = env_k;
         else env_n = 0;
     }
-    KdChoice best{1, 1, 1, 1};
+    KdChoice best{1, 1, 1, 1, 1};
     double best_cost = 1e300;
     // the last sorted dim is decided per warp: its open fraction scales with the warp's RW origins, not the CTA's RT
     (void)RT;
@@ -48,25 +48,32 @@ inline KdChoice kd_choose(int D, int64_t n_lab, int64_t RT, int64_t RW, int64_t 
     const int kcap = std::min(DDKS_KD_MAX, std::min(D, kmax));
     for (int K = 1; K <= kcap; ++K) {
         if (forced_k && K != forced_k) continue;
-        const int64_t m0 = K >= 2 ? (K >= 3 ? 64 : 256) : 1, m1 = K >= 3 ? 64 : 1, m2 = K >= 4 ? 32 : 1;
+        const int64_t m0 = K >= 2 ? (K >= 3 ? 64 : 256) : 1, m1 = K >= 3 ? 64 : 1, m2 = K >= 4 ? 32 : 1,
+                      m3 = K >= 5 ? 16 : 1;
+        // K = 5 keeps only the loop variants with <= 2 open dims (kd_max_open): tiles with more run all 5 compares
+        const double k5 = K >= 5 ? 0.1 : 0.0;
         for (int64_t g0 = 1; g0 <= m0; ++g0)
             for (int64_t g1 = 1; g1 <= m1; ++g1)
-                for (int64_t g2 = 1; g2 <= m2; ++g2) {
-                    const int64_t cells = g0 * g1 * g2;
-                    if (cells > 1 && n_lab / cells < A) break;  // a cell holds >= one origin block on average
-                    double cost = (double)(D - K) + c * (double)cells;
-                    if (K >= 2) cost += 1.5 / (double)g0;
-                    if (K >= 3) cost += 1.5 / (double)g1;
-                    if (K >= 4) cost += 1.5 / (double)g2;
-                    if (cost < best_cost - 1e-12) { best_cost = cost; best = {K, g0, g1, g2}; }
-                }
+                for (int64_t g2 = 1; g2 <= m2; ++g2)
+                    for (int64_t g3 = 1; g3 <= m3; ++g3) {
+                        const int64_t cells = g0 * g1 * g2 * g3;
+                        if (cells > 1 && n_lab / cells < A) break;  // a cell holds >= one origin block on average
+                        double cost = (double)(D - K) + c * (double)cells + k5;
+                        if (K >= 2) cost += 1.5 / (double)g0;
+                        if (K >= 3) cost += 1.5 / (double)g1;
+                        if (K >= 4) cost += 1.5 / (double)g2;
+                        if (K >= 5) cost += 1.5 / (double)g3;
+                        if (cost < best_cost - 1e-12) { best_cost = cost; best = {K, g0, g1, g2, g3}; }
+                    }
     }
     if (env_n >= 2) best.G0 = std::max<long long>(1, env_g[0]);
     if (env_n >= 3) best.G1 = std::max<long long>(1, env_g[1]);
     if (env_n >= 4) best.G2 = std::max<long long>(1, env_g[2]);
+    if (env_n >= 5) best.G3 = std::max<long long>(1, env_g[3]);
     if (best.K < 2) best.G0 = 1;
     if (best.K < 3) best.G1 = 1;
     if (best.K < 4) best.G2 = 1;
+    if (best.K < 5) best.G3 = 1;
     return best;
 }
 
@@ -87,7 +94,7 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     const int forced = (int)((ctx->flags >> DDKS_FLAG_KD_SHIFT) & 3u);
     // the tie-convention test variant (GT) is instantiated with one level only
     const KdChoice kc = kd_choose(D, std::min(n_P, n_Q), G::ORIGINS, 32 * G::R, G::TILE, A, gt ? 1 : forced,
-                                  gt ? 1 : 4);
+                                  gt ? 1 : 5);
     const int K = kc.K;
     const int ib = std::max(1, bits_for((uint64_t)(N - 1)));
     const int tiles_rs = (int)((N + ddks::RS_TILE - 1) / ddks::RS_TILE);
@@ -110,9 +117,11 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     const float* src_pts = packed;
     const int32_t* src_perm = nullptr;
     for (int level = 0; level < K; ++level) {
-        const int64_t cells = level == 0 ? 1 : (level == 1 ? kc.G0 : (level == 2 ? kc.G0 * kc.G1 : kc.G0 * kc.G1 * kc.G2));
+        const int64_t gl[4] = {kc.G0, kc.G1, kc.G2, kc.G3};
+        int64_t cells = 1;
+        for (int l = 0; l < level; ++l) cells *= gl[l];
         const int cb = cells > 1 ? bits_for((uint64_t)(cells - 1)) : 0;
-        ddks::k_kd_keys<<<g, 256, 0, st>>>(src_pts, DP, N, n_P, level, kc.G0, kc.G1, kc.G2, A, ib, cb, k0);
+        ddks::k_kd_keys<<<g, 256, 0, st>>>(src_pts, DP, N, n_P, level, kc.G0, kc.G1, kc.G2, kc.G3, A, ib, cb, k0);
         CHECK_LAUNCH();
         ctx->launches++;
         uint64_t* sorted = nullptr;
@@ -169,6 +178,9 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     }
     if constexpr (D >= 4 && DDKS_KD_MAX >= 4) {
         if (K == 4) return launch_kd<D, SPLIT, false, 4>(ctx, pl, a, st);
+    }
+    if constexpr (D >= 5 && DDKS_KD_MAX >= 5) {
+        if (K == 5) return launch_kd<D, SPLIT, false, 5>(ctx, pl, a, st);
     }
     return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "kd levels %d for d=%d", K, D);
 }

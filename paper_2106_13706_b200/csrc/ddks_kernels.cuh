@@ -435,7 +435,14 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
     }
 }
 
-// count_points for the undecided-dims mask um (one instantiation per mask; um is uniform over the CTA)
+// Loop variants instantiated for KX levels: every undecided-dims mask for KX <= 4 (restricting K = 4 to <= 2 open dims
+// measured 1 % slower); for KX = 5 only the masks with at most 2 undecided dims (plus "all undecided"), 17 variants
+// instead of 32; a tile with more open dims is counted by the all-undecided variant (the caller drops its decided
+// weights).
+__host__ __device__ constexpr int kd_max_open(int KX) { return KX >= 5 ? 2 : KX; }
+__host__ __device__ constexpr int popc_c(int v) { return v ? (v & 1) + popc_c(v >> 1) : 0; }
+
+// count_points for the undecided-dims mask um (one instantiation per instantiated mask; um is warp-uniform)
 template <int D, bool GT, int R, int RP, int NB_, int WPB, int DP, int KX, int UM = (1 << KX) - 1>
 __device__ __forceinline__ void count_points_um(int um, const float* tile, int lo, int hi, const float (&o)[R][D],
                                                 const float (&base)[NB_], uint32_t ubase, uint32_t inc_lo,
@@ -443,8 +450,13 @@ __device__ __forceinline__ void count_points_um(int um, const float* tile, int l
     if constexpr (UM == 0) {
         count_points<D, GT, R, RP, NB_, WPB, DP, KX, 0>(tile, lo, hi, o, base, ubase, inc_lo, inc_hi, hbytes);
     } else {
-        if (um == UM) count_points<D, GT, R, RP, NB_, WPB, DP, KX, UM>(tile, lo, hi, o, base, ubase, inc_lo, inc_hi, hbytes);
-        else count_points_um<D, GT, R, RP, NB_, WPB, DP, KX, UM - 1>(um, tile, lo, hi, o, base, ubase, inc_lo, inc_hi, hbytes);
+        if constexpr (popc_c(UM) <= kd_max_open(KX) || UM == (1 << KX) - 1) {
+            if (um == UM) {
+                count_points<D, GT, R, RP, NB_, WPB, DP, KX, UM>(tile, lo, hi, o, base, ubase, inc_lo, inc_hi, hbytes);
+                return;
+            }
+        }
+        count_points_um<D, GT, R, RP, NB_, WPB, DP, KX, UM - 1>(um, tile, lo, hi, o, base, ubase, inc_lo, inc_hi, hbytes);
     }
 }
 
@@ -459,6 +471,7 @@ __device__ __forceinline__ void count_points_um(int um, const float* tile, int l
 template <int D, bool SPLIT, bool GT, int KX = 0, bool WX = false>
 __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a) {
     static_assert(!(WX && KX > 0), "WX and KX are exclusive");
+    static_assert(KX <= 5 && KX <= D, "at most 5 kd levels");
     using G = Geo<D, SPLIT>;
     constexpr int R = G::R, RP = G::RP, T = G::T, DP = G::DP, TILE = G::TILE, S = G::S, NBASE = G::NBASE,
                   WPB = G::WPB;
@@ -614,6 +627,10 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
                     add += (float)(4 * (1 << WD) * WPB);
                 }
             }
+            // more open dims than any instantiated variant: compare them all (and drop the decided weights)
+            if constexpr (kd_max_open(KX) < KX) {
+                if (__popc(um) > kd_max_open(KX)) um = (1 << KX) - 1, add = 0.0f;
+            }
         }
 #pragma unroll 1
         for (int part = 0; part < 2; ++part) {
@@ -755,11 +772,11 @@ __device__ __forceinline__ int64_t kd_part(int64_t j, int64_t s, int64_t e, int6
     return i;
 }
 
-// keys of level `level` (0 <= level < 4) for rows already in the order of the previous level:
+// keys of level `level` (0 <= level < 5) for rows already in the order of the previous level:
 // key = label (1 bit) | cell of the previous levels (cb bits) | order key of x_level (the top 63 - cb - ib bits of
 // f32_key) | row index (ib bits). A stable LSD sort of bits [ib, 64) gives the level's order.
 __global__ void k_kd_keys(const float* __restrict__ pts, int DP, int64_t N, int64_t n_P, int level, int64_t G0,
-                          int64_t G1, int64_t G2, int64_t A, int ib, int cb, uint64_t* __restrict__ keys) {
+                          int64_t G1, int64_t G2, int64_t G3, int64_t A, int ib, int cb, uint64_t* __restrict__ keys) {
     const int kb = 63 - cb - ib;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
         const bool lab = j >= n_P;
@@ -774,7 +791,12 @@ __global__ void k_kd_keys(const float* __restrict__ pts, int DP, int64_t N, int6
                 cell = (uint64_t)(i0 * G1 + i1);
                 if (level >= 3) {
                     const int64_t s2 = kd_cut(s1, e1, G1, i1, A), e2 = kd_cut(s1, e1, G1, i1 + 1, A);
-                    cell = cell * (uint64_t)G2 + (uint64_t)kd_part(j, s2, e2, G2, A);
+                    const int64_t i2 = kd_part(j, s2, e2, G2, A);
+                    cell = cell * (uint64_t)G2 + (uint64_t)i2;
+                    if (level >= 4) {
+                        const int64_t s3 = kd_cut(s2, e2, G2, i2, A), e3 = kd_cut(s2, e2, G2, i2 + 1, A);
+                        cell = cell * (uint64_t)G3 + (uint64_t)kd_part(j, s3, e3, G3, A);
+                    }
                 }
             }
         }
