@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <type_traits>
 #include <cmath>
 #include <cstdarg>
@@ -282,11 +283,11 @@ ddks_status launch_perm_d(ddks_ctx* ctx, const float* pooled_packed, const int32
     using G = ddks::PermGeo<D>;
     const bool gt = (ctx->flags & DDKS_FLAG_TIES_GT) != 0;
     auto kern = gt ? ddks::k_perm_count<D, true> : ddks::k_perm_count<D, false>;
-    static bool attr[kMaxDevices][2] = {};
+    static std::atomic<bool> attr[kMaxDevices][2] = {};
     if (ctx->device >= kMaxDevices) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device index %d >= %d", ctx->device, kMaxDevices);
-    if (!attr[ctx->device][gt]) {
+    if (!attr[ctx->device][gt].load(std::memory_order_acquire)) {
         CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES));
-        attr[ctx->device][gt] = true;
+        attr[ctx->device][gt].store(true, std::memory_order_release);
     }
     const int64_t N = n_P + n_Q;
     const int64_t chunks = (n_perm + G::J - 1) / G::J;

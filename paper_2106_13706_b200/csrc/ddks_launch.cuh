@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <utility>
 
@@ -25,12 +26,13 @@ template <int D, bool SPLIT, bool GT, int KX = 0, bool WX = false>
 ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a, cudaStream_t st) {
     using G = ddks::Geo<D, SPLIT>;
     auto kern = ddks::k_count<D, SPLIT, GT, KX, WX>;
-    // function attributes are per device: remember which devices this instantiation was configured on
-    static bool attr_done[kMaxDevices] = {};
+    // function attributes are per device: remember which devices this instantiation was configured on (atomics:
+    // contexts on different host threads may launch the same instantiation; setting the attribute twice is harmless)
+    static std::atomic<bool> attr_done[kMaxDevices] = {};
     if (ctx->device >= kMaxDevices) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device index %d >= %d", ctx->device, kMaxDevices);
-    if (!attr_done[ctx->device]) {
+    if (!attr_done[ctx->device].load(std::memory_order_acquire)) {
         CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES));
-        attr_done[ctx->device] = true;
+        attr_done[ctx->device].store(true, std::memory_order_release);
     }
     const int n_orig = pl.o_end - pl.o_begin;
     const int blocks_all = (n_orig + G::ORIGINS - 1) / G::ORIGINS;
@@ -46,11 +48,12 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
     // segment length: at most the int16 flush window. Among the segment counts that respect it, pick the one with
     // the least modelled time: waves x per-CTA cost, where a CTA costs its segment's points (x its origins) plus the
     // flush of NB int32 partials per origin (global atomics; ~FLUSH_COST point-equivalents each) and the setup.
-    static int per_sm_dev[kMaxDevices] = {};
-    int& per_sm = per_sm_dev[ctx->device];
+    static std::atomic<int> per_sm_dev[kMaxDevices] = {};
+    int per_sm = per_sm_dev[ctx->device].load(std::memory_order_relaxed);
     if (!per_sm) {
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::T, G::SMEM_BYTES));
         per_sm = std::max(per_sm, 1);
+        per_sm_dev[ctx->device].store(per_sm, std::memory_order_relaxed);
     }
     int nsm = 148;
     CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));

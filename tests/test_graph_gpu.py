@@ -74,3 +74,29 @@ def test_graph_pinned_host_inputs():
         hP.copy_(torch.from_numpy(Pr))  # new contents of the same pinned buffer: the replay's H2D copy reads them
         r = c.stat(hP, hQ)
         assert (r.num, r.den, r.D, r.argmax_origin) == O.ddks(Pr, Q)
+
+
+def test_contexts_on_concurrent_host_threads():
+    # one context per host thread (include/ddks.h); contexts on different threads share only the per-kernel launch
+    # caches, which are atomics: concurrent calls must give the same exact results
+    import threading
+    cases = [I.random_pair(900 + i, 3000 + 100 * i, 2500, 2 + i % 6, "mixed") for i in range(6)]
+    want = [O.ddks(P, Q) for P, Q in cases]
+    got = [None] * len(cases)
+
+    def work(i):
+        P, Q = cases[i]
+        with K.Context(flags=K.DDKS_FLAG_FORCE_X0 if i % 2 else 0) as c:
+            torch.cuda.set_device(0)
+            rs = [c.stat(P, Q) for _ in range(3)]  # host inputs: staged by the library
+            got[i] = rs
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(cases))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for i, rs in enumerate(got):
+        assert rs is not None
+        for r in rs:
+            assert (r.num, r.den, r.D, r.argmax_origin) == want[i], i
