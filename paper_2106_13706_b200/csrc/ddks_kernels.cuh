@@ -439,7 +439,10 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
 // measured 1 % slower); for KX = 5 only the masks with at most 2 undecided dims (plus "all undecided"), 17 variants
 // instead of 32; a tile with more open dims is counted by the all-undecided variant (the caller drops its decided
 // weights).
-__host__ __device__ constexpr int kd_max_open(int KX) { return KX >= 5 ? 2 : KX; }
+#ifndef DDKS_KD_OPEN4  // experiments: open dims instantiated for K = 4
+#define DDKS_KD_OPEN4 4
+#endif
+__host__ __device__ constexpr int kd_max_open(int KX) { return KX >= 5 ? 2 : (KX == 4 ? DDKS_KD_OPEN4 : KX); }
 __host__ __device__ constexpr int popc_c(int v) { return v ? (v & 1) + popc_c(v >> 1) : 0; }
 
 // count_points for the undecided-dims mask um (one instantiation per instantiated mask; um is warp-uniform)
