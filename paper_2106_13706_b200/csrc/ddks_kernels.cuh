@@ -77,7 +77,11 @@ template <int D> struct CfgSplit {
     static constexpr int R = Cfg<D>::R > 2 ? Cfg<D>::R / 2 : Cfg<D>::R;
     static constexpr int T = Cfg<D>::R <= 2 ? Cfg<D>::T / 2 : Cfg<D>::T;
 };
-template <> struct CfgSplit<5> { static constexpr int R = 4, T = 384; };  // A/B: 12 warps beat R=6 x 8 warps
+#ifndef DDKS_S5R  // experiments: SPLIT geometry at d = 5 (the significance's count)
+#define DDKS_S5R 4
+#define DDKS_S5T 384
+#endif
+template <> struct CfgSplit<5> { static constexpr int R = DDKS_S5R, T = DDKS_S5T; };  // A/B: 12 warps beat R=6 x 8 warps
 template <> struct CfgSplit<7> { static constexpr int R = 1, T = 384; };  // 12 balanced warps: -9% vs R=2 x 6
 
 template <int D, bool SPLIT, int DPX = padded_dim<D>()> struct Geo {
