@@ -15,7 +15,7 @@ reported time is the MAX over ranks. `value` = K * N^2 / that time. `e2e` repeat
 C-ABI with PINNED HOST input buffers (H2D inside the timed call) and the host result read.
 `roofline`: the classify+count kernel's FP32 compares/s (d per pair) vs the ALU-pipe compare peak
 148 SMs x 64 lanes/clk (FSET.BF, measured by microbench/pipes.cu) x sm_max_mhz (MEASURED_PEAKS.json). With the kd
-ordering (N >= 200000) most tiles decide up to 3 of the d bits once per tile, so frac can exceed 1.
+ordering (N >= 80000) most tiles decide up to 4 of the d bits once per tile, so frac can exceed 1.
 `cpu_baseline`: the CPU oracle (oracle/ddks_oracle.c, as it stands) on this host's cores over a bounded
 sample of origins of the same workload (rank 0, N = 1 only).
 """

@@ -23,7 +23,7 @@
  *   - A context is bound to one device and one host thread; it is not thread-safe.
  *   - Multi-GPU (world > 1): every rank makes the same call with the same (replicated) inputs.
  *       ddks_stat /              shard the pooled ORIGINS -- `world` contiguous ranges of the pooled order, or, when
- *       ddks_significance        the kd-ordered count runs (N >= 200000, 2 <= d <= 8), the origin blocks r, r + world,
+ *       ddks_significance        the kd-ordered count runs (N >= 80000, 2 <= d <= 8), the origin blocks r, r + world,
  *                                r + 2 world, ... of the kd order (every rank computes the same order) -- and combine
  *                                the per-rank maxima with one NCCL all-reduce(max) of a uint64 (+ one all-reduce(min)
  *                                for the argmax); the significance also all-reduces its M_T histogram.
@@ -74,7 +74,7 @@ typedef enum {
                                       full classification (the default label-invariant path classifies each pair once
                                       for a chunk of permutations; both give identical results)                    */
 #define DDKS_FLAG_NO_X0 32u        /* TEST ONLY: never use the kd-ordered count (ddks_stat / ddks_significance reorder the
-                                      pooled points hierarchically by x_0 .. x_{K-1} when 2 <= d <= 8 and N >= 200000,
+                                      pooled points hierarchically by x_0 .. x_{K-1} when 2 <= d <= 8 and N >= 80000, 
                                       so whole tiles share those bits; identical results)                          */
 #define DDKS_FLAG_FORCE_X0 64u     /* TEST ONLY: use the kd-ordered count for any N (2 <= d <= 8)                      */
 #define DDKS_FLAG_KD_SHIFT 9u      /* TEST ONLY: bits 9..10 = K in 1..3 force the number of kd levels (0: cost model) */

@@ -193,7 +193,8 @@ bool diff_counters_ok(int64_t n_P, int64_t n_Q) {
 bool x0_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q) {
     if (ctx->flags & DDKS_FLAG_NO_X0) return false;
     // the sort (~0.1 ms) pays for itself once the O(N^2) count dominates; DDKS_FLAG_FORCE_X0 (tests) lowers the bar
-    const int64_t min_n = (ctx->flags & DDKS_FLAG_FORCE_X0) ? 2 : 200000;
+    // crossover measured at N ~ 60k-75k for d = 2..8 (microbench/kd_threshold.py)
+    const int64_t min_n = (ctx->flags & DDKS_FLAG_FORCE_X0) ? 2 : 80000;
     return d >= 2 && d <= 8 && n_P + n_Q >= min_n;
 }
 
