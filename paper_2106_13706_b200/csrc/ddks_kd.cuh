@@ -121,11 +121,17 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
         int64_t cells = 1;
         for (int l = 0; l < level; ++l) cells *= gl[l];
         const int cb = cells > 1 ? bits_for((uint64_t)(cells - 1)) : 0;
-        ddks::k_kd_keys<<<g, 256, 0, st>>>(src_pts, DP, N, n_P, level, kc.G0, kc.G1, kc.G2, kc.G3, A, ib, cb, k0);
+        // the full 32-bit order key whenever it fits (truncated keys tie points across cut points, and the touching
+        // cell ranges then leave bits open: C5 709 -> 733 ms with 16 / 24-bit keys); only the top 1 + cb + kb bits
+        // are sorted, so the index bits below them cost no radix passes
+        const int kb = std::min(32, 63 - cb - ib);
+        const int passes = (1 + cb + kb + 7) / 8;
+        const int shift_begin = std::max(0, 64 - 8 * passes);
+        ddks::k_kd_keys<<<g, 256, 0, st>>>(src_pts, DP, N, n_P, level, kc.G0, kc.G1, kc.G2, kc.G3, A, ib, cb, kb, k0);
         CHECK_LAUNCH();
         ctx->launches++;
         uint64_t* sorted = nullptr;
-        if ((s = radix_sort_keys(ctx, k0, k1, N, 1, ib, hist, st, &sorted))) return s;
+        if ((s = radix_sort_keys(ctx, k0, k1, N, 1, shift_begin, hist, st, &sorted))) return s;
         // the last level lands in x0_pts / x0_perm; earlier ones alternate with x0_pts2 / x0_perm2
         const bool fin = ((K - 1 - level) % 2) == 0;
         float* dst_pts = (float*)(fin ? ctx->x0_pts.p : ctx->x0_pts2.p);

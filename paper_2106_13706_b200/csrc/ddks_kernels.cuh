@@ -780,11 +780,12 @@ __device__ __forceinline__ int64_t kd_part(int64_t j, int64_t s, int64_t e, int6
 }
 
 // keys of level `level` (0 <= level < 5) for rows already in the order of the previous level:
-// key = label (1 bit) | cell of the previous levels (cb bits) | order key of x_level (the top 63 - cb - ib bits of
-// f32_key) | row index (ib bits). A stable LSD sort of bits [ib, 64) gives the level's order.
+// key = label (1 bit) | cell of the previous levels (cb bits) | the top kb bits of f32_key(x_level) | ... | row index
+// (low ib bits; kb <= 63 - cb - ib). A stable LSD sort of the top 1 + cb + kb bits gives the level's order (ties keep
+// the previous order); kb < 32 only coarsens the order inside a cell, which changes speed, never counts.
 __global__ void k_kd_keys(const float* __restrict__ pts, int DP, int64_t N, int64_t n_P, int level, int64_t G0,
-                          int64_t G1, int64_t G2, int64_t G3, int64_t A, int ib, int cb, uint64_t* __restrict__ keys) {
-    const int kb = 63 - cb - ib;
+                          int64_t G1, int64_t G2, int64_t G3, int64_t A, int ib, int cb, int kb,
+                          uint64_t* __restrict__ keys) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
         const bool lab = j >= n_P;
         const int64_t s = lab ? n_P : 0, e = lab ? N : n_P;
@@ -809,7 +810,7 @@ __global__ void k_kd_keys(const float* __restrict__ pts, int DP, int64_t N, int6
         }
         uint64_t k = f32_key(pts[j * DP + level]);
         if (kb < 32) k >>= (32 - kb);
-        keys[j] = ((uint64_t)lab << 63) | (cb ? cell << (63 - cb) : 0ull) | (k << ib) | (uint64_t)j;
+        keys[j] = ((uint64_t)lab << 63) | (cb ? cell << (63 - cb) : 0ull) | (k << (63 - cb - kb)) | (uint64_t)j;
     }
 }
 
