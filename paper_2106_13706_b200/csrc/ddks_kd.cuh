@@ -142,6 +142,21 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
         src_pts = dst_pts;
         src_perm = dst_perm;
     }
+    // TEST ONLY (DDKS_KD_SHUFFLE=m): scramble the rows inside each label run (position p -> p * m mod n, m odd and
+    // coprime to n) after the kd sort. The counts must not depend on the order -- only the speed does.
+    if (const char* e = getenv("DDKS_KD_SHUFFLE")) {
+        const long long m = atoll(e);
+        if (m > 1) {
+            if ((s = ensure(ctx, ctx->x0_pts2, (size_t)N * DP * 4))) return s;
+            if ((s = ensure(ctx, ctx->x0_perm2, (size_t)N * 4))) return s;
+            CU(cudaMemcpyAsync(ctx->x0_pts2.p, ctx->x0_pts.p, (size_t)N * DP * 4, cudaMemcpyDeviceToDevice, st));
+            CU(cudaMemcpyAsync(ctx->x0_perm2.p, ctx->x0_perm.p, (size_t)N * 4, cudaMemcpyDeviceToDevice, st));
+            ddks::k_shuffle_runs<<<g, 256, 0, st>>>((const float*)ctx->x0_pts2.p, (const int32_t*)ctx->x0_perm2.p, DP,
+                                                     N, n_P, m, (float*)ctx->x0_pts.p, (int32_t*)ctx->x0_perm.p);
+            CHECK_LAUNCH();
+            ctx->launches++;
+        }
+    }
     float* spts = (float*)ctx->x0_pts.p;
     CU(cudaMemsetAsync(spts + N * DP, 0, 4 * DP * 4, st));  // the prefetch past the last row reads zeros
     ddks::k_tile_boxes<<<(int)std::max<int64_t>(1, std::min<int64_t>((n_tiles + 7) / 8, 148 * 16)), 256, 0, st>>>(

@@ -831,6 +831,29 @@ __global__ void k_permute_rows(const float* __restrict__ pts, int DP, int64_t N,
     }
 }
 
+// TEST ONLY: row p of each label run [s, s + n) goes to s + (p * m mod n'), with m made coprime to the run length by
+// stepping it up (a bijection), rows and permutation together
+__device__ __forceinline__ int64_t gcd_i64(int64_t a, int64_t b) {
+    while (b) { const int64_t t = a % b; a = b; b = t; }
+    return a;
+}
+__global__ void k_shuffle_runs(const float* __restrict__ pts, const int32_t* __restrict__ perm_in, int DP, int64_t N,
+                               int64_t n_P, int64_t m, float* __restrict__ out, int32_t* __restrict__ perm_out) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+        const bool lab = j >= n_P;
+        const int64_t s = lab ? n_P : 0, n = lab ? N - n_P : n_P;
+        int64_t mm = m % n;
+        if (mm == 0) mm = 1;
+        while (gcd_i64(mm, n) != 1) ++mm;
+        const int64_t dst = s + (int64_t)(((unsigned __int128)(j - s) * (unsigned __int128)mm) % (unsigned __int128)n);
+        const float4* src = reinterpret_cast<const float4*>(pts + j * DP);
+        float4* o = reinterpret_cast<float4*>(out + dst * DP);
+        o[0] = src[0];
+        if (DP == 8) o[1] = src[1];
+        perm_out[dst] = perm_in[j];
+    }
+}
+
 // boxes[t][k] = {min, max} of x_k over rows [t*TILE, min(N, (t+1)*TILE)), k < KX: one warp per tile
 __global__ void k_tile_boxes(const float* __restrict__ pts, int DP, int64_t N, int TILE, int KX,
                              float* __restrict__ boxes) {
