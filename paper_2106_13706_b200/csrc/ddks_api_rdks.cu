@@ -11,6 +11,21 @@
 
 using namespace ddks_host;
 
+// distance keys (+ bucket counts when cnt): per point for d <= 8 (x' computed once), per (point, corner) otherwise
+static void launch_rd_keys(const float* P, const float* Q, const double* xn, int64_t N, int64_t n_P, int d,
+                           const uint32_t* keys, int cb, int ce, uint64_t* key, uint32_t* cnt, int nbk, double scale,
+                           cudaStream_t st) {
+    auto grid_for = [](int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); };
+    switch (xn ? 0 : d) {
+#define RDK(D) case D: ddks::k_rd_keys_pt<D><<<grid_for(N), 256, 0, st>>>(P, Q, N, n_P, keys, cb, ce, key, cnt, nbk, scale); return;
+        RDK(1) RDK(2) RDK(3) RDK(4) RDK(5) RDK(6) RDK(7) RDK(8)
+#undef RDK
+        default:
+            ddks::k_rd_keys<<<grid_for(N * (ce - cb)), 256, 0, st>>>(P, Q, xn, N, n_P, d, keys, cb, ce, key, cnt, nbk,
+                                                                      scale);
+    }
+}
+
 extern "C" {
 
 // ------------------------------------------------------------------------------------- rdKS (Alg. 2)
@@ -90,8 +105,8 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     const bool pruned = !(ctx->flags & DDKS_FLAG_RDKS_FULL_SORT);
     if (nc > 0) {
         if (!pruned) {
-            ddks::k_rd_keys<<<grid_for(N * nc), 256, 0, st>>>((const float*)dP, (const float*)dQ, xn, N, n_P, d, keys,
-                                                              (int)cb, (int)ce, k0, nullptr, 0, 0.0);
+            launch_rd_keys((const float*)dP, (const float*)dQ, xn, N, n_P, d, keys, (int)cb, (int)ce, k0, nullptr, 0,
+                           0.0, st);
             CHECK_LAUNCH();
             ctx->launches++;
             if ((s = full_sort())) return s;
@@ -112,8 +127,8 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
             CU(cudaMemsetAsync(bcnt, 0, nb * 8, st));
             CU(cudaMemsetAsync(ctx->rdb_fill.p, 0, nb * 4, st));
             // distance keys and their bucket counts in one pass (NormalizeData fused)
-            ddks::k_rd_keys<<<grid_for(N * nc), 256, 0, st>>>((const float*)dP, (const float*)dQ, xn, N, n_P, d, keys,
-                                                              (int)cb, (int)ce, k0, bcnt, nbk, scale);
+            launch_rd_keys((const float*)dP, (const float*)dQ, xn, N, n_P, d, keys, (int)cb, (int)ce, k0, bcnt, nbk,
+                           scale, st);
             const int nch = (nbk + ddks::RDB_CH - 1) / ddks::RDB_CH;
             uint64_t* csum = (uint64_t*)ctx->rdb_csum.p;
             uint32_t* segc = (uint32_t*)(csum + (size_t)nc * nch);

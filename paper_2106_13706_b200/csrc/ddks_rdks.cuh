@@ -105,6 +105,32 @@ __global__ void k_rd_keys(const float* __restrict__ P, const float* __restrict__
     }
 }
 
+// d <= 8: one thread per point computes x' once (d divisions instead of d per corner) and every corner's key in
+// the same literal sequential f64 order as k_rd_keys (bit-identical keys); keys of corner c stay coalesced.
+template <int D>
+__global__ void k_rd_keys_pt(const float* __restrict__ P, const float* __restrict__ Q, int64_t N, int64_t n_P,
+                             const uint32_t* __restrict__ keys, int c_begin, int c_end, uint64_t* __restrict__ key,
+                             uint32_t* __restrict__ cnt, int nbk, double scale) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        const float* row = i < n_P ? P + i * D : Q + (i - n_P) * D;
+        double x[D];
+#pragma unroll
+        for (int m = 0; m < D; ++m) x[m] = rd_norm(row, m, keys, D);
+        const uint64_t lab = (uint64_t)(i >= n_P);
+        for (int c = c_begin; c < c_end; ++c) {
+            double s = 0.0;
+#pragma unroll
+            for (int m = 0; m < D; ++m) {
+                const double t = __dsub_rn(x[m], (c >= 1 && m == c - 1) ? 1.0 : 0.0);
+                s = __dadd_rn(s, __dmul_rn(t, t));
+            }
+            const uint64_t k = ((uint64_t)__double_as_longlong(__dsqrt_rn(s)) << 1) | lab;
+            key[(int64_t)(c - c_begin) * N + i] = k;
+            if (cnt) atomicAdd(&cnt[2 * ((int64_t)(c - c_begin) * nbk + rdb_bucket(k, scale, nbk)) + lab], 1u);
+        }
+    }
+}
+
 // ------------------------------------------------------------------------------------ GetDFromCornerLists sweep
 // tcnt[seg * tiles + tile] = # P keys (label 0) in the tile
 __global__ void __launch_bounds__(RS_T) k_rd_count(const uint64_t* __restrict__ key, int64_t N, int tiles,
