@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <cstring>
 
 #include "ddks_internal.h"
@@ -54,7 +55,18 @@ ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     ddks_shard_range(N, ctx->world, ctx->rank, &pb, &pe);
     const int blk = 256;
     auto grid_for = [](int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); };
-    if (pe > pb) {
+    const bool aligned = (((uintptr_t)dP | (uintptr_t)dQ) & 15) == 0;
+    if (pb == 0 && pe == N && aligned) {  // one rank holds all points: vectorised min / max
+        const int gv = (int)std::max<int64_t>(1, std::min<int64_t>((N / 4 + 255) / 256, 148 * 8));
+        const int val = !(ctx->flags & DDKS_FLAG_NO_VALIDATE);
+        switch (d) {
+#define MMV(D) case D: ddks::k_minmax_vec<D><<<gv, blk, 0, st>>>((const float*)dP, n_P, (const float*)dQ, n_Q, keys, val, &dres->flag); break;
+            MMV(1) MMV(2) MMV(3) MMV(4) MMV(5) MMV(6) MMV(7) MMV(8)
+#undef MMV
+        }
+        CHECK_LAUNCH();
+        ctx->launches++;
+    } else if (pe > pb) {
         ddks::k_minmax<<<(int)std::max<int64_t>(1, std::min<int64_t>((pe - pb + 255) / 256, 148 * 8)), blk, 0, st>>>(
             (const float*)dP, (const float*)dQ, n_P, pb, pe, d, keys, !(ctx->flags & DDKS_FLAG_NO_VALIDATE),
             &dres->flag);
