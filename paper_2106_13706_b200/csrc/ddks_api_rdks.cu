@@ -4,9 +4,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <cstring>
 
 #include "ddks_internal.h"
+#include "ddks_minmax.cuh"
 #include "ddks_rdks.cuh"
 
 using namespace ddks_host;
@@ -73,8 +75,17 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     CU(cudaMemsetAsync(cnum, 0, (size_t)(d + 1) * 8, st));
     const int gy = std::min(d, 1024);
     const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((N + 1023) / 1024, std::max(1, 296 / gy)));
-    ddks::k_rd_minmax<<<dim3(gx, gy), 256, 0, st>>>(
-        (const float*)dP, n_P, (const float*)dQ, n_Q, d, keys, &dres->flag);
+    if (d <= 8 && ((((uintptr_t)dP | (uintptr_t)dQ) & 15) == 0)) {  // float4 rows-in-fours
+        const int gv = (int)std::max<int64_t>(1, std::min<int64_t>((N / 4 + 255) / 256, 148 * 8));
+        switch (d) {
+#define MMV(D) case D: ddks::k_minmax_vec<D><<<gv, 256, 0, st>>>((const float*)dP, n_P, (const float*)dQ, n_Q, keys, D, 1, &dres->flag); break;
+            MMV(1) MMV(2) MMV(3) MMV(4) MMV(5) MMV(6) MMV(7) MMV(8)
+#undef MMV
+        }
+    } else {
+        ddks::k_rd_minmax<<<dim3(gx, gy), 256, 0, st>>>(
+            (const float*)dP, n_P, (const float*)dQ, n_Q, d, keys, &dres->flag);
+    }
     CHECK_LAUNCH();
     ctx->launches++;
     auto grid_for = [](int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); };

@@ -60,7 +60,7 @@ ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
         const int gv = (int)std::max<int64_t>(1, std::min<int64_t>((N / 4 + 255) / 256, 148 * 8));
         const int val = !(ctx->flags & DDKS_FLAG_NO_VALIDATE);
         switch (d) {
-#define MMV(D) case D: ddks::k_minmax_vec<D><<<gv, blk, 0, st>>>((const float*)dP, n_P, (const float*)dQ, n_Q, keys, val, &dres->flag); break;
+#define MMV(D) case D: ddks::k_minmax_vec<D><<<gv, blk, 0, st>>>((const float*)dP, n_P, (const float*)dQ, n_Q, keys, 8, val, &dres->flag); break;
             MMV(1) MMV(2) MMV(3) MMV(4) MMV(5) MMV(6) MMV(7) MMV(8)
 #undef MMV
         }

@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include "ddks_common.cuh"
+#include "ddks_minmax.cuh"
 
 namespace ddks {
 
@@ -66,65 +67,6 @@ __global__ void __launch_bounds__(256) k_minmax(const float* __restrict__ P, con
     }
     __syncthreads();
     if (threadIdx.x < d) {
-        const int m = threadIdx.x;
-        uint32_t a = 0xffffffffu, b = 0u;
-        for (int w = 0; w < 8; ++w) a = min(a, sa[w][m]), b = max(b, sb[w][m]);
-        atomicMin(&keys[m], a);
-        atomicMax(&keys[8 + m], b);
-    }
-}
-
-// The same min / max for one rank holding all points (world == 1) and 16-byte aligned inputs: 4 rows = D float4 per
-// step (dims fixed at compile time), the < 4 leftover rows of each sample scalar.
-template <int D>
-__global__ void __launch_bounds__(256) k_minmax_vec(const float* __restrict__ P, int64_t n_P,
-                                                    const float* __restrict__ Q, int64_t n_Q, uint32_t* keys,
-                                                    int validate, uint32_t* flag) {
-    __shared__ uint32_t sa[8][8], sb[8][8];
-    uint32_t mn[D], mx[D];
-    bool bad = false;
-#pragma unroll
-    for (int m = 0; m < D; ++m) mn[m] = 0xffffffffu, mx[m] = 0u;
-    auto take = [&](float v, int m) {
-        if (validate && !isfinite(v)) bad = true;
-        const uint32_t k = f32_key(v == 0.0f ? 0.0f : v);
-        mn[m] = k < mn[m] ? k : mn[m];
-        mx[m] = k > mx[m] ? k : mx[m];
-    };
-    const int64_t gP = n_P / 4, gQ = n_Q / 4;
-    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < gP + gQ; g += (int64_t)gridDim.x * blockDim.x) {
-        const float4* src = reinterpret_cast<const float4*>(g < gP ? P + g * 4 * D : Q + (g - gP) * 4 * D);
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-            const float4 v = __ldg(src + j);
-            take(v.x, (4 * j + 0) % D);
-            take(v.y, (4 * j + 1) % D);
-            take(v.z, (4 * j + 2) % D);
-            take(v.w, (4 * j + 3) % D);
-        }
-    }
-    if (blockIdx.x == 0 && threadIdx.x < 8) {  // leftover rows
-        const int r = threadIdx.x;
-        const float* row = r < 4 ? (4 * gP + r < n_P ? P + (4 * gP + r) * D : nullptr)
-                                 : (4 * gQ + (r - 4) < n_Q ? Q + (4 * gQ + (r - 4)) * D : nullptr);
-        if (row) {
-#pragma unroll
-            for (int m = 0; m < D; ++m) take(row[m], m);
-        }
-    }
-    if (bad) atomicOr(flag, 1u);
-#pragma unroll
-    for (int m = 0; m < D; ++m) {
-        uint32_t a = mn[m], b = mx[m];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
-            b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
-        }
-        if ((threadIdx.x & 31) == 0) sa[threadIdx.x >> 5][m] = a, sb[threadIdx.x >> 5][m] = b;
-    }
-    __syncthreads();
-    if (threadIdx.x < D) {
         const int m = threadIdx.x;
         uint32_t a = 0xffffffffu, b = 0u;
         for (int w = 0; w < 8; ++w) a = min(a, sa[w][m]), b = max(b, sb[w][m]);
