@@ -97,6 +97,10 @@ class ClockSampler:
         t1 = time.perf_counter()
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        # a very short run can end before nvidia-smi's first row: wait (<= 3 s) for one so there is a clock reading
+        deadline = time.perf_counter() + 3.0
+        while not any(len(r) == 7 for _, r in self.rows) and time.perf_counter() < deadline:
+            time.sleep(0.02)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -108,6 +112,9 @@ class ClockSampler:
         if not rows:
             rows = [r for t, r in self.rows if len(r) == 7 and t <= t1]
             window = "whole run up to the end of the timed region (timed region shorter than the 50 ms period)"
+        if not rows:
+            rows = [r for t, r in self.rows if len(r) == 7][:3]
+            window = "first samples after the timed region (the run ended before nvidia-smi's first row)"
         sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
