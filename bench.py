@@ -127,7 +127,19 @@ def workload(name):
     from paper_2106_13706_b200 import inputs as I
     P, Q = I.config(name)
     return P, Q, {"workload": f"{name}: {I.CONFIG_NAMES[name]}", "n_P": int(P.shape[0]), "n_Q": int(Q.shape[0]),
-                  "d": int(P.shape[1]), "pairs_per_step": int((P.shape[0] + Q.shape[0]) ** 2)}
+                  "d": int(P.shape[1]), "pairs_per_step": int((P.shape[0] + Q.shape[0]) ** 2),
+                  "input_sha256": I.sha256_pq(P, Q)}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def cpu_oracle_sample(P, Q, seconds: float):
@@ -149,7 +161,7 @@ def cpu_oracle_sample(P, Q, seconds: float):
         O.per_origin(P, Q, int(s), int(s) + 64, threads=cores)
         done += 64
     dt = time.perf_counter() - t0
-    return {"value": done * N / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": done * N / dt, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
             "sample": f"{done} origins ({len(starts)} evenly spaced blocks of 64) x all {N} points = {done * N:.3e} "
                       f"pair classifications in {dt:.2f} s, OpenMP over origins on {cores} host threads"}
 
@@ -187,7 +199,7 @@ def cpu_oracle_method(method, P, Q, seconds: float, k: int = 16):
         full = dt * V / nv
         sample = (f"voxels [0, {nv}) of {V} (histogram + literal orthant sums over every voxel) in {dt:.2f} s, "
                   f"scaled to all voxels")
-    return {"value": N / full, "unit": "points/s", "cores": cores, "kind": "oracle",
+    return {"value": N / full, "unit": "points/s", "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
             "sample": sample + f", OpenMP on {cores} host threads"}
 
 
@@ -240,7 +252,8 @@ class Step:
             pooled = np.concatenate([P[I.C4_PERM_PAIR], Q[I.C4_PERM_PAIR]])
             B, n, d = P.shape
             self.cfg = {"workload": f"C4: {I.CONFIG_NAMES['C4']}", "B": B, "n_P": n, "n_Q": n, "d": d,
-                        "n_perm": int(perms.shape[0]),
+                        "n_perm": int(perms.shape[0]), "input_sha256": I.sha256_pq(P, Q),
+                        "perms_sha256": __import__("hashlib").sha256(perms.tobytes()).hexdigest(),
                         "pairs_per_step": int(B * (2 * n) ** 2 + perms.shape[0] * (2 * n) ** 2)}
             self.host = (P, Q, pooled, perms)
             self.dev = tuple(torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in self.host)
@@ -275,7 +288,7 @@ class Step:
             self.metric = f"{m} statistic throughput (pooled points/s)"
             self.unit, self.units = "points/s", N
 
-    def roofline(self, kern_ms, kern_launches, kern_pairs, step_ms, peaks_):
+    def roofline(self, kern_ms, kern_launches, kern_pairs, step_ms, peaks_, executed=0):
         d = self.cfg["d"]
         sm_max = float(peaks_.get("sm_max_mhz", 1965.0))
         if self.args.method in ("exact", "significance"):
@@ -283,11 +296,24 @@ class Step:
             pairs_per_launch = kern_pairs / max(kern_launches, 1)
             achieved = d * pairs_per_launch / (per_launch_ms / 1e3) / 1e12  # T compares / s (per GPU)
             peak = N_SM * FSET_LANES_PER_CLK_PER_SM * sm_max * 1e6 / 1e12
-            return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tcompare/s", "frac": achieved / peak,
-                    "kernel": "k_count / k_perm_count (classify + count)", "kernel_ms_per_launch": per_launch_ms,
-                    "kernel_launches_per_step": kern_launches / max(self.args.steps, 1),
-                    "peak_source": f"{N_SM} SMs x {FSET_LANES_PER_CLK_PER_SM} FSET lanes/clk/SM x {sm_max} MHz "
-                                   "(MEASURED_PEAKS.json sm_max_mhz; lane rate measured by microbench/pipes.cu)"}
+            r = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tcompare/s", "frac": achieved / peak,
+                 "frac_note": "algorithmic work (SURVEY §8d): d FP32 compares per pair classification; with the kd "
+                              "ordering fewer compares are executed, so this can exceed 1 -- executed_frac is the "
+                              "hardware-side figure",
+                 "kernel": "k_count / k_perm_count (classify + count)", "kernel_ms_per_launch": per_launch_ms,
+                 "kernel_launches_per_step": kern_launches / max(self.args.steps, 1),
+                 "peak_source": f"{N_SM} SMs x {FSET_LANES_PER_CLK_PER_SM} FSET lanes/clk/SM x {sm_max} MHz "
+                                "(MEASURED_PEAKS.json sm_max_mhz; lane rate measured by microbench/pipes.cu)"}
+            if executed and kern_ms:
+                # compares the kernels EXECUTED (counted in-kernel, every lane of every warp: ddks_profile_work), over
+                # the same ALU-pipe compare peak: a fraction that bounds the kernel whatever ordering ran
+                ex = executed / (kern_ms / 1e3) / 1e12
+                r["executed"] = {"compares_per_pair": executed / max(kern_pairs, 1), "achieved": ex, "peak": peak,
+                                 "unit": "Tcompare/s", "frac": ex / peak,
+                                 "source": "in-kernel count of executed FP32 compares (ddks_profile_work) over the "
+                                           "kernel's CUDA-event time, this run"}
+                r["executed_frac"] = ex / peak
+            return r
         N = self.N
         if self.args.method == "vdks":
             V = self.args.vdks_k ** d
@@ -362,6 +388,7 @@ def main():
         res = step.call(*step.dev)
     ctx.profile_read()  # discard warm-up profile
     ctx.profile_clock()
+    ctx.profile_work()
     barrier()
     clocks.mark()
     launches0 = ctx.launch_count
@@ -381,6 +408,7 @@ def main():
     t_wall = time.perf_counter() - t_wall0
     launches = ctx.launch_count - launches0
     kern_ms, kern_launches, kern_pairs = ctx.profile_read()
+    executed = ctx.profile_work()
     clk = clocks.stop()
     if args.method in ("exact", "significance"):
         # the SM clock the count kernel actually ran at (one clock64 / %globaltimer probe per CTA)
@@ -413,7 +441,7 @@ def main():
 
     pk = peaks()
     kern_ms_max = max_over_ranks(kern_ms)
-    roof = step.roofline(kern_ms, kern_launches, kern_pairs, total_ms / args.steps, pk)
+    roof = step.roofline(kern_ms, kern_launches, kern_pairs, total_ms / args.steps, pk, executed)
     if args.method in ("exact", "significance"):
         roof["kernel_share_of_step"] = kern_ms_max / total_ms if total_ms else None
         roof["kd_levels"] = ctx.kd_levels
@@ -421,24 +449,16 @@ def main():
             roof["note"] = (f"kd ordering: bits 0..{ctx.kd_levels - 1} are decided once per tile for most tiles, so fewer "
                             "than d compares are executed per pair and frac (algorithmic d compares per pair) can "
                             "exceed 1; DESIGN.md §7 'kd ordering'")
+    # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture of this workload
+    # (profiles/traffic.json), used only when it was taken on the kernel variant that ran here (kd levels match)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp) and args.method == "exact":
         try:
-            tj = json.load(open(tp))
-            traffic = tj.get(args.workload)
-            ipp = tj.get(f"{args.workload}_detail", {}).get("per_pair", {}).get("thread_instructions")
-            if ipp and kern_ms:
-                # issue-side view of the same kernel: live pair rate x ncu-measured instructions per pair vs the SM
-                # issue peak (4 warp-instructions / clk / SM)
-                sm_max = float(pk.get("sm_max_mhz", 1965.0))
-                rate = kern_pairs / (kern_ms / 1e3)
-                ach = rate * ipp / 32.0
-                peak_i = N_SM * 4 * sm_max * 1e6
-                roof["issue"] = {"instr_per_pair": round(ipp, 3), "achieved_warp_inst_per_s": ach,
-                                 "peak_warp_inst_per_s": peak_i, "frac": ach / peak_i,
-                                 "source": "thread instructions per pair from ncu smsp__inst_executed.sum of one "
-                                           "full-size launch (profiles/traffic.json); pair rate measured live"}
+            tj = json.load(open(tp)).get(args.workload)
+            if isinstance(tj, dict) and tj.get("kd_levels") == ctx.kd_levels:
+                traffic = tj.get("dram_bytes_per_launch")
+                roof["traffic_source"] = tj.get("source")
         except Exception:
             traffic = None
     roof = dict({k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac")}, traffic=traffic,

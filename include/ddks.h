@@ -23,13 +23,15 @@
  *   - A context is bound to one device and one host thread; it is not thread-safe.
  *   - Multi-GPU (world > 1): every rank makes the same call with the same (replicated) inputs.
  *       ddks_stat /              shard the pooled ORIGINS -- `world` contiguous ranges of the pooled order, or, when
- *       ddks_significance        the kd-ordered count runs (N >= 80000, 2 <= d <= 8), the origin blocks r, r + world,
- *                                r + 2 world, ... of the kd order (every rank computes the same order) -- and combine
- *                                the per-rank maxima with one NCCL all-reduce(max) of a uint64 (+ one all-reduce(min)
- *                                for the argmax); the significance also all-reduces its M_T histogram.
+ *       ddks_significance        the kd-ordered count runs (2 <= d <= 8 and N large enough), the origin blocks r,
+ *                                r + world, r + 2 world, ... of the kd order (every rank computes the same order).
+ *                                ddks_stat combines with ONE collective: an ncclAllGather of every rank's 32-byte record
+ *                                {num, argmax candidate, flags}, reduced on the host by ddks_combine_records; the
+ *                                significance all-reduces num, the argmax candidate, the flags and its M_T histogram.
  *       ddks_stat_batch /
- *       ddks_permutation_null    shard ITEMS (pairs / permutations) contiguously and all-gather the per-item nums,
- *                                so every rank returns the full result.
+ *       ddks_permutation_null    shard ITEMS (pairs / permutations) contiguously and gather the per-item nums plus the
+ *                                rank's flags in ONE ncclAllGather of records padded to the largest shard (unpadded on
+ *                                the host by ddks_unpad_items), so every rank returns the full result.
  *       ddks_vdks / ddks_rdks    shard points + voxels / corners (see each call).
  *   - Limits: 1 <= d <= 8 (ddks_rdks: any d >= 1); n_P, n_Q >= 1; n_P + n_Q < 2^31; n_P*n_Q < 2^53 (so D is one
  *     exact IEEE division).
@@ -77,8 +79,9 @@ typedef enum {
                                       pooled points hierarchically by x_0 .. x_{K-1} when 2 <= d <= 8 and N >= 80000, 
                                       so whole tiles share those bits; identical results)                          */
 #define DDKS_FLAG_FORCE_X0 64u     /* TEST ONLY: use the kd-ordered count for any N (2 <= d <= 8)                      */
-#define DDKS_FLAG_KD_SHIFT 9u      /* TEST ONLY: bits 9..10 = K in 1..3 force the number of kd levels (0: cost model) */
-#define DDKS_FLAG_KD_LEVELS(k) ((unsigned)(k) << DDKS_FLAG_KD_SHIFT)
+#define DDKS_FLAG_KD_SHIFT 16u     /* TEST ONLY: bits 16..18 = K in 1..4 force the number of kd levels (0: cost model;
+                                      K is capped at d and at the deepest level built, 4)                           */
+#define DDKS_FLAG_KD_LEVELS(k) (((unsigned)(k) & 7u) << DDKS_FLAG_KD_SHIFT)
 #define DDKS_FLAG_NO_GRAPH 4096u   /* never capture ddks_stat into a CUDA graph (by default the second identical call --
                                       same input pointers, sizes and workspace -- is captured and later calls replay it
                                       with one cudaGraphLaunch; identical results)                                     */
@@ -194,6 +197,27 @@ DDKS_API ddks_status ddks_stat_shard(ddks_ctx* ctx, const float* P, int64_t n_P,
  * owns out of `total` units. Ranges are balanced to within one unit and cover 0..total exactly. */
 DDKS_API ddks_status ddks_shard_range(int64_t total, int world, int rank, int64_t* begin, int64_t* end);
 
+/* ---- Multi-GPU combine steps (host-only, no GPU needed; the library calls them after its one all-gather, and they
+ * are exported so the combine logic can be tested and reused with any transport, e.g. torch.distributed gloo) ---- */
+typedef struct {
+    uint64_t num;          /* this rank's max num(o) over its origin shard (0 if the shard is empty)            */
+    int64_t argmax_origin; /* smallest pooled origin of the shard attaining num; -1 if none                     */
+    uint32_t flags;        /* bit 0: non-finite input, bit 1: bad permutation row                              */
+    uint32_t reserved;
+} ddks_rank_record;
+
+/* Combine the `world` per-rank records of one statistic (the max over the union of the origin shards):
+ * out->num = max num; out->argmax_origin = the smallest argmax among the records attaining it (-1 if none);
+ * out->flags = OR of the flags. recs: host [world]. */
+DDKS_API ddks_status ddks_combine_records(const ddks_rank_record* recs, int world, ddks_rank_record* out);
+
+/* Unpad the all-gathered per-item block of a sharded batch / permutation / batched-significance call. Layout: world
+ * records of stride = n_arr * chunk + 1 uint64, chunk = ceil(total / world) (rank 0's shard, the largest); record r
+ * holds rank r's slice ddks_shard_range(total, world, r) of each of the n_arr arrays, each padded to chunk, then
+ * rank r's flags word. out: host [n_arr][total]; *flags (may be NULL) = OR of the ranks' flags. */
+DDKS_API ddks_status ddks_unpad_items(const uint64_t* gathered, int64_t total, int world, int n_arr, uint64_t* out,
+                                      uint32_t* flags);
+
 /* Number of kernels the library launched on this context since creation (for the bench's gpu_launches). */
 DDKS_API int64_t ddks_launch_count(const ddks_ctx* ctx);
 
@@ -212,6 +236,13 @@ DDKS_API ddks_status ddks_profile_read(ddks_ctx* ctx, double* count_ms, int64_t*
  * %globaltimer around its classify+count loop; *sm_mhz = summed SM cycles / summed ns over those CTAs since the last
  * read (0 if none), i.e. the SM clock the counting actually ran at. Resets the totals. */
 DDKS_API ddks_status ddks_profile_clock(ddks_ctx* ctx, double* sm_mhz);
+
+/* Executed work of the count kernels (context created with DDKS_FLAG_PROFILE), totals since the last read, then reset:
+ * *compares = FP32 orthant compares the classify kernels actually executed (every lane of every warp, clamped tail
+ * slots included; the bits the kd / warp-level orderings decide once per tile or sub-tile are not compares). The
+ * method's algorithmic work is d compares per pair classification; with the kd ordering the executed count is lower.
+ * Counted in-kernel (one add per warp and tile), so it tracks whichever kernel variant ran. */
+DDKS_API ddks_status ddks_profile_work(ddks_ctx* ctx, uint64_t* compares);
 
 /* Destroy a context (NULL-safe). Frees workspace and the NCCL communicator. */
 DDKS_API ddks_status ddks_destroy(ddks_ctx* ctx);

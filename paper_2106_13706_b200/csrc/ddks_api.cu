@@ -55,6 +55,22 @@ ddks_status ensure(ddks_ctx* ctx, DevBuf& b, size_t bytes) {
     return DDKS_OK;
 }
 
+ddks_status ensure_zeroed(ddks_ctx* ctx, DevBuf& b, size_t bytes, cudaStream_t st) {
+    if (bytes <= b.bytes) return DDKS_OK;
+    ddks_status s = ensure(ctx, b, bytes);
+    if (s) return s;
+    CU(cudaMemsetAsync(b.p, 0, b.bytes, st));
+    return DDKS_OK;
+}
+
+ddks_status ensure_prof(ddks_ctx* ctx) {
+    if (ctx->prof_clk.p) return DDKS_OK;
+    ddks_status s = ensure(ctx, ctx->prof_clk, 32);
+    if (s) return s;
+    CU(cudaMemset(ctx->prof_clk.p, 0, 32));
+    return DDKS_OK;
+}
+
 bool is_device_ptr(const void* p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -117,7 +133,7 @@ ddks_status launch_count_d(ddks_ctx* ctx, const CountPlan& pl, const ddks::Count
 // force_split + hist (significance): SPLIT counters, and the finaliser histograms c_Q into hist[n_Q + 1].
 ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int64_t n_P, int64_t n_Q,
                       int64_t o_begin, int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st,
-                      bool force_split, unsigned long long* hist, bool wx) {
+                      bool force_split, unsigned long long* hist, bool wx, unsigned long long* best_key) {
     const int64_t N = n_P + n_Q;
     const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
     const uint64_t a_ = (uint64_t)n_Q / g, b_ = (uint64_t)n_P / g;
@@ -143,6 +159,8 @@ ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int6
     a.per_origin = per_origin;
     a.hist = split ? hist : nullptr;
     a.hist_stride = n_Q + 1;
+    a.best_key = B == 1 ? best_key : nullptr;
+    a.key_div = g;
     if (B > 65535) {  // grid.z limit: run the items in chunks
         for (int64_t b0 = 0; b0 < B; b0 += 65535) {
             const int64_t nb = std::min<int64_t>(65535, B - b0);
@@ -200,33 +218,49 @@ bool x0_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q) {
 
 ddks_status run_count_kd(ddks_ctx* ctx, const float* packed, int d, int64_t n_P, int64_t n_Q, int sw, int sr,
                          uint64_t* item_num, uint64_t* per_origin, cudaStream_t st, bool split,
-                         unsigned long long* hist) {
+                         unsigned long long* hist, unsigned long long* best_key) {
     switch (d) {
-#define KD_CASE(D) case D: return run_count_kd_d<D>(ctx, packed, n_P, n_Q, sw, sr, item_num, per_origin, st, split, hist);
+#define KD_CASE(D) case D: return run_count_kd_d<D>(ctx, packed, n_P, n_Q, sw, sr, item_num, per_origin, st, split, hist, best_key);
         KD_CASE(2) KD_CASE(3) KD_CASE(4) KD_CASE(5) KD_CASE(6) KD_CASE(7) KD_CASE(8)
 #undef KD_CASE
     }
     return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "kd mode d=%d", d);
 }
 
-// One statistic (B == 1) over the origin shard [ob, oe) of this rank: count (x0-ordered when it applies, else
-// position-ordered), then -- unless export_per (debug export of per-origin nums for [ob, oe)) -- the NCCL max of
-// num and this rank's argmax candidate into dres->arg (min-combined by the caller). split/hist: significance.
+bool argmax_key_fits(int64_t n_P, int64_t n_Q) {
+    if (getenv("DDKS_NO_KEY")) return false;  // TEST ONLY: per-origin nums + k_argmax for any size
+    const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
+    return (double)n_P * (double)n_Q / (double)g < 8589934592.0;  // num / g < 2^33: the packed key fits 64 bits
+}
+
+// One statistic (B == 1) over the origin shard [ob, oe) of this rank: count (kd-ordered when it applies, else
+// position-ordered) into dres->num and, unless export_per (debug export of per-origin nums for [ob, oe)), this rank's
+// argmax candidate: fused into the count kernel as the packed key dres->key when it fits (argmax_key_fits), else
+// per-origin nums + k_argmax into dres->arg. No collective unless reduce_num_first (significance: the global num is
+// all-reduced before the k_argmax path matches against it). split/hist: significance.
 ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n_P, int64_t n_Q, int64_t ob,
                             int64_t oe, int sw, int sr, DevResult* dres, bool export_per, bool split,
-                            unsigned long long* hist, cudaStream_t st, uint64_t** per_out) {
+                            unsigned long long* hist, cudaStream_t st, uint64_t** per_out, bool reduce_num_first) {
     const int64_t N = n_P + n_Q;
     ddks_status s;
+    const bool use_key = !export_per && argmax_key_fits(n_P, n_Q);
+    unsigned long long* key = use_key ? &dres->key : nullptr;
     const bool x0 = !export_per && x0_applicable(ctx, d, n_P, n_Q);
+    *per_out = nullptr;
     if (x0) {
-        // origins are positions of the x_0 order; per-origin nums land in pooled order in per[N] (zeros elsewhere)
-        if ((s = ensure(ctx, ctx->per_origin, (size_t)N * 8))) return s;
-        uint64_t* per = (uint64_t*)ctx->per_origin.p;
+        // origins are positions of the kd order; per-origin nums (k_argmax path only) land in pooled order in per[N]
+        uint64_t* per = nullptr;
+        if (!use_key) {
+            if ((s = ensure(ctx, ctx->per_origin, (size_t)N * 8))) return s;
+            per = (uint64_t*)ctx->per_origin.p;
+            CU(cudaMemsetAsync(per, 0, (size_t)N * 8, st));
+        }
         *per_out = per;
         // SPLIT counters when the significance needs c_Q or DIFF counters would overflow (as in run_count)
         const bool sp = split || !diff_counters_ok(n_P, n_Q);
-        if ((s = run_count_kd(ctx, packed, d, n_P, n_Q, sw, sr, (uint64_t*)&dres->num, per, st, sp, hist))) return s;
-        if (ctx->comm) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
+        if ((s = run_count_kd(ctx, packed, d, n_P, n_Q, sw, sr, (uint64_t*)&dres->num, per, st, sp, hist, key))) return s;
+        if (use_key) return DDKS_OK;
+        if (ctx->comm && reduce_num_first) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
         ddks::k_argmax<<<(int)std::min<int64_t>((N + 255) / 256, 148 * 4), 256, 0, st>>>(
             per, N, 0, (const uint64_t*)&dres->num, &dres->arg);
         CHECK_LAUNCH();
@@ -234,13 +268,17 @@ ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n
         return DDKS_OK;
     }
     ctx->kd_levels = 0;
-    if ((s = ensure(ctx, ctx->per_origin, (size_t)std::max<int64_t>(oe - ob, 1) * 8))) return s;
-    uint64_t* per = (uint64_t*)ctx->per_origin.p;
+    uint64_t* per = nullptr;
+    if (!use_key) {
+        if ((s = ensure(ctx, ctx->per_origin, (size_t)std::max<int64_t>(oe - ob, 1) * 8))) return s;
+        per = (uint64_t*)ctx->per_origin.p;
+    }
     *per_out = per;
-    if (oe > ob && (s = run_count(ctx, packed, d, 1, n_P, n_Q, ob, oe, (uint64_t*)&dres->num, per, st, split, hist)))
+    if (oe > ob && (s = run_count(ctx, packed, d, 1, n_P, n_Q, ob, oe, (uint64_t*)&dres->num, per, st, split, hist,
+                                  false, key)))
         return s;
-    if (export_per) return DDKS_OK;
-    if (ctx->comm) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
+    if (export_per || use_key) return DDKS_OK;
+    if (ctx->comm && reduce_num_first) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
     if (oe > ob) {
         ddks::k_argmax<<<(int)std::min<int64_t>((oe - ob + 255) / 256, 148 * 4), 256, 0, st>>>(
             per, oe - ob, ob, (const uint64_t*)&dres->num, &dres->arg);
@@ -248,6 +286,21 @@ ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n
         ctx->launches++;
     }
     return DDKS_OK;
+}
+
+// A rank's device result block -> its host record (decodes the packed argmax key when the fused path ran).
+ddks_rank_record decode_record(const DevResult& r, int64_t n_P, int64_t n_Q, bool use_key) {
+    ddks_rank_record o{};
+    o.flags = r.flag;
+    if (use_key) {
+        const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
+        o.num = (r.key >> 31) * g;
+        o.argmax_origin = r.key ? (int64_t)(0x7fffffffull - (r.key & 0x7fffffffull)) : -1;
+    } else {
+        o.num = r.num;
+        o.argmax_origin = r.arg == ~0ull ? -1 : (int64_t)r.arg;
+    }
+    return o;
 }
 
 ddks_status launch_pack(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d, int64_t B,
@@ -318,12 +371,20 @@ ddks_status launch_perm_d(ddks_ctx* ctx, const float* pooled_packed, const int32
     pa.b = (uint32_t)((uint64_t)n_P / g);
     pa.g = g;
     pa.num = nums;
+    pa.clk = nullptr;
     dim3 grid((unsigned)chunks, (unsigned)((N + G::T - 1) / G::T));
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
     if (ctx->flags & DDKS_FLAG_PROFILE) {
-        CU(cudaEventCreate(&ev.first));
-        CU(cudaEventCreate(&ev.second));
+        if (!ctx->ev_free.empty()) {
+            ev = ctx->ev_free.back();
+            ctx->ev_free.pop_back();
+        } else {
+            CU(cudaEventCreate(&ev.first));
+            CU(cudaEventCreate(&ev.second));
+        }
         CU(record_event(ev.first, st));
+        if ((s = ensure_prof(ctx))) return s;
+        pa.clk = (unsigned long long*)ctx->prof_clk.p;
     }
     kern<<<grid, G::T, G::SMEM_BYTES, st>>>(pa);
     CHECK_LAUNCH();
@@ -385,26 +446,33 @@ ddks_status bind_device(ddks_ctx* ctx) {
     return DDKS_OK;
 }
 
-// Items [i0, i1) of an already-packed batch -> nums into dev item_num[i0..i1).
-ddks_status all_gather_items(ddks_ctx* ctx, uint64_t* dev_nums, int64_t total, cudaStream_t st) {
-    // every rank owns a contiguous shard; NCCL all-gather needs equal counts -> pad to the largest shard
+// Items sharded contiguously over the ranks (ddks_shard_range): ONE ncclAllGather of a padded per-rank record --
+// this rank's slice of each of the n_arr device arrays dev[k][total] (8-byte elements), each padded to chunk = rank 0's
+// (largest) shard, then this rank's flag word -- into ctx->gather, copied to host hbuf[world * stride] (stride =
+// n_arr * chunk + 1). The caller unpads it with ddks_unpad_items (host), which also ORs the flags.
+ddks_status gather_items(ddks_ctx* ctx, uint64_t* const* dev, int n_arr, int64_t total, const uint32_t* dflag,
+                         cudaStream_t st, uint64_t* hbuf) {
     int64_t b0, b1;
     ddks_shard_range(total, ctx->world, 0, &b0, &b1);
-    const int64_t chunk = b1 - b0;  // rank 0 holds the largest shard
-    ddks_status s = ensure(ctx, ctx->packed2, (size_t)chunk * ctx->world * 8);
+    const int64_t chunk = b1 - b0;
+    const int64_t stride = chunk * n_arr + 1;
+    ddks_status s = ensure(ctx, ctx->gather, (size_t)(ctx->world + 1) * stride * 8);
     if (s) return s;
+    uint64_t* all = (uint64_t*)ctx->gather.p;
+    uint64_t* send = all + (int64_t)ctx->world * stride;
     int64_t mb, me;
     ddks_shard_range(total, ctx->world, ctx->rank, &mb, &me);
-    uint64_t* gathered = (uint64_t*)ctx->packed2.p;
-    NC(ncclAllGather(dev_nums + mb, gathered, (size_t)chunk, ncclUint64, ctx->comm, st));
-    for (int r = 0; r < ctx->world; ++r) {
-        int64_t rb, re;
-        ddks_shard_range(total, ctx->world, r, &rb, &re);
-        if (re > rb)
-            CU(cudaMemcpyAsync(dev_nums + rb, gathered + (int64_t)r * chunk, (size_t)(re - rb) * 8,
-                               cudaMemcpyDeviceToDevice, st));
-    }
+    CU(cudaMemsetAsync(send, 0, (size_t)stride * 8, st));
+    for (int k = 0; k < n_arr; ++k)
+        if (me > mb) CU(cudaMemcpyAsync(send + k * chunk, dev[k] + mb, (size_t)(me - mb) * 8, cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpyAsync(send + n_arr * chunk, dflag, 4, cudaMemcpyDeviceToDevice, st));
+    NC(ncclAllGather(send, all, (size_t)stride, ncclUint64, ctx->comm, st));
+    CU(cudaMemcpyAsync(hbuf, all, (size_t)ctx->world * stride * 8, cudaMemcpyDeviceToHost, st));
     return DDKS_OK;
+}
+
+int64_t gather_stride(int64_t total, int world, int n_arr) {
+    return (total / world + (total % world ? 1 : 0)) * n_arr + 1;
 }
 
 }  // namespace ddks_host
@@ -421,6 +489,40 @@ ddks_status ddks_shard_range(int64_t total, int world, int rank, int64_t* begin,
     const int64_t base = total / world, rem = total % world;
     *begin = rank * base + std::min<int64_t>(rank, rem);
     *end = *begin + base + (rank < rem ? 1 : 0);
+    return DDKS_OK;
+}
+
+ddks_status ddks_combine_records(const ddks_rank_record* recs, int world, ddks_rank_record* out) {
+    if (!recs || !out || world < 1) return DDKS_ERR_INVALID_ARGUMENT;
+    ddks_rank_record r{0ull, -1, 0u, 0u};
+    for (int i = 0; i < world; ++i) {
+        r.flags |= recs[i].flags;
+        if (recs[i].num > r.num) r.num = recs[i].num;
+    }
+    for (int i = 0; i < world; ++i)
+        if (recs[i].num == r.num && recs[i].argmax_origin >= 0 &&
+            (r.argmax_origin < 0 || recs[i].argmax_origin < r.argmax_origin))
+            r.argmax_origin = recs[i].argmax_origin;
+    *out = r;
+    return DDKS_OK;
+}
+
+ddks_status ddks_unpad_items(const uint64_t* gathered, int64_t total, int world, int n_arr, uint64_t* out,
+                             uint32_t* flags) {
+    if (!gathered || !out || total < 0 || world < 1 || n_arr < 1) return DDKS_ERR_INVALID_ARGUMENT;
+    int64_t b0, b1;
+    ddks_shard_range(total, world, 0, &b0, &b1);
+    const int64_t chunk = b1 - b0, stride = chunk * n_arr + 1;
+    uint32_t f = 0;
+    for (int r = 0; r < world; ++r) {
+        int64_t rb, re;
+        ddks_shard_range(total, world, r, &rb, &re);
+        const uint64_t* rec = gathered + (int64_t)r * stride;
+        for (int k = 0; k < n_arr; ++k)
+            for (int64_t i = rb; i < re; ++i) out[(int64_t)k * total + i] = rec[(int64_t)k * chunk + (i - rb)];
+        f |= (uint32_t)rec[(int64_t)n_arr * chunk];
+    }
+    if (flags) *flags = f;
     return DDKS_OK;
 }
 
@@ -441,7 +543,7 @@ ddks_status ddks_create(ddks_ctx** out, int device, int world, int rank, const v
     if (world < 1 || rank < 0 || rank >= world) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad world/rank");
     if ((world == 1) != (nccl_id == nullptr))
         return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "nccl_id must be NULL iff world == 1");
-    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT | DDKS_FLAG_PROFILE | DDKS_FLAG_PERM_GATHER | DDKS_FLAG_NO_X0 | DDKS_FLAG_FORCE_X0 | DDKS_FLAG_RDKS_FULL_SORT | DDKS_FLAG_KD_LEVELS(3) | DDKS_FLAG_NCCL_SELF | DDKS_FLAG_NO_GRAPH)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
+    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT | DDKS_FLAG_PROFILE | DDKS_FLAG_PERM_GATHER | DDKS_FLAG_NO_X0 | DDKS_FLAG_FORCE_X0 | DDKS_FLAG_RDKS_FULL_SORT | DDKS_FLAG_KD_LEVELS(7) | DDKS_FLAG_NCCL_SELF | DDKS_FLAG_NO_GRAPH)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
     int ndev = 0;
     CU(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device %d of %d", device, ndev);
@@ -500,7 +602,7 @@ ddks_status ddks_destroy(ddks_ctx* ctx) {
             cudaEventDestroy(ctx->ev_pending[i].second);
         }
     for (DevBuf* b : {&ctx->raw_a, &ctx->raw_b, &ctx->raw_perm, &ctx->packed, &ctx->packed2, &ctx->pool_packed, &ctx->per_origin,
-                      &ctx->accum, &ctx->item_num, &ctx->bitmap, &ctx->labels, &ctx->res, &ctx->sig_hist,
+                      &ctx->accum, &ctx->blk_done, &ctx->gather, &ctx->item_num, &ctx->bitmap, &ctx->labels, &ctx->res, &ctx->sig_hist,
                       &ctx->sig_lf, &ctx->sig_scratch, &ctx->sig_table, &ctx->sig_contrib, &ctx->sig_part,
                       &ctx->vox_keys, &ctx->vox_cnt, &ctx->vox_S, &ctx->rd_keys, &ctx->rd_xn, &ctx->rd_k0,
                       &ctx->rd_k1, &ctx->rd_hist, &ctx->rd_tcnt, &ctx->rd_cnum, &ctx->x0_keys0,
@@ -546,8 +648,23 @@ ddks_status ddks_profile_clock(ddks_ctx* ctx, double* sm_mhz) {
     return DDKS_OK;
 }
 
-// Enqueue one statistic on st, ending with the D2H of the result block into host_pinned (no sync): staging of host
-// inputs, pack, count, finalise, argmax, collectives. Everything here is stream-ordered, so it can be captured.
+ddks_status ddks_profile_work(ddks_ctx* ctx, uint64_t* compares) {
+    if (!ctx || !compares) return DDKS_ERR_INVALID_ARGUMENT;
+    *compares = 0;
+    if (!ctx->prof_clk.p) return DDKS_OK;
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaDeviceSynchronize());
+    unsigned long long c = 0;
+    CU(cudaMemcpy(&c, (unsigned long long*)ctx->prof_clk.p + 2, 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemset((unsigned long long*)ctx->prof_clk.p + 2, 0, 8));
+    *compares = c;
+    return DDKS_OK;
+}
+
+// Enqueue one statistic on st, ending with the D2H of the result record(s) into host_pinned (no sync): staging of host
+// inputs, pack, count (+ fused argmax), and with world > 1 the ONE collective: the all-gather of every rank's 32-byte
+// result record (host_pinned then holds world records, combined by ddks_combine_records after the sync). Everything
+// here is stream-ordered, so it can be captured.
 static ddks_status stat_enqueue(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
                                 cudaStream_t st, int64_t ob, int64_t oe, uint64_t* per_origin_out, int sw, int sr) {
     ddks_status s;
@@ -558,23 +675,28 @@ static ddks_status stat_enqueue(ddks_ctx* ctx, const float* P, int64_t n_P, cons
     if ((s = stage_input(ctx, P, (size_t)n_P * d * 4, ctx->raw_a, st, &dP))) return s;
     if ((s = stage_input(ctx, Q, (size_t)n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
     if ((s = ensure(ctx, ctx->packed, (size_t)N * DP * 4))) return s;
-    if ((s = ensure(ctx, ctx->per_origin, (size_t)std::max<int64_t>(oe - ob, 1) * 8))) return s;
+    const bool gather = ctx->comm && !export_mode;
+    if (gather && (s = ensure(ctx, ctx->gather, (size_t)ctx->world * sizeof(DevResult)))) return s;
     DevResult* dres = (DevResult*)ctx->res.p;
     DevResult* hres = (DevResult*)ctx->host_pinned;
-    *hres = DevResult{0ull, ~0ull, 0u, 0u};  // re-written by the host before every graph replay as well
+    *hres = DevResult{0ull, ~0ull, 0ull, 0u, 0u};  // re-written by the host before every graph replay as well
     CU(cudaMemcpyAsync(dres, hres, sizeof(DevResult), cudaMemcpyHostToDevice, st));
     float* packed = (float*)ctx->packed.p;
     if ((s = launch_pack(ctx, (const float*)dP, n_P, (const float*)dQ, n_Q, d, 1, packed, &dres->flag, st))) return s;
     uint64_t* per = nullptr;
-    if ((s = count_statistic(ctx, packed, d, n_P, n_Q, ob, oe, sw, sr, dres, export_mode, false, nullptr, st, &per))) return s;
-    if (ctx->comm && !export_mode) {
-        NC(ncclAllReduce(&dres->arg, &dres->arg, 1, ncclUint64, ncclMin, ctx->comm, st));
-        NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
-    }
+    if ((s = count_statistic(ctx, packed, d, n_P, n_Q, ob, oe, sw, sr, dres, export_mode, false, nullptr, st, &per,
+                             false)))
+        return s;
     if (export_mode && oe > ob) {
         CU(cudaMemcpyAsync(per_origin_out, per, (size_t)(oe - ob) * 8, cudaMemcpyDefault, st));
     }
-    CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+    if (gather) {
+        static_assert(sizeof(DevResult) % 8 == 0, "record of uint64 words");
+        NC(ncclAllGather(dres, ctx->gather.p, sizeof(DevResult) / 8, ncclUint64, ctx->comm, st));
+        CU(cudaMemcpyAsync(hres, ctx->gather.p, (size_t)ctx->world * sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+    } else {
+        CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+    }
     return DDKS_OK;
 }
 
@@ -666,7 +788,11 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
         ddks_shard_range(N, ctx->world, ctx->rank, &ob, &oe);
     }
     const int sw = shard_world > 0 ? shard_world : ctx->world, sr = shard_world > 0 ? shard_rank : ctx->rank;
-    const bool graphable = !export_mode && shard_world == 0 && !(ctx->flags & DDKS_FLAG_NO_GRAPH) &&
+    if ((s = ensure_host(ctx, std::max<size_t>(4096, (size_t)ctx->world * sizeof(DevResult))))) return s;
+    // environment overrides (tuning / test knobs) change the plan: a graph captured under other values is not reused
+    const bool env_override = getenv("DDKS_KD") || getenv("DDKS_SEGS") || getenv("DDKS_KD_SHUFFLE") ||
+                              getenv("DDKS_NO_KEY") || getenv("DDKS_GRIDY");
+    const bool graphable = !export_mode && shard_world == 0 && !(ctx->flags & DDKS_FLAG_NO_GRAPH) && !env_override &&
                            graph_input_ok(P) && graph_input_ok(Q);
     const ddks_ctx::StatKey key{P, Q, n_P, n_Q, d, ctx->alloc_epoch};
     bool replay = graphable && ctx->sg_exec && ctx->sg_key == key;
@@ -676,7 +802,7 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
     DevResult* hres;
     if (replay) {
         hres = (DevResult*)ctx->host_pinned;
-        *hres = DevResult{0ull, ~0ull, 0u, 0u};  // the graph's first node copies it to the device
+        *hres = DevResult{0ull, ~0ull, 0ull, 0u, 0u};  // the graph's first node copies it to the device
         CU(cudaGraphLaunch(ctx->sg_exec, st));
         ctx->launches += ctx->sg_launches;
         ctx->kd_levels = ctx->sg_kd_levels;
@@ -695,12 +821,24 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
     }
     CU(cudaStreamSynchronize(st));
     if ((s = collect_profile(ctx))) return s;
-    if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
+    // this rank's record, or (world > 1) the all-gathered records of every rank, combined on the host
+    const bool use_key = !export_mode && argmax_key_fits(n_P, n_Q);
+    const int nrec = (ctx->comm && !export_mode) ? ctx->world : 1;
+    ddks_rank_record recs[64], comb;
+    std::vector<ddks_rank_record> big;
+    ddks_rank_record* rp = recs;
+    if (nrec > 64) {
+        big.resize(nrec);
+        rp = big.data();
+    }
+    for (int r = 0; r < nrec; ++r) rp[r] = decode_record(hres[r], n_P, n_Q, use_key);
+    ddks_combine_records(rp, nrec, &comb);
+    if (comb.flags & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
     if (out) {
-        out->num = hres->num;
+        out->num = comb.num;
         out->den = (uint64_t)n_P * (uint64_t)n_Q;
         out->D = (double)out->num / (double)out->den;
-        out->argmax_origin = hres->arg == ~0ull ? -1 : (int64_t)hres->arg;
+        out->argmax_origin = comb.argmax_origin;
     }
     return DDKS_OK;
 }
@@ -766,17 +904,22 @@ ddks_status ddks_stat_batch(ddks_ctx* ctx, const float* P, const float* Q, int64
             return s;
         if ((s = run_count(ctx, packed, d, nb, n_P, n_Q, 0, N, nums + ib, nullptr, st, false, nullptr, wx))) return s;
     }
-    if (ctx->comm) {
-        if ((s = all_gather_items(ctx, nums, B, st))) return s;
-        NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
-    }
-    if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)B * 8))) return s;
+    // world > 1: one all-gather of the padded per-rank records (this rank's nums + its flags), unpadded on the host
+    const int64_t gstride = ctx->comm ? gather_stride(B, ctx->world, 1) : 0;
+    if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)B * 8 + (size_t)ctx->world * gstride * 8))) return s;
     DevResult* hres = (DevResult*)ctx->host_pinned;
     uint64_t* hnums = (uint64_t*)((char*)ctx->host_pinned + sizeof(DevResult));
-    CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(hnums, nums, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
+    uint64_t* hgath = hnums + B;
+    if (ctx->comm) {
+        uint64_t* arrs[1] = {nums};
+        if ((s = gather_items(ctx, arrs, 1, B, &dres->flag, st, hgath))) return s;
+    } else {
+        CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(hnums, nums, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
+    }
     CU(cudaStreamSynchronize(st));
     if ((s = collect_profile(ctx))) return s;
+    if (ctx->comm) ddks_unpad_items(hgath, B, ctx->world, 1, hnums, &hres->flag);
     if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
     const uint64_t den = (uint64_t)n_P * (uint64_t)n_Q;
     for (int64_t b = 0; b < B; ++b) {
@@ -849,17 +992,24 @@ ddks_status ddks_permutation_null(ddks_ctx* ctx, const float* pooled, int64_t n_
                 return s;
         }
     }
-    if (ctx->comm) {
-        if ((s = all_gather_items(ctx, nums + 1, n_perm, st))) return s;
-        NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
-    }
-    if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)total * 8))) return s;
+    // world > 1: the observed num (slot 0) is every rank's own; one all-gather of the padded per-rank records (this
+    // rank's permutation nums + its flags), unpadded on the host
+    const int64_t gstride = ctx->comm ? gather_stride(n_perm, ctx->world, 1) : 0;
+    if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)total * 8 + (size_t)ctx->world * gstride * 8))) return s;
     DevResult* hres = (DevResult*)ctx->host_pinned;
     uint64_t* hnums = (uint64_t*)((char*)ctx->host_pinned + sizeof(DevResult));
-    CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(hnums, nums, (size_t)total * 8, cudaMemcpyDeviceToHost, st));
+    uint64_t* hgath = hnums + total;
+    if (ctx->comm) {
+        uint64_t* arrs[1] = {nums + 1};
+        if ((s = gather_items(ctx, arrs, 1, n_perm, &dres->flag, st, hgath))) return s;
+        CU(cudaMemcpyAsync(hnums, nums, 8, cudaMemcpyDeviceToHost, st));
+    } else {
+        CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(hnums, nums, (size_t)total * 8, cudaMemcpyDeviceToHost, st));
+    }
     CU(cudaStreamSynchronize(st));
     if ((s = collect_profile(ctx))) return s;
+    if (ctx->comm) ddks_unpad_items(hgath, n_perm, ctx->world, 1, hnums + 1, &hres->flag);
     if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
     if (hres->flag & 2u) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "a perms row is not a permutation of 0..N-1");
     const uint64_t obs = hnums[0];

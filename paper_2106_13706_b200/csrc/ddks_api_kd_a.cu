@@ -4,9 +4,9 @@
 
 namespace ddks_host {
 template ddks_status run_count_kd_d<2>(ddks_ctx*, const float*, int64_t, int64_t, int, int, uint64_t*, uint64_t*,
-                                         cudaStream_t, bool, unsigned long long*);
+                                         cudaStream_t, bool, unsigned long long*, unsigned long long*);
 template ddks_status run_count_kd_d<3>(ddks_ctx*, const float*, int64_t, int64_t, int, int, uint64_t*, uint64_t*,
-                                         cudaStream_t, bool, unsigned long long*);
+                                         cudaStream_t, bool, unsigned long long*, unsigned long long*);
 template ddks_status run_count_kd_d<4>(ddks_ctx*, const float*, int64_t, int64_t, int, int, uint64_t*, uint64_t*,
-                                         cudaStream_t, bool, unsigned long long*);
+                                         cudaStream_t, bool, unsigned long long*, unsigned long long*);
 }  // namespace ddks_host

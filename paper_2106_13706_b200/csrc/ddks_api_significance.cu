@@ -37,7 +37,6 @@ ddks_status ddks_significance(ddks_ctx* ctx, const float* P, int64_t n_P, const 
     if ((s = stage_input(ctx, P, (size_t)n_P * d * 4, ctx->raw_a, st, &dP))) return s;
     if ((s = stage_input(ctx, Q, (size_t)n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
     if ((s = ensure(ctx, ctx->packed, (size_t)N * DP * 4))) return s;
-    if ((s = ensure(ctx, ctx->per_origin, (size_t)std::max<int64_t>(oe - ob, 1) * 8))) return s;
     const int64_t nm = n_Q + 1;  // M_T in 0..n_Q
     const int64_t n_max = std::max(n_P, n_Q);
     // log n! for n <= n_max, plus room for the Poisson mass beyond N (mean < N, ~14 sd above it is below e^-100)
@@ -57,13 +56,20 @@ ddks_status ddks_significance(ddks_ctx* ctx, const float* P, int64_t n_P, const 
     CU(cudaMemsetAsync(contrib, 0, (size_t)nm * 8, st));
     DevResult* dres = (DevResult*)ctx->res.p;
     DevResult* hres = (DevResult*)ctx->host_pinned;
-    *hres = DevResult{0ull, ~0ull, 0u, 0u};
+    *hres = DevResult{0ull, ~0ull, 0ull, 0u, 0u};
     CU(cudaMemcpyAsync(dres, hres, sizeof(DevResult), cudaMemcpyHostToDevice, st));
     float* packed = (float*)ctx->packed.p;
     if ((s = launch_pack(ctx, (const float*)dP, n_P, (const float*)dQ, n_Q, d, 1, packed, &dres->flag, st))) return s;
     uint64_t* per = nullptr;
-    if ((s = count_statistic(ctx, packed, d, n_P, n_Q, ob, oe, ctx->world, ctx->rank, dres, false, true, hist, st, &per))) return s;
+    if ((s = count_statistic(ctx, packed, d, n_P, n_Q, ob, oe, ctx->world, ctx->rank, dres, false, true, hist, st, &per,
+                             true)))
+        return s;
+    const bool use_key = argmax_key_fits(n_P, n_Q);
     if (ctx->comm) {
+        if (use_key) {  // (the k_argmax path all-reduced num inside count_statistic)
+            NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
+            NC(ncclAllReduce(&dres->key, &dres->key, 1, ncclUint64, ncclMax, ctx->comm, st));
+        }
         NC(ncclAllReduce(&dres->arg, &dres->arg, 1, ncclUint64, ncclMin, ctx->comm, st));
         NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
         NC(ncclAllReduce(hist, hist, (size_t)nm, ncclUint64, ncclSum, ctx->comm, st));
@@ -135,10 +141,11 @@ ddks_status ddks_significance(ddks_ctx* ctx, const float* P, int64_t n_P, const 
         CU(cudaMemcpyAsync(log_p_table, table, (size_t)nm * 8, cudaMemcpyDefault, st));
     }
     CU(cudaStreamSynchronize(st));
-    out->stat.num = hres->num;
+    const ddks_rank_record rec = decode_record(*hres, n_P, n_Q, use_key);
+    out->stat.num = rec.num;
     out->stat.den = (uint64_t)n_P * (uint64_t)n_Q;
     out->stat.D = (double)out->stat.num / (double)out->stat.den;
-    out->stat.argmax_origin = hres->arg == ~0ull ? -1 : (int64_t)hres->arg;
+    out->stat.argmax_origin = rec.argmax_origin;
     out->log_prod = log_prod;
     out->S = 0.0 - std::expm1(log_prod);  // (0.0 - x: no negative zero when log_prod == 0)
     out->cells = ((int64_t)1 << d) * N;
@@ -235,20 +242,24 @@ ddks_status ddks_significance_batch(ddks_ctx* ctx, const float* P, const float* 
             CU(cudaMemsetAsync(&dres->flag, 0, 4, st));
         }
     }
-    if (ctx->comm) {
-        if ((s = all_gather_items(ctx, nums, B, st))) return s;
-        if ((s = all_gather_items(ctx, (uint64_t*)parts, B, st))) return s;
-        NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
-    }
-    if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)B * 16))) return s;
+    // world > 1: one all-gather of the padded per-rank records (nums, log_prod bits, flags), unpadded on the host
+    const int64_t gstride = ctx->comm ? gather_stride(B, ctx->world, 2) : 0;
+    if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)B * 16 + (size_t)ctx->world * gstride * 8))) return s;
     DevResult* hres = (DevResult*)ctx->host_pinned;
     uint64_t* hnums = (uint64_t*)((char*)ctx->host_pinned + sizeof(DevResult));
     double* hparts = (double*)(hnums + B);
-    CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(hnums, nums, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(hparts, parts, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
+    uint64_t* hgath = hnums + 2 * B;
+    if (ctx->comm) {
+        uint64_t* arrs[2] = {nums, (uint64_t*)parts};
+        if ((s = gather_items(ctx, arrs, 2, B, &dres->flag, st, hgath))) return s;
+    } else {
+        CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(hnums, nums, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(hparts, parts, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
+    }
     CU(cudaStreamSynchronize(st));
     if ((s = collect_profile(ctx))) return s;
+    if (ctx->comm) ddks_unpad_items(hgath, B, ctx->world, 2, hnums, &hres->flag);  // nums then parts: contiguous
     if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
     const uint64_t den = (uint64_t)n_P * (uint64_t)n_Q;
     for (int64_t b = 0; b < B; ++b) {

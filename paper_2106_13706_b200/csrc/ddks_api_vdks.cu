@@ -45,7 +45,7 @@ ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     int64_t* S = (int64_t*)ctx->vox_S.p;
     DevResult* dres = (DevResult*)ctx->res.p;
     DevResult* hres = (DevResult*)ctx->host_pinned;
-    *hres = DevResult{0ull, ~0ull, 0u, 0u};
+    *hres = DevResult{0ull, ~0ull, 0ull, 0u, 0u};
     CU(cudaMemcpyAsync(dres, hres, sizeof(DevResult), cudaMemcpyHostToDevice, st));
     CU(cudaMemsetAsync(keys, 0xff, 8 * 4, st));
     CU(cudaMemsetAsync(keys + 8, 0, 8 * 4, st));

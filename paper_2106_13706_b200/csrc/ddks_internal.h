@@ -19,24 +19,29 @@ struct DevBuf {
     size_t bytes = 0;
 };
 
-struct DevResult {  // device-side result block (one D2H per call)
-    unsigned long long num;
-    unsigned long long arg;
-    uint32_t flag;
+// Device-side result block of one statistic on one rank (one D2H per call; with world > 1 it is also the 32-byte record
+// every rank contributes to the single all-gather of ddks_stat, combined on the host by ddks_combine_records).
+struct DevResult {
+    unsigned long long num;  // max num(o) over this rank's origins
+    unsigned long long arg;  // smallest pooled origin attaining it (~0: none / not computed; k_argmax path)
+    unsigned long long key;  // packed argmax (num / key_div) << 31 | (2^31 - 1 - origin) (0: none; fused path)
+    uint32_t flag;           // bit 0: non-finite input, bit 1: bad permutation row, bit 2: significance scratch
     uint32_t pad;
 };
+static_assert(sizeof(DevResult) == 32, "DevResult is the 32-byte all-gather record");
 
 struct ddks_ctx {
     int device = 0, world = 1, rank = 0;
     uint32_t flags = 0;
     ncclComm_t comm = nullptr;
-    DevBuf raw_a, raw_b, raw_perm, packed, packed2, pool_packed, per_origin, accum, item_num, bitmap, labels, res;
+    DevBuf raw_a, raw_b, raw_perm, packed, packed2, pool_packed, per_origin, accum, blk_done, item_num, bitmap, labels, res;
+    DevBuf gather;  // world > 1: all-gather send + receive buffers
     DevBuf sig_hist, sig_lf, sig_scratch, sig_table, sig_contrib, sig_part;  // ddks_significance workspace
     DevBuf vox_keys, vox_cnt, vox_S;                                           // ddks_vdks workspace
     DevBuf rd_keys, rd_xn, rd_k0, rd_k1, rd_hist, rd_tcnt, rd_cnum;              // ddks_rdks workspace
     DevBuf x0_keys0, x0_keys1, x0_hist, x0_pts, x0_perm, x0_pts2, x0_perm2, x0_boxes;  // kd-ordered count workspace
     DevBuf rdb_cnt, rdb_pst, rdb_coff, rdb_fill, rdb_clist, rdb_csum;            // rdKS bucket-pruned sweep
-    DevBuf prof_clk;  // [2] u64: SM cycles, globaltimer ns summed over count CTAs (DDKS_FLAG_PROFILE)
+    DevBuf prof_clk;  // [3] u64: SM cycles, globaltimer ns, executed compares summed over count CTAs (DDKS_FLAG_PROFILE)
     void* host_pinned = nullptr;  // DevResult + scratch
     size_t host_pinned_bytes = 0;
     int64_t launches = 0;
@@ -105,6 +110,10 @@ inline cudaError_t record_event(cudaEvent_t e, cudaStream_t st) {
 
 // grow-only device workspace; host (pinned) scratch
 ddks_status ensure(ddks_ctx* ctx, DevBuf& b, size_t bytes);
+// as ensure, and a (re)allocated buffer is zeroed on st (buffers whose users leave them zero: count partials)
+ddks_status ensure_zeroed(ddks_ctx* ctx, DevBuf& b, size_t bytes, cudaStream_t st);
+// the profiling counters (DDKS_FLAG_PROFILE): prof_clk allocated and zeroed once
+ddks_status ensure_prof(ddks_ctx* ctx);
 ddks_status ensure_host(ddks_ctx* ctx, size_t bytes);
 // device pointers are used in place, host pointers copied on st into buf
 ddks_status stage_input(ddks_ctx* ctx, const void* src, size_t bytes, DevBuf& buf, cudaStream_t st, const void** out);
@@ -119,24 +128,31 @@ ddks_status launch_pack(ddks_ctx* ctx, const float* P, int64_t n_P, const float*
 // batches: near-x_0-sorted pack of every label run when the items are small (*wx: the count may use k_count<WX>)
 ddks_status launch_pack_batch(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d,
                               int64_t B, float* dst, uint32_t* flag, cudaStream_t st, bool* wx);
-// one statistic over the origin shard [ob, oe): count, NCCL max of num, this rank's argmax candidate (see ddks_api.cu)
-// (kd order: the strided origin blocks of shard sr of sw instead of [ob, oe))
+// one statistic over the origin shard [ob, oe): count + this rank's argmax candidate, no collective unless
+// reduce_num_first (see ddks_api.cu); (kd order: the strided origin blocks of shard sr of sw instead of [ob, oe))
 ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n_P, int64_t n_Q, int64_t ob,
                             int64_t oe, int sw, int sr, DevResult* dres, bool export_per, bool split,
-                            unsigned long long* hist, cudaStream_t st, uint64_t** per_out);
+                            unsigned long long* hist, cudaStream_t st, uint64_t** per_out, bool reduce_num_first);
+// the fused packed-key argmax applies (n_P n_Q / gcd < 2^33)
+bool argmax_key_fits(int64_t n_P, int64_t n_Q);
+// a rank's device result -> host record (decodes the packed key when use_key)
+ddks_rank_record decode_record(const DevResult& r, int64_t n_P, int64_t n_Q, bool use_key);
 // B items of N packed points: classify + count (+ finalise); force_split + hist: SPLIT counters and per-item M_T
-// histograms hist[B][n_Q + 1] (significance)
+// histograms hist[B][n_Q + 1] (significance); best_key (B == 1): the fused packed argmax
 ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int64_t n_P, int64_t n_Q,
                       int64_t o_begin, int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st,
-                      bool force_split = false, unsigned long long* hist = nullptr, bool wx = false);
-// items sharded contiguously over ranks: all-gather every rank's slice of dev_nums[total] (8-byte elements)
-ddks_status all_gather_items(ddks_ctx* ctx, uint64_t* dev_nums, int64_t total, cudaStream_t st);
+                      bool force_split = false, unsigned long long* hist = nullptr, bool wx = false,
+                      unsigned long long* best_key = nullptr);
+// items sharded contiguously over ranks: one all-gather of padded records (n_arr arrays + flags) into host hbuf
+ddks_status gather_items(ddks_ctx* ctx, uint64_t* const* dev, int n_arr, int64_t total, const uint32_t* dflag,
+                         cudaStream_t st, uint64_t* hbuf);
+int64_t gather_stride(int64_t total, int world, int n_arr);
 // kd-ordered count of one statistic (B == 1, 2 <= D <= 8; ddks_kd.cuh, instantiated in ddks_api_kd_*.cu): the origin
 // blocks shard_rank, shard_rank + shard_world, ... of the kd order
 template <int D>
 ddks_status run_count_kd_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int64_t n_Q, int shard_world,
                            int shard_rank, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st, bool split,
-                           unsigned long long* hist);
+                           unsigned long long* hist, unsigned long long* best_key);
 ddks_status radix_sort_keys(ddks_ctx* ctx, uint64_t* src, uint64_t* dst, int64_t N, int nseg, int shift_begin,
                             uint32_t* hist, cudaStream_t st, uint64_t** sorted);
 

@@ -85,13 +85,13 @@ ddks_status launch_kd(ddks_ctx* ctx, const CountPlan& pl, const ddks::CountArgs&
 template <int D, bool SPLIT>
 ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int64_t n_Q, int shard_world,
                            int shard_rank, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st,
-                           unsigned long long* hist_out) {
+                           unsigned long long* hist_out, unsigned long long* best_key) {
     using G = ddks::Geo<D, SPLIT>;
     const int64_t N = n_P + n_Q;
     const int DP = pad_dim(D);
     const bool gt = (ctx->flags & DDKS_FLAG_TIES_GT) != 0;
     const int64_t A = lcm_i64(G::ORIGINS, G::TILE);
-    const int forced = (int)((ctx->flags >> DDKS_FLAG_KD_SHIFT) & 3u);
+    const int forced = (int)((ctx->flags >> DDKS_FLAG_KD_SHIFT) & 7u);
     // the tie-convention test variant (GT) is instantiated with one level only
     const KdChoice kc = kd_choose(D, std::min(n_P, n_Q), G::ORIGINS, 32 * G::R, G::TILE, A, gt ? 1 : forced,
                                   gt ? 1 : 5);
@@ -163,7 +163,6 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
         spts, DP, N, G::TILE, K, (float*)ctx->x0_boxes.p);
     CHECK_LAUNCH();
     ctx->launches++;
-    CU(cudaMemsetAsync(per_origin, 0, (size_t)N * 8, st));
     const uint64_t gg = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
     const uint32_t a_ = (uint32_t)((uint64_t)n_Q / gg), b_ = (uint32_t)((uint64_t)n_P / gg);
     // all N origins (positions of the kd order); shard r of W takes origin blocks r, r + W, r + 2W, ... so every
@@ -188,6 +187,8 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     a.boxes = (const float*)ctx->x0_boxes.p;
     a.hist = SPLIT ? hist_out : nullptr;
     a.hist_stride = n_Q + 1;
+    a.best_key = best_key;
+    a.key_div = gg;
     ctx->kd_levels = K;
     if (gt) return launch_kd<D, SPLIT, true, 1>(ctx, pl, a, st);
     if (K == 1) return launch_kd<D, SPLIT, false, 1>(ctx, pl, a, st);
@@ -209,9 +210,11 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
 template <int D>
 ddks_status run_count_kd_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int64_t n_Q, int shard_world,
                            int shard_rank, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st, bool split,
-                           unsigned long long* hist) {
-    return split ? run_count_kd_t<D, true>(ctx, packed, n_P, n_Q, shard_world, shard_rank, item_num, per_origin, st, hist)
-                 : run_count_kd_t<D, false>(ctx, packed, n_P, n_Q, shard_world, shard_rank, item_num, per_origin, st, hist);
+                           unsigned long long* hist, unsigned long long* best_key) {
+    return split ? run_count_kd_t<D, true>(ctx, packed, n_P, n_Q, shard_world, shard_rank, item_num, per_origin, st, hist,
+                                           best_key)
+                 : run_count_kd_t<D, false>(ctx, packed, n_P, n_Q, shard_world, shard_rank, item_num, per_origin, st, hist,
+                                            best_key);
 }
 
 }  // namespace ddks_host

@@ -276,16 +276,27 @@ struct CountArgs {
     uint32_t incP, incQ;     // DIFF: +a and -b (two's complement); SPLIT: 1 and 1
     uint64_t g;              // DIFF: gcd(n_P, n_Q) multiplier
     int64_t nP, nQ;          // SPLIT finalisation
-    uint64_t* item_num;      // [B] atomicMax target (direct mode)
-    uint64_t* per_origin;    // [o_end - o_begin] or nullptr (direct mode, B == 1)
-    int32_t* accum;          // accumulate mode: [B][NB][acc_stride] int32 counters, else nullptr (direct mode)
+    uint64_t* item_num;      // [B] atomicMax target
+    uint64_t* per_origin;    // [o_end - o_begin] or nullptr (B == 1)
+    int32_t* accum;          // accumulate mode: [B][NB][acc_stride] int32 counters (zero on entry, left zero on exit),
+                             // else nullptr (direct mode: the whole point set is one segment)
+    uint32_t* blk_done;      // accumulate mode: [B][n_blk] arrival counters (zero on entry, left zero on exit)
+    int32_t n_blk = 0;       // origin blocks of this launch (all grid.y chunks)
+    int32_t blk_base = 0;    // this launch's first origin block (grid.y is chunked at 65535)
+    // packed argmax (B == 1, or nullptr): atomicMax of (num(o) / key_div) << 31 | (2^31 - 1 - pooled index) over the
+    // origins, i.e. the max num and, among origins attaining it, the smallest pooled index (R7); the host
+    // uses it only when n_P n_Q / gcd < 2^33, so the key fits 64 bits
+    unsigned long long* best_key;
+    uint64_t key_div;
     const float* boxes;      // kd-ordered mode: [n_tiles][KX][2] min / max of dims < KX per TILE rows, else nullptr
     const int32_t* perm;     // kd-ordered mode: perm[j] = pooled index of sorted origin j; per_origin is then a
                              // full [N] array in pooled order (else nullptr: per_origin indexed o - o_begin)
     unsigned long long* hist;  // SPLIT only, or nullptr: hist[item * hist_stride + c_Q] += 1 for every (origin,
                                // orthant) cell (the M_T histogram of the analytic significance, ddks_significance.cuh)
     int64_t hist_stride;       // n_Q + 1 (one histogram per batch item)
-    unsigned long long* clk = nullptr;  // profiling: += SM cycles and globaltimer ns of every CTA's count loop
+    // profiling (or nullptr): [0] += SM cycles and [1] += globaltimer ns of every CTA's count loop, [2] += FP32
+    // compares executed (every lane of every warp, decided kd / WX bits excluded: the work the ALU pipe really did)
+    unsigned long long* clk = nullptr;
 };
 
 // decode the two signed 16-bit halves of a counter word (value = lo + 65536 * hi, both in int16 range)
@@ -492,8 +503,9 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
     const int t = threadIdx.x;
     const int64_t item = blockIdx.z;
     const float* pts = a.pts + item * a.item_stride;
-    const int32_t blk_o0 = a.o_begin + ((int32_t)blockIdx.y * a.blk_stride + a.blk_off) * G::ORIGINS;
-    const int32_t li0 = (int32_t)blockIdx.y * G::ORIGINS;  // this CTA's first accumulator slot
+    const int32_t by = a.blk_base + (int32_t)blockIdx.y;  // origin block of this launch
+    const int32_t blk_o0 = a.o_begin + (by * a.blk_stride + a.blk_off) * G::ORIGINS;
+    const int32_t li0 = by * G::ORIGINS;  // this CTA's first accumulator slot
     const int32_t seg0 = (int32_t)blockIdx.x * a.seg_points;
     const int32_t seg1 = min(a.N, seg0 + a.seg_points);
     const int n_tiles = (seg1 - seg0 + TILE - 1) / TILE;
@@ -594,6 +606,7 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
     // in-kernel clock probe (one lane per CTA, profiling only): the SM clock this launch actually ran at
     unsigned long long clk0 = 0, ns0 = 0;
     if (a.clk && t == 0) clk0 = clock64(), ns0 = globaltimer_ns();
+    unsigned long long exec_cmp = 0;  // profiling: compares this warp executed / (32 R)
 
     for (int it = 0; it < n_tiles; ++it) {
         const int s = it % S;
@@ -669,10 +682,12 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
                     float wb[NBASE];
 #pragma unroll
                     for (int b = 0; b < NBASE; ++b) wb[b] = bb[b] + wadd;
+                    if (a.clk) exec_cmp += (unsigned long long)((D - 1 + wm) * (se - sb));
                     count_points_um<D, GT, R, RP, NBASE, WPB, DP, 1>(wm, tile, sb, se, o, wb, ubase, il, ih,
                                                                     G::HIST_WORDS * 4u);
                 }
             } else {
+                if (a.clk) exec_cmp += (unsigned long long)((D - KX + __popc(um)) * (hi - lo));
                 count_points_um<D, GT, R, RP, NBASE, WPB, DP, KX>(um, tile, lo, hi, o, bb, ubase, il, ih,
                                                                  G::HIST_WORDS * 4u);
             }
@@ -708,13 +723,29 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
         }
     }
     __syncthreads();  // all red.shared retired before reading the counters
-    if (a.clk && t == 0) {
-        atomicAdd(&a.clk[0], (unsigned long long)(clock64() - clk0));
-        atomicAdd(&a.clk[1], globaltimer_ns() - ns0);
+    if (a.clk) {
+        if (t == 0) {
+            atomicAdd(&a.clk[0], (unsigned long long)(clock64() - clk0));
+            atomicAdd(&a.clk[1], globaltimer_ns() - ns0);
+        }
+        if (lane == 0) atomicAdd(&a.clk[2], exec_cmp * (unsigned long long)(32 * R));
     }
 
+    // per-origin epilogue shared by both modes: num(o) -> per-origin export, the CTA max, the packed argmax key
+    uint64_t best = 0;
+    unsigned long long bkey = 0;
+    auto take = [&](int32_t oi, uint64_t m) {
+        const int32_t pooled = a.perm ? a.perm[oi] : oi;
+        if (a.per_origin) a.per_origin[a.perm ? pooled : oi - a.o_begin] = m;
+        best = m > best ? m : best;
+        if (a.best_key) {
+            const unsigned long long k = ((unsigned long long)(m / a.key_div) << 31) | (unsigned long long)(0x7fffffff - pooled);
+            bkey = k > bkey ? k : bkey;
+        }
+    };
+
     if (a.accum != nullptr) {
-        // flush: exact int32 partial counters -> global (red.global.add), finalised by k_finalize
+        // flush: exact int32 partial counters -> global (red.global.add)
         int32_t* acc = a.accum + item * (int64_t)G::NB * a.acc_stride;
 #pragma unroll 1
         for (int r = 0; r < R; ++r) {
@@ -731,25 +762,84 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
                 if (v) atomicAdd(&acc[(int64_t)q * a.acc_stride + (li0 + r * T + t)], v);
             }
         }
-        return;
-    }
-    uint64_t best = 0;
+        // the last CTA of this origin block (over the point segments, grid.x) finalises the block from the int32
+        // partials and leaves the partials and its arrival counter zeroed for the next launch: no memset and no
+        // separate finaliser launch (threadfence-reduction pattern)
+        __shared__ uint32_t s_last;
+        __threadfence();
+        __syncthreads();
+        if (t == 0) {
+            uint32_t* cnt = a.blk_done + item * (int64_t)a.n_blk + by;
+            DDKS_ASSERT(by < a.n_blk);
+            s_last = atomicAdd(cnt, 1u) == gridDim.x - 1 ? 1u : 0u;
+            if (s_last) *cnt = 0u;
+        }
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+        // SPLIT + significance histogram: the dead counter region becomes a CTA-private histogram of the small M_T
+        // values (a CTA's cells all belong to one item), flushed once; larger values go to global memory directly
+        constexpr int HSZ = G::HIST_WORDS < 2048 ? G::HIST_WORDS : 2048;
+        uint32_t* shh = hist;
+        if (SPLIT && a.hist) {
+            for (int i = t; i < HSZ; i += T) shh[i] = 0u;
+            __syncthreads();
+        }
 #pragma unroll 1
-    for (int r = 0; r < R; ++r) {
-        const int32_t oi = origin_of(r);
-        if (oi >= a.o_end) continue;
-        const uint64_t m = origin_num<D, SPLIT>(hist, r, t, a, item);
-        if (a.per_origin) a.per_origin[a.perm ? a.perm[oi] : oi - a.o_begin] = m;
-        best = m > best ? m : best;
+        for (int r = 0; r < R; ++r) {
+            const int32_t oi = origin_of(r);
+            if (oi >= a.o_end) continue;
+            int32_t* p = acc + (li0 + r * T + t);
+            uint64_t m = 0;
+            if constexpr (!SPLIT) {
+                uint32_t mm = 0;
+                for (int q = 0; q < G::NQ; ++q) {
+                    const int32_t v = __ldcg(p + (int64_t)q * a.acc_stride);
+                    __stcg(p + (int64_t)q * a.acc_stride, 0);
+                    const uint32_t av = (uint32_t)(v < 0 ? -v : v);
+                    mm = av > mm ? av : mm;
+                }
+                m = (uint64_t)mm * a.g;
+            } else {
+                for (int q = 0; q < G::NQ; ++q) {
+                    const int64_t cP = __ldcg(p + (int64_t)q * a.acc_stride);
+                    const int64_t cQ = __ldcg(p + (int64_t)(G::NQ + q) * a.acc_stride);
+                    __stcg(p + (int64_t)q * a.acc_stride, 0);
+                    __stcg(p + (int64_t)(G::NQ + q) * a.acc_stride, 0);
+                    if (a.hist) {
+                        if (cQ < HSZ) atomicAdd(&shh[cQ], 1u);
+                        else atomicAdd(&a.hist[item * a.hist_stride + cQ], 1ull);
+                    }
+                    const int64_t df = cP * a.nQ - cQ * a.nP;
+                    const uint64_t av = (uint64_t)(df < 0 ? -df : df);
+                    m = av > m ? av : m;
+                }
+            }
+            take(oi, m);
+        }
+        if (SPLIT && a.hist) {
+            __syncthreads();
+            for (int i = t; i < HSZ; i += T)
+                if (shh[i]) atomicAdd(&a.hist[item * a.hist_stride + i], (unsigned long long)shh[i]);
+        }
+    } else {
+#pragma unroll 1
+        for (int r = 0; r < R; ++r) {
+            const int32_t oi = origin_of(r);
+            if (oi >= a.o_end) continue;
+            take(oi, origin_num<D, SPLIT>(hist, r, t, a, item));
+        }
     }
     best = warp_max_u64(best);
-    __shared__ uint64_t wmax[32];
-    if ((t & 31) == 0) wmax[t >> 5] = best;
+    bkey = warp_max_u64(bkey);
+    __shared__ uint64_t wmax[32], wkey[32];
+    if ((t & 31) == 0) wmax[t >> 5] = best, wkey[t >> 5] = bkey;
     __syncthreads();
     if (t == 0) {
-        uint64_t m = 0;
-        for (int w = 0; w < T / 32; ++w) m = wmax[w] > m ? wmax[w] : m;
+        uint64_t m = 0, k = 0;
+        for (int w = 0; w < T / 32; ++w) m = wmax[w] > m ? wmax[w] : m, k = wkey[w] > k ? wkey[w] : k;
         atomicMax(reinterpret_cast<unsigned long long*>(&a.item_num[item]), (unsigned long long)m);
+        if (a.best_key) atomicMax(a.best_key, (unsigned long long)k);
     }
 }
 
@@ -878,84 +968,6 @@ __global__ void k_tile_boxes(const float* __restrict__ pts, int DP, int64_t N, i
     }
 }
 
-// SPLIT with a.hist (significance): M_T values below HS are histogrammed in a block-private SMEM histogram first and
-// flushed once per block; larger values (rare) go straight to global memory.
-constexpr int HS = 2048;
-
-template <int D, bool SPLIT>
-__global__ void k_finalize(const CountArgs a, int64_t B) {
-    constexpr int NQ = 1 << D;
-    constexpr int NB = Geo<D, SPLIT>::NB;
-    const int32_t n_orig = a.o_end - a.o_begin;
-    __shared__ uint32_t sh_hist[SPLIT ? HS : 1];
-    const bool priv = SPLIT && a.hist && B == 1;  // a block-private histogram only when every cell is one item's
-    if constexpr (SPLIT) {
-        if (priv) {
-            for (int i = threadIdx.x; i < HS; i += blockDim.x) sh_hist[i] = 0u;
-            __syncthreads();
-        }
-    }
-    constexpr int ORIG = Geo<D, SPLIT>::ORIGINS;
-    const int64_t ns = a.acc_stride;  // accumulator slots per item
-    const int64_t total = B * ns;
-    uint64_t best = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t item = i / ns, li = i - item * ns;
-        // slot li -> origin offset oi in [0, n_orig) (block li / ORIG of this launch is block
-        // (li / ORIG) * blk_stride + blk_off of the range); slots past the range hold no origin
-        const int64_t sl = li % ORIG;  // slot r*T + t inside the block
-        int64_t off = sl;
-        if (a.warp_major) {
-            constexpr int TT = Geo<D, SPLIT>::T, RR = Geo<D, SPLIT>::R;
-            const int64_t r = sl / TT, tt = sl % TT;
-            off = (tt >> 5) * (32 * RR) + r * 32 + (tt & 31);
-        }
-        const int64_t oi = ((li / ORIG) * a.blk_stride + a.blk_off) * ORIG + off;
-        if (oi >= n_orig) continue;
-        const int32_t* acc = a.accum + item * (int64_t)NB * ns + li;
-        uint64_t m = 0;
-        if constexpr (!SPLIT) {
-            uint32_t mm = 0;
-            for (int q = 0; q < NQ; ++q) {
-                const int32_t v = (int32_t)acc[(int64_t)q * ns];
-                const uint32_t av = (uint32_t)(v < 0 ? -v : v);
-                mm = av > mm ? av : mm;
-            }
-            m = (uint64_t)mm * a.g;
-        } else {
-            for (int q = 0; q < NQ; ++q) {
-                const int64_t cP = (int64_t)acc[(int64_t)q * ns];
-                const int64_t cQ = (int64_t)acc[(int64_t)(NQ + q) * ns];
-                if (a.hist) {
-                    if (priv && cQ < HS) atomicAdd(&sh_hist[cQ], 1u);
-                    else hist_add_aggregated(a.hist, item * a.hist_stride + cQ);
-                }
-                const int64_t df = cP * a.nQ - cQ * a.nP;
-                const uint64_t av = (uint64_t)(df < 0 ? -df : df);
-                m = av > m ? av : m;
-            }
-        }
-        if (a.per_origin && B == 1) a.per_origin[a.perm ? a.perm[a.o_begin + oi] : oi] = m;
-        if (B == 1) {
-            best = m > best ? m : best;
-        } else {
-            atomicMax(reinterpret_cast<unsigned long long*>(&a.item_num[item]), (unsigned long long)m);
-        }
-    }
-    if (B == 1) {
-        best = warp_max_u64(best);
-        if ((threadIdx.x & 31) == 0)
-            atomicMax(reinterpret_cast<unsigned long long*>(&a.item_num[0]), (unsigned long long)best);
-    }
-    if constexpr (SPLIT) {
-        if (priv) {
-            __syncthreads();
-            for (int i = threadIdx.x; i < HS; i += blockDim.x)
-                if (sh_hist[i]) atomicAdd(&a.hist[i], (unsigned long long)sh_hist[i]);
-        }
-    }
-}
-
 // ----------------------------------------------------------------------------------------------- a9: label-invariant permutation null
 // SURVEY.md §8f NEXT-2. code(o, x) does not depend on the labels, so one classification of a pair serves J
 // permutations at once: for permutation j only the P'-count is needed, because with T[q] = all points in orthant q,
@@ -991,6 +1003,7 @@ struct PermArgs {
     uint32_t a, b;            // DIFF weights
     uint64_t g;
     uint64_t* num;            // [n_perm] atomicMax targets
+    unsigned long long* clk;  // profiling (or nullptr): [2] += FP32 compares executed (as CountArgs::clk)
 };
 
 // labels + validation: for row j of perms, check it is a permutation of 0..N-1 (range + no duplicate via bitmap,
@@ -1099,6 +1112,7 @@ __global__ void __launch_bounds__(PermGeo<D>::T, 1) k_perm_count(const PermArgs 
         }
     }
     __syncthreads();
+    if (a.clk && t == 0) atomicAdd(&a.clk[2], (unsigned long long)D * (unsigned long long)a.N * (unsigned long long)T);
 
     // finalise: num_j(o) = g * max_q |(a+b) c_P'[q] - b T[q]|, then max over this warp's origins per permutation
     __shared__ uint64_t wmax[T / 32][J];

@@ -82,18 +82,22 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
     const int tiles_per_seg = (n_tiles + segs - 1) / segs;
     segs = (n_tiles + tiles_per_seg - 1) / tiles_per_seg;
     a.seg_points = tiles_per_seg * G::TILE;
-    if (segs > 65535) return fail(ctx, DDKS_ERR_TOO_LARGE, "too many point segments");
+    if (segs > 0x7fffffff / 2) return fail(ctx, DDKS_ERR_TOO_LARGE, "too many point segments");
+    a.n_blk = blocks_o;
     if (segs > 1) {
+        // int32 partials and per-block arrival counters: zeroed when (re)allocated, and every launch leaves them zero
+        // (the last CTA of each origin block finalises and clears its slots), so no memset per call
         const size_t acc_bytes = (size_t)pl.B * G::NB * (size_t)a.acc_stride * 4;
-        ddks_status s = ensure(ctx, ctx->accum, acc_bytes);
+        ddks_status s = ensure_zeroed(ctx, ctx->accum, acc_bytes, st);
         if (s) return s;
-        CU(cudaMemsetAsync(ctx->accum.p, 0, acc_bytes, st));
+        if ((s = ensure_zeroed(ctx, ctx->blk_done, (size_t)pl.B * blocks_o * 4, st))) return s;
         a.accum = (int32_t*)ctx->accum.p;
+        a.blk_done = (uint32_t*)ctx->blk_done.p;
     } else {
         a.accum = nullptr;
+        a.blk_done = nullptr;
     }
-    if (pl.B > 65535 || blocks_o > 65535) return fail(ctx, DDKS_ERR_TOO_LARGE, "grid too large");
-    dim3 grid((unsigned)segs, (unsigned)blocks_o, (unsigned)pl.B);
+    if (pl.B > 65535) return fail(ctx, DDKS_ERR_TOO_LARGE, "grid too large");
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
     if (ctx->flags & DDKS_FLAG_PROFILE) {
         if (!ctx->ev_free.empty()) {
@@ -104,16 +108,20 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
             CU(cudaEventCreate(&ev.second));
         }
         CU(record_event(ev.first, st));
-        if (!ctx->prof_clk.p) {
-            ddks_status s = ensure(ctx, ctx->prof_clk, 16);
-            if (s) return s;
-            CU(cudaMemset(ctx->prof_clk.p, 0, 16));
-        }
+        ddks_status s = ensure_prof(ctx);
+        if (s) return s;
         a.clk = (unsigned long long*)ctx->prof_clk.p;
     }
-    kern<<<grid, G::T, G::SMEM_BYTES, st>>>(a);
-    CHECK_LAUNCH();
-    ctx->launches++;
+    // grid: x = point segment, y = origin block (chunks of 65535; DDKS_GRIDY, TEST ONLY, lowers the chunk), z = item
+    int ych = 65535;
+    if (const char* e = getenv("DDKS_GRIDY")) ych = std::max(1, std::min(65535, atoi(e)));
+    for (int y0 = 0; y0 < blocks_o; y0 += ych) {
+        a.blk_base = y0;
+        dim3 grid((unsigned)segs, (unsigned)std::min(ych, blocks_o - y0), (unsigned)pl.B);
+        kern<<<grid, G::T, G::SMEM_BYTES, st>>>(a);
+        CHECK_LAUNCH();
+        ctx->launches++;
+    }
     if (ev.first) {
         CU(record_event(ev.second, st));
         ctx->ev_pending.push_back(ev);
@@ -122,14 +130,6 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
         const bool last_own = (blocks_all - 1 - pl.blk_off) % pl.blk_stride == 0;
         const uint64_t own = (uint64_t)blocks_o * G::ORIGINS - (last_own ? (uint64_t)blocks_all * G::ORIGINS - n_orig : 0);
         ctx->ev_pairs.push_back((uint64_t)pl.B * own * (uint64_t)pl.N);
-    }
-    if (segs > 1) {
-        const int64_t total = pl.B * a.acc_stride;
-        const int threads = 256;
-        const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 16);
-        ddks::k_finalize<D, SPLIT><<<blocks, threads, 0, st>>>(a, pl.B);
-        CHECK_LAUNCH();
-        ctx->launches++;
     }
     return DDKS_OK;
 }

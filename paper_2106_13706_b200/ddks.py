@@ -28,14 +28,14 @@ DDKS_FLAG_PERM_GATHER = 16
 DDKS_FLAG_NO_X0 = 32
 DDKS_FLAG_FORCE_X0 = 64
 DDKS_FLAG_RDKS_FULL_SORT = 128
-DDKS_FLAG_KD_SHIFT = 9
+DDKS_FLAG_KD_SHIFT = 16
 DDKS_FLAG_NCCL_SELF = 2048
 DDKS_FLAG_NO_GRAPH = 4096
 
 
 def DDKS_FLAG_KD_LEVELS(k: int) -> int:
-    """TEST ONLY: force k (1..3) levels of kd ordering (include/ddks.h)."""
-    return (k & 3) << DDKS_FLAG_KD_SHIFT
+    """TEST ONLY: force k (1..4) levels of kd ordering (include/ddks.h)."""
+    return (k & 7) << DDKS_FLAG_KD_SHIFT
 DDKS_SIG_POISSON = 1
 
 
@@ -48,6 +48,11 @@ class DDKSError(RuntimeError):
 class ddks_result(ctypes.Structure):
     _fields_ = [("num", ctypes.c_uint64), ("den", ctypes.c_uint64), ("D", ctypes.c_double),
                 ("argmax_origin", ctypes.c_int64)]
+
+
+class ddks_rank_record(ctypes.Structure):
+    _fields_ = [("num", ctypes.c_uint64), ("argmax_origin", ctypes.c_int64), ("flags", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32)]
 
 
 class ddks_significance_result(ctypes.Structure):
@@ -92,6 +97,10 @@ def _load() -> ctypes.CDLL:
         "ddks_vdks": ([vp, vp, i64, vp, i64, i32, i64, vp, ctypes.POINTER(ddks_result)], ctypes.c_int),
         "ddks_rdks": ([vp, vp, i64, vp, i64, i32, vp, ctypes.POINTER(ddks_result)], ctypes.c_int),
         "ddks_shard_range": ([i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)], ctypes.c_int),
+        "ddks_combine_records": ([ctypes.POINTER(ddks_rank_record), ctypes.c_int, ctypes.POINTER(ddks_rank_record)],
+                                 ctypes.c_int),
+        "ddks_unpad_items": ([vp, i64, ctypes.c_int, ctypes.c_int, vp, ctypes.POINTER(u32)], ctypes.c_int),
+        "ddks_profile_work": ([vp, ctypes.POINTER(ctypes.c_uint64)], ctypes.c_int),
         "ddks_launch_count": ([vp], i64),
         "ddks_kd_levels": ([vp], i32),
         "ddks_profile_clock": ([vp, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
@@ -110,7 +119,8 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 EXPORTED = ("ddks_get_nccl_id", "ddks_create", "ddks_stat", "ddks_stat_batch", "ddks_permutation_null",
-            "ddks_stat_per_origin", "ddks_stat_shard", "ddks_significance", "ddks_significance_batch", "ddks_vdks", "ddks_rdks", "ddks_shard_range", "ddks_launch_count", "ddks_kd_levels", "ddks_profile_clock", "ddks_profile_read", "ddks_destroy",
+            "ddks_stat_per_origin", "ddks_stat_shard", "ddks_significance", "ddks_significance_batch", "ddks_vdks", "ddks_rdks", "ddks_shard_range", "ddks_combine_records", "ddks_unpad_items", "ddks_launch_count",
+            "ddks_kd_levels", "ddks_profile_clock", "ddks_profile_read", "ddks_profile_work", "ddks_destroy",
             "ddks_last_error", "ddks_version")
 
 
@@ -119,17 +129,41 @@ def _check(st: int, ctx=None):
         raise DDKSError(st, (LIB.ddks_last_error(ctx) or b"").decode())
 
 
-class _Arg:
-    """Holds a pointer to a float32/int32 C-contiguous buffer (torch tensor or NumPy array) alive for a call."""
+def _torch_stream(stream):
+    """The torch stream a call's conversions must run on: the caller's `stream` (a torch.cuda.Stream or a raw
+    cudaStream_t handle), else torch's current stream."""
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream()
+    if isinstance(stream, torch.cuda.Stream):
+        return stream
+    return torch.cuda.ExternalStream(int(stream))
 
-    def __init__(self, x, dtype):
+
+class _Arg:
+    """Holds a pointer to a float32/int32 C-contiguous buffer (torch tensor or NumPy array) alive for a call.
+    A CUDA tensor of another dtype or layout is converted ON THE CALL'S STREAM (the library reads it there), and a
+    float64 input is cast to float32 with a warning: the library's coordinates are float32 (BASELINE.json configs), and
+    the cast can merge distinct values into ties, which can change D relative to the float64 definition."""
+
+    def __init__(self, x, dtype, stream=None):
+        import warnings
         self.keep = None
         try:
             import torch
             if isinstance(x, torch.Tensor):
                 tdt = torch.float32 if dtype == np.float32 else torch.int32
+                if x.dtype == torch.float64 and tdt == torch.float32:
+                    warnings.warn("float64 input cast to float32 (ddks computes on float32 coordinates)", stacklevel=3)
                 if x.dtype != tdt or not x.is_contiguous():
-                    x = x.to(tdt).contiguous()
+                    if x.is_cuda:
+                        st = _torch_stream(stream)
+                        st.wait_stream(torch.cuda.current_stream(x.device))  # x is ready on the current stream
+                        with torch.cuda.stream(st):
+                            x = x.to(tdt).contiguous()
+                        x.record_stream(st)
+                    else:
+                        x = x.to(tdt).contiguous()
                 self.keep = x
                 self.ptr = x.data_ptr()
                 self.shape = tuple(x.shape)
@@ -137,15 +171,38 @@ class _Arg:
                 return
         except ImportError:
             pass
-        a = np.ascontiguousarray(np.asarray(x, dtype=dtype))
+        a = np.asarray(x)
+        if a.dtype == np.float64 and dtype == np.float32:
+            warnings.warn("float64 input cast to float32 (ddks computes on float32 coordinates)", stacklevel=3)
+        a = np.ascontiguousarray(a, dtype=dtype)
         self.keep = a
         self.ptr = a.ctypes.data
         self.shape = a.shape
         self.is_cuda = False
 
 
+def _pair(P, Q, stream):
+    p, q = _Arg(P, np.float32, stream), _Arg(Q, np.float32, stream)
+    if len(p.shape) != 2 or len(q.shape) != 2 or p.shape[1] != q.shape[1]:
+        raise ValueError(f"P {p.shape} and Q {q.shape} must be [n, d] with the same d")
+    return p, q
+
+
+def _batch(P, Q, stream):
+    p, q = _Arg(P, np.float32, stream), _Arg(Q, np.float32, stream)
+    if len(p.shape) != 3 or len(q.shape) != 3 or p.shape[0] != q.shape[0] or p.shape[2] != q.shape[2]:
+        raise ValueError(f"P {p.shape} and Q {q.shape} must be [B, n, d] with the same B and d")
+    return p, q
+
+
 def _stream(stream):
     if stream is not None:
+        try:
+            import torch
+            if isinstance(stream, torch.cuda.Stream):
+                return ctypes.c_void_p(stream.cuda_stream)
+        except ImportError:
+            pass
         return ctypes.c_void_p(int(stream))
     try:
         import torch
@@ -187,9 +244,7 @@ def ddks_destroy(ctx) -> None:
 
 
 def ddks_stat(ctx, P, Q, stream=None) -> Result:
-    p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
-    if len(p.shape) != 2 or len(q.shape) != 2 or p.shape[1] != q.shape[1]:
-        raise ValueError(f"P {p.shape} and Q {q.shape} must be [n, d] with the same d")
+    p, q = _pair(P, Q, stream)
     r = ddks_result()
     _check(LIB.ddks_stat(ctx, p.ptr, p.shape[0], q.ptr, q.shape[0], p.shape[1], _stream(stream), ctypes.byref(r)), ctx)
     return Result(r.num, r.den, r.D, r.argmax_origin)
@@ -221,9 +276,7 @@ class BatchResult:
 
 
 def ddks_stat_batch(ctx, P, Q, stream=None) -> BatchResult:
-    p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
-    if len(p.shape) != 3 or len(q.shape) != 3 or p.shape[0] != q.shape[0] or p.shape[2] != q.shape[2]:
-        raise ValueError(f"P {p.shape} and Q {q.shape} must be [B, n, d] with the same B and d")
+    p, q = _batch(P, Q, stream)
     B = p.shape[0]
     arr = np.zeros(B, dtype=_RESULT_DTYPE)
     assert _RESULT_DTYPE.itemsize == ctypes.sizeof(ddks_result)
@@ -234,8 +287,10 @@ def ddks_stat_batch(ctx, P, Q, stream=None) -> BatchResult:
 
 def ddks_permutation_null(ctx, pooled, n_P: int, perms, stream=None):
     """-> (null_num: np.uint64 [n_perm], observed: Result, p_value: float)."""
-    a = _Arg(pooled, np.float32)
-    pr = _Arg(perms, np.int32)
+    a = _Arg(pooled, np.float32, stream)
+    pr = _Arg(perms, np.int32, stream)
+    if len(a.shape) != 2:
+        raise ValueError(f"pooled {a.shape} must be [n_P + n_Q, d]")
     N, d = a.shape
     n_perm = pr.shape[0] if len(pr.shape) == 2 else 0
     if n_perm and pr.shape[1] != N:
@@ -250,7 +305,7 @@ def ddks_permutation_null(ctx, pooled, n_P: int, perms, stream=None):
 
 def ddks_stat_shard(ctx, P, Q, world: int, rank: int, stream=None) -> Result:
     """ddks_stat restricted to the origin shard rank `rank` of `world` would own (no collective)."""
-    p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
+    p, q = _pair(P, Q, stream)
     r = ddks_result()
     _check(LIB.ddks_stat_shard(ctx, p.ptr, p.shape[0], q.ptr, q.shape[0], p.shape[1], world, rank, _stream(stream),
                                ctypes.byref(r)), ctx)
@@ -258,7 +313,7 @@ def ddks_stat_shard(ctx, P, Q, world: int, rank: int, stream=None) -> Result:
 
 
 def ddks_stat_per_origin(ctx, P, Q, o_begin: int, o_end: int, stream=None) -> np.ndarray:
-    p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
+    p, q = _pair(P, Q, stream)
     out = np.zeros(max(o_end - o_begin, 0), dtype=np.uint64)
     _check(LIB.ddks_stat_per_origin(ctx, p.ptr, p.shape[0], q.ptr, q.shape[0], p.shape[1], o_begin, o_end,
                                     out.ctypes.data if out.size else ctypes.c_void_p(8), _stream(stream)), ctx)
@@ -267,9 +322,7 @@ def ddks_stat_per_origin(ctx, P, Q, o_begin: int, o_end: int, stream=None) -> np
 
 def ddks_significance(ctx, P, Q, poisson: bool = False, detail: bool = False, stream=None) -> Significance:
     """Analytic significance (§3). detail=True also returns mt_hist [n_Q+1] and log_p_table [n_Q+1]."""
-    p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
-    if len(p.shape) != 2 or len(q.shape) != 2 or p.shape[1] != q.shape[1]:
-        raise ValueError(f"P {p.shape} and Q {q.shape} must be [n, d] with the same d")
+    p, q = _pair(P, Q, stream)
     r = ddks_significance_result()
     hist = np.zeros(q.shape[0] + 1, dtype=np.uint64) if detail else None
     table = np.zeros(q.shape[0] + 1, dtype=np.float64) if detail else None
@@ -282,9 +335,7 @@ def ddks_significance(ctx, P, Q, poisson: bool = False, detail: bool = False, st
 
 def ddks_significance_batch(ctx, P, Q, poisson: bool = False, stream=None) -> list[Significance]:
     """B independent pairs P [B, n_P, d], Q [B, n_Q, d] -> one Significance per pair (no histogram/table)."""
-    p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
-    if len(p.shape) != 3 or len(q.shape) != 3 or p.shape[0] != q.shape[0] or p.shape[2] != q.shape[2]:
-        raise ValueError(f"P {p.shape} and Q {q.shape} must be [B, n, d] with the same B and d")
+    p, q = _batch(P, Q, stream)
     B = p.shape[0]
     out = (ddks_significance_result * B)()
     _check(LIB.ddks_significance_batch(ctx, p.ptr, q.ptr, B, p.shape[1], q.shape[1], p.shape[2],
@@ -295,9 +346,7 @@ def ddks_significance_batch(ctx, P, Q, poisson: bool = False, stream=None) -> li
 
 def ddks_vdks(ctx, P, Q, k: int, stream=None) -> Result:
     """vdKS (Alg. 1) with k voxels per dimension."""
-    p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
-    if len(p.shape) != 2 or len(q.shape) != 2 or p.shape[1] != q.shape[1]:
-        raise ValueError(f"P {p.shape} and Q {q.shape} must be [n, d] with the same d")
+    p, q = _pair(P, Q, stream)
     r = ddks_result()
     _check(LIB.ddks_vdks(ctx, p.ptr, p.shape[0], q.ptr, q.shape[0], p.shape[1], k, _stream(stream), ctypes.byref(r)),
            ctx)
@@ -306,12 +355,40 @@ def ddks_vdks(ctx, P, Q, k: int, stream=None) -> Result:
 
 def ddks_rdks(ctx, P, Q, stream=None) -> Result:
     """rdKS (Alg. 2); argmax_origin is the first corner attaining num (0 = origin, m + 1 = e_m)."""
-    p, q = _Arg(P, np.float32), _Arg(Q, np.float32)
-    if len(p.shape) != 2 or len(q.shape) != 2 or p.shape[1] != q.shape[1]:
-        raise ValueError(f"P {p.shape} and Q {q.shape} must be [n, d] with the same d")
+    p, q = _pair(P, Q, stream)
     r = ddks_result()
     _check(LIB.ddks_rdks(ctx, p.ptr, p.shape[0], q.ptr, q.shape[0], p.shape[1], _stream(stream), ctypes.byref(r)), ctx)
     return Result(r.num, r.den, r.D, r.argmax_origin)
+
+
+def ddks_combine_records(records) -> tuple[int, int, int]:
+    """Host combine of per-rank records [(num, argmax_origin, flags), ...] -> (num, argmax_origin, flags)."""
+    n = len(records)
+    arr = (ddks_rank_record * n)(*[ddks_rank_record(int(a), int(b), int(c), 0) for a, b, c in records])
+    out = ddks_rank_record()
+    _check(LIB.ddks_combine_records(arr, n, ctypes.byref(out)))
+    return int(out.num), int(out.argmax_origin), int(out.flags)
+
+
+def ddks_unpad_items(gathered, total: int, world: int, n_arr: int = 1):
+    """Host unpad of an all-gathered per-item block (include/ddks.h) -> (uint64 [n_arr, total], flags)."""
+    g = np.ascontiguousarray(np.asarray(gathered, dtype=np.uint64))
+    out = np.zeros((n_arr, total), dtype=np.uint64)
+    fl = ctypes.c_uint32()
+    _check(LIB.ddks_unpad_items(g.ctypes.data, total, world, n_arr, out.ctypes.data, ctypes.byref(fl)))
+    return out, int(fl.value)
+
+
+def gather_stride(total: int, world: int, n_arr: int = 1) -> int:
+    """uint64 words per rank record of ddks_unpad_items' layout: n_arr * ceil(total / world) + 1."""
+    return n_arr * (-(-total // world)) + 1
+
+
+def ddks_profile_work(ctx) -> int:
+    """FP32 compares the classify kernels executed since the last read (context needs DDKS_FLAG_PROFILE)."""
+    v = ctypes.c_uint64()
+    _check(LIB.ddks_profile_work(ctx, ctypes.byref(v)), ctx)
+    return int(v.value)
 
 
 def ddks_launch_count(ctx) -> int:
@@ -380,6 +457,9 @@ class Context:
 
     def profile_clock(self) -> float:
         return ddks_profile_clock(self.ctx)
+
+    def profile_work(self) -> int:
+        return ddks_profile_work(self.ctx)
 
     @property
     def kd_levels(self) -> int:

@@ -69,6 +69,19 @@ def test_vdks_c2_full(ctx):
         assert (got.num, got.den) == O.vdks(P, Q, k)[:2]
 
 
+def test_vdks_c5_k16_vs_stored_oracle(ctx):
+    # the bench's vdKS configuration (C5, k = 16) against the oracle's full literal run (Alg. 1 SumOrthants over
+    # every voxel for every filled voxel; tests/golden/make_c5_vdks_oracle.py, minutes of CPU, so stored): bit-exact
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "c5_vdks16_oracle.json")
+    g = json.load(open(path))
+    P, Q = I.config("C5")
+    assert I.sha256_pq(P, Q) == g["input_sha256"] and g["k"] == 16
+    got = ctx.vdks(dev(P), dev(Q), 16)
+    assert (got.num, got.den) == (g["num"], g["den"]) and float.hex(got.D) == g["D_hex"]
+
+
 def test_vdks_c5_properties(ctx):
     # full C5 (10^6 + 10^6, d = 5, k = 16): the oracle's literal SumOrthants is O(F k^d); use properties that hold
     # at any size: symmetry and power-of-two scale invariance (NormalizeData removes it exactly)

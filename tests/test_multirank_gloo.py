@@ -1,7 +1,8 @@
-"""Multi-rank host logic on CPU (gloo, world_size 2): the sharding the library uses (ddks_shard_range, a
-host-only C-ABI call) and the combine semantics it implements with NCCL — all-reduce(max) of num, then
-all-reduce(min) of the argmax candidates for ddks_stat (position-ordered and x0-ordered origin shards);
-contiguous item shards + all-gather for batch and permutation calls; histogram all-reduce(sum) + sharded table +
+"""Multi-rank host logic on CPU (gloo, world_size 2 and 3): the sharding the library uses (ddks_shard_range, a
+host-only C-ABI call) and the combine steps it runs after its one NCCL all-gather, driven through the library's
+own exported host functions — ddks_combine_records for ddks_stat (one {num, argmax, flags} record per rank; also
+the x0-ordered origin shards below), ddks_unpad_items for the padded per-item records of batch, permutation and
+batched-significance calls (totals not divisible by the world size, fewer items than ranks); histogram all-reduce(sum) + sharded table +
 rank-ordered partial sums for the significance; voxel shards (vdKS) and corner shards (rdKS) with max / min-index
 combines — reproduce the single-rank oracle result. Per-rank partial results come from the
 oracle restricted to the rank's shard (there is no GPU here); on a GPU box the same shards run in k_count."""
@@ -17,6 +18,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+STAT_CASES = [(37, 41, 3, "grid"), (200, 150, 5, "mixed"), (1, 2, 2, "normal"), (6, 5, 2, "grid")]
+BATCH_SIZES = [5, 7, 2, 1]  # totals not divisible by the world size, and fewer items than ranks
 
 
 def _free_port():
@@ -38,38 +41,38 @@ def _worker(rank, world, port, q):
         from paper_2106_13706_b200 import inputs as I
 
         out = {}
-        # ---- ddks_stat: origins sharded, max + argmax combine
-        for seed, (n_P, n_Q, d, kind) in enumerate([(37, 41, 3, "grid"), (200, 150, 5, "mixed"), (1, 2, 2, "normal")]):
+        # ---- ddks_stat: origins sharded; every rank contributes ONE record {num, argmax candidate, flags} (the library's
+        # single all-gather), combined by the library's exported host step ddks_combine_records
+        for seed, (n_P, n_Q, d, kind) in enumerate(STAT_CASES):
             P, Q = I.random_pair(700 + seed, n_P, n_Q, d, kind)
             N = n_P + n_Q
             b, e = K.ddks_shard_range(N, world, rank)
             per = O.per_origin(P, Q, b, e) if e > b else np.zeros(0, np.uint64)
             local = int(per.max()) if per.size else 0
-            t = torch.tensor([local], dtype=torch.int64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            num = int(t.item())
-            cand = b + int(np.argmax(per == num)) if per.size and (per == num).any() else 2**62
-            a = torch.tensor([cand], dtype=torch.int64)
-            dist.all_reduce(a, op=dist.ReduceOp.MIN)
-            out[f"stat{seed}"] = (num, int(a.item()))
-        # ---- ddks_stat_batch: items sharded, all-gather (padded to the largest shard)
+            cand = b + int(np.argmax(per == local)) if per.size else -1
+            rec = torch.tensor([local, cand, 1 if seed == 2 and rank == world - 1 else 0], dtype=torch.int64)
+            recs = [torch.zeros(3, dtype=torch.int64) for _ in range(world)]
+            dist.all_gather(recs, rec)
+            out[f"stat{seed}"] = K.ddks_combine_records([tuple(int(v) for v in r.tolist()) for r in recs])
+        # ---- ddks_stat_batch / ddks_permutation_null: items sharded; ONE all-gather of records padded to the largest
+        # shard (this rank's nums, then its flags word), unpadded by the library's exported ddks_unpad_items
         rng = np.random.default_rng(3)
-        B = 5
-        Pb = rng.integers(0, 4, (B, 9, 3)).astype(np.float32)
-        Qb = rng.integers(0, 4, (B, 8, 3)).astype(np.float32)
-        b, e = K.ddks_shard_range(B, world, rank)
-        b0, e0 = K.ddks_shard_range(B, world, 0)
-        chunk = e0 - b0
-        mine = np.zeros(chunk, np.int64)
-        if e > b:
-            mine[: e - b] = O.batch(Pb[b:e], Qb[b:e]).astype(np.int64)
-        gathered = [torch.zeros(chunk, dtype=torch.int64) for _ in range(world)]
-        dist.all_gather(gathered, torch.from_numpy(mine))
-        full = []
-        for r in range(world):
-            rb, re = K.ddks_shard_range(B, world, r)
-            full += gathered[r][: re - rb].tolist()
-        out["batch"] = full
+        for B in BATCH_SIZES:
+            Pb = rng.integers(0, 4, (B, 9, 3)).astype(np.float32)
+            Qb = rng.integers(0, 4, (B, 8, 3)).astype(np.float32)
+            b, e = K.ddks_shard_range(B, world, rank)
+            stride = K.gather_stride(B, world, 2)
+            chunk = (stride - 1) // 2
+            rec = np.zeros(stride, np.uint64)
+            if e > b:
+                rec[: e - b] = O.batch(Pb[b:e], Qb[b:e])
+                rec[chunk: chunk + e - b] = np.arange(b, e, dtype=np.uint64) * 7  # a second per-item array
+            rec[2 * chunk] = 2 if rank == 0 and B == 7 else 0  # flags word
+            gathered = [torch.zeros(stride, dtype=torch.int64) for _ in range(world)]
+            dist.all_gather(gathered, torch.from_numpy(rec.view(np.int64)))
+            flat = torch.cat(gathered).numpy().view(np.uint64)
+            items, flags = K.ddks_unpad_items(flat, B, world, 2)
+            out[f"batch{B}"] = (items[0].tolist(), items[1].tolist(), flags, O.batch(Pb, Qb).tolist())
 
         # ---- x0-ordered ddks_stat: ranks shard POSITIONS of the x_0 order (ties keep pooled order); each rank's
         # per-origin nums land in a zeroed pooled-order array; max, then argmax over the full array, min over ranks
@@ -130,7 +133,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 3])
 def test_sharded_combine_equals_single_rank(world):
     sys.path.insert(0, ROOT)
     from oracle import oracle as O
@@ -146,17 +149,16 @@ def test_sharded_combine_equals_single_rank(world):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for seed, (n_P, n_Q, d, kind) in enumerate([(37, 41, 3, "grid"), (200, 150, 5, "mixed"), (1, 2, 2, "normal")]):
+    for seed, (n_P, n_Q, d, kind) in enumerate(STAT_CASES):
         P, Q = I.random_pair(700 + seed, n_P, n_Q, d, kind)
         num, den, D, arg = O.ddks(P, Q)
         for r in range(world):
-            assert res[r][f"stat{seed}"] == (num, arg)
-    rng = np.random.default_rng(3)
-    Pb = rng.integers(0, 4, (5, 9, 3)).astype(np.float32)
-    Qb = rng.integers(0, 4, (5, 8, 3)).astype(np.float32)
-    want = O.batch(Pb, Qb).tolist()
-    for r in range(world):
-        assert res[r]["batch"] == want
+            assert res[r][f"stat{seed}"] == (num, arg, 1 if seed == 2 else 0)
+    for B in BATCH_SIZES:
+        for r in range(world):
+            nums, second, flags, want = res[r][f"batch{B}"]
+            assert nums == want and second == [7 * i for i in range(B)]
+            assert flags == (2 if B == 7 else 0)
     # x0-ordered sharding == single-rank statistic and argmax
     P, Q = I.random_pair(733, 90, 70, 4, "grid")
     num, den, D, arg = O.ddks(P, Q)

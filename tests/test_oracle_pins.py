@@ -300,6 +300,25 @@ def test_c4_spots():
     assert p_num == 1 and p == 1 / 1001
 
 
+def test_stored_c4_oracle_matches_survey_aggregates(golden_dir):
+    # tests/golden/c4_oracle.json (every C4a item, every C4b permutation; written by make_c4_oracle.py, oracle only)
+    # belongs to these input bytes and this oracle source, and agrees with the survey's independent NumPy computation
+    # (SURVEY.md §8c C4a/C4b rows): the per-pair spots, the max and the sum over all 4096 items, the null's max and sum
+    import hashlib
+    g = json.load(open(os.path.join(golden_dir, "c4_oracle.json")))
+    assert g["input_sha256"] == I.SURVEY_SHA256["C4"] and g["perms_sha256"] == I.SURVEY_SHA256["C4_perms"]
+    src = open(os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "ddks_oracle.c"), "rb").read()
+    assert g["oracle_c_sha256"] == hashlib.sha256(src).hexdigest()
+    b = np.array(g["batch_num"], dtype=np.int64)
+    assert len(b) == 4096 and g["den"] == 512 * 512
+    assert b[:5].tolist() == [19968, 19456, 31232, 24576, 19456]
+    assert b[2048:2053].tolist() == [39936, 36352, 30208, 39424, 30720]
+    assert int(b.max()) == 56_320 and int(b.sum()) == 122_770_432
+    null = np.array(g["null_num"], dtype=np.int64)
+    assert len(null) == 1000 and int(null.max()) == 34_816 and int(null.sum()) == 23_215_616
+    assert g["observed_num"] == 39_936 == b[2048] and g["p_num"] == 1 and g["p_value"] == 1 / 1001
+
+
 # ------------------------------------------------------------------------------------ analytic significance (§3)
 
 def test_significance_pmf_pins():
@@ -358,6 +377,30 @@ def test_significance_statistic_pins():
     S_b, _, _ = O.significance(P, Q)
     S_p, _, _ = O.significance(P, Q, poisson=True)
     assert 0.0 <= S_b <= 1.0 and 0.0 <= S_p <= 1.0
+
+
+def test_significance_hand_derived_golden(golden_dir):
+    # tests/golden/significance_hand.json: S derived by hand from P:L208-209 (test points = both sets)
+    # (lambda-hat = (M_T+1)/(N_T+2)), P:L244-268 (binomial pmf, Delta band), P:L276 (product over all 2^d x N cells,
+    # empty orthants included) and P:L278-281 (Poisson). The alternative readings (lambda = M_T/N_T; T-only test
+    # points) give values far outside the tolerance, so either mistake fails here.
+    g = json.load(open(os.path.join(golden_dir, "significance_hand.json")))
+    for c in g["cases"]:
+        P, Q = np.array(c["P"], np.float32), np.array(c["Q"], np.float32)
+        S, lp, num = O.significance(P, Q)
+        assert num == c["num"] and P.shape[0] * Q.shape[0] == c["den"], c["name"]
+        assert abs(lp - c["log_prod_value"]) <= 1e-14, (c["name"], lp)
+        assert abs(S - c["S_value"]) <= 1e-14, (c["name"], S)
+        for reading, alt in c.get("other_readings", {}).items():
+            assert abs(alt["log_prod_value"] - c["log_prod_value"]) > 0.1, reading
+        if "poisson" in c:
+            _, lpp, _ = O.significance(P, Q, poisson=True)
+            assert abs(lpp - c["poisson"]["log_prod_value"]) <= 1e-14, (c["name"], lpp)
+        # the factors themselves: p(d <= D | lambda-hat) per M_T value
+        for key, frac in c["factors"].items():
+            m = int(key.split("=")[1])
+            lam = (m + 1) / (Q.shape[0] + 2)
+            assert abs(O.p_le(c["num"], P.shape[0], Q.shape[0], lam) - float(Fraction(frac))) <= 1e-15, (c["name"], key)
 
 
 # ------------------------------------------------------------------------------------ vdKS (Alg. 1) and rdKS (Alg. 2)
@@ -482,3 +525,16 @@ def test_stored_c5_oracle_matches_inputs_and_oracle_source():
     assert g["den"] == 10**12 and 0 < g["num"] <= g["den"] and float.fromhex(g["D_hex"]) == g["num"] / g["den"]
     # the survey's independent per-origin spot values bound it from below
     assert g["num"] >= 42316 * 10**6
+
+
+def test_stored_c5_vdks_oracle_matches_inputs_and_oracle_source(golden_dir):
+    # tests/golden/c5_vdks16_oracle.json (make_c5_vdks_oracle.py, oracle only) belongs to these input bytes and this
+    # oracle source; vdKS is an approximation of the exact statistic (R16), so it sits below the whole-C5
+    # exact num of c5_oracle.json and above the survey's per-origin spots' cell-level counterpart is not implied
+    import hashlib
+    g = json.load(open(os.path.join(golden_dir, "c5_vdks16_oracle.json")))
+    assert g["input_sha256"] == I.SURVEY_SHA256["C5"] and g["k"] == 16
+    src = open(os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "ddks_oracle.c"), "rb").read()
+    assert g["oracle_c_sha256"] == hashlib.sha256(src).hexdigest()
+    assert g["den"] == 10**12 and 0 < g["num"] <= g["den"] and float.fromhex(g["D_hex"]) == g["num"] / g["den"]
+    assert g["num"] % 10**6 == 0  # n_P = n_Q: every |orthant sum| is a multiple of n_P (exact integer Diff, R16)

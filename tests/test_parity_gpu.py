@@ -242,20 +242,33 @@ def test_config_c1_c2_c3_full(ctx):
         check_pair(ctx, P, Q)
 
 
-def test_config_c4_batch_and_perms(ctx):
+def test_config_c4_every_item_and_permutation(ctx, golden_dir):
+    # full C4 in the bench's launch configuration: EVERY one of the 4096 batch items and EVERY one of the 1000
+    # null permutations element by element against the oracle's full run (tests/golden/c4_oracle.json, written by
+    # make_c4_oracle.py from oracle/ only and pinned to the survey's independent aggregates in test_oracle_pins.py),
+    # plus a live oracle run on a seeded sample of items and permutations
+    g = json.load(open(os.path.join(golden_dir, "c4_oracle.json")))
     P, Q = I.config("C4")
+    assert I.sha256_pq(P, Q) == g["input_sha256"]
     got = ctx.stat_batch(dev(P), dev(Q))
-    idx = [0, 1, 2, 3, 4, 777, 2047, 2048, 2049, 2050, 2051, 2052, 4095]
-    want = O.batch(P[idx], Q[idx])
-    assert [got[i].num for i in idx] == want.tolist()
     nums = np.array([r.num for r in got], dtype=np.uint64)
-    assert int(nums.max()) == 56_320 and int(nums.sum()) == 122_770_432  # SURVEY.md §8c C4a (independent)
+    want = np.array(g["batch_num"], dtype=np.uint64)
+    bad = np.nonzero(nums != want)[0]
+    assert bad.size == 0, (bad[:10], nums[bad[:10]], want[bad[:10]])
+    assert all(r.den == g["den"] and r.D == r.num / g["den"] for r in got)
+    rng = np.random.default_rng(44)
+    idx = np.sort(rng.choice(4096, 96, replace=False))
+    assert nums[idx].tolist() == O.batch(P[idx], Q[idx]).tolist()
     perms = I.c4_perms()
     pooled = np.concatenate([P[I.C4_PERM_PAIR], Q[I.C4_PERM_PAIR]])
     null, obs, p = ctx.permutation_null(dev(pooled), 512, dev(perms))
-    o_null, o_obs, o_pnum, o_p = O.permutation_null(pooled, 512, perms[:64])
-    assert np.array_equal(null[:64], o_null) and obs.num == o_obs == 39_936
-    assert int(null.max()) == 34_816 and int(null.sum()) == 23_215_616 and p == 1 / 1001
+    want_null = np.array(g["null_num"], dtype=np.uint64)
+    bad = np.nonzero(null != want_null)[0]
+    assert bad.size == 0, (bad[:10], null[bad[:10]], want_null[bad[:10]])
+    assert obs.num == g["observed_num"] and p == g["p_value"]
+    jdx = np.sort(rng.choice(1000, 48, replace=False))
+    o_null, o_obs, _, _ = O.permutation_null(pooled, 512, perms[jdx])
+    assert np.array_equal(null[jdx], o_null) and o_obs == obs.num
 
 
 def test_config_c5_sampled(ctx):
@@ -342,7 +355,7 @@ KD_CASES = [(2, "2,5,1", 9000, 7000, 2, "normal"), (2, "2,3,1", 6000, 6000, 3, "
 def test_kd_ordered_parity(monkeypatch, ctx_nox0, K_, env, n_P, n_Q, d, kind):
     # K levels of kd ordering (bits 0..K-1 decided per tile where the tile's box does not interleave with the CTA's
     # origins'); DDKS_KD fixes the level and the slab / cell counts so small inputs still get several cells (and
-    # empty ones: 3,9,9 and 4,5,5,5); K = 4 is reached through DDKS_KD only (the test flag holds 1..3)
+    # empty ones: 3,9,9 and 4,5,5,5)
     if env is None:
         monkeypatch.delenv("DDKS_KD", raising=False)
     else:

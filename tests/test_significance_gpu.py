@@ -224,3 +224,22 @@ def test_significance_batch_many_small(ctx):
         assert got[b].stat.num == num_o
         assert abs(got[b].log_prod - lp_o) <= got[b].cells * tol_entry(50, 50) + 1e-12 * abs(lp_o)
     assert all(0.0 <= g.S <= 1.0 for g in got)
+
+
+def test_significance_hand_derived_golden(ctx):
+    # the GPU path against the hand-derived values of tests/golden/significance_hand.json (pinned for the
+    # oracle in test_oracle_pins.py): integers exact, log_prod / S within the derived per-cell tolerance
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "significance_hand.json")))
+    for c in g["cases"]:
+        P, Q = np.array(c["P"], np.float32), np.array(c["Q"], np.float32)
+        r = ctx.significance(dev(P), dev(Q))
+        tol = sum(c["cells"].values()) * tol_entry(P.shape[0], Q.shape[0])
+        assert (r.stat.num, r.stat.den) == (c["num"], c["den"]), c["name"]
+        assert r.cells == sum(c["cells"].values())
+        assert abs(r.log_prod - c["log_prod_value"]) <= tol, (c["name"], r.log_prod)
+        assert abs(r.S - c["S_value"]) <= tol, (c["name"], r.S)
+        if "poisson" in c:
+            rp = ctx.significance(dev(P), dev(Q), poisson=True)
+            assert abs(rp.log_prod - c["poisson"]["log_prod_value"]) <= tol, (c["name"], rp.log_prod)
