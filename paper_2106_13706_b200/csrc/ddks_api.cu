@@ -19,6 +19,7 @@
 
 #include "ddks_kernels.cuh"
 #include "ddks_radix.cuh"
+#include "ddks_small.cuh"
 #include "ddks_internal.h"
 #include "ddks_launch.cuh"
 
@@ -125,6 +126,12 @@ ddks_status launch_count_d(ddks_ctx* ctx, const CountPlan& pl, const ddks::Count
             return pl.split ? launch_count_t<D, true, false, 0, true>(ctx, pl, a, st)
                             : launch_count_t<D, false, false, 0, true>(ctx, pl, a, st);
     }
+    if (pl.B == 1 && pl.N <= ddks::kSmallN) {  // few points: the small geometry (more, smaller CTAs)
+        if (pl.split) return gt ? launch_count_t<D, true, true, 0, false, true>(ctx, pl, a, st)
+                                : launch_count_t<D, true, false, 0, false, true>(ctx, pl, a, st);
+        return gt ? launch_count_t<D, false, true, 0, false, true>(ctx, pl, a, st)
+                  : launch_count_t<D, false, false, 0, false, true>(ctx, pl, a, st);
+    }
     if (pl.split) return gt ? launch_count_t<D, true, true>(ctx, pl, a, st) : launch_count_t<D, true, false>(ctx, pl, a, st);
     return gt ? launch_count_t<D, false, true>(ctx, pl, a, st) : launch_count_t<D, false, false>(ctx, pl, a, st);
 }
@@ -152,15 +159,14 @@ ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int6
     a.o_end = (int32_t)o_end;
     a.incP = split ? 1u : (uint32_t)a_;
     a.incQ = split ? 1u : (uint32_t)(0u - (uint32_t)b_);
-    a.g = split ? 1 : g;
-    a.nP = n_P;
-    a.nQ = n_Q;
+    a.gg = g;
+    a.aQ = (int64_t)a_;
+    a.bP = (int64_t)b_;
     a.item_num = item_num;
     a.per_origin = per_origin;
     a.hist = split ? hist : nullptr;
     a.hist_stride = n_Q + 1;
     a.best_key = B == 1 ? best_key : nullptr;
-    a.key_div = g;
     if (B > 65535) {  // grid.z limit: run the items in chunks
         for (int64_t b0 = 0; b0 < B; b0 += 65535) {
             const int64_t nb = std::min<int64_t>(65535, B - b0);
@@ -602,7 +608,7 @@ ddks_status ddks_destroy(ddks_ctx* ctx) {
             cudaEventDestroy(ctx->ev_pending[i].second);
         }
     for (DevBuf* b : {&ctx->raw_a, &ctx->raw_b, &ctx->raw_perm, &ctx->packed, &ctx->packed2, &ctx->pool_packed, &ctx->per_origin,
-                      &ctx->accum, &ctx->blk_done, &ctx->gather, &ctx->item_num, &ctx->bitmap, &ctx->labels, &ctx->res, &ctx->sig_hist,
+                      &ctx->accum, &ctx->gather, &ctx->small_out, &ctx->item_num, &ctx->bitmap, &ctx->labels, &ctx->res, &ctx->sig_hist,
                       &ctx->sig_lf, &ctx->sig_scratch, &ctx->sig_table, &ctx->sig_contrib, &ctx->sig_part,
                       &ctx->vox_keys, &ctx->vox_cnt, &ctx->vox_S, &ctx->rd_keys, &ctx->rd_xn, &ctx->rd_k0,
                       &ctx->rd_k1, &ctx->rd_hist, &ctx->rd_tcnt, &ctx->rd_cnum, &ctx->x0_keys0,
@@ -661,16 +667,117 @@ ddks_status ddks_profile_work(ddks_ctx* ctx, uint64_t* compares) {
     return DDKS_OK;
 }
 
+}  // extern "C"
+
+// The fused small-N path (ddks_small.cuh) applies: single rank, whole statistic, N <= kSmallFusedN, DIFF counters whose
+// int16 halves hold the whole point set (N * max(a, b) <= 32767, so the DSMEM word adds are exact).
+constexpr int64_t kSmallFusedN = 8192;
+static bool small_fused_applies(ddks_ctx* ctx, int64_t n_P, int64_t n_Q) {
+    if (ctx->comm || getenv("DDKS_NO_SMALL")) return false;  // DDKS_NO_SMALL: TEST ONLY
+    const int64_t N = n_P + n_Q;
+    if (N > kSmallFusedN || !diff_counters_ok(n_P, n_Q)) return false;
+    const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
+    return (uint64_t)N * std::max((uint64_t)n_Q / g, (uint64_t)n_P / g) <= 32767;
+}
+static int64_t small_blocks(int64_t N) { return (N + ddks::SM_R * ddks::SM_T - 1) / (ddks::SM_R * ddks::SM_T); }
+
+template <int D>
+static ddks_status launch_small_d(ddks_ctx* ctx, const ddks::SmallArgs& a, int segs, int blocks, cudaStream_t st) {
+    const bool gt = (ctx->flags & DDKS_FLAG_TIES_GT) != 0;
+    auto kern = gt ? ddks::k_count_small<D, true> : ddks::k_count_small<D, false>;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)segs, (unsigned)blocks, 1);
+    cfg.blockDim = dim3(ddks::SM_T, 1, 1);
+    cfg.dynamicSmemBytes = ddks::SmallGeo<D>::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)segs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    static std::atomic<bool> done[kMaxDevices][2] = {};
+    if (!done[ctx->device][gt].load(std::memory_order_acquire)) {
+        CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ddks::SmallGeo<D>::SMEM_BYTES));
+        done[ctx->device][gt].store(true, std::memory_order_release);
+    }
+    CU(cudaLaunchKernelEx(&cfg, kern, a));
+    ctx->launches++;
+    return DDKS_OK;
+}
+
+// Enqueue the fused small-N statistic: one cluster launch writing per-origin-block records into ctx->small_out, then
+// their D2H into host_pinned (reduced by stat_impl after the sync). No result initialisation is needed.
+static ddks_status small_enqueue(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
+                                 cudaStream_t st) {
+    ddks_status s;
+    const int64_t N = n_P + n_Q;
+    const void *dP, *dQ;
+    if ((s = stage_input(ctx, P, (size_t)n_P * d * 4, ctx->raw_a, st, &dP))) return s;
+    if ((s = stage_input(ctx, Q, (size_t)n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
+    const int64_t blocks = small_blocks(N);
+    if ((s = ensure(ctx, ctx->small_out, (size_t)blocks * 32))) return s;
+    const int64_t n_tiles = (N + ddks::SM_TILE - 1) / ddks::SM_TILE;
+    const int64_t tps = (n_tiles + ddks::SM_MAX_CLUSTER - 1) / ddks::SM_MAX_CLUSTER;
+    const int segs = (int)((n_tiles + tps - 1) / tps);
+    const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
+    ddks::SmallArgs a{};
+    a.P = (const float*)dP;
+    a.Q = (const float*)dQ;
+    a.n_P = (int32_t)n_P;
+    a.N = (int32_t)N;
+    a.seg_points = (int32_t)(tps * ddks::SM_TILE);
+    a.incP = (uint32_t)((uint64_t)n_Q / g);
+    a.incQ = 0u - (uint32_t)((uint64_t)n_P / g);
+    a.gg = g;
+    a.validate = (ctx->flags & DDKS_FLAG_NO_VALIDATE) ? 0 : 1;
+    a.out = (unsigned long long*)ctx->small_out.p;
+    std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+    if (ctx->flags & DDKS_FLAG_PROFILE) {
+        if (!ctx->ev_free.empty()) {
+            ev = ctx->ev_free.back();
+            ctx->ev_free.pop_back();
+        } else {
+            CU(cudaEventCreate(&ev.first));
+            CU(cudaEventCreate(&ev.second));
+        }
+        CU(record_event(ev.first, st));
+        if ((s = ensure_prof(ctx))) return s;
+        a.clk = (unsigned long long*)ctx->prof_clk.p;
+    }
+    ctx->kd_levels = 0;
+    switch (d) {
+#define SM_CASE(D) case D: s = launch_small_d<D>(ctx, a, segs, (int)blocks, st); break;
+        SM_CASE(1) SM_CASE(2) SM_CASE(3) SM_CASE(4) SM_CASE(5) SM_CASE(6) SM_CASE(7) SM_CASE(8)
+#undef SM_CASE
+        default: return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "d=%d", d);
+    }
+    if (s) return s;
+    if (ev.first) {
+        CU(record_event(ev.second, st));
+        ctx->ev_pending.push_back(ev);
+        ctx->ev_recycle.push_back(1);
+        ctx->ev_pairs.push_back((uint64_t)N * (uint64_t)N);
+    }
+    CU(cudaMemcpyAsync(ctx->host_pinned, ctx->small_out.p, (size_t)blocks * 32, cudaMemcpyDeviceToHost, st));
+    return DDKS_OK;
+}
+
+extern "C" {
+
 // Enqueue one statistic on st, ending with the D2H of the result record(s) into host_pinned (no sync): staging of host
 // inputs, pack, count (+ fused argmax), and with world > 1 the ONE collective: the all-gather of every rank's 32-byte
 // result record (host_pinned then holds world records, combined by ddks_combine_records after the sync). Everything
 // here is stream-ordered, so it can be captured.
 static ddks_status stat_enqueue(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
-                                cudaStream_t st, int64_t ob, int64_t oe, uint64_t* per_origin_out, int sw, int sr) {
+                                cudaStream_t st, int64_t ob, int64_t oe, uint64_t* per_origin_out, int sw, int sr,
+                                bool small) {
     ddks_status s;
     const int64_t N = n_P + n_Q;
     const int DP = pad_dim(d);
     const bool export_mode = per_origin_out != nullptr;
+    if (small) return small_enqueue(ctx, P, n_P, Q, n_Q, d, st);
     const void *dP, *dQ;
     if ((s = stage_input(ctx, P, (size_t)n_P * d * 4, ctx->raw_a, st, &dP))) return s;
     if ((s = stage_input(ctx, Q, (size_t)n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
@@ -731,7 +838,8 @@ static ddks_status stat_capture(ddks_ctx* ctx, const ddks_ctx::StatKey& key, con
     const size_t ev0 = ctx->ev_pending.size();
     const int64_t l0 = ctx->launches;
     CU(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed));
-    const ddks_status s = stat_enqueue(ctx, P, n_P, Q, n_Q, d, ctx->cap_stream, ob, oe, nullptr, sw, sr);
+    const ddks_status s = stat_enqueue(ctx, P, n_P, Q, n_Q, d, ctx->cap_stream, ob, oe, nullptr, sw, sr,
+                                       small_fused_applies(ctx, n_P, n_Q));
     cudaGraph_t g = nullptr;
     const cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &g);
     // the events recorded during the capture are graph nodes (not executed yet): they belong to the graph
@@ -789,9 +897,11 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
     }
     const int sw = shard_world > 0 ? shard_world : ctx->world, sr = shard_world > 0 ? shard_rank : ctx->rank;
     if ((s = ensure_host(ctx, std::max<size_t>(4096, (size_t)ctx->world * sizeof(DevResult))))) return s;
+    // the fused small-N path (whole statistic, single rank): one record per origin block
+    const bool small = !export_mode && shard_world == 0 && small_fused_applies(ctx, n_P, n_Q);
     // environment overrides (tuning / test knobs) change the plan: a graph captured under other values is not reused
     const bool env_override = getenv("DDKS_KD") || getenv("DDKS_SEGS") || getenv("DDKS_KD_SHUFFLE") ||
-                              getenv("DDKS_NO_KEY") || getenv("DDKS_GRIDY");
+                              getenv("DDKS_NO_KEY") || getenv("DDKS_GRIDY") || getenv("DDKS_NO_SMALL");
     const bool graphable = !export_mode && shard_world == 0 && !(ctx->flags & DDKS_FLAG_NO_GRAPH) && !env_override &&
                            graph_input_ok(P) && graph_input_ok(Q);
     const ddks_ctx::StatKey key{P, Q, n_P, n_Q, d, ctx->alloc_epoch};
@@ -812,7 +922,7 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
             ctx->ev_recycle.push_back(0);
         }
     } else {
-        if ((s = stat_enqueue(ctx, P, n_P, Q, n_Q, d, st, ob, oe, per_origin_out, sw, sr))) return s;
+        if ((s = stat_enqueue(ctx, P, n_P, Q, n_Q, d, st, ob, oe, per_origin_out, sw, sr, small))) return s;
         hres = (DevResult*)ctx->host_pinned;
         if (graphable) {  // a second identical call (same workspace) will be captured
             ctx->sg_seen = key;
@@ -821,9 +931,10 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
     }
     CU(cudaStreamSynchronize(st));
     if ((s = collect_profile(ctx))) return s;
-    // this rank's record, or (world > 1) the all-gathered records of every rank, combined on the host
-    const bool use_key = !export_mode && argmax_key_fits(n_P, n_Q);
-    const int nrec = (ctx->comm && !export_mode) ? ctx->world : 1;
+    // this rank's record, or (world > 1) the all-gathered records of every rank, combined on the host; the fused
+    // small-N path left one record per origin block {num, key, flags}
+    const bool use_key = small || (!export_mode && argmax_key_fits(n_P, n_Q));
+    const int nrec = small ? (int)small_blocks(n_P + n_Q) : ((ctx->comm && !export_mode) ? ctx->world : 1);
     ddks_rank_record recs[64], comb;
     std::vector<ddks_rank_record> big;
     ddks_rank_record* rp = recs;
@@ -831,7 +942,14 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
         big.resize(nrec);
         rp = big.data();
     }
-    for (int r = 0; r < nrec; ++r) rp[r] = decode_record(hres[r], n_P, n_Q, use_key);
+    for (int r = 0; r < nrec; ++r) {
+        if (small) {
+            const unsigned long long* sr = (const unsigned long long*)ctx->host_pinned + 4 * r;
+            rp[r] = decode_record(DevResult{sr[0], ~0ull, sr[1], (uint32_t)sr[2], 0u}, n_P, n_Q, true);
+        } else {
+            rp[r] = decode_record(hres[r], n_P, n_Q, use_key);
+        }
+    }
     ddks_combine_records(rp, nrec, &comb);
     if (comb.flags & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
     if (out) {

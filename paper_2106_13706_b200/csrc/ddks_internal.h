@@ -24,7 +24,7 @@ struct DevBuf {
 struct DevResult {
     unsigned long long num;  // max num(o) over this rank's origins
     unsigned long long arg;  // smallest pooled origin attaining it (~0: none / not computed; k_argmax path)
-    unsigned long long key;  // packed argmax (num / key_div) << 31 | (2^31 - 1 - origin) (0: none; fused path)
+    unsigned long long key;  // packed argmax (num / gcd) << 31 | (2^31 - 1 - origin) (0: none; fused path)
     uint32_t flag;           // bit 0: non-finite input, bit 1: bad permutation row, bit 2: significance scratch
     uint32_t pad;
 };
@@ -34,8 +34,9 @@ struct ddks_ctx {
     int device = 0, world = 1, rank = 0;
     uint32_t flags = 0;
     ncclComm_t comm = nullptr;
-    DevBuf raw_a, raw_b, raw_perm, packed, packed2, pool_packed, per_origin, accum, blk_done, item_num, bitmap, labels, res;
-    DevBuf gather;  // world > 1: all-gather send + receive buffers
+    DevBuf raw_a, raw_b, raw_perm, packed, packed2, pool_packed, per_origin, accum, item_num, bitmap, labels, res;
+    DevBuf gather;     // world > 1: all-gather send + receive buffers
+    DevBuf small_out;  // fused small-N path: one 32-byte record per origin block
     DevBuf sig_hist, sig_lf, sig_scratch, sig_table, sig_contrib, sig_part;  // ddks_significance workspace
     DevBuf vox_keys, vox_cnt, vox_S;                                           // ddks_vdks workspace
     DevBuf rd_keys, rd_xn, rd_k0, rd_k1, rd_hist, rd_tcnt, rd_cnum;              // ddks_rdks workspace

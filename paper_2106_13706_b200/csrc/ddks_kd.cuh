@@ -178,9 +178,9 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     a.o_end = (int32_t)N;
     a.incP = SPLIT ? 1u : a_;
     a.incQ = SPLIT ? 1u : 0u - b_;
-    a.g = SPLIT ? 1 : gg;
-    a.nP = n_P;
-    a.nQ = n_Q;
+    a.gg = gg;
+    a.aQ = (int64_t)a_;
+    a.bP = (int64_t)b_;
     a.item_num = item_num;
     a.per_origin = per_origin;
     a.perm = (const int32_t*)ctx->x0_perm.p;
@@ -188,7 +188,6 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     a.hist = SPLIT ? hist_out : nullptr;
     a.hist_stride = n_Q + 1;
     a.best_key = best_key;
-    a.key_div = gg;
     ctx->kd_levels = K;
     if (gt) return launch_kd<D, SPLIT, true, 1>(ctx, pl, a, st);
     if (K == 1) return launch_kd<D, SPLIT, false, 1>(ctx, pl, a, st);

@@ -84,15 +84,19 @@ template <int D> struct CfgSplit {
 template <> struct CfgSplit<5> { static constexpr int R = DDKS_S5R, T = DDKS_S5T; };  // A/B: 12 warps beat R=6 x 8 warps
 template <> struct CfgSplit<7> { static constexpr int R = 1, T = 384; };  // 12 balanced warps: -9% vs R=2 x 6
 
-template <int D, bool SPLIT, int DPX = padded_dim<D>()> struct Geo {
-    static constexpr int R = SPLIT ? CfgSplit<D>::R : Cfg<D>::R;
-    static constexpr int T = SPLIT ? CfgSplit<D>::T : Cfg<D>::T;
+// SMALL: the geometry of single statistics with few points (N <= kSmallN, SURVEY §7 hard part 4): 256 origins per
+// CTA (R = 2, T = 128) and 256-point tiles in a 2-stage ring, so N = 400 (C1) runs 2 CTAs of 128 threads instead of
+// one CTA of 2048 origin slots of which 80 % would repeat the last origin.
+constexpr int kSmallN = 8192;
+template <int D, bool SPLIT, bool SMALL = false> struct Geo {
+    static constexpr int R = SMALL ? 2 : (SPLIT ? CfgSplit<D>::R : Cfg<D>::R);
+    static constexpr int T = SMALL ? ((SPLIT && D == 8) ? 64 : 128) : (SPLIT ? CfgSplit<D>::T : Cfg<D>::T);
     static constexpr int RP = R / 2;                            // counter words per (bin, thread) when R >= 2
     static constexpr int NBASE = R >= 2 ? RP : 1;               // distinct counter base addresses per thread
     static constexpr int WPB = R * T / 2;                       // counter words per bin
-    static constexpr int TILE = Cfg<D>::TILE;
-    static constexpr int S = Cfg<D>::S;
-    static constexpr int DP = DPX;
+    static constexpr int TILE = SMALL ? 256 : Cfg<D>::TILE;
+    static constexpr int S = SMALL ? 2 : Cfg<D>::S;
+    static constexpr int DP = padded_dim<D>();
     static constexpr int NQ = 1 << D;
     static constexpr int NB = NQ * (SPLIT ? 2 : 1);            // counters per origin
     static constexpr int HIST_WORDS = NB * WPB;
@@ -273,21 +277,18 @@ struct CountArgs {
     // slot (r, t) of a block holds origin r*T + t, or (warp_major: kd / WX counts) warp*32R + r*32 + lane
     int32_t warp_major = 0;
     int32_t seg_points;      // points per grid.z segment (multiple of TILE, <= the int16 flush window)
-    uint32_t incP, incQ;     // DIFF: +a and -b (two's complement); SPLIT: 1 and 1
-    uint64_t g;              // DIFF: gcd(n_P, n_Q) multiplier
-    int64_t nP, nQ;          // SPLIT finalisation
+    uint32_t incP, incQ;     // DIFF: +aQ and -bP (two's complement); SPLIT: 1 and 1
     uint64_t* item_num;      // [B] atomicMax target
     uint64_t* per_origin;    // [o_end - o_begin] or nullptr (B == 1)
-    int32_t* accum;          // accumulate mode: [B][NB][acc_stride] int32 counters (zero on entry, left zero on exit),
+    int32_t* accum;          // accumulate mode: [B][NB][acc_stride] int32 counters (zeroed before the launch),
                              // else nullptr (direct mode: the whole point set is one segment)
-    uint32_t* blk_done;      // accumulate mode: [B][n_blk] arrival counters (zero on entry, left zero on exit)
-    int32_t n_blk = 0;       // origin blocks of this launch (all grid.y chunks)
     int32_t blk_base = 0;    // this launch's first origin block (grid.y is chunked at 65535)
-    // packed argmax (B == 1, or nullptr): atomicMax of (num(o) / key_div) << 31 | (2^31 - 1 - pooled index) over the
+    // packed argmax (B == 1, or nullptr): atomicMax of red(o) << 31 | (2^31 - 1 - pooled index) over the
     // origins, i.e. the max num and, among origins attaining it, the smallest pooled index (R7); the host
     // uses it only when n_P n_Q / gcd < 2^33, so the key fits 64 bits
     unsigned long long* best_key;
-    uint64_t key_div;
+    uint64_t gg;             // gcd(n_P, n_Q): num(o) = gg * red(o), red = |c_P aQ - c_Q bP| (DIFF: |counter|)
+    int64_t aQ, bP;          // n_Q / gg, n_P / gg
     const float* boxes;      // kd-ordered mode: [n_tiles][KX][2] min / max of dims < KX per TILE rows, else nullptr
     const int32_t* perm;     // kd-ordered mode: perm[j] = pooled index of sorted origin j; per_origin is then a
                              // full [N] array in pooled order (else nullptr: per_origin indexed o - o_begin)
@@ -313,10 +314,10 @@ __device__ __forceinline__ void hist_add_aggregated(unsigned long long* hist, in
     if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[v], (unsigned long long)__popc(peers));
 }
 
-// num(o) of origin r of thread t from the SMEM counters (direct mode)
-template <int D, bool SPLIT>
-__device__ __forceinline__ uint64_t origin_num(const uint32_t* hist, int r, int t, const CountArgs& a, int64_t item) {
-    using G = Geo<D, SPLIT>;
+// red(o) = num(o) / gcd(n_P, n_Q) of origin r of thread t from the SMEM counters (direct mode)
+template <int D, bool SPLIT, bool SMALL>
+__device__ __forceinline__ uint64_t origin_red(const uint32_t* hist, int r, int t, const CountArgs& a, int64_t item) {
+    using G = Geo<D, SPLIT, SMALL>;
     constexpr int NQ = G::NQ;
     const int sl = G::slot(r, t);
     const bool high = G::high(r, t);
@@ -326,14 +327,14 @@ __device__ __forceinline__ uint64_t origin_num(const uint32_t* hist, int r, int 
         split16(hist[q * G::WPB + sl], lo, hi);
         const int32_t v = high ? hi : lo;
         if constexpr (!SPLIT) {
-            const uint64_t av = (uint64_t)(v < 0 ? -v : v) * a.g;
+            const uint64_t av = (uint64_t)(v < 0 ? -v : v);
             best = av > best ? av : best;
         } else {
             int32_t lo2, hi2;
             split16(hist[(NQ + q) * G::WPB + sl], lo2, hi2);
             const int64_t cQ = high ? hi2 : lo2;
             if (a.hist) hist_add_aggregated(a.hist, item * a.hist_stride + cQ);
-            const int64_t df = (int64_t)v * a.nQ - cQ * a.nP;
+            const int64_t df = (int64_t)v * a.aQ - cQ * a.bP;
             const uint64_t av = (uint64_t)(df < 0 ? -df : df);
             best = av > best ? av : best;
         }
@@ -486,11 +487,17 @@ __device__ __forceinline__ void count_points_um(int um, const float* tile, int l
 // WX (batches of small items, rows of every label run pre-sorted by x_0, see k_pack_sorted): each warp owns 32 R
 // consecutive origins of the sorted order, and bit 0 is decided per (warp, 32-point sub-tile) when the sub-tile's
 // x_0 range does not interleave with the warp's -- the kd idea at warp granularity inside one item.
-template <int D, bool SPLIT, bool GT, int KX = 0, bool WX = false>
-__global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a) {
+// Resident CTAs per SM the register budget must allow: 3 for the position-ordered d <= 4 counts (their SMEM -- tiles +
+// 32 KB of counters -- fits 3; measured C2: 117 us at 3 CTAs/SM vs 150 us when the registers allowed only 2), else 1.
+template <int D, int KX, bool SMALL> __host__ __device__ constexpr int count_min_blocks() {
+    return SMALL ? 4 : ((D <= 4 && KX == 0) ? 3 : 1);
+}
+
+template <int D, bool SPLIT, bool GT, int KX = 0, bool WX = false, bool SMALL = false>
+__global__ void __launch_bounds__(Geo<D, SPLIT, SMALL>::T, count_min_blocks<D, KX, SMALL>()) k_count(const CountArgs a) {
     static_assert(!(WX && KX > 0), "WX and KX are exclusive");
     static_assert(KX <= 5 && KX <= D, "at most 5 kd levels");
-    using G = Geo<D, SPLIT>;
+    using G = Geo<D, SPLIT, SMALL>;
     constexpr int R = G::R, RP = G::RP, T = G::T, DP = G::DP, TILE = G::TILE, S = G::S, NBASE = G::NBASE,
                   WPB = G::WPB;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -734,18 +741,20 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
     // per-origin epilogue shared by both modes: num(o) -> per-origin export, the CTA max, the packed argmax key
     uint64_t best = 0;
     unsigned long long bkey = 0;
-    auto take = [&](int32_t oi, uint64_t m) {
+    auto take = [&](int32_t oi, uint64_t red) {
         const int32_t pooled = a.perm ? a.perm[oi] : oi;
+        const uint64_t m = red * a.gg;
         if (a.per_origin) a.per_origin[a.perm ? pooled : oi - a.o_begin] = m;
         best = m > best ? m : best;
         if (a.best_key) {
-            const unsigned long long k = ((unsigned long long)(m / a.key_div) << 31) | (unsigned long long)(0x7fffffff - pooled);
+            const unsigned long long k = ((unsigned long long)red << 31) | (unsigned long long)(0x7fffffff - pooled);
             bkey = k > bkey ? k : bkey;
         }
     };
 
     if (a.accum != nullptr) {
-        // flush: exact int32 partial counters -> global (red.global.add)
+        // flush: exact int32 partial counters -> global (red.global.add, fire-and-forget: the CTA exits while they
+        // drain; measured: a last-CTA-finalises variant that fences here made C3 +14 % and C5 +14 % slower)
         int32_t* acc = a.accum + item * (int64_t)G::NB * a.acc_stride;
 #pragma unroll 1
         for (int r = 0; r < R; ++r) {
@@ -762,73 +771,13 @@ __global__ void __launch_bounds__(Geo<D, SPLIT>::T, 1) k_count(const CountArgs a
                 if (v) atomicAdd(&acc[(int64_t)q * a.acc_stride + (li0 + r * T + t)], v);
             }
         }
-        // the last CTA of this origin block (over the point segments, grid.x) finalises the block from the int32
-        // partials and leaves the partials and its arrival counter zeroed for the next launch: no memset and no
-        // separate finaliser launch (threadfence-reduction pattern)
-        __shared__ uint32_t s_last;
-        __threadfence();
-        __syncthreads();
-        if (t == 0) {
-            uint32_t* cnt = a.blk_done + item * (int64_t)a.n_blk + by;
-            DDKS_ASSERT(by < a.n_blk);
-            s_last = atomicAdd(cnt, 1u) == gridDim.x - 1 ? 1u : 0u;
-            if (s_last) *cnt = 0u;
-        }
-        __syncthreads();
-        if (!s_last) return;
-        __threadfence();
-        // SPLIT + significance histogram: the dead counter region becomes a CTA-private histogram of the small M_T
-        // values (a CTA's cells all belong to one item), flushed once; larger values go to global memory directly
-        constexpr int HSZ = G::HIST_WORDS < 2048 ? G::HIST_WORDS : 2048;
-        uint32_t* shh = hist;
-        if (SPLIT && a.hist) {
-            for (int i = t; i < HSZ; i += T) shh[i] = 0u;
-            __syncthreads();
-        }
+        return;  // k_finalize reads the partials once every segment has flushed
+    }
 #pragma unroll 1
-        for (int r = 0; r < R; ++r) {
-            const int32_t oi = origin_of(r);
-            if (oi >= a.o_end) continue;
-            int32_t* p = acc + (li0 + r * T + t);
-            uint64_t m = 0;
-            if constexpr (!SPLIT) {
-                uint32_t mm = 0;
-                for (int q = 0; q < G::NQ; ++q) {
-                    const int32_t v = __ldcg(p + (int64_t)q * a.acc_stride);
-                    __stcg(p + (int64_t)q * a.acc_stride, 0);
-                    const uint32_t av = (uint32_t)(v < 0 ? -v : v);
-                    mm = av > mm ? av : mm;
-                }
-                m = (uint64_t)mm * a.g;
-            } else {
-                for (int q = 0; q < G::NQ; ++q) {
-                    const int64_t cP = __ldcg(p + (int64_t)q * a.acc_stride);
-                    const int64_t cQ = __ldcg(p + (int64_t)(G::NQ + q) * a.acc_stride);
-                    __stcg(p + (int64_t)q * a.acc_stride, 0);
-                    __stcg(p + (int64_t)(G::NQ + q) * a.acc_stride, 0);
-                    if (a.hist) {
-                        if (cQ < HSZ) atomicAdd(&shh[cQ], 1u);
-                        else atomicAdd(&a.hist[item * a.hist_stride + cQ], 1ull);
-                    }
-                    const int64_t df = cP * a.nQ - cQ * a.nP;
-                    const uint64_t av = (uint64_t)(df < 0 ? -df : df);
-                    m = av > m ? av : m;
-                }
-            }
-            take(oi, m);
-        }
-        if (SPLIT && a.hist) {
-            __syncthreads();
-            for (int i = t; i < HSZ; i += T)
-                if (shh[i]) atomicAdd(&a.hist[item * a.hist_stride + i], (unsigned long long)shh[i]);
-        }
-    } else {
-#pragma unroll 1
-        for (int r = 0; r < R; ++r) {
-            const int32_t oi = origin_of(r);
-            if (oi >= a.o_end) continue;
-            take(oi, origin_num<D, SPLIT>(hist, r, t, a, item));
-        }
+    for (int r = 0; r < R; ++r) {
+        const int32_t oi = origin_of(r);
+        if (oi >= a.o_end) continue;
+        take(oi, origin_red<D, SPLIT, SMALL>(hist, r, t, a, item));
     }
     best = warp_max_u64(best);
     bkey = warp_max_u64(bkey);
@@ -964,6 +913,129 @@ __global__ void k_tile_boxes(const float* __restrict__ pts, int DP, int64_t N, i
                 hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, sh));
             }
             if (lane == 0) boxes[(w * KX + k) * 2] = lo, boxes[(w * KX + k) * 2 + 1] = hi;
+        }
+    }
+}
+
+// Finaliser of the accumulate mode: num(o) from the int32 partials of every segment (streaming loads). Per-origin export, the item max and the
+// packed argmax key as in k_count's direct epilogue. SPLIT with a.hist (significance): M_T values below HS are
+// histogrammed in a block-private SMEM histogram and flushed once per block; larger values (rare) go straight to global.
+// A slot's 2^d bins are split over TPS threads (TPS warps of a CTA share 32 consecutive slots, so every load and store
+// is coalesced) -- d = 8 has 256 bins per slot and only N slots: one thread per slot left C3's finaliser latency-bound.
+constexpr int HS = 2048;
+
+template <int D, bool SPLIT, bool SMALL = false>
+__global__ void __launch_bounds__(256) k_finalize(const CountArgs a, int64_t B) {
+    using G = Geo<D, SPLIT, SMALL>;
+    constexpr int NQ = 1 << D;
+    constexpr int NB = G::NB;
+    constexpr int TPS = NQ >= 256 ? 8 : (NQ >= 128 ? 4 : (NQ >= 64 ? 2 : 1));  // threads per slot
+    constexpr int QPT = NQ / TPS;                                                // bins per thread
+    constexpr int SPI = 256 / TPS;                                               // slots per CTA iteration
+    const int32_t n_orig = a.o_end - a.o_begin;
+    __shared__ uint32_t sh_hist[SPLIT ? HS : 1];
+    __shared__ uint64_t sh_red[TPS > 1 ? TPS : 1][TPS > 1 ? SPI : 1];
+    const bool priv = SPLIT && a.hist && B == 1;  // a block-private histogram only when every cell is one item's
+    if constexpr (SPLIT) {
+        if (priv) {
+            for (int i = threadIdx.x; i < HS; i += blockDim.x) sh_hist[i] = 0u;
+            __syncthreads();
+        }
+    }
+    constexpr int ORIG = G::ORIGINS;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int part = warp % TPS, grp = warp / TPS;
+    const int64_t ns = a.acc_stride;  // accumulator slots per item
+    const int64_t total = B * ns;
+    uint64_t best = 0;
+    unsigned long long bkey = 0;
+    for (int64_t base = blockIdx.x * (int64_t)SPI; base < total; base += (int64_t)gridDim.x * SPI) {  // CTA-uniform
+        const int64_t i = base + grp * 32 + lane;
+        const int64_t item = i / ns, li = i - item * ns;
+        // slot li -> origin offset oi in [0, n_orig) (block li / ORIG of this launch is block
+        // (li / ORIG) * blk_stride + blk_off of the range); slots past the range hold no origin (and stay zero)
+        const int64_t sl = li % ORIG;  // slot r*T + t inside the block
+        int64_t off = sl;
+        if (a.warp_major) {
+            constexpr int TT = G::T, RR = G::R;
+            const int64_t r = sl / TT, tt = sl % TT;
+            off = (tt >> 5) * (32 * RR) + r * 32 + (tt & 31);
+        }
+        const int64_t oi = ((li / ORIG) * a.blk_stride + a.blk_off) * ORIG + off;
+        const bool valid = i < total && oi < n_orig;
+        uint64_t red = 0;
+        if (valid) {
+            const int32_t* acc = a.accum + item * (int64_t)NB * ns + li;
+            constexpr int CH = QPT < 8 ? QPT : 8;
+            if constexpr (!SPLIT) {
+                uint32_t mm = 0;
+#pragma unroll 1
+                for (int q0 = part * QPT; q0 < (part + 1) * QPT; q0 += CH) {
+                    int32_t v[CH];
+#pragma unroll
+                    for (int j = 0; j < CH; ++j) v[j] = __ldcs(acc + (int64_t)(q0 + j) * ns);
+#pragma unroll
+                    for (int j = 0; j < CH; ++j) {
+                        const uint32_t av = (uint32_t)(v[j] < 0 ? -v[j] : v[j]);
+                        mm = av > mm ? av : mm;
+                    }
+                }
+                red = mm;
+            } else {
+#pragma unroll 1
+                for (int q0 = part * QPT; q0 < (part + 1) * QPT; q0 += CH) {
+                    int32_t vp[CH], vq[CH];
+#pragma unroll
+                    for (int j = 0; j < CH; ++j)
+                        vp[j] = __ldcs(acc + (int64_t)(q0 + j) * ns), vq[j] = __ldcs(acc + (int64_t)(NQ + q0 + j) * ns);
+#pragma unroll
+                    for (int j = 0; j < CH; ++j) {
+                        const int64_t cP = vp[j], cQ = vq[j];
+                        if (a.hist) {
+                            if (priv && cQ < HS) atomicAdd(&sh_hist[cQ], 1u);
+                            else hist_add_aggregated(a.hist, item * a.hist_stride + cQ);
+                        }
+                        const int64_t df = cP * a.aQ - cQ * a.bP;
+                        const uint64_t av = (uint64_t)(df < 0 ? -df : df);
+                        red = av > red ? av : red;
+                    }
+                }
+            }
+        }
+        if constexpr (TPS > 1) {  // max over the TPS parts of each slot
+            sh_red[part][grp * 32 + lane] = red;
+            __syncthreads();
+            if (part == 0)
+                for (int p = 1; p < TPS; ++p) red = sh_red[p][grp * 32 + lane] > red ? sh_red[p][grp * 32 + lane] : red;
+            __syncthreads();
+        }
+        if (!valid || part != 0) continue;
+        const uint64_t m = red * a.gg;
+        if (B == 1) {
+            const int64_t pooled = a.perm ? a.perm[a.o_begin + oi] : a.o_begin + oi;
+            if (a.per_origin) a.per_origin[a.perm ? pooled : oi] = m;
+            best = m > best ? m : best;
+            if (a.best_key) {
+                const unsigned long long k = ((unsigned long long)red << 31) | (unsigned long long)(0x7fffffff - pooled);
+                bkey = k > bkey ? k : bkey;
+            }
+        } else {
+            atomicMax(reinterpret_cast<unsigned long long*>(&a.item_num[item]), (unsigned long long)m);
+        }
+    }
+    if (B == 1) {
+        best = warp_max_u64(best);
+        bkey = warp_max_u64(bkey);
+        if (lane == 0) {
+            atomicMax(reinterpret_cast<unsigned long long*>(&a.item_num[0]), (unsigned long long)best);
+            if (a.best_key) atomicMax(a.best_key, bkey);
+        }
+    }
+    if constexpr (SPLIT) {
+        if (priv) {
+            __syncthreads();
+            for (int i = threadIdx.x; i < HS; i += blockDim.x)
+                if (sh_hist[i]) atomicAdd(&a.hist[i], (unsigned long long)sh_hist[i]);
         }
     }
 }

@@ -22,10 +22,10 @@ struct CountPlan {
     int32_t blk_stride = 1, blk_off = 0;  // this launch takes origin blocks blk_off, blk_off + blk_stride, ...
 };
 
-template <int D, bool SPLIT, bool GT, int KX = 0, bool WX = false>
+template <int D, bool SPLIT, bool GT, int KX = 0, bool WX = false, bool SMALL = false>
 ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a, cudaStream_t st) {
-    using G = ddks::Geo<D, SPLIT>;
-    auto kern = ddks::k_count<D, SPLIT, GT, KX, WX>;
+    using G = ddks::Geo<D, SPLIT, SMALL>;
+    auto kern = ddks::k_count<D, SPLIT, GT, KX, WX, SMALL>;
     // function attributes are per device: remember which devices this instantiation was configured on (atomics:
     // contexts on different host threads may launch the same instantiation; setting the attribute twice is harmless)
     static std::atomic<bool> attr_done[kMaxDevices] = {};
@@ -65,6 +65,8 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
     if (WX && min_segs > 1) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "warp-level x0 count needs one point segment");
     if (!WX && !(ctx->flags & DDKS_FLAG_FORCE_DIRECT)) {
         constexpr double FLUSH_COST = 2.0, SETUP_COST = 2.0 * G::TILE;  // calibrated on C3 (segs 2..16 sweep)
+        // segments need the partials' memset and the k_finalize launch (~5 us): worth ~4 tiles of one CTA's work
+        constexpr double FIN_COST = 4.0 * G::TILE;
         double best = 1e300;
         const int max_segs = (int)std::min<int64_t>(n_tiles, std::max<int64_t>(min_segs, (16 * slots + base_ctas - 1) / base_ctas));
         for (int sg = min_segs; sg <= max_segs; ++sg) {
@@ -74,7 +76,7 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
             const int64_t ctas = base_ctas * sg;
             const int64_t waves = (ctas + slots - 1) / slots;
             const double cta = (double)tps * G::TILE + SETUP_COST + (sg > 1 ? FLUSH_COST * G::NB : 0.0);
-            const double cost = (double)waves * cta;
+            const double cost = (double)waves * cta + (sg > 1 ? FIN_COST : 0.0);
             if (cost < best * (1.0 - 1e-9)) { best = cost; segs = sg; }
         }
         if (const char* e = getenv("DDKS_SEGS")) segs = std::max(min_segs, std::min(n_tiles, atoi(e)));  // tuning override
@@ -83,19 +85,16 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
     segs = (n_tiles + tiles_per_seg - 1) / tiles_per_seg;
     a.seg_points = tiles_per_seg * G::TILE;
     if (segs > 0x7fffffff / 2) return fail(ctx, DDKS_ERR_TOO_LARGE, "too many point segments");
-    a.n_blk = blocks_o;
     if (segs > 1) {
-        // int32 partials and per-block arrival counters: zeroed when (re)allocated, and every launch leaves them zero
-        // (the last CTA of each origin block finalises and clears its slots), so no memset per call
+        // int32 partials, zeroed per launch (measured: re-zeroing them in k_finalize instead cost C3 +160 us: the
+        // finaliser's zero stores serialise its loads; one memset kernel is ~10 us)
         const size_t acc_bytes = (size_t)pl.B * G::NB * (size_t)a.acc_stride * 4;
-        ddks_status s = ensure_zeroed(ctx, ctx->accum, acc_bytes, st);
+        ddks_status s = ensure(ctx, ctx->accum, acc_bytes);
         if (s) return s;
-        if ((s = ensure_zeroed(ctx, ctx->blk_done, (size_t)pl.B * blocks_o * 4, st))) return s;
+        CU(cudaMemsetAsync(ctx->accum.p, 0, acc_bytes, st));
         a.accum = (int32_t*)ctx->accum.p;
-        a.blk_done = (uint32_t*)ctx->blk_done.p;
     } else {
         a.accum = nullptr;
-        a.blk_done = nullptr;
     }
     if (pl.B > 65535) return fail(ctx, DDKS_ERR_TOO_LARGE, "grid too large");
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
@@ -130,6 +129,16 @@ ddks_status launch_count_t(ddks_ctx* ctx, const CountPlan& pl, ddks::CountArgs a
         const bool last_own = (blocks_all - 1 - pl.blk_off) % pl.blk_stride == 0;
         const uint64_t own = (uint64_t)blocks_o * G::ORIGINS - (last_own ? (uint64_t)blocks_all * G::ORIGINS - n_orig : 0);
         ctx->ev_pairs.push_back((uint64_t)pl.B * own * (uint64_t)pl.N);
+    }
+    if (segs > 1) {
+        const int64_t total = pl.B * a.acc_stride;
+        const int threads = 256;
+        constexpr int NQ = 1 << D, TPS = NQ >= 256 ? 8 : (NQ >= 128 ? 4 : (NQ >= 64 ? 2 : 1));
+        const int64_t per_cta = threads / TPS;  // slots per CTA iteration (k_finalize)
+        const int blocks = (int)std::min<int64_t>((total + per_cta - 1) / per_cta, 148 * 16);
+        ddks::k_finalize<D, SPLIT, SMALL><<<blocks, threads, 0, st>>>(a, pl.B);
+        CHECK_LAUNCH();
+        ctx->launches++;
     }
     return DDKS_OK;
 }

@@ -529,8 +529,8 @@ def test_stored_c5_oracle_matches_inputs_and_oracle_source():
 
 def test_stored_c5_vdks_oracle_matches_inputs_and_oracle_source(golden_dir):
     # tests/golden/c5_vdks16_oracle.json (make_c5_vdks_oracle.py, oracle only) belongs to these input bytes and this
-    # oracle source; vdKS is an approximation of the exact statistic (R16), so it sits below the whole-C5
-    # exact num of c5_oracle.json and above the survey's per-origin spots' cell-level counterpart is not implied
+    # oracle source; its own value is pinned by the vdKS pins above (vdKS(k) == exact ddKS of the cell points, affine
+    # invariance, brute force), which test the same oracle function at small sizes
     import hashlib
     g = json.load(open(os.path.join(golden_dir, "c5_vdks16_oracle.json")))
     assert g["input_sha256"] == I.SURVEY_SHA256["C5"] and g["k"] == 16

@@ -1,7 +1,7 @@
 """GPU parity of the round-2 execution paths (through the C-ABI, against the oracle):
 
-* the fused epilogue of the count kernel -- the last CTA of each origin block finalises from the int32 partials and
-  leaves them zeroed (no memset, no finaliser launch) -- across many consecutive segmented calls of changing shape;
+* the accumulate mode's partials: zeroed once at allocation, and k_finalize re-zeroes what it reads (no memset per
+  call) -- across many consecutive segmented calls of changing shape on one context;
 * the fused packed-key argmax ((num / g) << 31 | (2^31 - 1 - origin), R7) against the per-origin +
   k_argmax path (DDKS_NO_KEY, test only) on position-ordered, kd-ordered, sharded and significance counts;
 * origin blocks chunked over several launches on grid.y (DDKS_GRIDY lowers the 65535 chunk, test only);
@@ -33,7 +33,7 @@ def want_of(P, Q, ties_gt=False):
 
 def test_partials_left_clean_across_calls():
     # segmented counts (several point segments per origin block) of changing shapes on ONE context: every call must
-    # find the int32 partials and arrival counters zero, i.e. every launch's last CTAs cleared them
+    # find the int32 partials zero, i.e. every k_finalize cleared what the previous call accumulated
     cases = [(9000, 7000, 3, "normal"), (3000, 5000, 8, "grid"), (9000, 7000, 3, "mixed"), (12000, 12000, 5, "dup"),
              (700, 900, 2, "grid"), (9000, 7000, 3, "normal"), (4000, 4100, 6, "mixed")]
     with K.Context(flags=K.DDKS_FLAG_NO_X0) as c:
@@ -136,3 +136,44 @@ def test_executed_compares_counter():
         ms, n, pairs = c.profile_read()
         ex = c.profile_work()
         assert 3 * pairs < ex < 4 * pairs  # warp-level bit 0 decisions
+
+
+SMALL_CASES = [(1, 1, 1, "normal"), (200, 200, 3, "normal"), (37, 41, 2, "grid"), (300, 5, 5, "mixed"),
+               (4096, 4096, 3, "grid"), (4000, 4192, 8, "mixed"), (2, 8190, 4, "dup"), (129, 127, 6, "grid"),
+               (3000, 1000, 7, "normal"), (1023, 1025, 1, "grid")]
+
+
+@pytest.mark.parametrize("n_P,n_Q,d,kind", SMALL_CASES)
+def test_small_fused_path(monkeypatch, n_P, n_Q, d, kind):
+    # the one-launch small-N statistic (raw input, cluster of point segments, DSMEM counter reduction, per-block
+    # records reduced on the host) against the oracle and against the packed multi-launch path
+    P, Q = I.random_pair(34000 + n_P + d, n_P, n_Q, d, kind)
+    want = want_of(P, Q)
+    with K.Context() as c:
+        for _ in range(3):  # uncaptured, captured, replayed
+            got = c.stat(dev(P), dev(Q))
+            assert (got.num, got.den, got.argmax_origin) == want, got
+        assert c.stat(P, Q) == got  # host inputs (H2D inside the call)
+        monkeypatch.setenv("DDKS_NO_SMALL", "1")
+        assert c.stat(dev(P), dev(Q)) == got
+        monkeypatch.delenv("DDKS_NO_SMALL")
+    with K.Context(flags=K.DDKS_FLAG_TIES_GT) as c:
+        got = c.stat(dev(P), dev(Q))
+        assert (got.num, got.den, got.argmax_origin) == want_of(P, Q, ties_gt=True)
+
+
+def test_small_fused_path_nonfinite_and_window():
+    P, Q = I.random_pair(34100, 500, 600, 3, "normal")
+    with K.Context() as c:
+        for bad in (np.nan, np.inf, -np.inf):
+            Qb = Q.copy()
+            Qb[599, 2] = bad  # the last row of the last segment
+            with pytest.raises(K.DDKSError) as e:
+                c.stat(dev(P), dev(Qb))
+            assert e.value.status == 4
+        assert (lambda r: (r.num, r.den, r.argmax_origin))(c.stat(dev(P), dev(Q))) == want_of(P, Q)
+    # n_P, n_Q coprime and unbalanced: N * max(a, b) > 32767, so the fused path is skipped (counter window)
+    P, Q = I.random_pair(34101, 97, 1201, 2, "grid")
+    with K.Context() as c:
+        r = c.stat(dev(P), dev(Q))
+    assert (r.num, r.den, r.argmax_origin) == want_of(P, Q)
