@@ -608,7 +608,7 @@ ddks_status ddks_destroy(ddks_ctx* ctx) {
             cudaEventDestroy(ctx->ev_pending[i].second);
         }
     for (DevBuf* b : {&ctx->raw_a, &ctx->raw_b, &ctx->raw_perm, &ctx->packed, &ctx->packed2, &ctx->pool_packed, &ctx->per_origin,
-                      &ctx->accum, &ctx->gather, &ctx->small_out, &ctx->item_num, &ctx->bitmap, &ctx->labels, &ctx->res, &ctx->sig_hist,
+                      &ctx->accum, &ctx->gather, &ctx->item_num, &ctx->bitmap, &ctx->labels, &ctx->res, &ctx->sig_hist,
                       &ctx->sig_lf, &ctx->sig_scratch, &ctx->sig_table, &ctx->sig_contrib, &ctx->sig_part,
                       &ctx->vox_keys, &ctx->vox_cnt, &ctx->vox_S, &ctx->rd_keys, &ctx->rd_xn, &ctx->rd_k0,
                       &ctx->rd_k1, &ctx->rd_hist, &ctx->rd_tcnt, &ctx->rd_cnum, &ctx->x0_keys0,
@@ -673,7 +673,8 @@ ddks_status ddks_profile_work(ddks_ctx* ctx, uint64_t* compares) {
 // int16 halves hold the whole point set (N * max(a, b) <= 32767, so the DSMEM word adds are exact).
 constexpr int64_t kSmallFusedN = 8192;
 static bool small_fused_applies(ddks_ctx* ctx, int64_t n_P, int64_t n_Q) {
-    if (ctx->comm || getenv("DDKS_NO_SMALL")) return false;  // DDKS_NO_SMALL: TEST ONLY
+    // DDKS_NO_SMALL and the FORCE_X0 / FORCE_DIRECT test flags keep the packed path reachable at small N
+    if (ctx->comm || getenv("DDKS_NO_SMALL") || (ctx->flags & (DDKS_FLAG_FORCE_X0 | DDKS_FLAG_FORCE_DIRECT))) return false;
     const int64_t N = n_P + n_Q;
     if (N > kSmallFusedN || !diff_counters_ok(n_P, n_Q)) return false;
     const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
@@ -707,8 +708,8 @@ static ddks_status launch_small_d(ddks_ctx* ctx, const ddks::SmallArgs& a, int s
     return DDKS_OK;
 }
 
-// Enqueue the fused small-N statistic: one cluster launch writing per-origin-block records into ctx->small_out, then
-// their D2H into host_pinned (reduced by stat_impl after the sync). No result initialisation is needed.
+// Enqueue the fused small-N statistic: one cluster launch whose leaders write per-origin-block records into the pinned
+// host buffer (reduced by stat_impl after the sync). No result initialisation, no copy: the call is one graph node.
 static ddks_status small_enqueue(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
                                  cudaStream_t st) {
     ddks_status s;
@@ -717,22 +718,25 @@ static ddks_status small_enqueue(ddks_ctx* ctx, const float* P, int64_t n_P, con
     if ((s = stage_input(ctx, P, (size_t)n_P * d * 4, ctx->raw_a, st, &dP))) return s;
     if ((s = stage_input(ctx, Q, (size_t)n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
     const int64_t blocks = small_blocks(N);
-    if ((s = ensure(ctx, ctx->small_out, (size_t)blocks * 32))) return s;
-    const int64_t n_tiles = (N + ddks::SM_TILE - 1) / ddks::SM_TILE;
-    const int64_t tps = (n_tiles + ddks::SM_MAX_CLUSTER - 1) / ddks::SM_MAX_CLUSTER;
-    const int segs = (int)((n_tiles + tps - 1) / tps);
+    // the points split over a full cluster (8 CTAs, segments of whole warps' worth of rows): at N = 400 every CTA
+    // counts 64 points for its 256 origins, latency rather than issue being the limit at this size
+    const int64_t seg_points = std::max<int64_t>(32, (N + 8 * ddks::SM_MAX_CLUSTER - 1) / (8 * ddks::SM_MAX_CLUSTER) * 8);
+    const int segs = (int)((N + seg_points - 1) / seg_points);
     const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
     ddks::SmallArgs a{};
     a.P = (const float*)dP;
     a.Q = (const float*)dQ;
     a.n_P = (int32_t)n_P;
     a.N = (int32_t)N;
-    a.seg_points = (int32_t)(tps * ddks::SM_TILE);
+    a.seg_points = (int32_t)seg_points;
     a.incP = (uint32_t)((uint64_t)n_Q / g);
     a.incQ = 0u - (uint32_t)((uint64_t)n_P / g);
     a.gg = g;
     a.validate = (ctx->flags & DDKS_FLAG_NO_VALIDATE) ? 0 : 1;
-    a.out = (unsigned long long*)ctx->small_out.p;
+    // the leaders write their records straight into the context's pinned host buffer (zero-copy: no D2H node)
+    void* hdev = nullptr;
+    CU(cudaHostGetDevicePointer(&hdev, ctx->host_pinned, 0));
+    a.out = (unsigned long long*)hdev;
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
     if (ctx->flags & DDKS_FLAG_PROFILE) {
         if (!ctx->ev_free.empty()) {
@@ -760,7 +764,6 @@ static ddks_status small_enqueue(ddks_ctx* ctx, const float* P, int64_t n_P, con
         ctx->ev_recycle.push_back(1);
         ctx->ev_pairs.push_back((uint64_t)N * (uint64_t)N);
     }
-    CU(cudaMemcpyAsync(ctx->host_pinned, ctx->small_out.p, (size_t)blocks * 32, cudaMemcpyDeviceToHost, st));
     return DDKS_OK;
 }
 

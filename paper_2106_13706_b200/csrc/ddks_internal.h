@@ -35,8 +35,7 @@ struct ddks_ctx {
     uint32_t flags = 0;
     ncclComm_t comm = nullptr;
     DevBuf raw_a, raw_b, raw_perm, packed, packed2, pool_packed, per_origin, accum, item_num, bitmap, labels, res;
-    DevBuf gather;     // world > 1: all-gather send + receive buffers
-    DevBuf small_out;  // fused small-N path: one 32-byte record per origin block
+    DevBuf gather;  // world > 1: all-gather send + receive buffers
     DevBuf sig_hist, sig_lf, sig_scratch, sig_table, sig_contrib, sig_part;  // ddks_significance workspace
     DevBuf vox_keys, vox_cnt, vox_S;                                           // ddks_vdks workspace
     DevBuf rd_keys, rd_xn, rd_k0, rd_k1, rd_hist, rd_tcnt, rd_cnum;              // ddks_rdks workspace

@@ -10,9 +10,9 @@
 //     (red.shared::cluster via a mapped pointer), so no global partials, no memset and no finaliser launch.
 //     Word-wise adds of the packed int16 halves are exact because the whole point set fits one int16 window
 //     (the host checks N * max(a, b) <= 32767: every partial and the total stay inside int16);
-//   * the leader writes one 32-byte record per origin block {num, packed argmax key, flags} with plain stores; the
-//     host reduces the records (ddks_combine_records semantics) after the D2H -- no result initialisation, no
-//     atomics, so the whole call is one kernel node plus one copy.
+//   * the leader writes one 32-byte record per origin block {num, packed argmax key, flags} with plain stores straight
+//     into the context's pinned host buffer (zero-copy); the host reduces the records (ddks_combine_records
+//     semantics) after the stream sync -- no result initialisation, no atomics, no copy: the call is ONE graph node.
 // The counting itself is k_count's: FSET.BF + FFMA build the float-encoded SMEM counter address, one red.shared per
 // pair, thread-private counters (two origins per thread, 16-bit halves).
 #pragma once
@@ -38,11 +38,12 @@ struct SmallArgs {
     const float* P;           // [n_P][d] row-major (caller's buffer)
     const float* Q;           // [n_Q][d]
     int32_t n_P, N;           // pooled points (P rows, then Q rows)
-    int32_t seg_points;       // points per cluster rank (multiple of SM_TILE)
+    int32_t seg_points;       // points per cluster rank
     uint32_t incP, incQ;      // DIFF increments +aQ, -bP (two's complement)
     uint64_t gg;              // gcd(n_P, n_Q): num(o) = gg * |counter|
     int validate;
     unsigned long long* out;  // [blocks][4]: {num, key, flags, 0} per origin block, written by the cluster leader
+                              // (device view of pinned host memory)
     unsigned long long* clk;  // profiling (or nullptr): [2] += executed compares
 };
 

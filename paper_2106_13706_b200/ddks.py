@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import warnings
 from typing import NamedTuple
 
 import numpy as np
@@ -129,6 +130,12 @@ def _check(st: int, ctx=None):
         raise DDKSError(st, (LIB.ddks_last_error(ctx) or b"").decode())
 
 
+try:  # torch is optional for the binding (NumPy inputs work without it); looked up once, not per call
+    import torch as _torch
+except ImportError:  # pragma: no cover
+    _torch = None
+
+
 def _torch_stream(stream):
     """The torch stream a call's conversions must run on: the caller's `stream` (a torch.cuda.Stream or a raw
     cudaStream_t handle), else torch's current stream."""
@@ -147,30 +154,32 @@ class _Arg:
     the cast can merge distinct values into ties, which can change D relative to the float64 definition."""
 
     def __init__(self, x, dtype, stream=None):
-        import warnings
         self.keep = None
-        try:
-            import torch
-            if isinstance(x, torch.Tensor):
-                tdt = torch.float32 if dtype == np.float32 else torch.int32
-                if x.dtype == torch.float64 and tdt == torch.float32:
-                    warnings.warn("float64 input cast to float32 (ddks computes on float32 coordinates)", stacklevel=3)
-                if x.dtype != tdt or not x.is_contiguous():
-                    if x.is_cuda:
-                        st = _torch_stream(stream)
-                        st.wait_stream(torch.cuda.current_stream(x.device))  # x is ready on the current stream
-                        with torch.cuda.stream(st):
-                            x = x.to(tdt).contiguous()
-                        x.record_stream(st)
-                    else:
-                        x = x.to(tdt).contiguous()
+        torch = _torch
+        if torch is not None and isinstance(x, torch.Tensor):
+            if dtype == np.float32 and x.dtype is torch.float32 and x.is_contiguous():  # the common case: as is
                 self.keep = x
                 self.ptr = x.data_ptr()
                 self.shape = tuple(x.shape)
                 self.is_cuda = x.is_cuda
                 return
-        except ImportError:
-            pass
+            tdt = torch.float32 if dtype == np.float32 else torch.int32
+            if x.dtype == torch.float64 and tdt == torch.float32:
+                warnings.warn("float64 input cast to float32 (ddks computes on float32 coordinates)", stacklevel=3)
+            if x.dtype != tdt or not x.is_contiguous():
+                if x.is_cuda:
+                    st = _torch_stream(stream)
+                    st.wait_stream(torch.cuda.current_stream(x.device))  # x is ready on the current stream
+                    with torch.cuda.stream(st):
+                        x = x.to(tdt).contiguous()
+                    x.record_stream(st)
+                else:
+                    x = x.to(tdt).contiguous()
+            self.keep = x
+            self.ptr = x.data_ptr()
+            self.shape = tuple(x.shape)
+            self.is_cuda = x.is_cuda
+            return
         a = np.asarray(x)
         if a.dtype == np.float64 and dtype == np.float32:
             warnings.warn("float64 input cast to float32 (ddks computes on float32 coordinates)", stacklevel=3)
@@ -196,21 +205,14 @@ def _batch(P, Q, stream):
 
 
 def _stream(stream):
+    torch = _torch
     if stream is not None:
-        try:
-            import torch
-            if isinstance(stream, torch.cuda.Stream):
-                return ctypes.c_void_p(stream.cuda_stream)
-        except ImportError:
-            pass
-        return ctypes.c_void_p(int(stream))
-    try:
-        import torch
-        if torch.cuda.is_available():
-            return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    except ImportError:
-        pass
-    return ctypes.c_void_p(0)
+        if torch is not None and isinstance(stream, torch.cuda.Stream):
+            return stream.cuda_stream
+        return int(stream)
+    if torch is not None and torch.cuda.is_available():
+        return torch._C._cuda_getCurrentRawStream(torch.cuda.current_device())  # torch's current stream, raw
+    return 0
 
 
 # ------------------------------------------------------------------------------------------ C-ABI mirrors
