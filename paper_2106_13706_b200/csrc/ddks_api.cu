@@ -337,12 +337,12 @@ ddks_status launch_pack_batch(ddks_ctx* ctx, const float* P, int64_t n_P, const 
 }
 
 // Label-invariant permutation null (NEXT-2): labels + validation, then one classification per pair for J perms.
-template <int D>
-ddks_status launch_perm_d(ddks_ctx* ctx, const float* pooled_packed, const int32_t* perms, int64_t n_perm,
-                          int64_t n_P, int64_t n_Q, uint64_t* nums, uint32_t* flag, cudaStream_t st) {
-    using G = ddks::PermGeo<D>;
+template <int D, int F>
+ddks_status launch_perm_df(ddks_ctx* ctx, const float* pooled_packed, const int32_t* perms, int64_t n_perm,
+                           int64_t n_P, int64_t n_Q, uint64_t* nums, uint32_t* flag, cudaStream_t st) {
+    using G = ddks::PermGeo<D, F>;
     const bool gt = (ctx->flags & DDKS_FLAG_TIES_GT) != 0;
-    auto kern = gt ? ddks::k_perm_count<D, true> : ddks::k_perm_count<D, false>;
+    auto kern = gt ? ddks::k_perm_count<D, true, F> : ddks::k_perm_count<D, false, F>;
     static std::atomic<bool> attr[kMaxDevices][2] = {};
     if (ctx->device >= kMaxDevices) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device index %d >= %d", ctx->device, kMaxDevices);
     if (!attr[ctx->device][gt].load(std::memory_order_acquire)) {
@@ -353,7 +353,7 @@ ddks_status launch_perm_d(ddks_ctx* ctx, const float* pooled_packed, const int32
     const int64_t chunks = (n_perm + G::J - 1) / G::J;
     const int64_t words = (N + 31) / 32;
     // [chunks][chunk_words] increment words; rows padded to 16 bytes (+16: the last bulk copy rounds up to 16)
-    const int64_t chunk_words = (N * G::JP + 3) & ~int64_t(3);
+    const int64_t chunk_words = (N * G::JW + 3) & ~int64_t(3);
     const size_t lab_bytes = (size_t)chunks * chunk_words * 4 + 16;
     ddks_status s;
     if ((s = ensure(ctx, ctx->labels, lab_bytes))) return s;
@@ -362,8 +362,8 @@ ddks_status launch_perm_d(ddks_ctx* ctx, const float* pooled_packed, const int32
     CU(cudaMemsetAsync(ctx->bitmap.p, 0, (size_t)n_perm * words * 4, st));
     const int64_t tot = n_perm * N;
     const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
-    ddks::k_labels<<<blocks, 256, 0, st>>>(perms, n_perm, N, n_P, G::J, chunk_words, (uint32_t*)ctx->labels.p,
-                                           (uint32_t*)ctx->bitmap.p, flag);
+    ddks::k_labels<<<blocks, 256, 0, st>>>(perms, n_perm, N, n_P, G::J, G::JW, F, chunk_words,
+                                           (uint32_t*)ctx->labels.p, (uint32_t*)ctx->bitmap.p, flag);
     CHECK_LAUNCH();
     ctx->launches++;
     const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
@@ -403,6 +403,14 @@ ddks_status launch_perm_d(ddks_ctx* ctx, const float* pooled_packed, const int32
         ctx->ev_pairs.push_back((uint64_t)chunks * (uint64_t)N * (uint64_t)N);
     }
     return DDKS_OK;
+}
+
+template <int D>
+ddks_status launch_perm_d(ddks_ctx* ctx, const float* pooled_packed, const int32_t* perms, int64_t n_perm,
+                          int64_t n_P, int64_t n_Q, uint64_t* nums, uint32_t* flag, cudaStream_t st) {
+    // 10-bit label counters (three permutations per word) whenever c_P' <= n_P fits them
+    if (n_P <= 1023) return launch_perm_df<D, 10>(ctx, pooled_packed, perms, n_perm, n_P, n_Q, nums, flag, st);
+    return launch_perm_df<D, 16>(ctx, pooled_packed, perms, n_perm, n_P, n_Q, nums, flag, st);
 }
 
 ddks_status launch_perm(ddks_ctx* ctx, int d, const float* pooled_packed, const int32_t* perms, int64_t n_perm,

@@ -1044,33 +1044,40 @@ __global__ void __launch_bounds__(256) k_finalize(const CountArgs a, int64_t B) 
 // SURVEY.md §8f NEXT-2. code(o, x) does not depend on the labels, so one classification of a pair serves J
 // permutations at once: for permutation j only the P'-count is needed, because with T[q] = all points in orthant q,
 //     c_P' a - c_Q' b = (a + b) c_P' - b T[q]          (a = n_Q/g, b = n_P/g, exact integers).
-// Counters are unsigned 16-bit halves, two permutations per 32-bit word (c_P' <= n_P < 2^16, T <= N < 2^16; the
-// host guarantees N <= 65535). The labels arrive pre-spread: for point x and permutation pair i the increment word
-// is [x in P' of perm 2i] | [x in P' of perm 2i+1] << 16, so per pair the kernel does d FSET + d FFMA (address, once)
-// + one ATOMS for T + J/2 ATOMS with the label word as the increment (no predicates, no branches).
-template <int D> struct PermCfg;
-template <> struct PermCfg<1> { static constexpr int J = 16, T = 256; };
-template <> struct PermCfg<2> { static constexpr int J = 16, T = 256; };
-template <> struct PermCfg<3> { static constexpr int J = 16, T = 256; };
-template <> struct PermCfg<4> { static constexpr int J = 8, T = 256; };
-template <> struct PermCfg<5> { static constexpr int J = 16, T = 160; };
-template <> struct PermCfg<6> { static constexpr int J = 8, T = 128; };
-template <> struct PermCfg<7> { static constexpr int J = 4, T = 128; };
-template <> struct PermCfg<8> { static constexpr int J = 2, T = 96; };
+// Counters are unsigned F-bit fields, PPW = 32 / F permutations per 32-bit word: F = 10 (three per word) when
+// c_P' <= n_P <= 1023, else F = 16 (two per word; the host guarantees N <= 65535); T[q] has a word of its own. The
+// labels arrive pre-spread: for point x and label word i the increment word has bit F*m set iff x is in P' of
+// permutation PPW*i + m, so per pair the kernel does d FSET + d FFMA (address, once) + one ATOMS for T + JW ATOMS with
+// the label word as the increment (no predicates, no branches). F = 10 gives 1.5x the permutations per classification
+// and per ATOMS at the same shared memory (the SMEM-instruction queue is what bounds this kernel).
+template <int D> struct PermCfg;  // JW label words per point, T origins (threads) per CTA
+template <> struct PermCfg<1> { static constexpr int JW = 8, T = 256; };
+template <> struct PermCfg<2> { static constexpr int JW = 8, T = 256; };
+template <> struct PermCfg<3> { static constexpr int JW = 8, T = 256; };
+#ifndef DDKS_P4T
+#define DDKS_P4T 128  // C4b: 128 -> 116 us, 64 -> 117 us, 256 -> 138 us (wave tail of 336 CTAs on 296 slots)
+#endif
+template <> struct PermCfg<4> { static constexpr int JW = 4, T = DDKS_P4T; };
+template <> struct PermCfg<5> { static constexpr int JW = 8, T = 160; };
+template <> struct PermCfg<6> { static constexpr int JW = 4, T = 128; };
+template <> struct PermCfg<7> { static constexpr int JW = 2, T = 128; };
+template <> struct PermCfg<8> { static constexpr int JW = 1, T = 96; };
 
-template <int D> struct PermGeo {
-    static constexpr int J = PermCfg<D>::J, T = PermCfg<D>::T, JP = J / 2;
+template <int D, int F> struct PermGeo {
+    static_assert(F == 10 || F == 16, "label field width");
+    static constexpr int PPW = 32 / F, JW = PermCfg<D>::JW, J = JW * PPW, T = PermCfg<D>::T;
+    static constexpr uint32_t MASK = (1u << F) - 1u;
     static constexpr int NQ = 1 << D, DP = padded_dim<D>(), TILE = 256, S = 2;
-    static constexpr int CNT_WORDS = NQ * (JP + 1) * T;   // [q][JP + 1][T]; slot JP holds T[q]
-    static constexpr int STAGE_BYTES = TILE * DP * 4 + TILE * JP * 4;
+    static constexpr int CNT_WORDS = NQ * (JW + 1) * T;   // [q][JW + 1][T]; slot JW holds T[q]
+    static constexpr int STAGE_BYTES = TILE * DP * 4 + TILE * JW * 4;
     static constexpr int SMEM_BYTES = CNT_WORDS * 4 + S * STAGE_BYTES + 64;
     static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 };
 
 struct PermArgs {
     const float* pts;         // pooled packed [N][DP]
-    const uint32_t* labels;   // [n_chunks][chunk_words] spread increment words [N][JP] (see above)
-    int64_t chunk_words;      // N*JP rounded up to 4 (16-byte aligned chunk rows for the bulk copies)
+    const uint32_t* labels;   // [n_chunks][chunk_words] spread increment words [N][JW] (see above)
+    int64_t chunk_words;      // N*JW rounded up to 4 (16-byte aligned chunk rows for the bulk copies)
     int32_t N, n_perm;
     uint32_t a, b;            // DIFF weights
     uint64_t g;
@@ -1079,13 +1086,14 @@ struct PermArgs {
 };
 
 // labels + validation: for row j of perms, check it is a permutation of 0..N-1 (range + no duplicate via bitmap,
-// else *flag |= 2) and, for i < n_P, add the P' bit of permutation j to the increment word of point perms[j][i].
-__global__ void k_labels(const int32_t* __restrict__ perms, int64_t n_perm, int64_t N, int64_t n_P, int J,
-                         int64_t chunk_words, uint32_t* __restrict__ labels, uint32_t* __restrict__ bitmap,
+// else *flag |= 2) and, for i < n_P, set the P' bit of permutation j in the increment word of point perms[j][i]
+// (chunk j / J, word (j % J) / PPW, bit F * ((j % J) % PPW)).
+__global__ void k_labels(const int32_t* __restrict__ perms, int64_t n_perm, int64_t N, int64_t n_P, int J, int JW,
+                         int F, int64_t chunk_words, uint32_t* __restrict__ labels, uint32_t* __restrict__ bitmap,
                          uint32_t* flag) {
     const int64_t words = (N + 31) / 32;
     const int64_t total = n_perm * N;
-    const int JP = J / 2;
+    const int PPW = 32 / F;
     bool bad = false;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = i / N, pos = i - j * N;
@@ -1094,17 +1102,17 @@ __global__ void k_labels(const int32_t* __restrict__ perms, int64_t n_perm, int6
         const uint32_t bit = 1u << (src & 31);
         if (atomicOr(&bitmap[j * words + (src >> 5)], bit) & bit) bad = true;
         if (pos < n_P) {
-            const int64_t jj = j % J;
-            atomicOr(&labels[(j / J) * chunk_words + (int64_t)src * JP + (jj >> 1)], 1u << (16 * (jj & 1)));
+            const int jj = (int)(j % J);
+            atomicOr(&labels[(j / J) * chunk_words + (int64_t)src * JW + jj / PPW], 1u << (F * (jj % PPW)));
         }
     }
     if (bad) atomicOr(flag, 2u);
 }
 
-template <int D, bool GT>
-__global__ void __launch_bounds__(PermGeo<D>::T, 1) k_perm_count(const PermArgs a) {
-    using G = PermGeo<D>;
-    constexpr int J = G::J, JP = G::JP, T = G::T, DP = G::DP, TILE = G::TILE, S = G::S, NQ = G::NQ;
+template <int D, bool GT, int F>
+__global__ void __launch_bounds__(PermGeo<D, F>::T, 1) k_perm_count(const PermArgs a) {
+    using G = PermGeo<D, F>;
+    constexpr int J = G::J, JP = G::JW, T = G::T, DP = G::DP, TILE = G::TILE, S = G::S, NQ = G::NQ;
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t* cnt = reinterpret_cast<uint32_t*>(smem);                                 // [NQ][JP+1][T]
     uint8_t* stages = smem + G::CNT_WORDS * 4;                                          // S x (points, labels)
@@ -1152,30 +1160,44 @@ __global__ void __launch_bounds__(PermGeo<D>::T, 1) k_perm_count(const PermArgs 
         const float* sp = reinterpret_cast<const float*>(stages + s * G::STAGE_BYTES);
         const uint32_t* sl = reinterpret_cast<const uint32_t*>(stages + s * G::STAGE_BYTES + TILE * DP * 4);
         const int n = min(TILE, a.N - it * TILE);
+        // software-pipelined: the point and label words of the next point are loaded before this point's REDs are
+        // issued (program order would otherwise put every LDS behind the previous point's fire-and-forget REDs and
+        // expose the full SMEM latency per point; C4b measured 30 % issue-active that way). Prefetches read at most
+        // one point past n: inside the stage (or the next stage / the barriers), values unused.
+        float xn[D];
+        uint32_t ln[JP];
+        auto load_pt = [&](int p, float (&x)[D], uint32_t (&l)[JP]) {
+            load_point<D>(sp + p * DP, x);
+            const uint32_t* lw = sl + p * JP;
+            if constexpr (JP % 4 == 0) {
+#pragma unroll
+                for (int i = 0; i < JP; i += 4) {
+                    const uint4 w = *reinterpret_cast<const uint4*>(lw + i);
+                    l[i] = w.x, l[i + 1] = w.y, l[i + 2] = w.z, l[i + 3] = w.w;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < JP; ++i) l[i] = lw[i];
+            }
+        };
+        load_pt(0, xn, ln);
 #pragma unroll 4
         for (int p = 0; p < n; ++p) {
             float x[D];
-            load_point<D>(sp + p * DP, x);
+            uint32_t lw[JP];
+#pragma unroll
+            for (int k = 0; k < D; ++k) x[k] = xn[k];
+#pragma unroll
+            for (int i = 0; i < JP; ++i) lw[i] = ln[i];
+            load_pt(p + 1, xn, ln);
             float f = base;
 #pragma unroll
             for (int k = 0; k < D; ++k) f = fmaf(cmp_bit<GT>(x[k], o[k]), (float)(4 * (1 << k) * (JP + 1) * T), f);
             const uint32_t addr = __float_as_uint(f) + ubase;
             DDKS_ASSERT(__float_as_uint(f) - 0x4B000000u + JP * SLOT < (uint32_t)G::CNT_WORDS * 4u);
             red_add_shared(addr + JP * SLOT, 1u);  // T[q]
-            const uint32_t* lw = sl + p * JP;
-            if constexpr (JP % 4 == 0) {
 #pragma unroll
-                for (int i = 0; i < JP; i += 4) {
-                    const uint4 w = *reinterpret_cast<const uint4*>(lw + i);
-                    red_add_shared(addr + (i + 0) * SLOT, w.x);
-                    red_add_shared(addr + (i + 1) * SLOT, w.y);
-                    red_add_shared(addr + (i + 2) * SLOT, w.z);
-                    red_add_shared(addr + (i + 3) * SLOT, w.w);
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < JP; ++i) red_add_shared(addr + i * SLOT, lw[i]);
-            }
+            for (int i = 0; i < JP; ++i) red_add_shared(addr + i * SLOT, lw[i]);
         }
         __syncthreads();
         if (t == 0 && it + S < n_tiles) {
@@ -1192,9 +1214,9 @@ __global__ void __launch_bounds__(PermGeo<D>::T, 1) k_perm_count(const PermArgs 
         uint64_t m = 0;
         if (valid) {
             for (int q = 0; q < NQ; ++q) {
-                const uint32_t w = cnt[(q * (JP + 1) + (j >> 1)) * T + t];
-                const int64_t cP = (j & 1) ? (w >> 16) : (w & 0xffffu);
-                const int64_t Tq = cnt[(q * (JP + 1) + JP) * T + t] & 0xffffu;
+                const uint32_t w = cnt[(q * (JP + 1) + j / G::PPW) * T + t];
+                const int64_t cP = (w >> (F * (j % G::PPW))) & G::MASK;
+                const int64_t Tq = cnt[(q * (JP + 1) + JP) * T + t];
                 const int64_t v = (int64_t)(a.a + a.b) * cP - (int64_t)a.b * Tq;
                 const uint64_t av = (uint64_t)(v < 0 ? -v : v);
                 m = av > m ? av : m;
