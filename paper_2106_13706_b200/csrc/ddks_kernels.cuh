@@ -399,6 +399,37 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
     int p = lo;
     // prefetches read at most two points past hi <= TILE: still inside the SMEM allocation (the next stage or the
     // counters), and the values are never used
+#ifndef DDKS_NO_ONEDIM
+    if constexpr (KX > 0 && UM == 0 && n_cmp<D, KX, UM>() == 1 && R >= 2) {
+        // kd tile with every sorted bit decided and ONE compared dim left (d = 5 at K = 4: x_4): every pair is still
+        // classified by its own compare, and its increment goes to one of two counters of the origin; the compare bit
+        // (FSET.BF, 1.0 / 0.0) is accumulated in a float register (FADD: exact, <= TILE) and the two counters are
+        // updated once per origin and tile part with the exact totals -- per pair 1 FSET + 1 FADD instead of
+        // FSET + FFMA + ATOMS, on the ALU and FMA pipes in balance.
+        constexpr int K1 = KX;  // the compared dim (D == KX + 1)
+        constexpr float W1 = (float)(4 * (1 << K1) * WPB);
+        float sacc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) sacc[r] = 0.0f;
+        float xn = tile[p * DP + K1];
+#pragma unroll 8
+        for (; p < hi; ++p) {
+            const float x = xn;
+            xn = tile[(p + 1) * DP + K1];
+#pragma unroll
+            for (int r = 0; r < R; ++r) sacc[r] += cmp_bit<GT>(x, o[r][K1]);
+        }
+        const uint32_t n = (uint32_t)(hi - lo);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t inc = (r < RP) ? inc_lo : inc_hi;
+            const uint32_t n1 = (uint32_t)sacc[r];
+            if (n1) red_counter(base[r % NB_] + W1, ubase, inc * n1, hbytes);
+            if (n1 != n) red_counter(base[r % NB_], ubase, inc * (n - n1), hbytes);
+        }
+        return;
+    }
+#endif
     if constexpr (R <= 2) {
         float na[D], nb[D];
         load_point<D>(tile + p * DP, na);
