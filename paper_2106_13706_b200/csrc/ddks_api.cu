@@ -20,6 +20,7 @@
 #include "ddks_kernels.cuh"
 #include "ddks_radix.cuh"
 #include "ddks_small.cuh"
+#include "ddks_perm_mma.cuh"
 #include "ddks_internal.h"
 #include "ddks_launch.cuh"
 
@@ -411,6 +412,88 @@ ddks_status launch_perm_d(ddks_ctx* ctx, const float* pooled_packed, const int32
     // 10-bit label counters (three permutations per word) whenever c_P' <= n_P fits them
     if (n_P <= 1023) return launch_perm_df<D, 10>(ctx, pooled_packed, perms, n_perm, n_P, n_Q, nums, flag, st);
     return launch_perm_df<D, 16>(ctx, pooled_packed, perms, n_perm, n_P, n_Q, nums, flag, st);
+}
+
+// Tensor-core null (ddks_perm_mma.cuh): label images + validation, then the one-hot x label contraction per
+// 128 x 256 tile. pooled_packed must hold ceil(N / 64) * 64 rows (the tail zeroed by the caller).
+template <int D>
+ddks_status launch_perm_mma_d(ddks_ctx* ctx, const float* pooled_packed, const int32_t* perms, int64_t n_perm,
+                              int64_t n_P, int64_t n_Q, uint64_t* nums, uint32_t* flag, cudaStream_t st) {
+    using G = ddks::PermMmaGeo<D>;
+    const bool gt = (ctx->flags & DDKS_FLAG_TIES_GT) != 0;
+    auto kern = gt ? ddks::k_perm_mma<D, true> : ddks::k_perm_mma<D, false>;
+    static std::atomic<bool> attr[kMaxDevices][2] = {};
+    if (!attr[ctx->device][gt].load(std::memory_order_acquire)) {
+        CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES));
+        attr[ctx->device][gt].store(true, std::memory_order_release);
+    }
+    const int64_t N = n_P + n_Q;
+    const int64_t kblocks = (N + ddks::PM_KB - 1) / ddks::PM_KB;
+    const int64_t n_tiles = (n_perm + ddks::PM_N - 1) / ddks::PM_N;
+    const size_t bimg_bytes = (size_t)n_tiles * kblocks * ddks::PM_B_BYTES;
+    const int64_t words = (N + 31) / 32;
+    ddks_status s;
+    if ((s = ensure(ctx, ctx->labels, bimg_bytes))) return s;
+    if ((s = ensure(ctx, ctx->bitmap, (size_t)n_perm * words * 4))) return s;
+    CU(cudaMemsetAsync(ctx->labels.p, 0, bimg_bytes, st));
+    CU(cudaMemsetAsync(ctx->bitmap.p, 0, (size_t)n_perm * words * 4, st));
+    const int64_t tot = n_perm * N;
+    ddks::k_labels_mma<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, st>>>(
+        perms, n_perm, N, n_P, (int)kblocks, (uint8_t*)ctx->labels.p, (uint32_t*)ctx->bitmap.p, flag);
+    CHECK_LAUNCH();
+    ctx->launches++;
+    const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
+    ddks::PermMmaArgs pa{};
+    pa.pts = pooled_packed;
+    pa.bimg = (const uint8_t*)ctx->labels.p;
+    pa.N = (int32_t)N;
+    pa.n_perm = (int32_t)n_perm;
+    pa.k_blocks = (int32_t)kblocks;
+    pa.a = (uint32_t)((uint64_t)n_Q / g);
+    pa.b = (uint32_t)((uint64_t)n_P / g);
+    pa.g = g;
+    pa.num = nums;
+    pa.clk = nullptr;
+    std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+    if (ctx->flags & DDKS_FLAG_PROFILE) {
+        if (!ctx->ev_free.empty()) {
+            ev = ctx->ev_free.back();
+            ctx->ev_free.pop_back();
+        } else {
+            CU(cudaEventCreate(&ev.first));
+            CU(cudaEventCreate(&ev.second));
+        }
+        CU(record_event(ev.first, st));
+        if ((s = ensure_prof(ctx))) return s;
+        pa.clk = (unsigned long long*)ctx->prof_clk.p;
+    }
+    const dim3 grid((unsigned)((N + G::OPT - 1) / G::OPT), (unsigned)n_tiles);
+    kern<<<grid, ddks::PM_THREADS, G::SMEM_BYTES, st>>>(pa);
+    CHECK_LAUNCH();
+    ctx->launches++;
+    if (ev.first) {
+        CU(record_event(ev.second, st));
+        ctx->ev_pending.push_back(ev);
+        ctx->ev_recycle.push_back(1);
+        // pair classifications performed: every (origin, point) pair once per tile column group of 256 permutations
+        ctx->ev_pairs.push_back((uint64_t)n_tiles * (uint64_t)N * (uint64_t)N);
+    }
+    return DDKS_OK;
+}
+
+// the tensor-core null applies: d <= 7, the label path's N <= 65535 (exact fp32 sums, u32 column maxima)
+bool perm_mma_applies(ddks_ctx* ctx, int d, int64_t N) {
+    return d <= 7 && N <= 65535 && !getenv("DDKS_NO_MMA") && !(ctx->flags & DDKS_FLAG_PERM_GATHER);
+}
+
+ddks_status launch_perm_mma(ddks_ctx* ctx, int d, const float* pooled_packed, const int32_t* perms, int64_t n_perm,
+                            int64_t n_P, int64_t n_Q, uint64_t* nums, uint32_t* flag, cudaStream_t st) {
+    switch (d) {
+#define PMMA_CASE(D) case D: return launch_perm_mma_d<D>(ctx, pooled_packed, perms, n_perm, n_P, n_Q, nums, flag, st);
+        PMMA_CASE(1) PMMA_CASE(2) PMMA_CASE(3) PMMA_CASE(4) PMMA_CASE(5) PMMA_CASE(6) PMMA_CASE(7)
+#undef PMMA_CASE
+    }
+    return fail(ctx, DDKS_ERR_DIM_UNSUPPORTED, "tensor-core null d=%d", d);
 }
 
 ddks_status launch_perm(ddks_ctx* ctx, int d, const float* pooled_packed, const int32_t* perms, int64_t n_perm,
@@ -1083,9 +1166,11 @@ ddks_status ddks_permutation_null(ddks_ctx* ctx, const float* pooled, int64_t n_
     CU(cudaMemsetAsync(nums, 0, (size_t)total * 8, st));
     DevResult* dres = (DevResult*)ctx->res.p;
     CU(cudaMemsetAsync(dres, 0, sizeof(DevResult), st));
-    // pack the pooled sample once: [N][DP]
-    if ((s = ensure(ctx, ctx->pool_packed, (size_t)N * DP * 4))) return s;
+    // pack the pooled sample once: [N][DP], rows up to a multiple of 64 (the tensor-core null's k-blocks) zeroed
+    const int64_t N_pad = (N + 63) / 64 * 64;
+    if ((s = ensure(ctx, ctx->pool_packed, (size_t)N_pad * DP * 4))) return s;
     float* pooled_packed = (float*)ctx->pool_packed.p;
+    if (N_pad > N) CU(cudaMemsetAsync(pooled_packed + N * DP, 0, (size_t)(N_pad - N) * DP * 4, st));
     if ((s = launch_pack(ctx, (const float*)dpool, n_P, (const float*)dpool + n_P * d, n_Q, d, 1, pooled_packed,
                          &dres->flag, st)))
         return s;
@@ -1095,9 +1180,10 @@ ddks_status ddks_permutation_null(ddks_ctx* ctx, const float* pooled, int64_t n_
     ddks_shard_range(n_perm, ctx->world, ctx->rank, &jb, &je);
     const bool label_path = N <= 65535 && !(ctx->flags & DDKS_FLAG_PERM_GATHER);
     if (label_path) {
+        auto fn = perm_mma_applies(ctx, d, N) ? launch_perm_mma : launch_perm;
         if (je > jb &&
-            (s = launch_perm(ctx, d, pooled_packed, (const int32_t*)dperm + jb * N, je - jb, n_P, n_Q, nums + 1 + jb,
-                             &dres->flag, st)))
+            (s = fn(ctx, d, pooled_packed, (const int32_t*)dperm + jb * N, je - jb, n_P, n_Q, nums + 1 + jb, &dres->flag,
+                    st)))
             return s;
     } else {
         const int64_t chunk_max = std::max<int64_t>(1, (int64_t)((256ull << 20) / ((size_t)N * DP * 4)));

@@ -1,4 +1,5 @@
-"""Summarise an ncu --set full report (raw page) into the metrics DESIGN.md / bench.py cite."""
+"""Summarise an ncu --set full capture into the metrics DESIGN.md / bench.py cite. Accepts a .ncu-rep (exported with
+`ncu -i REP --page raw --csv`) or the raw-page CSV itself (what microbench/r2_profile.sh brings back)."""
 import csv
 import io
 import json
@@ -9,6 +10,7 @@ KEYS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "sm__cycles_elapsed.avg.per_second",
     "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__warps_active.avg.per_cycle_active", "launch__registers_per_thread", "launch__occupancy_limit_shared_mem",
     "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum", "lts__t_sector_hit_rate.pct",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
@@ -23,12 +25,18 @@ KEYS = [
     "smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_dispatch_stall_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_branch_resolving_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_membar_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_sleeping_per_issue_active.ratio",
 ]
 
 
-def summarise(rep):
-    out = subprocess.check_output(["ncu", "-i", rep, "--page", "raw", "--csv"], text=True)
-    rows = list(csv.reader(io.StringIO(out)))
+def summarise(path):
+    if path.endswith(".ncu-rep"):
+        text = subprocess.check_output(["ncu", "-i", path, "--page", "raw", "--csv"], text=True)
+    else:
+        text = open(path).read()
+    lines = [l for l in text.splitlines() if l.startswith('"')]
+    rows = list(csv.reader(io.StringIO("\n".join(lines))))
     hdr, units = rows[0], rows[1]
     res = []
     for vals in rows[2:]:

@@ -29,13 +29,15 @@ if name in ("C5x0", "C5kd"):
 else:
     P, Q = I.config(name)
 dP, dQ = torch.from_numpy(P).cuda(), torch.from_numpy(Q).cuda()
-with K.Context(flags=flags) as c:
-    for _ in range(2):
+with K.Context(flags=flags | K.DDKS_FLAG_PROFILE) as c:
+    for i in range(2):
         if name == "C4":
             r = c.stat_batch(dP, dQ)[0]
         elif len(sys.argv) > 3:
             r = int(c.stat_per_origin(dP, dQ, int(sys.argv[2]), int(sys.argv[3])).max())
         else:
             r = c.stat(dP, dQ)
+        # executed FP32 compares of this call's count kernel(s) (in-kernel counter; ncu's FSET count x 32 must match)
+        print(name, "call", i, "executed_compares", c.profile_work(), "kd_levels", c.kd_levels, flush=True)
     torch.cuda.synchronize()
     print(name, r, "launches", c.launch_count)

@@ -177,3 +177,42 @@ def test_small_fused_path_nonfinite_and_window():
     with K.Context() as c:
         r = c.stat(dev(P), dev(Q))
     assert (r.num, r.den, r.argmax_origin) == want_of(P, Q)
+
+
+MMA_CASES = [(512, 512, 4, 1000, "normal"), (37, 41, 1, 300, "grid"), (200, 150, 2, 257, "mixed"),
+             (500, 333, 3, 256, "grid"), (130, 190, 5, 40, "dup"), (100, 123, 6, 511, "normal"),
+             (70, 60, 7, 9, "grid"), (1, 1, 3, 5, "normal"), (1500, 1200, 4, 64, "mixed"), (3, 61, 2, 700, "grid")]
+
+
+@pytest.mark.parametrize("n_P,n_Q,d,n_perm,kind", MMA_CASES)
+def test_tensor_core_null(monkeypatch, n_P, n_Q, d, n_perm, kind):
+    # the label-invariant null as a tcgen05 contraction (one-hot orthant matrix x label matrix, fp16 -> fp32 TMEM)
+    # against the oracle and against the SMEM-counter kernel (DDKS_NO_MMA); ragged N (not a multiple of 64), ragged
+    # n_perm (not a multiple of 256), empty origin rows of the last tile, ties
+    P, Q = I.random_pair(35000 + n_P + d, n_P, n_Q, d, kind)
+    pooled = np.concatenate([P, Q])
+    N = n_P + n_Q
+    rng = np.random.default_rng(35000 + n_perm)
+    perms = np.stack([rng.permutation(N) for _ in range(n_perm)]).astype(np.int32)
+    o_null, o_obs, _, o_p = O.permutation_null(pooled, n_P, perms)
+    with K.Context() as c:
+        null, obs, p = c.permutation_null(dev(pooled), n_P, dev(perms))
+        monkeypatch.setenv("DDKS_NO_MMA", "1")
+        null2, obs2, p2 = c.permutation_null(dev(pooled), n_P, dev(perms))
+        monkeypatch.delenv("DDKS_NO_MMA")
+    assert np.array_equal(null, o_null) and obs.num == o_obs and p == o_p
+    assert np.array_equal(null2, o_null) and p2 == p
+    with K.Context(flags=K.DDKS_FLAG_TIES_GT) as c:
+        null_gt, _, _ = c.permutation_null(dev(pooled), n_P, dev(perms))
+    assert np.array_equal(null_gt, O.permutation_null(pooled, n_P, perms, ties_gt=True)[0])
+
+
+def test_tensor_core_null_rejects_bad_rows():
+    P, Q = I.random_pair(35100, 100, 90, 3, "normal")
+    pooled = np.concatenate([P, Q])
+    perms = np.stack([np.random.default_rng(i).permutation(190) for i in range(20)]).astype(np.int32)
+    perms[7, 3] = perms[7, 4]  # a duplicate index: not a permutation
+    with K.Context() as c:
+        with pytest.raises(K.DDKSError) as e:
+            c.permutation_null(dev(pooled), 100, dev(perms))
+        assert e.value.status == 1
