@@ -415,7 +415,7 @@ ddks_status launch_perm_d(ddks_ctx* ctx, const float* pooled_packed, const int32
 }
 
 // Tensor-core null (ddks_perm_mma.cuh): label images + validation, then the one-hot x label contraction per
-// 128 x 256 tile. pooled_packed must hold ceil(N / 64) * 64 rows (the tail zeroed by the caller).
+// 128 x 256 tile. pooled_packed must hold ceil(N / PM_KB) * PM_KB rows (the tail zeroed by the caller).
 template <int D>
 ddks_status launch_perm_mma_d(ddks_ctx* ctx, const float* pooled_packed, const int32_t* perms, int64_t n_perm,
                               int64_t n_P, int64_t n_Q, uint64_t* nums, uint32_t* flag, cudaStream_t st) {
@@ -1166,8 +1166,8 @@ ddks_status ddks_permutation_null(ddks_ctx* ctx, const float* pooled, int64_t n_
     CU(cudaMemsetAsync(nums, 0, (size_t)total * 8, st));
     DevResult* dres = (DevResult*)ctx->res.p;
     CU(cudaMemsetAsync(dres, 0, sizeof(DevResult), st));
-    // pack the pooled sample once: [N][DP], rows up to a multiple of 64 (the tensor-core null's k-blocks) zeroed
-    const int64_t N_pad = (N + 63) / 64 * 64;
+    // pack the pooled sample once: [N][DP], rows up to a multiple of the tensor-core null's k-block zeroed
+    const int64_t N_pad = (N + ddks::PM_KB - 1) / ddks::PM_KB * ddks::PM_KB;
     if ((s = ensure(ctx, ctx->pool_packed, (size_t)N_pad * DP * 4))) return s;
     float* pooled_packed = (float*)ctx->pool_packed.p;
     if (N_pad > N) CU(cudaMemsetAsync(pooled_packed + N * DP, 0, (size_t)(N_pad - N) * DP * 4, st));

@@ -8,17 +8,19 @@
 // then C = A L holds every permutation's P'-count c_P'[o][q][j] at once, T[o][q] = sum_x A[(o, q)][x], and
 //     num_j = g * max_{o, q} |(a + b) C[(o, q)][j] - b T[o][q]|          (a = n_Q / g, b = n_P / g)
 // exactly as the SMEM-counter kernel k_perm_count computes it. The contraction is dense (a GEMM of M = 2^d N,
-// K = N, N_gemm = n_perm) and exact: fp16 0/1 operands, fp32 accumulation of at most N <= 65535 < 2^24 ones.
+// K = N, N_gemm = n_perm) and exact: FP8 E4M3 0/1 operands (1.0 = 0x38), fp32 accumulation of at most
+// N <= 65535 < 2^24 ones (tcgen05.mma kind::f8f6f4: half the operand bytes and twice the rate of fp16).
 //
 // One CTA computes a 128 x 256 tile of C (128 (origin, orthant) rows, 256 permutations) over all points:
-//   * warp 4 (one lane) streams the label tile B[j][x] (prepared by k_labels_mma in the UMMA canonical K-major layout,
-//     so a whole tile is one cp.async.bulk) and the k-block's 64 packed points into a 3-stage ring (mbarriers);
-//   * warps 0-3 classify: the 2^d-code of every (origin of the tile, point of the k-block) pair with d FP32 >=
-//     compares (the pair classification of the hot path), then expand each code into its one-hot fp16 row of A
-//     directly in SMEM (thread t owns row t = (origin t / 2^d, orthant t % 2^d) and counts T in a register);
-//   * warp 5 (one lane) issues tcgen05.mma.kind::f16 (M = 128, N = 256, K = 16) x 4 per k-block into a TMEM
+//   * warp 8 (one lane) streams the label tile B[j][x] (prepared by k_labels_mma in the UMMA canonical K-major layout,
+//     so a whole tile is one cp.async.bulk) and the k-block's 128 packed points into a 3-stage ring (mbarriers);
+//   * warps 0-7 classify: the 2^d-code of every (origin of the tile, point of the k-block) pair with d FP32 >=
+//     compares (the pair classification of the hot path), then expand the codes into the one-hot fp8 rows of A
+//     directly in SMEM (byte-SIMD: 4 codes compared with the row's orthant per instruction; two threads per row,
+//     each counting its half of T in a register);
+//   * warp 9 (one lane) issues tcgen05.mma.kind::f8f6f4 (M = 128, N = 256, K = 32) x 4 per k-block into a TMEM
 //     accumulator of 256 columns and commits each stage back to the ring;
-//   * epilogue: warps 0-3 read their 128 TMEM lanes (tcgen05.ld 32x32b.x32), form |(a + b) C - b T| per column,
+//   * epilogue: warps 0-7 read the 128 TMEM lanes (two warps per lane quadrant, half the columns each) (tcgen05.ld 32x32b.x32), form |(a + b) C - b T| per column,
 //     reduce it over the 128 rows (redux.sync max + SMEM atomicMax) and atomicMax g * that into num[j].
 #pragma once
 #include <cstdint>
@@ -28,15 +30,18 @@
 namespace ddks {
 namespace {
 
-constexpr int PM_M = 128, PM_N = 256, PM_KB = 64, PM_S = 3;          // tile rows, permutations, points per k-block
-constexpr int PM_A_BYTES = PM_M * PM_KB * 2, PM_B_BYTES = PM_N * PM_KB * 2;  // 16 KB, 32 KB fp16 tiles
-constexpr int PM_THREADS = 192;                                       // warps 0-3 classify + epilogue, 4 TMA, 5 MMA
+constexpr int PM_M = 128, PM_N = 256, PM_KB = 128, PM_S = 3;         // tile rows, permutations, points per k-block
+constexpr int PM_A_BYTES = PM_M * PM_KB, PM_B_BYTES = PM_N * PM_KB;   // 16 KB, 32 KB fp8 tiles
+constexpr uint8_t PM_ONE = 0x38;                                      // FP8 E4M3 1.0
+constexpr int PM_GEN = 256;                                           // classify + epilogue threads (warps 0-7)
+constexpr int PM_THREADS = PM_GEN + 64;                               // + warp 8 (TMA producer) + warp 9 (MMA issuer)
+constexpr int PM_WTMA = PM_GEN / 32, PM_WMMA = PM_WTMA + 1;
 
-// Byte offset of element (row, k) of a [rows][PM_KB] fp16 tile in the canonical K-major, no-swizzle UMMA layout:
-// core matrices of 8 rows x 8 elements (128 contiguous bytes), the 8 K-chunks of an 8-row group adjacent (LBO = 128 B),
-// 8-row groups 1024 B apart (SBO).
+// Byte offset of element (row, k) of a [rows][PM_KB] fp8 tile in the canonical K-major, no-swizzle UMMA layout:
+// core matrices of 8 rows x 16 elements (128 contiguous bytes), the 8 K-chunks of an 8-row group adjacent
+// (LBO = 128 B), 8-row groups 1024 B apart (SBO).
 __host__ __device__ constexpr uint32_t pm_off(int row, int k) {
-    return (uint32_t)((row >> 3) * 1024 + (k >> 3) * 128 + (row & 7) * 16 + (k & 7) * 2);
+    return (uint32_t)((row >> 3) * 1024 + (k >> 4) * 128 + (row & 7) * 16 + (k & 15));
 }
 
 template <int D> struct PermMmaGeo {
@@ -45,7 +50,7 @@ template <int D> struct PermMmaGeo {
     static constexpr int PTS_BYTES = PM_KB * DP * 4;
     static constexpr int STAGE_BYTES = PM_B_BYTES + PM_A_BYTES + PTS_BYTES;
     static constexpr int CODE_BYTES = OPT * PM_KB;  // one byte per (origin, point) of a k-block
-    static constexpr int SMEM_BYTES = PM_S * STAGE_BYTES + PM_S * CODE_BYTES + OPT * DP * 4 + PM_N * 4 + 128;
+    static constexpr int SMEM_BYTES = PM_S * STAGE_BYTES + PM_S * CODE_BYTES + OPT * DP * 4 + PM_N * 4 + 2 * PM_M * 4 + 128;
     static_assert(D >= 1 && D <= 7, "tensor-core null: d <= 7 (128-row tiles of whole origins)");
     static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 };
@@ -60,7 +65,7 @@ struct PermMmaArgs {
     unsigned long long* clk; // profiling (or nullptr): [2] += FP32 compares executed
 };
 
-// ---------------------------------------------------------------------------------------------- PTX wrappers
+// ---------------------------------------------------------------------------------------------- PTX wrappers (tcgen05: alloc / mma / commit / ld)
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -73,14 +78,15 @@ __device__ __forceinline__ uint64_t pm_desc(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
            ((uint64_t)1 << 46);
 }
-// instruction descriptor, kind::f16: D f32 (bits 4-5 = 1), A = B = f16 (0), both K-major, N >> 3 at [17,23), M >> 4 at [24,29)
+// instruction descriptor, kind::f8f6f4: D f32 (bits 4-5 = 1), A = B = E4M3 (0), both K-major, N >> 3 at [17,23),
+// M >> 4 at [24,29)
 constexpr uint32_t PM_IDESC = (1u << 4) | ((uint32_t)(PM_N >> 3) << 17) | ((uint32_t)(PM_M >> 4) << 24);
 
 __device__ __forceinline__ void pm_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(PM_IDESC), "r"(accumulate)
         : "memory");
 }
@@ -101,8 +107,8 @@ __device__ __forceinline__ void pm_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 }
 
 // ---------------------------------------------------------------------------------------------- label images
-// B[j][x] = 1.0h iff point x is in P' of permutation j (perms[j][0 .. n_P)), in the canonical layout of the tile
-// (n_tile = j / 256, k_block = x / 64); the buffer is zeroed first. Validates every perms row as in k_labels.
+// B[j][x] = 1.0 (E4M3) iff point x is in P' of permutation j (perms[j][0 .. n_P)), in the canonical layout of the tile
+// (n_tile = j / 256, k_block = x / 128); the buffer is zeroed first. Validates every perms row as in k_labels.
 __global__ void k_labels_mma(const int32_t* __restrict__ perms, int64_t n_perm, int64_t N, int64_t n_P, int k_blocks,
                              uint8_t* __restrict__ bimg, uint32_t* __restrict__ bitmap, uint32_t* flag) {
     const int64_t words = (N + 31) / 32;
@@ -116,8 +122,7 @@ __global__ void k_labels_mma(const int32_t* __restrict__ perms, int64_t n_perm, 
         if (atomicOr(&bitmap[j * words + (src >> 5)], bit) & bit) bad = true;
         if (pos < n_P) {
             const int64_t tile = (j / PM_N) * k_blocks + src / PM_KB;
-            *reinterpret_cast<uint16_t*>(bimg + tile * PM_B_BYTES + pm_off((int)(j % PM_N), (int)(src % PM_KB))) =
-                (uint16_t)0x3C00u;  // fp16 1.0
+            bimg[tile * PM_B_BYTES + pm_off((int)(j % PM_N), (int)(src % PM_KB))] = PM_ONE;
         }
     }
     if (bad) atomicOr(flag, 2u);
@@ -133,7 +138,8 @@ __global__ void __launch_bounds__(PM_THREADS, 1) k_perm_mma(const PermMmaArgs a)
     uint8_t* codes = smem + PM_S * G::STAGE_BYTES;                                // [S][OPT][PM_KB]
     float* ocoord = reinterpret_cast<float*>(codes + PM_S * G::CODE_BYTES);       // [OPT][DP]
     uint32_t* colmax = reinterpret_cast<uint32_t*>(ocoord + OPT * DP);            // [PM_N]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(colmax + PM_N);                  // full[S], aready[S], empty[S], done
+    uint32_t* tsh = colmax + PM_N;                                                // [2][PM_M] half-row T counts
+    uint64_t* bars = reinterpret_cast<uint64_t*>(tsh + 2 * PM_M);                 // full[S], aready[S], empty[S], done
     uint64_t* full = bars;
     uint64_t* aready = bars + PM_S;
     uint64_t* empty = bars + 2 * PM_S;
@@ -146,11 +152,11 @@ __global__ void __launch_bounds__(PM_THREADS, 1) k_perm_mma(const PermMmaArgs a)
     const int KB = a.k_blocks;
 
     if (t == 0) {
-        for (int s = 0; s < PM_S; ++s) mbar_init(&full[s], 1), mbar_init(&aready[s], 128), mbar_init(&empty[s], 1);
+        for (int s = 0; s < PM_S; ++s) mbar_init(&full[s], 1), mbar_init(&aready[s], PM_GEN), mbar_init(&empty[s], 1);
         mbar_init(done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 5) {  // TMEM: 256 fp32 columns x 128 lanes for the accumulator
+    if (warp == PM_WMMA) {  // TMEM: 256 fp32 columns x 128 lanes for the accumulator
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
                      "n"(PM_N));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -165,7 +171,7 @@ __global__ void __launch_bounds__(PM_THREADS, 1) k_perm_mma(const PermMmaArgs a)
     tc_fence_after();
     const uint32_t tmem = tmem_base;
 
-    if (warp == 4) {
+    if (warp == PM_WTMA) {
         if (lane == 0) {  // producer: label tile + the k-block's points per stage (codes[s] is rewritten only S
                           // k-blocks later, after S - 1 further classify barriers)
             const uint8_t* bsrc = a.bimg + (int64_t)n_tile * KB * PM_B_BYTES;
@@ -179,7 +185,7 @@ __global__ void __launch_bounds__(PM_THREADS, 1) k_perm_mma(const PermMmaArgs a)
             }
         }
         __syncwarp();
-    } else if (warp == 5) {
+    } else if (warp == PM_WMMA) {
         if (lane == 0) {  // MMA issuer
             for (int kb = 0; kb < KB; ++kb) {
                 const int s = kb % PM_S;
@@ -190,7 +196,7 @@ __global__ void __launch_bounds__(PM_THREADS, 1) k_perm_mma(const PermMmaArgs a)
                 const uint32_t bsa = smem_u32(stages + s * G::STAGE_BYTES);
                 const uint32_t asa = bsa + PM_B_BYTES;
 #pragma unroll
-                for (int k = 0; k < PM_KB / 16; ++k)
+                for (int k = 0; k < PM_KB / 32; ++k)  // K = 32 fp8 per MMA: two 16-byte chunks, 256 bytes apart
                     pm_mma(tmem, pm_desc(asa + k * 256), pm_desc(bsa + k * 256), (kb | k) ? 1u : 0u);
                 pm_commit(&empty[s]);  // the stage is free once these MMAs have read it
             }
@@ -198,8 +204,12 @@ __global__ void __launch_bounds__(PM_THREADS, 1) k_perm_mma(const PermMmaArgs a)
         }
         __syncwarp();
     } else {
-        // classify (warps 0-3): codes of every (origin, point) pair of the k-block, then the one-hot A row of thread t
-        const int orow = t / NQ, qrow = t % NQ;
+        // classify (warps 0-7): the code of every (origin, point) pair of the k-block (invalid origins / points get
+        // code 0xFF, which no orthant matches), then thread t writes half h = t / 128 of A row r = t % 128 =
+        // (origin r / 2^d, orthant r % 2^d): four 16-byte chunks of 16 fp8, built 4 codes at a time with byte SIMD
+        const int r = t & (PM_M - 1), h = t >> 7;
+        const int orow = r / NQ, qrow = r % NQ;
+        const uint32_t qrep = (uint32_t)qrow * 0x01010101u;
         uint32_t Tcnt = 0;
         unsigned long long exec_cmp = 0;
         for (int kb = 0; kb < KB; ++kb) {
@@ -208,7 +218,8 @@ __global__ void __launch_bounds__(PM_THREADS, 1) k_perm_mma(const PermMmaArgs a)
             uint8_t* st = stages + s * G::STAGE_BYTES;
             const float* pts = reinterpret_cast<const float*>(st + PM_B_BYTES + PM_A_BYTES);
             uint8_t* cd = codes + s * G::CODE_BYTES;
-            for (int i = t; i < OPT * PM_KB; i += 128) {
+            const int xvalid = min(PM_KB, a.N - kb * PM_KB);
+            for (int i = t; i < OPT * PM_KB; i += PM_GEN) {
                 const int o = i / PM_KB, x = i % PM_KB;
                 uint32_t c = 0;
 #pragma unroll
@@ -216,47 +227,47 @@ __global__ void __launch_bounds__(PM_THREADS, 1) k_perm_mma(const PermMmaArgs a)
                     const float xv = pts[x * DP + k], ov = ocoord[o * DP + k];
                     c |= (GT ? (xv > ov) : (xv >= ov)) ? (1u << k) : 0u;
                 }
-                cd[i] = (uint8_t)c;
+                cd[i] = (x < xvalid && o0 + o < a.N) ? (uint8_t)c : (uint8_t)0xFF;
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            const int xvalid = min(PM_KB, a.N - kb * PM_KB);  // points past N are zero columns of A
-            const bool rvalid = o0 + orow < a.N;
+            asm volatile("bar.sync 1, %0;" ::"n"(PM_GEN) : "memory");
             uint8_t* A = st + PM_B_BYTES;
-            const uint32_t* crow = reinterpret_cast<const uint32_t*>(cd + orow * PM_KB);
+            const uint4* crow = reinterpret_cast<const uint4*>(cd + orow * PM_KB);
 #pragma unroll
-            for (int kc = 0; kc < PM_KB / 8; ++kc) {
-                uint32_t h[4];
+            for (int c4 = 0; c4 < PM_KB / 32; ++c4) {
+                const int kc = h * (PM_KB / 32) + c4;  // this thread's 16-point chunks
+                const uint4 cw = crow[kc];
+                uint32_t w[4] = {cw.x, cw.y, cw.z, cw.w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int x0 = kc * 8 + 2 * e;
-                    const uint32_t cw = crow[x0 >> 2] >> (8 * (x0 & 3));
-                    const bool m0 = rvalid && x0 < xvalid && (cw & 0xffu) == (uint32_t)qrow;
-                    const bool m1 = rvalid && x0 + 1 < xvalid && ((cw >> 8) & 0xffu) == (uint32_t)qrow;
-                    h[e] = (m0 ? 0x3C00u : 0u) | (m1 ? 0x3C000000u : 0u);
-                    Tcnt += (uint32_t)m0 + (uint32_t)m1;
+                for (int wi = 0; wi < 4; ++wi) {
+                    const uint32_t y = w[wi] ^ qrep;                                        // zero byte <=> code == q
+                    const uint32_t z = ~(((y & 0x7f7f7f7fu) + 0x7f7f7f7fu) | y) & 0x80808080u;  // 0x80 per match
+                    Tcnt += __popc(z);
+                    w[wi] = (z >> 7) * (uint32_t)PM_ONE;                                      // E4M3 1.0 per match
                 }
-                *reinterpret_cast<uint4*>(A + pm_off(t, kc * 8)) = make_uint4(h[0], h[1], h[2], h[3]);
+                *reinterpret_cast<uint4*>(A + pm_off(r, kc * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
             }
-            exec_cmp += (unsigned long long)D * OPT * PM_KB / 128;
+            exec_cmp += (unsigned long long)D * OPT * PM_KB / PM_GEN;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
             mbar_arrive(&aready[s]);
         }
-        if (a.clk && t == 0) atomicAdd(&a.clk[2], exec_cmp * 128ull);
+        if (a.clk && t == 0) atomicAdd(&a.clk[2], exec_cmp * (unsigned long long)PM_GEN);
+        tsh[h * PM_M + r] = Tcnt;
+        asm volatile("bar.sync 1, %0;" ::"n"(PM_GEN) : "memory");
 
-        // epilogue: this thread's row (TMEM lane t) against every permutation column of the tile
+        // epilogue: warp w reads TMEM lanes 32 (w % 4) .. (its 32 rows) for the columns [128 (w / 4), + 128)
         mbar_wait(done, 0);
         tc_fence_after();
-        const bool rvalid = o0 + orow < a.N;
-        const int64_t bT = (int64_t)a.b * Tcnt;
+        const int er = (warp & 3) * 32 + lane;
+        const int64_t bT = (int64_t)a.b * (tsh[er] + tsh[PM_M + er]);
 #pragma unroll 1
-        for (int c0 = 0; c0 < PM_N; c0 += 32) {
+        for (int c0 = (warp >> 2) * (PM_N / 2); c0 < (warp >> 2) * (PM_N / 2) + PM_N / 2; c0 += 32) {
             uint32_t v[32];
-            pm_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+            pm_ld32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0, v);
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
                 const int64_t cP = (int64_t)__uint_as_float(v[j]);  // an exact integer count (< 2^24)
                 const int64_t df = (int64_t)(a.a + a.b) * cP - bT;
-                uint32_t val = rvalid ? (uint32_t)(df < 0 ? -df : df) : 0u;
+                uint32_t val = (uint32_t)(df < 0 ? -df : df);  // invalid rows: C = T = 0
                 val = __reduce_max_sync(0xffffffffu, val);
                 if (lane == 0) atomicMax(&colmax[c0 + j], val);
             }
@@ -264,7 +275,7 @@ __global__ void __launch_bounds__(PM_THREADS, 1) k_perm_mma(const PermMmaArgs a)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 5) {
+    if (warp == PM_WMMA) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(PM_N));
     }
