@@ -41,13 +41,30 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+// The wait carries a suspend-time hint: a waiting warp sleeps until the phase completes (or the hint expires) instead
+// of re-issuing try_wait every ~70 cycles (at C5 the re-issued try_waits of warps ahead of their TMA stage were 13 % of
+// the kd count's executed instructions). Measured neutral to -0.2 % (C5 637.5 -> 636.5 ms; C2, C3 unchanged:
+// microbench/r2_hint_sweep.sh) -- the sleeping warps were not taking issue slots the counting warps needed.
+#ifndef DDKS_MBAR_HINT_NS
+#define DDKS_MBAR_HINT_NS 1000000
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if DDKS_MBAR_HINT_NS == 0
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "DDKS_WAIT_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra DDKS_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
         "r"(parity)
+        : "memory");
+    return;
+#endif
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "DDKS_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra DDKS_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(DDKS_MBAR_HINT_NS)
         : "memory");
 }
 // 1-D bulk copy global -> shared through the TMA engine, completion counted on an mbarrier (bytes % 16 == 0).
