@@ -93,8 +93,15 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     const int64_t A = lcm_i64(G::ORIGINS, G::TILE);
     const int forced = (int)((ctx->flags >> DDKS_FLAG_KD_SHIFT) & 7u);
     // the tie-convention test variant (GT) is instantiated with one level only
+    // mid N (< 80000 rows, one rank): bucket counting sorts (3 launches per level) instead of the exact radix sort
+    // (~17 launches per level, latency-bound below ~10^5 rows). The bucket scatter places equal-bucket rows in
+    // arbitrary (atomic) order, so the order is not reproducible from call to call: counts and results are exact
+    // either way, but origin shards are defined on the order, so sharded runs (world > 1 and the shard rehearsal)
+    // keep the deterministic radix sort. Each level costs ~35 us here, so at most 2 levels (C3: K = 2 1.20 ms vs
+    // K = 3 1.47 ms per call). DDKS_KD_RADIX (test only) forces the radix sort.
+    const bool bucket = N < 80000 && shard_world <= 1 && !getenv("DDKS_KD_RADIX");
     const KdChoice kc = kd_choose(D, std::min(n_P, n_Q), G::ORIGINS, 32 * G::R, G::TILE, A, gt ? 1 : forced,
-                                  gt ? 1 : 5);
+                                  gt ? 1 : (bucket && !forced ? 2 : 5));
     const int K = kc.K;
     const int ib = std::max(1, bits_for((uint64_t)(N - 1)));
     const int tiles_rs = (int)((N + ddks::RS_TILE - 1) / ddks::RS_TILE);
@@ -116,7 +123,39 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 16));
     const float* src_pts = packed;
     const int32_t* src_perm = nullptr;
-    for (int level = 0; level < K; ++level) {
+    if (bucket) {
+        int64_t cells_max = 1;
+        const int64_t gl[4] = {kc.G0, kc.G1, kc.G2, kc.G3};
+        for (int l = 0; l + 1 < K; ++l) cells_max *= gl[l];
+        const int64_t nkeys = 2 * cells_max * ddks::KB_NBK;
+        if ((s = ensure(ctx, ctx->x0_hist, (size_t)std::max<int64_t>(nkeys, (int64_t)tiles_rs * 256) * 4 + 4 * K * 4 + 64)))
+            return s;
+        hist = (uint32_t*)ctx->x0_hist.p;
+        unsigned int* rng = (unsigned int*)(hist + nkeys);
+        uint32_t* keys = (uint32_t*)k0;  // [N] u32 keys in the first key buffer
+        ddks::k_kdb_range_init<<<1, 32, 0, st>>>(rng, 2 * K);  // min keys ~0, max keys 0
+        ddks::k_kdb_range<<<std::min(g, 148 * 2), 256, 0, st>>>(src_pts, DP, N, n_P, K, rng);
+        CHECK_LAUNCH();
+        ctx->launches += 2;
+        int64_t cells = 1;
+        for (int level = 0; level < K; ++level) {
+            const int64_t nk = 2 * cells * ddks::KB_NBK;
+            CU(cudaMemsetAsync(hist, 0, (size_t)nk * 4, st));
+            ddks::k_kdb_hist<<<g, 256, 0, st>>>(src_pts, DP, N, n_P, level, K, kc.G0, kc.G1, kc.G2, A, cells, rng,
+                                                 keys, hist);
+            ddks::k_kdb_scan<<<1, 1024, 0, st>>>(hist, nk);
+            const bool fin = ((K - 1 - level) % 2) == 0;
+            float* dst_pts = (float*)(fin ? ctx->x0_pts.p : ctx->x0_pts2.p);
+            int32_t* dst_perm = (int32_t*)(fin ? ctx->x0_perm.p : ctx->x0_perm2.p);
+            ddks::k_kdb_scatter<<<g, 256, 0, st>>>(src_pts, DP, N, keys, hist, src_perm, dst_pts, dst_perm);
+            CHECK_LAUNCH();
+            ctx->launches += 3;
+            src_pts = dst_pts;
+            src_perm = dst_perm;
+            cells *= gl[level];
+        }
+    }
+    for (int level = 0; level < (bucket ? 0 : K); ++level) {
         const int64_t gl[4] = {kc.G0, kc.G1, kc.G2, kc.G3};
         int64_t cells = 1;
         for (int l = 0; l < level; ++l) cells *= gl[l];

@@ -884,6 +884,130 @@ __global__ void k_kd_keys(const float* __restrict__ pts, int DP, int64_t N, int6
     }
 }
 
+// ---- mid-N kd ordering by bucket counting sorts (N < 80000; DESIGN.md §7 "kd ordering, mid N") -------------------
+// Level l reorders every (label, cell of the previous levels) run by x_l quantised to KB_NBK equal-width buckets of the
+// label's [min, max] of x_l: one histogram, one scan, one scatter instead of the radix sort's ~17 launches per level.
+// Rows of a bucket keep an arbitrary order (atomic slots) -- the order only changes speed, never counts.
+constexpr int KB_NBK = 1024;
+
+__global__ void k_kdb_range_init(unsigned int* rng, int pairs) {
+    for (int i = threadIdx.x; i < pairs; i += blockDim.x) rng[2 * i] = ~0u, rng[2 * i + 1] = 0u;
+}
+
+// rng[(lab * K + k) * 2 + {0, 1}] = order-preserving keys of min / max of x_k over the label's rows (init ~0 / 0)
+__global__ void k_kdb_range(const float* __restrict__ pts, int DP, int64_t N, int64_t n_P, int K,
+                            unsigned int* __restrict__ rng) {
+    for (int k = 0; k < K; ++k) {
+        unsigned int lo[2] = {~0u, ~0u}, hi[2] = {0u, 0u};
+        for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+            const unsigned int v = f32_key(pts[j * DP + k]);
+            const int lab = j >= n_P;
+            lo[lab] = v < lo[lab] ? v : lo[lab];
+            hi[lab] = v > hi[lab] ? v : hi[lab];
+        }
+#pragma unroll
+        for (int lab = 0; lab < 2; ++lab) {
+#pragma unroll
+            for (int sh = 16; sh; sh >>= 1) {
+                lo[lab] = min(lo[lab], __shfl_xor_sync(0xffffffffu, lo[lab], sh));
+                hi[lab] = max(hi[lab], __shfl_xor_sync(0xffffffffu, hi[lab], sh));
+            }
+            if ((threadIdx.x & 31) == 0) {
+                atomicMin(&rng[(lab * K + k) * 2], lo[lab]);
+                atomicMax(&rng[(lab * K + k) * 2 + 1], hi[lab]);
+            }
+        }
+    }
+}
+
+// the (label, cell, bucket) key of row j at level `level` (cells: position cuts of the previous levels, as k_kd_keys)
+__device__ __forceinline__ uint32_t kdb_key(const float* pts, int DP, int64_t j, int64_t N, int64_t n_P, int level,
+                                            int K, int64_t G0, int64_t G1, int64_t G2, int64_t A, int64_t cells,
+                                            const unsigned int* rng) {
+    const bool lab = j >= n_P;
+    const int64_t s = lab ? n_P : 0, e = lab ? N : n_P;
+    int64_t cell = 0;
+    if (level >= 1) {
+        const int64_t i0 = kd_part(j, s, e, G0, A);
+        cell = i0;
+        if (level >= 2) {
+            const int64_t s1 = kd_cut(s, e, G0, i0, A), e1 = kd_cut(s, e, G0, i0 + 1, A);
+            const int64_t i1 = kd_part(j, s1, e1, G1, A);
+            cell = i0 * G1 + i1;
+            if (level >= 3) {
+                const int64_t s2 = kd_cut(s1, e1, G1, i1, A), e2 = kd_cut(s1, e1, G1, i1 + 1, A);
+                cell = cell * G2 + kd_part(j, s2, e2, G2, A);
+            }
+        }
+    }
+    const float lo = key_f32(rng[((int)lab * K + level) * 2]), hi = key_f32(rng[((int)lab * K + level) * 2 + 1]);
+    const float x = pts[j * DP + level];
+    const float scale = hi > lo ? (float)KB_NBK / (hi - lo) : 0.0f;
+    const float v = (x - lo) * scale;
+    const int b = v >= (float)(KB_NBK - 1) ? KB_NBK - 1 : (v > 0.0f ? (int)v : 0);
+    return (uint32_t)((((int64_t)lab * cells + cell) * KB_NBK) + b);
+}
+
+__global__ void k_kdb_hist(const float* __restrict__ pts, int DP, int64_t N, int64_t n_P, int level, int K,
+                           int64_t G0, int64_t G1, int64_t G2, int64_t A, int64_t cells,
+                           const unsigned int* __restrict__ rng, uint32_t* __restrict__ keys,
+                           unsigned int* __restrict__ hist) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t key = kdb_key(pts, DP, j, N, n_P, level, K, G0, G1, G2, A, cells, rng);
+        keys[j] = key;
+        atomicAdd(&hist[key], 1u);
+    }
+}
+
+// exclusive scan of n bucket counts in place, one CTA of 1024 threads (n <= a few 10^5)
+__global__ void __launch_bounds__(1024) k_kdb_scan(unsigned int* __restrict__ hist, int64_t n) {
+    __shared__ unsigned int wsum[32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int64_t per = (n + 1023) / 1024;
+    const int64_t b0 = t * per, b1 = min(n, b0 + per);
+    unsigned int sum = 0;
+    for (int64_t i = b0; i < b1; ++i) sum += hist[i];
+    unsigned int x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        unsigned int v = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        wsum[lane] = v;
+    }
+    __syncthreads();
+    unsigned int run = x - sum + (w ? wsum[w - 1] : 0u);
+    for (int64_t i = b0; i < b1; ++i) {
+        const unsigned int c = hist[i];
+        hist[i] = run;
+        run += c;
+    }
+}
+
+// row j goes to the next free slot of its key: out[pos] = pts[j], perm_out[pos] = perm_in[j] (perm_in null: j)
+__global__ void k_kdb_scatter(const float* __restrict__ pts, int DP, int64_t N, const uint32_t* __restrict__ keys,
+                              unsigned int* __restrict__ offs, const int32_t* __restrict__ perm_in,
+                              float* __restrict__ out, int32_t* __restrict__ perm_out) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t pos = atomicAdd(&offs[keys[j]], 1u);
+        DDKS_ASSERT(pos < N);
+        const float4* src = reinterpret_cast<const float4*>(pts + j * DP);
+        float4* dst = reinterpret_cast<float4*>(out + pos * DP);
+        dst[0] = src[0];
+        if (DP == 8) dst[1] = src[1];
+        perm_out[pos] = perm_in ? perm_in[j] : (int32_t)j;
+    }
+}
+
 // out[j] = pts[idx_j] (whole padded rows), perm_out[j] = perm_in[idx_j] (perm_in == nullptr: idx_j), idx_j = the low
 // ib bits of the sorted key j (pooled indices < 2^31)
 __global__ void k_permute_rows(const float* __restrict__ pts, int DP, int64_t N, const uint64_t* __restrict__ keys,
