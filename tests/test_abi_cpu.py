@@ -90,3 +90,33 @@ def test_null_context_is_an_argument_error_not_a_crash(lib):
     assert L.ddks_rdks(NULL, NULL, 1, NULL, 1, 2, NULL, NULL) == 1
     assert L.ddks_profile_read(NULL, NULL, NULL, NULL) == 1
     assert L.ddks_destroy(NULL) == 0 and L.ddks_launch_count(NULL) == 0
+
+
+def test_binding_argument_checks(lib):
+    # every wrapper checks shapes before the C call (a Q with fewer columns than P would be over-read), and a
+    # float64 input is cast to the library's float32 with a warning (the cast can merge distinct values into ties)
+    import numpy as np
+    import warnings
+    P = np.zeros((5, 3), np.float32)
+    Q = np.zeros((4, 2), np.float32)
+    for fn in (lambda: lib.ddks_stat_shard(None, P, Q, 2, 0), lambda: lib.ddks_stat_per_origin(None, P, Q, 0, 1),
+               lambda: lib.ddks_stat(None, P, Q), lambda: lib.ddks_vdks(None, P, Q, 4)):
+        with pytest.raises(ValueError):
+            fn()
+    with warnings.catch_warnings(record=True) as w:
+        warnings.simplefilter("always")
+        a = lib._Arg(np.zeros((3, 2), np.float64), np.float32)
+        assert a.keep.dtype == np.float32 and any("float64" in str(x.message) for x in w)
+
+
+def test_host_combine_helpers(lib):
+    # the host steps after the single all-gather (include/ddks.h): max num, smallest argmax among the ranks attaining
+    # it (records without origins carry -1), OR of the flags; padded per-rank item records unpadded in rank order
+    assert lib.ddks_combine_records([(5, 10, 0), (7, 3, 1), (7, 2, 0), (0, -1, 0)]) == (7, 2, 1)
+    assert lib.ddks_combine_records([(0, -1, 0), (0, 4, 2)]) == (0, 4, 2)
+    import numpy as np
+    total, world = 5, 3  # shards 2, 2, 1; chunk 2; stride 2 * 2 + 1
+    g = np.array([1, 2, 11, 12, 0,   3, 4, 13, 14, 4,   5, 99, 15, 99, 1], np.uint64)
+    out, flags = lib.ddks_unpad_items(g, total, world, 2)
+    assert out[0].tolist() == [1, 2, 3, 4, 5] and out[1].tolist() == [11, 12, 13, 14, 15] and flags == 5
+    assert lib.gather_stride(total, world, 2) == 5
