@@ -69,7 +69,11 @@ template <> struct Cfg<4> { static constexpr int R = 4, T = 256, TILE = 512, S =
 template <> struct Cfg<5> { static constexpr int R = DDKS_C5R, T = DDKS_C5T, TILE = DDKS_C5TILE, S = DDKS_C5S; };
 template <> struct Cfg<6> { static constexpr int R = 4, T = 384, TILE = 256, S = 3; };
 template <> struct Cfg<7> { static constexpr int R = 2, T = 384, TILE = 256, S = 3; };
-template <> struct Cfg<8> { static constexpr int R = 1, T = 384, TILE = 256, S = 3; };
+#ifndef DDKS_C8R  // geometry experiments (d = 8): -DDDKS_C8R=.. -DDDKS_C8T=..
+#define DDKS_C8R 1
+#define DDKS_C8T 384
+#endif
+template <> struct Cfg<8> { static constexpr int R = DDKS_C8R, T = DDKS_C8T, TILE = 256, S = 3; };
 
 
 // SPLIT (c_P and c_Q kept apart) doubles the bins: halve R (keeping it even or 1), or T when R is already <= 2
