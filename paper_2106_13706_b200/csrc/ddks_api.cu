@@ -218,10 +218,11 @@ bool diff_counters_ok(int64_t n_P, int64_t n_Q) {
 bool x0_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q) {
     if (ctx->flags & DDKS_FLAG_NO_X0) return false;
     // the sort pays for itself once the O(N^2) count dominates; DDKS_FLAG_FORCE_X0 (tests) lowers the bar. Crossover
-    // (microbench/kd_threshold.py): radix-sorted kd at N ~ 60k-75k for d = 2..8; with the mid-N bucket sort (single
-    // rank) at N ~ 40k for d >= 5 (d = 8, N = 40k: 1.06x; d = 3, 4 only from ~60k-80k)
+    // (microbench/kd_threshold.py, profiles/r2_kd_midN_bucket.txt): radix-sorted kd at N ~ 60k-75k for d = 2..8; with
+    // the mid-N bucket sort (single rank) at N ~ 40k for d = 3..8 (N = 40k: d = 3 1.05x, d = 4 1.05x, d = 5 1.04x,
+    // d = 8 1.13x; N = 20k: 0.72-0.93x)
     const bool single = ctx->world == 1;
-    const int64_t min_n = (ctx->flags & DDKS_FLAG_FORCE_X0) ? 2 : ((single && d >= 5) ? 40000 : 80000);
+    const int64_t min_n = (ctx->flags & DDKS_FLAG_FORCE_X0) ? 2 : (single && d >= 3 ? 40000 : 80000);
     return d >= 2 && d <= 8 && n_P + n_Q >= min_n;
 }
 

@@ -217,3 +217,4 @@ def test_tensor_core_null_rejects_bad_rows():
         with pytest.raises(K.DDKSError) as e:
             c.permutation_null(dev(pooled), 100, dev(perms))
         assert e.value.status == 1
+
