@@ -41,12 +41,12 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-// The wait carries a suspend-time hint: a waiting warp sleeps until the phase completes (or the hint expires) instead
-// of re-issuing try_wait every ~70 cycles (at C5 the re-issued try_waits of warps ahead of their TMA stage were 13 % of
-// the kd count's executed instructions). Measured neutral to -0.2 % (C5 637.5 -> 636.5 ms; C2, C3 unchanged:
-// microbench/r2_hint_sweep.sh) -- the sleeping warps were not taking issue slots the counting warps needed.
+// DDKS_MBAR_HINT_NS > 0 builds the wait with a suspend-time hint (a waiting warp sleeps until the phase completes or
+// the hint expires instead of re-issuing try_wait every ~70 cycles; at C5 those re-issues were 13 % of the kd count's
+// executed instructions). Measured: neutral at C5 / C3 / C2 (microbench/r2_hint_sweep.sh) but C4 +8 % (1.427 ->
+// 1.547 ms: 4096 short CTAs that each wait for their first tiles; microbench/r2_c4hint.sh), so the default is off.
 #ifndef DDKS_MBAR_HINT_NS
-#define DDKS_MBAR_HINT_NS 1000000
+#define DDKS_MBAR_HINT_NS 0
 #endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #if DDKS_MBAR_HINT_NS == 0
