@@ -998,7 +998,8 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
     const bool small = !export_mode && shard_world == 0 && small_fused_applies(ctx, n_P, n_Q);
     // environment overrides (tuning / test knobs) change the plan: a graph captured under other values is not reused
     const bool env_override = getenv("DDKS_KD") || getenv("DDKS_SEGS") || getenv("DDKS_KD_SHUFFLE") ||
-                              getenv("DDKS_NO_KEY") || getenv("DDKS_GRIDY") || getenv("DDKS_NO_SMALL");
+                              getenv("DDKS_NO_KEY") || getenv("DDKS_GRIDY") || getenv("DDKS_NO_SMALL") ||
+                              getenv("DDKS_KD_RADIX");
     const bool graphable = !export_mode && shard_world == 0 && !(ctx->flags & DDKS_FLAG_NO_GRAPH) && !env_override &&
                            graph_input_ok(P) && graph_input_ok(Q);
     const ddks_ctx::StatKey key{P, Q, n_P, n_Q, d, ctx->alloc_epoch};
