@@ -1,8 +1,10 @@
 // ddks_api.cu — host side of libddks.so: the C ABI declared in include/ddks.h.
 //
-// Context = device + grow-only workspace + (world > 1, or the NCCL_SELF test flag) an NCCL communicator (NCCL 2.28.9, the copy torch
-// bundles). Each public call: argument checks -> optional H2D of host inputs -> k_pack (validate + pack) ->
-// k_count (classify + count + per-origin max) [-> k_finalize] -> k_argmax -> NCCL combine -> one D2H -> sync.
+// Context = device + grow-only workspace + (world > 1, or the NCCL_SELF test flag) an NCCL communicator (NCCL 2.28.9, the
+// copy torch bundles). A statistic: argument checks -> optional H2D of host inputs -> k_pack (validate + pack) ->
+// [kd ordering] -> k_count (classify + count + per-origin max + packed argmax key) [-> k_finalize] -> (world > 1) one
+// all-gather of the per-rank records -> one D2H -> sync -> host combine; N <= 8192 on one rank: the single fused
+// k_count_small launch instead (ddks_small.cuh). Repeated identical ddks_stat calls replay a captured CUDA graph.
 #include <cuda_runtime.h>
 #include <nccl.h>
 

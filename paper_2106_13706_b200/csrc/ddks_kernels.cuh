@@ -16,11 +16,13 @@
 //   * DIFF mode keeps one signed counter per orthant: c_P*a - c_Q*b with a = n_Q/g, b = n_P/g
 //     (g = gcd(n_P, n_Q)), so |counter| * g is exactly |c_P n_Q - c_Q n_P| (P:L238 cross-multiplied);
 //     SPLIT mode (when DIFF would overflow, and for the significance, which needs c_Q) keeps c_P and c_Q apart;
-//   * kd ordering (large N): rows pre-sorted label-major and hierarchically by x_0 .. x_{KX-1}, so for most tiles the
-//     bits of those dims are decided once per tile and only the other dims are compared (DESIGN.md §7 "kd ordering");
-//   * finalisation is exact integer arithmetic; the max is a warp-shuffle + CTA + atomicMax(u64) reduction;
+//   * kd ordering (N >= 40 000): rows pre-sorted label-major and hierarchically by x_0 .. x_{KX-1}, so for most tiles
+//     the bits of those dims are decided once per tile and only the other dims are compared (DESIGN.md §7 "kd
+//     ordering"); a tile left with ONE compared dim sums its compare bits in registers (count_points, one-dim path);
+//   * finalisation is exact integer arithmetic; the max (and the packed argmax key: red(o) << 31 | ~origin) is a
+//     warp-shuffle + CTA + atomicMax(u64) reduction, or k_finalize after segmented counts;
 //   * the label-invariant permutation null (k_labels / k_perm_count) classifies each pair once per chunk of
-//     permutations.
+//     permutations (the tensor-core version is ddks_perm_mma.cuh; the fused small-N statistic ddks_small.cuh).
 #pragma once
 #include <cstdint>
 #include <utility>
