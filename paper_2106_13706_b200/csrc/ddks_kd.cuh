@@ -28,7 +28,7 @@ inline int bits_for(uint64_t v) { int b = 0; while (v) { ++b; v >>= 1; } return 
 
 // Levels and cuts from a cost model of the compares per pair: D - K compared dims always, plus the expected
 // undecided bits: a tile in the same slab (or, across labels, the neighbouring one) leaves bit 0 open
-// (~1.5 / G0), likewise bit 1 (~1.5 / G1), and the last sorted dim interleaves for (origins per CTA + TILE) /
+// (~1.0 / G0, fitted), bit 1 (~1.5 / G1), and the last sorted dim interleaves for (origins per CTA + TILE) /
 // cell rows of the tiles (per warp for the last dim). Cells must keep at least A rows on average. forced_k (1..3) fixes K (tests); kmax caps it.
 inline KdChoice kd_choose(int D, int64_t n_lab, int64_t RT, int64_t RW, int64_t TILE, int64_t A, int forced_k,
                           int kmax) {
@@ -59,7 +59,10 @@ inline KdChoice kd_choose(int D, int64_t n_lab, int64_t RT, int64_t RW, int64_t 
                         const int64_t cells = g0 * g1 * g2 * g3;
                         if (cells > 1 && n_lab / cells < A) break;  // a cell holds >= one origin block on average
                         double cost = (double)(D - K) + c * (double)cells + k5;
-                        if (K >= 2) cost += 1.5 / (double)g0;
+                        // level 0 weighs 1.0, not 1.5 (round 2, with the one-dim register path: C5 picks 6 x 9 x 9
+                        // instead of 7 x 8 x 8, 630.9 -> 622 ms count; N = 4e5 at d = 5..8 within +-0.7 %;
+                        // profiles/r2_kd_cuts_c5.txt, r2_kd_level0_weight.txt)
+                        if (K >= 2) cost += 1.0 / (double)g0;
                         if (K >= 3) cost += 1.5 / (double)g1;
                         if (K >= 4) cost += 1.5 / (double)g2;
                         if (K >= 5) cost += 1.5 / (double)g3;
