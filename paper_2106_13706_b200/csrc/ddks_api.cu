@@ -1187,10 +1187,16 @@ ddks_status ddks_permutation_null(ddks_ctx* ctx, const float* pooled, int64_t n_
     const bool label_path = N <= 65535 && !(ctx->flags & DDKS_FLAG_PERM_GATHER);
     if (label_path) {
         auto fn = perm_mma_applies(ctx, d, N) ? launch_perm_mma : launch_perm;
-        if (je > jb &&
-            (s = fn(ctx, d, pooled_packed, (const int32_t*)dperm + jb * N, je - jb, n_P, n_Q, nums + 1 + jb, &dres->flag,
-                    st)))
-            return s;
+        // permutations in groups whose label images / counters and validation bitmaps stay within ~256 MB (about
+        // 1.5 N bytes per permutation; DDKS_PERM_GROUP, test only, overrides the group size)
+        int64_t grp = std::max<int64_t>(768, ((256ll << 20) / (3 * N / 2 + 1)) / 768 * 768);
+        if (const char* e = getenv("DDKS_PERM_GROUP")) grp = std::max(1, atoi(e));
+        for (int64_t j0 = jb; j0 < je; j0 += grp) {
+            const int64_t nj = std::min(grp, je - j0);
+            if ((s = fn(ctx, d, pooled_packed, (const int32_t*)dperm + j0 * N, nj, n_P, n_Q, nums + 1 + j0, &dres->flag,
+                        st)))
+                return s;
+        }
     } else {
         const int64_t chunk_max = std::max<int64_t>(1, (int64_t)((256ull << 20) / ((size_t)N * DP * 4)));
         for (int64_t j0 = jb; j0 < je; j0 += chunk_max) {

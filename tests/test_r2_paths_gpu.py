@@ -218,3 +218,22 @@ def test_tensor_core_null_rejects_bad_rows():
             c.permutation_null(dev(pooled), 100, dev(perms))
         assert e.value.status == 1
 
+
+
+@pytest.mark.parametrize("mma", [True, False])
+def test_permutation_groups(monkeypatch, mma):
+    # permutations processed in groups (bounded label-image / bitmap memory): group boundaries inside tensor-core
+    # tiles and label words, the last group ragged; identical to one group and to the oracle
+    P, Q = I.random_pair(37000, 300, 250, 4, "grid")
+    pooled = np.concatenate([P, Q])
+    rng = np.random.default_rng(37001)
+    perms = np.stack([rng.permutation(550) for _ in range(601)]).astype(np.int32)
+    if not mma:
+        monkeypatch.setenv("DDKS_NO_MMA", "1")
+    o_null, o_obs, _, o_p = O.permutation_null(pooled, 300, perms)
+    with K.Context() as c:
+        one = c.permutation_null(dev(pooled), 300, dev(perms))
+        monkeypatch.setenv("DDKS_PERM_GROUP", "257")
+        grp = c.permutation_null(dev(pooled), 300, dev(perms))
+    assert np.array_equal(one[0], o_null) and np.array_equal(grp[0], o_null)
+    assert one[1].num == grp[1].num == o_obs and one[2] == grp[2] == o_p
