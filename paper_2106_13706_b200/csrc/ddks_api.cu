@@ -706,7 +706,7 @@ ddks_status ddks_destroy(ddks_ctx* ctx) {
     for (DevBuf* b : {&ctx->raw_a, &ctx->raw_b, &ctx->raw_perm, &ctx->packed, &ctx->packed2, &ctx->pool_packed, &ctx->per_origin,
                       &ctx->accum, &ctx->gather, &ctx->item_num, &ctx->bitmap, &ctx->labels, &ctx->res, &ctx->sig_hist,
                       &ctx->sig_lf, &ctx->sig_scratch, &ctx->sig_table, &ctx->sig_contrib, &ctx->sig_part,
-                      &ctx->vox_keys, &ctx->vox_cnt, &ctx->vox_S, &ctx->rd_keys, &ctx->rd_xn, &ctx->rd_k0,
+                      &ctx->vox_keys, &ctx->vox_cnt, &ctx->vox_S, &ctx->vox_fill, &ctx->vox_slab, &ctx->rd_keys, &ctx->rd_xn, &ctx->rd_k0,
                       &ctx->rd_k1, &ctx->rd_hist, &ctx->rd_tcnt, &ctx->rd_cnum, &ctx->x0_keys0,
                       &ctx->x0_keys1, &ctx->x0_hist, &ctx->x0_pts, &ctx->x0_perm, &ctx->x0_pts2,
                       &ctx->x0_perm2, &ctx->x0_boxes, &ctx->prof_clk, &ctx->rdb_cnt,

@@ -76,7 +76,7 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     const int gy = std::min(d, 1024);
     const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((N + 1023) / 1024, std::max(1, 296 / gy)));
     if (d <= 8 && ((((uintptr_t)dP | (uintptr_t)dQ) & 15) == 0)) {  // float4 rows-in-fours
-        const int gv = (int)std::max<int64_t>(1, std::min<int64_t>((N / 4 + 255) / 256, 148 * 8));
+        const int gv = (int)std::max<int64_t>(1, std::min<int64_t>((N / 4 + 255) / 256, ddks::MINMAX_BLOCKS));
         switch (d) {
 #define MMV(D) case D: ddks::k_minmax_vec<D><<<gv, 256, 0, st>>>((const float*)dP, n_P, (const float*)dQ, n_Q, keys, D, 1, &dres->flag); break;
             MMV(1) MMV(2) MMV(3) MMV(4) MMV(5) MMV(6) MMV(7) MMV(8)

@@ -37,7 +37,9 @@ struct ddks_ctx {
     DevBuf raw_a, raw_b, raw_perm, packed, packed2, pool_packed, per_origin, accum, item_num, bitmap, labels, res;
     DevBuf gather;  // world > 1: all-gather send + receive buffers
     DevBuf sig_hist, sig_lf, sig_scratch, sig_table, sig_contrib, sig_part;  // ddks_significance workspace
-    DevBuf vox_keys, vox_cnt, vox_S;                                           // ddks_vdks workspace
+    DevBuf vox_keys, vox_cnt, vox_S, vox_fill, vox_slab;                      // ddks_vdks workspace
+    void* vox_zero_p = nullptr;  // vox_cnt.p whose first vox_zero bytes are known zero (slab scans clean the counts)
+    size_t vox_zero = 0;
     DevBuf rd_keys, rd_xn, rd_k0, rd_k1, rd_hist, rd_tcnt, rd_cnum;              // ddks_rdks workspace
     DevBuf x0_keys0, x0_keys1, x0_hist, x0_pts, x0_perm, x0_pts2, x0_perm2, x0_boxes;  // kd-ordered count workspace
     DevBuf rdb_cnt, rdb_pst, rdb_coff, rdb_fill, rdb_clist, rdb_csum;            // rdKS bucket-pruned sweep

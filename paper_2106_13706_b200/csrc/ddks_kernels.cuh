@@ -555,9 +555,11 @@ __global__ void __launch_bounds__(Geo<D, SPLIT, SMALL>::T, count_min_blocks<D, K
     const int n_tiles = (seg1 - seg0 + TILE - 1) / TILE;
 
     __shared__ uint32_t done_cnt[S];  // warps done with each stage (monotone over the rounds)
+    __shared__ unsigned long long s_exec;  // profiling: this CTA's executed compares
     if (t == 0) {
 #pragma unroll
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1), done_cnt[s] = 0u;
+        s_exec = 0ull;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = t; i < G::HIST_WORDS; i += T) hist[i] = 0u;
@@ -647,9 +649,11 @@ __global__ void __launch_bounds__(Geo<D, SPLIT, SMALL>::T, count_min_blocks<D, K
         for (int k = 0; k < 2 * KX; ++k) bnext[k] = __ldg(a.boxes + (int64_t)(seg0 / TILE) * 2 * KX + k);
     }
 
-    // in-kernel clock probe (one lane per CTA, profiling only): the SM clock this launch actually ran at
+    // in-kernel clock probe (profiling only; one lane of every 8th CTA -- the clk / ns ratio needs a sample, and
+    // thousands of same-address atomics at the kernel tail cost ~8 us at C2): the SM clock this launch ran at
+    const bool probe = a.clk && t == 0 && ((blockIdx.x + blockIdx.y) & 7) == 0;
     unsigned long long clk0 = 0, ns0 = 0;
-    if (a.clk && t == 0) clk0 = clock64(), ns0 = globaltimer_ns();
+    if (probe) clk0 = clock64(), ns0 = globaltimer_ns();
     unsigned long long exec_cmp = 0;  // profiling: compares this warp executed / (32 R)
 
     for (int it = 0; it < n_tiles; ++it) {
@@ -766,13 +770,14 @@ __global__ void __launch_bounds__(Geo<D, SPLIT, SMALL>::T, count_min_blocks<D, K
             }
         }
     }
+    if (a.clk && lane == 0) atomicAdd(&s_exec, exec_cmp * (unsigned long long)(32 * R));
     __syncthreads();  // all red.shared retired before reading the counters
-    if (a.clk) {
-        if (t == 0) {
+    if (a.clk && t == 0) {
+        atomicAdd(&a.clk[2], s_exec);  // one global atomic per CTA
+        if (probe) {
             atomicAdd(&a.clk[0], (unsigned long long)(clock64() - clk0));
             atomicAdd(&a.clk[1], globaltimer_ns() - ns0);
         }
-        if (lane == 0) atomicAdd(&a.clk[2], exec_cmp * (unsigned long long)(32 * R));
     }
 
     // per-origin epilogue shared by both modes: num(o) -> per-origin export, the CTA max, the packed argmax key

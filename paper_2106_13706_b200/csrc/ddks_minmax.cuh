@@ -7,6 +7,13 @@
 
 namespace ddks {
 
+#ifndef DDKS_MINMAX_BLOCKS
+#define DDKS_MINMAX_BLOCKS (148 * 2)
+#endif
+// grid cap of k_minmax_vec: every block ends in 2 D same-address atomics, so fewer, longer blocks (two groups of
+// rows in flight per thread keep the loads overlapped)
+constexpr int MINMAX_BLOCKS = DDKS_MINMAX_BLOCKS;
+
 // Per-dimension min / max of all pooled points as order-preserving keys (-0 as +0): keys[m] = min (init 0xffffffff),
 // keys[max_off + m] = max (init 0); validate: a non-finite coordinate sets *flag |= 1. For 16-byte aligned row-major
 // [n][D] inputs: 4 rows = D float4 per step (dims fixed at compile time), the < 4 leftover rows of each sample scalar.
@@ -26,16 +33,29 @@ __global__ void __launch_bounds__(256) k_minmax_vec(const float* __restrict__ P,
         mn[m] = k < mn[m] ? k : mn[m];
         mx[m] = k > mx[m] ? k : mx[m];
     };
-    const int64_t gP = n_P / 4, gQ = n_Q / 4;
-    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < gP + gQ; g += (int64_t)gridDim.x * blockDim.x) {
-        const float4* src = reinterpret_cast<const float4*>(g < gP ? P + g * 4 * D : Q + (g - gP) * 4 * D);
+    const int64_t gP = n_P / 4, gQ = n_Q / 4, gs = (int64_t)gridDim.x * blockDim.x;
+    constexpr int U = 2;  // groups of 4 rows in flight per thread
+    for (int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g0 < gP + gQ; g0 += U * gs) {
+        float4 v[U][D];
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-            const float4 v = __ldg(src + j);
-            take(v.x, (4 * j + 0) % D);
-            take(v.y, (4 * j + 1) % D);
-            take(v.z, (4 * j + 2) % D);
-            take(v.w, (4 * j + 3) % D);
+        for (int u = 0; u < U; ++u) {
+            const int64_t g = g0 + u * gs;
+            if (g < gP + gQ) {
+                const float4* src = reinterpret_cast<const float4*>(g < gP ? P + g * 4 * D : Q + (g - gP) * 4 * D);
+#pragma unroll
+                for (int j = 0; j < D; ++j) v[u][j] = __ldg(src + j);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (g0 + u * gs >= gP + gQ) break;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                take(v[u][j].x, (4 * j + 0) % D);
+                take(v[u][j].y, (4 * j + 1) % D);
+                take(v[u][j].z, (4 * j + 2) % D);
+                take(v[u][j].w, (4 * j + 3) % D);
+            }
         }
     }
     if (blockIdx.x == 0 && threadIdx.x < 8) {  // leftover rows

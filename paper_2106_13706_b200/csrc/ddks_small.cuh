@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(SM_T) k_count_small(const SmallArgs a) {
         exec_cmp += (unsigned long long)D * cnt;
     }
     if (bad) atomicOr(sflag, 1u);
-    if (a.clk && (t & 31) == 0) atomicAdd(&a.clk[2], exec_cmp * (unsigned long long)(32 * R));
+    // every thread executed the same compares: one global atomic per CTA
+    if (a.clk && t == 0) atomicAdd(&a.clk[2], exec_cmp * (unsigned long long)(T * R));
 
     // cluster reduction: every rank's counts into the leader's counters (DSMEM), then the leader finalises
     __syncthreads();

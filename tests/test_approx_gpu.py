@@ -39,6 +39,55 @@ def test_vdks_parity(ctx, n_P, n_Q, d, k, kind):
     assert (got.num, got.den) == want[:2] and got.D == want[2], (got, want)
 
 
+# slab scans (L = k^J <= 4096 voxels per slab scanned in SMEM, then the outer dimensions in SMEM column chunks or, past
+# 512 slabs, line passes; k > 4096 line passes only) and the filled-voxel list: non-power-of-two k, every J
+SLAB_CASES = [(3000, 2500, 4, 17), (2000, 2200, 3, 50), (2500, 2000, 5, 10), (1500, 1800, 6, 7), (1200, 1000, 8, 4),
+              (1000, 1100, 2, 300), (1500, 1200, 3, 64), (600, 700, 7, 5), (300, 250, 2, 1024), (500, 400, 1, 5000),
+              (60, 50, 2, 4200), (700, 650, 3, 33)]
+
+
+@pytest.mark.parametrize("n_P,n_Q,d,k", SLAB_CASES)
+@pytest.mark.parametrize("kind", ["normal", "dup"])
+def test_vdks_slab_parity(ctx, n_P, n_Q, d, k, kind):
+    P, Q = I.random_pair(4100 + n_P + d * 10 + k, n_P, n_Q, d, kind)
+    want = O.vdks(P, Q, k)
+    got = ctx.vdks(dev(P), dev(Q), k)
+    assert (got.num, got.den) == want[:2] and got.D == want[2], (got, want)
+
+
+def test_vdks_count_buffer_reuse():
+    # the slab scans leave the voxel counts zeroed for the next call, which then skips the memset over the known-zero
+    # prefix: a line-pass call (k > 4096) dirties a large buffer, a small slab call cleans only its own prefix, and a
+    # larger slab call must not read the rest as clean
+    P2, Q2 = I.random_pair(71, 60, 50, 2, "dup")
+    P3, Q3 = I.random_pair(72, 700, 650, 3, "dup")
+    P4, Q4 = I.random_pair(73, 300, 250, 2, "dup")
+    want = [O.vdks(P2, Q2, 4200)[:2], O.vdks(P3, Q3, 33)[:2], O.vdks(P4, Q4, 1024)[:2]]
+    with K.Context() as c:
+        for _ in range(2):
+            assert c.vdks(dev(P2), dev(Q2), 4200)[:2] == want[0]
+            assert c.vdks(dev(P3), dev(Q3), 33)[:2] == want[1]
+            assert c.vdks(dev(P4), dev(Q4), 1024)[:2] == want[2]
+            assert c.vdks(dev(P4), dev(Q4), 1024)[:2] == want[2]
+
+
+@pytest.mark.parametrize("d,k", [(3, 64), (5, 16), (4, 23), (2, 1000), (8, 5)])
+def test_vdks_aligned_vs_unaligned(ctx, d, k):
+    # larger inputs than the oracle's literal SumOrthants takes in seconds: the vectorised histogram (16-byte aligned
+    # inputs) and the scalar one (rows offset by one, unaligned) must agree exactly; a skewed mixture like C5's
+    rng = np.random.default_rng(d * 1000 + k)
+    P = rng.standard_normal((60001, d)).astype(np.float32)
+    A = rng.standard_normal((50003, d))
+    Q = np.where((rng.random(50003) < 0.2)[:, None], 0.3 * A + 1.0, A).astype(np.float32)
+    a = ctx.vdks(dev(P), dev(Q), k)
+    bufP = torch.empty(P.size + 1, dtype=torch.float32, device="cuda")
+    bufQ = torch.empty(Q.size + 1, dtype=torch.float32, device="cuda")
+    bufP[1:] = dev(P.ravel())
+    bufQ[1:] = dev(Q.ravel())
+    b = ctx.vdks(bufP[1:].view(P.shape), bufQ[1:].view(Q.shape), k)
+    assert a == b and a.num > 0
+
+
 def test_vdks_grid_and_edges(ctx):
     # integer grids: every point on a voxel boundary; k = #values makes vdKS the exact ddKS (oracle pin)
     rng = np.random.default_rng(8)
