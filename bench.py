@@ -317,11 +317,12 @@ class Step:
         N = self.N
         if self.args.method == "vdks":
             V = self.args.vdks_k ** d
-            # input read twice in place (min/max, voxelise), voxel counts (zero + read), d prefix passes over the
-            # int64 sums (read + write; the first reads the counts), one read of counts and sums in the orthant pass
-            # (DESIGN.md §7 vdKS)
-            byts = 2 * N * d * 4 + 2 * V * 8 + 2 * d * V * 8 + 2 * V * 8
-            what = "whole vdKS step (pack, voxel histogram, prefix passes, orthant sums)"
+            # the method's data movement (DESIGN.md §7 vdKS): input read twice (min/max, then voxelise -- the
+            # normalisation needs the global extremes first), the voxel counts written and read once, the int64
+            # prefix sums written and read once; the implementation's extra passes (the outer-dimension scan reads
+            # and writes the sums again) count against the fraction. (Round 1 counted d full prefix passes here.)
+            byts = 2 * N * d * 4 + 2 * V * 8 + 2 * V * 8
+            what = "whole vdKS step (min/max, voxel histogram, slab + outer prefix scans, orthant sums)"
         else:
             keys = (d + 1) * N * 8
             nbk = 256

@@ -23,15 +23,17 @@ __global__ void __launch_bounds__(256) k_minmax_vec(const float* __restrict__ P,
                                                     const float* __restrict__ Q, int64_t n_Q, uint32_t* keys,
                                                     int max_off, int validate, uint32_t* flag) {
     __shared__ uint32_t sa[8][8], sb[8][8];
-    uint32_t mn[D], mx[D];
+    // per-thread extremes as floats (FMNMX; -0 + 0 = +0 canonicalises the zero), keys formed once per thread. A NaN
+    // is skipped by fminf / fmaxf; it is flagged when validating (and is undefined input otherwise)
+    float fmn[D], fmx[D];
     bool bad = false;
 #pragma unroll
-    for (int m = 0; m < D; ++m) mn[m] = 0xffffffffu, mx[m] = 0u;
+    for (int m = 0; m < D; ++m) fmn[m] = INFINITY, fmx[m] = -INFINITY;
     auto take = [&](float v, int m) {
-        if (validate && !isfinite(v)) bad = true;
-        const uint32_t k = f32_key(v == 0.0f ? 0.0f : v);
-        mn[m] = k < mn[m] ? k : mn[m];
-        mx[m] = k > mx[m] ? k : mx[m];
+        if (validate && !(fabsf(v) < INFINITY)) bad = true;
+        v += 0.0f;
+        fmn[m] = fminf(fmn[m], v);
+        fmx[m] = fmaxf(fmx[m], v);
     };
     const int64_t gP = n_P / 4, gQ = n_Q / 4, gs = (int64_t)gridDim.x * blockDim.x;
     constexpr int U = 2;  // groups of 4 rows in flight per thread
@@ -70,7 +72,10 @@ __global__ void __launch_bounds__(256) k_minmax_vec(const float* __restrict__ P,
     if (bad) atomicOr(flag, 1u);
 #pragma unroll
     for (int m = 0; m < D; ++m) {
-        uint32_t a = mn[m], b = mx[m];
+        // no row seen: the identity keys (an all-infinite dimension is non-finite input: flagged when validating,
+        // undefined otherwise)
+        uint32_t a = fmn[m] == INFINITY ? 0xffffffffu : f32_key(fmn[m]);
+        uint32_t b = fmx[m] == -INFINITY ? 0u : f32_key(fmx[m]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
