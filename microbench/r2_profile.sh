@@ -37,6 +37,8 @@ cap c3 k_count python profiles/profile_run.py C3
 cap c2 k_count python profiles/profile_run.py C2
 cap c4 k_count python profiles/profile_run.py C4
 cap c4perm k_perm python bench.py --workload C4 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e
+cap vdkshist k_vox_hist_vec python microbench/approx_c5.py 1 vdks
+cap vdksslab k_vox_prefix_slab python microbench/approx_c5.py 1 vdks
 # DRAM traffic of the full-size C5 count launch and per-opcode counts for the executed-compare check
 timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,smsp__inst_executed.sum,sm__inst_executed_pipe_alu.sum --clock-control none -k regex:k_count -s 3 -c 1 --csv --log-file $O/${TAG}_traffic_c5.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 for w in C2 C3 C4; do
