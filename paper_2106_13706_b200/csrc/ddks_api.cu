@@ -46,6 +46,9 @@ ddks_status fail(ddks_ctx* c, ddks_status s, const char* fmt, ...) {
 ddks_status ensure(ddks_ctx* ctx, DevBuf& b, size_t bytes) {
     if (bytes <= b.bytes) return DDKS_OK;
     if (b.p) cudaFree(b.p);
+    // a new allocation may reuse the old address: the self-cleaning count buffers lose their known-zero state
+    if (&b == &ctx->vox_cnt) ctx->vox_zero_p = nullptr;
+    if (&b == &ctx->rdb_cnt) ctx->rdb_zero_p = nullptr;
     b.p = nullptr;
     b.bytes = 0;
     size_t want = std::max(bytes, (size_t)256);

@@ -114,6 +114,7 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
         return DDKS_OK;
     };
     const bool pruned = !(ctx->flags & DDKS_FLAG_RDKS_FULL_SORT);
+    size_t rdb_clean_bytes = 0;  // pruned path: bytes of the bucket counts zero again once the call completes
     if (nc > 0) {
         if (!pruned) {
             launch_rd_keys((const float*)dP, (const float*)dQ, xn, N, n_P, d, keys, (int)cb, (int)ce, k0, nullptr, 0,
@@ -131,12 +132,17 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
             if ((s = ensure(ctx, ctx->rdb_pst, nb * 8))) return s;
             if ((s = ensure(ctx, ctx->rdb_coff, nb * 4))) return s;
             if ((s = ensure(ctx, ctx->rdb_fill, nb * 4))) return s;
+            if ((s = ensure(ctx, ctx->rdb_bits, nb / 8))) return s;
             if ((s = ensure(ctx, ctx->rdb_clist, nb * 4))) return s;
             if ((s = ensure(ctx, ctx->rdb_csum, ((size_t)nc * ((nbk + ddks::RDB_CH - 1) / ddks::RDB_CH) + nc) * 8))) return s;
             uint32_t* bcnt = (uint32_t*)ctx->rdb_cnt.p;
             int32_t* clist = (int32_t*)ctx->rdb_clist.p;
-            CU(cudaMemsetAsync(bcnt, 0, nb * 8, st));
-            CU(cudaMemsetAsync(ctx->rdb_fill.p, 0, nb * 4, st));
+            // the bucket counts must start at zero: k_rdb_cand / k_rdb_finish re-zero every bucket they read, so after
+            // a completed call the first rdb_zero bytes of the buffer are known zero (no memset of nb * 8 bytes)
+            const size_t zero = ctx->rdb_zero_p == ctx->rdb_cnt.p ? ctx->rdb_zero : 0;
+            ctx->rdb_zero_p = nullptr;  // until this call completes
+            if (zero < nb * 8) CU(cudaMemsetAsync((uint8_t*)bcnt + zero, 0, nb * 8 - zero, st));
+            rdb_clean_bytes = std::max(zero, nb * 8);
             // distance keys and their bucket counts in one pass (NormalizeData fused)
             launch_rd_keys((const float*)dP, (const float*)dQ, xn, N, n_P, d, keys, (int)cb, (int)ce, k0, bcnt, nbk,
                            scale, st);
@@ -149,9 +155,18 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
             ddks::k_rdb_chunk_scan<<<nc, 256, 0, st>>>(csum, nch);
             ddks::k_rdb_down<<<dim3(nch, nc), 256, 0, st>>>(bcnt, nbk, csum, n_P, n_Q, (uint2*)ctx->rdb_pst.p, cnum);
             ddks::k_rdb_cand<<<grid_for((int64_t)nb), 256, 0, st>>>(bcnt, (const uint2*)ctx->rdb_pst.p, nc, nbk, n_P,
-                                                                    n_Q, cnum, (uint32_t*)ctx->rdb_coff.p, clist, segc);
-            ddks::k_rdb_compact<<<grid_for(N * nc), 256, 0, st>>>(k0, N, nc, nbk, scale, (const uint32_t*)ctx->rdb_coff.p,
-                                                                  (uint32_t*)ctx->rdb_fill.p, k1);
+                                                                    n_Q, cnum, (uint32_t*)ctx->rdb_coff.p,
+                                                                    (uint32_t*)ctx->rdb_fill.p,
+                                                                    (uint32_t*)ctx->rdb_bits.p, clist, segc);
+            // compaction: ~2 CTAs per SM in all, split over the segments; the segment's bitmap in dynamic SMEM
+            const int cbytes = nbk / 8;
+            if (cbytes > 48 * 1024)
+                CU(cudaFuncSetAttribute(ddks::k_rdb_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
+            const int64_t cchunks = std::max<int64_t>(1, std::min<int64_t>((148 * 2 + nc - 1) / nc,
+                                                                           (N + ddks::RDB_CT - 1) / ddks::RDB_CT));
+            ddks::k_rdb_compact<<<dim3((unsigned)cchunks, nc), ddks::RDB_CT, cbytes, st>>>(
+                k0, N, nbk, scale, (const uint32_t*)ctx->rdb_bits.p, (const uint32_t*)ctx->rdb_coff.p,
+                (uint32_t*)ctx->rdb_fill.p, k1);
             ddks::k_rdb_finish<<<dim3(std::max(1, std::min(1024, (148 * 4 + nc - 1) / nc)), nc), 256, 0, st>>>(
                 k1, N, nbk, bcnt, (const uint2*)ctx->rdb_pst.p, (const uint32_t*)ctx->rdb_coff.p, clist, segc, n_P,
                 n_Q, cnum, &dres->flag);
@@ -165,6 +180,10 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(hc, cnum, (size_t)std::max(nc, 0) * 8, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    if (nc > 0 && pruned && !(hres->flag & 256u)) {  // every bucket was read and re-zeroed
+        ctx->rdb_zero_p = ctx->rdb_cnt.p;
+        ctx->rdb_zero = rdb_clean_bytes;
+    }
     if (nc > 0 && pruned && (hres->flag & 256u)) {  // a candidate bucket too large for SMEM: sort everything
         if ((s = full_sort())) return s;
         CU(cudaMemcpyAsync(hc, cnum, (size_t)nc * 8, cudaMemcpyDeviceToHost, st));

@@ -303,41 +303,71 @@ __global__ void __launch_bounds__(256) k_rdb_down(const uint32_t* __restrict__ c
 
 // Candidates: at least two keys inside, and the reachable extreme beats the best bucket end (cnum[s] after
 // k_rdb_down). Each gets a slot in the segment's candidate buffer (coff) and list (clist) by atomics on the
-// segment's counters seg[2 * s] (keys) and seg[2 * s + 1] (buckets); non-candidates get coff = ~0u.
-__global__ void k_rdb_cand(const uint32_t* __restrict__ cnt, const uint2* __restrict__ pst, int nseg,
+// segment's counters seg[2 * s] (keys) and seg[2 * s + 1] (buckets), a zeroed fill counter, and its bit in the
+// candidate bitmap cbits (one ballot word per 32 buckets; nbk is a power of two >= 256, so a warp's 32 consecutive
+// buckets are one word). Non-candidate buckets' counts are re-zeroed here (the candidates' in k_rdb_finish), so the
+// next call needs no memset of the count array.
+__global__ void k_rdb_cand(uint32_t* __restrict__ cnt, const uint2* __restrict__ pst, int nseg,
                            int nbk, int64_t n_P, int64_t n_Q, const unsigned long long* __restrict__ cnum,
-                           uint32_t* __restrict__ coff, int32_t* __restrict__ clist, uint32_t* __restrict__ seg) {
+                           uint32_t* __restrict__ coff, uint32_t* __restrict__ fill, uint32_t* __restrict__ cbits,
+                           int32_t* __restrict__ clist, uint32_t* __restrict__ seg) {
     const int64_t total = (int64_t)nseg * nbk;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int s = (int)(i / nbk);
-        const uint2 st = pst[i];
-        const int64_t cp = cnt[2 * i], cq = cnt[2 * i + 1];
-        const int64_t t0 = (int64_t)st.x * n_Q - (int64_t)st.y * n_P;
-        const int64_t hi = t0 + cp * n_Q, lo = t0 - cq * n_P;
-        const uint64_t bound = (uint64_t)max(hi < 0 ? -hi : hi, lo < 0 ? -lo : lo);
-        if (cp + cq >= 2 && bound > cnum[s]) {
-            coff[i] = atomicAdd(&seg[2 * s], (uint32_t)(cp + cq));
-            clist[(int64_t)s * nbk + atomicAdd(&seg[2 * s + 1], 1u)] = (int32_t)(i - (int64_t)s * nbk);
-        } else {
-            coff[i] = ~0u;
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;  // a multiple of 32: every warp stays word-aligned
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - (threadIdx.x & 31) < total; i += step) {
+        bool cand = false;
+        if (i < total) {
+            const int s = (int)(i / nbk);
+            const uint2 c2 = reinterpret_cast<const uint2*>(cnt)[i];
+            const int64_t cp = c2.x, cq = c2.y;
+            const uint2 st = pst[i];
+            const int64_t t0 = (int64_t)st.x * n_Q - (int64_t)st.y * n_P;
+            const int64_t hi = t0 + cp * n_Q, lo = t0 - cq * n_P;
+            const uint64_t bound = (uint64_t)max(hi < 0 ? -hi : hi, lo < 0 ? -lo : lo);
+            cand = cp + cq >= 2 && bound > cnum[s];
+            if (cand) {
+                coff[i] = atomicAdd(&seg[2 * s], (uint32_t)(cp + cq));
+                fill[i] = 0u;
+                clist[(int64_t)s * nbk + atomicAdd(&seg[2 * s + 1], 1u)] = (int32_t)(i - (int64_t)s * nbk);
+            } else if (cp + cq) {
+                reinterpret_cast<uint2*>(cnt)[i] = make_uint2(0u, 0u);
+            }
         }
+        const uint32_t w = __ballot_sync(0xffffffffu, cand);
+        if ((threadIdx.x & 31) == 0 && i < total) cbits[i >> 5] = w;
     }
 }
 
-// candidate keys, grouped by bucket (order inside a bucket arbitrary): ck[s * N + coff[b] + k]
-__global__ void k_rdb_compact(const uint64_t* __restrict__ key, int64_t N, int nseg, int nbk, double scale,
-                              const uint32_t* __restrict__ coff, uint32_t* __restrict__ fill,
-                              uint64_t* __restrict__ ck) {
-    const int64_t total = N * nseg;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t s = e / N;
-        const uint64_t k = key[e];
-        const int64_t b = s * nbk + rdb_bucket(k, scale, nbk);
-        const uint32_t o = coff[b];
-        if (o != ~0u) {
-            const uint32_t pos = o + atomicAdd(&fill[b], 1u);
-            DDKS_ASSERT(pos < N);
-            ck[s * N + pos] = k;
+// candidate keys, grouped by bucket (order inside a bucket arbitrary): ck[s * N + coff[b] + k]. grid (chunks, nseg):
+// the CTA holds segment s's candidate bitmap in SMEM (nbk / 8 bytes), so a non-candidate key costs its coalesced
+// load, its bucket and one shared-memory bit test; only candidate keys touch coff / fill (global).
+constexpr int RDB_CT = 512;
+__global__ void __launch_bounds__(RDB_CT) k_rdb_compact(const uint64_t* __restrict__ key, int64_t N, int nbk,
+                                                        double scale, const uint32_t* __restrict__ cbits,
+                                                        const uint32_t* __restrict__ coff, uint32_t* __restrict__ fill,
+                                                        uint64_t* __restrict__ ck) {
+    extern __shared__ uint4 sbits4[];
+    const int s = blockIdx.y;
+    const uint4* src = reinterpret_cast<const uint4*>(cbits + (int64_t)s * (nbk / 32));
+    for (int i = threadIdx.x; i < nbk / 128; i += RDB_CT) sbits4[i] = src[i];
+    __syncthreads();
+    const uint32_t* sbits = reinterpret_cast<const uint32_t*>(sbits4);
+    const uint64_t* ks = key + (int64_t)s * N;
+    constexpr int U = 4;  // keys in flight per thread
+    const int64_t gs = (int64_t)gridDim.x * RDB_CT;
+    for (int64_t e0 = blockIdx.x * (int64_t)RDB_CT + threadIdx.x; e0 < N; e0 += U * gs) {
+        uint64_t k[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) k[u] = e0 + u * gs < N ? __ldcs(ks + e0 + u * gs) : 0ull;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (e0 + u * gs >= N) break;
+            const int b = rdb_bucket(k[u], scale, nbk);
+            if ((sbits[b >> 5] >> (b & 31)) & 1u) {
+                const int64_t bi = (int64_t)s * nbk + b;
+                const uint32_t pos = coff[bi] + atomicAdd(&fill[bi], 1u);
+                DDKS_ASSERT(pos < N);
+                ck[(int64_t)s * N + pos] = k[u];
+            }
         }
     }
 }
@@ -345,7 +375,7 @@ __global__ void k_rdb_compact(const uint64_t* __restrict__ key, int64_t N, int n
 // One CTA per candidate bucket (grid-stride over the segment's list): bitonic sort of its <= RDB_CAPK keys in SMEM,
 // then the exact sweep from the bucket's start counts; atomicMax into cnum[s].
 __global__ void __launch_bounds__(256) k_rdb_finish(const uint64_t* __restrict__ ck, int64_t N, int nbk,
-                                                    const uint32_t* __restrict__ cnt, const uint2* __restrict__ pst,
+                                                    uint32_t* __restrict__ cnt, const uint2* __restrict__ pst,
                                                     const uint32_t* __restrict__ coff,
                                                     const int32_t* __restrict__ clist,
                                                     const uint32_t* __restrict__ seg, int64_t n_P, int64_t n_Q,
@@ -373,6 +403,8 @@ __global__ void __launch_bounds__(256) k_rdb_finish(const uint64_t* __restrict__
                 mx = max(mx, (uint64_t)__shfl_xor_sync(0xffffffffu, mx, o));
             }
             if ((threadIdx.x & 31) == 0 && mn != mx) atomicOr(flag, 256u);
+            __syncthreads();  // every thread has read the counts
+            if (threadIdx.x == 0) reinterpret_cast<uint2*>(cnt)[i] = make_uint2(0u, 0u);
             continue;
         }
         int np2 = 1;
@@ -415,7 +447,8 @@ __global__ void __launch_bounds__(256) k_rdb_finish(const uint64_t* __restrict__
             best = v > best ? v : best;
         }
         if ((threadIdx.x & 31) == 0 && best) atomicMax(&cnum[s], (unsigned long long)best);
-        __syncthreads();  // sk is reused by the next bucket
+        __syncthreads();  // sk is reused by the next bucket; every thread has read the counts
+        if (threadIdx.x == 0) reinterpret_cast<uint2*>(cnt)[i] = make_uint2(0u, 0u);  // clean for the next call
     }
 }
 

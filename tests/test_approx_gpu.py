@@ -178,6 +178,24 @@ def test_rdks_ties_and_edges(ctx):
     assert e.value.status == 4
 
 
+def test_rdks_count_buffer_reuse():
+    # the sweep re-zeroes every bucket count it reads (k_rdb_cand / k_rdb_finish), so a completed call leaves the
+    # count buffer clean and the next call skips its memset over the known-zero prefix; a larger call must still
+    # zero the rest, and a call that falls back to the full sort (flag 256) must leave the buffer marked dirty
+    rng = np.random.default_rng(7)
+    Pf = np.concatenate([rng.random((200, 2)), 0.5 + 1e-4 * rng.random((10000, 2))]).astype(np.float32)
+    Qf = np.concatenate([rng.random((300, 2)), 0.5 + 1e-4 * rng.random((9000, 2)) + 2e-5]).astype(np.float32)
+    Pf[0], Qf[0] = 0.0, 1.0
+    cases = [I.random_pair(81, 3000, 2000, 3, "normal"), I.random_pair(82, 40000, 30000, 2, "mixed"),
+             (Pf, Qf), I.random_pair(83, 9000, 11000, 4, "dup"), I.random_pair(84, 500, 700, 5, "grid")]
+    want = [O.rdks(P, Q) for P, Q in cases]
+    with K.Context() as c:
+        for _ in range(2):
+            for (P, Q), w in zip(cases, want):
+                got = c.rdks(dev(P), dev(Q))
+                assert (got.num, got.den, got.argmax_origin) == (w[0], w[1], w[3]), (got, w)
+
+
 @pytest.mark.parametrize("name", ["C2", "C3", "C5"])
 def test_rdks_configs_full(ctx, name):
     # full-size parity: the oracle's rdKS is O((d+1) N log N) too, so it runs on whole BASELINE configs
