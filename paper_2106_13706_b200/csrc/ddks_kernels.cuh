@@ -45,6 +45,9 @@ template <int D> struct Cfg;
 #define DDKS_UNROLL 8
 #endif
 constexpr int kUnrollPts = DDKS_UNROLL;
+#ifndef DDKS_R1_PTS  // points per step of the R == 1 inner loop (d = 8)
+#define DDKS_R1_PTS 2
+#endif
 #ifndef DDKS_UNROLL_PARTIAL  // the same for the kd variants that compare some of the first KX dims (colder code)
 #define DDKS_UNROLL_PARTIAL DDKS_UNROLL
 #endif
@@ -75,7 +78,10 @@ template <> struct Cfg<7> { static constexpr int R = 2, T = 384, TILE = 256, S =
 #define DDKS_C8R 1
 #define DDKS_C8T 384
 #endif
-template <> struct Cfg<8> { static constexpr int R = DDKS_C8R, T = DDKS_C8T, TILE = 256, S = 3; };
+#ifndef DDKS_C8TILE
+#define DDKS_C8TILE 256
+#endif
+template <> struct Cfg<8> { static constexpr int R = DDKS_C8R, T = DDKS_C8T, TILE = DDKS_C8TILE, S = 3; };
 
 
 // SPLIT (c_P and c_Q kept apart) doubles the bins: halve R (keeping it even or 1), or T when R is already <= 2
@@ -403,7 +409,7 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
                                              uint32_t inc_hi, uint32_t hbytes) {
     if (lo >= hi) return;
     int p = lo;
-    // prefetches read at most two points past hi <= TILE: still inside the SMEM allocation (the next stage or the
+    // prefetches read at most PPS (<= 4) points past hi <= TILE: still inside the SMEM allocation (the next stage or the
     // counters), and the values are never used
 #ifndef DDKS_NO_ONEDIM
     if constexpr (KX > 0 && UM == 0 && n_cmp<D, KX, UM>() == 1 && R >= 2) {
@@ -437,35 +443,42 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
     }
 #endif
     if constexpr (R <= 2) {
-        float na[D], nb[D];
-        load_point<D>(tile + p * DP, na);
-        load_point<D>(tile + (p + 1) * DP, nb);
+        // PPS points per step (R == 1: DDKS_R1_PTS), the next PPS loaded before this step's compares: a warp has
+        // PPS * R independent address chains in flight
+        constexpr int PPS = R == 1 ? DDKS_R1_PTS : 2;
+        float nx[PPS][D];
+#pragma unroll
+        for (int j = 0; j < PPS; ++j) load_point<D>(tile + (p + j) * DP, nx[j]);
 #pragma unroll 4
-        for (; p + 1 < hi; p += 2) {
-            float xa[D], xb[D];
+        for (; p + PPS - 1 < hi; p += PPS) {
+            float x[PPS][D];
 #pragma unroll
-            for (int k = 0; k < D; ++k) xa[k] = na[k], xb[k] = nb[k];
-            load_point<D>(tile + (p + 2) * DP, na);
-            load_point<D>(tile + (p + 3) * DP, nb);
-            float fa[R], fb[R];
+            for (int j = 0; j < PPS; ++j)
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                // two points in flight already give 2R independent chains: no chain split
-                fa[r] = code_addr<D, GT, WPB, KX, UM, false>(xa, o[r], base[r % NB_]);
-                fb[r] = code_addr<D, GT, WPB, KX, UM, false>(xb, o[r], base[r % NB_]);
-            }
+                for (int k = 0; k < D; ++k) x[j][k] = nx[j][k];
+#pragma unroll
+            for (int j = 0; j < PPS; ++j) load_point<D>(tile + (p + PPS + j) * DP, nx[j]);
+            float f[PPS][R];
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int j = 0; j < PPS; ++j)  // PPS points in flight already give independent chains: no split
+                    f[j][r] = code_addr<D, GT, WPB, KX, UM, false>(x[j], o[r], base[r % NB_]);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const uint32_t inc = (R >= 2 && r < RP) ? inc_lo : inc_hi;
-                red_counter(fa[r], ubase, inc, hbytes);
-                red_counter(fb[r], ubase, inc, hbytes);
+#pragma unroll
+                for (int j = 0; j < PPS; ++j) red_counter(f[j][r], ubase, inc, hbytes);
             }
         }
-        if (p < hi) {
 #pragma unroll
-            for (int r = 0; r < R; ++r)
-                red_counter(code_addr<D, GT, WPB, KX, UM>(na, o[r], base[r % NB_]), ubase,
-                            (R >= 2 && r < RP) ? inc_lo : inc_hi, hbytes);
+        for (int j = 0; j < PPS - 1; ++j) {
+            if (p + j < hi) {
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    red_counter(code_addr<D, GT, WPB, KX, UM>(nx[j], o[r], base[r % NB_]), ubase,
+                                (R >= 2 && r < RP) ? inc_lo : inc_hi, hbytes);
+            }
         }
         return;
     }
