@@ -335,7 +335,7 @@ ddks_status launch_pack(ddks_ctx* ctx, const float* P, int64_t n_P, const float*
 // count can decide bit 0 per warp (*wx = true); otherwise the plain pack.
 ddks_status launch_pack_batch(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int d,
                               int64_t B, float* dst, uint32_t* flag, cudaStream_t st, bool* wx) {
-    *wx = d >= 2 && n_P <= 2 * ddks::KPS_T && n_Q <= 2 * ddks::KPS_T && B <= 0x7fffffff &&
+    *wx = d >= 2 && n_P <= ddks::KPS_T * ddks::KPS_R && n_Q <= ddks::KPS_T * ddks::KPS_R && B <= 0x7fffffff &&
           !(ctx->flags & (DDKS_FLAG_TIES_GT | DDKS_FLAG_NO_X0));
     if (!*wx) return launch_pack(ctx, P, n_P, Q, n_Q, d, B, dst, flag, st);
     ddks::k_pack_sorted<<<dim3((unsigned)B, 2), ddks::KPS_T, 0, st>>>(P, n_P, Q, n_Q, d, dst, pad_dim(d),

@@ -167,11 +167,16 @@ __global__ void k_pack(const float* __restrict__ P, int64_t n_P, const float* __
 }
 
 // a1 for batches of small items, rows of every (item, label) run ordered by x_0 (for k_count<WX>): one CTA of KPS_T
-// threads per run of n <= 2 KPS_T rows. The order only has to be close to sorted (it changes speed, never counts):
+// threads per run of n <= KPS_T KPS_R rows. The order only has to be close to sorted (it changes speed, never counts):
 // a one-pass bucket sort into 256 equal-width x_0 buckets between the run's min and max (SMEM histogram, scan,
 // atomic slots), then the rows are written in bucket order (validated, -0 -> +0, pad dims = 0). Row order inside a
 // label run does not change the statistic.
-constexpr int KPS_T = 512;
+// Small CTAs (KPS_T threads, up to KPS_R rows each) so that ~16 runs are resident per SM: the kernel is a chain of
+// block barriers per run, latency-bound with one row per thread of 512-thread CTAs (C4: 54 us for 8192 runs).
+#ifndef DDKS_KPS_T  // experiments: threads per run (KPS_T * KPS_R must stay 1024)
+#define DDKS_KPS_T 128
+#endif
+constexpr int KPS_T = DDKS_KPS_T, KPS_R = 1024 / KPS_T;  // n <= KPS_T * KPS_R = 1024 rows per run
 __global__ void __launch_bounds__(KPS_T) k_pack_sorted(const float* __restrict__ P, int64_t n_P,
                                                        const float* __restrict__ Q, int64_t n_Q, int d,
                                                        float* __restrict__ dst, int DP, int validate, uint32_t* flag) {
@@ -185,16 +190,18 @@ __global__ void __launch_bounds__(KPS_T) k_pack_sorted(const float* __restrict__
     float* out = dst + (b * (n_P + n_Q) + (lab ? n_P : 0)) * DP;
     const int t = threadIdx.x;
     for (int i = t; i < NBK; i += KPS_T) cnt[i] = 0u;
-    // this thread's (up to two) rows: x_0 and the run's min / max (non-finite values are flagged below and excluded
-    // from the range so the bucket arithmetic stays finite)
-    float x[2];
+    // x_0 of this thread's rows (all loads in flight) and the run's min / max (non-finite values are flagged below and
+    // excluded from the range so the bucket arithmetic stays finite)
+    float x[KPS_R];
     float lo = INFINITY, hi = -INFINITY;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < KPS_R; ++k) {
         const int i = t + k * KPS_T;
         x[k] = i < n ? src[(int64_t)i * d] : 0.0f;
-        if (i < n && isfinite(x[k])) lo = fminf(lo, x[k]), hi = fmaxf(hi, x[k]);
     }
+#pragma unroll
+    for (int k = 0; k < KPS_R; ++k)
+        if (t + k * KPS_T < n && isfinite(x[k])) lo = fminf(lo, x[k]), hi = fmaxf(hi, x[k]);
 #pragma unroll
     for (int sh = 16; sh; sh >>= 1) {
         lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, sh));
@@ -203,16 +210,16 @@ __global__ void __launch_bounds__(KPS_T) k_pack_sorted(const float* __restrict__
     if ((t & 31) == 0) red[0][t >> 5] = lo, red[1][t >> 5] = hi;
     __syncthreads();
     lo = red[0][0], hi = red[1][0];
+#pragma unroll
     for (int w = 1; w < KPS_T / 32; ++w) lo = fminf(lo, red[0][w]), hi = fmaxf(hi, red[1][w]);
     const float scale = hi > lo ? (float)NBK / (hi - lo) : 0.0f;
-    int bk[2], rk[2];
+    uint32_t slot[KPS_R];  // bucket << 16 | rank inside the bucket
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const int i = t + k * KPS_T;
-        if (i < n) {
+    for (int k = 0; k < KPS_R; ++k) {
+        if (t + k * KPS_T < n) {
             const float v = isfinite(x[k]) ? (x[k] - lo) * scale : 0.0f;
-            bk[k] = v >= (float)(NBK - 1) ? NBK - 1 : (v > 0.0f ? (int)v : 0);
-            rk[k] = (int)atomicAdd(&cnt[bk[k]], 1u);
+            const int bk = v >= (float)(NBK - 1) ? NBK - 1 : (v > 0.0f ? (int)v : 0);
+            slot[k] = ((uint32_t)bk << 16) | atomicAdd(&cnt[bk], 1u);
         }
     }
     __syncthreads();
@@ -231,20 +238,28 @@ __global__ void __launch_bounds__(KPS_T) k_pack_sorted(const float* __restrict__
         for (int j = 0; j < NBK / 32; ++j) cnt[t * (NBK / 32) + j] = off, off += v[j];
     }
     __syncthreads();
+    // whole rows (re-read: L1 / L2 hits; one 16-byte load when d == 4 and aligned) -> validated, -0 -> +0, pad = 0
+    const bool vec4 = d == 4 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0;
     bool bad = false;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < KPS_R; ++k) {
         const int i = t + k * KPS_T;
         if (i >= n) continue;
         const float* s = src + (int64_t)i * d;
         float v[8];
+        if (vec4) {
+            const float4 q = *reinterpret_cast<const float4*>(s);
+            v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w, v[4] = v[5] = v[6] = v[7] = 0.0f;
+        } else {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) v[m] = (m < d) ? s[m] : 0.0f;
+        }
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
-            const float u = (m < d) ? s[m] : 0.0f;
-            if (m < d && validate && !isfinite(u)) bad = true;
-            v[m] = (u == 0.0f) ? 0.0f : u;
+            if (m < d && validate && !isfinite(v[m])) bad = true;
+            v[m] = (v[m] == 0.0f) ? 0.0f : v[m];
         }
-        const int dstrow = (int)cnt[bk[k]] + rk[k];
+        const int dstrow = (int)cnt[slot[k] >> 16] + (int)(slot[k] & 0xffffu);
         DDKS_ASSERT(dstrow < n);
         float4* o = reinterpret_cast<float4*>(out + (int64_t)dstrow * DP);
         o[0] = make_float4(v[0], v[1], v[2], v[3]);
