@@ -695,8 +695,10 @@ ddks_status ddks_destroy(ddks_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     if (ctx->sg_exec) cudaGraphExecDestroy(ctx->sg_exec);
+    for (auto* cg : {&ctx->cg_batch, &ctx->cg_null})
+        if (cg->exec) cudaGraphExecDestroy(cg->exec);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
-    for (auto* v : {&ctx->ev_free, &ctx->sg_evs})
+    for (auto* v : {&ctx->ev_free, &ctx->sg_evs, &ctx->cg_batch.evs, &ctx->cg_null.evs})
         for (auto& e : *v) {
             cudaEventDestroy(e.first);
             cudaEventDestroy(e.second);
@@ -713,7 +715,7 @@ ddks_status ddks_destroy(ddks_ctx* ctx) {
                       &ctx->rd_k1, &ctx->rd_hist, &ctx->rd_tcnt, &ctx->rd_cnum, &ctx->x0_keys0,
                       &ctx->x0_keys1, &ctx->x0_hist, &ctx->x0_pts, &ctx->x0_perm, &ctx->x0_pts2,
                       &ctx->x0_perm2, &ctx->x0_boxes, &ctx->prof_clk, &ctx->rdb_cnt,
-                      &ctx->rdb_pst, &ctx->rdb_coff, &ctx->rdb_fill, &ctx->rdb_clist, &ctx->rdb_csum})
+                      &ctx->rdb_pst, &ctx->rdb_coff, &ctx->rdb_fill, &ctx->rdb_clist, &ctx->rdb_csum, &ctx->rdb_bits})
         if (b->p) cudaFree(b->p);
     if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
     delete ctx;
@@ -810,7 +812,7 @@ static ddks_status launch_small_d(ddks_ctx* ctx, const ddks::SmallArgs& a, int s
 // Enqueue the fused small-N statistic: one cluster launch whose leaders write per-origin-block records into the pinned
 // host buffer (reduced by stat_impl after the sync). No result initialisation, no copy: the call is one graph node.
 static ddks_status small_enqueue(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q, int64_t n_Q, int32_t d,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, void* host_rec = nullptr) {
     ddks_status s;
     const int64_t N = n_P + n_Q;
     const void *dP, *dQ;
@@ -834,7 +836,7 @@ static ddks_status small_enqueue(ddks_ctx* ctx, const float* P, int64_t n_P, con
     a.validate = (ctx->flags & DDKS_FLAG_NO_VALIDATE) ? 0 : 1;
     // the leaders write their records straight into the context's pinned host buffer (zero-copy: no D2H node)
     void* hdev = nullptr;
-    CU(cudaHostGetDevicePointer(&hdev, ctx->host_pinned, 0));
+    CU(cudaHostGetDevicePointer(&hdev, host_rec ? host_rec : ctx->host_pinned, 0));
     a.out = (unsigned long long*)hdev;
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
     if (ctx->flags & DDKS_FLAG_PROFILE) {
@@ -972,6 +974,92 @@ static ddks_status stat_capture(ddks_ctx* ctx, const ddks_ctx::StatKey& key, con
     return DDKS_OK;
 }
 
+// environment overrides (tuning / test knobs) change the plan: a graph captured under other values is not reused
+static bool env_overrides() {
+    return getenv("DDKS_KD") || getenv("DDKS_SEGS") || getenv("DDKS_KD_SHUFFLE") || getenv("DDKS_NO_KEY") ||
+           getenv("DDKS_GRIDY") || getenv("DDKS_NO_SMALL") || getenv("DDKS_KD_RADIX") || getenv("DDKS_NO_MMA") ||
+           getenv("DDKS_PERM_GROUP");
+}
+
+static void drop_call_graph(ddks_ctx* ctx, ddks_ctx::CallGraph& cg) {
+    if (cg.exec) cudaGraphExecDestroy(cg.exec);
+    cg.exec = nullptr;
+    cg.key.clear();
+    for (auto& e : cg.evs) ctx->ev_free.push_back(e);
+    cg.evs.clear();
+    cg.ev_pairs.clear();
+}
+
+static void launch_call_graph(ddks_ctx* ctx, ddks_ctx::CallGraph& cg, cudaStream_t st, cudaError_t* e) {
+    *e = cudaGraphLaunch(cg.exec, st);
+    ctx->launches += cg.launches;
+    for (size_t i = 0; i < cg.evs.size(); ++i) {
+        ctx->ev_pending.push_back(cg.evs[i]);
+        ctx->ev_pairs.push_back(cg.ev_pairs[i]);
+        ctx->ev_recycle.push_back(0);
+    }
+}
+
+// Run the stream-ordered part of a C-ABI call (enq: staging, kernels, collectives, the D2H into host_pinned; no sync)
+// through a per-call-shape CUDA graph: the second call with the same key (pointers, sizes, flags; + the workspace
+// epoch) is captured on the context's capture stream and every identical call after it is one cudaGraphLaunch on st.
+// Not graphable (host inputs in pageable memory, DDKS_FLAG_NO_GRAPH, environment overrides): enq runs on st.
+extern "C++" {
+template <class F>
+ddks_status run_call(ddks_ctx* ctx, ddks_ctx::CallGraph& cg, std::vector<uint64_t> key, bool graphable,
+                            cudaStream_t st, F&& enq) {
+    graphable = graphable && !(ctx->flags & DDKS_FLAG_NO_GRAPH) && !env_overrides();
+    key.push_back(ctx->alloc_epoch);
+    cudaError_t e;
+    if (graphable && cg.exec && cg.key == key) {
+        launch_call_graph(ctx, cg, st, &e);
+        CU(e);
+        return DDKS_OK;
+    }
+    if (graphable && cg.seen == key) {
+        drop_call_graph(ctx, cg);
+        if (!ctx->cap_stream) CU(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+        const size_t ev0 = ctx->ev_pending.size();
+        const int64_t l0 = ctx->launches;
+        CU(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed));
+        const ddks_status s = enq(ctx->cap_stream);
+        cudaGraph_t g = nullptr;
+        e = cudaStreamEndCapture(ctx->cap_stream, &g);
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs(ctx->ev_pending.begin() + ev0, ctx->ev_pending.end());
+        std::vector<uint64_t> pairs(ctx->ev_pairs.begin() + ev0, ctx->ev_pairs.end());
+        ctx->ev_pending.resize(ev0);
+        ctx->ev_pairs.resize(ev0);
+        ctx->ev_recycle.resize(ev0);
+        const int64_t nl = ctx->launches - l0;
+        ctx->launches = l0;
+        cudaGraphExec_t ex = nullptr;
+        const bool good = s == DDKS_OK && e == cudaSuccess && g && ctx->alloc_epoch == key.back() &&
+                          cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+        if (g) cudaGraphDestroy(g);
+        if (good) {
+            cg.exec = ex;
+            cg.key = key;
+            cg.launches = nl;
+            cg.evs = evs;
+            cg.ev_pairs = pairs;
+            launch_call_graph(ctx, cg, st, &e);
+            CU(e);
+            return DDKS_OK;
+        }
+        cudaGetLastError();  // capture refused or the workspace moved: run uncaptured
+        for (auto& v : evs) ctx->ev_free.push_back(v);
+        ctx->err.clear();
+    }
+    ddks_status s = enq(st);
+    if (s) return s;
+    if (graphable) {  // a second identical call (same workspace) will be captured
+        cg.seen = key;
+        cg.seen.back() = ctx->alloc_epoch;
+    }
+    return DDKS_OK;
+}
+}  // extern "C++"
+
 // a1-a7 for one pair, origins sharded across ranks; optional per-origin export (debug path, single rank).
 // shard_world > 0: compute only the origin shard that rank shard_rank of shard_world would own (ddks_stat_shard).
 // Repeated identical ddks_stat calls (same input pointers and sizes, same workspace) are captured into a CUDA graph
@@ -1002,9 +1090,7 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
     // the fused small-N path (whole statistic, single rank): one record per origin block
     const bool small = !export_mode && shard_world == 0 && small_fused_applies(ctx, n_P, n_Q);
     // environment overrides (tuning / test knobs) change the plan: a graph captured under other values is not reused
-    const bool env_override = getenv("DDKS_KD") || getenv("DDKS_SEGS") || getenv("DDKS_KD_SHUFFLE") ||
-                              getenv("DDKS_NO_KEY") || getenv("DDKS_GRIDY") || getenv("DDKS_NO_SMALL") ||
-                              getenv("DDKS_KD_RADIX");
+    const bool env_override = env_overrides();
     const bool graphable = !export_mode && shard_world == 0 && !(ctx->flags & DDKS_FLAG_NO_GRAPH) && !env_override &&
                            graph_input_ok(P) && graph_input_ok(Q);
     const ddks_ctx::StatKey key{P, Q, n_P, n_Q, d, ctx->alloc_epoch};
@@ -1107,38 +1193,49 @@ ddks_status ddks_stat_batch(ddks_ctx* ctx, const float* P, const float* Q, int64
     const int DP = pad_dim(d);
     int64_t ib, ie;
     ddks_shard_range(B, ctx->world, ctx->rank, &ib, &ie);
-    const void *dP, *dQ;
-    if ((s = stage_input(ctx, P, (size_t)B * n_P * d * 4, ctx->raw_a, st, &dP))) return s;
-    if ((s = stage_input(ctx, Q, (size_t)B * n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
-    if ((s = ensure(ctx, ctx->item_num, (size_t)B * 8))) return s;
-    uint64_t* nums = (uint64_t*)ctx->item_num.p;
-    CU(cudaMemsetAsync(nums, 0, (size_t)B * 8, st));
-    DevResult* dres = (DevResult*)ctx->res.p;
-    CU(cudaMemsetAsync(dres, 0, sizeof(DevResult), st));
-    const int64_t nb = ie - ib;
-    if (nb > 0) {
-        if ((s = ensure(ctx, ctx->packed, (size_t)nb * N * DP * 4))) return s;
-        float* packed = (float*)ctx->packed.p;
-        bool wx = false;
-        if ((s = launch_pack_batch(ctx, (const float*)dP + ib * n_P * d, n_P, (const float*)dQ + ib * n_Q * d, n_Q, d,
-                                   nb, packed, &dres->flag, st, &wx)))
-            return s;
-        if ((s = run_count(ctx, packed, d, nb, n_P, n_Q, 0, N, nums + ib, nullptr, st, false, nullptr, wx))) return s;
-    }
-    // world > 1: one all-gather of the padded per-rank records (this rank's nums + its flags), unpadded on the host
     const int64_t gstride = ctx->comm ? gather_stride(B, ctx->world, 1) : 0;
-    if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)B * 8 + (size_t)ctx->world * gstride * 8))) return s;
+    auto enq = [&](cudaStream_t st) -> ddks_status {
+        ddks_status s;
+        const void *dP, *dQ;
+        if ((s = stage_input(ctx, P, (size_t)B * n_P * d * 4, ctx->raw_a, st, &dP))) return s;
+        if ((s = stage_input(ctx, Q, (size_t)B * n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
+        if ((s = ensure(ctx, ctx->item_num, (size_t)B * 8))) return s;
+        uint64_t* nums = (uint64_t*)ctx->item_num.p;
+        CU(cudaMemsetAsync(nums, 0, (size_t)B * 8, st));
+        DevResult* dres = (DevResult*)ctx->res.p;
+        CU(cudaMemsetAsync(dres, 0, sizeof(DevResult), st));
+        const int64_t nb = ie - ib;
+        if (nb > 0) {
+            if ((s = ensure(ctx, ctx->packed, (size_t)nb * N * DP * 4))) return s;
+            float* packed = (float*)ctx->packed.p;
+            bool wx = false;
+            if ((s = launch_pack_batch(ctx, (const float*)dP + ib * n_P * d, n_P, (const float*)dQ + ib * n_Q * d, n_Q,
+                                       d, nb, packed, &dres->flag, st, &wx)))
+                return s;
+            if ((s = run_count(ctx, packed, d, nb, n_P, n_Q, 0, N, nums + ib, nullptr, st, false, nullptr, wx)))
+                return s;
+        }
+        // world > 1: one all-gather of the padded per-rank records (this rank's nums + its flags), unpadded on the
+        // host
+        if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)B * 8 + (size_t)ctx->world * gstride * 8))) return s;
+        DevResult* hres = (DevResult*)ctx->host_pinned;
+        uint64_t* hnums = (uint64_t*)((char*)ctx->host_pinned + sizeof(DevResult));
+        if (ctx->comm) {
+            uint64_t* arrs[1] = {nums};
+            if ((s = gather_items(ctx, arrs, 1, B, &dres->flag, st, hnums + B))) return s;
+        } else {
+            CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+            CU(cudaMemcpyAsync(hnums, nums, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
+        }
+        return DDKS_OK;
+    };
+    const std::vector<uint64_t> key{(uint64_t)(uintptr_t)P, (uint64_t)(uintptr_t)Q, (uint64_t)B, (uint64_t)n_P,
+                                    (uint64_t)n_Q, (uint64_t)d, (uint64_t)ctx->flags};
+    if ((s = run_call(ctx, ctx->cg_batch, key, graph_input_ok(P) && graph_input_ok(Q), st, enq))) return s;
+    CU(cudaStreamSynchronize(st));
     DevResult* hres = (DevResult*)ctx->host_pinned;
     uint64_t* hnums = (uint64_t*)((char*)ctx->host_pinned + sizeof(DevResult));
     uint64_t* hgath = hnums + B;
-    if (ctx->comm) {
-        uint64_t* arrs[1] = {nums};
-        if ((s = gather_items(ctx, arrs, 1, B, &dres->flag, st, hgath))) return s;
-    } else {
-        CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
-        CU(cudaMemcpyAsync(hnums, nums, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
-    }
-    CU(cudaStreamSynchronize(st));
     if ((s = collect_profile(ctx))) return s;
     if (ctx->comm) ddks_unpad_items(hgath, B, ctx->world, 1, hnums, &hres->flag);
     if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
@@ -1164,84 +1261,120 @@ ddks_status ddks_permutation_null(ddks_ctx* ctx, const float* pooled, int64_t n_
     if ((s = bind_device(ctx))) return s;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t N = n_P + n_Q;
-    const int DP = pad_dim(d);
-    const void *dpool, *dperm = nullptr;
-    if ((s = stage_input(ctx, pooled, (size_t)N * d * 4, ctx->raw_a, st, &dpool))) return s;
-    if (n_perm > 0 && (s = stage_input(ctx, perms, (size_t)n_perm * N * 4, ctx->raw_perm, st, &dperm))) return s;
     // slot 0 = observed (identity split), slots 1..n_perm = permutations
     const int64_t total = n_perm + 1;
-    if ((s = ensure(ctx, ctx->item_num, (size_t)total * 8))) return s;
-    uint64_t* nums = (uint64_t*)ctx->item_num.p;
-    CU(cudaMemsetAsync(nums, 0, (size_t)total * 8, st));
-    DevResult* dres = (DevResult*)ctx->res.p;
-    CU(cudaMemsetAsync(dres, 0, sizeof(DevResult), st));
-    // pack the pooled sample once: [N][DP], rows up to a multiple of the tensor-core null's k-block zeroed
-    const int64_t N_pad = (N + ddks::PM_KB - 1) / ddks::PM_KB * ddks::PM_KB;
-    if ((s = ensure(ctx, ctx->pool_packed, (size_t)N_pad * DP * 4))) return s;
-    float* pooled_packed = (float*)ctx->pool_packed.p;
-    if (N_pad > N) CU(cudaMemsetAsync(pooled_packed + N * DP, 0, (size_t)(N_pad - N) * DP * 4, st));
-    if ((s = launch_pack(ctx, (const float*)dpool, n_P, (const float*)dpool + n_P * d, n_Q, d, 1, pooled_packed,
-                         &dres->flag, st)))
-        return s;
-    // observed: every rank computes it (cheap relative to the null), no collective needed
-    if ((s = run_count(ctx, pooled_packed, d, 1, n_P, n_Q, 0, N, nums, nullptr, st))) return s;
-    int64_t jb, je;
-    ddks_shard_range(n_perm, ctx->world, ctx->rank, &jb, &je);
-    const bool label_path = N <= 65535 && !(ctx->flags & DDKS_FLAG_PERM_GATHER);
-    if (label_path) {
-        auto fn = perm_mma_applies(ctx, d, N) ? launch_perm_mma : launch_perm;
-        // permutations in groups whose label images / counters and validation bitmaps stay within ~256 MB (about
-        // 1.5 N bytes per permutation; DDKS_PERM_GROUP, test only, overrides the group size)
-        int64_t grp = std::max<int64_t>(768, ((256ll << 20) / (3 * N / 2 + 1)) / 768 * 768);
-        if (const char* e = getenv("DDKS_PERM_GROUP")) grp = std::max(1, atoi(e));
-        for (int64_t j0 = jb; j0 < je; j0 += grp) {
-            const int64_t nj = std::min(grp, je - j0);
-            if ((s = fn(ctx, d, pooled_packed, (const int32_t*)dperm + j0 * N, nj, n_P, n_Q, nums + 1 + j0, &dres->flag,
-                        st)))
-                return s;
-        }
-    } else {
-        const int64_t chunk_max = std::max<int64_t>(1, (int64_t)((256ull << 20) / ((size_t)N * DP * 4)));
-        for (int64_t j0 = jb; j0 < je; j0 += chunk_max) {
-            const int64_t nc = std::min(chunk_max, je - j0);
-            if ((s = ensure(ctx, ctx->packed, (size_t)nc * N * DP * 4))) return s;
-            const int64_t words = (N + 31) / 32;
-            if ((s = ensure(ctx, ctx->bitmap, (size_t)nc * words * 4))) return s;
-            CU(cudaMemsetAsync(ctx->bitmap.p, 0, (size_t)nc * words * 4, st));
-            const int64_t tot = nc * N;
-            const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
-            if (DP == 4)
-                ddks::k_gather<4><<<blocks, 256, 0, st>>>(pooled_packed, (const int32_t*)dperm + j0 * N, nc, N,
-                                                          (float*)ctx->packed.p, (uint32_t*)ctx->bitmap.p, &dres->flag);
-            else
-                ddks::k_gather<8><<<blocks, 256, 0, st>>>(pooled_packed, (const int32_t*)dperm + j0 * N, nc, N,
-                                                          (float*)ctx->packed.p, (uint32_t*)ctx->bitmap.p, &dres->flag);
-            CHECK_LAUNCH();
-            ctx->launches++;
-            if ((s = run_count(ctx, (const float*)ctx->packed.p, d, nc, n_P, n_Q, 0, N, nums + 1 + j0, nullptr, st)))
-                return s;
-        }
-    }
-    // world > 1: the observed num (slot 0) is every rank's own; one all-gather of the padded per-rank records (this
-    // rank's permutation nums + its flags), unpadded on the host
     const int64_t gstride = ctx->comm ? gather_stride(n_perm, ctx->world, 1) : 0;
-    if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)total * 8 + (size_t)ctx->world * gstride * 8))) return s;
+    const bool obs_small = small_fused_applies(ctx, n_P, n_Q);
+    const int64_t nsrec = obs_small ? small_blocks(N) : 0;
+    const int DP = pad_dim(d);
+    auto enq = [&](cudaStream_t st) -> ddks_status {
+        ddks_status s;
+        const void *dpool, *dperm = nullptr;
+        if ((s = stage_input(ctx, pooled, (size_t)N * d * 4, ctx->raw_a, st, &dpool))) return s;
+        if (n_perm > 0 && (s = stage_input(ctx, perms, (size_t)n_perm * N * 4, ctx->raw_perm, st, &dperm))) return s;
+        if ((s = ensure(ctx, ctx->item_num, (size_t)total * 8))) return s;
+        uint64_t* nums = (uint64_t*)ctx->item_num.p;
+        CU(cudaMemsetAsync(nums, 0, (size_t)total * 8, st));
+        DevResult* dres = (DevResult*)ctx->res.p;
+        CU(cudaMemsetAsync(dres, 0, sizeof(DevResult), st));
+        // pack the pooled sample once: [N][DP], rows up to a multiple of the tensor-core null's k-block zeroed
+        const int64_t N_pad = (N + ddks::PM_KB - 1) / ddks::PM_KB * ddks::PM_KB;
+        if ((s = ensure(ctx, ctx->pool_packed, (size_t)N_pad * DP * 4))) return s;
+        float* pooled_packed = (float*)ctx->pool_packed.p;
+        if (N_pad > N) CU(cudaMemsetAsync(pooled_packed + N * DP, 0, (size_t)(N_pad - N) * DP * 4, st));
+        if ((s = launch_pack(ctx, (const float*)dpool, n_P, (const float*)dpool + n_P * d, n_Q, d, 1, pooled_packed,
+                             &dres->flag, st)))
+            return s;
+        // pinned host layout: result record, total nums, the all-gathered rank records (world > 1), and the fused small
+        // statistic's per-origin-block records (allocated before anything is enqueued: the small kernel writes there)
+        if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)(total + (size_t)ctx->world * gstride + 4 * nsrec) * 8)))
+            return s;
+        unsigned long long* hsrec =
+            (unsigned long long*)((char*)ctx->host_pinned + sizeof(DevResult)) + total + (size_t)ctx->world * gstride;
+        // observed: every rank computes it (cheap relative to the null), no collective needed; at small N (single rank)
+        // the fused cluster kernel on the raw halves of the pooled sample (its records land in hsrec, combined below)
+        if (obs_small) {
+            if ((s = small_enqueue(ctx, (const float*)dpool, n_P, (const float*)dpool + n_P * d, n_Q, d, st, hsrec))) return s;
+        } else if ((s = run_count(ctx, pooled_packed, d, 1, n_P, n_Q, 0, N, nums, nullptr, st))) {
+            return s;
+        }
+        int64_t jb, je;
+        ddks_shard_range(n_perm, ctx->world, ctx->rank, &jb, &je);
+        const bool label_path = N <= 65535 && !(ctx->flags & DDKS_FLAG_PERM_GATHER);
+        if (label_path) {
+            auto fn = perm_mma_applies(ctx, d, N) ? launch_perm_mma : launch_perm;
+            // permutations in groups whose label images / counters and validation bitmaps stay within ~256 MB (about
+            // 1.5 N bytes per permutation; DDKS_PERM_GROUP, test only, overrides the group size)
+            int64_t grp = std::max<int64_t>(768, ((256ll << 20) / (3 * N / 2 + 1)) / 768 * 768);
+            if (const char* e = getenv("DDKS_PERM_GROUP")) grp = std::max(1, atoi(e));
+            for (int64_t j0 = jb; j0 < je; j0 += grp) {
+                const int64_t nj = std::min(grp, je - j0);
+                if ((s = fn(ctx, d, pooled_packed, (const int32_t*)dperm + j0 * N, nj, n_P, n_Q, nums + 1 + j0, &dres->flag,
+                            st)))
+                    return s;
+            }
+        } else {
+            const int64_t chunk_max = std::max<int64_t>(1, (int64_t)((256ull << 20) / ((size_t)N * DP * 4)));
+            for (int64_t j0 = jb; j0 < je; j0 += chunk_max) {
+                const int64_t nc = std::min(chunk_max, je - j0);
+                if ((s = ensure(ctx, ctx->packed, (size_t)nc * N * DP * 4))) return s;
+                const int64_t words = (N + 31) / 32;
+                if ((s = ensure(ctx, ctx->bitmap, (size_t)nc * words * 4))) return s;
+                CU(cudaMemsetAsync(ctx->bitmap.p, 0, (size_t)nc * words * 4, st));
+                const int64_t tot = nc * N;
+                const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
+                if (DP == 4)
+                    ddks::k_gather<4><<<blocks, 256, 0, st>>>(pooled_packed, (const int32_t*)dperm + j0 * N, nc, N,
+                                                              (float*)ctx->packed.p, (uint32_t*)ctx->bitmap.p, &dres->flag);
+                else
+                    ddks::k_gather<8><<<blocks, 256, 0, st>>>(pooled_packed, (const int32_t*)dperm + j0 * N, nc, N,
+                                                              (float*)ctx->packed.p, (uint32_t*)ctx->bitmap.p, &dres->flag);
+                CHECK_LAUNCH();
+                ctx->launches++;
+                if ((s = run_count(ctx, (const float*)ctx->packed.p, d, nc, n_P, n_Q, 0, N, nums + 1 + j0, nullptr, st)))
+                    return s;
+            }
+        }
+        // world > 1: the observed num (slot 0) is every rank's own; one all-gather of the padded per-rank records (this
+        // rank's permutation nums + its flags), unpadded on the host
+        DevResult* hres = (DevResult*)ctx->host_pinned;
+        uint64_t* hnums = (uint64_t*)((char*)ctx->host_pinned + sizeof(DevResult));
+        uint64_t* hgath = hnums + total;
+        if (ctx->comm) {
+            uint64_t* arrs[1] = {nums + 1};
+            if ((s = gather_items(ctx, arrs, 1, n_perm, &dres->flag, st, hgath))) return s;
+            CU(cudaMemcpyAsync(hnums, nums, 8, cudaMemcpyDeviceToHost, st));
+        } else {
+            CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+            CU(cudaMemcpyAsync(hnums, nums, (size_t)total * 8, cudaMemcpyDeviceToHost, st));
+        }
+        return DDKS_OK;
+    };
+    const std::vector<uint64_t> key{(uint64_t)(uintptr_t)pooled, (uint64_t)(uintptr_t)perms, (uint64_t)n_P,
+                                    (uint64_t)n_Q, (uint64_t)d, (uint64_t)n_perm, (uint64_t)ctx->flags};
+    if ((s = run_call(ctx, ctx->cg_null, key, graph_input_ok(pooled) && (n_perm == 0 || graph_input_ok(perms)), st,
+                      enq)))
+        return s;
     DevResult* hres = (DevResult*)ctx->host_pinned;
     uint64_t* hnums = (uint64_t*)((char*)ctx->host_pinned + sizeof(DevResult));
     uint64_t* hgath = hnums + total;
-    if (ctx->comm) {
-        uint64_t* arrs[1] = {nums + 1};
-        if ((s = gather_items(ctx, arrs, 1, n_perm, &dres->flag, st, hgath))) return s;
-        CU(cudaMemcpyAsync(hnums, nums, 8, cudaMemcpyDeviceToHost, st));
-    } else {
-        CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
-        CU(cudaMemcpyAsync(hnums, nums, (size_t)total * 8, cudaMemcpyDeviceToHost, st));
-    }
+    const unsigned long long* hsrec = (const unsigned long long*)hgath + (size_t)ctx->world * gstride;
     CU(cudaStreamSynchronize(st));
     if ((s = collect_profile(ctx))) return s;
     if (ctx->comm) ddks_unpad_items(hgath, n_perm, ctx->world, 1, hnums + 1, &hres->flag);
     if (hres->flag & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
     if (hres->flag & 2u) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "a perms row is not a permutation of 0..N-1");
+    if (obs_small) {  // the fused statistic's per-origin-block records {num, key, flags}
+        std::vector<ddks_rank_record> recs((size_t)nsrec);
+        for (int64_t r = 0; r < nsrec; ++r) {
+            const unsigned long long* sr = hsrec + 4 * r;
+            recs[r] = decode_record(DevResult{sr[0], ~0ull, sr[1], (uint32_t)sr[2], 0u}, n_P, n_Q, true);
+        }
+        ddks_rank_record comb;
+        ddks_combine_records(recs.data(), (int)nsrec, &comb);
+        if (comb.flags & 1u) return fail(ctx, DDKS_ERR_NONFINITE, "non-finite coordinate in input");
+        hnums[0] = comb.num;
+    }
     const uint64_t obs = hnums[0];
     int64_t ge = 0;
     for (int64_t j = 0; j < n_perm; ++j) {

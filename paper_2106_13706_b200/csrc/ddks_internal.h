@@ -74,6 +74,16 @@ struct ddks_ctx {
     int sg_kd_levels = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> sg_evs;
     std::vector<uint64_t> sg_ev_pairs;
+    // the same for ddks_stat_batch and ddks_permutation_null (run_call in ddks_api.cu): key = the call's pointers,
+    // sizes, flags and the workspace epoch; captured on the second identical call, replayed from the third
+    struct CallGraph {
+        std::vector<uint64_t> seen, key;
+        cudaGraphExec_t exec = nullptr;
+        int64_t launches = 0;
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
+        std::vector<uint64_t> ev_pairs;
+    };
+    CallGraph cg_batch, cg_null;
     double prof_ms = 0.0;
     int64_t prof_launches = 0;
     uint64_t prof_pairs = 0;

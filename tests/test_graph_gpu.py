@@ -100,3 +100,66 @@ def test_contexts_on_concurrent_host_threads():
         assert rs is not None
         for r in rs:
             assert (r.num, r.den, r.D, r.argmax_origin) == want[i], i
+
+
+@pytest.mark.parametrize("B,n_P,n_Q,d,fl", [(64, 200, 150, 4, 0), (7, 1500, 1200, 3, K.DDKS_FLAG_PROFILE),
+                                            (33, 512, 512, 5, K.DDKS_FLAG_NCCL_SELF)])
+def test_graph_batch_replay(B, n_P, n_Q, d, fl):
+    # ddks_stat_batch through its call graph (run_call): captured on the second identical call, then replayed; the
+    # replay reads the buffers' current contents, and a shape change leaves a correct result
+    rng = np.random.default_rng(31 + d)
+    P1 = rng.standard_normal((B, n_P, d)).astype(np.float32)
+    Q1 = (1.1 * rng.standard_normal((B, n_Q, d))).astype(np.float32)
+    P2 = np.ascontiguousarray(P1[::-1] * 0.9)  # same shapes, new contents
+    Q2 = np.ascontiguousarray(Q1[::-1])
+    w1 = [O.ddks(P1[b], Q1[b])[0] for b in range(B)]
+    w2 = [O.ddks(P2[b], Q2[b])[0] for b in range(B)]
+    dP, dQ = dev(P1), dev(Q1)
+    with K.Context(flags=fl) as c:
+        l = []
+        for _ in range(4):  # plain, capture, replay, replay
+            l0 = c.launch_count
+            r = c.stat_batch(dP, dQ)
+            l.append(c.launch_count - l0)
+            assert [int(v) for v in r.num] == w1
+        assert l[1] == l[2] == l[3] > 0
+        dP.copy_(dev(P2))
+        dQ.copy_(dev(Q2))
+        assert [int(v) for v in c.stat_batch(dP, dQ).num] == w2
+        assert [int(v) for v in c.stat_batch(dP[: B // 2], dQ[: B // 2]).num] == w2[: B // 2]
+        assert [int(v) for v in c.stat_batch(dP, dQ).num] == w2
+        if fl & K.DDKS_FLAG_PROFILE:
+            ms, n, pairs = c.profile_read()
+            assert n > 0 and ms > 0
+
+
+@pytest.mark.parametrize("n_P,n_Q,d,n_perm,fl", [(300, 200, 3, 50, 0), (512, 512, 4, 300, K.DDKS_FLAG_PROFILE),
+                                                 (5000, 4000, 2, 20, 0), (400, 300, 8, 40, K.DDKS_FLAG_NCCL_SELF)])
+def test_graph_permutation_null_replay(n_P, n_Q, d, n_perm, fl):
+    # ddks_permutation_null through its call graph: new permutations / points in the same buffers are read by the
+    # replay (null, observed and p-value equal the oracle), including the fused small observed statistic
+    P, Q = I.random_pair(41 + d, n_P, n_Q, d, "mixed")
+    pooled = np.concatenate([P, Q])
+    rng = np.random.default_rng(5 + d)
+    N = n_P + n_Q
+    perms1 = np.stack([rng.permutation(N) for _ in range(n_perm)]).astype(np.int32)
+    perms2 = np.stack([rng.permutation(N) for _ in range(n_perm)]).astype(np.int32)
+    pooled2 = np.ascontiguousarray(pooled[::-1])
+
+    def want(pool, perms):
+        null = [O.ddks(pool[p[:n_P]], pool[p[n_P:]])[0] for p in perms]
+        obs = O.ddks(pool[:n_P], pool[n_P:])[0]
+        return null, obs, (1 + sum(v >= obs for v in null)) / (1 + n_perm)
+
+    dpool, dperm = dev(pooled), dev(perms1)
+    with K.Context(flags=fl) as c:
+        w = want(pooled, perms1)
+        for _ in range(4):
+            null, obs, pv = c.permutation_null(dpool, n_P, dperm)
+            assert [int(v) for v in null] == w[0] and obs.num == w[1] and pv == w[2]
+        dperm.copy_(dev(perms2))
+        dpool.copy_(dev(pooled2))
+        w = want(pooled2, perms2)
+        for _ in range(2):
+            null, obs, pv = c.permutation_null(dpool, n_P, dperm)
+            assert [int(v) for v in null] == w[0] and obs.num == w[1] and pv == w[2]
