@@ -40,6 +40,9 @@ FSET_LANES_PER_CLK_PER_SM = 64  # measured: microbench/pipes.cu FSET.BF.GE = 63.
 N_SM = 148
 
 
+RED_PEAK = 1.93e11  # global RED.ADD.u32 per second into L2-resident counts, measured (profiles/r3_red_global.txt)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -335,9 +338,24 @@ class Step:
             what = "whole rdKS step (normalise, distance keys, bucket-pruned sweep)"
         achieved = byts / (step_ms / 1e3) / 1e9
         peak = float(peaks_.get("hbm_gbs", 6536.7))
-        return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "algorithmic_bytes_per_step": int(byts), "kernel": what,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
+        r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+             "algorithmic_bytes_per_step": int(byts), "kernel": what,
+             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
+        if kern_ms and kern_pairs:
+            # the step's dominant kernel (the vdKS voxel histogram / the rdKS distance-key pass) is bound by L2 atomic
+            # throughput, not HBM: one global RED per point (vdKS) or per key (rdKS), timed live by CUDA events
+            per_launch_ms = kern_ms / max(kern_launches, 1)
+            reds = kern_pairs / max(kern_launches, 1)
+            ach = reds / (per_launch_ms / 1e3)
+            r["dominant_kernel"] = {
+                "kernel": "k_vox_hist_vec (voxel histogram)" if self.args.method == "vdks"
+                          else "k_rd_keys_pt (distance keys + bucket counts)",
+                "bound": "l2_atomics", "achieved": ach, "peak": RED_PEAK, "unit": "RED/s", "frac": ach / RED_PEAK,
+                "reds_per_launch": int(reds), "kernel_ms_per_launch": per_launch_ms,
+                "kernel_share_of_step": per_launch_ms / step_ms if step_ms else None,
+                "peak_source": "microbench/red_global.cu: 12e6 uniform global RED.ADD.u32 into an L2-resident count "
+                               "array, steady state (profiles/r3_red_global.txt)"}
+        return r
 
 
 def main():

@@ -98,5 +98,25 @@ int main() {
                        us, n / (us * 1e-6));
             }
     }
+    // steady-state peak: 12e6 uniform REDs (the rdKS key pass's count) into count arrays of several sizes
+    {
+        const int n2 = 12000000;
+        uint32_t* d_ids2;
+        cudaMalloc(&d_ids2, (size_t)n2 * 4);
+        for (size_t w2 : {(size_t)1 << 21, (size_t)6291456, (size_t)1 << 24}) {
+            std::vector<uint32_t> ids2(n2);
+            std::uniform_int_distribution<uint32_t> wd(0, (uint32_t)w2 - 1);
+            for (auto& v : ids2) v = wd(rng);
+            uint32_t* d_cnt2;
+            cudaMalloc(&d_cnt2, w2 * 4);
+            cudaMemcpy(d_ids2, ids2.data(), (size_t)n2 * 4, cudaMemcpyHostToDevice);
+            for (int variant = 0; variant < 2; ++variant) {
+                const float us = time_red(d_ids2, n2, d_cnt2, w2, variant, 148 * 16);
+                printf("12e6 uniform REDs into %6.1f MB  %s  %8.2f us  %.3e RED/s\n", w2 * 4 / 1e6,
+                       variant ? "4/thread" : "1/thread", us, n2 / (us * 1e-6));
+            }
+            cudaFree(d_cnt2);
+        }
+    }
     return 0;
 }

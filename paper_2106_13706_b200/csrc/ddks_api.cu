@@ -530,6 +530,29 @@ ddks_status ensure_host(ddks_ctx* ctx, size_t bytes) {
     return DDKS_OK;
 }
 
+ddks_status prof_begin(ddks_ctx* ctx, cudaStream_t st, std::pair<cudaEvent_t, cudaEvent_t>* ev) {
+    *ev = {nullptr, nullptr};
+    if (!(ctx->flags & DDKS_FLAG_PROFILE)) return DDKS_OK;
+    if (!ctx->ev_free.empty()) {
+        *ev = ctx->ev_free.back();
+        ctx->ev_free.pop_back();
+    } else {
+        CU(cudaEventCreate(&ev->first));
+        CU(cudaEventCreate(&ev->second));
+    }
+    CU(record_event(ev->first, st));
+    return DDKS_OK;
+}
+
+ddks_status prof_end(ddks_ctx* ctx, cudaStream_t st, const std::pair<cudaEvent_t, cudaEvent_t>& ev, uint64_t units) {
+    if (!ev.first) return DDKS_OK;
+    CU(record_event(ev.second, st));
+    ctx->ev_pending.push_back(ev);
+    ctx->ev_recycle.push_back(1);
+    ctx->ev_pairs.push_back(units);
+    return DDKS_OK;
+}
+
 // After a stream sync: fold the pending count-kernel events into the profile totals.
 ddks_status collect_profile(ddks_ctx* ctx) {
     for (size_t i = 0; i < ctx->ev_pending.size(); ++i) {

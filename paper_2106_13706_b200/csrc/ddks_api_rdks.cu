@@ -143,9 +143,13 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
             ctx->rdb_zero_p = nullptr;  // until this call completes
             if (zero < nb * 8) CU(cudaMemsetAsync((uint8_t*)bcnt + zero, 0, nb * 8 - zero, st));
             rdb_clean_bytes = std::max(zero, nb * 8);
-            // distance keys and their bucket counts in one pass (NormalizeData fused)
+            // distance keys and their bucket counts in one pass (NormalizeData fused); profiled: the call's dominant
+            // kernel, bound by L2 RED throughput (one bucket RED per key)
+            std::pair<cudaEvent_t, cudaEvent_t> pev;
+            if ((s = prof_begin(ctx, st, &pev))) return s;
             launch_rd_keys((const float*)dP, (const float*)dQ, xn, N, n_P, d, keys, (int)cb, (int)ce, k0, bcnt, nbk,
                            scale, st);
+            if ((s = prof_end(ctx, st, pev, (uint64_t)nc * (uint64_t)N))) return s;
             const int nch = (nbk + ddks::RDB_CH - 1) / ddks::RDB_CH;
             uint64_t* csum = (uint64_t*)ctx->rdb_csum.p;
             uint32_t* segc = (uint32_t*)(csum + (size_t)nc * nch);
@@ -180,6 +184,7 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(hc, cnum, (size_t)std::max(nc, 0) * 8, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    if ((s = collect_profile(ctx))) return s;
     if (nc > 0 && pruned && !(hres->flag & 256u)) {  // every bucket was read and re-zeroed
         ctx->rdb_zero_p = ctx->rdb_cnt.p;
         ctx->rdb_zero = rdb_clean_bytes;

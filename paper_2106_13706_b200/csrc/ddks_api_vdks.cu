@@ -96,6 +96,9 @@ ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
         NC(ncclAllReduce(keys, keys, 8, ncclUint32, ncclMin, ctx->comm, st));
         NC(ncclAllReduce(keys + 8, keys + 8, 8, ncclUint32, ncclMax, ctx->comm, st));
     }
+    // profiled: the voxel histogram (the call's dominant kernel, bound by L2 RED throughput), one RED per point
+    std::pair<cudaEvent_t, cudaEvent_t> pev;
+    if ((s = prof_begin(ctx, st, &pev))) return s;
     if (whole) {
         const int gh = (int)std::max<int64_t>(1, std::min<int64_t>((N / 4 + 255) / 256, 148 * 8));
         switch (d) {
@@ -111,6 +114,7 @@ ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
         CHECK_LAUNCH();
         ctx->launches++;
     }
+    if ((s = prof_end(ctx, st, pev, (uint64_t)(whole ? N : std::max<int64_t>(pe - pb, 0))))) return s;
     if (ctx->comm) {
         NC(ncclAllReduce(cnt, cnt, (size_t)V * 2, ncclUint32, ncclSum, ctx->comm, st));
         NC(ncclAllReduce(&dres->flag, &dres->flag, 1, ncclUint32, ncclMax, ctx->comm, st));
@@ -162,6 +166,7 @@ ddks_status ddks_vdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     if (ctx->comm) NC(ncclAllReduce(&dres->num, &dres->num, 1, ncclUint64, ncclMax, ctx->comm, st));
     CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    if ((s = collect_profile(ctx))) return s;
     if (J > 0) {  // every slab zeroed its counts: [0, max(zero, 8 V)) is zero again
         ctx->vox_zero_p = ctx->vox_cnt.p;
         ctx->vox_zero = std::max(zero, (size_t)V * 8);

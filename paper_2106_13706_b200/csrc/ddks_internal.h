@@ -122,6 +122,12 @@ inline cudaError_t record_event(cudaEvent_t e, cudaStream_t st) {
                                                : cudaEventRecord(e, st);
 }
 
+// DDKS_FLAG_PROFILE: an event pair around the dominant launch of a call (no-op without the flag); prof_end queues it
+// with its work units (pair classifications, or REDs for the approximations) for collect_profile after the sync
+ddks_status prof_begin(ddks_ctx* ctx, cudaStream_t st, std::pair<cudaEvent_t, cudaEvent_t>* ev);
+ddks_status prof_end(ddks_ctx* ctx, cudaStream_t st, const std::pair<cudaEvent_t, cudaEvent_t>& ev, uint64_t units);
+ddks_status collect_profile(ddks_ctx* ctx);
+
 // grow-only device workspace; host (pinned) scratch
 ddks_status ensure(ddks_ctx* ctx, DevBuf& b, size_t bytes);
 // as ensure, and a (re)allocated buffer is zeroed on st (buffers whose users leave them zero: count partials)
