@@ -30,7 +30,10 @@
 namespace ddks {
 namespace {
 
-constexpr int PM_M = 128, PM_N = 256, PM_KB = 128, PM_S = 3;         // tile rows, permutations, points per k-block
+#ifndef DDKS_PM_S  // pipeline stages: 2 (two CTAs per SM, one's epilogue under the other's MMAs; C4b null 120 -> 99 us vs 3)
+#define DDKS_PM_S 2
+#endif
+constexpr int PM_M = 128, PM_N = 256, PM_KB = 128, PM_S = DDKS_PM_S;  // tile rows, permutations, points per k-block
 constexpr int PM_A_BYTES = PM_M * PM_KB, PM_B_BYTES = PM_N * PM_KB;   // 16 KB, 32 KB fp8 tiles
 constexpr uint8_t PM_ONE = 0x38;                                      // FP8 E4M3 1.0
 constexpr int PM_GEN = 256;                                           // classify + epilogue threads (warps 0-7)
@@ -130,7 +133,7 @@ __global__ void k_labels_mma(const int32_t* __restrict__ perms, int64_t n_perm, 
 
 // ---------------------------------------------------------------------------------------------- the null kernel
 template <int D, bool GT>
-__global__ void __launch_bounds__(PM_THREADS, 1) k_perm_mma(const PermMmaArgs a) {
+__global__ void __launch_bounds__(PM_THREADS, PM_S <= 2 ? 2 : 1) k_perm_mma(const PermMmaArgs a) {
     using G = PermMmaGeo<D>;
     constexpr int NQ = G::NQ, OPT = G::OPT, DP = G::DP;
     extern __shared__ __align__(1024) uint8_t smem[];
