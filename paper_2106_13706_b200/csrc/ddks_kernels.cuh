@@ -45,6 +45,10 @@ template <int D> struct Cfg;
 #define DDKS_UNROLL 8
 #endif
 constexpr int kUnrollPts = DDKS_UNROLL;
+#ifndef DDKS_TWODIM  // experiment, measured slower (C5 651 vs 627 ms, profiles/r3_twodim_rejected.txt): kd tiles with two
+                     // compared dims left accumulate sum a, sum b, sum ab in registers
+#define DDKS_TWODIM 0
+#endif
 #ifndef DDKS_R1_PTS  // points per step of the R == 1 inner loop (d = 8)
 #define DDKS_R1_PTS 2
 #endif
@@ -380,6 +384,16 @@ template <int D, int KX, int UM> __host__ __device__ constexpr int n_cmp() {
     return c;
 }
 
+// the i-th compared dim (ascending), -1 if fewer
+template <int D, int KX, int UM> __host__ __device__ constexpr int cmp_dim_idx(int i) {
+    for (int k = 0; k < D; ++k)
+        if (cmp_dim<KX, UM>(k)) {
+            if (i == 0) return k;
+            --i;
+        }
+    return -1;
+}
+
 template <int D, bool GT, int WPB, int KX = 0, int UM = 0, bool SPLIT_CHAIN = (D >= 6)>
 __device__ __forceinline__ float code_addr(const float (&x)[D], const float (&o)[D], float base) {
     constexpr int NC = n_cmp<D, KX, UM>();
@@ -453,6 +467,47 @@ __device__ __forceinline__ void count_points(const float* tile, int lo, int hi, 
             const uint32_t n1 = (uint32_t)sacc[r];
             if (n1) red_counter(base[r % NB_] + W1, ubase, inc * n1, hbytes);
             if (n1 != n) red_counter(base[r % NB_], ubase, inc * (n - n1), hbytes);
+        }
+        return;
+    }
+#endif
+#if DDKS_TWODIM
+    if constexpr (KX > 0 && n_cmp<D, KX, UM>() == 2 && R >= 2) {
+        // kd tile with TWO compared dims left (one open sorted dim + the unsorted last dim at d = K + 1): every pair
+        // is still classified by its own two compares, and its increment goes to one of four counters of the
+        // origin; the compare bits a, b (FSET.BF, 1.0 / 0.0) are accumulated as sum a, sum b and sum ab (FADD, FADD,
+        // FFMA; exact, <= TILE) and the four counters receive the exact totals once per origin and tile part:
+        // n11 = sum ab, n10 = sum a - sum ab, n01 = sum b - sum ab, n00 = n - sum a - sum b + sum ab.
+        constexpr int C0 = cmp_dim_idx<D, KX, UM>(0), C1 = cmp_dim_idx<D, KX, UM>(1);
+        constexpr float W0 = (float)(4 * (1 << C0) * WPB), W1 = (float)(4 * (1 << C1) * WPB);
+        float sa[R], sb[R], sab[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) sa[r] = 0.0f, sb[r] = 0.0f, sab[r] = 0.0f;
+        float xa = tile[p * DP + C0], xb = tile[p * DP + C1];
+#pragma unroll 8
+        for (; p < hi; ++p) {
+            const float x0 = xa, x1 = xb;
+            xa = tile[(p + 1) * DP + C0];
+            xb = tile[(p + 1) * DP + C1];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const float ba = cmp_bit<GT>(x0, o[r][C0]), bb = cmp_bit<GT>(x1, o[r][C1]);
+                sa[r] += ba;
+                sb[r] += bb;
+                sab[r] = fmaf(ba, bb, sab[r]);
+            }
+        }
+        const uint32_t n = (uint32_t)(hi - lo);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t inc = (r < RP) ? inc_lo : inc_hi;
+            const uint32_t n11 = (uint32_t)sab[r], na = (uint32_t)sa[r], nb = (uint32_t)sb[r];
+            const uint32_t n10 = na - n11, n01 = nb - n11, n00 = n - na - nb + n11;
+            const float b0 = base[r % NB_];
+            if (n00) red_counter(b0, ubase, inc * n00, hbytes);
+            if (n10) red_counter(b0 + W0, ubase, inc * n10, hbytes);
+            if (n01) red_counter(b0 + W1, ubase, inc * n01, hbytes);
+            if (n11) red_counter(b0 + W0 + W1, ubase, inc * n11, hbytes);
         }
         return;
     }
