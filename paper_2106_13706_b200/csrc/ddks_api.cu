@@ -603,6 +603,42 @@ int64_t gather_stride(int64_t total, int world, int n_arr) {
     return (total / world + (total % world ? 1 : 0)) * n_arr + 1;
 }
 
+// a graph may read this input at replay time: device (or managed) memory, or page-locked host memory
+bool graph_input_ok(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged || a.type == cudaMemoryTypeHost;
+}
+
+// environment overrides (tuning / test knobs) change the plan: a graph captured under other values is not reused
+bool env_overrides() {
+    return getenv("DDKS_KD") || getenv("DDKS_SEGS") || getenv("DDKS_KD_SHUFFLE") || getenv("DDKS_NO_KEY") ||
+           getenv("DDKS_GRIDY") || getenv("DDKS_NO_SMALL") || getenv("DDKS_KD_RADIX") || getenv("DDKS_NO_MMA") ||
+           getenv("DDKS_PERM_GROUP");
+}
+
+void drop_call_graph(ddks_ctx* ctx, ddks_ctx::CallGraph& cg) {
+    if (cg.exec) cudaGraphExecDestroy(cg.exec);
+    cg.exec = nullptr;
+    cg.key.clear();
+    for (auto& e : cg.evs) ctx->ev_free.push_back(e);
+    cg.evs.clear();
+    cg.ev_pairs.clear();
+}
+
+void launch_call_graph(ddks_ctx* ctx, ddks_ctx::CallGraph& cg, cudaStream_t st, cudaError_t* e) {
+    *e = cudaGraphLaunch(cg.exec, st);
+    ctx->launches += cg.launches;
+    for (size_t i = 0; i < cg.evs.size(); ++i) {
+        ctx->ev_pending.push_back(cg.evs[i]);
+        ctx->ev_pairs.push_back(cg.ev_pairs[i]);
+        ctx->ev_recycle.push_back(0);
+    }
+}
+
 }  // namespace ddks_host
 
 using namespace ddks_host;
@@ -718,10 +754,11 @@ ddks_status ddks_destroy(ddks_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     if (ctx->sg_exec) cudaGraphExecDestroy(ctx->sg_exec);
-    for (auto* cg : {&ctx->cg_batch, &ctx->cg_null})
+    for (auto* cg : {&ctx->cg_batch, &ctx->cg_null, &ctx->cg_vdks, &ctx->cg_rdks})
         if (cg->exec) cudaGraphExecDestroy(cg->exec);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
-    for (auto* v : {&ctx->ev_free, &ctx->sg_evs, &ctx->cg_batch.evs, &ctx->cg_null.evs})
+    for (auto* v : {&ctx->ev_free, &ctx->sg_evs, &ctx->cg_batch.evs, &ctx->cg_null.evs, &ctx->cg_vdks.evs,
+                    &ctx->cg_rdks.evs})
         for (auto& e : *v) {
             cudaEventDestroy(e.first);
             cudaEventDestroy(e.second);
@@ -934,15 +971,6 @@ static ddks_status stat_enqueue(ddks_ctx* ctx, const float* P, int64_t n_P, cons
     return DDKS_OK;
 }
 
-// a graph may read this input at replay time: device (or managed) memory, or page-locked host memory
-static bool graph_input_ok(const void* p) {
-    cudaPointerAttributes a;
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged || a.type == cudaMemoryTypeHost;
-}
 
 static void drop_stat_graph(ddks_ctx* ctx) {
     if (ctx->sg_exec) cudaGraphExecDestroy(ctx->sg_exec);
@@ -997,91 +1025,9 @@ static ddks_status stat_capture(ddks_ctx* ctx, const ddks_ctx::StatKey& key, con
     return DDKS_OK;
 }
 
-// environment overrides (tuning / test knobs) change the plan: a graph captured under other values is not reused
-static bool env_overrides() {
-    return getenv("DDKS_KD") || getenv("DDKS_SEGS") || getenv("DDKS_KD_SHUFFLE") || getenv("DDKS_NO_KEY") ||
-           getenv("DDKS_GRIDY") || getenv("DDKS_NO_SMALL") || getenv("DDKS_KD_RADIX") || getenv("DDKS_NO_MMA") ||
-           getenv("DDKS_PERM_GROUP");
-}
 
-static void drop_call_graph(ddks_ctx* ctx, ddks_ctx::CallGraph& cg) {
-    if (cg.exec) cudaGraphExecDestroy(cg.exec);
-    cg.exec = nullptr;
-    cg.key.clear();
-    for (auto& e : cg.evs) ctx->ev_free.push_back(e);
-    cg.evs.clear();
-    cg.ev_pairs.clear();
-}
 
-static void launch_call_graph(ddks_ctx* ctx, ddks_ctx::CallGraph& cg, cudaStream_t st, cudaError_t* e) {
-    *e = cudaGraphLaunch(cg.exec, st);
-    ctx->launches += cg.launches;
-    for (size_t i = 0; i < cg.evs.size(); ++i) {
-        ctx->ev_pending.push_back(cg.evs[i]);
-        ctx->ev_pairs.push_back(cg.ev_pairs[i]);
-        ctx->ev_recycle.push_back(0);
-    }
-}
 
-// Run the stream-ordered part of a C-ABI call (enq: staging, kernels, collectives, the D2H into host_pinned; no sync)
-// through a per-call-shape CUDA graph: the second call with the same key (pointers, sizes, flags; + the workspace
-// epoch) is captured on the context's capture stream and every identical call after it is one cudaGraphLaunch on st.
-// Not graphable (host inputs in pageable memory, DDKS_FLAG_NO_GRAPH, environment overrides): enq runs on st.
-extern "C++" {
-template <class F>
-ddks_status run_call(ddks_ctx* ctx, ddks_ctx::CallGraph& cg, std::vector<uint64_t> key, bool graphable,
-                            cudaStream_t st, F&& enq) {
-    graphable = graphable && !(ctx->flags & DDKS_FLAG_NO_GRAPH) && !env_overrides();
-    key.push_back(ctx->alloc_epoch);
-    cudaError_t e;
-    if (graphable && cg.exec && cg.key == key) {
-        launch_call_graph(ctx, cg, st, &e);
-        CU(e);
-        return DDKS_OK;
-    }
-    if (graphable && cg.seen == key) {
-        drop_call_graph(ctx, cg);
-        if (!ctx->cap_stream) CU(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
-        const size_t ev0 = ctx->ev_pending.size();
-        const int64_t l0 = ctx->launches;
-        CU(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed));
-        const ddks_status s = enq(ctx->cap_stream);
-        cudaGraph_t g = nullptr;
-        e = cudaStreamEndCapture(ctx->cap_stream, &g);
-        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs(ctx->ev_pending.begin() + ev0, ctx->ev_pending.end());
-        std::vector<uint64_t> pairs(ctx->ev_pairs.begin() + ev0, ctx->ev_pairs.end());
-        ctx->ev_pending.resize(ev0);
-        ctx->ev_pairs.resize(ev0);
-        ctx->ev_recycle.resize(ev0);
-        const int64_t nl = ctx->launches - l0;
-        ctx->launches = l0;
-        cudaGraphExec_t ex = nullptr;
-        const bool good = s == DDKS_OK && e == cudaSuccess && g && ctx->alloc_epoch == key.back() &&
-                          cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
-        if (g) cudaGraphDestroy(g);
-        if (good) {
-            cg.exec = ex;
-            cg.key = key;
-            cg.launches = nl;
-            cg.evs = evs;
-            cg.ev_pairs = pairs;
-            launch_call_graph(ctx, cg, st, &e);
-            CU(e);
-            return DDKS_OK;
-        }
-        cudaGetLastError();  // capture refused or the workspace moved: run uncaptured
-        for (auto& v : evs) ctx->ev_free.push_back(v);
-        ctx->err.clear();
-    }
-    ddks_status s = enq(st);
-    if (s) return s;
-    if (graphable) {  // a second identical call (same workspace) will be captured
-        cg.seen = key;
-        cg.seen.back() = ctx->alloc_epoch;
-    }
-    return DDKS_OK;
-}
-}  // extern "C++"
 
 // a1-a7 for one pair, origins sharded across ranks; optional per-origin export (debug path, single rank).
 // shard_world > 0: compute only the origin shard that rank shard_rank of shard_world would own (ddks_stat_shard).

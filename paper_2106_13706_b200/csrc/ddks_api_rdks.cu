@@ -49,9 +49,6 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     ddks_status s;
     if ((s = bind_device(ctx))) return s;
     cudaStream_t st = (cudaStream_t)stream;
-    const void *dP, *dQ;
-    if ((s = stage_input(ctx, P, (size_t)n_P * d * 4, ctx->raw_a, st, &dP))) return s;
-    if ((s = stage_input(ctx, Q, (size_t)n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
     int64_t cb, ce;
     ddks_shard_range(d + 1, ctx->world, ctx->rank, &cb, &ce);
     const int nc = (int)(ce - cb);
@@ -62,6 +59,7 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     if ((s = ensure(ctx, ctx->rd_hist, (size_t)std::max(nc, 1) * tiles * 256 * 4))) return s;
     if ((s = ensure(ctx, ctx->rd_tcnt, (size_t)std::max(nc, 1) * tiles * 4))) return s;
     if ((s = ensure(ctx, ctx->rd_cnum, (size_t)(d + 1) * 8))) return s;
+    if (d > 16 && nc > 0 && (s = ensure(ctx, ctx->rd_xn, (size_t)N * d * 8))) return s;
     uint32_t* keys = (uint32_t*)ctx->rd_keys.p;
     uint64_t* k0 = (uint64_t*)ctx->rd_k0.p;
     uint64_t* k1 = (uint64_t*)ctx->rd_k1.p;
@@ -69,39 +67,9 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     uint32_t* tcnt = (uint32_t*)ctx->rd_tcnt.p;
     unsigned long long* cnum = (unsigned long long*)ctx->rd_cnum.p;
     DevResult* dres = (DevResult*)ctx->res.p;
-    CU(cudaMemsetAsync(dres, 0, sizeof(DevResult), st));
-    CU(cudaMemsetAsync(keys, 0xff, (size_t)d * 4, st));
-    CU(cudaMemsetAsync(keys + d, 0, (size_t)d * 4, st));
-    CU(cudaMemsetAsync(cnum, 0, (size_t)(d + 1) * 8, st));
-    const int gy = std::min(d, 1024);
-    const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((N + 1023) / 1024, std::max(1, 296 / gy)));
-    if (d <= 8 && ((((uintptr_t)dP | (uintptr_t)dQ) & 15) == 0)) {  // float4 rows-in-fours
-        const int gv = (int)std::max<int64_t>(1, std::min<int64_t>((N / 4 + 255) / 256, ddks::MINMAX_BLOCKS));
-        switch (d) {
-#define MMV(D) case D: ddks::k_minmax_vec<D><<<gv, 256, 0, st>>>((const float*)dP, n_P, (const float*)dQ, n_Q, keys, D, 1, &dres->flag); break;
-            MMV(1) MMV(2) MMV(3) MMV(4) MMV(5) MMV(6) MMV(7) MMV(8)
-#undef MMV
-        }
-    } else {
-        ddks::k_rd_minmax<<<dim3(gx, gy), 256, 0, st>>>(
-            (const float*)dP, n_P, (const float*)dQ, n_Q, d, keys, &dres->flag);
-    }
-    CHECK_LAUNCH();
-    ctx->launches++;
     auto grid_for = [](int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); };
-    // small d: NormalizeData is fused into the key kernel (x' recomputed per corner, no N x d f64 round trip);
-    // large d (the paper's d = 1000 shape): normalise once, the key kernel reads x'
-    const double* xn = nullptr;
-    if (d > 16 && nc > 0) {
-        if ((s = ensure(ctx, ctx->rd_xn, (size_t)N * d * 8))) return s;
-        ddks::k_rd_normalize<<<grid_for(N * d), 256, 0, st>>>((const float*)dP, n_P, (const float*)dQ, n_Q, d, keys,
-                                                              (double*)ctx->rd_xn.p);
-        CHECK_LAUNCH();
-        ctx->launches++;
-        xn = (const double*)ctx->rd_xn.p;
-    }
     // full path: segmented 8-pass LSD radix sort of every corner's keys, then the tie-complete sweep
-    auto full_sort = [&]() -> ddks_status {
+    auto full_sort = [&](cudaStream_t st) -> ddks_status {
         const int blocks = nc * tiles;
         uint64_t* src = nullptr;
         CU(cudaMemsetAsync(cnum, 0, (size_t)(d + 1) * 8, st));
@@ -113,36 +81,79 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
         ctx->launches += 2;
         return DDKS_OK;
     };
+    // bucket-pruned sweep (default): workspace, and the known-zero state of the bucket counts -- k_rdb_cand /
+    // k_rdb_finish re-zero every bucket they read, so after a completed call the first rdb_zero bytes of the buffer
+    // are known zero (no memset of nb * 8 bytes); the memset this implies is part of the call graph and its key
     const bool pruned = !(ctx->flags & DDKS_FLAG_RDKS_FULL_SORT);
-    size_t rdb_clean_bytes = 0;  // pruned path: bytes of the bucket counts zero again once the call completes
-    if (nc > 0) {
-        if (!pruned) {
+    int nbk = 256;
+    while (nbk < N / 4 && nbk < (1 << 20)) nbk <<= 1;
+    const double scale = (double)nbk / (std::sqrt((double)d) * (1.0 + 1e-9));
+    const size_t nb = (size_t)nc * nbk;
+    const int nch = (nbk + ddks::RDB_CH - 1) / ddks::RDB_CH;
+    const int cbytes = nbk / 8;  // the compaction's SMEM bitmap of one segment
+    size_t zero = 0, rdb_clean_bytes = 0;
+    if (nc > 0 && pruned) {
+        if ((s = ensure(ctx, ctx->rdb_cnt, nb * 8))) return s;
+        if ((s = ensure(ctx, ctx->rdb_pst, nb * 8))) return s;
+        if ((s = ensure(ctx, ctx->rdb_coff, nb * 4))) return s;
+        if ((s = ensure(ctx, ctx->rdb_fill, nb * 4))) return s;
+        if ((s = ensure(ctx, ctx->rdb_bits, nb / 8))) return s;
+        if ((s = ensure(ctx, ctx->rdb_clist, nb * 4))) return s;
+        if ((s = ensure(ctx, ctx->rdb_csum, ((size_t)nc * nch + nc) * 8))) return s;
+        zero = ctx->rdb_zero_p == ctx->rdb_cnt.p ? ctx->rdb_zero : 0;
+        ctx->rdb_zero_p = nullptr;  // until this call completes
+        rdb_clean_bytes = std::max(zero, nb * 8);
+        if (cbytes > 48 * 1024)
+            CU(cudaFuncSetAttribute(ddks::k_rdb_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
+    }
+    if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)(d + 1) * 8))) return s;
+    DevResult* hres = (DevResult*)ctx->host_pinned;
+    uint64_t* hc = (uint64_t*)((char*)ctx->host_pinned + sizeof(DevResult));
+    auto enq = [&](cudaStream_t st) -> ddks_status {
+        ddks_status s;
+        const void *dP, *dQ;
+        if ((s = stage_input(ctx, P, (size_t)n_P * d * 4, ctx->raw_a, st, &dP))) return s;
+        if ((s = stage_input(ctx, Q, (size_t)n_Q * d * 4, ctx->raw_b, st, &dQ))) return s;
+        CU(cudaMemsetAsync(dres, 0, sizeof(DevResult), st));
+        CU(cudaMemsetAsync(keys, 0xff, (size_t)d * 4, st));
+        CU(cudaMemsetAsync(keys + d, 0, (size_t)d * 4, st));
+        CU(cudaMemsetAsync(cnum, 0, (size_t)(d + 1) * 8, st));
+        const int gy = std::min(d, 1024);
+        const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((N + 1023) / 1024, std::max(1, 296 / gy)));
+        if (d <= 8 && ((((uintptr_t)dP | (uintptr_t)dQ) & 15) == 0)) {  // float4 rows-in-fours
+            const int gv = (int)std::max<int64_t>(1, std::min<int64_t>((N / 4 + 255) / 256, ddks::MINMAX_BLOCKS));
+            switch (d) {
+#define MMV(D) case D: ddks::k_minmax_vec<D><<<gv, 256, 0, st>>>((const float*)dP, n_P, (const float*)dQ, n_Q, keys, D, 1, &dres->flag); break;
+                MMV(1) MMV(2) MMV(3) MMV(4) MMV(5) MMV(6) MMV(7) MMV(8)
+#undef MMV
+            }
+        } else {
+            ddks::k_rd_minmax<<<dim3(gx, gy), 256, 0, st>>>(
+                (const float*)dP, n_P, (const float*)dQ, n_Q, d, keys, &dres->flag);
+        }
+        CHECK_LAUNCH();
+        ctx->launches++;
+        // small d: NormalizeData is fused into the key kernel (x' recomputed per corner, no N x d f64 round trip);
+        // large d (the paper's d = 1000 shape): normalise once, the key kernel reads x'
+        const double* xn = nullptr;
+        if (d > 16 && nc > 0) {
+            ddks::k_rd_normalize<<<grid_for(N * d), 256, 0, st>>>((const float*)dP, n_P, (const float*)dQ, n_Q, d,
+                                                                  keys, (double*)ctx->rd_xn.p);
+            CHECK_LAUNCH();
+            ctx->launches++;
+            xn = (const double*)ctx->rd_xn.p;
+        }
+        if (nc > 0 && !pruned) {
             launch_rd_keys((const float*)dP, (const float*)dQ, xn, N, n_P, d, keys, (int)cb, (int)ce, k0, nullptr, 0,
                            0.0, st);
             CHECK_LAUNCH();
             ctx->launches++;
-            if ((s = full_sort())) return s;
-        } else {
+            if ((s = full_sort(st))) return s;
+        } else if (nc > 0) {
             // bucket-pruned sweep: bucket counts, exact bucket-end values, sort only the buckets that can beat them
-            int nbk = 256;
-            while (nbk < N / 4 && nbk < (1 << 20)) nbk <<= 1;
-            const double scale = (double)nbk / (std::sqrt((double)d) * (1.0 + 1e-9));
-            const size_t nb = (size_t)nc * nbk;
-            if ((s = ensure(ctx, ctx->rdb_cnt, nb * 8))) return s;
-            if ((s = ensure(ctx, ctx->rdb_pst, nb * 8))) return s;
-            if ((s = ensure(ctx, ctx->rdb_coff, nb * 4))) return s;
-            if ((s = ensure(ctx, ctx->rdb_fill, nb * 4))) return s;
-            if ((s = ensure(ctx, ctx->rdb_bits, nb / 8))) return s;
-            if ((s = ensure(ctx, ctx->rdb_clist, nb * 4))) return s;
-            if ((s = ensure(ctx, ctx->rdb_csum, ((size_t)nc * ((nbk + ddks::RDB_CH - 1) / ddks::RDB_CH) + nc) * 8))) return s;
             uint32_t* bcnt = (uint32_t*)ctx->rdb_cnt.p;
             int32_t* clist = (int32_t*)ctx->rdb_clist.p;
-            // the bucket counts must start at zero: k_rdb_cand / k_rdb_finish re-zero every bucket they read, so after
-            // a completed call the first rdb_zero bytes of the buffer are known zero (no memset of nb * 8 bytes)
-            const size_t zero = ctx->rdb_zero_p == ctx->rdb_cnt.p ? ctx->rdb_zero : 0;
-            ctx->rdb_zero_p = nullptr;  // until this call completes
             if (zero < nb * 8) CU(cudaMemsetAsync((uint8_t*)bcnt + zero, 0, nb * 8 - zero, st));
-            rdb_clean_bytes = std::max(zero, nb * 8);
             // distance keys and their bucket counts in one pass (NormalizeData fused); profiled: the call's dominant
             // kernel, bound by L2 RED throughput (one bucket RED per key)
             std::pair<cudaEvent_t, cudaEvent_t> pev;
@@ -150,11 +161,9 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
             launch_rd_keys((const float*)dP, (const float*)dQ, xn, N, n_P, d, keys, (int)cb, (int)ce, k0, bcnt, nbk,
                            scale, st);
             if ((s = prof_end(ctx, st, pev, (uint64_t)nc * (uint64_t)N))) return s;
-            const int nch = (nbk + ddks::RDB_CH - 1) / ddks::RDB_CH;
             uint64_t* csum = (uint64_t*)ctx->rdb_csum.p;
             uint32_t* segc = (uint32_t*)(csum + (size_t)nc * nch);
             CU(cudaMemsetAsync(segc, 0, (size_t)nc * 8, st));
-            CU(cudaMemsetAsync(cnum, 0, (size_t)(d + 1) * 8, st));
             ddks::k_rdb_reduce<<<dim3(nch, nc), 256, 0, st>>>(bcnt, nbk, csum);
             ddks::k_rdb_chunk_scan<<<nc, 256, 0, st>>>(csum, nch);
             ddks::k_rdb_down<<<dim3(nch, nc), 256, 0, st>>>(bcnt, nbk, csum, n_P, n_Q, (uint2*)ctx->rdb_pst.p, cnum);
@@ -163,9 +172,6 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
                                                                     (uint32_t*)ctx->rdb_fill.p,
                                                                     (uint32_t*)ctx->rdb_bits.p, clist, segc);
             // compaction: ~2 CTAs per SM in all, split over the segments; the segment's bitmap in dynamic SMEM
-            const int cbytes = nbk / 8;
-            if (cbytes > 48 * 1024)
-                CU(cudaFuncSetAttribute(ddks::k_rdb_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
             const int64_t cchunks = std::max<int64_t>(1, std::min<int64_t>((148 * 2 + nc - 1) / nc,
                                                                            (N + ddks::RDB_CT - 1) / ddks::RDB_CT));
             ddks::k_rdb_compact<<<dim3((unsigned)cchunks, nc), ddks::RDB_CT, cbytes, st>>>(
@@ -177,12 +183,13 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
             CHECK_LAUNCH();
             ctx->launches += 7;
         }
-    }
-    if ((s = ensure_host(ctx, sizeof(DevResult) + (size_t)(d + 1) * 8))) return s;
-    DevResult* hres = (DevResult*)ctx->host_pinned;
-    uint64_t* hc = (uint64_t*)((char*)ctx->host_pinned + sizeof(DevResult));
-    CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(hc, cnum, (size_t)std::max(nc, 0) * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(hc, cnum, (size_t)std::max(nc, 0) * 8, cudaMemcpyDeviceToHost, st));
+        return DDKS_OK;
+    };
+    const std::vector<uint64_t> key{(uint64_t)(uintptr_t)P, (uint64_t)(uintptr_t)Q, (uint64_t)n_P, (uint64_t)n_Q,
+                                    (uint64_t)d, (uint64_t)ctx->flags, zero >= nb * 8 ? ~0ull : (uint64_t)zero};
+    if ((s = run_call(ctx, ctx->cg_rdks, key, graph_input_ok(P) && graph_input_ok(Q), st, enq))) return s;
     CU(cudaStreamSynchronize(st));
     if ((s = collect_profile(ctx))) return s;
     if (nc > 0 && pruned && !(hres->flag & 256u)) {  // every bucket was read and re-zeroed
@@ -190,7 +197,7 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
         ctx->rdb_zero = rdb_clean_bytes;
     }
     if (nc > 0 && pruned && (hres->flag & 256u)) {  // a candidate bucket too large for SMEM: sort everything
-        if ((s = full_sort())) return s;
+        if ((s = full_sort(st))) return s;
         CU(cudaMemcpyAsync(hc, cnum, (size_t)nc * 8, cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
     }

@@ -83,7 +83,7 @@ struct ddks_ctx {
         std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
         std::vector<uint64_t> ev_pairs;
     };
-    CallGraph cg_batch, cg_null;
+    CallGraph cg_batch, cg_null, cg_vdks, cg_rdks;
     double prof_ms = 0.0;
     int64_t prof_launches = 0;
     uint64_t prof_pairs = 0;
@@ -175,5 +175,70 @@ ddks_status run_count_kd_d(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
                            unsigned long long* hist, unsigned long long* best_key);
 ddks_status radix_sort_keys(ddks_ctx* ctx, uint64_t* src, uint64_t* dst, int64_t N, int nseg, int shift_begin,
                             uint32_t* hist, cudaStream_t st, uint64_t** sorted);
+
+// ---- per-call-shape CUDA graphs (ddks_api.cu) ------------------------------------------------------------------
+bool graph_input_ok(const void* p);   // a graph may read p at replay time (device, managed or pinned host memory)
+bool env_overrides();                 // a tuning / test environment knob is set: no graphs
+void drop_call_graph(ddks_ctx* ctx, ddks_ctx::CallGraph& cg);
+void launch_call_graph(ddks_ctx* ctx, ddks_ctx::CallGraph& cg, cudaStream_t st, cudaError_t* e);
+
+// Run the stream-ordered part of a C-ABI call (enq: staging, kernels, collectives, the D2H into host_pinned; no sync)
+// through a per-call-shape CUDA graph: the second call with the same key (pointers, sizes, flags, plan state; + the
+// workspace epoch) is captured on the context's capture stream and every identical call after it is one
+// cudaGraphLaunch on st. Not graphable (host inputs in pageable memory, DDKS_FLAG_NO_GRAPH, environment
+// overrides): enq runs on st. Host-side state updates belong outside enq (a replay does not run it).
+template <class F>
+ddks_status run_call(ddks_ctx* ctx, ddks_ctx::CallGraph& cg, std::vector<uint64_t> key, bool graphable,
+                     cudaStream_t st, F&& enq) {
+    graphable = graphable && !(ctx->flags & DDKS_FLAG_NO_GRAPH) && !env_overrides();
+    key.push_back(ctx->alloc_epoch);
+    cudaError_t e;
+    if (graphable && cg.exec && cg.key == key) {
+        launch_call_graph(ctx, cg, st, &e);
+        CU(e);
+        return DDKS_OK;
+    }
+    if (graphable && cg.seen == key) {
+        drop_call_graph(ctx, cg);
+        if (!ctx->cap_stream) CU(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+        const size_t ev0 = ctx->ev_pending.size();
+        const int64_t l0 = ctx->launches;
+        CU(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed));
+        const ddks_status s = enq(ctx->cap_stream);
+        cudaGraph_t g = nullptr;
+        e = cudaStreamEndCapture(ctx->cap_stream, &g);
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs(ctx->ev_pending.begin() + ev0, ctx->ev_pending.end());
+        std::vector<uint64_t> pairs(ctx->ev_pairs.begin() + ev0, ctx->ev_pairs.end());
+        ctx->ev_pending.resize(ev0);
+        ctx->ev_pairs.resize(ev0);
+        ctx->ev_recycle.resize(ev0);
+        const int64_t nl = ctx->launches - l0;
+        ctx->launches = l0;
+        cudaGraphExec_t ex = nullptr;
+        const bool good = s == DDKS_OK && e == cudaSuccess && g && ctx->alloc_epoch == key.back() &&
+                          cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+        if (g) cudaGraphDestroy(g);
+        if (good) {
+            cg.exec = ex;
+            cg.key = key;
+            cg.launches = nl;
+            cg.evs = evs;
+            cg.ev_pairs = pairs;
+            launch_call_graph(ctx, cg, st, &e);
+            CU(e);
+            return DDKS_OK;
+        }
+        cudaGetLastError();  // capture refused or the workspace moved: run uncaptured
+        for (auto& v : evs) ctx->ev_free.push_back(v);
+        ctx->err.clear();
+    }
+    ddks_status s = enq(st);
+    if (s) return s;
+    if (graphable) {  // a second identical call (same workspace) will be captured
+        cg.seen = key;
+        cg.seen.back() = ctx->alloc_epoch;
+    }
+    return DDKS_OK;
+}
 
 }  // namespace ddks_host

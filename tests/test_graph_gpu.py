@@ -163,3 +163,50 @@ def test_graph_permutation_null_replay(n_P, n_Q, d, n_perm, fl):
         for _ in range(2):
             null, obs, pv = c.permutation_null(dpool, n_P, dperm)
             assert [int(v) for v in null] == w[0] and obs.num == w[1] and pv == w[2]
+
+
+@pytest.mark.parametrize("n_P,n_Q,d,k", [(3000, 2500, 3, 16), (2000, 2000, 5, 8), (500, 700, 2, 5000)])
+def test_graph_vdks_replay(n_P, n_Q, d, k):
+    # ddks_vdks through its call graph: the known-zero state of the voxel counts is part of the key (it decides the
+    # memset node), so alternating shapes and a line-pass call (k > 4096 dirties the counts) stay exact
+    P1, Q1 = I.random_pair(61 + d, n_P, n_Q, d, "mixed")
+    P2, Q2 = I.random_pair(62 + d, n_P, n_Q, d, "dup")
+    Po, Qo = I.random_pair(63, 300, 200, 2, "dup")
+    dP, dQ, dPo, dQo = dev(P1), dev(Q1), dev(Po), dev(Qo)
+    w1, w2, wo = O.vdks(P1, Q1, k)[:2], O.vdks(P2, Q2, k)[:2], O.vdks(Po, Qo, 4200)[:2]
+    with K.Context() as c:
+        for _ in range(4):
+            assert c.vdks(dP, dQ, k)[:2] == w1
+        dP.copy_(dev(P2))
+        dQ.copy_(dev(Q2))
+        for _ in range(3):
+            assert c.vdks(dP, dQ, k)[:2] == w2
+            assert c.vdks(dPo, dQo, 4200)[:2] == wo
+        assert c.vdks(dP, dQ, k)[:2] == w2
+
+
+def test_graph_rdks_replay():
+    # ddks_rdks through its call graph: the bucket counts' known-zero state is part of the key; a call that falls
+    # back to the full sort (flag 256) leaves them dirty, and the next call must memset again (another key)
+    P1, Q1 = I.random_pair(71, 30000, 25000, 4, "normal")
+    P2, Q2 = I.random_pair(72, 30000, 25000, 4, "mixed")
+    rng = np.random.default_rng(7)
+    Pf = np.concatenate([rng.random((200, 2)), 0.5 + 1e-4 * rng.random((10000, 2))]).astype(np.float32)
+    Qf = np.concatenate([rng.random((300, 2)), 0.5 + 1e-4 * rng.random((9000, 2)) + 2e-5]).astype(np.float32)
+    Pf[0], Qf[0] = 0.0, 1.0
+    w1, w2, wf = (O.rdks(a, b) for a, b in ((P1, Q1), (P2, Q2), (Pf, Qf)))
+    dP, dQ, dPf, dQf = dev(P1), dev(Q1), dev(Pf), dev(Qf)
+
+    def same(r, w):
+        return (r.num, r.den, r.argmax_origin) == (w[0], w[1], w[3])
+
+    with K.Context() as c:
+        for _ in range(4):
+            assert same(c.rdks(dP, dQ), w1)
+        dP.copy_(dev(P2))
+        dQ.copy_(dev(Q2))
+        for _ in range(3):
+            assert same(c.rdks(dP, dQ), w2)
+            assert same(c.rdks(dPf, dQf), wf)
+        for _ in range(3):
+            assert same(c.rdks(dP, dQ), w2)
