@@ -40,7 +40,7 @@ FSET_LANES_PER_CLK_PER_SM = 64  # measured: microbench/pipes.cu FSET.BF.GE = 63.
 N_SM = 148
 
 
-RED_PEAK = 1.93e11  # global RED.ADD.u32 per second into L2-resident counts, measured (profiles/r3_red_global.txt)
+RED_PEAK = 1.93e11  # global RED.ADD.u32 per second into L2-resident counts, measured (profiles/r2b_red_global.txt)
 
 
 def parse():
@@ -354,7 +354,7 @@ class Step:
                 "reds_per_launch": int(reds), "kernel_ms_per_launch": per_launch_ms,
                 "kernel_share_of_step": per_launch_ms / step_ms if step_ms else None,
                 "peak_source": "microbench/red_global.cu: 12e6 uniform global RED.ADD.u32 into an L2-resident count "
-                               "array, steady state (profiles/r3_red_global.txt)"}
+                               "array, steady state (profiles/r2b_red_global.txt)"}
         return r
 
 

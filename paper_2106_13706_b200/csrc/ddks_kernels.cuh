@@ -45,7 +45,7 @@ template <int D> struct Cfg;
 #define DDKS_UNROLL 8
 #endif
 constexpr int kUnrollPts = DDKS_UNROLL;
-#ifndef DDKS_TWODIM  // experiment, measured slower (C5 651 vs 627 ms, profiles/r3_twodim_rejected.txt): kd tiles with two
+#ifndef DDKS_TWODIM  // experiment, measured slower (C5 651 vs 627 ms, profiles/r2b_twodim_rejected.txt): kd tiles with two
                      // compared dims left accumulate sum a, sum b, sum ab in registers
 #define DDKS_TWODIM 0
 #endif
