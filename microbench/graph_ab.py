@@ -9,16 +9,19 @@ from paper_2106_13706_b200 import ddks as K, inputs as I
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
 P5, Q5 = I.config("C5")
 P2, Q2 = I.config("C2")
+P3, Q3 = I.config("C3")
 P4, Q4 = I.config("C4")
 perms = I.c4_perms()
 pooled = np.concatenate([P4[I.C4_PERM_PAIR], Q4[I.C4_PERM_PAIR]])
 d5 = [torch.from_numpy(a).cuda() for a in (P5, Q5)]
 d2 = [torch.from_numpy(a).cuda() for a in (P2, Q2)]
+d3 = [torch.from_numpy(a).cuda() for a in (P3, Q3)]
 d4 = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (P4, Q4, pooled, perms)]
 calls = {
     "vdks C5 k16": lambda c: c.vdks(d5[0], d5[1], 16),
     "rdks C5": lambda c: c.rdks(d5[0], d5[1]),
     "stat C2": lambda c: c.stat(d2[0], d2[1]),
+    "stat C3": lambda c: c.stat(d3[0], d3[1]),
     "batch C4": lambda c: c.stat_batch(d4[0], d4[1]),
     "null C4": lambda c: c.permutation_null(d4[2], 512, d4[3]),
 }

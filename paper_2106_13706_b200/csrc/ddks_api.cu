@@ -775,7 +775,8 @@ ddks_status ddks_destroy(ddks_ctx* ctx) {
                       &ctx->rd_k1, &ctx->rd_hist, &ctx->rd_tcnt, &ctx->rd_cnum, &ctx->x0_keys0,
                       &ctx->x0_keys1, &ctx->x0_hist, &ctx->x0_pts, &ctx->x0_perm, &ctx->x0_pts2,
                       &ctx->x0_perm2, &ctx->x0_boxes, &ctx->prof_clk, &ctx->rdb_cnt,
-                      &ctx->rdb_pst, &ctx->rdb_coff, &ctx->rdb_fill, &ctx->rdb_clist, &ctx->rdb_csum, &ctx->rdb_bits})
+                      &ctx->rdb_pst, &ctx->rdb_coff, &ctx->rdb_fill, &ctx->rdb_clist, &ctx->rdb_csum, &ctx->rdb_bits,
+                      &ctx->kdf_bar, &ctx->kdf_buf})
         if (b->p) cudaFree(b->p);
     if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
     delete ctx;

@@ -172,7 +172,7 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
                                                                     (uint32_t*)ctx->rdb_fill.p,
                                                                     (uint32_t*)ctx->rdb_bits.p, clist, segc);
             // compaction: ~2 CTAs per SM in all, split over the segments; the segment's bitmap in dynamic SMEM
-            const int64_t cchunks = std::max<int64_t>(1, std::min<int64_t>((148 * 2 + nc - 1) / nc,
+            const int64_t cchunks = std::max<int64_t>(1, std::min<int64_t>((148 * DDKS_RDB_CPS + nc - 1) / nc,
                                                                            (N + ddks::RDB_CT - 1) / ddks::RDB_CT));
             ddks::k_rdb_compact<<<dim3((unsigned)cchunks, nc), ddks::RDB_CT, cbytes, st>>>(
                 k0, N, nbk, scale, (const uint32_t*)ctx->rdb_bits.p, (const uint32_t*)ctx->rdb_coff.p,

@@ -43,6 +43,7 @@ struct ddks_ctx {
     DevBuf rd_keys, rd_xn, rd_k0, rd_k1, rd_hist, rd_tcnt, rd_cnum;              // ddks_rdks workspace
     DevBuf x0_keys0, x0_keys1, x0_hist, x0_pts, x0_perm, x0_pts2, x0_perm2, x0_boxes;  // kd-ordered count workspace
     DevBuf rdb_cnt, rdb_pst, rdb_coff, rdb_fill, rdb_clist, rdb_csum, rdb_bits;  // rdKS bucket-pruned sweep
+    DevBuf kdf_bar, kdf_buf;  // fused mid-N kd ordering (k_kdb_fused): grid barrier; ranges, chunk totals, histograms
     void* rdb_zero_p = nullptr;  // rdb_cnt.p whose first rdb_zero bytes are known zero (the sweep re-zeroes the counts)
     size_t rdb_zero = 0;
     DevBuf prof_clk;  // [3] u64: SM cycles, globaltimer ns, executed compares summed over count CTAs (DDKS_FLAG_PROFILE)

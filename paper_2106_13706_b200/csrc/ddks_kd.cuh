@@ -127,36 +127,60 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     const float* src_pts = packed;
     const int32_t* src_perm = nullptr;
     if (bucket) {
-        int64_t cells_max = 1;
+        // the whole ordering (ranges, K bucket-sort levels, pad rows, tile boxes) in one cooperative launch; its
+        // histograms and ranges live in a buffer zeroed when allocated and left zeroed / reset by every launch
+        int64_t hwords = 0, cells = 1;
         const int64_t gl[4] = {kc.G0, kc.G1, kc.G2, kc.G3};
-        for (int l = 0; l + 1 < K; ++l) cells_max *= gl[l];
-        const int64_t nkeys = 2 * cells_max * ddks::KB_NBK;
-        if ((s = ensure(ctx, ctx->x0_hist, (size_t)std::max<int64_t>(nkeys, (int64_t)tiles_rs * 256) * 4 + 4 * K * 4 + 64)))
-            return s;
-        hist = (uint32_t*)ctx->x0_hist.p;
-        unsigned int* rng = (unsigned int*)(hist + nkeys);
-        uint32_t* keys = (uint32_t*)k0;  // [N] u32 keys in the first key buffer
-        ddks::k_kdb_range_init<<<1, 32, 0, st>>>(rng, 2 * K);  // min keys ~0, max keys 0
-        ddks::k_kdb_range<<<std::min(g, 148 * 2), 256, 0, st>>>(src_pts, DP, N, n_P, K, rng);
-        CHECK_LAUNCH();
-        ctx->launches += 2;
-        int64_t cells = 1;
-        for (int level = 0; level < K; ++level) {
-            const int64_t nk = 2 * cells * ddks::KB_NBK;
-            CU(cudaMemsetAsync(hist, 0, (size_t)nk * 4, st));
-            ddks::k_kdb_hist<<<g, 256, 0, st>>>(src_pts, DP, N, n_P, level, K, kc.G0, kc.G1, kc.G2, A, cells, rng,
-                                                 keys, hist);
-            ddks::k_kdb_scan<<<1, 1024, 0, st>>>(hist, nk);
-            const bool fin = ((K - 1 - level) % 2) == 0;
-            float* dst_pts = (float*)(fin ? ctx->x0_pts.p : ctx->x0_pts2.p);
-            int32_t* dst_perm = (int32_t*)(fin ? ctx->x0_perm.p : ctx->x0_perm2.p);
-            ddks::k_kdb_scatter<<<g, 256, 0, st>>>(src_pts, DP, N, keys, hist, src_perm, dst_pts, dst_perm);
+        for (int l = 0; l < K; ++l) hwords += 2 * cells * ddks::KB_NBK, cells *= gl[l];
+        int nsm = 148;
+        CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
+        nsm = std::min(nsm, ddks::KDF_MAXB);
+        // layout: ranges [2][4][2] words, chunk totals [KDF_MAXB], histograms [hwords]
+        const size_t kb_bytes = (size_t)(16 + ddks::KDF_MAXB + hwords) * 4;
+        if (ctx->kdf_buf.bytes < kb_bytes) {
+            if ((s = ensure(ctx, ctx->kdf_buf, kb_bytes))) return s;
+            CU(cudaMemsetAsync(ctx->kdf_buf.p, 0, ctx->kdf_buf.bytes, st));
+            ddks::k_kdb_range_init<<<1, 32, 0, st>>>((unsigned int*)ctx->kdf_buf.p, 8);  // ranges start at (~0, 0)
             CHECK_LAUNCH();
-            ctx->launches += 3;
-            src_pts = dst_pts;
-            src_perm = dst_perm;
-            cells *= gl[level];
+            ctx->launches++;
         }
+        if ((s = ensure_zeroed(ctx, ctx->kdf_bar, 64, st))) return s;  // barrier: arrived stays 0 between launches
+        if (K > 1) {
+            if ((s = ensure(ctx, ctx->x0_pts2, (size_t)N * DP * 4))) return s;
+            if ((s = ensure(ctx, ctx->x0_perm2, (size_t)N * 4))) return s;
+        }
+        ddks::KdbFusedArgs fa{};
+        fa.pts = packed;
+        fa.DP = DP;
+        fa.K = K;
+        fa.N = N;
+        fa.n_P = n_P;
+        fa.G0 = kc.G0;
+        fa.G1 = kc.G1;
+        fa.G2 = kc.G2;
+        fa.A = A;
+        fa.out[0] = (float*)ctx->x0_pts.p;
+        fa.out[1] = (float*)ctx->x0_pts2.p;
+        fa.perm[0] = (int32_t*)ctx->x0_perm.p;
+        fa.perm[1] = (int32_t*)ctx->x0_perm2.p;
+        fa.keys = (uint32_t*)k0;
+        fa.rng = (uint32_t*)ctx->kdf_buf.p;
+        fa.tot = fa.rng + 16;
+        fa.hist = fa.tot + ddks::KDF_MAXB;
+        fa.bar = (uint32_t*)ctx->kdf_bar.p;
+        fa.boxes = (float*)ctx->x0_boxes.p;
+        fa.TILE = G::TILE;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)nsm, 1, 1);
+        cfg.blockDim = dim3(ddks::KDF_T, 1, 1);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;  // every CTA resident: the grid barriers cannot deadlock
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CU(cudaLaunchKernelEx(&cfg, ddks::k_kdb_fused, fa));
+        ctx->launches++;
     }
     for (int level = 0; level < (bucket ? 0 : K); ++level) {
         const int64_t gl[4] = {kc.G0, kc.G1, kc.G2, kc.G3};
@@ -184,6 +208,7 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
         src_pts = dst_pts;
         src_perm = dst_perm;
     }
+    bool boxes_done = bucket;  // the fused mid-N ordering wrote the pad rows and the tile boxes
     // TEST ONLY (DDKS_KD_SHUFFLE=m): scramble the rows inside each label run (position p -> p * m mod n, m odd and
     // coprime to n) after the kd sort. The counts must not depend on the order -- only the speed does.
     if (const char* e = getenv("DDKS_KD_SHUFFLE")) {
@@ -193,6 +218,7 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
             if ((s = ensure(ctx, ctx->x0_perm2, (size_t)N * 4))) return s;
             CU(cudaMemcpyAsync(ctx->x0_pts2.p, ctx->x0_pts.p, (size_t)N * DP * 4, cudaMemcpyDeviceToDevice, st));
             CU(cudaMemcpyAsync(ctx->x0_perm2.p, ctx->x0_perm.p, (size_t)N * 4, cudaMemcpyDeviceToDevice, st));
+            boxes_done = false;  // the boxes must describe the shuffled rows
             ddks::k_shuffle_runs<<<g, 256, 0, st>>>((const float*)ctx->x0_pts2.p, (const int32_t*)ctx->x0_perm2.p, DP,
                                                      N, n_P, m, (float*)ctx->x0_pts.p, (int32_t*)ctx->x0_perm.p);
             CHECK_LAUNCH();
@@ -200,11 +226,13 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
         }
     }
     float* spts = (float*)ctx->x0_pts.p;
-    CU(cudaMemsetAsync(spts + N * DP, 0, 4 * DP * 4, st));  // the prefetch past the last row reads zeros
-    ddks::k_tile_boxes<<<(int)std::max<int64_t>(1, std::min<int64_t>((n_tiles + 7) / 8, 148 * 16)), 256, 0, st>>>(
-        spts, DP, N, G::TILE, K, (float*)ctx->x0_boxes.p);
-    CHECK_LAUNCH();
-    ctx->launches++;
+    if (!boxes_done) {
+        CU(cudaMemsetAsync(spts + N * DP, 0, 4 * DP * 4, st));  // the prefetch past the last row reads zeros
+        ddks::k_tile_boxes<<<(int)std::max<int64_t>(1, std::min<int64_t>((n_tiles + 7) / 8, 148 * 16)), 256, 0, st>>>(
+            spts, DP, N, G::TILE, K, (float*)ctx->x0_boxes.p);
+        CHECK_LAUNCH();
+        ctx->launches++;
+    }
     const uint64_t gg = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
     const uint32_t a_ = (uint32_t)((uint64_t)n_Q / gg), b_ = (uint32_t)((uint64_t)n_P / gg);
     // all N origins (positions of the kd order); shard r of W takes origin blocks r, r + W, r + 2W, ... so every

@@ -1102,6 +1102,192 @@ __global__ void k_kdb_scatter(const float* __restrict__ pts, int DP, int64_t N, 
     }
 }
 
+// ---- the whole mid-N kd ordering in ONE cooperative launch (k_kdb_fused) -------------------------------------------
+// The same bucket counting sorts as k_kdb_range / k_kdb_hist / k_kdb_scan / k_kdb_scatter / k_tile_boxes (identical
+// keys, cells and boxes), phase after phase inside one persistent grid separated by grid barriers, instead of ~10
+// dependent launches and memsets. The scan of a level's histogram is spread over all CTAs (each scans its chunk;
+// the scatter adds the exclusive prefix of the chunk totals, which every CTA forms in SMEM), and the histograms and
+// ranges are left zeroed / reset at the end of the launch for the next one (the buffer is zeroed when allocated).
+// Launched with the cooperative attribute (every CTA resident, so the barriers cannot deadlock).
+constexpr int KDF_T = 512, KDF_MAXB = 1024;  // threads per CTA, CTAs at most (chunk totals in SMEM)
+struct KdbFusedArgs {
+    const float* pts;              // packed rows [N][DP] (P rows, then Q rows)
+    int DP, K;
+    int64_t N, n_P, G0, G1, G2, A;
+    float* out[2];                 // ping-pong row buffers; level l writes out[(K - 1 - l) & 1] (the last: out[0])
+    int32_t* perm[2];              // the same for the permutations (sorted position -> pooled index)
+    uint32_t* keys;                // [N] this level's key of every row
+    uint32_t* hist;                // levels' histograms back to back: 2 cells_l KB_NBK words each (zero at entry)
+    uint32_t* rng;                 // [2 labels][K][2] order-preserving min / max keys (~0 / 0 at entry)
+    uint32_t* tot;                 // [gridDim.x] chunk totals of the current level's histogram
+    uint32_t* bar;                 // grid barrier {arrived, generation} (arrived 0 between launches)
+    float* boxes;                  // [n_tiles][K][2] tile min / max of x_0..x_{K-1}
+    int TILE;
+};
+
+// sense-reversing grid barrier (all CTAs resident: cooperative launch)
+__device__ __forceinline__ void kdf_grid_sync(uint32_t* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile uint32_t* vb = bar;
+        const uint32_t gen = vb[1];
+        __threadfence();
+        if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
+            bar[0] = 0u;
+            __threadfence();
+            atomicAdd(&bar[1], 1u);
+        } else {
+            while (vb[1] == gen) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// exclusive scan of h[0, n) in place by one CTA of KDF_T threads (contiguous sub-chunks per thread); returns the total
+__device__ __forceinline__ uint32_t kdf_block_scan(uint32_t* h, int64_t n, uint32_t* wsum) {
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int64_t per = (n + KDF_T - 1) / KDF_T;
+    const int64_t b0 = min(n, t * per), b1 = min(n, b0 + per);
+    uint32_t sum = 0;
+    for (int64_t i = b0; i < b1; ++i) sum += __ldcg(h + i);
+    uint32_t x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t v = lane < KDF_T / 32 ? wsum[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        if (lane < KDF_T / 32) wsum[lane] = v;
+    }
+    __syncthreads();
+    uint32_t run = x - sum + (w ? wsum[w - 1] : 0u);
+    const uint32_t total = wsum[KDF_T / 32 - 1];
+    for (int64_t i = b0; i < b1; ++i) {
+        const uint32_t c = __ldcg(h + i);
+        h[i] = run;
+        run += c;
+    }
+    __syncthreads();  // wsum is reused
+    return total;
+}
+
+__global__ void __launch_bounds__(KDF_T) k_kdb_fused(const KdbFusedArgs a) {
+    __shared__ uint32_t wsum[KDF_T / 32];
+    __shared__ uint32_t toff[KDF_MAXB];  // exclusive prefix of the chunk totals
+    const int64_t gt = blockIdx.x * (int64_t)KDF_T + threadIdx.x, gs = (int64_t)gridDim.x * KDF_T;
+    const int K = a.K, DP = a.DP, nb = gridDim.x;
+    const int64_t N = a.N, n_P = a.n_P;
+    const int64_t gl[3] = {a.G0, a.G1, a.G2};
+    // phase 1: per-label min / max of x_0..x_{K-1} (as k_kdb_range)
+    for (int k = 0; k < K; ++k) {
+        uint32_t lo[2] = {~0u, ~0u}, hi[2] = {0u, 0u};
+        for (int64_t j = gt; j < N; j += gs) {
+            const uint32_t v = f32_key(a.pts[j * DP + k]);
+            const int lab = j >= n_P;
+            lo[lab] = v < lo[lab] ? v : lo[lab];
+            hi[lab] = v > hi[lab] ? v : hi[lab];
+        }
+#pragma unroll
+        for (int lab = 0; lab < 2; ++lab) {
+#pragma unroll
+            for (int sh = 16; sh; sh >>= 1) {
+                lo[lab] = min(lo[lab], __shfl_xor_sync(0xffffffffu, lo[lab], sh));
+                hi[lab] = max(hi[lab], __shfl_xor_sync(0xffffffffu, hi[lab], sh));
+            }
+            if ((threadIdx.x & 31) == 0) {
+                atomicMin(&a.rng[(lab * K + k) * 2], lo[lab]);
+                atomicMax(&a.rng[(lab * K + k) * 2 + 1], hi[lab]);
+            }
+        }
+    }
+    kdf_grid_sync(a.bar);
+    // levels: histogram of the (label, cell, bucket) keys, distributed scan, scatter (as k_kdb_hist / _scan / _scatter)
+    const float* src = a.pts;
+    const int32_t* src_perm = nullptr;
+    int64_t cells = 1, hoff = 0;
+    for (int level = 0; level < K; ++level) {
+        uint32_t* h = a.hist + hoff;
+        const int64_t nk = 2 * cells * KB_NBK;
+        const int64_t chunk = (nk + nb - 1) / nb;
+        for (int64_t j = gt; j < N; j += gs) {
+            const uint32_t key = kdb_key(src, DP, j, N, n_P, level, K, a.G0, a.G1, a.G2, a.A, cells, a.rng);
+            a.keys[j] = key;
+            atomicAdd(&h[key], 1u);
+        }
+        kdf_grid_sync(a.bar);
+        {
+            const int64_t c0 = min(nk, blockIdx.x * chunk), c1 = min(nk, c0 + chunk);
+            const uint32_t t = kdf_block_scan(h + c0, c1 - c0, wsum);
+            if (threadIdx.x == 0) a.tot[blockIdx.x] = t;
+        }
+        kdf_grid_sync(a.bar);
+        // every CTA: exclusive prefix of the chunk totals in SMEM (nb <= KDF_MAXB)
+        for (int i = threadIdx.x; i < nb; i += KDF_T) toff[i] = __ldcg(a.tot + i);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t run = 0;
+            for (int i = 0; i < nb; ++i) {
+                const uint32_t c = toff[i];
+                toff[i] = run;
+                run += c;
+            }
+        }
+        __syncthreads();
+        const int o = (K - 1 - level) & 1;
+        float* dst = a.out[o];
+        int32_t* dperm = a.perm[o];
+        for (int64_t j = gt; j < N; j += gs) {
+            const uint32_t key = a.keys[j];
+            const int64_t pos = (int64_t)toff[key / chunk] + atomicAdd(&h[key], 1u);
+            DDKS_ASSERT(pos < N);
+            const float4* sp = reinterpret_cast<const float4*>(src + j * DP);
+            float4* dp = reinterpret_cast<float4*>(dst + pos * DP);
+            dp[0] = __ldcg(sp);  // rows written by other CTAs before the barrier: read through L2
+            if (DP == 8) dp[1] = __ldcg(sp + 1);
+            dperm[pos] = src_perm ? __ldcg(src_perm + j) : (int32_t)j;
+        }
+        kdf_grid_sync(a.bar);
+        src = dst;
+        src_perm = dperm;
+        hoff += nk;
+        cells *= (level < 3 ? gl[level] : 1);
+    }
+    // tail: 4 zero rows after the last one (the count's prefetch reads them), tile boxes (as k_tile_boxes), and the
+    // histograms / ranges reset for the next launch
+    for (int64_t i = gt; i < hoff; i += gs) a.hist[i] = 0u;
+    if (gt < 2 * K) a.rng[2 * gt] = ~0u, a.rng[2 * gt + 1] = 0u;
+    float* fin = a.out[0];
+    if (gt < 4 * DP) fin[N * DP + gt] = 0.0f;
+    const int64_t n_tiles = (N + a.TILE - 1) / a.TILE;
+    const int lane = threadIdx.x & 31;
+    for (int64_t w = gt >> 5; w < n_tiles; w += gs >> 5) {
+        const int64_t r0 = w * a.TILE, r1 = min(N, r0 + a.TILE);
+        for (int k = 0; k < K; ++k) {
+            float lo = INFINITY, hi = -INFINITY;
+            for (int64_t r = r0 + lane; r < r1; r += 32) {
+                const float v = __ldcg(fin + r * DP + k);
+                lo = fminf(lo, v), hi = fmaxf(hi, v);
+            }
+#pragma unroll
+            for (int sh = 16; sh; sh >>= 1) {
+                lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, sh));
+                hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, sh));
+            }
+            if (lane == 0) a.boxes[(w * K + k) * 2] = lo, a.boxes[(w * K + k) * 2 + 1] = hi;
+        }
+    }
+}
+
 // out[j] = pts[idx_j] (whole padded rows), perm_out[j] = perm_in[idx_j] (perm_in == nullptr: idx_j), idx_j = the low
 // ib bits of the sorted key j (pooled indices < 2^31)
 __global__ void k_permute_rows(const float* __restrict__ pts, int DP, int64_t N, const uint64_t* __restrict__ keys,

@@ -341,6 +341,12 @@ __global__ void k_rdb_cand(uint32_t* __restrict__ cnt, const uint2* __restrict__
 // the CTA holds segment s's candidate bitmap in SMEM (nbk / 8 bytes), so a non-candidate key costs its coalesced
 // load, its bucket and one shared-memory bit test; only candidate keys touch coff / fill (global).
 constexpr int RDB_CT = 512;
+#ifndef DDKS_RDB_U  // experiments: keys in flight per compaction thread, compaction CTAs per SM
+#define DDKS_RDB_U 4
+#endif
+#ifndef DDKS_RDB_CPS
+#define DDKS_RDB_CPS 3
+#endif
 __global__ void __launch_bounds__(RDB_CT) k_rdb_compact(const uint64_t* __restrict__ key, int64_t N, int nbk,
                                                         double scale, const uint32_t* __restrict__ cbits,
                                                         const uint32_t* __restrict__ coff, uint32_t* __restrict__ fill,
@@ -352,7 +358,7 @@ __global__ void __launch_bounds__(RDB_CT) k_rdb_compact(const uint64_t* __restri
     __syncthreads();
     const uint32_t* sbits = reinterpret_cast<const uint32_t*>(sbits4);
     const uint64_t* ks = key + (int64_t)s * N;
-    constexpr int U = 4;  // keys in flight per thread
+    constexpr int U = DDKS_RDB_U;  // keys in flight per thread
     const int64_t gs = (int64_t)gridDim.x * RDB_CT;
     for (int64_t e0 = blockIdx.x * (int64_t)RDB_CT + threadIdx.x; e0 < N; e0 += U * gs) {
         uint64_t k[U];
