@@ -82,9 +82,10 @@ typedef enum {
 #define DDKS_FLAG_KD_SHIFT 16u     /* TEST ONLY: bits 16..18 = K in 1..4 force the number of kd levels (0: cost model;
                                       K is capped at d and at the deepest level built, 4)                           */
 #define DDKS_FLAG_KD_LEVELS(k) (((unsigned)(k) & 7u) << DDKS_FLAG_KD_SHIFT)
-#define DDKS_FLAG_NO_GRAPH 4096u   /* never capture ddks_stat into a CUDA graph (by default the second identical call --
-                                      same input pointers, sizes and workspace -- is captured and later calls replay it
-                                      with one cudaGraphLaunch; identical results)                                     */
+#define DDKS_FLAG_NO_GRAPH 4096u   /* never capture a call into a CUDA graph (by default the second identical call of
+                                      ddks_stat, ddks_stat_batch, ddks_permutation_null, ddks_vdks or ddks_rdks -- same
+                                      input pointers, sizes, flags and workspace -- is captured and later calls replay
+                                      it with one cudaGraphLaunch; identical results; host inputs must then be pinned) */
 #define DDKS_FLAG_NCCL_SELF 2048u  /* TEST ONLY (world == 1): create a one-rank NCCL communicator and run every collective
                                       of the multi-GPU path (all-reduce / all-gather) through it; identical results */
 #define DDKS_FLAG_RDKS_FULL_SORT 128u /* TEST ONLY: ddks_rdks sorts every key (8-pass radix sort) instead of the bucket-pruned
