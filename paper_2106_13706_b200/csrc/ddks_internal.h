@@ -71,6 +71,9 @@ struct ddks_ctx {
     StatKey sg_seen, sg_key;
     cudaGraphExec_t sg_exec = nullptr;
     cudaStream_t cap_stream = nullptr;
+    // host-input batches: H2D copies of item chunks on copy_stream, overlapped with the counts of earlier chunks
+    cudaStream_t copy_stream = nullptr;
+    std::vector<cudaEvent_t> copy_evs;
     int64_t sg_launches = 0;
     int sg_kd_levels = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> sg_evs;

@@ -210,3 +210,27 @@ def test_graph_rdks_replay():
             assert same(c.rdks(dPf, dQf), wf)
         for _ in range(3):
             assert same(c.rdks(dP, dQ), w2)
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_batch_host_inputs_chunked_copies(pinned):
+    # host-input batches of >= 8 MB: the H2D copies run in item chunks on a copy stream, overlapped with the counts of
+    # the earlier chunks (captured with a fork / join when the inputs are pinned); results equal the device-input call
+    B, n_P, n_Q, d = 600, 1024, 1000, 4
+    rng = np.random.default_rng(91)
+    P = rng.standard_normal((B, n_P, d)).astype(np.float32)
+    Q = (1.1 * rng.standard_normal((B, n_Q, d))).astype(np.float32)
+    spots = [0, 149, 150, 151, 299, 300, 449, 450, 599]
+    want = {b: O.ddks(P[b], Q[b])[0] for b in spots}
+    with K.Context() as c:
+        ref = [int(v) for v in c.stat_batch(dev(P), dev(Q)).num]
+        assert all(ref[b] == w for b, w in want.items())
+        hP, hQ = torch.from_numpy(P), torch.from_numpy(Q)
+        if pinned:
+            hP, hQ = hP.pin_memory(), hQ.pin_memory()
+        for _ in range(4):  # plain, capture, replay, replay (pinned)
+            assert [int(v) for v in c.stat_batch(hP, hQ).num] == ref
+        P2 = np.ascontiguousarray(P[::-1])
+        hP.copy_(torch.from_numpy(P2))  # new contents in the same host buffer
+        got = [int(v) for v in c.stat_batch(hP, hQ).num]
+        assert all(got[b] == O.ddks(P2[b], Q[b])[0] for b in (0, 300, 599))
