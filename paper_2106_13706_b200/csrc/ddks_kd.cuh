@@ -9,6 +9,7 @@
 #include <cstdlib>
 
 #include "ddks_kernels.cuh"
+#include "ddks_kd_cluster.cuh"
 #include "ddks_internal.h"
 #include "ddks_launch.cuh"
 
@@ -126,7 +127,44 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 16));
     const float* src_pts = packed;
     const int32_t* src_perm = nullptr;
-    if (bucket) {
+    // mid-N ordering, preferred form: one thread-block cluster per label run (runs <= 65536 rows, <= 16384 cells)
+    bool cluster_path = false;
+    if (bucket && !getenv("DDKS_KD_FUSED")) {
+        int64_t cmax = 1;
+        const int64_t gl[4] = {kc.G0, kc.G1, kc.G2, kc.G3};
+        for (int l = 0; l + 1 < K; ++l) cmax *= gl[l];
+        cluster_path = K <= 4 && cmax <= ddks::KDC_HW &&
+                       std::max(n_P, n_Q) <= (int64_t)ddks::KDC_CS * ddks::KDC_T * ddks::KDC_RPT;
+    }
+    if (cluster_path) {
+        if (K > 1) {
+            if ((s = ensure(ctx, ctx->x0_pts2, (size_t)N * DP * 4))) return s;
+            if ((s = ensure(ctx, ctx->x0_perm2, (size_t)N * 4))) return s;
+        }
+        static std::atomic<bool> attr_set[kMaxDevices] = {};
+        if (!attr_set[ctx->device].load(std::memory_order_acquire)) {
+            CU(cudaFuncSetAttribute(ddks::k_kdb_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, ddks::KDC_SMEM));
+            attr_set[ctx->device].store(true, std::memory_order_release);
+        }
+        ddks::KdcArgs ca{};
+        ca.pts = packed;
+        ca.DP = DP;
+        ca.K = K;
+        ca.N = N;
+        ca.n_P = n_P;
+        ca.G0 = kc.G0;
+        ca.G1 = kc.G1;
+        ca.G2 = kc.G2;
+        ca.A = A;
+        ca.out[0] = (float*)ctx->x0_pts.p;
+        ca.out[1] = (float*)ctx->x0_pts2.p;
+        ca.perm[0] = (int32_t*)ctx->x0_perm.p;
+        ca.perm[1] = (int32_t*)ctx->x0_perm2.p;
+        ddks::k_kdb_cluster<<<2 * ddks::KDC_CS, ddks::KDC_T, ddks::KDC_SMEM, st>>>(ca);
+        CHECK_LAUNCH();
+        ctx->launches++;
+    }
+    if (bucket && !cluster_path) {
         // the whole ordering (ranges, K bucket-sort levels, pad rows, tile boxes) in one cooperative launch; its
         // histograms and ranges live in a buffer zeroed when allocated and left zeroed / reset by every launch
         int64_t hwords = 0, cells = 1;
@@ -208,7 +246,7 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
         src_pts = dst_pts;
         src_perm = dst_perm;
     }
-    bool boxes_done = bucket;  // the fused mid-N ordering wrote the pad rows and the tile boxes
+    bool boxes_done = bucket && !cluster_path;  // the fused mid-N ordering wrote the pad rows and the tile boxes
     // TEST ONLY (DDKS_KD_SHUFFLE=m): scramble the rows inside each label run (position p -> p * m mod n, m odd and
     // coprime to n) after the kd sort. The counts must not depend on the order -- only the speed does.
     if (const char* e = getenv("DDKS_KD_SHUFFLE")) {
