@@ -617,7 +617,7 @@ bool graph_input_ok(const void* p) {
 bool env_overrides() {
     return getenv("DDKS_KD") || getenv("DDKS_SEGS") || getenv("DDKS_KD_SHUFFLE") || getenv("DDKS_NO_KEY") ||
            getenv("DDKS_GRIDY") || getenv("DDKS_NO_SMALL") || getenv("DDKS_KD_RADIX") || getenv("DDKS_NO_MMA") ||
-           getenv("DDKS_PERM_GROUP");
+           getenv("DDKS_PERM_GROUP") || getenv("DDKS_KD_FUSED");
 }
 
 void drop_call_graph(ddks_ctx* ctx, ddks_ctx::CallGraph& cg) {
