@@ -133,7 +133,7 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
         int64_t cmax = 1;
         const int64_t gl[4] = {kc.G0, kc.G1, kc.G2, kc.G3};
         for (int l = 0; l + 1 < K; ++l) cmax *= gl[l];
-        cluster_path = K <= 4 && cmax <= ddks::KDC_HW &&
+        cluster_path = K <= 4 && cmax < ddks::KDC_HW &&  // cells + 1 cell starts fit the offset words
                        std::max(n_P, n_Q) <= (int64_t)ddks::KDC_CS * ddks::KDC_T * ddks::KDC_RPT;
     }
     if (cluster_path) {
