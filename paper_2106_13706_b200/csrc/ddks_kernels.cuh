@@ -65,7 +65,11 @@ template <> struct Cfg<2> { static constexpr int R = 8, T = 256, TILE = 512, S =
 #define DDKS_C3TILE 512
 #endif
 template <> struct Cfg<3> { static constexpr int R = DDKS_C3R, T = DDKS_C3T, TILE = DDKS_C3TILE, S = 3; };
-template <> struct Cfg<4> { static constexpr int R = 4, T = 256, TILE = 512, S = 3; };
+#ifndef DDKS_C4R  // geometry experiments (d = 4; the C4 batch: one 1024-origin item per CTA)
+#define DDKS_C4R 4
+#define DDKS_C4T 256
+#endif
+template <> struct Cfg<4> { static constexpr int R = DDKS_C4R, T = DDKS_C4T, TILE = 512, S = 3; };
 #ifndef DDKS_C5R  // geometry experiments: -DDDKS_C5R=.. -DDDKS_C5T=.. -DDDKS_C5TILE=.. -DDDKS_C5S=..
 // d = 5: R = 4 x 16 warps, 2048 origins per CTA (round 2, with the one-dim register path: C5 count 636.6 -> 630.7 ms
 // vs R = 6 x 16 warps; R = 8 x 12 643, R = 6 x 12 653, R = 4 x 24 721, R = 12 x 8 684, R = 2 x 32 782 ms --
