@@ -329,7 +329,7 @@ class Step:
         else:
             keys = (d + 1) * N * 8
             nbk = 256
-            while nbk < N // 4 and nbk < (1 << 20):
+            while nbk < N // (8 if N >= (1 << 20) else 4) and nbk < (1 << 20):  # as ddks_api_rdks.cu
                 nbk <<= 1
             # input read twice in place (min/max; distance keys with NormalizeData fused), key write, one key read
             # (candidate compaction), and per bucket: count atomics, two scan reads, start-count write, candidate

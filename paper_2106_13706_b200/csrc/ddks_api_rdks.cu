@@ -13,6 +13,13 @@
 
 using namespace ddks_host;
 
+// about N / 4 distance buckets per corner, N / 8 from 2^20 rows (C5: 189 -> 175 us per graphed call; N / 8 is 2-3 us
+// slower at C2 / C3, N / 16 slower everywhere: profiles/r2b_rdks_buckets.txt); DDKS_RDB_DIV (experiments) forces one
+#ifndef DDKS_RDB_DIV
+#define DDKS_RDB_DIV 0
+#endif
+static int64_t rdb_bucket_div(int64_t N) { return DDKS_RDB_DIV ? DDKS_RDB_DIV : (N >= (int64_t(1) << 20) ? 8 : 4); }
+
 // distance keys (+ bucket counts when cnt): per point for d <= 8 (x' computed once), per (point, corner) otherwise
 static void launch_rd_keys(const float* P, const float* Q, const double* xn, int64_t N, int64_t n_P, int d,
                            const uint32_t* keys, int cb, int ce, uint64_t* key, uint32_t* cnt, int nbk, double scale,
@@ -86,7 +93,7 @@ ddks_status ddks_rdks(ddks_ctx* ctx, const float* P, int64_t n_P, const float* Q
     // are known zero (no memset of nb * 8 bytes); the memset this implies is part of the call graph and its key
     const bool pruned = !(ctx->flags & DDKS_FLAG_RDKS_FULL_SORT);
     int nbk = 256;
-    while (nbk < N / 4 && nbk < (1 << 20)) nbk <<= 1;
+    while (nbk < N / rdb_bucket_div(N) && nbk < (1 << 20)) nbk <<= 1;
     const double scale = (double)nbk / (std::sqrt((double)d) * (1.0 + 1e-9));
     const size_t nb = (size_t)nc * nbk;
     const int nch = (nbk + ddks::RDB_CH - 1) / ddks::RDB_CH;
