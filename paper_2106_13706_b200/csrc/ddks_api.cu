@@ -226,8 +226,11 @@ bool x0_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q) {
     // (microbench/kd_threshold.py, profiles/r2_kd_midN_bucket.txt): radix-sorted kd at N ~ 60k-75k for d = 2..8; with
     // the mid-N bucket sort (single rank) at N ~ 40k for d = 3..8 (N = 40k: d = 3 1.05x, d = 4 1.05x, d = 5 1.04x,
     // d = 8 1.13x; N = 20k: 0.72-0.93x)
+    // With the cluster ordering (round 2, second session; profiles/r2b_kd_threshold.txt): d = 8 pays from N = 20 000
+    // (1.03x, 1.12x at 30 000), d = 3 from ~30 000 (1.15x), d = 4..6 only from ~40 000 (1.00-1.06x)
     const bool single = ctx->world == 1;
-    const int64_t min_n = (ctx->flags & DDKS_FLAG_FORCE_X0) ? 2 : (single && d >= 3 ? 40000 : 80000);
+    const int64_t mid = d >= 8 ? 20000 : (d == 3 ? 28000 : 40000);
+    const int64_t min_n = (ctx->flags & DDKS_FLAG_FORCE_X0) ? 2 : (single && d >= 3 ? mid : 80000);
     return d >= 2 && d <= 8 && n_P + n_Q >= min_n;
 }
 
