@@ -483,3 +483,17 @@ def test_profile_clock_probe():
     with K.Context() as c:
         c.stat(dev(P), dev(Q))
         assert c.profile_clock() == 0.0  # no probe without the flag
+
+
+@pytest.mark.parametrize("n_P,n_Q,d,kind", [(12000, 11000, 8, "normal"), (15000, 14000, 3, "mixed"),
+                                            (21000, 19500, 5, "grid")])
+def test_default_mid_n_kd_path(n_P, n_Q, d, kind):
+    # sizes just above the default kd thresholds (d = 8 from 20 000 rows, d = 3 from 28 000, d = 5 from 40 000): the
+    # unforced call takes the kd count with the cluster mid-N ordering and must equal the oracle bit for bit
+    P, Q = I.random_pair(9700 + d, n_P, n_Q, d, kind)
+    if kind == "grid":
+        P[:, :2] = np.round(P[:, :2] * 4) / 4
+        Q[:, :2] = np.round(Q[:, :2] * 4) / 4
+    with K.Context() as c:
+        check_pair(c, P, Q)
+        assert c.kd_levels >= 1
