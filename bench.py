@@ -464,6 +464,13 @@ def main():
     if args.method in ("exact", "significance"):
         roof["kernel_share_of_step"] = kern_ms_max / total_ms if total_ms else None
         roof["kd_levels"] = ctx.kd_levels
+        roof["rank_lanes"] = ctx.rank_lanes
+        if ctx.rank_lanes:
+            roof["kernel"] = "k_count_rank (classify + count on 10-bit rank lanes)"
+            roof["note"] = ("rank-lane count (d >= 6): each pair's d compares run as three 32-bit integer adds on "
+                            "per-CTA 10-bit rank lanes (exact; DESIGN.md §7 'rank lanes'), so d compares per pair "
+                            "against the FP32-compare lane peak is the compare-equivalent rate, and the kernel is "
+                            "bound by instruction issue (~11 instructions per pair), not by the compare pipe")
         if ctx.kd_levels:
             roof["note"] = (f"kd ordering: bits 0..{ctx.kd_levels - 1} are decided once per tile for most tiles, so fewer "
                             "than d compares are executed per pair and frac (algorithmic d compares per pair) can "

@@ -123,6 +123,22 @@ ddks_status check_sizes(ddks_ctx* ctx, int64_t n_P, int64_t n_Q, int32_t d) {
 int pad_dim(int d) { return d <= 4 ? 4 : 8; }
 
 // ------------------------------------------------------------------------------------- count dispatch
+// DIFF counters fit (|c_P a - c_Q b| stays in int32 and the int16 window is >= 4096 points); else SPLIT
+bool diff_counters_ok(int64_t n_P, int64_t n_Q);
+
+// the rank-lane count (ddks_rank.cuh) takes a position-ordered DIFF statistic at 6 <= d <= 8 in its measured range
+// (any size with DDKS_FLAG_FORCE_RANK); the >= convention only; not for the small geometry
+bool rank_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q) {
+    if (ctx->flags & (DDKS_FLAG_NO_RANK | DDKS_FLAG_TIES_GT)) return false;
+    if (d < 6 || d > 8 || n_P + n_Q <= ddks::kSmallN || !diff_counters_ok(n_P, n_Q)) return false;
+    if (ctx->flags & DDKS_FLAG_FORCE_RANK) return true;
+    // measured against the kd-ordered and position-ordered FP32 counts (microbench/rank_ab.py,
+    // profiles/r2e_rank_ab.txt): d = 8 faster at N = 1e4 .. 4e5 (C3 0.90 vs 1.16 ms per call; 78 vs 81 ms at 4e5,
+    // the kd count's decided bits catch up beyond), d = 6 and 7 up to N ~ 5e4
+    const int64_t N = n_P + n_Q;
+    return d == 8 ? N <= 600000 : N <= 50000;
+}
+
 template <int D>
 ddks_status launch_count_d(ddks_ctx* ctx, const CountPlan& pl, const ddks::CountArgs& a, cudaStream_t st, bool wx) {
     const bool gt = (ctx->flags & DDKS_FLAG_TIES_GT) != 0;
@@ -147,6 +163,8 @@ ddks_status launch_count_d(ddks_ctx* ctx, const CountPlan& pl, const ddks::Count
 ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int64_t n_P, int64_t n_Q,
                       int64_t o_begin, int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st,
                       bool force_split, unsigned long long* hist, bool wx, unsigned long long* best_key) {
+    if (B == 1 && !force_split && rank_applicable(ctx, d, n_P, n_Q))  // d = 8: the rank-lane count (ddks_rank.cuh)
+        return run_count_rank(ctx, packed, d, n_P, n_Q, o_begin, o_end, item_num, per_origin, st, best_key);
     const int64_t N = n_P + n_Q;
     const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
     const uint64_t a_ = (uint64_t)n_Q / g, b_ = (uint64_t)n_P / g;
@@ -228,6 +246,8 @@ bool x0_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q) {
     // d = 8 1.13x; N = 20k: 0.72-0.93x)
     // With the cluster ordering (round 2, second session; profiles/r2b_kd_threshold.txt): d = 8 pays from N = 20 000
     // (1.03x, 1.12x at 30 000), d = 3 from ~30 000 (1.15x), d = 4..6 only from ~40 000 (1.00-1.06x)
+    // the rank-lane count beats the kd ordering at d = 8 (and is position-ordered: no sort)
+    if (!(ctx->flags & DDKS_FLAG_FORCE_X0) && rank_applicable(ctx, d, n_P, n_Q)) return false;
     const bool single = ctx->world == 1;
     const int64_t mid = d >= 8 ? 20000 : (d == 3 ? 28000 : 40000);
     const int64_t min_n = (ctx->flags & DDKS_FLAG_FORCE_X0) ? 2 : (single && d >= 3 ? mid : 80000);
@@ -286,6 +306,7 @@ ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n
         return DDKS_OK;
     }
     ctx->kd_levels = 0;
+    ctx->rank_lanes = 0;  // set by run_count_rank when the rank-lane count runs
     uint64_t* per = nullptr;
     if (!use_key) {
         if ((s = ensure(ctx, ctx->per_origin, (size_t)std::max<int64_t>(oe - ob, 1) * 8))) return s;
@@ -620,7 +641,7 @@ bool graph_input_ok(const void* p) {
 bool env_overrides() {
     return getenv("DDKS_KD") || getenv("DDKS_SEGS") || getenv("DDKS_KD_SHUFFLE") || getenv("DDKS_NO_KEY") ||
            getenv("DDKS_GRIDY") || getenv("DDKS_NO_SMALL") || getenv("DDKS_KD_RADIX") || getenv("DDKS_NO_MMA") ||
-           getenv("DDKS_PERM_GROUP") || getenv("DDKS_KD_FUSED");
+           getenv("DDKS_PERM_GROUP") || getenv("DDKS_KD_FUSED") || getenv("DDKS_RANK_SK");
 }
 
 void drop_call_graph(ddks_ctx* ctx, ddks_ctx::CallGraph& cg) {
@@ -710,7 +731,7 @@ ddks_status ddks_create(ddks_ctx** out, int device, int world, int rank, const v
     if (world < 1 || rank < 0 || rank >= world) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad world/rank");
     if ((world == 1) != (nccl_id == nullptr))
         return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "nccl_id must be NULL iff world == 1");
-    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT | DDKS_FLAG_PROFILE | DDKS_FLAG_PERM_GATHER | DDKS_FLAG_NO_X0 | DDKS_FLAG_FORCE_X0 | DDKS_FLAG_RDKS_FULL_SORT | DDKS_FLAG_KD_LEVELS(7) | DDKS_FLAG_NCCL_SELF | DDKS_FLAG_NO_GRAPH)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
+    if (flags & ~(DDKS_FLAG_NO_VALIDATE | DDKS_FLAG_TIES_GT | DDKS_FLAG_FORCE_DIRECT | DDKS_FLAG_PROFILE | DDKS_FLAG_PERM_GATHER | DDKS_FLAG_NO_X0 | DDKS_FLAG_FORCE_X0 | DDKS_FLAG_RDKS_FULL_SORT | DDKS_FLAG_KD_LEVELS(7) | DDKS_FLAG_NCCL_SELF | DDKS_FLAG_NO_GRAPH | DDKS_FLAG_NO_RANK | DDKS_FLAG_FORCE_RANK)) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "bad flags");
     int ndev = 0;
     CU(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(ctx, DDKS_ERR_INVALID_ARGUMENT, "device %d of %d", device, ndev);
@@ -781,7 +802,7 @@ ddks_status ddks_destroy(ddks_ctx* ctx) {
                       &ctx->x0_keys1, &ctx->x0_hist, &ctx->x0_pts, &ctx->x0_perm, &ctx->x0_pts2,
                       &ctx->x0_perm2, &ctx->x0_boxes, &ctx->prof_clk, &ctx->rdb_cnt,
                       &ctx->rdb_pst, &ctx->rdb_coff, &ctx->rdb_fill, &ctx->rdb_clist, &ctx->rdb_csum, &ctx->rdb_bits,
-                      &ctx->kdf_bar, &ctx->kdf_buf})
+                      &ctx->kdf_bar, &ctx->kdf_buf, &ctx->rank_v})
         if (b->p) cudaFree(b->p);
     if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
     delete ctx;
@@ -793,6 +814,8 @@ const char* ddks_last_error(const ddks_ctx* ctx) { return ctx ? ctx->err.c_str()
 int64_t ddks_launch_count(const ddks_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 int32_t ddks_kd_levels(const ddks_ctx* ctx) { return ctx ? ctx->kd_levels : 0; }
+
+int32_t ddks_rank_lanes(const ddks_ctx* ctx) { return ctx ? ctx->rank_lanes : 0; }
 
 ddks_status ddks_profile_read(ddks_ctx* ctx, double* count_ms, int64_t* launches, uint64_t* pairs) {
     if (!ctx) return DDKS_ERR_INVALID_ARGUMENT;
@@ -918,6 +941,7 @@ static ddks_status small_enqueue(ddks_ctx* ctx, const float* P, int64_t n_P, con
         a.clk = (unsigned long long*)ctx->prof_clk.p;
     }
     ctx->kd_levels = 0;
+    ctx->rank_lanes = 0;
     switch (d) {
 #define SM_CASE(D) case D: s = launch_small_d<D>(ctx, a, segs, (int)blocks, st); break;
         SM_CASE(1) SM_CASE(2) SM_CASE(3) SM_CASE(4) SM_CASE(5) SM_CASE(6) SM_CASE(7) SM_CASE(8)
@@ -1025,6 +1049,7 @@ static ddks_status stat_capture(ddks_ctx* ctx, const ddks_ctx::StatKey& key, con
     ctx->sg_key = key;
     ctx->sg_launches = nl;
     ctx->sg_kd_levels = ctx->kd_levels;
+    ctx->sg_rank_lanes = ctx->rank_lanes;
     ctx->sg_evs = evs;
     ctx->sg_ev_pairs = pairs;
     *ok = true;
@@ -1080,6 +1105,7 @@ static ddks_status stat_impl(ddks_ctx* ctx, const float* P, int64_t n_P, const f
         CU(cudaGraphLaunch(ctx->sg_exec, st));
         ctx->launches += ctx->sg_launches;
         ctx->kd_levels = ctx->sg_kd_levels;
+        ctx->rank_lanes = ctx->sg_rank_lanes;
         for (size_t i = 0; i < ctx->sg_evs.size(); ++i) {
             ctx->ev_pending.push_back(ctx->sg_evs[i]);
             ctx->ev_pairs.push_back(ctx->sg_ev_pairs[i]);

@@ -43,6 +43,7 @@ struct ddks_ctx {
     DevBuf rd_keys, rd_xn, rd_k0, rd_k1, rd_hist, rd_tcnt, rd_cnum;              // ddks_rdks workspace
     DevBuf x0_keys0, x0_keys1, x0_hist, x0_pts, x0_perm, x0_pts2, x0_perm2, x0_boxes;  // kd-ordered count workspace
     DevBuf rdb_cnt, rdb_pst, rdb_coff, rdb_fill, rdb_clist, rdb_csum, rdb_bits;  // rdKS bucket-pruned sweep
+    DevBuf rank_v;            // rank-lane count: V_k of every origin block in Eytzinger order (ddks_rank.cuh)
     DevBuf kdf_bar, kdf_buf;  // fused mid-N kd ordering (k_kdb_fused): grid barrier; ranges, chunk totals, histograms
     void* rdb_zero_p = nullptr;  // rdb_cnt.p whose first rdb_zero bytes are known zero (the sweep re-zeroes the counts)
     size_t rdb_zero = 0;
@@ -51,6 +52,7 @@ struct ddks_ctx {
     size_t host_pinned_bytes = 0;
     int64_t launches = 0;
     int kd_levels = 0;  // levels of the last kd-ordered count (0: position order)
+    int rank_lanes = 0;  // the last count was the rank-lane count (ddks_rank.cuh)
     std::string err;
     // profiling (DDKS_FLAG_PROFILE)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending, ev_free;
@@ -75,7 +77,7 @@ struct ddks_ctx {
     cudaStream_t copy_stream = nullptr;
     std::vector<cudaEvent_t> copy_evs;
     int64_t sg_launches = 0;
-    int sg_kd_levels = 0;
+    int sg_kd_levels = 0, sg_rank_lanes = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> sg_evs;
     std::vector<uint64_t> sg_ev_pairs;
     // the same for ddks_stat_batch and ddks_permutation_null (run_call in ddks_api.cu): key = the call's pointers,
@@ -167,6 +169,11 @@ ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int6
                       int64_t o_begin, int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st,
                       bool force_split = false, unsigned long long* hist = nullptr, bool wx = false,
                       unsigned long long* best_key = nullptr);
+// the rank-lane count (ddks_rank.cuh, ddks_api_rank.cu): one DIFF statistic (B == 1) at 6 <= d <= 8, >= convention,
+// position order, origins [o_begin, o_end); results as run_count
+ddks_status run_count_rank(ddks_ctx* ctx, const float* packed, int d, int64_t n_P, int64_t n_Q, int64_t o_begin,
+                           int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st,
+                           unsigned long long* best_key);
 // items sharded contiguously over ranks: one all-gather of padded records (n_arr arrays + flags) into host hbuf
 ddks_status gather_items(ddks_ctx* ctx, uint64_t* const* dev, int n_arr, int64_t total, const uint32_t* dflag,
                          cudaStream_t st, uint64_t* hbuf);

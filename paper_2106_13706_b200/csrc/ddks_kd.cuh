@@ -297,6 +297,7 @@ ddks_status run_count_kd_t(ddks_ctx* ctx, const float* packed, int64_t n_P, int6
     a.hist_stride = n_Q + 1;
     a.best_key = best_key;
     ctx->kd_levels = K;
+    ctx->rank_lanes = 0;
     if (gt) return launch_kd<D, SPLIT, true, 1>(ctx, pl, a, st);
     if (K == 1) return launch_kd<D, SPLIT, false, 1>(ctx, pl, a, st);
     if constexpr (D >= 2) {

@@ -1,0 +1,330 @@
+// ddks_rank.cuh — the rank-lane count: rows a3 + a4 (orthant classification + per-orthant counting)
+// for d = 6..8 in position order, with three integer adds per pair instead of d FP32 compares + d FFMAs.
+//
+// What it computes is unchanged (Eq. 3: bit k of the orthant code = [x_k >= o_k], P:L46 loop
+// method, P:L238 normalised difference): every (origin, point) pair of the CTA's 384 origins and the segment's points
+// is classified by its own d comparisons and increments exactly one counter of its origin.
+//
+// How the comparisons are done (DESIGN.md §7 "rank lanes"): a CTA owns 384 origins. For each dim k let V_k be the
+// multiset of its origins' x_k values. For any real x and any o in V_k
+//     x >= o   <=>   #{v in V_k : v <= x}  >=  #{v in V_k : v <= o}
+// (if x >= o every v <= o is <= x; if x < o, o itself is counted on the right and not on the left, and nothing counted
+// on the left is missing on the right). Both counts lie in [0, 512] (V_k is padded to 511 entries with +inf), so the
+// compare of two floats becomes the compare of two small integers rx = rank(x), ro = rank(o), and three of those fit
+// one 32-bit word: 10-bit lanes holding rx + (512 - ro) in [0, 1023] — no borrow, no carry between lanes — whose top
+// bit is exactly [x_k >= o_k]. Dim k lives in word k % 3, lane k / 3, at bit offset (k % 3) + 10 (k / 3), so the d
+// result bits of the three words sit at bits 9+j+10i (j = k % 3, i = k / 3) — three groups of three adjacent bits —
+// and one multiply by 1 + 2^7 + 2^14 moves group i to bits 23+3i.. with no overlapping partial products (DESIGN.md
+// derivation), leaving the orthant code sum_k [x_k >= o_k] 2^k in bits 23..31 exactly. Per pair: LDS.128 (broadcast),
+// 3 IADD, 3 LOP3, IMAD, SHF, IMAD (counter address), ATOMS — ~12 instructions at d = 8 against ~18 for the FP32 path
+// (8 FSET + 8 FFMA + ATOMS + 2 LDS.128 at one origin per thread).
+//
+// The ranks of the points are taken per CTA and tile: each thread maps one point of the 384-point tile (d branch-free
+// searches of V_k, stored in Eytzinger order so the nine probe levels spread over the SMEM banks), the rank words go to
+// a double-buffered SMEM tile, and all threads then classify the tile against their origin. V_k is sorted once per
+// origin block by k_rank_sort (a bitonic network in SMEM, one CTA per (block, dim)).
+#pragma once
+#include "ddks_kernels.cuh"
+
+namespace ddks {
+namespace {
+
+#ifndef DDKS_RK_PTS  // points per step of the rank-lane count loop
+#define DDKS_RK_PTS 24
+#endif
+constexpr int RK_PTS = DDKS_RK_PTS;
+#ifndef DDKS_RK_R  // origins per thread of the rank-lane count (1: 384 threads, 2: 192 threads)
+#define DDKS_RK_R 1
+#endif
+
+template <int D> struct RankGeo {
+    static_assert(D >= 3 && D <= 9, "three 10-bit lanes per word, three words");
+    static constexpr int ORIGINS = 384;        // origins per CTA (384 / RR threads, RR origins each)
+    static constexpr int TILE = ORIGINS;       // points per tile: RR per thread to rank
+    static constexpr int WPB = ORIGINS / 2;    // counter words per bin (two signed 16-bit halves per word)
+    static constexpr int NQ = 1 << D, NB = NQ; // DIFF counters only
+    static constexpr int VN = 511;             // Eytzinger tree of 9 levels: 384 origin values + 127 x +inf
+    static constexpr int VW = 512;             // floats per (block, dim) in the workspace and in SMEM
+    static constexpr int HIST_WORDS = NB * WPB;
+    static constexpr int SMEM_BYTES = HIST_WORDS * 4 + D * VW * 4 + 2 * TILE * 16 + 64;
+    static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+    __host__ __device__ static constexpr int slot(int t) { return t % WPB; }
+    __host__ __device__ static constexpr bool high(int t) { return t >= WPB; }
+};
+
+// result-bit mask of word j: bits 9 + j + 10 i for the dims k = 3 i + j < D
+__host__ __device__ constexpr uint32_t rank_mask(int j, int D) {
+    uint32_t m = 0;
+    for (int i = 0; 3 * i + j < D; ++i) m |= 1u << (9 + j + 10 * i);
+    return m;
+}
+
+// 16-byte SMEM load kept in program order with the counter REDs (asm volatile): a step's RK_PTS loads all issue
+// before its first RED (the compiler otherwise interleaves them with the classification and exposes their latency)
+__device__ __forceinline__ uint4 lds_v4(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(smem_u32(p)));
+    return v;
+}
+
+// #{v in V : v <= x} for the 511-node Eytzinger tree E (node i's children 2i+1, 2i+2): nine probes, branch-free
+__device__ __forceinline__ uint32_t eyt_rank(const float* E, float x) {
+    uint32_t i = 0;
+#pragma unroll
+    for (int l = 0; l < 9; ++l) i = 2u * i + 1u + (E[i] <= x ? 1u : 0u);
+    return i - 511u;
+}
+
+// V_k of every origin block, sorted and laid out as an Eytzinger tree: one CTA of 256 threads per (block, dim).
+// out[(blk * D + k) * 512 + i] = node i (i < 511). Origin slots past o_end repeat origin o_end - 1 (as k_count's
+// clamped slots), which only duplicates a value of V_k.
+template <int D>
+__global__ void __launch_bounds__(256) k_rank_sort(const float* __restrict__ pts, int DP, int32_t o_begin,
+                                                   int32_t o_end, float* __restrict__ out) {
+    __shared__ float s[512];
+    const int blk = blockIdx.x, k = blockIdx.y, t = threadIdx.x;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int i = t + 256 * h;
+        float v = INFINITY;
+        if (i < RankGeo<D>::ORIGINS) {
+            int32_t oi = o_begin + blk * RankGeo<D>::ORIGINS + i;
+            oi = oi < o_end ? oi : o_end - 1;
+            v = pts[(int64_t)oi * DP + k];
+        }
+        s[i] = v;
+    }
+    __syncthreads();
+    // bitonic sort of 512 values, ascending (one compare-exchange per thread and step)
+    for (int kk = 2; kk <= 512; kk <<= 1) {
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            const int i = 2 * t - (t & (j - 1)), l = i + j;
+            const float a = s[i], b = s[l];
+            const bool up = (i & kk) == 0;
+            if ((a > b) == up) s[i] = b, s[l] = a;
+            __syncthreads();
+        }
+    }
+    // node i at level L (i in [2^L - 1, 2^(L+1) - 1)), position q in its level: in-order index (2q + 1) 2^(8-L) - 1
+    float* o = out + ((int64_t)blk * D + k) * RankGeo<D>::VW;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int i = t + 256 * h;
+        if (i >= RankGeo<D>::VN) continue;
+        const int L = 31 - __clz(i + 1), q = i + 1 - (1 << L);
+        o[i] = s[(2 * q + 1) * (1 << (8 - L)) - 1];
+    }
+}
+
+// the three rank words of a point (or, with neg, of an origin: 512 - rank in each lane)
+template <int D, bool NEG>
+__device__ __forceinline__ void rank_words(const float* V, const float (&x)[D], uint32_t (&w)[3]) {
+    w[0] = w[1] = w[2] = 0u;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        const uint32_t r = eyt_rank(V + k * RankGeo<D>::VW, x[k]);
+        w[k % 3] |= (NEG ? 512u - r : r) << ((k % 3) + 10 * (k / 3));
+    }
+}
+
+// Work: units = (origin block, 384-point tile) pairs, linearised block-major; CTA c owns units
+// [c U / grid, (c + 1) U / grid) (stream-K: every SM gets the same number of tiles, and a CTA visits at most a few
+// blocks). Per visited block the CTA loads V_k and its origin's rank words, classifies its tile range in chunks of at
+// most chunk_tiles (the int16 window) and flushes exact int32 partials to a.accum after each chunk (k_finalize sums
+// them), or -- a.accum == nullptr, one CTA per whole block -- finalises in-kernel.
+struct RankArgs {
+    const float* vsorted;  // [blocks][D][VW] Eytzinger trees (k_rank_sort)
+    int32_t n_tiles;       // tiles per block (the point set in 384-point tiles)
+    int32_t chunk_tiles;   // tiles per flush window
+    int64_t units;         // blocks * n_tiles
+};
+
+// RR origins per thread (T = 384 / RR threads): thread t owns origins t + r T of the block, i.e. with RR = 2 both
+// 16-bit halves of counter column t, and every point's rank words (one LDS.128) serve RR classifications.
+template <int D, int RR>
+__global__ void __launch_bounds__(RankGeo<D>::ORIGINS / RR, D >= 8 ? 1 : 2) k_count_rank(const CountArgs a, const RankArgs ra) {
+    using G = RankGeo<D>;
+    constexpr int OB = G::ORIGINS, T = OB / RR, TILE = G::TILE, WPB = G::WPB, DP = padded_dim<D>();
+    static_assert(RR == 1 || RR == 2, "one or two origins per thread");
+    constexpr uint32_t M0 = rank_mask(0, D), M1 = rank_mask(1, D), M2 = rank_mask(2, D);
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem);                                   // [NB][WPB]
+    float* V = reinterpret_cast<float*>(smem + G::HIST_WORDS * 4);                      // [D][VW] Eytzinger
+    uint4* W = reinterpret_cast<uint4*>(smem + G::HIST_WORDS * 4 + D * G::VW * 4);     // [2][TILE] rank words
+
+    const int t = threadIdx.x;
+    const float* pts = a.pts;
+    uint32_t ubase[RR], incP[RR], incQ[RR];
+#pragma unroll
+    for (int r = 0; r < RR; ++r) {
+        const int oo = t + r * T;  // origin offset in the block
+        ubase[r] = smem_u32(hist) + 4u * (uint32_t)G::slot(oo);
+        incP[r] = G::high(oo) ? a.incP << 16 : a.incP;
+        incQ[r] = G::high(oo) ? a.incQ << 16 : a.incQ;
+    }
+    const int64_t u_begin = (int64_t)blockIdx.x * ra.units / gridDim.x;
+    const int64_t u_end = (int64_t)(blockIdx.x + 1) * ra.units / gridDim.x;
+
+    const bool probe = a.clk && t == 0 && (blockIdx.x & 7) == 0;
+    unsigned long long clk0 = 0, ns0 = 0;
+    if (probe) clk0 = clock64(), ns0 = globaltimer_ns();
+    unsigned long long pts_done = 0, visits = 0;
+
+    for (int i = t; i < G::HIST_WORDS; i += T) hist[i] = 0u;
+    for (int64_t u = u_begin; u < u_end;) {
+        const int32_t by = (int32_t)(u / ra.n_tiles);
+        const int32_t tb = (int32_t)(u - (int64_t)by * ra.n_tiles);
+        const int32_t te = (int32_t)min((int64_t)min(ra.n_tiles, tb + ra.chunk_tiles), (int64_t)tb + (u_end - u));
+        u += te - tb;
+        const int32_t blk_o0 = a.o_begin + by * OB;
+        const int32_t seg0 = tb * TILE, seg1 = min(a.N, te * TILE);
+        const int n_tiles = te - tb;
+        ++visits;
+        pts_done += (unsigned long long)(seg1 - seg0);
+        __syncthreads();  // the previous chunk's V, W and counters are no longer read
+        {
+            const float4* src = reinterpret_cast<const float4*>(ra.vsorted + (int64_t)by * D * G::VW);
+            float4* dst = reinterpret_cast<float4*>(V);
+            for (int i = t; i < D * G::VW / 4; i += T) dst[i] = __ldg(src + i);
+        }
+        // this thread's origins (clamped slots repeat o_end - 1 and are ignored at the end) and its first points
+        float o[RR][D], xn[RR][D];
+#pragma unroll
+        for (int r = 0; r < RR; ++r) {
+            int32_t oi = blk_o0 + t + r * T;
+            oi = oi < a.o_end ? oi : a.o_end - 1;
+            load_point<D>(pts + (int64_t)oi * DP, o[r]);
+            if (seg0 + t + r * T < seg1) load_point<D>(pts + (int64_t)(seg0 + t + r * T) * DP, xn[r]);
+        }
+        __syncthreads();  // V visible
+        uint32_t ow[RR][3];
+#pragma unroll
+        for (int r = 0; r < RR; ++r) {
+            rank_words<D, true>(V, o[r], ow[r]);
+            if (seg0 + t + r * T < seg1) {
+                uint32_t xw[3];
+                rank_words<D, false>(V, xn[r], xw);
+                W[t + r * T] = make_uint4(xw[0], xw[1], xw[2], 0u);
+            }
+        }
+        for (int it = 0; it < n_tiles; ++it) {
+            // the next tile's points of this thread (global / L2 loads in flight during the count)
+            const int32_t pn = seg0 + (it + 1) * TILE + t;
+#pragma unroll
+            for (int r = 0; r < RR; ++r)
+                if (it + 1 < n_tiles && pn + r * T < seg1) load_point<D>(pts + (int64_t)(pn + r * T) * DP, xn[r]);
+            __syncthreads();  // tile it's words written; tile it - 1's words no longer read
+            const uint4* Wt = W + (it & 1) * TILE;
+            const int32_t p0 = seg0 + it * TILE;
+            const int32_t cnt = min(TILE, seg1 - p0);
+            int32_t split = a.n_P - p0;
+            split = split < 0 ? 0 : (split > cnt ? cnt : split);
+#pragma unroll 1
+            for (int part = 0; part < 2; ++part) {
+                const int lo = part ? split : 0, hi = part ? cnt : split;
+                uint32_t inc[RR];
+#pragma unroll
+                for (int r = 0; r < RR; ++r) inc[r] = part ? incQ[r] : incP[r];
+                auto count = [&](const uint4& xv) {
+#pragma unroll
+                    for (int r = 0; r < RR; ++r) {
+                        const uint32_t w = ((xv.x + ow[r][0]) & M0) | ((xv.y + ow[r][1]) & M1) | ((xv.z + ow[r][2]) & M2);
+                        const uint32_t code = (w * 0x4081u) >> 23;  // sum_k [x_k >= o_k] 2^k
+                        DDKS_ASSERT(code < (uint32_t)G::NQ);
+                        red_add_shared(ubase[r] + code * (4u * WPB), inc[r]);
+                    }
+                };
+                int p = lo;
+                // RK_PTS points per step, all loads issued first: RK_PTS x RR independent chains per warp
+#pragma unroll 1
+                for (; p + RK_PTS <= hi; p += RK_PTS) {
+                    uint4 xv[RK_PTS];
+#pragma unroll
+                    for (int j = 0; j < RK_PTS; ++j) xv[j] = lds_v4(Wt + p + j);
+#pragma unroll
+                    for (int j = 0; j < RK_PTS; ++j) count(xv[j]);
+                }
+                for (; p < hi; ++p) count(Wt[p]);
+            }
+            // the next tile's rank words into the other buffer (read by nobody until the barrier above)
+#pragma unroll
+            for (int r = 0; r < RR; ++r) {
+                if (it + 1 < n_tiles && pn + r * T < seg1) {
+                    uint32_t xw[3];
+                    rank_words<D, false>(V, xn[r], xw);
+                    W[((it + 1) & 1) * TILE + t + r * T] = make_uint4(xw[0], xw[1], xw[2], 0u);
+                }
+            }
+        }
+        __syncthreads();  // all red.shared retired before reading the counters
+        if (a.accum != nullptr) {
+            // exact int32 partials -> global (fire-and-forget REDs); each counter word (two origins' halves) is read
+            // and re-zeroed by one thread, coalesced over consecutive slots
+            int32_t* acc = a.accum + (int64_t)by * OB;
+            for (int wi = t; wi < G::HIST_WORDS; wi += T) {
+                const int q = wi / WPB, s2 = wi - q * WPB;
+                const uint32_t wv = hist[wi];
+                if (wv == 0u) continue;
+                hist[wi] = 0u;
+                int32_t lo, hi;
+                split16(wv, lo, hi);
+                DDKS_ASSERT((int64_t)by * OB + s2 + WPB < a.acc_stride + OB);
+                if (lo && blk_o0 + s2 < a.o_end) atomicAdd(&acc[(int64_t)q * a.acc_stride + s2], lo);
+                if (hi && blk_o0 + s2 + WPB < a.o_end) atomicAdd(&acc[(int64_t)q * a.acc_stride + s2 + WPB], hi);
+            }
+            continue;
+        }
+        // direct mode (this CTA owns the whole block): num(o), the per-origin export, the CTA max, the argmax key
+        uint64_t best = 0;
+        unsigned long long bkey = 0;
+#pragma unroll
+        for (int r = 0; r < RR; ++r) {
+            const int oo = t + r * T;
+            const int32_t myo = blk_o0 + oo;
+            if (myo >= a.o_end) continue;
+            uint32_t mm = 0;
+            for (int q = 0; q < G::NQ; ++q) {
+                int32_t lo, hi;
+                split16(hist[q * WPB + G::slot(oo)], lo, hi);
+                const int32_t v = G::high(oo) ? hi : lo;
+                const uint32_t av = (uint32_t)(v < 0 ? -v : v);
+                mm = av > mm ? av : mm;
+            }
+            const uint64_t red = mm;
+            const uint64_t m = red * a.gg;
+            if (a.per_origin) a.per_origin[myo - a.o_begin] = m;
+            best = m > best ? m : best;
+            if (a.best_key) {
+                const unsigned long long k = ((unsigned long long)red << 31) | (unsigned long long)(0x7fffffff - myo);
+                bkey = k > bkey ? k : bkey;
+            }
+        }
+        best = warp_max_u64(best);
+        bkey = warp_max_u64(bkey);
+        __shared__ uint64_t wmax[T / 32], wkey[T / 32];
+        if ((t & 31) == 0) wmax[t >> 5] = best, wkey[t >> 5] = bkey;
+        __syncthreads();
+        if (t == 0) {
+            uint64_t m = 0, k = 0;
+            for (int w = 0; w < T / 32; ++w) m = wmax[w] > m ? wmax[w] : m, k = wkey[w] > k ? wkey[w] : k;
+            atomicMax(reinterpret_cast<unsigned long long*>(&a.item_num[0]), (unsigned long long)m);
+            if (a.best_key) atomicMax(a.best_key, (unsigned long long)k);
+        }
+        __syncthreads();
+        for (int i = t; i < G::HIST_WORDS; i += T) hist[i] = 0u;
+    }
+    if (a.clk && t == 0) {
+        // executed compares: the d of every pair (done as three 32-bit adds on 10-bit lanes) and the rank searches'
+        // FP32 compares (9 per point, dim and visit)
+        atomicAdd(&a.clk[2], (unsigned long long)D * pts_done * OB + 9ull * D * (pts_done + visits * OB));
+        if (probe) {
+            atomicAdd(&a.clk[0], (unsigned long long)(clock64() - clk0));
+            atomicAdd(&a.clk[1], globaltimer_ns() - ns0);
+        }
+    }
+}
+
+}  // namespace
+}  // namespace ddks

@@ -29,6 +29,8 @@ DDKS_FLAG_PERM_GATHER = 16
 DDKS_FLAG_NO_X0 = 32
 DDKS_FLAG_FORCE_X0 = 64
 DDKS_FLAG_RDKS_FULL_SORT = 128
+DDKS_FLAG_NO_RANK = 256
+DDKS_FLAG_FORCE_RANK = 512
 DDKS_FLAG_KD_SHIFT = 16
 DDKS_FLAG_NCCL_SELF = 2048
 DDKS_FLAG_NO_GRAPH = 4096
@@ -104,6 +106,7 @@ def _load() -> ctypes.CDLL:
         "ddks_profile_work": ([vp, ctypes.POINTER(ctypes.c_uint64)], ctypes.c_int),
         "ddks_launch_count": ([vp], i64),
         "ddks_kd_levels": ([vp], i32),
+        "ddks_rank_lanes": ([vp], i32),
         "ddks_profile_clock": ([vp, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
         "ddks_profile_read": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_uint64)],
                               ctypes.c_int),
@@ -121,7 +124,7 @@ def _load() -> ctypes.CDLL:
 LIB = _load()
 EXPORTED = ("ddks_get_nccl_id", "ddks_create", "ddks_stat", "ddks_stat_batch", "ddks_permutation_null",
             "ddks_stat_per_origin", "ddks_stat_shard", "ddks_significance", "ddks_significance_batch", "ddks_vdks", "ddks_rdks", "ddks_shard_range", "ddks_combine_records", "ddks_unpad_items", "ddks_launch_count",
-            "ddks_kd_levels", "ddks_profile_clock", "ddks_profile_read", "ddks_profile_work", "ddks_destroy",
+            "ddks_kd_levels", "ddks_rank_lanes", "ddks_profile_clock", "ddks_profile_read", "ddks_profile_work", "ddks_destroy",
             "ddks_last_error", "ddks_version")
 
 
@@ -409,6 +412,11 @@ def ddks_kd_levels(ctx) -> int:
     return int(LIB.ddks_kd_levels(ctx))
 
 
+def ddks_rank_lanes(ctx) -> int:
+    """1 if the last count was the rank-lane count (DESIGN.md §7 "rank lanes"), else 0."""
+    return int(LIB.ddks_rank_lanes(ctx))
+
+
 def ddks_profile_read(ctx):
     """-> (count_kernel_ms, count_launches, pairs) since the last read (context needs DDKS_FLAG_PROFILE)."""
     ms, n, pairs = ctypes.c_double(), ctypes.c_int64(), ctypes.c_uint64()
@@ -466,6 +474,10 @@ class Context:
     @property
     def kd_levels(self) -> int:
         return ddks_kd_levels(self.ctx)
+
+    @property
+    def rank_lanes(self) -> int:
+        return ddks_rank_lanes(self.ctx)
 
     def close(self):
         if self.ctx is not None:

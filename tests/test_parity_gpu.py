@@ -486,7 +486,7 @@ def test_profile_clock_probe():
 
 
 @pytest.mark.parametrize("n_P,n_Q,d,kind", [(12000, 11000, 8, "normal"), (15000, 14000, 3, "mixed"),
-                                            (21000, 19500, 5, "grid")])
+                                            (21000, 19500, 5, "grid"), (11000, 11000, 7, "mixed")])
 def test_default_mid_n_kd_path(n_P, n_Q, d, kind):
     # sizes just above the default kd thresholds (d = 8 from 20 000 rows, d = 3 from 28 000, d = 5 from 40 000): the
     # unforced call takes the kd count with the cluster mid-N ordering and must equal the oracle bit for bit
@@ -496,4 +496,10 @@ def test_default_mid_n_kd_path(n_P, n_Q, d, kind):
         Q[:, :2] = np.round(Q[:, :2] * 4) / 4
     with K.Context() as c:
         check_pair(c, P, Q)
-        assert c.kd_levels >= 1
+        # d = 8 with DIFF counters takes the rank-lane count (position order; test_rank_gpu.py); 12000 + 11000 needs
+        # SPLIT counters (a = 11, b = 12), which the rank-lane count does not have, so it stays on the kd count
+        assert c.kd_levels >= 1 and c.rank_lanes == 0
+    if d == 8:
+        with K.Context(flags=K.DDKS_FLAG_NO_RANK) as c:
+            check_pair(c, P, Q)
+            assert c.kd_levels >= 1

@@ -1,0 +1,121 @@
+"""GPU parity of the rank-lane count (csrc/ddks_rank.cuh; DESIGN.md §7 "rank lanes"): every (origin, point) pair is
+classified from 10-bit per-CTA rank lanes instead of FP32 compares, which must give exactly the statistic of the
+definition (Eq. 3, bit k = [x_k >= o_k]; Eq. 6). Compared with the CPU oracle element by
+element: num, den, the D bits, the argmax origin and the per-origin nums; tie-heavy, ragged and sharded cases."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import oracle as O  # noqa: E402
+from paper_2106_13706_b200 import ddks as K  # noqa: E402
+from paper_2106_13706_b200 import inputs as I  # noqa: E402
+
+RANK = K.DDKS_FLAG_FORCE_RANK
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def check(c, P, Q, want=None):
+    want = want or O.ddks(P, Q)
+    got = c.stat(dev(P), dev(Q))
+    assert (got.num, got.den, got.argmax_origin) == (want[0], want[1], want[3]), (got, want)
+    assert np.float64(got.D).tobytes() == np.float64(want[2]).tobytes()
+    return got
+
+
+# N > 8192 (the small geometry ends there): ragged origin blocks (N % 384 != 0), unequal and equal sample sizes
+SIZES = [(4100, 4093), (5000, 7001), (6144, 6144), (9001, 3000)]
+
+
+@pytest.mark.parametrize("d", [6, 7, 8])
+@pytest.mark.parametrize("kind", ["normal", "grid", "mixed", "dup"])
+def test_rank_lane_parity(d, kind):
+    with K.Context(flags=RANK) as c, K.Context(flags=RANK | K.DDKS_FLAG_FORCE_DIRECT) as cd:
+        for i, (n_P, n_Q) in enumerate(SIZES):
+            P, Q = I.random_pair(31000 + 100 * d + 7 * i + hash(kind) % 89, n_P, n_Q, d, kind)
+            want = O.ddks(P, Q)
+            check(c, P, Q, want)
+            assert c.rank_lanes == 1
+            if i % 2 == 0:
+                check(cd, P, Q, want)  # one point segment: the in-kernel finalisation
+
+
+@pytest.mark.parametrize("d", [6, 8])
+def test_rank_lane_per_origin(d):
+    P, Q = I.random_pair(32000 + d, 5200, 4700, d, "mixed")
+    want = O.per_origin(P, Q)
+    with K.Context(flags=RANK) as c:
+        got = c.stat_per_origin(dev(P), dev(Q), 0, 9900)
+        assert np.array_equal(got, want)
+        got = c.stat_per_origin(dev(P), dev(Q), 383, 4000)  # a range that starts inside an origin block
+        assert np.array_equal(got, want[383:4000])
+
+
+def test_rank_lane_shards():
+    P, Q = I.random_pair(32100, 7000, 6500, 8, "grid")
+    want = O.ddks(P, Q)
+    with K.Context(flags=RANK) as c:
+        check(c, P, Q, want)
+        for world in (2, 3, 8):
+            parts = [c.stat_shard(dev(P), dev(Q), world, r) for r in range(world)]
+            num = max(p.num for p in parts)
+            arg = min(p.argmax_origin for p in parts if p.num == num)
+            assert (num, arg) == (want[0], want[3]), (world, parts)
+
+
+def test_rank_lane_extreme_values():
+    # denormals, signed zeros, 1-ulp neighbours, huge magnitudes and many exact ties in one input: the per-CTA
+    # ranks must order them exactly as the IEEE >= of the oracle
+    rng = np.random.default_rng(32200)
+    vals = np.array([0.0, -0.0, 2.0 ** -149, -(2.0 ** -149), 2.0 ** -126, 1.0, np.nextafter(np.float32(1), np.float32(2)),
+                     -1.0, 3.0e38, -3.0e38, 1e-30, 7.0], np.float32)
+    P = vals[rng.integers(0, len(vals), (4800, 8))].astype(np.float32)
+    Q = vals[rng.integers(0, len(vals), (4500, 8))].astype(np.float32)
+    Q[:, 3] = rng.standard_normal(4500).astype(np.float32)
+    with K.Context(flags=RANK) as c:
+        check(c, P, Q)
+
+
+def test_rank_lane_is_the_default_at_d8_and_equals_the_fp32_paths():
+    # d = 8, N = 60 000: the default call takes the rank-lane count (no kd ordering); the position-ordered FP32 count
+    # and the kd-ordered count give the same statistic, argmax and per-origin nums
+    P, Q = I.random_pair(32300, 30000, 30000, 8, "normal")
+    with K.Context() as c, K.Context(flags=K.DDKS_FLAG_NO_RANK | K.DDKS_FLAG_NO_X0) as cf, \
+            K.Context(flags=K.DDKS_FLAG_NO_RANK) as ck:
+        a = c.stat(dev(P), dev(Q))
+        assert c.kd_levels == 0 and c.rank_lanes == 1
+        b = cf.stat(dev(P), dev(Q))
+        k = ck.stat(dev(P), dev(Q))
+        assert ck.kd_levels >= 1 and ck.rank_lanes == 0 and cf.rank_lanes == 0
+        assert a == b == k
+        pa = c.stat_per_origin(dev(P), dev(Q), 20000, 21000)
+        pb = cf.stat_per_origin(dev(P), dev(Q), 20000, 21000)
+        assert np.array_equal(pa, pb)
+        # and a sample of origins against the oracle's per-origin definition
+        assert np.array_equal(pa[:64], O.per_origin(P, Q, 20000, 20064))
+
+
+def test_rank_lane_graph_replay_and_fallbacks():
+    # the captured call graph replays the rank-lane count (and reports it); SPLIT-only sizes and the > convention
+    # take the FP32 counts
+    P, Q = I.random_pair(32400, 6000, 5000, 8, "mixed")
+    want = O.ddks(P, Q)
+    dP, dQ = dev(P), dev(Q)
+    with K.Context() as c:
+        for _ in range(4):
+            r = c.stat(dP, dQ)
+            assert (r.num, r.argmax_origin) == (want[0], want[3]) and c.rank_lanes == 1
+    with K.Context(flags=K.DDKS_FLAG_TIES_GT) as c:
+        r = c.stat(dP, dQ)
+        assert c.rank_lanes == 0 and r.num == O.ddks(P, Q, ties_gt=True)[0]
+    P1, Q1 = I.random_pair(32401, 9000, 7, 8, "normal")  # a = 9000 / gcd: DIFF counters would overflow -> SPLIT
+    with K.Context(flags=RANK) as c:
+        r = c.stat(dev(P1), dev(Q1))
+        assert c.rank_lanes == 0 and (r.num, r.argmax_origin) == (O.ddks(P1, Q1)[0], O.ddks(P1, Q1)[3])
