@@ -19,13 +19,14 @@ def timed(c, f, reps=7):
     return r, float(np.median(ts)), kms / max(kl, 1) * 1.0
 
 
-cases = [("C3", None)] + [(f"d{d} N{n}", (d, n)) for d in (8, 7, 6) for n in (10000, 20000, 40000, 100000, 400000)]
+cases = [("C3", None), ("C2", None)] + [(f"d{d} N{n}", (d, n)) for d in (8, 7, 6, 5, 4, 3, 2)
+                                        for n in (10000, 20000, 40000, 100000, 400000)]
 if len(sys.argv) > 1:
     cases = [c for c in cases if any(s in c[0] for s in sys.argv[1:])]
 modes = [("rank", K.DDKS_FLAG_FORCE_RANK), ("fp32-auto", K.DDKS_FLAG_NO_RANK), ("fp32-pos", K.DDKS_FLAG_NO_RANK | K.DDKS_FLAG_NO_X0)]
 for name, spec in cases:
     if spec is None:
-        P, Q = I.config("C3")
+        P, Q = I.config(name)
     else:
         d, n = spec
         P, Q = I.random_pair(4242 + n + d, n // 2, n // 2, d, "normal")

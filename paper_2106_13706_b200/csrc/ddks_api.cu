@@ -126,17 +126,27 @@ int pad_dim(int d) { return d <= 4 ? 4 : 8; }
 // DIFF counters fit (|c_P a - c_Q b| stays in int32 and the int16 window is >= 4096 points); else SPLIT
 bool diff_counters_ok(int64_t n_P, int64_t n_Q);
 
-// the rank-lane count (ddks_rank.cuh) takes a position-ordered DIFF statistic at 6 <= d <= 8 in its measured range
-// (any size with DDKS_FLAG_FORCE_RANK); the >= convention only; not for the small geometry
+// the rank-lane count (ddks_rank.cuh) takes a position-ordered DIFF statistic at d = 3 and 5..8 in its measured range
+// (d = 2..8 at any size with DDKS_FLAG_FORCE_RANK); the >= convention only; not for the small geometry
 bool rank_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q) {
     if (ctx->flags & (DDKS_FLAG_NO_RANK | DDKS_FLAG_TIES_GT)) return false;
-    if (d < 6 || d > 8 || n_P + n_Q <= ddks::kSmallN || !diff_counters_ok(n_P, n_Q)) return false;
+    if (d < 2 || d > 8 || n_P + n_Q <= ddks::kSmallN || !diff_counters_ok(n_P, n_Q)) return false;
     if (ctx->flags & DDKS_FLAG_FORCE_RANK) return true;
     // measured against the kd-ordered and position-ordered FP32 counts (microbench/rank_ab.py,
-    // profiles/r2e_rank_ab.txt): d = 8 faster at N = 1e4 .. 4e5 (C3 0.90 vs 1.16 ms per call; 78 vs 81 ms at 4e5,
-    // the kd count's decided bits catch up beyond), d = 6 and 7 up to N ~ 5e4
+    // profiles/r2e_rank_ab.txt, r2f_rank_ab.txt; warm call times). d = 8 (three rank words): faster at N = 1e4 .. 4e5
+    // (C3 0.88 vs 1.17 ms; 78 vs 82 ms at 4e5, the kd count's decided bits catch up beyond); d = 7: up to N ~ 5e4;
+    // d = 6 (two words): 0.64 vs 0.89 ms at 4e4, 3.48 vs 3.87 at 1e5, 54 vs 46 at 4e5; d = 5: 0.58 vs 0.67 at 4e4,
+    // 3.21 vs 3.10 at 1e5; d = 3 (one word; C2 0.156 vs 0.164 ms): 0.430 vs 0.453 at 4e4, 2.34 vs 2.01 at 1e5;
+    // d = 4 ties and d = 2 loses (their FP32 counts are 9.6 / 5.7 instructions per pair already)
     const int64_t N = n_P + n_Q;
-    return d == 8 ? N <= 600000 : N <= 50000;
+    switch (d) {
+        case 8: return N <= 600000;
+        case 7: return N <= 50000;
+        case 6: return N <= 120000;
+        case 5: return N <= 60000;
+        case 3: return N <= 50000;
+    }
+    return false;
 }
 
 template <int D>
@@ -163,7 +173,7 @@ ddks_status launch_count_d(ddks_ctx* ctx, const CountPlan& pl, const ddks::Count
 ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int64_t n_P, int64_t n_Q,
                       int64_t o_begin, int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st,
                       bool force_split, unsigned long long* hist, bool wx, unsigned long long* best_key) {
-    if (B == 1 && !force_split && rank_applicable(ctx, d, n_P, n_Q))  // d = 8: the rank-lane count (ddks_rank.cuh)
+    if (B == 1 && !force_split && rank_applicable(ctx, d, n_P, n_Q))  // the rank-lane count (ddks_rank.cuh)
         return run_count_rank(ctx, packed, d, n_P, n_Q, o_begin, o_end, item_num, per_origin, st, best_key);
     const int64_t N = n_P + n_Q;
     const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
@@ -285,6 +295,7 @@ ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n
     unsigned long long* key = use_key ? &dres->key : nullptr;
     const bool x0 = !export_per && x0_applicable(ctx, d, n_P, n_Q);
     *per_out = nullptr;
+    ctx->rank_lanes = 0;  // set by run_count_rank when the rank-lane count runs
     if (x0) {
         // origins are positions of the kd order; per-origin nums (k_argmax path only) land in pooled order in per[N]
         uint64_t* per = nullptr;

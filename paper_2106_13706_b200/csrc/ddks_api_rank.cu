@@ -154,6 +154,10 @@ ddks_status run_count_rank(ddks_ctx* ctx, const float* packed, int d, int64_t n_
     a.best_key = best_key;
     ctx->rank_lanes = 1;
     switch (d) {
+        case 2: return launch_count_rank_d<2>(ctx, pl, a, st);
+        case 3: return launch_count_rank_d<3>(ctx, pl, a, st);
+        case 4: return launch_count_rank_d<4>(ctx, pl, a, st);
+        case 5: return launch_count_rank_d<5>(ctx, pl, a, st);
         case 6: return launch_count_rank_d<6>(ctx, pl, a, st);
         case 7: return launch_count_rank_d<7>(ctx, pl, a, st);
         case 8: return launch_count_rank_d<8>(ctx, pl, a, st);

@@ -38,7 +38,17 @@ constexpr int RK_PTS = DDKS_RK_PTS;
 #endif
 
 template <int D> struct RankGeo {
-    static_assert(D >= 3 && D <= 9, "three 10-bit lanes per word, three words");
+    static_assert(D >= 1 && D <= 9, "three 10-bit lanes per word, up to three words");
+    static constexpr int NW = (D + 2) / 3;     // rank words per point / origin: dim k in word k % NW, lane k / NW
+    static constexpr int NWS = NW == 3 ? 4 : NW;  // words stored per point in the SMEM tile (16 B holds 4 / NWS points)
+    static constexpr int PPL = 4 / NWS;        // points per LDS.128
+    // the gather multiply: result bits 9 + j + 10 i (word j, lane i) -> orthant code in the product's top bits
+    //   NW = 1: bits 9, 19, 29           x (1 + 2^9 + 2^18) -> bits 27..29 (others land on 9, 18, 19)
+    //   NW = 2: bits {9,10} + 10 i       x (2 + 2^9 + 2^17) -> bits 26..31 (others on 10, 11, 18..21)
+    //   NW = 3: bits {9,10,11} + 10 i    x (1 + 2^7 + 2^14) -> bits 23..31 (others on 9..11, 16..21)
+    // every partial product occupies its own bits, so the sum has no carries
+    static constexpr uint32_t MUL = NW == 1 ? 0x40201u : (NW == 2 ? 0x20202u : 0x4081u);
+    static constexpr int SH = NW == 1 ? 27 : (NW == 2 ? 26 : 23);
     static constexpr int ORIGINS = 384;        // origins per CTA (384 / RR threads, RR origins each)
     static constexpr int TILE = ORIGINS;       // points per tile: RR per thread to rank
     static constexpr int WPB = ORIGINS / 2;    // counter words per bin (two signed 16-bit halves per word)
@@ -46,16 +56,19 @@ template <int D> struct RankGeo {
     static constexpr int VN = 511;             // Eytzinger tree of 9 levels: 384 origin values + 127 x +inf
     static constexpr int VW = 512;             // floats per (block, dim) in the workspace and in SMEM
     static constexpr int HIST_WORDS = NB * WPB;
-    static constexpr int SMEM_BYTES = HIST_WORDS * 4 + D * VW * 4 + 2 * TILE * 16 + 64;
+    static constexpr int SMEM_BYTES = HIST_WORDS * 4 + D * VW * 4 + 2 * TILE * NWS * 4 + 64;
+    static constexpr int MIN_CTAS = D >= 8 ? 1 : (D >= 6 ? 2 : 3);
     static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
     __host__ __device__ static constexpr int slot(int t) { return t % WPB; }
     __host__ __device__ static constexpr bool high(int t) { return t >= WPB; }
 };
 
-// result-bit mask of word j: bits 9 + j + 10 i for the dims k = 3 i + j < D
+// result-bit mask of word j: bits 9 + j + 10 i for the dims k = NW i + j < D
 __host__ __device__ constexpr uint32_t rank_mask(int j, int D) {
+    const int NW = (D + 2) / 3;
     uint32_t m = 0;
-    for (int i = 0; 3 * i + j < D; ++i) m |= 1u << (9 + j + 10 * i);
+    if (j >= NW) return 0u;
+    for (int i = 0; NW * i + j < D; ++i) m |= 1u << (9 + j + 10 * i);
     return m;
 }
 
@@ -121,11 +134,12 @@ __global__ void __launch_bounds__(256) k_rank_sort(const float* __restrict__ pts
 // the three rank words of a point (or, with neg, of an origin: 512 - rank in each lane)
 template <int D, bool NEG>
 __device__ __forceinline__ void rank_words(const float* V, const float (&x)[D], uint32_t (&w)[3]) {
+    constexpr int NW = RankGeo<D>::NW;
     w[0] = w[1] = w[2] = 0u;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
         const uint32_t r = eyt_rank(V + k * RankGeo<D>::VW, x[k]);
-        w[k % 3] |= (NEG ? 512u - r : r) << ((k % 3) + 10 * (k / 3));
+        w[k % NW] |= (NEG ? 512u - r : r) << ((k % NW) + 10 * (k / NW));
     }
 }
 
@@ -144,15 +158,17 @@ struct RankArgs {
 // RR origins per thread (T = 384 / RR threads): thread t owns origins t + r T of the block, i.e. with RR = 2 both
 // 16-bit halves of counter column t, and every point's rank words (one LDS.128) serve RR classifications.
 template <int D, int RR>
-__global__ void __launch_bounds__(RankGeo<D>::ORIGINS / RR, D >= 8 ? 1 : 2) k_count_rank(const CountArgs a, const RankArgs ra) {
+__global__ void __launch_bounds__(RankGeo<D>::ORIGINS / RR, RankGeo<D>::MIN_CTAS) k_count_rank(const CountArgs a, const RankArgs ra) {
     using G = RankGeo<D>;
     constexpr int OB = G::ORIGINS, T = OB / RR, TILE = G::TILE, WPB = G::WPB, DP = padded_dim<D>();
+    constexpr int NW = G::NW, NWS = G::NWS, PPL = G::PPL;
+    static_assert(RK_PTS % 4 == 0, "whole LDS.128 groups per step");
     static_assert(RR == 1 || RR == 2, "one or two origins per thread");
     constexpr uint32_t M0 = rank_mask(0, D), M1 = rank_mask(1, D), M2 = rank_mask(2, D);
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem);                                   // [NB][WPB]
     float* V = reinterpret_cast<float*>(smem + G::HIST_WORDS * 4);                      // [D][VW] Eytzinger
-    uint4* W = reinterpret_cast<uint4*>(smem + G::HIST_WORDS * 4 + D * G::VW * 4);     // [2][TILE] rank words
+    uint32_t* W = reinterpret_cast<uint32_t*>(smem + G::HIST_WORDS * 4 + D * G::VW * 4);  // [2][TILE][NWS] rank words
 
     const int t = threadIdx.x;
     const float* pts = a.pts;
@@ -206,7 +222,8 @@ __global__ void __launch_bounds__(RankGeo<D>::ORIGINS / RR, D >= 8 ? 1 : 2) k_co
             if (seg0 + t + r * T < seg1) {
                 uint32_t xw[3];
                 rank_words<D, false>(V, xn[r], xw);
-                W[t + r * T] = make_uint4(xw[0], xw[1], xw[2], 0u);
+#pragma unroll
+                for (int j = 0; j < NW; ++j) W[(t + r * T) * NWS + j] = xw[j];
             }
         }
         for (int it = 0; it < n_tiles; ++it) {
@@ -216,7 +233,7 @@ __global__ void __launch_bounds__(RankGeo<D>::ORIGINS / RR, D >= 8 ? 1 : 2) k_co
             for (int r = 0; r < RR; ++r)
                 if (it + 1 < n_tiles && pn + r * T < seg1) load_point<D>(pts + (int64_t)(pn + r * T) * DP, xn[r]);
             __syncthreads();  // tile it's words written; tile it - 1's words no longer read
-            const uint4* Wt = W + (it & 1) * TILE;
+            const uint32_t* Wt = W + (it & 1) * (TILE * NWS);
             const int32_t p0 = seg0 + it * TILE;
             const int32_t cnt = min(TILE, seg1 - p0);
             int32_t split = a.n_P - p0;
@@ -227,26 +244,38 @@ __global__ void __launch_bounds__(RankGeo<D>::ORIGINS / RR, D >= 8 ? 1 : 2) k_co
                 uint32_t inc[RR];
 #pragma unroll
                 for (int r = 0; r < RR; ++r) inc[r] = part ? incQ[r] : incP[r];
-                auto count = [&](const uint4& xv) {
+                auto count = [&](uint32_t x0, uint32_t x1, uint32_t x2) {
 #pragma unroll
                     for (int r = 0; r < RR; ++r) {
-                        const uint32_t w = ((xv.x + ow[r][0]) & M0) | ((xv.y + ow[r][1]) & M1) | ((xv.z + ow[r][2]) & M2);
-                        const uint32_t code = (w * 0x4081u) >> 23;  // sum_k [x_k >= o_k] 2^k
+                        uint32_t w = (x0 + ow[r][0]) & M0;
+                        if (NW > 1) w |= (x1 + ow[r][1]) & M1;
+                        if (NW > 2) w |= (x2 + ow[r][2]) & M2;
+                        const uint32_t code = (w * G::MUL) >> G::SH;  // sum_k [x_k >= o_k] 2^k
                         DDKS_ASSERT(code < (uint32_t)G::NQ);
                         red_add_shared(ubase[r] + code * (4u * WPB), inc[r]);
                     }
                 };
+                auto count_one = [&](int q) {
+                    const uint32_t* wq = Wt + q * NWS;
+                    count(wq[0], NW > 1 ? wq[1] : 0u, NW > 2 ? wq[2] : 0u);
+                };
+                auto count_v4 = [&](const uint4& v) {  // one LDS.128 = PPL points
+                    if (PPL == 1) count(v.x, v.y, v.z);
+                    if (PPL == 2) count(v.x, v.y, 0u), count(v.z, v.w, 0u);
+                    if (PPL == 4) count(v.x, 0u, 0u), count(v.y, 0u, 0u), count(v.z, 0u, 0u), count(v.w, 0u, 0u);
+                };
                 int p = lo;
+                for (; p < hi && (p % PPL) != 0; ++p) count_one(p);  // up to a 16-byte boundary of the tile
                 // RK_PTS points per step, all loads issued first: RK_PTS x RR independent chains per warp
 #pragma unroll 1
                 for (; p + RK_PTS <= hi; p += RK_PTS) {
-                    uint4 xv[RK_PTS];
+                    uint4 xv[RK_PTS / PPL];
 #pragma unroll
-                    for (int j = 0; j < RK_PTS; ++j) xv[j] = lds_v4(Wt + p + j);
+                    for (int j = 0; j < RK_PTS / PPL; ++j) xv[j] = lds_v4(reinterpret_cast<const uint4*>(Wt + p * NWS) + j);
 #pragma unroll
-                    for (int j = 0; j < RK_PTS; ++j) count(xv[j]);
+                    for (int j = 0; j < RK_PTS / PPL; ++j) count_v4(xv[j]);
                 }
-                for (; p < hi; ++p) count(Wt[p]);
+                for (; p < hi; ++p) count_one(p);
             }
             // the next tile's rank words into the other buffer (read by nobody until the barrier above)
 #pragma unroll
@@ -254,7 +283,8 @@ __global__ void __launch_bounds__(RankGeo<D>::ORIGINS / RR, D >= 8 ? 1 : 2) k_co
                 if (it + 1 < n_tiles && pn + r * T < seg1) {
                     uint32_t xw[3];
                     rank_words<D, false>(V, xn[r], xw);
-                    W[((it + 1) & 1) * TILE + t + r * T] = make_uint4(xw[0], xw[1], xw[2], 0u);
+#pragma unroll
+                    for (int j = 0; j < NW; ++j) W[(((it + 1) & 1) * TILE + t + r * T) * NWS + j] = xw[j];
                 }
             }
         }

@@ -486,7 +486,7 @@ def test_profile_clock_probe():
 
 
 @pytest.mark.parametrize("n_P,n_Q,d,kind", [(12000, 11000, 8, "normal"), (15000, 14000, 3, "mixed"),
-                                            (21000, 19500, 5, "grid"), (11000, 11000, 7, "mixed")])
+                                            (21000, 19500, 5, "grid")])
 def test_default_mid_n_kd_path(n_P, n_Q, d, kind):
     # sizes just above the default kd thresholds (d = 8 from 20 000 rows, d = 3 from 28 000, d = 5 from 40 000): the
     # unforced call takes the kd count with the cluster mid-N ordering and must equal the oracle bit for bit

@@ -114,7 +114,7 @@ def test_kd_four_levels_from_the_flag_alone(monkeypatch):
 def test_executed_compares_counter():
     P, Q = I.random_pair(33300, 20000, 20000, 5, "normal")
     N, d = 40000, 5
-    with K.Context(flags=K.DDKS_FLAG_PROFILE | K.DDKS_FLAG_NO_X0) as c:
+    with K.Context(flags=K.DDKS_FLAG_PROFILE | K.DDKS_FLAG_NO_X0 | K.DDKS_FLAG_NO_RANK) as c:  # the FP32 count
         c.stat(dev(P), dev(Q))
         ms, n, pairs = c.profile_read()
         ex = c.profile_work()

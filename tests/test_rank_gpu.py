@@ -30,11 +30,13 @@ def check(c, P, Q, want=None):
     return got
 
 
-# N > 8192 (the small geometry ends there): ragged origin blocks (N % 384 != 0), unequal and equal sample sizes
-SIZES = [(4100, 4093), (5000, 7001), (6144, 6144), (9001, 3000)]
+# N > 8192 (the small geometry ends there) with DIFF counters (max(n_P, n_Q) / gcd <= 7): ragged origin blocks
+# (N % 384 != 0), equal and unequal sample sizes; 7000 + 6000 (a = 6, b = 7, lcm 42 000 > 32 767) needs several
+# int16 windows, so its counters are flushed in chunks of 12 tiles
+SIZES = [(4100, 4100), (5001, 3334), (6144, 6144), (7000, 6000)]
 
 
-@pytest.mark.parametrize("d", [6, 7, 8])
+@pytest.mark.parametrize("d", [2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("kind", ["normal", "grid", "mixed", "dup"])
 def test_rank_lane_parity(d, kind):
     with K.Context(flags=RANK) as c, K.Context(flags=RANK | K.DDKS_FLAG_FORCE_DIRECT) as cd:
@@ -47,22 +49,24 @@ def test_rank_lane_parity(d, kind):
                 check(cd, P, Q, want)  # one point segment: the in-kernel finalisation
 
 
-@pytest.mark.parametrize("d", [6, 8])
+@pytest.mark.parametrize("d", [3, 5, 6, 8])
 def test_rank_lane_per_origin(d):
-    P, Q = I.random_pair(32000 + d, 5200, 4700, d, "mixed")
+    P, Q = I.random_pair(32000 + d, 5200, 3900, d, "mixed")
     want = O.per_origin(P, Q)
     with K.Context(flags=RANK) as c:
-        got = c.stat_per_origin(dev(P), dev(Q), 0, 9900)
+        got = c.stat_per_origin(dev(P), dev(Q), 0, 9100)
+        assert c.rank_lanes == 1
         assert np.array_equal(got, want)
         got = c.stat_per_origin(dev(P), dev(Q), 383, 4000)  # a range that starts inside an origin block
         assert np.array_equal(got, want[383:4000])
 
 
 def test_rank_lane_shards():
-    P, Q = I.random_pair(32100, 7000, 6500, 8, "grid")
+    P, Q = I.random_pair(32100, 7000, 6000, 8, "grid")
     want = O.ddks(P, Q)
     with K.Context(flags=RANK) as c:
         check(c, P, Q, want)
+        assert c.rank_lanes == 1
         for world in (2, 3, 8):
             parts = [c.stat_shard(dev(P), dev(Q), world, r) for r in range(world)]
             num = max(p.num for p in parts)
@@ -77,10 +81,14 @@ def test_rank_lane_extreme_values():
     vals = np.array([0.0, -0.0, 2.0 ** -149, -(2.0 ** -149), 2.0 ** -126, 1.0, np.nextafter(np.float32(1), np.float32(2)),
                      -1.0, 3.0e38, -3.0e38, 1e-30, 7.0], np.float32)
     P = vals[rng.integers(0, len(vals), (4800, 8))].astype(np.float32)
-    Q = vals[rng.integers(0, len(vals), (4500, 8))].astype(np.float32)
-    Q[:, 3] = rng.standard_normal(4500).astype(np.float32)
+    Q = vals[rng.integers(0, len(vals), (4000, 8))].astype(np.float32)
+    Q[:, 3] = rng.standard_normal(4000).astype(np.float32)
     with K.Context(flags=RANK) as c:
         check(c, P, Q)
+        assert c.rank_lanes == 1
+        check(c, P[:, :3].copy(), Q[:, :3].copy())  # one rank word per point
+        check(c, P[:, :5].copy(), Q[:, :5].copy())  # two
+        assert c.rank_lanes == 1
 
 
 def test_rank_lane_is_the_default_at_d8_and_equals_the_fp32_paths():
@@ -100,6 +108,14 @@ def test_rank_lane_is_the_default_at_d8_and_equals_the_fp32_paths():
         assert np.array_equal(pa, pb)
         # and a sample of origins against the oracle's per-origin definition
         assert np.array_equal(pa[:64], O.per_origin(P, Q, 20000, 20064))
+
+
+def test_rank_lane_default_at_d7_mid_n():
+    # d = 7, N = 22 000 (below the kd threshold, inside the rank-lane range): the unforced call takes the rank lanes
+    P, Q = I.random_pair(9707, 11000, 11000, 7, "mixed")
+    with K.Context() as c:
+        check(c, P, Q)
+        assert c.kd_levels == 0 and c.rank_lanes == 1
 
 
 def test_rank_lane_graph_replay_and_fallbacks():
