@@ -467,22 +467,23 @@ def main():
         roof["rank_lanes"] = ctx.rank_lanes
         if ctx.rank_lanes:
             roof["kernel"] = "k_count_rank (classify + count on 10-bit rank lanes)"
-            roof["note"] = ("rank-lane count (d >= 6): each pair's d compares run as three 32-bit integer adds on "
+            roof["note"] = ("rank-lane count: each pair's d compares run as ceil(d/3) 32-bit integer adds on "
                             "per-CTA 10-bit rank lanes (exact; DESIGN.md §7 'rank lanes'), so d compares per pair "
                             "against the FP32-compare lane peak is the compare-equivalent rate, and the kernel is "
-                            "bound by instruction issue (~11 instructions per pair), not by the compare pipe")
+                            "bound by instruction issue (ncu: 7.6 instructions per pair at d = 3, 13.1 at d = 8), "
+                            "not by the compare pipe")
         if ctx.kd_levels:
             roof["note"] = (f"kd ordering: bits 0..{ctx.kd_levels - 1} are decided once per tile for most tiles, so fewer "
                             "than d compares are executed per pair and frac (algorithmic d compares per pair) can "
                             "exceed 1; DESIGN.md §7 'kd ordering'")
     # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture of this workload
-    # (profiles/traffic.json), used only when it was taken on the kernel variant that ran here (kd levels match)
+    # (profiles/traffic.json), used only when it was taken on the kernel variant that ran here (kd levels and rank lanes match)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp) and args.method == "exact":
         try:
             tj = json.load(open(tp)).get(args.workload)
-            if isinstance(tj, dict) and tj.get("kd_levels") == ctx.kd_levels:
+            if isinstance(tj, dict) and tj.get("kd_levels") == ctx.kd_levels and tj.get("rank_lanes", 0) == ctx.rank_lanes:
                 traffic = tj.get("dram_bytes_per_launch")
                 roof["traffic_source"] = tj.get("source")
         except Exception:
