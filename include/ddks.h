@@ -90,10 +90,11 @@ typedef enum {
                                       of the multi-GPU path (all-reduce / all-gather) through it; identical results */
 #define DDKS_FLAG_RDKS_FULL_SORT 128u /* TEST ONLY: ddks_rdks sorts every key (8-pass radix sort) instead of the bucket-pruned
                                          sweep that sorts only the buckets able to hold the maximum; identical results */
-#define DDKS_FLAG_NO_RANK 256u    /* TEST ONLY: never use the rank-lane count (ddks_stat at d = 8 compares each pair's
-                                      coordinates as 10-bit rank lanes, three integer adds per pair, instead of d FP32
-                                      compares; identical results)                                                  */
-#define DDKS_FLAG_FORCE_RANK 512u /* TEST ONLY: the rank-lane count also at d = 6 and 7 (identical results)            */
+#define DDKS_FLAG_NO_RANK 256u    /* TEST ONLY: never use the rank-lane count (ddks_stat at d = 3 and d = 5..8 and mid N
+                                      compares each pair's coordinates as 10-bit per-CTA rank lanes, ceil(d/3) integer
+                                      adds per pair, instead of d FP32 compares; identical results)                 */
+#define DDKS_FLAG_FORCE_RANK 512u /* TEST ONLY: the rank-lane count at every 2 <= d <= 8 and every N > 8192 whose sample
+                                      sizes allow DIFF counters (max(n_P, n_Q) / gcd <= 7); identical results         */
 #define DDKS_FLAG_PROFILE 8u      /* record CUDA events around every count-kernel launch (see ddks_profile_read) */
 
 typedef struct {
@@ -230,8 +231,8 @@ DDKS_API int64_t ddks_launch_count(const ddks_ctx* ctx);
  * K >= 1: bits 0..K-1 decided per tile where possible). Host-only, for tests and the bench line. */
 DDKS_API int32_t ddks_kd_levels(const ddks_ctx* ctx);
 
-/* 1 if the last count on this context was the rank-lane count (6 <= d <= 8, position order: each pair's d compares
- * are three 32-bit integer adds on 10-bit per-CTA rank lanes; DESIGN.md §7 "rank lanes"), else 0. Host-only. */
+/* 1 if the last count on this context was the rank-lane count (position order: each pair's d compares are
+ * ceil(d/3) 32-bit integer adds on 10-bit per-CTA rank lanes; DESIGN.md §7 "rank lanes"), else 0. Host-only. */
 DDKS_API int32_t ddks_rank_lanes(const ddks_ctx* ctx);
 
 /* Profiling (context created with DDKS_FLAG_PROFILE): totals since the last read, then reset.

@@ -1,5 +1,6 @@
 // ddks_rank.cuh — the rank-lane count: rows a3 + a4 (orthant classification + per-orthant counting)
-// for d = 6..8 in position order, with three integer adds per pair instead of d FP32 compares + d FFMAs.
+// for single DIFF statistics in position order, with ceil(d / 3) integer adds per pair instead of d FP32 compares +
+// d FFMAs (default at d = 3 and d = 5..8 in the measured N ranges of rank_applicable, ddks_api.cu).
 //
 // What it computes is unchanged (Eq. 3: bit k of the orthant code = [x_k >= o_k], P:L46 loop
 // method, P:L238 normalised difference): every (origin, point) pair of the CTA's 384 origins and the segment's points
@@ -9,15 +10,16 @@
 // multiset of its origins' x_k values. For any real x and any o in V_k
 //     x >= o   <=>   #{v in V_k : v <= x}  >=  #{v in V_k : v <= o}
 // (if x >= o every v <= o is <= x; if x < o, o itself is counted on the right and not on the left, and nothing counted
-// on the left is missing on the right). Both counts lie in [0, 512] (V_k is padded to 511 entries with +inf), so the
+// on the left is missing on the right). Both counts lie in [0, 511] (V_k is padded to 511 entries with +inf), so the
 // compare of two floats becomes the compare of two small integers rx = rank(x), ro = rank(o), and three of those fit
-// one 32-bit word: 10-bit lanes holding rx + (512 - ro) in [0, 1023] — no borrow, no carry between lanes — whose top
-// bit is exactly [x_k >= o_k]. Dim k lives in word k % 3, lane k / 3, at bit offset (k % 3) + 10 (k / 3), so the d
-// result bits of the three words sit at bits 9+j+10i (j = k % 3, i = k / 3) — three groups of three adjacent bits —
-// and one multiply by 1 + 2^7 + 2^14 moves group i to bits 23+3i.. with no overlapping partial products (DESIGN.md
-// derivation), leaving the orthant code sum_k [x_k >= o_k] 2^k in bits 23..31 exactly. Per pair: LDS.128 (broadcast),
-// 3 IADD, 3 LOP3, IMAD, SHF, IMAD (counter address), ATOMS — ~12 instructions at d = 8 against ~18 for the FP32 path
-// (8 FSET + 8 FFMA + ATOMS + 2 LDS.128 at one origin per thread).
+// one 32-bit word: 10-bit lanes holding rx + (512 - ro) in [1, 1023] — no borrow, no carry between lanes — whose top
+// bit is exactly [x_k >= o_k]. A point has NW = ceil(d / 3) rank words (1 for d <= 3, 2 for d = 4..6, 3 for d = 7, 8):
+// dim k lives in word j = k % NW, lane i = k / NW, at bit offset j + 10 i, so the d result bits of the OR of the masked
+// words sit at bits 9 + j + 10 i — three groups of NW adjacent bits — and one multiply (RankGeo::MUL: a sum of three
+// powers of two whose partial products never overlap, so no carries) moves group i next to group i - 1 at the top of
+// the word, leaving the orthant code sum_k [x_k >= o_k] 2^k after one shift. Per pair: NW IADD, NW LOP3, IMAD, SHF,
+// IMAD (counter address), ATOMS and 1 / PPL of a broadcast LDS.128 (PPL = 4, 2, 1 points per load): ~6.3
+// instructions at d = 3 and ~11 at d = 8, against d FSET + d FFMA + ATOMS + LDS for the FP32 path.
 //
 // The ranks of the points are taken per CTA and tile: each thread maps one point of the 384-point tile (d branch-free
 // searches of V_k, stored in Eytzinger order so the nine probe levels spread over the SMEM banks), the rank words go to

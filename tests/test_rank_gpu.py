@@ -2,6 +2,8 @@
 classified from 10-bit per-CTA rank lanes instead of FP32 compares, which must give exactly the statistic of the
 definition (Eq. 3, bit k = [x_k >= o_k]; Eq. 6). Compared with the CPU oracle element by
 element: num, den, the D bits, the argmax origin and the per-origin nums; tie-heavy, ragged and sharded cases."""
+import os
+
 import numpy as np
 import pytest
 
@@ -135,3 +137,24 @@ def test_rank_lane_graph_replay_and_fallbacks():
     with K.Context(flags=RANK) as c:
         r = c.stat(dev(P1), dev(Q1))
         assert c.rank_lanes == 0 and (r.num, r.argmax_origin) == (O.ddks(P1, Q1)[0], O.ddks(P1, Q1)[3])
+
+
+def _fuzz_cases(seed, n):
+    # DIFF-counter sizes n_P = m b', n_Q = m a' (a', b' <= 7) with 8192 < N <= ~15 000, so origin blocks, tiles and
+    # the P / Q boundary fall at arbitrary offsets; lcm > 32 767 for the larger ratios (several flush windows)
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        a, b = int(rng.integers(1, 8)), int(rng.integers(1, 8))
+        m = int(rng.integers(8193 // (a + b) + 1, 15000 // (a + b) + 1))
+        out.append((m * b, m * a, int(rng.integers(2, 9)), str(rng.choice(["normal", "grid", "mixed", "dup"])),
+                    int(rng.integers(0, 2 ** 31))))
+    return out
+
+
+@pytest.mark.parametrize("n_P,n_Q,d,kind,seed", _fuzz_cases(2025, int(os.environ.get("DDKS_FUZZ_CASES", "36")) // 3))
+def test_rank_lane_fuzz(n_P, n_Q, d, kind, seed):
+    P, Q = I.random_pair(seed, n_P, n_Q, d, kind)
+    with K.Context(flags=RANK) as c:
+        check(c, P, Q)
+        assert c.rank_lanes == 1
