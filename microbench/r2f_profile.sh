@@ -20,3 +20,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
    python bench.py --workload C3 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 timeout 300 python microbench/graph_ab.py 30 > $O/${TAG}_graph_ab.txt 2>&1
 du -sh $O; tail -2 $O/${TAG}_pytest_gpu.log; tail -2 $O/${TAG}_smoke.log; cat $O/${TAG}_bench_c5_default.json | head -c 600
+bash microbench/r2f_ncu_rank.sh C3 $TAG > $O/${TAG}_ncu_full_rank_c3.json 2>/dev/null
+bash microbench/r2f_ncu_rank.sh C2 $TAG > $O/${TAG}_ncu_full_rank_c2.json 2>/dev/null
+rm -f $O/${TAG}_full_rank_*_source.csv
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${TAG}_launches_C2.csv \
+   python bench.py --workload C2 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
