@@ -19,10 +19,15 @@ def timed(c, f, reps=7):
     return r, float(np.median(ts)), kms / max(kl, 1) * 1.0
 
 
-cases = [("C3", None), ("C2", None)] + [(f"d{d} N{n}", (d, n)) for d in (8, 7, 6, 5, 4, 3, 2)
-                                        for n in (10000, 20000, 40000, 100000, 400000)]
-if len(sys.argv) > 1:
-    cases = [c for c in cases if any(s in c[0] for s in sys.argv[1:])]
+NS = (10000, 20000, 40000, 100000, 400000)
+args = sys.argv[1:]
+for a in list(args):  # --n=60000,80000: other sizes (threshold search)
+    if a.startswith("--n="):
+        NS = tuple(int(x) for x in a[4:].split(","))
+        args.remove(a)
+cases = [("C3", None), ("C2", None)] + [(f"d{d} N{n}", (d, n)) for d in (8, 7, 6, 5, 4, 3, 2) for n in NS]
+if args:
+    cases = [c for c in cases if any(s in c[0] for s in args)]
 modes = [("rank", K.DDKS_FLAG_FORCE_RANK), ("fp32-auto", K.DDKS_FLAG_NO_RANK), ("fp32-pos", K.DDKS_FLAG_NO_RANK | K.DDKS_FLAG_NO_X0)]
 for name, spec in cases:
     if spec is None:

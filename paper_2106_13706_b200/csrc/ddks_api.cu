@@ -137,14 +137,16 @@ bool rank_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q) {
     // (C3 0.88 vs 1.17 ms; 78 vs 82 ms at 4e5, the kd count's decided bits catch up beyond); d = 7: up to N ~ 5e4;
     // d = 6 (two words): 0.64 vs 0.89 ms at 4e4, 3.48 vs 3.87 at 1e5, 54 vs 46 at 4e5; d = 5: 0.58 vs 0.67 at 4e4,
     // 3.21 vs 3.10 at 1e5; d = 3 (one word; C2 0.156 vs 0.164 ms): 0.430 vs 0.453 at 4e4, 2.34 vs 2.01 at 1e5;
-    // d = 4 ties and d = 2 loses (their FP32 counts are 9.6 / 5.7 instructions per pair already)
+    // d = 4 ties and d = 2 loses (their FP32 counts are 9.6 / 5.7 instructions per pair already). Finer sweep
+    // (N = 6e4, 8e4, 1.5e5, 2e5; call ms rank vs kd): d = 7 1.85 / 1.91, 3.23 / 3.09; d = 6 1.31 / 1.62, 2.26 / 2.70,
+    // 7.71 / 8.13, 13.6 / 13.2; d = 5 1.20 / 1.23, 2.08 / 2.14, 7.08 / 6.11; d = 3 0.860 / 0.880, 1.477 / 1.467
     const int64_t N = n_P + n_Q;
     switch (d) {
         case 8: return N <= 600000;
-        case 7: return N <= 50000;
-        case 6: return N <= 120000;
-        case 5: return N <= 60000;
-        case 3: return N <= 50000;
+        case 7: return N <= 70000;
+        case 6: return N <= 170000;
+        case 5: return N <= 90000;
+        case 3: return N <= 65000;
     }
     return false;
 }

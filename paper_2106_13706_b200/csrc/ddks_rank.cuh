@@ -35,6 +35,13 @@ namespace {
 #define DDKS_RK_PTS 24
 #endif
 constexpr int RK_PTS = DDKS_RK_PTS;
+#ifndef DDKS_RK_PTS1  // the same for one rank word per point (d <= 3: four points per LDS.128)
+#define DDKS_RK_PTS1 16
+#endif
+#ifndef DDKS_RK_CTAS1  // resident CTAs per SM the d <= 3 kernels are register-capped for (16 x 4 measured best at C2:
+                       // count 0.107 ms against 0.109 - 0.111 for 24 x 3, 32 x 3, 16 x 3, 24 x 4)
+#define DDKS_RK_CTAS1 4
+#endif
 #ifndef DDKS_RK_R  // origins per thread of the rank-lane count (1: 384 threads, 2: 192 threads)
 #define DDKS_RK_R 1
 #endif
@@ -59,7 +66,8 @@ template <int D> struct RankGeo {
     static constexpr int VW = 512;             // floats per (block, dim) in the workspace and in SMEM
     static constexpr int HIST_WORDS = NB * WPB;
     static constexpr int SMEM_BYTES = HIST_WORDS * 4 + D * VW * 4 + 2 * TILE * NWS * 4 + 64;
-    static constexpr int MIN_CTAS = D >= 8 ? 1 : (D >= 6 ? 2 : 3);
+    static constexpr int MIN_CTAS = D >= 8 ? 1 : (D >= 6 ? 2 : (D >= 4 ? 3 : DDKS_RK_CTAS1));
+    static constexpr int PTS = NW == 1 ? DDKS_RK_PTS1 : RK_PTS;  // points per step of the count loop
     static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
     __host__ __device__ static constexpr int slot(int t) { return t % WPB; }
     __host__ __device__ static constexpr bool high(int t) { return t >= WPB; }
@@ -164,7 +172,8 @@ __global__ void __launch_bounds__(RankGeo<D>::ORIGINS / RR, RankGeo<D>::MIN_CTAS
     using G = RankGeo<D>;
     constexpr int OB = G::ORIGINS, T = OB / RR, TILE = G::TILE, WPB = G::WPB, DP = padded_dim<D>();
     constexpr int NW = G::NW, NWS = G::NWS, PPL = G::PPL;
-    static_assert(RK_PTS % 4 == 0, "whole LDS.128 groups per step");
+    constexpr int PTS = G::PTS;
+    static_assert(PTS % 4 == 0, "whole LDS.128 groups per step");
     static_assert(RR == 1 || RR == 2, "one or two origins per thread");
     constexpr uint32_t M0 = rank_mask(0, D), M1 = rank_mask(1, D), M2 = rank_mask(2, D);
     extern __shared__ __align__(128) uint8_t smem[];
@@ -268,14 +277,14 @@ __global__ void __launch_bounds__(RankGeo<D>::ORIGINS / RR, RankGeo<D>::MIN_CTAS
                 };
                 int p = lo;
                 for (; p < hi && (p % PPL) != 0; ++p) count_one(p);  // up to a 16-byte boundary of the tile
-                // RK_PTS points per step, all loads issued first: RK_PTS x RR independent chains per warp
+                // PTS points per step, all loads issued first: PTS x RR independent chains per warp
 #pragma unroll 1
-                for (; p + RK_PTS <= hi; p += RK_PTS) {
-                    uint4 xv[RK_PTS / PPL];
+                for (; p + PTS <= hi; p += PTS) {
+                    uint4 xv[PTS / PPL];
 #pragma unroll
-                    for (int j = 0; j < RK_PTS / PPL; ++j) xv[j] = lds_v4(reinterpret_cast<const uint4*>(Wt + p * NWS) + j);
+                    for (int j = 0; j < PTS / PPL; ++j) xv[j] = lds_v4(reinterpret_cast<const uint4*>(Wt + p * NWS) + j);
 #pragma unroll
-                    for (int j = 0; j < RK_PTS / PPL; ++j) count_v4(xv[j]);
+                    for (int j = 0; j < PTS / PPL; ++j) count_v4(xv[j]);
                 }
                 for (; p < hi; ++p) count_one(p);
             }
