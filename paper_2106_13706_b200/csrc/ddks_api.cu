@@ -126,12 +126,30 @@ int pad_dim(int d) { return d <= 4 ? 4 : 8; }
 // DIFF counters fit (|c_P a - c_Q b| stays in int32 and the int16 window is >= 4096 points); else SPLIT
 bool diff_counters_ok(int64_t n_P, int64_t n_Q);
 
-// the rank-lane count (ddks_rank.cuh) takes a position-ordered DIFF statistic at d = 3 and 5..8 in its measured range
-// (d = 2..8 at any size with DDKS_FLAG_FORCE_RANK); the >= convention only; not for the small geometry
-bool rank_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q) {
+// the rank-lane count (ddks_rank.cuh) takes a position-ordered statistic at d = 3 and 5..8 in its measured range
+// (d = 2..8 at any size with DDKS_FLAG_FORCE_RANK); the >= convention only; not for the small geometry. force_split:
+// the caller needs SPLIT counters (significance); sample sizes whose DIFF counters would overflow need them too.
+bool rank_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q, bool force_split) {
     if (ctx->flags & (DDKS_FLAG_NO_RANK | DDKS_FLAG_TIES_GT)) return false;
-    if (d < 2 || d > 8 || n_P + n_Q <= ddks::kSmallN || !diff_counters_ok(n_P, n_Q)) return false;
+    if (d < 2 || d > 8 || n_P + n_Q <= ddks::kSmallN) return false;
+    const bool split = force_split || !diff_counters_ok(n_P, n_Q);
     if (ctx->flags & DDKS_FLAG_FORCE_RANK) return true;
+    const int64_t N = n_P + n_Q;
+    if (split) {
+        // SPLIT (two launches, +1 per pair; ddks_api_rank.cu) against the FP32 SPLIT counts, kd-ordered where that
+        // applies, which run 6 warps per SM at d = 8 (microbench/rank_split_ab.py, profiles/r2f_rank_split_ab.txt; warm
+        // ms, significance | statistic with coprime sizes): d = 8 0.46 vs 1.20 | 0.33 vs 0.58 at N = 2e4, 1.14 vs 1.69 |
+        // 0.93 vs 1.48 at 4e4 (C3), 20.6 vs 31.6 | 19.7 vs 30.4 at 2e5; d = 7 0.42 vs 0.49 at 2e4, 20.5 vs 22.4 | 19.6 vs
+        // 21.0 at 2e5, slower at 1e4; d = 6 0.35 vs 0.40 at 2e4, 4.10 vs 4.98 | 3.57 vs 3.98 at 1e5, even at 2e5,
+        // slower at 1e4; d = 5 0.85 vs 0.97 | 0.59 vs 0.71 at 4e4, 3.77 vs 4.04 | 3.17 vs 2.97 at 1e5; d = 3 never
+        switch (d) {
+            case 8: return N <= 600000;
+            case 7: return N >= 15000 && N <= 250000;
+            case 6: return N >= 15000 && N <= 150000;
+            case 5: return N >= 30000 && N <= 90000;
+        }
+        return false;
+    }
     // measured against the kd-ordered and position-ordered FP32 counts (microbench/rank_ab.py,
     // profiles/r2e_rank_ab.txt, r2f_rank_ab.txt; warm call times). d = 8 (three rank words): faster at N = 1e4 .. 4e5
     // (C3 0.88 vs 1.17 ms; 78 vs 82 ms at 4e5, the kd count's decided bits catch up beyond); d = 7: up to N ~ 5e4;
@@ -140,7 +158,6 @@ bool rank_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q) {
     // d = 4 ties and d = 2 loses (their FP32 counts are 9.6 / 5.7 instructions per pair already). Finer sweep
     // (N = 6e4, 8e4, 1.5e5, 2e5; call ms rank vs kd): d = 7 1.85 / 1.91, 3.23 / 3.09; d = 6 1.31 / 1.62, 2.26 / 2.70,
     // 7.71 / 8.13, 13.6 / 13.2; d = 5 1.20 / 1.23, 2.08 / 2.14, 7.08 / 6.11; d = 3 0.860 / 0.880, 1.477 / 1.467
-    const int64_t N = n_P + n_Q;
     switch (d) {
         case 8: return N <= 600000;
         case 7: return N <= 70000;
@@ -175,8 +192,9 @@ ddks_status launch_count_d(ddks_ctx* ctx, const CountPlan& pl, const ddks::Count
 ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int64_t n_P, int64_t n_Q,
                       int64_t o_begin, int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st,
                       bool force_split, unsigned long long* hist, bool wx, unsigned long long* best_key) {
-    if (B == 1 && !force_split && rank_applicable(ctx, d, n_P, n_Q))  // the rank-lane count (ddks_rank.cuh)
-        return run_count_rank(ctx, packed, d, n_P, n_Q, o_begin, o_end, item_num, per_origin, st, best_key);
+    if (B == 1 && !wx && rank_applicable(ctx, d, n_P, n_Q, force_split))  // the rank-lane count (ddks_rank.cuh)
+        return run_count_rank(ctx, packed, d, n_P, n_Q, o_begin, o_end, item_num, per_origin, st, best_key,
+                              force_split || !diff_counters_ok(n_P, n_Q), hist);
     const int64_t N = n_P + n_Q;
     const uint64_t g = gcd_u64((uint64_t)n_P, (uint64_t)n_Q);
     const uint64_t a_ = (uint64_t)n_Q / g, b_ = (uint64_t)n_P / g;
@@ -250,7 +268,7 @@ bool diff_counters_ok(int64_t n_P, int64_t n_Q) {
     return !(std::max(a_, b_) > 32767 / 4096 || (uint64_t)n_P * a_ >= 0x7fffffffull || (uint64_t)n_Q * b_ >= 0x7fffffffull);
 }
 
-bool x0_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q) {
+bool x0_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q, bool force_split) {
     if (ctx->flags & DDKS_FLAG_NO_X0) return false;
     // the sort pays for itself once the O(N^2) count dominates; DDKS_FLAG_FORCE_X0 (tests) lowers the bar. Crossover
     // (microbench/kd_threshold.py, profiles/r2_kd_midN_bucket.txt): radix-sorted kd at N ~ 60k-75k for d = 2..8; with
@@ -259,7 +277,7 @@ bool x0_applicable(ddks_ctx* ctx, int d, int64_t n_P, int64_t n_Q) {
     // With the cluster ordering (round 2, second session; profiles/r2b_kd_threshold.txt): d = 8 pays from N = 20 000
     // (1.03x, 1.12x at 30 000), d = 3 from ~30 000 (1.15x), d = 4..6 only from ~40 000 (1.00-1.06x)
     // the rank-lane count beats the kd ordering at d = 8 (and is position-ordered: no sort)
-    if (!(ctx->flags & DDKS_FLAG_FORCE_X0) && rank_applicable(ctx, d, n_P, n_Q)) return false;
+    if (!(ctx->flags & DDKS_FLAG_FORCE_X0) && rank_applicable(ctx, d, n_P, n_Q, force_split)) return false;
     const bool single = ctx->world == 1;
     const int64_t mid = d >= 8 ? 20000 : (d == 3 ? 28000 : 40000);
     const int64_t min_n = (ctx->flags & DDKS_FLAG_FORCE_X0) ? 2 : (single && d >= 3 ? mid : 80000);
@@ -295,7 +313,7 @@ ddks_status count_statistic(ddks_ctx* ctx, const float* packed, int d, int64_t n
     ddks_status s;
     const bool use_key = !export_per && argmax_key_fits(n_P, n_Q);
     unsigned long long* key = use_key ? &dres->key : nullptr;
-    const bool x0 = !export_per && x0_applicable(ctx, d, n_P, n_Q);
+    const bool x0 = !export_per && x0_applicable(ctx, d, n_P, n_Q, split);
     *per_out = nullptr;
     ctx->rank_lanes = 0;  // set by run_count_rank when the rank-lane count runs
     if (x0) {

@@ -169,11 +169,12 @@ ddks_status run_count(ddks_ctx* ctx, const float* packed, int d, int64_t B, int6
                       int64_t o_begin, int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st,
                       bool force_split = false, unsigned long long* hist = nullptr, bool wx = false,
                       unsigned long long* best_key = nullptr);
-// the rank-lane count (ddks_rank.cuh, ddks_api_rank.cu): one DIFF statistic (B == 1) at 6 <= d <= 8, >= convention,
-// position order, origins [o_begin, o_end); results as run_count
+// the rank-lane count (ddks_rank.cuh, ddks_api_rank.cu): one statistic (B == 1) at 2 <= d <= 8, >= convention,
+// position order, origins [o_begin, o_end); DIFF counters, or SPLIT (c_P and c_Q apart, hist as run_count) in two
+// launches over the P rows and the Q rows; results as run_count
 ddks_status run_count_rank(ddks_ctx* ctx, const float* packed, int d, int64_t n_P, int64_t n_Q, int64_t o_begin,
                            int64_t o_end, uint64_t* item_num, uint64_t* per_origin, cudaStream_t st,
-                           unsigned long long* best_key);
+                           unsigned long long* best_key, bool split = false, unsigned long long* hist = nullptr);
 // items sharded contiguously over ranks: one all-gather of padded records (n_arr arrays + flags) into host hbuf
 ddks_status gather_items(ddks_ctx* ctx, uint64_t* const* dev, int n_arr, int64_t total, const uint32_t* dflag,
                          cudaStream_t st, uint64_t* hbuf);

@@ -160,7 +160,9 @@ __device__ __forceinline__ void rank_words(const float* V, const float (&x)[D], 
 // them), or -- a.accum == nullptr, one CTA per whole block -- finalises in-kernel.
 struct RankArgs {
     const float* vsorted;  // [blocks][D][VW] Eytzinger trees (k_rank_sort)
-    int32_t n_tiles;       // tiles per block (the point set in 384-point tiles)
+    int32_t pt_begin;      // the rows counted by this launch: [pt_begin, pt_end) -- all N rows for DIFF counters; SPLIT
+    int32_t pt_end;        //   counters (c_P and c_Q kept apart) take the P rows and the Q rows in two launches
+    int32_t n_tiles;       // tiles per block (the rows of the launch in 384-point tiles)
     int32_t chunk_tiles;   // tiles per flush window
     int64_t units;         // blocks * n_tiles
 };
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(RankGeo<D>::ORIGINS / RR, RankGeo<D>::MIN_CTAS
         const int32_t te = (int32_t)min((int64_t)min(ra.n_tiles, tb + ra.chunk_tiles), (int64_t)tb + (u_end - u));
         u += te - tb;
         const int32_t blk_o0 = a.o_begin + by * OB;
-        const int32_t seg0 = tb * TILE, seg1 = min(a.N, te * TILE);
+        const int32_t seg0 = ra.pt_begin + tb * TILE, seg1 = min(ra.pt_end, ra.pt_begin + te * TILE);
         const int n_tiles = te - tb;
         ++visits;
         pts_done += (unsigned long long)(seg1 - seg0);

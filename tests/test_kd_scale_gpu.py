@@ -20,7 +20,8 @@ def dev(a):
 
 @pytest.fixture(scope="module")
 def ctxs():
-    with K.Context() as kd, K.Context(flags=K.DDKS_FLAG_NO_X0) as pos:
+    # NO_RANK: these tests are about the kd-ordered FP32 count (the rank-lane count would take some of the sizes)
+    with K.Context(flags=K.DDKS_FLAG_NO_RANK) as kd, K.Context(flags=K.DDKS_FLAG_NO_X0 | K.DDKS_FLAG_NO_RANK) as pos:
         yield kd, pos
 
 

@@ -488,18 +488,17 @@ def test_profile_clock_probe():
 @pytest.mark.parametrize("n_P,n_Q,d,kind", [(12000, 11000, 8, "normal"), (15000, 14000, 3, "mixed"),
                                             (21000, 19500, 5, "grid")])
 def test_default_mid_n_kd_path(n_P, n_Q, d, kind):
-    # sizes just above the default kd thresholds (d = 8 from 20 000 rows, d = 3 from 28 000, d = 5 from 40 000): the
-    # unforced call takes the kd count with the cluster mid-N ordering and must equal the oracle bit for bit
+    # sizes just above the default kd thresholds (d = 8 from 20 000 rows, d = 3 from 28 000, d = 5 from 40 000) whose
+    # sample-size ratios need SPLIT counters: without the rank lanes the unforced call takes the kd count with the
+    # cluster mid-N ordering; with them (the default at d = 5..8 here) the two-launch SPLIT rank-lane count. Both must
+    # equal the oracle bit for bit
     P, Q = I.random_pair(9700 + d, n_P, n_Q, d, kind)
     if kind == "grid":
         P[:, :2] = np.round(P[:, :2] * 4) / 4
         Q[:, :2] = np.round(Q[:, :2] * 4) / 4
     with K.Context() as c:
         check_pair(c, P, Q)
-        # d = 8 with DIFF counters takes the rank-lane count (position order; test_rank_gpu.py); 12000 + 11000 needs
-        # SPLIT counters (a = 11, b = 12), which the rank-lane count does not have, so it stays on the kd count
+        assert (c.rank_lanes == 1 and c.kd_levels == 0) if d >= 5 else (c.kd_levels >= 1 and c.rank_lanes == 0)
+    with K.Context(flags=K.DDKS_FLAG_NO_RANK) as c:
+        check_pair(c, P, Q)
         assert c.kd_levels >= 1 and c.rank_lanes == 0
-    if d == 8:
-        with K.Context(flags=K.DDKS_FLAG_NO_RANK) as c:
-            check_pair(c, P, Q)
-            assert c.kd_levels >= 1

@@ -63,8 +63,9 @@ def test_rank_lane_per_origin(d):
         assert np.array_equal(got, want[383:4000])
 
 
-def test_rank_lane_shards():
-    P, Q = I.random_pair(32100, 7000, 6000, 8, "grid")
+@pytest.mark.parametrize("n_P,n_Q", [(7000, 6000), (7000, 6001)])  # DIFF counters; SPLIT counters
+def test_rank_lane_shards(n_P, n_Q):
+    P, Q = I.random_pair(32100, n_P, n_Q, 8, "grid")
     want = O.ddks(P, Q)
     with K.Context(flags=RANK) as c:
         check(c, P, Q, want)
@@ -121,8 +122,8 @@ def test_rank_lane_default_at_d7_mid_n():
 
 
 def test_rank_lane_graph_replay_and_fallbacks():
-    # the captured call graph replays the rank-lane count (and reports it); SPLIT-only sizes and the > convention
-    # take the FP32 counts
+    # the captured call graph replays the rank-lane count (and reports it); the > convention and small N take the
+    # FP32 counts; sizes that need SPLIT counters take the two-launch SPLIT rank-lane count
     P, Q = I.random_pair(32400, 6000, 5000, 8, "mixed")
     want = O.ddks(P, Q)
     dP, dQ = dev(P), dev(Q)
@@ -134,9 +135,17 @@ def test_rank_lane_graph_replay_and_fallbacks():
         r = c.stat(dP, dQ)
         assert c.rank_lanes == 0 and r.num == O.ddks(P, Q, ties_gt=True)[0]
     P1, Q1 = I.random_pair(32401, 9000, 7, 8, "normal")  # a = 9000 / gcd: DIFF counters would overflow -> SPLIT
-    with K.Context(flags=RANK) as c:
+    with K.Context() as c:
+        for _ in range(3):
+            r = c.stat(dev(P1), dev(Q1))
+            assert c.rank_lanes == 1 and (r.num, r.argmax_origin) == (O.ddks(P1, Q1)[0], O.ddks(P1, Q1)[3])
+    with K.Context(flags=K.DDKS_FLAG_NO_RANK) as c:
         r = c.stat(dev(P1), dev(Q1))
         assert c.rank_lanes == 0 and (r.num, r.argmax_origin) == (O.ddks(P1, Q1)[0], O.ddks(P1, Q1)[3])
+    P2, Q2 = I.random_pair(32402, 3000, 2000, 8, "normal")  # N <= 8192: the fused small-N statistic
+    with K.Context(flags=RANK) as c:
+        r = c.stat(dev(P2), dev(Q2))
+        assert c.rank_lanes == 0 and r.num == O.ddks(P2, Q2)[0]
 
 
 def _fuzz_cases(seed, n):
@@ -158,3 +167,51 @@ def test_rank_lane_fuzz(n_P, n_Q, d, kind, seed):
     with K.Context(flags=RANK) as c:
         check(c, P, Q)
         assert c.rank_lanes == 1
+
+
+# ---------------------------------------------------------------------------------------- SPLIT counters
+# sample sizes whose DIFF counters would overflow (max(n_P, n_Q) / gcd > 7) and the significance's M_T histogram: the
+# rank-lane count keeps c_P and c_Q apart (P rows and Q rows in two launches, +1 per pair; Eq. 5)
+
+SPLIT_SIZES = [(4100, 4093), (5000, 7001), (9001, 3000), (300, 8000)]
+
+
+@pytest.mark.parametrize("d", [2, 3, 5, 6, 7, 8])
+@pytest.mark.parametrize("kind", ["normal", "grid", "dup"])
+def test_rank_lane_split_parity(d, kind):
+    with K.Context(flags=RANK) as c:
+        for i, (n_P, n_Q) in enumerate(SPLIT_SIZES):
+            P, Q = I.random_pair(34000 + 100 * d + 7 * i + 11 * ["normal", "grid", "dup"].index(kind), n_P, n_Q, d, kind)
+            check(c, P, Q)
+            assert c.rank_lanes == 1
+
+
+def test_rank_lane_split_window_and_per_origin():
+    # n_P = 40 000 > 32 767: the P pass flushes its 16-bit counters in two windows; per-origin nums of a range
+    P, Q = I.random_pair(34500, 40000, 1201, 6, "mixed")
+    want = O.per_origin(P, Q, 39000, 41201)
+    with K.Context(flags=RANK) as c, K.Context(flags=K.DDKS_FLAG_NO_RANK | K.DDKS_FLAG_NO_X0) as cf:
+        got = c.stat_per_origin(dev(P), dev(Q), 39000, 41201)
+        assert c.rank_lanes == 1
+        assert np.array_equal(got, want)
+        assert c.stat(dev(P), dev(Q)) == cf.stat(dev(P), dev(Q))
+        assert c.rank_lanes == 1 and cf.rank_lanes == 0
+
+
+@pytest.mark.parametrize("n_P,n_Q,d,kind", [(4200, 4100, 8, "normal"), (5000, 5000, 6, "grid"), (3000, 6000, 7, "mixed"),
+                                            (4500, 4000, 3, "dup")])
+def test_rank_lane_significance(n_P, n_Q, d, kind):
+    # the significance through the SPLIT rank-lane count: the M_T histogram equals the oracle's membership counts
+    # (P:L208-209), statistic and argmax equal the oracle's, and log_prod is bit-identical to the FP32 count's
+    P, Q = I.random_pair(34600 + d, n_P, n_Q, d, kind)
+    with K.Context(flags=RANK) as c, K.Context(flags=K.DDKS_FLAG_NO_RANK | K.DDKS_FLAG_NO_X0) as cf:
+        a = c.significance(dev(P), dev(Q), detail=True)
+        assert c.rank_lanes == 1
+        b = cf.significance(dev(P), dev(Q), detail=True)
+        assert cf.rank_lanes == 0
+    assert a.stat == b.stat and np.array_equal(a.mt_hist, b.mt_hist) and a.log_prod == b.log_prod
+    pooled = np.concatenate([P, Q])
+    MT = O.membership(Q, pooled)
+    assert np.array_equal(a.mt_hist, np.bincount(MT.ravel(), minlength=n_Q + 1).astype(np.uint64))
+    want = O.ddks(P, Q)
+    assert (a.stat.num, a.stat.argmax_origin) == (want[0], want[3])
