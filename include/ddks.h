@@ -93,8 +93,9 @@ typedef enum {
 #define DDKS_FLAG_NO_RANK 256u    /* TEST ONLY: never use the rank-lane count (ddks_stat at d = 3 and d = 5..8 and mid N
                                       compares each pair's coordinates as 10-bit per-CTA rank lanes, ceil(d/3) integer
                                       adds per pair, instead of d FP32 compares; identical results)                 */
-#define DDKS_FLAG_FORCE_RANK 512u /* TEST ONLY: the rank-lane count at every 2 <= d <= 8 and every N > 8192 whose sample
-                                      sizes allow DIFF counters (max(n_P, n_Q) / gcd <= 7); identical results         */
+#define DDKS_FLAG_FORCE_RANK 512u /* TEST ONLY: the rank-lane count at every 2 <= d <= 8 and every N > 8192 (DIFF counters
+                                      when max(n_P, n_Q) / gcd <= 7, else SPLIT in two launches; also for
+                                      ddks_significance); identical results                                          */
 #define DDKS_FLAG_PROFILE 8u      /* record CUDA events around every count-kernel launch (see ddks_profile_read) */
 
 typedef struct {

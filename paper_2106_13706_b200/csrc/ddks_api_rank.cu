@@ -1,7 +1,7 @@
 // ddks_api_rank.cu — host launch of the rank-lane count (ddks_rank.cuh): position-ordered single statistics at
-// d = 6..8 with DIFF counters and the >= convention. Segment planning and the finaliser are the ones of
-// launch_count_t (ddks_launch.cuh); the partial counters use the same [bin][origin offset] layout, so k_finalize<D>
-// reads them unchanged.
+// d = 2..8 with the >= convention; DIFF counters in one launch, SPLIT counters (c_P and c_Q apart) in two launches
+// over the P rows and the Q rows. The finaliser is the one of launch_count_t (ddks_launch.cuh); the partial counters
+// use the same [bin][origin offset] layout, so k_finalize<D, SPLIT> reads them unchanged.
 #include "ddks_launch.cuh"
 #include "ddks_rank.cuh"
 

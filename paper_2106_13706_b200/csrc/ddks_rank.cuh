@@ -1,6 +1,7 @@
 // ddks_rank.cuh — the rank-lane count: rows a3 + a4 (orthant classification + per-orthant counting)
-// for single DIFF statistics in position order, with ceil(d / 3) integer adds per pair instead of d FP32 compares +
-// d FFMAs (default at d = 3 and d = 5..8 in the measured N ranges of rank_applicable, ddks_api.cu).
+// for single statistics in position order, with ceil(d / 3) integer adds per pair instead of d FP32 compares +
+// d FFMAs (default at d = 3 and d = 5..8 in the measured N ranges of rank_applicable, ddks_api.cu). DIFF counters in
+// one launch; SPLIT counters as two launches over the P rows and the Q rows (RankArgs::pt_begin / pt_end).
 //
 // What it computes is unchanged (Eq. 3: bit k of the orthant code = [x_k >= o_k], P:L46 loop
 // method, P:L238 normalised difference): every (origin, point) pair of the CTA's 384 origins and the segment's points
