@@ -104,13 +104,15 @@ ddks_status launch_count_rank_d(ddks_ctx* ctx, const CountPlan& pl, ddks::CountA
         a.clk = (unsigned long long*)ctx->prof_clk.p;
     }
     int32_t* const acc0 = a.accum;
+    const int32_t N_all = a.N, nP_all = a.n_P;
     for (int ps = 0; ps < n_pass; ++ps) {
         const int32_t rows = rng[ps][1] - rng[ps][0];
         if (rows <= 0) continue;
         ddks::RankArgs ra{};
         ra.vsorted = vs;
-        ra.pt_begin = rng[ps][0];
-        ra.pt_end = rng[ps][1];
+        ra.pt_rows = a.pts + (size_t)rng[ps][0] * ddks::padded_dim<D>();
+        a.N = rows;                                          // rows of this launch ...
+        a.n_P = pl.split ? (ps == 0 ? rows : 0) : nP_all;    // ... of which the first n_P add inc P
         ra.n_tiles = (rows + G::TILE - 1) / G::TILE;
         ra.chunk_tiles = whole ? ra.n_tiles : std::max(1, (int)(pl.window / G::TILE));
         ra.units = (int64_t)blocks_o * ra.n_tiles;
@@ -121,6 +123,8 @@ ddks_status launch_count_rank_d(ddks_ctx* ctx, const CountPlan& pl, ddks::CountA
         CHECK_LAUNCH();
         ctx->launches++;
     }
+    a.N = N_all;
+    a.n_P = nP_all;
     a.accum = acc0;
     if (ev.first) {
         CU(record_event(ev.second, st));
@@ -134,8 +138,11 @@ ddks_status launch_count_rank_d(ddks_ctx* ctx, const CountPlan& pl, ddks::CountA
         constexpr int TPS = NQ >= 256 ? 8 : (NQ >= 128 ? 4 : (NQ >= 64 ? 2 : 1));
         const int64_t per_cta = threads / TPS;
         const int blocks = (int)std::min<int64_t>((total + per_cta - 1) / per_cta, 148 * 16);
+#ifndef DDKS_RANK_NO_SPLIT_FIN
         if (pl.split) ddks::k_finalize<D, true, false><<<blocks, threads, 0, st>>>(a, 1);
-        else ddks::k_finalize<D, false, false><<<blocks, threads, 0, st>>>(a, 1);
+        else
+#endif
+            ddks::k_finalize<D, false, false><<<blocks, threads, 0, st>>>(a, 1);
         CHECK_LAUNCH();
         ctx->launches++;
     }

@@ -1,7 +1,7 @@
 // ddks_rank.cuh — the rank-lane count: rows a3 + a4 (orthant classification + per-orthant counting)
 // for single statistics in position order, with ceil(d / 3) integer adds per pair instead of d FP32 compares +
 // d FFMAs (default at d = 3 and d = 5..8 in the measured N ranges of rank_applicable, ddks_api.cu). DIFF counters in
-// one launch; SPLIT counters as two launches over the P rows and the Q rows (RankArgs::pt_begin / pt_end).
+// one launch; SPLIT counters as two launches over the P rows and the Q rows (RankArgs::pt_rows with a.N / a.n_P set per launch).
 //
 // What it computes is unchanged (Eq. 3: bit k of the orthant code = [x_k >= o_k], P:L46 loop
 // method, P:L238 normalised difference): every (origin, point) pair of the CTA's 384 origins and the segment's points
@@ -161,8 +161,9 @@ __device__ __forceinline__ void rank_words(const float* V, const float (&x)[D], 
 // them), or -- a.accum == nullptr, one CTA per whole block -- finalises in-kernel.
 struct RankArgs {
     const float* vsorted;  // [blocks][D][VW] Eytzinger trees (k_rank_sort)
-    int32_t pt_begin;      // the rows counted by this launch: [pt_begin, pt_end) -- all N rows for DIFF counters; SPLIT
-    int32_t pt_end;        //   counters (c_P and c_Q kept apart) take the P rows and the Q rows in two launches
+    const float* pt_rows;  // the rows counted by this launch, a.N of them, the first a.n_P with inc P: all packed rows for
+                           //   DIFF counters; SPLIT counters (c_P and c_Q kept apart) take the P rows and the Q rows in
+                           //   two launches (the origins always come from a.pts)
     int32_t n_tiles;       // tiles per block (the rows of the launch in 384-point tiles)
     int32_t chunk_tiles;   // tiles per flush window
     int64_t units;         // blocks * n_tiles
@@ -186,6 +187,7 @@ __global__ void __launch_bounds__(RankGeo<D>::ORIGINS / RR, RankGeo<D>::MIN_CTAS
 
     const int t = threadIdx.x;
     const float* pts = a.pts;
+    const float* ppts = ra.pt_rows;
     uint32_t ubase[RR], incP[RR], incQ[RR];
 #pragma unroll
     for (int r = 0; r < RR; ++r) {
@@ -209,7 +211,7 @@ __global__ void __launch_bounds__(RankGeo<D>::ORIGINS / RR, RankGeo<D>::MIN_CTAS
         const int32_t te = (int32_t)min((int64_t)min(ra.n_tiles, tb + ra.chunk_tiles), (int64_t)tb + (u_end - u));
         u += te - tb;
         const int32_t blk_o0 = a.o_begin + by * OB;
-        const int32_t seg0 = ra.pt_begin + tb * TILE, seg1 = min(ra.pt_end, ra.pt_begin + te * TILE);
+        const int32_t seg0 = tb * TILE, seg1 = min(a.N, te * TILE);
         const int n_tiles = te - tb;
         ++visits;
         pts_done += (unsigned long long)(seg1 - seg0);
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(RankGeo<D>::ORIGINS / RR, RankGeo<D>::MIN_CTAS
             int32_t oi = blk_o0 + t + r * T;
             oi = oi < a.o_end ? oi : a.o_end - 1;
             load_point<D>(pts + (int64_t)oi * DP, o[r]);
-            if (seg0 + t + r * T < seg1) load_point<D>(pts + (int64_t)(seg0 + t + r * T) * DP, xn[r]);
+            if (seg0 + t + r * T < seg1) load_point<D>(ppts + (int64_t)(seg0 + t + r * T) * DP, xn[r]);
         }
         __syncthreads();  // V visible
         uint32_t ow[RR][3];
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(RankGeo<D>::ORIGINS / RR, RankGeo<D>::MIN_CTAS
             const int32_t pn = seg0 + (it + 1) * TILE + t;
 #pragma unroll
             for (int r = 0; r < RR; ++r)
-                if (it + 1 < n_tiles && pn + r * T < seg1) load_point<D>(pts + (int64_t)(pn + r * T) * DP, xn[r]);
+                if (it + 1 < n_tiles && pn + r * T < seg1) load_point<D>(ppts + (int64_t)(pn + r * T) * DP, xn[r]);
             __syncthreads();  // tile it's words written; tile it - 1's words no longer read
             const uint32_t* Wt = W + (it & 1) * (TILE * NWS);
             const int32_t p0 = seg0 + it * TILE;
